@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark: training images/sec of the batched raster fwd+bwd step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C2]
+
+Workload (BASELINE.json configs[1], "paper default"): synthetic head avatar,
+20 blendshapes, 50,176 Gaussians (UV 224), 512x512, batch 16 frames per GPU,
+random-init weights perturbed per SURVEY §8d, synthetic u8 RGBA targets.  A step
+is one full ``train_step`` (S/train.py:214-260): MLP, blend, projection, tile
+binning + radix sort (one host sync), forward compositing with the fused L1
+loss, the full adjoint chain, the gradient reduction (NCCL allreduce for N>1),
+the multi-group Adam update and the colour-initialisation estimate.
+
+Multi-GPU (torchrun, one process per GPU): weak scaling, 16 frames per GPU,
+global batch 16*N, one NCCL allreduce of the flat gradient per step; the timed
+region is max over ranks.
+
+``--impl reference`` times the CPU reference path on the host cores (the float64
+oracle port of headsplat's train_step under oracle/, all host threads) on the same
+config, metric and unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training images/sec (batched raster fwd+bwd)"
+UNIT = "images/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0          # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+L2_FLUSH_BYTES = 256 << 20
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() in ("active", "0x1", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ algorithmic bytes
+
+def stage_bytes(B, N, K, H, D, W, Hh, keys, params, color_init=True):
+    """Algorithmic (ideal-fusion) DRAM bytes per launch of each stage."""
+    HW = W * Hh
+    rec = 48
+    out = {
+        "mlp_fwd": 4 * (H * D + D * D + K * D + B * (H + 4 * D + K)),
+        "blend_fwd": 4 * (10 * N * K + 10 * N + B * 10 * N),
+        "project_fwd": B * N * (40 + rec + 4 + 4) + N * 32 + B * 1024 * 22 * 4,
+        "bin_sort": keys * (12 + 6 * 32 + 8),
+        "raster_fwd": keys * (4 + rec) + B * HW * (4 + 4 + 4) + (B * N * 20 if color_init else 0),
+        "raster_bwd": keys * (4 + rec) + B * HW * 8 + B * N * 36,
+        "project_bwd": B * N * (36 + 40 + 56) + N * 32 + B * 1024 * 22 * 4,
+        "blend_bwd": 4 * (B * 14 * N + 2 * 10 * N * K + 14 * N),
+        "adam": 28 * params,
+    }
+    return out
+
+
+# --------------------------------------------------------------- workloads
+
+CONFIGS = {
+    "C1": dict(uv=141, batch=4, size=256, desc="synthetic head avatar: 20 bases, 19,881 Gaussians, 256x256, batch 4"),
+    "C2": dict(uv=224, batch=16, size=512, desc="paper default: 20 bases, 50,176 Gaussians, 512x512, batch 16"),
+    "C4": dict(uv=317, batch=16, size=512, desc="batch-sharded: 20 bases, 100,489 Gaussians, 512x512, 16/GPU"),
+}
+
+
+def make_trainer(cfg, rank=0, world=1, pg=None):
+    import torch
+    from paper_2503_12886_b200 import synth
+    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    wl = synth.make_workload(cfg["uv"], cfg["batch"], cfg["size"], distinct_frames=min(cfg["batch"], 8),
+                             frames_seed=1 + rank)
+    av = wl.avatar
+    dev = AvatarParams.from_host(type("G", (), {a: av.base[a] for a in av.base})(), av.deltas, av.mlp,
+                                 av.tri_index, av.barycentric)
+    B = cfg["batch"]
+    tr = Trainer(dev, cfg["size"], cfg["size"], B, process_group=pg, global_batch=B * world, frame_offset=B * rank)
+    d = {
+        "thetas": torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda(),
+        "targets": torch.from_numpy(wl.targets).cuda(),
+        "frames": torch.from_numpy(wl.frames).cuda(),
+        "cameras": torch.from_numpy(np.tile(wl.camera.packed(), (B, 1))).cuda(),
+        "backgrounds": torch.from_numpy(np.asarray(wl.backgrounds, np.float32)).cuda(),
+    }
+    return tr, d, wl
+
+
+def cpu_reference_step_fn(cfg, frames_per_step, workers):
+    """The oracle port's train_step on a bounded sample of the workload (host cores)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2503_12886_b200 import synth
+    wl = synth.make_workload(cfg["uv"], frames_per_step, cfg["size"], distinct_frames=frames_per_step)
+    av = wl.avatar
+    f = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    model = O.Model(O.GSet(*(f(av.base[a]) for a in ("position", "rotation", "scale", "opacity", "color"))),
+                    f(av.deltas), {k: f(v) for k, v in av.mlp.items()}, av.tri_index, f(av.barycentric))
+    c = wl.camera
+    cam = O.Cam(c.fx, c.fy, c.cx, c.cy, np.asarray(c.rotation, np.float64), np.asarray(c.translation, np.float64),
+                c.width, c.height)
+    frames = [O.Frames(m.rotation, m.quat, m.tri_vertices) for m in wl.mesh]
+    state = O.State(model, cam, workers=workers)
+    images = wl.targets.astype(np.float64) / 255.0
+
+    def step():
+        O.train_step(state, wl.thetas, images, frames, wl.backgrounds)
+    return step, state
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = host_cores()
+    fps = max(1, min(cfg["batch"], cores))
+    step, state = cpu_reference_step_fn(cfg, fps, cores)
+    for _ in range(min(args.warmup, 1)):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    state.close()
+    ms = 1000.0 * statistics.median(times)
+    value = fps / (ms / 1000.0)
+    sample = (f"oracle train_step (float64 C port of headsplat, oracle/) on {fps} frames of the "
+              f"{args.config} workload per step, {cores} threads, median of {args.steps}")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "frames_per_step": fps},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    tr, d, wl = make_trainer(cfg, rank, world, pg)
+    B = cfg["batch"]
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        tr.step(d["thetas"], d["targets"], d["frames"], d["cameras"], d["backgrounds"])
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    # ---- device-resident timed region: K steps, L2 flushed between steps (outside the events)
+    clocks = ClockSampler(local)
+    clocks.start()
+    tr.enable_profiling(True)
+    launches0 = tr.launches
+    total_ms = 0.0
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        step()
+        e.record()
+        e.synchronize()
+        total_ms += s.elapsed_time(e)
+    barrier()
+    launches = tr.launches - launches0
+    stages = tr.stage_ms()
+    tr.enable_profiling(False)
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    value = B * world * args.steps / (float(t.item()) / 1000.0)
+
+    # ---- end-to-end through the host API (pinned H2D inputs, D2H losses) every step
+    h = {k: v.cpu().numpy() for k, v in d.items()}
+    for _ in range(2):
+        tr.step_from_host(h["thetas"], h["targets"], h["frames"], h["cameras"], h["backgrounds"])
+    barrier()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr.step_from_host(h["thetas"], h["targets"], h["frames"], h["cameras"], h["backgrounds"])
+        e2e_ms += (time.perf_counter() - t0) * 1000.0
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = B * world * args.steps / (float(t.item()) / 1000.0)
+    F = d["frames"].shape[1]
+
+    if rank == 0:
+        av = tr.av
+        peak, peak_kind = load_peaks()
+        sb = stage_bytes(B, av.N, av.K, av.H, av.D, tr.W, tr.H, tr.last_total, av.size)
+        per_step = {k: v / args.steps for k, v in stages.items()}
+        kern = {k: v for k, v in per_step.items() if k in sb}
+        dom = max(kern, key=kern.get)
+        achieved = sb[dom] / (kern[dom] / 1000.0) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(dom)
+        except Exception:
+            pass
+        step_bytes = sum(sb.values())
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "gaussians": av.N, "blendshapes": av.K, "image": tr.W,
+                       "frames_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world}",
+                       "l2": "256 MiB buffer written between timed steps (outside the CUDA events); "
+                             "per-step working set ~0.4 GB also exceeds L2",
+                       "keys_per_step": tr.last_total, "colour_init": "active (unvisited Gaussians)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+                         else "fallback (B200_PROFILING.md)",
+                         "algorithmic_bytes_per_launch": sb[dom]},
+            "step_roofline": {"algorithmic_bytes_per_step": step_bytes,
+                              "achieved_gbs": step_bytes / (ms / 1000.0) / 1e9,
+                              "frac": step_bytes / (ms / 1000.0) / 1e9 / peak},
+            "stages_ms": {k: round(v, 4) for k, v in per_step.items()},
+            "clocks": clk,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": tr.h2d_bytes(F),
+                    "d2h_bytes_per_step": tr.d2h_bytes()},
+            "gpu_launches": launches,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, args)
+        if world == 1 and not args.no_render:
+            line["render"] = render_fps(args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(cfg, args):
+    cores = host_cores()
+    fps = max(1, min(4, cores))
+    step, state = cpu_reference_step_fn(cfg, fps, cores)
+    t0 = time.perf_counter()
+    step()
+    t1 = time.perf_counter()
+    state.close()
+    v = fps / (t1 - t0)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"one oracle train_step (float64 C port, oracle/) on {fps} frames of the {args.config} "
+                      f"workload, {cores} threads: {t1 - t0:.2f} s"}
+
+
+def render_fps(args):
+    """Render-only FPS (BASELINE configs[2]: 100,489 Gaussians, 512^2, batch 64), device-resident."""
+    import torch
+    from paper_2503_12886_b200 import synth
+    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    wl = synth.make_workload(317, 64, 512, distinct_frames=8)
+    av = wl.avatar
+    dev = AvatarParams.from_host(type("G", (), {a: av.base[a] for a in av.base})(), av.deltas, av.mlp,
+                                 av.tri_index, av.barycentric)
+    tr = Trainer(dev, 512, 512, 64, color_init=False)
+    th = torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda()
+    fr = torch.from_numpy(wl.frames).cuda()
+    cams = torch.from_numpy(np.tile(wl.camera.packed(), (64, 1))).cuda()
+    bg = torch.zeros(64, 3, device="cuda")
+    out = torch.empty(64, 512, 512, 3, device="cuda")
+    for _ in range(3):
+        tr.render(th, fr, cams, bg, out)
+    torch.cuda.synchronize()
+    reps = 10
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        tr.render(th, fr, cams, bg, out)
+    e.record()
+    e.synchronize()
+    ms = s.elapsed_time(e) / reps
+    return {"metric": "render FPS (MLP + blend + transform + project + bin/sort + composite)", "value": 64 / (ms / 1000.0),
+            "unit": "frames/s", "ms_per_batch": ms, "config": "20 bases, 100,489 Gaussians, 512x512, batch 64",
+            "keys_per_batch": tr.last_total}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,223 @@
+/*
+ * hs_api.h -- C ABI of the B200 (sm_100a) RGBAvatar training hot path.
+ *
+ * One shared library, libhs_b200.so (paper_2503_12886_b200/lib/), built from
+ * paper_2503_12886_b200/csrc/*.cu with nvcc -gencode arch=compute_100a,code=sm_100a.
+ *
+ * Calling convention
+ *   - Every buffer argument is a caller-owned DEVICE pointer (e.g. a torch
+ *     tensor's data_ptr()); sizes are plain integers.  No torch types.
+ *   - Every call enqueues work on the caller-given stream (a cudaStream_t passed
+ *     as void*; NULL = legacy default stream) and returns without synchronizing.
+ *   - No allocation happens inside the library.  Scratch is sized by the
+ *     hs_*_size queries and allocated by the caller.
+ *   - Return value: HS_OK or an HS_ERR_* status; hs_last_error() returns a
+ *     thread-local message for the last failing call on the calling thread.
+ *   - Re-entrant per stream; no global mutable state besides the thread-local
+ *     error string.
+ *
+ * Data layout (fp32 unless stated; N Gaussians, K blendshapes, B frames):
+ *   params   flat [base 14N | deltas K*10N | mlp]  with
+ *            base  = [position 3N | rotation 4N (wxyz) | color 3N | scale 3N | opacity N]
+ *            delta = [position 3N | rotation 4N | color 3N]        (one block per k)
+ *            mlp   = [w1 D*H | b1 D | w2 D*D | b2 D | w3 K*D | b3 K]  (row-major)
+ *            raw values: log-scale, opacity/color logits (S/gaussians.py:24-69).
+ *   grads    same layout as params (the NCCL allreduce payload).
+ *   raw10    B x [position 3N | rotation 4N | color 3N]  blended (pre-activation)
+ *   g_raw14  B x 14N, the base layout.
+ *   world14  B x 14N activated world Gaussians, the base layout (compat path).
+ *   frames   B x F x 22: [rotation 9 (row-major, columns T,B,N) | quat 4 | tri 9
+ *            (vertex-major)]  (S/binding.py:47-53 MeshFrames).
+ *   cameras  B x 16: [R 9 row-major world->camera | t 3 | fx fy cx cy]
+ *            (S/render.py:40-84).  All frames of a call share width/height.
+ *   records  B x N x 12 splat records written by project:
+ *            [mx my | conic a b c | opacity | qmax | bbox_rows | bbox_cols | r g b]
+ *            bbox_* pack (lo | hi << 16) as uint32 bits; qmax = 2 ln(255 op) + 1e-9.
+ *   depth    B x N camera-space z of each splat; counts B x N tiles touched.
+ *   keys     uint64  frame << (tile_bits+32) | tile << 32 | float_bits(depth)
+ *   values   uint32  Gaussian index n
+ *   ranges   B x 2^tile_bits x uint2 [start, end) into the sorted key list
+ *            (tile_bits = bit length of tiles-1; index = key >> 32)
+ *   pixel    B x H x W: T_final (fp32) and state (uint32: stop | sign bits << 26)
+ *   g_splat  B x N x 9 [g_mean x y | g_conic a 2b c | g_opacity | g_color r g b]
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/headsplat):
+ *   see the per-function comments.
+ */
+#ifndef HS_API_H
+#define HS_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    HS_OK = 0,
+    HS_ERR_SHAPE = 1,      /* -> ValueError          (e.g. model.py:133-134, render.py:56-59) */
+    HS_ERR_NONFINITE = 2,  /* -> FloatingPointError  (render.py:204-208) */
+    HS_ERR_ZERO_QUAT = 3,  /* -> FloatingPointError  (model.py:224-227) */
+    HS_ERR_COLOR_INIT = 4, /* -> RuntimeError        (color_init.py:59-63) */
+    HS_ERR_CUDA = 5
+};
+
+/* Error-code word written with atomicMin by device kernels (HS_NO_ERROR = none):
+ *   bits 62-63 stage (0 frame-forward checks, 1 preprocess checks)
+ *   bits 40-61 frame, bits 32-39 attribute, bits 0-31 Gaussian index
+ * stage 0 attributes: 0 non-finite theta (model.py:135-136), 1 zero-norm quat (model.py:224-227)
+ * stage 1 attributes: 0 position, 1 rotation, 2 scale, 3 opacity, 4 color (render.py:204-208)
+ * stage 2 attribute 0: colour-init eligibility inconsistency (color_init.py:59-63) */
+#define HS_NO_ERROR 0xFFFFFFFFFFFFFFFFull
+
+const char *hs_last_error(void);
+int hs_version(void);
+int hs_device_sm_count(int device);
+
+/* ---- MLP (model.py:130-142 map_params, :145-162 mlp_backward) ----------- */
+/* psi[B,K] and the per-frame cache[B, 4D] = (z1, h1, z2, h2); err gets a stage-0
+ * attribute-0 code for a non-finite theta row. */
+int hs_mlp_fwd(int B, int H, int D, int K, const float *mlp, const float *theta,
+               float *cache, float *psi, unsigned long long *err, void *stream);
+/* Sums the weight gradients over the B frames in frame order into g_mlp (written).
+ * gpsi_partials[B*K][num_partials] come from hs_blend_bwd; scratch >= B*(K+2D) floats. */
+int hs_mlp_bwd(int B, int H, int D, int K, const float *mlp, const float *theta,
+               const float *cache, const float *gpsi_partials, int num_partials,
+               float *gpsi, float *scratch, float *g_mlp, void *stream);
+/* Number of floats in the mlp block. */
+int64_t hs_mlp_size(int H, int D, int K);
+
+/* ---- Blend (model.py:165-185 blend, :188-216 blend_backward + train.py:253-255) */
+/* raw10[b] = base10 + sum_k psi[b,k] * delta_k  (k ascending, psi==0 skipped, fmaf). */
+int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *deltas,
+                 const float *psi, float *raw10, void *stream);
+/* Reduces over all B frames in-kernel:  g_base14 = sum_b g_raw14[b];
+ * g_deltas[k] = sum_b psi[b,k] g_raw10[b];  gpsi partial sums per block.
+ * Both outputs are written (not accumulated).  Returns the partial count in
+ * *num_partials; gpsi_partials needs hs_blend_bwd_partials(N) * B * K floats. */
+int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
+                 const float *g_raw14, float *g_base14, float *g_deltas,
+                 float *gpsi_partials, int *num_partials, void *stream);
+int hs_blend_bwd_partials(int64_t N);
+
+/* ---- Projection (render.py:132-230 preprocess; model.py:219-234 activate;
+ *      binding.py:174-188 transform_to_deformed) -------------------------- */
+/* Fused activate + transform + project for B frames x N Gaussians in one launch.
+ * Writes records, depth, counts (tiles touched) and one partial sum of counts per
+ * 256 items (block_sums[ceil(B*N/256)]); err gets the first error code. */
+int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height,
+                          const float *raw10, const float *base14, const int32_t *tri_index,
+                          const float *bary, const float *frames, const float *cameras,
+                          float *records, float *depth, uint32_t *counts,
+                          uint32_t *block_sums, float *radius, unsigned long long *err,
+                          void *stream);
+/* Projection of already-activated world Gaussians (compat preprocess).
+ * radius (B*N, 0 for culled splats), x_cam (B*N*3) and cov_cam (B*N*9) are
+ * optional outputs (NULL to skip) in both projection calls. */
+int hs_project_world_fwd(int B, int64_t N, int width, int height, const float *world14,
+                         const float *cameras, float *records, float *depth,
+                         uint32_t *counts, uint32_t *block_sums, float *radius, float *x_cam,
+                         float *cov_cam, unsigned long long *err, void *stream);
+/* Adjoint of hs_project_avatar_fwd (render.py:432-497 _preprocess_backward,
+ * binding.py:191-204 transform_backward, model.py:237-248 activate_backward):
+ * g_splat[B,N,9] -> g_raw14[B,14N] (written). */
+int hs_project_avatar_bwd(int B, int64_t N, int F, const float *raw10, const float *base14,
+                          const int32_t *tri_index, const float *bary, const float *frames,
+                          const float *cameras, const float *g_splat, float *g_raw14,
+                          void *stream);
+/* Adjoint of hs_project_world_fwd: g_splat -> g_world14[B,14N] (written). */
+int hs_project_world_bwd(int B, int64_t N, const float *world14, const float *cameras,
+                         const float *g_splat, float *g_world14, void *stream);
+
+/* ---- Binning (new; replaces render.py:221-223 + :380-386) */
+int hs_scan_blocks(int64_t num_items);  /* = ceil(num_items / 256) */
+/* Exclusive scan of block_sums -> block_offsets; summary[0] = total keys,
+ * summary[1] = *err.  The caller copies summary to pinned host memory: the one
+ * device->host read of a training step. */
+int hs_bin_scan(int num_blocks, const uint32_t *block_sums, uint32_t *block_offsets,
+                const unsigned long long *err, unsigned long long *summary, void *stream);
+/* Writes keys/values in (frame, n, ty, tx) order. */
+int hs_bin_emit(int B, int64_t N, int width, int height, const float *records,
+                const float *depth, const uint32_t *counts, const uint32_t *block_offsets,
+                uint64_t *keys, uint32_t *values, void *stream);
+/* Bytes of scratch for hs_sort_pairs. */
+size_t hs_sort_workspace_size(int64_t num_keys);
+/* Stable LSD radix sort of (keys, values) over bits [0, key_bits).  Ping-pongs
+ * between the (keys, values) and (keys_alt, values_alt) buffers; *result_in_alt
+ * tells which pair holds the sorted output. */
+int hs_sort_pairs(int64_t num_keys, int key_bits, uint64_t *keys, uint32_t *values,
+                  uint64_t *keys_alt, uint32_t *values_alt, void *workspace,
+                  size_t workspace_bytes, int *result_in_alt, void *stream);
+/* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */
+int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);
+
+/* ---- Raster (render.py:233-273 _composite_kernel, :339-377 _weight_sums_kernel,
+ *      metrics.py:10-22 l1_loss, :80-85 composite_over, train.py:238-247) ---- */
+enum {
+    HS_RASTER_LOSS = 1,          /* fused L1 loss vs targets (u8 RGBA) composited over bg */
+    HS_RASTER_IMAGE = 2,         /* write image[B,H,W,3] */
+    HS_RASTER_MAXW_ALL = 4,      /* max blend weight per (frame, Gaussian) */
+    HS_RASTER_MAXW_UNVISITED = 8,/* same, only for Gaussians with visited[n] == 0 */
+    HS_RASTER_WSUMS = 16,        /* colour-init sums (sum w*target, sum w) for the same set */
+    HS_RASTER_WSUMS_IMAGE = 32   /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
+};
+int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records,
+                  const uint32_t *values, const uint32_t *ranges, int tile_bits,
+                  const float *backgrounds, const uint8_t *targets, const float *wsum_image,
+                  const uint8_t *visited, float *pix_T, uint32_t *pix_state, float *image,
+                  float *maxw, float *wsums, float *loss_partials, void *stream);
+/* Adjoint (render.py:276-336 _backward_kernel).  grad_image (B,H,W,3) may be NULL:
+ * then the L1 gradient sign(pred - target) * grad_scale recorded by the forward is used.
+ * g_splat must be zero-filled by the caller (accumulated with atomics after a warp reduce). */
+int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
+                  const uint32_t *values, const uint32_t *ranges, int tile_bits,
+                  const float *backgrounds, const float *pix_T, const uint32_t *pix_state,
+                  const float *grad_image, float grad_scale, float *g_splat, void *stream);
+/* loss_out[b] = sum|pred-target| / (H*W*3), loss_out[B+b] = black-bg L1,
+ * loss_out[2B] = mean over frames. */
+int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *loss_partials,
+                   float *loss_out, void *stream);
+
+/* ---- Optimizer (optim.py:28-40; groups train.py:164-199) ---------------- */
+/* lrs[9] = base position, rotation, color, scale, opacity, delta position,
+ * rotation, color, mlp.  step >= 1 (bias correction). */
+int hs_adam(int64_t N, int K, int64_t mlp_size, float *params, const float *grads,
+            float *m, float *v, const float *lrs, int step, float beta1, float beta2,
+            float eps, void *stream);
+
+/* ---- Colour init (train.py:263-278, color_init.py:45-80, model.py:260-263) */
+/* best frame = first argmax_b maxw[b,n]; need = !visited && best > threshold;
+ * base color[n] <- logit(clip(num/den, 1e-4, 1-1e-4)); visited[n] = 1.
+ * n_init (optional, device int) counts initialized Gaussians. */
+int hs_color_init(int B, int64_t N, const float *maxw, const float *wsums, float threshold,
+                  uint8_t *visited, float *params, int *n_init, unsigned long long *err,
+                  void *stream);
+/* Multi-GPU colour init, three steps around two allreduces:
+ *  pack:   packed[n] = max_b (float_bits(maxw[b,n]) << 32 | 0xFFFFFFFF - (frame_offset+b)),
+ *          0 for visited n -- an allreduce-MAX picks the largest weight, then the
+ *          smallest global frame (the reference's first-max argmax);
+ *  select: est4[n] = (num/den rgb, 1) where this rank owns the winning frame, else 0
+ *          -- then allreduce-SUM;
+ *  apply:  need = !visited && weight > threshold -> logit write + visited. */
+int hs_color_pack(int B, int64_t N, int frame_offset, const float *maxw, const uint8_t *visited,
+                  int64_t *packed, void *stream);
+int hs_color_select(int B, int64_t N, int frame_offset, const int64_t *packed, const float *wsums,
+                    float *est4, unsigned long long *err, void *stream);
+int hs_color_apply(int64_t N, const int64_t *packed, const float *est4, float threshold,
+                   uint8_t *visited, float *params, int *n_init, void *stream);
+
+/* ---- Elementwise compat ops (model.py:219-248, binding.py:174-204) ------- */
+int hs_activate_fwd(int64_t N, const float *raw14, float *act14, unsigned long long *err, void *stream);
+int hs_activate_bwd(int64_t N, const float *raw14, const float *act14, const float *g_act14,
+                    float *g_raw14, void *stream);
+int hs_transform_fwd(int64_t N, const float *tangent14, const float *frames,
+                     const int32_t *tri_index, const float *bary, float *world14, void *stream);
+int hs_transform_bwd(int64_t N, const float *tangent14, const float *frames,
+                     const int32_t *tri_index, const float *g_world14, float *g_tangent14,
+                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HS_API_H */

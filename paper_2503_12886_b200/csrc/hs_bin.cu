@@ -1,0 +1,335 @@
+// hs_bin.cu -- batched tile binning on sm_100a: key-offset scan, key emission,
+// a stable LSD radix sort of (frame, tile, depth) keys and per-tile ranges.
+//
+// The reference has no tiles: one global stable depth argsort per frame
+// (S/render.py:221-223) and a per-splat pixel-bbox scatter (:248-251).  The
+// device path keys every (frame, splat, tile) overlap and sorts all frames of a
+// step in one pass; oracle/binning.py is the bit-exact CPU restatement
+// (SURVEY Appendix B).  Stable sorting of keys emitted in Gaussian order makes
+// equal depth bits resolve to the lower index, the reference's tie-break.
+#include "hs_common.cuh"
+
+namespace hs {
+
+// ------------------------------------------------------------- offsets scan
+
+// One CTA: exclusive scan of the per-256-item tile-count sums.  Writes the key
+// total and the error word to `summary` (the step's single device->host read).
+__global__ void __launch_bounds__(1024) scan_kernel(int nb, const uint32_t *__restrict__ sums,
+                                                    uint32_t *__restrict__ offs,
+                                                    const unsigned long long *__restrict__ err,
+                                                    unsigned long long *__restrict__ summary) {
+    __shared__ unsigned long long warp_tot[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int per = (nb + blockDim.x - 1) / blockDim.x;
+    const int lo = min(nb, tid * per), hi = min(nb, lo + per);
+    unsigned long long local = 0;
+    for (int i = lo; i < hi; ++i) local += sums[i];
+    unsigned long long incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long v = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0ull;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        warp_tot[lane] = v;  // inclusive over warps
+    }
+    __syncthreads();
+    unsigned long long run = (w > 0 ? warp_tot[w - 1] : 0ull) + incl - local;
+    for (int i = lo; i < hi; ++i) {
+        offs[i] = (uint32_t)run;
+        run += sums[i];
+    }
+    if (tid == 0) {
+        summary[0] = warp_tot[(blockDim.x >> 5) - 1];
+        summary[1] = err ? *err : HS_NO_ERROR;
+    }
+}
+
+// ------------------------------------------------------------------ emission
+
+// Same 256-item partition as the projection kernel: block-local exclusive scan of
+// the tile counts plus the block offset gives each (frame, Gaussian) its slot.
+__global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int tiles_x, int tile_bits,
+                                                          const float *__restrict__ records,
+                                                          const float *__restrict__ depth,
+                                                          const uint32_t *__restrict__ counts,
+                                                          const uint32_t *__restrict__ offs,
+                                                          uint64_t *__restrict__ keys,
+                                                          uint32_t *__restrict__ vals) {
+    __shared__ uint32_t warp_tot[kScanBlock / 32];
+    const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+    const bool in = i < (int64_t)B * N;
+    const uint32_t cnt = in ? counts[i] : 0u;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int k = 0; k < w; ++k) wpre += warp_tot[k];
+    if (!in || cnt == 0) return;
+    uint32_t pos = offs[blockIdx.x] + wpre + incl - cnt;
+    const int b = (int)(i / N);
+    const uint32_t n = (uint32_t)(i - (int64_t)b * N);
+    const float *rec = records + i * kRec;
+    const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);
+    const int ty0 = unpack_lo(rows) / kTile, ty1 = unpack_hi(rows) / kTile;
+    const int tx0 = unpack_lo(cols) / kTile, tx1 = unpack_hi(cols) / kTile;
+    const uint64_t hi = ((uint64_t)b << (tile_bits + 32)) | (uint64_t)__float_as_uint(depth[i]);
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            keys[pos] = hi | ((uint64_t)(ty * tiles_x + tx) << 32);
+            vals[pos] = n;
+            ++pos;
+        }
+}
+
+// --------------------------------------------------------------- radix sort
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per CTA
+constexpr int kRadix = 256;
+
+// per-CTA digit histogram, stored digit-major: hist[d * tiles + tile]
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(int64_t n, int shift,
+                                                                  const uint64_t *__restrict__ keys,
+                                                                  uint32_t *__restrict__ hist, int tiles) {
+    __shared__ uint32_t h[kRadix];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int64_t idx = base + i * kSortThreads + threadIdx.x;
+        if (idx < n) atomicAdd(&h[(uint32_t)(keys[idx] >> shift) & (kRadix - 1)], 1u);
+    }
+    __syncthreads();
+    hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// one CTA per digit: exclusive scan of that digit's row over the CTAs; totals[d]
+__global__ void __launch_bounds__(256) radix_rowscan_kernel(uint32_t *__restrict__ hist, int tiles,
+                                                            uint32_t *__restrict__ totals) {
+    __shared__ uint32_t warp_tot[8];
+    uint32_t *row = hist + (int64_t)blockIdx.x * tiles;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t carry = 0;
+    for (int c0 = 0; c0 < tiles; c0 += 256) {
+        const int idx = c0 + tid;
+        const uint32_t v = idx < tiles ? row[idx] : 0u;
+        uint32_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[w] = incl;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+        for (int k = 0; k < 8; ++k) {
+            if (k < w) wpre += warp_tot[k];
+            tot += warp_tot[k];
+        }
+        if (idx < tiles) row[idx] = carry + wpre + incl - v;
+        carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) totals[blockIdx.x] = carry;
+}
+
+// Stable scatter.  Keys are read warp-striped (warp w owns 256 consecutive keys,
+// item i of lane l is key w*256 + i*32 + l), ranked per warp with match.any,
+// staged digit-sorted in shared memory and written out as contiguous runs.
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(int64_t n, int shift,
+                                                                     const uint64_t *__restrict__ keys_in,
+                                                                     const uint32_t *__restrict__ vals_in,
+                                                                     uint64_t *__restrict__ keys_out,
+                                                                     uint32_t *__restrict__ vals_out,
+                                                                     const uint32_t *__restrict__ hist,
+                                                                     const uint32_t *__restrict__ totals,
+                                                                     int tiles) {
+    __shared__ uint64_t s_keys[kSortTile];
+    __shared__ uint32_t s_vals[kSortTile];
+    __shared__ uint32_t warp_hist[kSortThreads / 32][kRadix];
+    __shared__ uint32_t digit_off[kRadix];
+    __shared__ uint32_t glob[kRadix];
+    __shared__ uint32_t warp_tot[8];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+
+    // global base of each digit: exclusive prefix of totals + this CTA's row offset
+    {
+        const uint32_t v = totals[tid];
+        uint32_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[w] = incl;
+        for (int k = 0; k < kSortThreads / 32; ++k) warp_hist[k][tid] = 0;
+        __syncthreads();
+        uint32_t wpre = 0;
+        for (int k = 0; k < w; ++k) wpre += warp_tot[k];
+        glob[tid] = wpre + incl - v + hist[(int64_t)tid * tiles + blockIdx.x];
+    }
+    __syncthreads();
+
+    uint64_t k_reg[kSortItems];
+    uint32_t v_reg[kSortItems];
+    uint32_t local[kSortItems];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int64_t idx = base + w * (32 * kSortItems) + i * 32 + lane;
+        const bool valid = idx < n;
+        k_reg[i] = valid ? keys_in[idx] : 0ull;
+        v_reg[i] = valid ? vals_in[idx] : 0u;
+        const uint32_t d = (uint32_t)(k_reg[i] >> shift) & (kRadix - 1);
+        const uint32_t mask = __ballot_sync(0xffffffffu, valid);
+        local[i] = 0;
+        if (valid) {
+            const uint32_t peers = __match_any_sync(mask, d);
+            const uint32_t rank = __popc(peers & lt);
+            const uint32_t cur = warp_hist[w][d];
+            __syncwarp(mask);
+            if (rank == 0) warp_hist[w][d] = cur + __popc(peers);
+            __syncwarp(mask);
+            local[i] = cur + rank;
+        }
+    }
+    __syncthreads();
+    // per digit: prefix over warps, then block-exclusive scan over digits
+    {
+        uint32_t run = 0;
+#pragma unroll
+        for (int k = 0; k < kSortThreads / 32; ++k) {
+            const uint32_t t = warp_hist[k][tid];
+            warp_hist[k][tid] = run;
+            run += t;
+        }
+        uint32_t incl = run;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        __syncthreads();
+        if (lane == 31) warp_tot[w] = incl;
+        __syncthreads();
+        uint32_t wpre = 0;
+        for (int k = 0; k < w; ++k) wpre += warp_tot[k];
+        digit_off[tid] = wpre + incl - run;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int64_t idx = base + w * (32 * kSortItems) + i * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = (uint32_t)(k_reg[i] >> shift) & (kRadix - 1);
+            const uint32_t p = digit_off[d] + warp_hist[w][d] + local[i];
+            s_keys[p] = k_reg[i];
+            s_vals[p] = v_reg[i];
+        }
+    }
+    __syncthreads();
+    const int cnt = (int)min((int64_t)kSortTile, n - base);
+    for (int j = tid; j < cnt; j += kSortThreads) {
+        const uint64_t key = s_keys[j];
+        const uint32_t d = (uint32_t)(key >> shift) & (kRadix - 1);
+        const uint32_t p = glob[d] + (uint32_t)j - digit_off[d];
+        keys_out[p] = key;
+        vals_out[p] = s_vals[j];
+    }
+}
+
+// ----------------------------------------------------------------- ranges
+
+__global__ void tile_ranges_kernel(int64_t n, const uint64_t *__restrict__ keys, uint32_t *__restrict__ ranges) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t t = keys[i] >> 32;
+    if (i == 0 || (keys[i - 1] >> 32) != t) ranges[2 * t] = (uint32_t)i;
+    if (i == n - 1 || (keys[i + 1] >> 32) != t) ranges[2 * t + 1] = (uint32_t)(i + 1);
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" {
+
+int hs_bin_scan(int num_blocks, const uint32_t *block_sums, uint32_t *block_offsets, const unsigned long long *err,
+                unsigned long long *summary, void *stream) {
+    scan_kernel<<<1, 1024, 0, HS_CHECK_STREAM(stream)>>>(num_blocks, block_sums, block_offsets, err, summary);
+    return check_launch("hs_bin_scan");
+}
+
+int hs_bin_emit(int B, int64_t N, int width, int height, const float *records, const float *depth,
+                const uint32_t *counts, const uint32_t *block_offsets, uint64_t *keys, uint32_t *values,
+                void *stream) {
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
+    const int frame_bits = bit_length_u32((uint32_t)(B - 1));
+    if (tile_bits + frame_bits > 32) {
+        set_error("hs_bin_emit: frame/tile key bits %d + %d exceed 32", frame_bits, tile_bits);
+        return HS_ERR_SHAPE;
+    }
+    const int64_t items = (int64_t)B * N;
+    emit_kernel<<<hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream)>>>(
+        B, N, tiles_x, tile_bits, records, depth, counts, block_offsets, keys, values);
+    return check_launch("hs_bin_emit");
+}
+
+size_t hs_sort_workspace_size(int64_t num_keys) {
+    const int64_t tiles = (num_keys + kSortTile - 1) / kSortTile;
+    return sizeof(uint32_t) * ((size_t)kRadix * (size_t)(tiles > 0 ? tiles : 1) + kRadix);
+}
+
+int hs_sort_pairs(int64_t num_keys, int key_bits, uint64_t *keys, uint32_t *values, uint64_t *keys_alt,
+                  uint32_t *values_alt, void *workspace, size_t workspace_bytes, int *result_in_alt,
+                  void *stream) {
+    if (result_in_alt) *result_in_alt = 0;
+    if (num_keys <= 0) return HS_OK;
+    if (workspace_bytes < hs_sort_workspace_size(num_keys)) {
+        set_error("hs_sort_pairs: workspace too small (%zu < %zu)", workspace_bytes, hs_sort_workspace_size(num_keys));
+        return HS_ERR_SHAPE;
+    }
+    if (num_keys > 0xFFFFFFFFll) {
+        set_error("hs_sort_pairs: too many keys");
+        return HS_ERR_SHAPE;
+    }
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    const int tiles = (int)((num_keys + kSortTile - 1) / kSortTile);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(workspace);
+    uint32_t *totals = hist + (size_t)kRadix * tiles;
+    uint64_t *ki = keys, *ko = keys_alt;
+    uint32_t *vi = values, *vo = values_alt;
+    int alt = 0;
+    for (int shift = 0; shift < key_bits; shift += 8) {
+        radix_hist_kernel<<<tiles, kSortThreads, 0, s>>>(num_keys, shift, ki, hist, tiles);
+        radix_rowscan_kernel<<<kRadix, 256, 0, s>>>(hist, tiles, totals);
+        radix_scatter_kernel<<<tiles, kSortThreads, 0, s>>>(num_keys, shift, ki, vi, ko, vo, hist, totals, tiles);
+        uint64_t *tk = ki; ki = ko; ko = tk;
+        uint32_t *tv = vi; vi = vo; vo = tv;
+        alt ^= 1;
+    }
+    if (result_in_alt) *result_in_alt = alt;
+    return check_launch("hs_sort_pairs");
+}
+
+int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream) {
+    if (num_keys <= 0) return HS_OK;
+    tile_ranges_kernel<<<grid_for(num_keys, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(num_keys, keys, ranges);
+    return check_launch("hs_tile_ranges");
+}
+
+}  // extern "C"

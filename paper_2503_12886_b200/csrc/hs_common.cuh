@@ -1,0 +1,107 @@
+// hs_common.cuh -- shared device helpers for the sm_100a RGBAvatar hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hs_api.h"
+
+namespace hs {
+
+// S/render.py:34-37
+constexpr float kNearPlane = 0.01f;
+constexpr float kMinRadius = 0.3f;
+constexpr float kAlphaCutoff = 1.0f / 255.0f;
+constexpr float kTermEps = 1e-14f;
+constexpr int kTile = 16;
+constexpr int kRec = 12;            // floats per splat record
+constexpr int kGS = 9;              // floats per splat gradient
+constexpr int kFrame = 22;          // floats per mesh frame
+constexpr int kCam = 16;            // floats per camera
+constexpr int kScanBlock = 256;     // items per project/emit scan block
+constexpr uint32_t kStopMask = (1u << 26) - 1u;
+
+// error codes (see hs_api.h)
+__host__ __device__ inline unsigned long long err_code(int stage, int frame, int attr, int64_t n) {
+    return ((unsigned long long)stage << 62) | ((unsigned long long)frame << 40) |
+           ((unsigned long long)attr << 32) | (unsigned long long)(uint32_t)n;
+}
+
+void set_error(const char *fmt, ...);
+int check_launch(const char *what);
+
+inline unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+__device__ __forceinline__ float sigmoidf_ref(float x) {
+    // S/model.py:251-257 two-branch stable sigmoid
+    if (x >= 0.0f) return 1.0f / (1.0f + expf(-x));
+    float ex = expf(x);
+    return ex / (1.0f + ex);
+}
+
+// S/quatmath.py:28-40 Hamilton product a (x) b
+__device__ __forceinline__ void quat_mul(const float a[4], const float b[4], float o[4]) {
+    o[0] = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];
+    o[1] = a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2];
+    o[2] = a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1];
+    o[3] = a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0];
+}
+
+// S/quatmath.py:43-55 adjoint of b -> a (x) b
+__device__ __forceinline__ void quat_mul_bwd_right(const float a[4], const float g[4], float o[4]) {
+    o[0] = a[0] * g[0] + a[1] * g[1] + a[2] * g[2] + a[3] * g[3];
+    o[1] = -a[1] * g[0] + a[0] * g[1] + a[3] * g[2] - a[2] * g[3];
+    o[2] = -a[2] * g[0] - a[3] * g[1] + a[0] * g[2] + a[1] * g[3];
+    o[3] = -a[3] * g[0] + a[2] * g[1] - a[1] * g[2] + a[0] * g[3];
+}
+
+// S/quatmath.py:58-76 (unit formula, no renormalization), row-major 3x3
+__device__ __forceinline__ void quat_to_mat(const float q[4], float m[9]) {
+    float w = q[0], x = q[1], y = q[2], z = q[3];
+    m[0] = 1.f - 2.f * (y * y + z * z);
+    m[1] = 2.f * (x * y - w * z);
+    m[2] = 2.f * (x * z + w * y);
+    m[3] = 2.f * (x * y + w * z);
+    m[4] = 1.f - 2.f * (x * x + z * z);
+    m[5] = 2.f * (y * z - w * x);
+    m[6] = 2.f * (x * z - w * y);
+    m[7] = 2.f * (y * z + w * x);
+    m[8] = 1.f - 2.f * (x * x + y * y);
+}
+
+// S/quatmath.py:79-102
+__device__ __forceinline__ void quat_to_mat_bwd(const float q[4], const float g[9], float o[4]) {
+    float w = q[0], x = q[1], y = q[2], z = q[3];
+    o[0] = 2.f * (x * (g[7] - g[5]) + y * (g[2] - g[6]) + z * (g[3] - g[1]));
+    o[1] = 2.f * (w * (g[7] - g[5]) + y * (g[3] + g[1]) + z * (g[6] + g[2]) - 2.f * x * (g[4] + g[8]));
+    o[2] = 2.f * (w * (g[2] - g[6]) + x * (g[3] + g[1]) + z * (g[7] + g[5]) - 2.f * y * (g[0] + g[8]));
+    o[3] = 2.f * (w * (g[3] - g[1]) + x * (g[6] + g[2]) + y * (g[7] + g[5]) - 2.f * z * (g[0] + g[4]));
+}
+
+// S/quatmath.py:21-25 adjoint of q -> q/|q|
+__device__ __forceinline__ void quat_normalize_bwd(const float q[4], const float g[4], float o[4]) {
+    float nrm = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    float inv = 1.0f / nrm;
+    float y0 = q[0] * inv, y1 = q[1] * inv, y2 = q[2] * inv, y3 = q[3] * inv;
+    float dot = y0 * g[0] + y1 * g[1] + y2 * g[2] + y3 * g[3];
+    o[0] = (g[0] - y0 * dot) * inv;
+    o[1] = (g[1] - y1 * dot) * inv;
+    o[2] = (g[2] - y2 * dot) * inv;
+    o[3] = (g[3] - y3 * dot) * inv;
+}
+
+__device__ __forceinline__ uint32_t pack_lohi(int lo, int hi) {
+    return (uint32_t)(lo & 0xFFFF) | ((uint32_t)(hi & 0xFFFF) << 16);
+}
+__device__ __forceinline__ int unpack_lo(uint32_t v) { return (int)(int16_t)(v & 0xFFFF); }
+__device__ __forceinline__ int unpack_hi(uint32_t v) { return (int)(int16_t)(v >> 16); }
+
+__host__ __device__ inline int bit_length_u32(uint32_t x) {
+    int n = 0;
+    while (x) { ++n; x >>= 1; }
+    return n;
+}
+
+}  // namespace hs
+
+#define HS_CHECK_STREAM(s) (reinterpret_cast<cudaStream_t>(s))

@@ -1,0 +1,689 @@
+// hs_model.cu -- reduced-blendshape model ops on sm_100a: MLP, blend (+adjoint),
+// multi-group Adam, colour-init apply, and the elementwise compat ops.
+//
+// Reference: S/model.py (map_params :130, mlp_backward :145, blend :165,
+// blend_backward :188, activate :219, activate_backward :237), S/optim.py:28-40,
+// S/train.py:164-199 (Adam groups), :253-255 (item-order reduce), :263-278 and
+// S/color_init.py:45-80 (colour init), S/binding.py:174-204 (transform).
+#include <cstdarg>
+#include <cstdio>
+#include <algorithm>
+#include <cmath>
+
+#include "hs_common.cuh"
+
+namespace hs {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return HS_ERR_CUDA;
+    }
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------- MLP
+
+// One CTA per frame.  S/model.py:130-142.
+__global__ void mlp_fwd_kernel(int H, int D, int K, const float *__restrict__ mlp,
+                               const float *__restrict__ theta, float *__restrict__ cache,
+                               float *__restrict__ psi, unsigned long long *err) {
+    extern __shared__ float sm[];
+    float *th = sm, *h1 = th + H, *h2 = h1 + D;
+    const int b = blockIdx.x;
+    const float *w1 = mlp, *b1 = w1 + D * H, *w2 = b1 + D, *b2 = w2 + D * D, *w3 = b2 + D, *b3 = w3 + K * D;
+    for (int i = threadIdx.x; i < H; i += blockDim.x) {
+        float t = theta[b * H + i];
+        th[i] = t;
+        if (!isfinite(t)) atomicMin(err, err_code(0, b, 0, 0));
+    }
+    __syncthreads();
+    float *c = cache + (int64_t)b * 4 * D;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) {
+        float acc = 0.f;
+        for (int j = 0; j < H; ++j) acc = fmaf(w1[i * H + j], th[j], acc);
+        float z = acc + b1[i];
+        float h = z > 0.f ? z : 0.f;
+        c[i] = z;
+        c[D + i] = h;
+        h1[i] = h;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < D; i += blockDim.x) {
+        float acc = 0.f;
+        const float *row = w2 + (int64_t)i * D;
+        for (int j = 0; j < D; ++j) acc = fmaf(row[j], h1[j], acc);
+        float z = acc + b2[i];
+        float h = z > 0.f ? z : 0.f;
+        c[2 * D + i] = z;
+        c[3 * D + i] = h;
+        h2[i] = h;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        float acc = 0.f;
+        for (int j = 0; j < D; ++j) acc = fmaf(w3[k * D + j], h2[j], acc);
+        psi[b * K + k] = acc + b3[k];
+    }
+}
+
+// Per frame: reduce the blend_bwd partials into g_psi (fixed order), then the
+// hidden-layer adjoints gz2, gz1 (S/model.py:151-160).
+__global__ void mlp_bwd_frame_kernel(int H, int D, int K, const float *__restrict__ mlp,
+                                     const float *__restrict__ cache,
+                                     const float *__restrict__ partials, int P,
+                                     float *__restrict__ gpsi, float *__restrict__ scratch) {
+    extern __shared__ float sm[];
+    float *gp = sm, *gz2 = gp + K;
+    const int b = blockIdx.x;
+    const int B = gridDim.x;
+    const float *w2 = mlp + D * H + D, *w3 = w2 + D * D + D;
+    const float *c = cache + (int64_t)b * 4 * D;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int k = warp; k < K; k += nw) {
+        const float *row = partials + ((int64_t)b * K + k) * P;
+        float s = 0.f;
+        for (int p = lane; p < P; p += 32) s += row[p];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            gp[k] = s;
+            gpsi[b * K + k] = s;
+        }
+    }
+    __syncthreads();
+    float *s_gz2 = scratch + (int64_t)b * D;             // [B][D]
+    float *s_gz1 = scratch + (int64_t)B * D + (int64_t)b * D;
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        float acc = 0.f;
+        for (int k = 0; k < K; ++k) acc = fmaf(w3[k * D + j], gp[k], acc);
+        float g = c[2 * D + j] > 0.f ? acc : 0.f;
+        gz2[j] = g;
+        s_gz2[j] = g;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        float acc = 0.f;
+        for (int i = 0; i < D; ++i) acc = fmaf(w2[(int64_t)i * D + j], gz2[i], acc);
+        s_gz1[j] = c[j] > 0.f ? acc : 0.f;
+    }
+}
+
+// One thread per MLP parameter, frames summed in order b = 0..B-1.
+__global__ void mlp_bwd_weights_kernel(int B, int H, int D, int K, const float *__restrict__ theta,
+                                       const float *__restrict__ cache,
+                                       const float *__restrict__ gpsi,
+                                       const float *__restrict__ scratch, float *__restrict__ g) {
+    const int64_t total = (int64_t)D * H + D + (int64_t)D * D + D + (int64_t)K * D + K;
+    const float *gz2 = scratch, *gz1 = scratch + (int64_t)B * D;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i;
+        float acc = 0.f;
+        if (r < (int64_t)D * H) {                   // w1[i][j] += gz1[i] theta[j]
+            int ii = r / H, j = r % H;
+            for (int b = 0; b < B; ++b) acc += gz1[b * D + ii] * theta[b * H + j];
+        } else if ((r -= (int64_t)D * H) < D) {     // b1
+            for (int b = 0; b < B; ++b) acc += gz1[b * D + r];
+        } else if ((r -= D) < (int64_t)D * D) {     // w2[i][j] += gz2[i] h1[j]
+            int ii = r / D, j = r % D;
+            for (int b = 0; b < B; ++b) acc += gz2[b * D + ii] * cache[(int64_t)b * 4 * D + D + j];
+        } else if ((r -= (int64_t)D * D) < D) {     // b2
+            for (int b = 0; b < B; ++b) acc += gz2[b * D + r];
+        } else if ((r -= D) < (int64_t)K * D) {     // w3[k][j] += gpsi[k] h2[j]
+            int k = r / D, j = r % D;
+            for (int b = 0; b < B; ++b) acc += gpsi[b * K + k] * cache[(int64_t)b * 4 * D + 3 * D + j];
+        } else {                                    // b3
+            r -= (int64_t)K * D;
+            for (int b = 0; b < B; ++b) acc += gpsi[b * K + r];
+        }
+        g[i] = acc;
+    }
+}
+
+// ----------------------------------------------------------------- blend
+
+// raw[b] = base + sum_k psi[b,k] delta_k over the 10N blended channels.  Each
+// thread owns VEC consecutive channels and keeps BC frames of accumulators, so
+// every delta element is read from HBM once per BC frames (once per step for
+// B <= BC).  S/model.py:165-185 (k ascending, psi == 0 skipped).
+template <int VEC, int BC>
+__global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
+                                                        const float *__restrict__ base,
+                                                        const float *__restrict__ deltas,
+                                                        const float *__restrict__ psi,
+                                                        float *__restrict__ raw) {
+    extern __shared__ float s_psi[];
+    for (int i = threadIdx.x; i < B * K; i += blockDim.x) s_psi[i] = psi[i];
+    __syncthreads();
+    const int64_t nvec = E / VEC;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = v * VEC;
+        float bv[VEC];
+        if constexpr (VEC == 4) {
+            float4 t = __ldg(reinterpret_cast<const float4 *>(base + e));
+            bv[0] = t.x; bv[1] = t.y; bv[2] = t.z; bv[3] = t.w;
+        } else {
+            bv[0] = base[e];
+        }
+        for (int b0 = 0; b0 < B; b0 += BC) {
+            const int nb = min(BC, B - b0);
+            float acc[BC][VEC];
+#pragma unroll
+            for (int j = 0; j < BC; ++j)
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) acc[j][c] = bv[c];
+            for (int k = 0; k < K; ++k) {
+                float dv[VEC];
+                if constexpr (VEC == 4) {
+                    float4 t = __ldcs(reinterpret_cast<const float4 *>(deltas + (int64_t)k * E + e));
+                    dv[0] = t.x; dv[1] = t.y; dv[2] = t.z; dv[3] = t.w;
+                } else {
+                    dv[0] = __ldcs(deltas + (int64_t)k * E + e);
+                }
+#pragma unroll
+                for (int j = 0; j < BC; ++j) {
+                    if (j < nb) {
+                        const float w = s_psi[(b0 + j) * K + k];
+                        if (w != 0.0f) {
+#pragma unroll
+                            for (int c = 0; c < VEC; ++c) acc[j][c] = fmaf(w, dv[c], acc[j][c]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < BC; ++j) {
+                if (j < nb) {
+                    float *o = raw + (int64_t)(b0 + j) * E + e;
+                    if constexpr (VEC == 4) {
+                        *reinterpret_cast<float4 *>(o) = make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+                    } else {
+                        o[0] = acc[j][0];
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Adjoint of blend, reduced over the frame batch in-kernel (S/model.py:188-216 +
+// the item-order sum of S/train.py:253-255).  A CTA owns a tile of kBE channels:
+//   g_base[e]     = sum_b g[b][e]                              (all 14N channels)
+//   g_delta[k][e] = sum_b psi[b][k] g[b][e]                    (10N blended channels)
+//   g_psi[b][k]   = sum_e delta[k][e] g[b][e]   -> one partial per tile (deterministic)
+// g and delta tiles are staged in shared memory; the g_psi contraction is register
+// blocked 4 (frames) x 4 (bases) per thread.
+constexpr int kBE = 512;
+constexpr int kBT = 256;
+constexpr int kBMaxB = 16;
+constexpr int kBMaxK = 32;
+
+__global__ void __launch_bounds__(kBT) blend_bwd_kernel(int64_t N, int K, int Bc, int b0, int Btot,
+                                                       const float *__restrict__ deltas,
+                                                       const float *__restrict__ psi,
+                                                       const float *__restrict__ g_raw,
+                                                       float *__restrict__ g_base,
+                                                       float *__restrict__ g_deltas,
+                                                       float *__restrict__ partials, int T10,
+                                                       int accumulate) {
+    extern __shared__ float sm[];
+    const int Bp = (Bc + 3) & ~3, Kp = (K + 3) & ~3;
+    float *g_s = sm;                       // [Bp][kBE]
+    float *d_s = g_s + Bp * kBE;           // [Kp][kBE]
+    float *p_s = d_s + Kp * kBE;           // [Bc][K] psi
+    float *red = p_s + Bc * K;             // [slices][Bp][Kp]
+    const int64_t E10 = 10 * N, E14 = 14 * N;
+    const int tile = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (tile >= T10) {   // scale/opacity channels: only the base gradient
+        const int64_t e0 = E10 + (int64_t)(tile - T10) * kBE;
+        for (int i = tid; i < kBE; i += kBT) {
+            const int64_t e = e0 + i;
+            if (e >= E14) break;
+            float s = accumulate ? g_base[e] : 0.f;
+            for (int b = 0; b < Bc; ++b) s += g_raw[(int64_t)(b0 + b) * E14 + e];
+            g_base[e] = s;
+        }
+        return;
+    }
+    const int64_t e0 = (int64_t)tile * kBE;
+    const int cnt = (int)min((int64_t)kBE, E10 - e0);
+    for (int i = tid; i < Bc * K; i += kBT) p_s[i] = psi[(b0 + i / K) * K + i % K];
+    for (int b = 0; b < Bp; ++b)
+        for (int i = tid; i < kBE; i += kBT)
+            g_s[b * kBE + i] = (b < Bc && i < cnt) ? g_raw[(int64_t)(b0 + b) * E14 + e0 + i] : 0.f;
+    for (int k = 0; k < Kp; ++k)
+        for (int i = tid; i < kBE; i += kBT)
+            d_s[k * kBE + i] = (k < K && i < cnt) ? __ldcs(deltas + (int64_t)k * E10 + e0 + i) : 0.f;
+    __syncthreads();
+    // phase 1: base and delta gradients, coalesced writes
+    for (int i = tid; i < cnt; i += kBT) {
+        const int64_t e = e0 + i;
+        float gv[kBMaxB];
+        float s = 0.f;
+#pragma unroll
+        for (int b = 0; b < kBMaxB; ++b) {
+            gv[b] = b < Bc ? g_s[b * kBE + i] : 0.f;
+            s += gv[b];
+        }
+        g_base[e] = accumulate ? g_base[e] + s : s;
+        for (int k = 0; k < K; ++k) {
+            float acc = 0.f;
+#pragma unroll
+            for (int b = 0; b < kBMaxB; ++b)
+                if (b < Bc) acc = fmaf(p_s[b * K + k], gv[b], acc);
+            float *o = g_deltas + (int64_t)k * E10 + e;
+            *o = accumulate ? *o + acc : acc;
+        }
+    }
+    // phase 2: g_psi partial over this tile, 4x4 register blocks
+    const int nbq = Bp / 4, nkq = Kp / 4, nsb = nbq * nkq;
+    const int slices = kBT / nsb;
+    const int sb = tid % nsb, sl = tid / nsb;
+    if (sl < slices) {
+        const int bq = sb / nkq, kq = sb % nkq;
+        const int span = (cnt + slices - 1) / slices;
+        const int i0 = sl * span, i1 = min(cnt, i0 + span);
+        float acc[4][4] = {};
+        for (int i = i0; i < i1; ++i) {
+            float gv[4], dv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                gv[j] = g_s[(bq * 4 + j) * kBE + i];
+                dv[j] = d_s[(kq * 4 + j) * kBE + i];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int l = 0; l < 4; ++l) acc[j][l] = fmaf(gv[j], dv[l], acc[j][l]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int l = 0; l < 4; ++l) red[(sl * Bp + bq * 4 + j) * Kp + kq * 4 + l] = acc[j][l];
+    }
+    __syncthreads();
+    for (int p = tid; p < Bc * K; p += kBT) {
+        const int b = p / K, k = p % K;
+        float s = 0.f;
+        for (int l = 0; l < slices; ++l) s += red[(l * Bp + b) * Kp + k];
+        partials[((int64_t)(b0 + b) * K + k) * T10 + tile] = s;
+    }
+    (void)Btot;
+}
+
+// ------------------------------------------------------------------ Adam
+
+// S/optim.py:28-40 over the whole flat parameter buffer; the learning rate of
+// each element comes from its group (S/train.py:184-199).
+__global__ void adam_kernel(int64_t total, int64_t N, int K, float *__restrict__ p,
+                            const float *__restrict__ g, float *__restrict__ m,
+                            float *__restrict__ v, float lr0, float lr1, float lr2, float lr3,
+                            float lr4, float lr5, float lr6, float lr7, float lr8, float b1,
+                            float b2, float inv_bc1, float inv_bc2, float eps) {
+    const int64_t base = 14 * N, dend = base + (int64_t)K * 10 * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float lr;
+        if (i < base) {
+            lr = i < 3 * N ? lr0 : i < 7 * N ? lr1 : i < 10 * N ? lr2 : i < 13 * N ? lr3 : lr4;
+        } else if (i < dend) {
+            int64_t j = (i - base) % (10 * N);
+            lr = j < 3 * N ? lr5 : j < 7 * N ? lr6 : lr7;
+        } else {
+            lr = lr8;
+        }
+        const float gi = g[i];
+        float mi = m[i] * b1;
+        mi = mi + (1.0f - b1) * gi;
+        float vi = v[i] * b2;
+        vi = vi + (1.0f - b2) * (gi * gi);
+        m[i] = mi;
+        v[i] = vi;
+        const float mh = mi * inv_bc1, vh = vi * inv_bc2;
+        p[i] = p[i] - lr * mh / (sqrtf(vh) + eps);
+    }
+}
+
+// ------------------------------------------------------------ colour init
+
+// S/train.py:263-278 + S/color_init.py:45-80 + S/model.py:260-263 (logit with clamp).
+__global__ void color_init_kernel(int B, int64_t N, const float *__restrict__ maxw,
+                                  const float *__restrict__ wsums, float thr,
+                                  uint8_t *__restrict__ visited, float *__restrict__ color,
+                                  int *n_init, unsigned long long *err) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    if (visited[n]) return;
+    int best = 0;
+    float bw = maxw[n];
+    for (int b = 1; b < B; ++b) {
+        float w = maxw[(int64_t)b * N + n];
+        if (w > bw) { bw = w; best = b; }   // first max wins (np.argmax)
+    }
+    if (!(bw > thr)) return;
+    const float4 s = reinterpret_cast<const float4 *>(wsums)[(int64_t)best * N + n];
+    if (s.w <= 0.f) {
+        atomicMin(err, err_code(2, best, 0, n));
+        return;
+    }
+    const float den = s.w;
+    const float est[3] = {s.x / den, s.y / den, s.z / den};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        float p = fminf(fmaxf(est[c], 1e-4f), 1.0f - 1e-4f);
+        color[3 * n + c] = logf(p) - log1pf(-p);
+    }
+    visited[n] = 1;
+    if (n_init) atomicAdd(n_init, 1);
+}
+
+// Multi-GPU colour init: order-preserving pack of (weight, -frame) into a signed
+// int64 (non-negative weights keep the top bit clear).
+__global__ void color_pack_kernel(int B, int64_t N, int frame_offset, const float *__restrict__ maxw,
+                                  const uint8_t *__restrict__ visited, int64_t *__restrict__ packed) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    unsigned long long best = 0;
+    if (!visited[n]) {
+        for (int b = 0; b < B; ++b) {
+            const float w = maxw[(int64_t)b * N + n];
+            const unsigned long long v = ((unsigned long long)__float_as_uint(fmaxf(w, 0.f)) << 32) |
+                                         (unsigned long long)(0xFFFFFFFFu - (uint32_t)(frame_offset + b));
+            best = v > best ? v : best;
+        }
+    }
+    packed[n] = (int64_t)best;
+}
+
+__global__ void color_select_kernel(int B, int64_t N, int frame_offset, const int64_t *__restrict__ packed,
+                                    const float *__restrict__ wsums, float *__restrict__ est4,
+                                    unsigned long long *err) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const unsigned long long v = (unsigned long long)packed[n];
+    const int f = (int)(0xFFFFFFFFu - (uint32_t)(v & 0xFFFFFFFFull));
+    const int b = f - frame_offset;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (v != 0ull && b >= 0 && b < B) {
+        const float4 s = reinterpret_cast<const float4 *>(wsums)[(int64_t)b * N + n];
+        if (s.w > 0.f) o = make_float4(s.x / s.w, s.y / s.w, s.z / s.w, 1.f);
+        else if (__uint_as_float((uint32_t)(v >> 32)) > 0.f) atomicMin(err, err_code(2, f, 0, n));
+    }
+    reinterpret_cast<float4 *>(est4)[n] = o;
+}
+
+__global__ void color_apply_kernel(int64_t N, const int64_t *__restrict__ packed, const float *__restrict__ est4,
+                                   float thr, uint8_t *__restrict__ visited, float *__restrict__ color,
+                                   int *n_init) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N || visited[n]) return;
+    const float w = __uint_as_float((uint32_t)((unsigned long long)packed[n] >> 32));
+    const float4 e = reinterpret_cast<const float4 *>(est4)[n];
+    if (!(w > thr) || !(e.w > 0.f)) return;
+    const float est[3] = {e.x, e.y, e.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        float p = fminf(fmaxf(est[c], 1e-4f), 1.0f - 1e-4f);
+        color[3 * n + c] = logf(p) - log1pf(-p);
+    }
+    visited[n] = 1;
+    if (n_init) atomicAdd(n_init, 1);
+}
+
+// ---------------------------------------------------------- compat ops
+
+// S/model.py:219-234 (layout [pos 3N | rot 4N | color 3N | scale 3N | opacity N])
+__global__ void activate_fwd_kernel(int64_t N, const float *__restrict__ raw, float *__restrict__ act,
+                                    unsigned long long *err) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const float *q = raw + 3 * N + 4 * n;
+    float nrm = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (!(nrm >= 1e-30f)) atomicMin(err, err_code(0, 0, 1, n));
+    for (int c = 0; c < 3; ++c) act[3 * n + c] = raw[3 * n + c];
+    for (int c = 0; c < 4; ++c) act[3 * N + 4 * n + c] = q[c] / nrm;
+    for (int c = 0; c < 3; ++c) act[7 * N + 3 * n + c] = sigmoidf_ref(raw[7 * N + 3 * n + c]);
+    for (int c = 0; c < 3; ++c) act[10 * N + 3 * n + c] = expf(raw[10 * N + 3 * n + c]);
+    act[13 * N + n] = sigmoidf_ref(raw[13 * N + n]);
+}
+
+// S/model.py:237-248
+__global__ void activate_bwd_kernel(int64_t N, const float *__restrict__ raw,
+                                    const float *__restrict__ act, const float *__restrict__ g,
+                                    float *__restrict__ o) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    for (int c = 0; c < 3; ++c) o[3 * n + c] = g[3 * n + c];
+    float q[4], gq[4], oq[4];
+    for (int c = 0; c < 4; ++c) { q[c] = raw[3 * N + 4 * n + c]; gq[c] = g[3 * N + 4 * n + c]; }
+    quat_normalize_bwd(q, gq, oq);
+    for (int c = 0; c < 4; ++c) o[3 * N + 4 * n + c] = oq[c];
+    for (int c = 0; c < 3; ++c) {
+        float a = act[7 * N + 3 * n + c];
+        o[7 * N + 3 * n + c] = g[7 * N + 3 * n + c] * a * (1.f - a);
+        o[10 * N + 3 * n + c] = g[10 * N + 3 * n + c] * act[10 * N + 3 * n + c];
+    }
+    float a = act[13 * N + n];
+    o[13 * N + n] = g[13 * N + n] * a * (1.f - a);
+}
+
+// S/binding.py:174-188
+__global__ void transform_fwd_kernel(int64_t N, const float *__restrict__ t, const float *__restrict__ frames,
+                                     const int32_t *__restrict__ tri, const float *__restrict__ bary,
+                                     float *__restrict__ w) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const float *fr = frames + (int64_t)tri[n] * kFrame;
+    const float *R = fr, *fq = fr + 9, *V = fr + 13;
+    const float x[3] = {t[3 * n], t[3 * n + 1], t[3 * n + 2]};
+    const float bb[3] = {bary[3 * n], bary[3 * n + 1], bary[3 * n + 2]};
+    for (int j = 0; j < 3; ++j)
+        w[3 * n + j] = (R[j * 3] * x[0] + R[j * 3 + 1] * x[1] + R[j * 3 + 2] * x[2]) +
+                       (bb[0] * V[j] + bb[1] * V[3 + j] + bb[2] * V[6 + j]);
+    float q[4], qf[4], qr[4];
+    for (int c = 0; c < 4; ++c) { q[c] = t[3 * N + 4 * n + c]; qf[c] = fq[c]; }
+    quat_mul(qf, q, qr);
+    float nrm = sqrtf(qr[0] * qr[0] + qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
+    for (int c = 0; c < 4; ++c) w[3 * N + 4 * n + c] = qr[c] / nrm;
+    for (int c = 0; c < 3; ++c) w[7 * N + 3 * n + c] = t[7 * N + 3 * n + c];
+    for (int c = 0; c < 3; ++c) w[10 * N + 3 * n + c] = t[10 * N + 3 * n + c];
+    w[13 * N + n] = t[13 * N + n];
+}
+
+// S/binding.py:191-204
+__global__ void transform_bwd_kernel(int64_t N, const float *__restrict__ t, const float *__restrict__ frames,
+                                     const int32_t *__restrict__ tri, const float *__restrict__ g,
+                                     float *__restrict__ o) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const float *fr = frames + (int64_t)tri[n] * kFrame;
+    const float *R = fr, *fq = fr + 9;
+    for (int i = 0; i < 3; ++i)
+        o[3 * n + i] = R[i] * g[3 * n] + R[3 + i] * g[3 * n + 1] + R[6 + i] * g[3 * n + 2];
+    float q[4], qf[4], qr[4], gq[4], gn[4], go[4];
+    for (int c = 0; c < 4; ++c) { q[c] = t[3 * N + 4 * n + c]; qf[c] = fq[c]; gq[c] = g[3 * N + 4 * n + c]; }
+    quat_mul(qf, q, qr);
+    quat_normalize_bwd(qr, gq, gn);
+    quat_mul_bwd_right(qf, gn, go);
+    for (int c = 0; c < 4; ++c) o[3 * N + 4 * n + c] = go[c];
+    for (int c = 0; c < 3; ++c) o[7 * N + 3 * n + c] = g[7 * N + 3 * n + c];
+    for (int c = 0; c < 3; ++c) o[10 * N + 3 * n + c] = g[10 * N + 3 * n + c];
+    o[13 * N + n] = g[13 * N + n];
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" {
+
+const char *hs_last_error(void) { return g_err; }
+int hs_version(void) { return 1; }
+
+int hs_device_sm_count(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+    return v;
+}
+
+int64_t hs_mlp_size(int H, int D, int K) {
+    return (int64_t)D * H + D + (int64_t)D * D + D + (int64_t)K * D + K;
+}
+
+int hs_mlp_fwd(int B, int H, int D, int K, const float *mlp, const float *theta, float *cache,
+               float *psi, unsigned long long *err, void *stream) {
+    if (B < 1 || H < 1 || D < 1 || K < 1) {
+        set_error("hs_mlp_fwd: bad sizes B=%d H=%d D=%d K=%d", B, H, D, K);
+        return HS_ERR_SHAPE;
+    }
+    int threads = D < 128 ? 128 : (D > 1024 ? 1024 : ((D + 31) / 32) * 32);
+    size_t smem = sizeof(float) * (H + 2 * D);
+    mlp_fwd_kernel<<<B, threads, smem, HS_CHECK_STREAM(stream)>>>(H, D, K, mlp, theta, cache, psi, err);
+    return check_launch("hs_mlp_fwd");
+}
+
+int hs_mlp_bwd(int B, int H, int D, int K, const float *mlp, const float *theta, const float *cache,
+               const float *gpsi_partials, int num_partials, float *gpsi, float *scratch, float *g_mlp,
+               void *stream) {
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    size_t smem = sizeof(float) * (K + D);
+    mlp_bwd_frame_kernel<<<B, 256, smem, s>>>(H, D, K, mlp, cache, gpsi_partials, num_partials, gpsi, scratch);
+    int64_t total = hs_mlp_size(H, D, K);
+    mlp_bwd_weights_kernel<<<grid_for(total, 256), 256, 0, s>>>(B, H, D, K, theta, cache, gpsi, scratch, g_mlp);
+    return check_launch("hs_mlp_bwd");
+}
+
+int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *deltas, const float *psi,
+                 float *raw10, void *stream) {
+    if (N < 1 || K < 1 || B < 1) {
+        set_error("hs_blend_fwd: bad sizes N=%lld K=%d B=%d", (long long)N, K, B);
+        return HS_ERR_SHAPE;
+    }
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    const int64_t E = 10 * N;
+    size_t smem = sizeof(float) * B * K;
+    const bool vec = (E % 4 == 0) && ((uintptr_t)base14 % 16 == 0) && ((uintptr_t)deltas % 16 == 0) &&
+                     ((uintptr_t)raw10 % 16 == 0);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (vec) {
+        int64_t nv = E / 4;
+        unsigned grid = (unsigned)std::min<int64_t>(grid_for(nv, 256), (int64_t)sms * 8);
+        blend_fwd_kernel<4, 16><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
+    } else {
+        unsigned grid = (unsigned)std::min<int64_t>(grid_for(E, 256), (int64_t)sms * 8);
+        blend_fwd_kernel<1, 16><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
+    }
+    return check_launch("hs_blend_fwd");
+}
+
+int hs_blend_bwd_partials(int64_t N) { return (int)((10 * N + kBE - 1) / kBE); }
+
+int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi, const float *g_raw14,
+                 float *g_base14, float *g_deltas, float *gpsi_partials, int *num_partials, void *stream) {
+    if (K > kBMaxK || K < 1 || B < 1 || N < 1) {
+        set_error("hs_blend_bwd: unsupported sizes N=%lld K=%d (max %d) B=%d", (long long)N, K, kBMaxK, B);
+        return HS_ERR_SHAPE;
+    }
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    const int T10 = hs_blend_bwd_partials(N);
+    const int T4 = (int)((4 * N + kBE - 1) / kBE);
+    const int Kp = (K + 3) & ~3;
+    for (int b0 = 0; b0 < B; b0 += kBMaxB) {
+        const int Bc = std::min(kBMaxB, B - b0);
+        const int Bp = (Bc + 3) & ~3;
+        const int nsb = (Bp / 4) * (Kp / 4);
+        const int slices = kBT / nsb;
+        size_t smem = sizeof(float) * ((size_t)(Bp + Kp) * kBE + Bc * K + (size_t)slices * Bp * Kp);
+        cudaFuncSetAttribute(blend_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        blend_bwd_kernel<<<T10 + T4, kBT, smem, s>>>(N, K, Bc, b0, B, deltas, psi, g_raw14, g_base14,
+                                                      g_deltas, gpsi_partials, T10, b0 > 0);
+    }
+    if (num_partials) *num_partials = T10;
+    return check_launch("hs_blend_bwd");
+}
+
+int hs_adam(int64_t N, int K, int64_t mlp_size, float *params, const float *grads, float *m, float *v,
+            const float *lrs, int step, float beta1, float beta2, float eps, void *stream) {
+    if (step < 1) {
+        set_error("hs_adam: step must be >= 1");
+        return HS_ERR_SHAPE;
+    }
+    const int64_t total = 14 * N + (int64_t)K * 10 * N + mlp_size;
+    const double bc1 = 1.0 - std::pow((double)beta1, step);
+    const double bc2 = 1.0 - std::pow((double)beta2, step);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    unsigned grid = (unsigned)std::min<int64_t>(grid_for(total, 256), (int64_t)sms * 16);
+    adam_kernel<<<grid, 256, 0, HS_CHECK_STREAM(stream)>>>(
+        total, N, K, params, grads, m, v, lrs[0], lrs[1], lrs[2], lrs[3], lrs[4], lrs[5], lrs[6], lrs[7],
+        lrs[8], beta1, beta2, (float)(1.0 / bc1), (float)(1.0 / bc2), eps);
+    return check_launch("hs_adam");
+}
+
+int hs_color_init(int B, int64_t N, const float *maxw, const float *wsums, float threshold,
+                  uint8_t *visited, float *params, int *n_init, unsigned long long *err, void *stream) {
+    color_init_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(
+        B, N, maxw, wsums, threshold, visited, params + 7 * N, n_init, err);
+    return check_launch("hs_color_init");
+}
+
+int hs_color_pack(int B, int64_t N, int frame_offset, const float *maxw, const uint8_t *visited, int64_t *packed,
+                  void *stream) {
+    color_pack_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(B, N, frame_offset, maxw, visited,
+                                                                              packed);
+    return check_launch("hs_color_pack");
+}
+
+int hs_color_select(int B, int64_t N, int frame_offset, const int64_t *packed, const float *wsums, float *est4,
+                    unsigned long long *err, void *stream) {
+    color_select_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(B, N, frame_offset, packed, wsums,
+                                                                                est4, err);
+    return check_launch("hs_color_select");
+}
+
+int hs_color_apply(int64_t N, const int64_t *packed, const float *est4, float threshold, uint8_t *visited,
+                   float *params, int *n_init, void *stream) {
+    color_apply_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, packed, est4, threshold, visited,
+                                                                               params + 7 * N, n_init);
+    return check_launch("hs_color_apply");
+}
+
+int hs_activate_fwd(int64_t N, const float *raw14, float *act14, unsigned long long *err, void *stream) {
+    activate_fwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, raw14, act14, err);
+    return check_launch("hs_activate_fwd");
+}
+
+int hs_activate_bwd(int64_t N, const float *raw14, const float *act14, const float *g_act14, float *g_raw14,
+                    void *stream) {
+    activate_bwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, raw14, act14, g_act14, g_raw14);
+    return check_launch("hs_activate_bwd");
+}
+
+int hs_transform_fwd(int64_t N, const float *tangent14, const float *frames, const int32_t *tri_index,
+                     const float *bary, float *world14, void *stream) {
+    transform_fwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, tangent14, frames, tri_index,
+                                                                                  bary, world14);
+    return check_launch("hs_transform_fwd");
+}
+
+int hs_transform_bwd(int64_t N, const float *tangent14, const float *frames, const int32_t *tri_index,
+                     const float *g_world14, float *g_tangent14, void *stream) {
+    transform_bwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, tangent14, frames, tri_index,
+                                                                                  g_world14, g_tangent14);
+    return check_launch("hs_transform_bwd");
+}
+
+}  // extern "C"

@@ -1,0 +1,434 @@
+// hs_raster.cu -- tile rasterizer (forward + adjoint) on sm_100a.
+//
+// One 256-thread CTA per (frame, 16x16 tile); one pixel per thread.  The
+// frame's depth-sorted key range for the tile is walked in chunks of 256 splat
+// records staged in shared memory (one coalesced gather per chunk, broadcast
+// reads in the inner loop).  Per pixel the math is exactly the reference's
+// front-to-back compositing (S/render.py:233-273): same bbox test, q / qmax and
+// alpha >= 1/255 cutoffs, no alpha clamp, termination at T < 1e-14 with the stop
+// index recorded for the adjoint.  Fused epilogue: background (:402), the L1
+// loss and its sign (S/metrics.py:10-22, :80-85, S/train.py:238-247), the black
+// background L1, and -- for colour init -- per-(frame, Gaussian) max blend weight
+// and the Eq. 3 weight sums (S/render.py:339-377) reduced across the warp with
+// shuffles before one atomic per warp.
+//
+// The adjoint (S/render.py:276-336) walks the same range back to front per pixel
+// with the suffix recurrence, reduces the 9 per-splat gradients across each warp
+// with xor shuffles and issues one atomic per attribute per warp.
+#include "hs_common.cuh"
+
+namespace hs {
+
+constexpr int kRT = kTile * kTile;   // 256 pixels / threads per CTA
+
+struct RasterArgs {
+    int B;
+    int64_t N;
+    int W, H, tiles_x, tile_bits;
+    const float *records;
+    const uint32_t *vals;
+    const uint32_t *ranges;
+    const float *bgs;
+    const uint8_t *targets;
+    const float *wsum_image;
+    const uint8_t *visited;
+    float *pix_T;
+    uint32_t *pix_state;
+    float *image;
+    float *maxw;
+    float *wsums;
+    float *loss_partials;
+    // backward
+    const float *grad_image;
+    float grad_scale;
+    float *g_splat;
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
+//     3 max weight + weight sums for splats whose Gaussian is not yet visited.
+template <bool kLoss, bool kImage, int CI>
+__global__ void __launch_bounds__(kRT) raster_fwd_kernel(RasterArgs a) {
+    __shared__ float4 s_a[kRT], s_b[kRT], s_c[kRT];
+    __shared__ uint32_t s_n[kRT];
+    __shared__ float red[2][kRT / 32];
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x, b = blockIdx.y;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid / kTile);
+    const bool inside = px < a.W && py < a.H;
+    const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
+    const uint32_t start = rg.x, end = rg.y;
+    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+    const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
+
+    float tgt[3] = {0.f, 0.f, 0.f}, rgba_a = 0.f, rgb[3] = {0.f, 0.f, 0.f};
+    const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
+    if ((kLoss || CI >= 2) && inside && a.targets) {
+        const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
+        rgba_a = (float)t.w / 255.0f;
+        rgb[0] = (float)t.x / 255.0f;
+        rgb[1] = (float)t.y / 255.0f;
+        rgb[2] = (float)t.z / 255.0f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tgt[c] = rgb[c] * rgba_a + (1.0f - rgba_a) * bg[c];
+    }
+    float ws_src[3] = {tgt[0], tgt[1], tgt[2]};
+    if (CI >= 2 && a.wsum_image && inside) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ws_src[c] = a.wsum_image[pix * 3 + c];
+    }
+
+    float T = 1.0f, C[3] = {0.f, 0.f, 0.f};
+    uint32_t stop = end - start;
+    bool done = !inside;
+    for (uint32_t c0 = start; c0 < end; c0 += kRT) {
+        if (__syncthreads_count(!done) == 0) break;
+        const uint32_t idx = c0 + tid;
+        if (idx < end) {
+            const uint32_t n = a.vals[idx];
+            const float4 *r = reinterpret_cast<const float4 *>(a.records + ((int64_t)b * a.N + n) * kRec);
+            s_a[tid] = __ldg(r);
+            s_b[tid] = __ldg(r + 1);
+            s_c[tid] = __ldg(r + 2);
+            uint32_t flag = n;
+            if (CI == 3 && a.visited[n]) flag |= 0x80000000u;   // visited: skip colour-init work
+            s_n[tid] = flag;
+        }
+        __syncthreads();
+        const int cnt = (int)min((uint32_t)kRT, end - c0);
+        for (int j = 0; j < cnt; ++j) {
+            float w = 0.f;
+            if (!done) {
+                const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
+                const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
+                if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) && px <= unpack_hi(cols)) {
+                    const float dx = fpx - A.x, dy = fpy - A.y;
+                    const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
+                    if (q <= Bv.z) {
+                        const float alpha = Bv.y * __expf(-0.5f * q);
+                        if (alpha >= kAlphaCutoff) {
+                            w = alpha * T;
+                            C[0] += w * Cv.y;
+                            C[1] += w * Cv.z;
+                            C[2] += w * Cv.w;
+                            T = T * (1.0f - alpha);
+                            if (T < kTermEps) {
+                                done = true;
+                                stop = c0 - start + (uint32_t)j + 1u;
+                            }
+                        }
+                    }
+                }
+            }
+            if (CI > 0) {
+                const uint32_t flag = s_n[j];
+                const bool want = CI != 3 || !(flag & 0x80000000u);
+                if (want && __any_sync(0xffffffffu, w > 0.f)) {
+                    const int64_t g = (int64_t)b * a.N + (flag & 0x7FFFFFFFu);
+                    const float wm = warp_max(w);
+                    if (CI >= 2) {
+                        const float s0 = warp_sum(w * ws_src[0]);
+                        const float s1 = warp_sum(w * ws_src[1]);
+                        const float s2 = warp_sum(w * ws_src[2]);
+                        const float sw = warp_sum(w);
+                        const int lane = tid & 31;
+                        if (lane < 4) {
+                            const float v = lane == 0 ? s0 : lane == 1 ? s1 : lane == 2 ? s2 : sw;
+                            atomicAdd(a.wsums + g * 4 + lane, v);
+                        }
+                    }
+                    if ((tid & 31) == 0) atomicMax(reinterpret_cast<int *>(a.maxw) + g, __float_as_int(wm));
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    float l1 = 0.f, black = 0.f;
+    if (inside) {
+        float pred[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pred[c] = C[c] + T * bg[c];
+        uint32_t signs = 0;
+        if (kLoss) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float d = pred[c] - tgt[c];
+                l1 += fabsf(d);
+                black += fabsf(C[c] - rgb[c] * rgba_a);
+                signs |= (d > 0.f ? 1u : d < 0.f ? 2u : 0u) << (2 * c);
+            }
+        }
+        a.pix_T[pix] = T;
+        a.pix_state[pix] = stop | (signs << 26);
+        if (kImage) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) a.image[pix * 3 + c] = pred[c];
+        }
+    }
+    if (kLoss) {
+        l1 = warp_sum(l1);
+        black = warp_sum(black);
+        if ((tid & 31) == 0) {
+            red[0][tid >> 5] = l1;
+            red[1][tid >> 5] = black;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            float s0 = 0.f, s1 = 0.f;
+            for (int i = 0; i < kRT / 32; ++i) { s0 += red[0][i]; s1 += red[1][i]; }
+            const int tiles = gridDim.x;
+            a.loss_partials[((int64_t)b * tiles + tile) * 2] = s0;
+            a.loss_partials[((int64_t)b * tiles + tile) * 2 + 1] = s1;
+        }
+    }
+}
+
+template <bool kExplicitGrad>
+__global__ void __launch_bounds__(kRT) raster_bwd_kernel(RasterArgs a) {
+    __shared__ float4 s_a[kRT], s_b[kRT], s_c[kRT];
+    __shared__ uint32_t s_n[kRT];
+    __shared__ uint32_t s_max[kRT / 32];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int tile = blockIdx.x, b = blockIdx.y;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid / kTile);
+    const bool inside = px < a.W && py < a.H;
+    const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
+    const uint32_t start = rg.x, end = rg.y;
+    if (start >= end) return;
+    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+    const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
+
+    float g[3] = {0.f, 0.f, 0.f};
+    uint32_t stop = 0;
+    float t_rev = 0.f, suffix = 0.f;
+    if (inside) {
+        const uint32_t st = a.pix_state[pix];
+        stop = st & kStopMask;
+        const float Tf = a.pix_T[pix];
+        if (kExplicitGrad) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[c] = a.grad_image[pix * 3 + c];
+        } else {
+            const uint32_t sg = st >> 26;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const uint32_t s2 = (sg >> (2 * c)) & 3u;
+                g[c] = s2 == 1u ? a.grad_scale : s2 == 2u ? -a.grad_scale : 0.f;
+            }
+        }
+        t_rev = Tf;
+        suffix = Tf * (g[0] * a.bgs[3 * b] + g[1] * a.bgs[3 * b + 1] + g[2] * a.bgs[3 * b + 2]);
+    }
+    // last local index any pixel of the tile needs
+    const uint32_t wmax = __reduce_max_sync(0xffffffffu, stop);
+    if (lane == 0) s_max[tid >> 5] = wmax;
+    __syncthreads();
+    uint32_t maxstop = 0;
+#pragma unroll
+    for (int i = 0; i < kRT / 32; ++i) maxstop = max(maxstop, s_max[i]);
+    const uint32_t last = start + maxstop;
+
+    for (uint32_t c_end = last; c_end > start;) {
+        const uint32_t c0 = c_end - start > (uint32_t)kRT ? c_end - kRT : start;
+        const uint32_t idx = c0 + tid;
+        __syncthreads();
+        if (idx < c_end) {
+            const uint32_t n = a.vals[idx];
+            const float4 *r = reinterpret_cast<const float4 *>(a.records + ((int64_t)b * a.N + n) * kRec);
+            s_a[tid] = __ldg(r);
+            s_b[tid] = __ldg(r + 1);
+            s_c[tid] = __ldg(r + 2);
+            s_n[tid] = n;
+        }
+        __syncthreads();
+        for (int j = (int)(c_end - c0) - 1; j >= 0; --j) {
+            const uint32_t jl = c0 - start + (uint32_t)j;
+            float gv[9];
+            bool contrib = false;
+            if (jl < stop) {
+                const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
+                const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
+                if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) && px <= unpack_hi(cols)) {
+                    const float dx = fpx - A.x, dy = fpy - A.y;
+                    const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
+                    if (q <= Bv.z) {
+                        const float G = __expf(-0.5f * q);
+                        const float alpha = Bv.y * G;
+                        if (alpha >= kAlphaCutoff) {
+                            contrib = true;
+                            const float one_m = 1.0f - alpha;
+                            const float t_prior = t_rev / one_m;
+                            const float gw = g[0] * Cv.y + g[1] * Cv.z + g[2] * Cv.w;
+                            const float wgt = alpha * t_prior;
+                            gv[6] = wgt * g[0];
+                            gv[7] = wgt * g[1];
+                            gv[8] = wgt * g[2];
+                            const float d_alpha = t_prior * gw - suffix / one_m;
+                            gv[5] = G * d_alpha;
+                            const float dq = -0.5f * alpha * d_alpha;
+                            gv[2] = dq * dx * dx;
+                            gv[3] = 2.0f * dq * dx * dy;
+                            gv[4] = dq * dy * dy;
+                            gv[0] = -2.0f * dq * (A.z * dx + A.w * dy);
+                            gv[1] = -2.0f * dq * (A.w * dx + Bv.x * dy);
+                            suffix += wgt * gw;
+                            t_rev = t_prior;
+                        }
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, contrib)) {
+                if (!contrib) {
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) gv[k] = 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < 9; ++k) gv[k] = warp_sum(gv[k]);
+                if (lane < 9) {
+                    float v = gv[0];
+#pragma unroll
+                    for (int k = 1; k < 9; ++k) v = lane == k ? gv[k] : v;
+                    atomicAdd(a.g_splat + ((int64_t)b * a.N + s_n[j]) * kGS + lane, v);
+                }
+            }
+        }
+        c_end = c0;
+    }
+}
+
+__global__ void loss_reduce_kernel(int B, int tiles, float inv_count, const float *__restrict__ partials,
+                                   float *__restrict__ out) {
+    __shared__ float red[2][32];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    float s0 = 0.f, s1 = 0.f;
+    for (int t = tid; t < tiles; t += blockDim.x) {
+        s0 += partials[((int64_t)b * tiles + t) * 2];
+        s1 += partials[((int64_t)b * tiles + t) * 2 + 1];
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if ((tid & 31) == 0) { red[0][tid >> 5] = s0; red[1][tid >> 5] = s1; }
+    __syncthreads();
+    if (tid == 0) {
+        float a0 = 0.f, a1 = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a0 += red[0][i]; a1 += red[1][i]; }
+        out[b] = a0 * inv_count;
+        out[B + b] = a1 * inv_count;
+    }
+}
+
+__global__ void loss_mean_kernel(int B, float *__restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        float s = 0.f;
+        for (int b = 0; b < B; ++b) s += out[b];
+        out[2 * B] = s / (float)B;
+    }
+}
+
+static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records, const uint32_t *values,
+                            const uint32_t *ranges, int tile_bits, const float *bgs) {
+    RasterArgs a{};
+    a.B = B;
+    a.N = N;
+    a.W = W;
+    a.H = H;
+    a.tiles_x = (W + kTile - 1) / kTile;
+    a.tile_bits = tile_bits;
+    a.records = records;
+    a.vals = values;
+    a.ranges = ranges;
+    a.bgs = bgs;
+    return a;
+}
+
+template <bool L, bool I>
+static void launch_fwd_ci(int ci, dim3 grid, cudaStream_t s, const RasterArgs &a) {
+    switch (ci) {
+        case 0: raster_fwd_kernel<L, I, 0><<<grid, kRT, 0, s>>>(a); break;
+        case 1: raster_fwd_kernel<L, I, 1><<<grid, kRT, 0, s>>>(a); break;
+        case 2: raster_fwd_kernel<L, I, 2><<<grid, kRT, 0, s>>>(a); break;
+        default: raster_fwd_kernel<L, I, 3><<<grid, kRT, 0, s>>>(a); break;
+    }
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" {
+
+int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records, const uint32_t *values,
+                  const uint32_t *ranges, int tile_bits, const float *backgrounds, const uint8_t *targets,
+                  const float *wsum_image, const uint8_t *visited, float *pix_T, uint32_t *pix_state, float *image,
+                  float *maxw, float *wsums, float *loss_partials, void *stream) {
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const bool loss = flags & HS_RASTER_LOSS, img = flags & HS_RASTER_IMAGE;
+    int ci = 0;
+    if (flags & HS_RASTER_MAXW_UNVISITED) ci = 3;
+    else if ((flags & HS_RASTER_MAXW_ALL) && (flags & HS_RASTER_WSUMS)) ci = 2;
+    else if (flags & HS_RASTER_MAXW_ALL) ci = 1;
+    if ((loss && !targets) || (img && !image) || (ci && !maxw) || (ci >= 2 && !wsums) || (ci == 3 && !visited) ||
+        (ci >= 2 && !targets && !wsum_image) || (loss && !loss_partials)) {
+        set_error("hs_raster_fwd: flags 0x%x need a buffer that is NULL", flags);
+        return HS_ERR_SHAPE;
+    }
+    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds);
+    a.targets = targets;
+    a.wsum_image = (flags & HS_RASTER_WSUMS_IMAGE) ? wsum_image : nullptr;
+    a.visited = visited;
+    a.pix_T = pix_T;
+    a.pix_state = pix_state;
+    a.image = image;
+    a.maxw = maxw;
+    a.wsums = wsums;
+    a.loss_partials = loss_partials;
+    dim3 grid(tiles_x * tiles_y, B);
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    if (loss && img) launch_fwd_ci<true, true>(ci, grid, s, a);
+    else if (loss) launch_fwd_ci<true, false>(ci, grid, s, a);
+    else if (img) launch_fwd_ci<false, true>(ci, grid, s, a);
+    else launch_fwd_ci<false, false>(ci, grid, s, a);
+    return check_launch("hs_raster_fwd");
+}
+
+int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records, const uint32_t *values,
+                  const uint32_t *ranges, int tile_bits, const float *backgrounds, const float *pix_T,
+                  const uint32_t *pix_state, const float *grad_image, float grad_scale, float *g_splat,
+                  void *stream) {
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds);
+    a.pix_T = const_cast<float *>(pix_T);
+    a.pix_state = const_cast<uint32_t *>(pix_state);
+    a.grad_image = grad_image;
+    a.grad_scale = grad_scale;
+    a.g_splat = g_splat;
+    dim3 grid(tiles_x * tiles_y, B);
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a);
+    else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a);
+    return check_launch("hs_raster_bwd");
+}
+
+int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *loss_partials, float *loss_out,
+                   void *stream) {
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    const float inv = (float)(1.0 / ((double)width * height * 3.0));
+    loss_reduce_kernel<<<B, 256, 0, s>>>(B, num_tiles, inv, loss_partials, loss_out);
+    loss_mean_kernel<<<1, 32, 0, s>>>(B, loss_out);
+    return check_launch("hs_loss_reduce");
+}
+
+}  // extern "C"

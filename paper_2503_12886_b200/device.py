@@ -1,0 +1,521 @@
+"""Device-resident training / rendering on one B200 (the fast API: torch tensors in, no host copies).
+
+This is the B200 replacement of the reference's ``train_step`` (S/train.py:214-260)
+and its render path (S/dataset.py:163-172, S/train.py:333-339).  The frame batch
+is a grid dimension of every kernel: one launch per stage per batch, and exactly
+ONE device->host read per step (the key total + error word after the tile-count
+scan, needed to size the sort), mirroring the paper's single GPU->CPU sync
+between the projection and rasterization stages (PAPER.md:156,
+S/scheduler.py:64-72).
+
+Step (N Gaussians, K bases, B frames):
+  mlp_fwd -> blend_fwd -> project_avatar_fwd (+ tile counts) -> bin_scan -> [sync]
+  -> bin_emit -> sort_pairs -> tile_ranges -> raster_fwd (+ L1 loss, colour-init
+  sums) -> loss_reduce -> raster_bwd -> project_avatar_bwd -> blend_bwd -> mlp_bwd
+  -> [allreduce of the flat gradient, multi-GPU] -> adam -> colour init.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+ATTRS = ("position", "rotation", "scale", "opacity", "color")
+ADAM_BETAS = (0.9, 0.999)       # S/optim.py:19-21
+ADAM_EPS = 1e-8
+TILE = 16
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2503_12886_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    L.load()
+
+
+def default_lrs(lr_position=0.0008, lr_opacity=0.25, lr_scale=0.025, lr_rotation=0.005, lr_color=0.0125,
+                delta_position_scale=0.05, delta_rotation_scale=0.5, delta_color_scale=0.5, lr_mlp=0.001):
+    """Per-group learning rates in hs_adam order (S/train.py:43-51, :63-68):
+    base position, rotation, color, scale, opacity, delta position, rotation, color, mlp."""
+    return [lr_position, lr_rotation, lr_color, lr_scale, lr_opacity, lr_position * delta_position_scale,
+            lr_rotation * delta_rotation_scale, lr_color * delta_color_scale, lr_mlp]
+
+
+def lrs_from_config(cfg):
+    """Learning rates from a reference-style TrainConfig (duck typed)."""
+    return default_lrs(cfg.lr_position, cfg.lr_opacity, cfg.lr_scale, cfg.lr_rotation, cfg.lr_color,
+                       cfg.delta_position_scale, cfg.delta_rotation_scale, cfg.delta_color_scale, cfg.lr_mlp)
+
+
+def key_layout(batch, width, height):
+    tiles_x = (width + TILE - 1) // TILE
+    tiles_y = (height + TILE - 1) // TILE
+    tiles = tiles_x * tiles_y
+    tile_bits = int(tiles - 1).bit_length()
+    frame_bits = int(batch - 1).bit_length()
+    return tiles_x, tiles_y, tiles, tile_bits, frame_bits
+
+
+def camera_array(camera) -> np.ndarray:
+    """(16,) float32 [R 9 | t 3 | fx fy cx cy] from a reference-style Camera (S/render.py:40-84)."""
+    return np.concatenate([np.asarray(camera.rotation, np.float64).ravel(),
+                           np.asarray(camera.translation, np.float64).ravel(),
+                           [camera.fx, camera.fy, camera.cx, camera.cy]]).astype(np.float32)
+
+
+def frames_array(frames) -> np.ndarray:
+    """(F, 22) float32 from a reference-style MeshFrames (S/binding.py:47-53)."""
+    f = np.asarray(frames.rotation).shape[0]
+    return np.concatenate([np.asarray(frames.rotation, np.float64).reshape(f, 9),
+                           np.asarray(frames.quat, np.float64).reshape(f, 4),
+                           np.asarray(frames.tri_vertices, np.float64).reshape(f, 9)], axis=1).astype(np.float32)
+
+
+# --------------------------------------------------------------------- model
+
+class AvatarParams:
+    """Device-resident reduced-blendshape avatar (S/model.py:98-127 AvatarModel).
+
+    params: flat fp32 [base 14N | deltas K*10N | mlp] (include/hs_api.h layout),
+    tri_index int32 (N,), barycentric fp32 (N, 3).
+    """
+
+    def __init__(self, N, K, H, D, device="cuda"):
+        require_cuda()
+        self.N, self.K, self.H, self.D = int(N), int(K), int(H), int(D)
+        self.mlp_size = int(L.load().hs_mlp_size(self.H, self.D, self.K))
+        self.size = 14 * self.N + 10 * self.K * self.N + self.mlp_size
+        self.device = torch.device(device)
+        self.params = torch.zeros(self.size, dtype=torch.float32, device=self.device)
+        self.tri_index = torch.zeros(self.N, dtype=torch.int32, device=self.device)
+        self.barycentric = torch.zeros(self.N, 3, dtype=torch.float32, device=self.device)
+
+    # views ------------------------------------------------------------
+    @property
+    def base14(self):
+        return self.params[:14 * self.N]
+
+    @property
+    def deltas(self):
+        return self.params[14 * self.N:14 * self.N + 10 * self.K * self.N]
+
+    @property
+    def mlp(self):
+        return self.params[14 * self.N + 10 * self.K * self.N:]
+
+    def base_view(self, name):
+        n = self.N
+        off = {"position": (0, 3), "rotation": (3 * n, 4), "color": (7 * n, 3), "scale": (10 * n, 3),
+               "opacity": (13 * n, 1)}[name]
+        v = self.params[off[0]:off[0] + off[1] * n]
+        return v if name == "opacity" else v.view(n, off[1])
+
+    # conversion -------------------------------------------------------
+    @staticmethod
+    def pack_base(base) -> np.ndarray:
+        return np.concatenate([np.asarray(base.position).ravel(), np.asarray(base.rotation).ravel(),
+                               np.asarray(base.color).ravel(), np.asarray(base.scale).ravel(),
+                               np.asarray(base.opacity).ravel()])
+
+    @staticmethod
+    def pack_deltas(deltas) -> np.ndarray:
+        if isinstance(deltas, np.ndarray):
+            return deltas.reshape(-1)
+        return np.concatenate([np.concatenate([np.asarray(d.position).ravel(), np.asarray(d.rotation).ravel(),
+                                               np.asarray(d.color).ravel()]) for d in deltas])
+
+    @staticmethod
+    def pack_mlp(mlp) -> np.ndarray:
+        get = (lambda k: mlp[k]) if isinstance(mlp, dict) else (lambda k: getattr(mlp, k))
+        return np.concatenate([np.asarray(get(k)).ravel() for k in ("w1", "b1", "w2", "b2", "w3", "b3")])
+
+    @classmethod
+    def from_host(cls, base, deltas, mlp, tri_index, barycentric, device="cuda"):
+        """From reference-style objects (GaussianSet, list[DeltaSet] or (K,10N) array,
+        MlpWeights or dict, bindings arrays)."""
+        get = (lambda k: mlp[k]) if isinstance(mlp, dict) else (lambda k: getattr(mlp, k))
+        w1 = np.asarray(get("w1"))
+        N = np.asarray(base.position).shape[0]
+        K = np.asarray(get("w3")).shape[0]
+        self = cls(N, K, w1.shape[1], w1.shape[0], device)
+        self.load_host(base, deltas, mlp)
+        self.tri_index.copy_(torch.from_numpy(np.asarray(tri_index, np.int32)))
+        self.barycentric.copy_(torch.from_numpy(np.asarray(barycentric, np.float32).reshape(N, 3)))
+        return self
+
+    def load_host(self, base, deltas, mlp):
+        flat = np.concatenate([self.pack_base(base), self.pack_deltas(deltas), self.pack_mlp(mlp)]).astype(np.float32)
+        if flat.size != self.size:
+            raise ValueError(f"parameter count {flat.size} != {self.size}")
+        self.params.copy_(torch.from_numpy(flat))
+
+    def host_flat(self) -> np.ndarray:
+        return self.params.detach().cpu().numpy()
+
+    def split_host(self, flat=None):
+        """(base dict, deltas (K,10N), mlp dict) float64 numpy from the device copy."""
+        flat = self.host_flat() if flat is None else flat
+        return split_flat(flat, self.N, self.K, self.H, self.D)
+
+
+def split_flat(flat, N, K, H, D):
+    flat = np.asarray(flat, np.float64)
+    n = N
+    base = {"position": flat[0:3 * n].reshape(n, 3), "rotation": flat[3 * n:7 * n].reshape(n, 4),
+            "color": flat[7 * n:10 * n].reshape(n, 3), "scale": flat[10 * n:13 * n].reshape(n, 3),
+            "opacity": flat[13 * n:14 * n].copy()}
+    o = 14 * n
+    deltas = flat[o:o + 10 * K * n].reshape(K, 10 * n)
+    o += 10 * K * n
+    mlp = {}
+    for k, shape in (("w1", (D, H)), ("b1", (D,)), ("w2", (D, D)), ("b2", (D,)), ("w3", (K, D)), ("b3", (K,))):
+        sz = int(np.prod(shape))
+        mlp[k] = flat[o:o + sz].reshape(shape)
+        o += sz
+    return base, deltas, mlp
+
+
+# -------------------------------------------------------------------- binning
+
+class Binner:
+    """Batched tile binning shared by training, rendering and the compat path:
+    project-stage outputs -> (keys, values, ranges) with one host read."""
+
+    def __init__(self, device):
+        self.device = device
+        self.cap = 0
+        self.keys = self.vals = self.keys_alt = self.vals_alt = self.ws = None
+        self.summary_host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        self.offsets = None
+        self.summary = torch.empty(2, dtype=torch.int64, device=device)
+        self.ranges = None
+        self.result = None
+
+    def _ensure(self, total):
+        if total <= self.cap:
+            return
+        cap = max(int(total * 1.25) + 1024, 1 << 16)
+        d = self.device
+        self.keys = torch.empty(cap, dtype=torch.int64, device=d)
+        self.keys_alt = torch.empty(cap, dtype=torch.int64, device=d)
+        self.vals = torch.empty(cap, dtype=torch.int32, device=d)
+        self.vals_alt = torch.empty(cap, dtype=torch.int32, device=d)
+        ws = int(L.load().hs_sort_workspace_size(cap))
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=d)
+        self.cap = cap
+
+    def scan(self, block_sums, nblocks, err):
+        """Exclusive scan of the per-block tile counts + the step's single D2H read."""
+        if self.offsets is None or self.offsets.numel() < nblocks:
+            self.offsets = torch.empty(max(nblocks, 1), dtype=torch.int32, device=self.device)
+        L.call("hs_bin_scan", nblocks, _p(block_sums), _p(self.offsets), _p(err), _p(self.summary), _stream())
+        self.summary_host.copy_(self.summary, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        total = int(self.summary_host[0])
+        code = int(self.summary_host[1]) & 0xFFFFFFFFFFFFFFFF
+        return total, code
+
+    def bin(self, B, N, width, height, records, depth, counts, total):
+        tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
+        self._ensure(total)
+        s = _stream()
+        nr = B << tile_bits
+        if self.ranges is None or self.ranges.numel() < 2 * nr:
+            self.ranges = torch.empty(2 * nr, dtype=torch.int32, device=self.device)
+        ranges = self.ranges[:2 * nr]
+        ranges.zero_()
+        if total:
+            L.call("hs_bin_emit", B, N, width, height, _p(records), _p(depth), _p(counts), _p(self.offsets),
+                   _p(self.keys), _p(self.vals), s)
+            alt = ctypes.c_int(0)
+            L.call("hs_sort_pairs", total, 32 + tile_bits + frame_bits, _p(self.keys), _p(self.vals),
+                   _p(self.keys_alt), _p(self.vals_alt), _p(self.ws), self.ws.numel(), ctypes.byref(alt), s)
+            keys, vals = (self.keys_alt, self.vals_alt) if alt.value else (self.keys, self.vals)
+            L.call("hs_tile_ranges", total, _p(keys), _p(ranges), s)
+        else:
+            keys, vals = self.keys, self.vals
+        self.result = (keys[:total], vals[:total], ranges, tile_bits, tiles)
+        return self.result
+
+
+def launches_binning(total, key_bits):
+    """Kernel launches issued by Binner.bin (for the bench's gpu_launches count)."""
+    if not total:
+        return 0
+    return 1 + 3 * ((key_bits + 7) // 8) + 1
+
+
+# -------------------------------------------------------------------- trainer
+
+@dataclass
+class StepResult:
+    loss: float
+    black_l1: np.ndarray
+    per_frame: np.ndarray
+    total_keys: int
+
+
+class Trainer:
+    """One batched training step per call, entirely on device.
+
+    Mirrors S/train.py:214-260 (``train_step``) + the Adam groups (:164-199) and
+    colour init (:258-278).  ``process_group`` (torch.distributed, NCCL) shards the
+    global batch: every rank renders its frames and the flat gradient buffer is
+    allreduced once per step; grads are scaled by 1/global_batch.
+    """
+
+    def __init__(self, avatar: AvatarParams, width, height, batch, lrs=None, color_init=True, threshold=0.1,
+                 process_group=None, global_batch=None, frame_offset=0):
+        require_cuda()
+        self.av = avatar
+        self.W, self.H = int(width), int(height)
+        self.B = int(batch)
+        self.global_batch = int(global_batch or batch)
+        self.frame_offset = int(frame_offset)
+        self.lrs = (ctypes.c_float * 9)(*(lrs or default_lrs()))
+        self.color_init = bool(color_init)
+        self.threshold = float(threshold)
+        self.pg = process_group
+        self.step_count = 0
+        d = avatar.device
+        N, K, B, D = avatar.N, avatar.K, self.B, avatar.D
+        self.tiles_x, self.tiles_y, self.tiles, self.tile_bits, self.frame_bits = key_layout(B, self.W, self.H)
+        f32 = dict(dtype=torch.float32, device=d)
+        self.grads = torch.zeros(avatar.size, **f32)
+        self.m = torch.zeros(avatar.size, **f32)
+        self.v = torch.zeros(avatar.size, **f32)
+        self.visited = torch.zeros(N, dtype=torch.uint8, device=d)
+        self.psi = torch.empty(B, K, **f32)
+        self.gpsi = torch.empty(B, K, **f32)
+        self.cache = torch.empty(B, 4 * D, **f32)
+        self.mlp_scratch = torch.empty(B * (K + 2 * D) + 16, **f32)
+        self.raw10 = torch.empty(B * 10 * N, **f32)
+        self.records = torch.empty(B * N * 12, **f32)
+        self.depth = torch.empty(B * N, **f32)
+        self.radius = None          # optional debug output (set to a tensor to capture)
+        self.counts = torch.empty(B * N, dtype=torch.int32, device=d)
+        self.nblocks = int(L.load().hs_scan_blocks(B * N))
+        self.block_sums = torch.empty(self.nblocks, dtype=torch.int32, device=d)
+        self.err = torch.empty(1, dtype=torch.int64, device=d)
+        self.pix_T = torch.empty(B * self.H * self.W, **f32)
+        self.pix_state = torch.empty(B * self.H * self.W, dtype=torch.int32, device=d)
+        self.maxw = torch.zeros(B * N, **f32)
+        self.wsums = torch.zeros(B * N * 4, **f32)
+        self.loss_partials = torch.empty(B * self.tiles * 2, **f32)
+        self.loss_out = torch.empty(2 * B + 1, **f32)
+        self.g_splat = torch.empty(B * N * 9, **f32)
+        self.g_raw14 = torch.empty(B * 14 * N, **f32)
+        self.nparts = int(L.load().hs_blend_bwd_partials(N))
+        self.gpsi_partials = torch.empty(B * K * self.nparts, **f32)
+        self.n_init = torch.zeros(1, dtype=torch.int32, device=d)
+        self.packed = torch.empty(N, dtype=torch.int64, device=d)
+        self.est4 = torch.empty(N * 4, **f32)
+        self.binner = Binner(d)
+        self.last_total = 0
+        self.launches = 0           # libhs_b200 kernel launches issued so far
+        self.events = None          # {stage: [(start, end), ...]} when profiling is enabled
+        # host staging for the end-to-end path (pinned)
+        self._host = None
+
+    # --------------------------------------------------------------- profiling
+    def enable_profiling(self, on=True):
+        """Record CUDA events around every stage (on the launching stream)."""
+        self.events = {} if on else None
+
+    def _mark(self, name):
+        if self.events is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.events.setdefault(name, []).append([ev, None])
+        return name
+
+    def _done(self, name):
+        if name is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.events[name][-1][1] = ev
+
+    def stage_ms(self):
+        """{stage: total ms} over everything recorded since enable_profiling()."""
+        torch.cuda.synchronize()
+        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in (self.events or {}).items()}
+
+    def _call(self, stage, name, *args, kernels=1):
+        m = self._mark(stage)
+        L.call(name, *args)
+        self._done(m)
+        self.launches += kernels
+
+    # ------------------------------------------------------------------ forward
+    def _forward_project(self, thetas, frames, cameras):
+        av = self.av
+        N, K, B = av.N, av.K, self.B
+        s = _stream()
+        self.err.fill_(-1)
+        self._call("mlp_fwd", "hs_mlp_fwd", B, av.H, av.D, K, _p(av.mlp), _p(thetas), _p(self.cache), _p(self.psi),
+                   _p(self.err), s)
+        self._call("blend_fwd", "hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(self.psi),
+                   _p(self.raw10), s)
+        F = frames.shape[-2] if frames.dim() == 3 else frames.numel() // (B * 22)
+        self._call("project_fwd", "hs_project_avatar_fwd", B, N, F, self.W, self.H, _p(self.raw10), _p(av.base14),
+                   _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
+                   _p(self.counts), _p(self.block_sums), _p(self.radius), _p(self.err), s)
+        m = self._mark("bin_scan+sync")
+        total, code = self.binner.scan(self.block_sums, self.nblocks, self.err)
+        self._done(m)
+        self.launches += 1
+        L.raise_device_error(code, self.frame_offset)
+        self.last_total = total
+        m = self._mark("bin_sort")
+        res = self.binner.bin(B, N, self.W, self.H, self.records, self.depth, self.counts, total)
+        self._done(m)
+        self.launches += launches_binning(total, 32 + self.tile_bits + self.frame_bits)
+        return F, res
+
+    def _cameras(self, cameras):
+        if cameras.dim() == 1:
+            cameras = cameras.view(1, 16).expand(self.B, 16).contiguous()
+        return cameras
+
+    # --------------------------------------------------------------------- step
+    def step(self, thetas, targets, frames, cameras, backgrounds) -> StepResult:
+        """thetas (B,H) f32, targets (B,H,W,4) u8 straight RGBA, frames (B,F,22) f32,
+        cameras (B,16) or (16,) f32, backgrounds (B,3) f32 -- all on the device."""
+        av = self.av
+        N, K, B = av.N, av.K, self.B
+        cameras = self._cameras(cameras)
+        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras)
+        s = _stream()
+        ci = self.color_init and not self._all_visited()
+        flags = L.RASTER_LOSS
+        if ci:
+            flags |= L.RASTER_MAXW_UNVISITED | L.RASTER_WSUMS
+            self.maxw.zero_()
+            self.wsums.zero_()
+        self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
+                   _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
+                   _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials), s)
+        self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
+                   _p(self.loss_out), s, kernels=2)
+        # backward: d loss_b / d pred = sign / (H W 3) / B_global  (S/metrics.py:19-22, S/train.py:244)
+        grad_scale = 1.0 / (self.H * self.W * 3.0) / self.global_batch
+        self.g_splat.zero_()
+        self._call("raster_bwd", "hs_raster_bwd", B, N, self.W, self.H, _p(self.records), _p(vals), _p(ranges),
+                   tile_bits, _p(backgrounds), _p(self.pix_T), _p(self.pix_state), None, ctypes.c_float(grad_scale),
+                   _p(self.g_splat), s)
+        self._call("project_bwd", "hs_project_avatar_bwd", B, N, F, _p(self.raw10), _p(av.base14), _p(av.tri_index),
+                   _p(av.barycentric), _p(frames), _p(cameras), _p(self.g_splat), _p(self.g_raw14), s)
+        nparts = ctypes.c_int(0)
+        self._call("blend_bwd", "hs_blend_bwd", N, K, B, _p(av.deltas), _p(self.psi), _p(self.g_raw14),
+                   _p(self.grads), _p(self.grads[14 * N:]), _p(self.gpsi_partials), ctypes.byref(nparts), s,
+                   kernels=(B + 15) // 16)
+        self._call("mlp_bwd", "hs_mlp_bwd", B, av.H, av.D, K, _p(av.mlp), _p(thetas), _p(self.cache),
+                   _p(self.gpsi_partials), nparts.value, _p(self.gpsi), _p(self.mlp_scratch),
+                   _p(self.grads[14 * N + 10 * K * N:]), s, kernels=2)
+        if self.pg is not None:
+            import torch.distributed as dist
+            m = self._mark("allreduce")
+            dist.all_reduce(self.grads, op=dist.ReduceOp.SUM, group=self.pg)
+            self._done(m)
+        self.step_count += 1
+        self._call("adam", "hs_adam", N, K, av.mlp_size, _p(av.params), _p(self.grads), _p(self.m), _p(self.v),
+                   self.lrs, self.step_count, ADAM_BETAS[0], ADAM_BETAS[1], ADAM_EPS, s)
+        if ci:
+            m = self._mark("color_init")
+            self._color_init()
+            self._done(m)
+        return self.loss_out
+
+    def result(self) -> StepResult:
+        """Host copy of the last step's losses (a device->host read)."""
+        lo = self.loss_out.cpu().numpy()
+        B = self.B
+        return StepResult(float(lo[2 * B]), lo[B:2 * B].copy(), lo[:B].copy(), self.last_total)
+
+    def _all_visited(self):
+        # visited is one-way; cache the host answer once it becomes True
+        if getattr(self, "_done", False):
+            return True
+        return False
+
+    def color_init_done(self) -> bool:
+        """Host check (a sync) of ColorInitState.done (S/color_init.py:28-30)."""
+        self._done = bool(self.visited.bool().all().item())
+        return self._done
+
+    def _color_init(self):
+        av = self.av
+        s = _stream()
+        if self.pg is None:
+            L.call("hs_color_init", self.B, av.N, _p(self.maxw), _p(self.wsums), ctypes.c_float(self.threshold),
+                   _p(self.visited), _p(av.params), _p(self.n_init), _p(self.err), s)
+            self.launches += 1
+            return
+        self.launches += 3
+        import torch.distributed as dist
+        L.call("hs_color_pack", self.B, av.N, self.frame_offset, _p(self.maxw), _p(self.visited), _p(self.packed), s)
+        dist.all_reduce(self.packed, op=dist.ReduceOp.MAX, group=self.pg)
+        L.call("hs_color_select", self.B, av.N, self.frame_offset, _p(self.packed), _p(self.wsums), _p(self.est4),
+               _p(self.err), s)
+        dist.all_reduce(self.est4, op=dist.ReduceOp.SUM, group=self.pg)
+        L.call("hs_color_apply", av.N, _p(self.packed), _p(self.est4), ctypes.c_float(self.threshold),
+               _p(self.visited), _p(av.params), _p(self.n_init), s)
+
+    # ------------------------------------------------------------------ render
+    def render(self, thetas, frames, cameras, backgrounds, out=None):
+        """Forward-only batched render (S/dataset.py:163-172 without the mesh rig):
+        returns images (B, H, W, 3) fp32 = C + T * background."""
+        av = self.av
+        cameras = self._cameras(cameras)
+        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras)
+        if out is None:
+            out = torch.empty(self.B, self.H, self.W, 3, dtype=torch.float32, device=av.device)
+        self._call("raster_fwd", "hs_raster_fwd", self.B, av.N, self.W, self.H, L.RASTER_IMAGE, _p(self.records),
+                   _p(vals), _p(ranges), tile_bits, _p(backgrounds), None, None, None, _p(self.pix_T),
+                   _p(self.pix_state), _p(out), None, None, None, _stream())
+        return out
+
+    # -------------------------------------------------------------- end to end
+    def step_from_host(self, thetas, targets, frames, cameras, backgrounds):
+        """End-to-end step through host buffers (numpy): pinned staging, H2D copies,
+        the device step, and the D2H read of the losses.  Returns StepResult."""
+        arrays = {"thetas": np.asarray(thetas, np.float32), "targets": np.asarray(targets, np.uint8),
+                  "frames": np.asarray(frames, np.float32), "cameras": np.asarray(cameras, np.float32),
+                  "backgrounds": np.asarray(backgrounds, np.float32)}
+        if self._host is None or any(self._host[k][0].shape != v.shape for k, v in arrays.items()):
+            self._host = {k: (torch.empty(v.shape, dtype=torch.from_numpy(v).dtype, pin_memory=True),
+                              torch.empty(v.shape, dtype=torch.from_numpy(v).dtype, device=self.av.device))
+                          for k, v in arrays.items()}
+            self._loss_host = torch.empty(2 * self.B + 1, dtype=torch.float32, pin_memory=True)
+        dev = {}
+        for k, v in arrays.items():
+            h, d = self._host[k]
+            h.numpy()[...] = v
+            d.copy_(h, non_blocking=True)
+            dev[k] = d
+        self.step(dev["thetas"], dev["targets"], dev["frames"], dev["cameras"], dev["backgrounds"])
+        self._loss_host.copy_(self.loss_out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        lo = self._loss_host.numpy()
+        B = self.B
+        return StepResult(float(lo[2 * B]), lo[B:2 * B].copy(), lo[:B].copy(), self.last_total)
+
+    def h2d_bytes(self, F):
+        return self.B * (self.av.H * 4 + self.H * self.W * 4 + F * 22 * 4 + 16 * 4 + 3 * 4)
+
+    def d2h_bytes(self):
+        return (2 * self.B + 1) * 4

@@ -1,0 +1,49 @@
+"""The C-ABI library loads on CPU and exports every symbol include/hs_api.h declares
+(no compute calls without a GPU)."""
+import os
+
+import pytest
+
+from paper_2503_12886_b200 import _lib as L
+from paper_2503_12886_b200 import build as B
+
+
+def test_library_built_in_tree():
+    B.build()
+    assert os.path.exists(L.LIB_PATH)
+    assert L.LIB_PATH.startswith(os.path.dirname(os.path.dirname(os.path.abspath(B.__file__))))
+
+
+def test_exports_every_header_symbol():
+    lib = L.load()
+    syms = L.header_symbols()
+    assert len(syms) >= 30
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in L.SIGNATURES, f"{s} has no ctypes signature"
+
+
+def test_pure_queries():
+    lib = L.load()
+    assert lib.hs_version() == 1
+    assert lib.hs_scan_blocks(1000) == 4
+    assert lib.hs_mlp_size(13, 128, 20) == 128 * 13 + 128 + 128 * 128 + 128 + 20 * 128 + 20
+    assert lib.hs_sort_workspace_size(1 << 20) > 0
+    assert lib.hs_blend_bwd_partials(100) == (1000 + 511) // 512
+
+
+def test_device_error_mapping():
+    with pytest.raises(FloatingPointError, match="non-finite scale at Gaussian index 7"):
+        L.raise_device_error((1 << 62) | (2 << 32) | 7)
+    with pytest.raises(FloatingPointError, match="zero-norm quaternion at Gaussian index 3"):
+        L.raise_device_error((1 << 32) | 3)
+    with pytest.raises(ValueError, match="non-finite"):
+        L.raise_device_error(0)
+    L.raise_device_error(L.HS_NO_ERROR)
+
+
+def test_status_mapping():
+    with pytest.raises(ValueError):
+        L.check(L.HS_ERR_SHAPE)
+    with pytest.raises(RuntimeError):
+        L.check(L.HS_ERR_COLOR_INIT)
