@@ -643,10 +643,15 @@ class State:
             self.pool.shutdown()
 
 
-def train_step(state: State, thetas, images, frames_list, backgrounds):
+def train_step(state: State, thetas, images, frames_list, backgrounds, replay=None):
     """S/train.py:214-260.  images: (B, H, W, 4) straight RGBA in [0, 1].
     Returns (mean loss, black-bg L1 per item).  The summed gradients passed to
-    Adam are kept on state.last_grads (g_base14, g_deltas, g_mlp)."""
+    Adam are kept on state.last_grads (g_base14, g_deltas, g_mlp).
+
+    ``replay`` (checker extension): per frame a dict with ``order``
+    (compositing order over the kept splats) and ``bbox`` (int pixel bbox per kept
+    splat) taken from the implementation under test, so the fp32-vs-fp64 decision
+    boundaries (depth ties, the 3-sigma bbox edge) are identical on both sides."""
     model = state.model
     cam = state.camera
     B = len(thetas)
@@ -658,7 +663,14 @@ def train_step(state: State, thetas, images, frames_list, backgrounds):
         worlds.append(world)
     # two-stage schedule (S/scheduler.py:64-72): all preprocess, one barrier, all raster
     splats = state.map(lambda w: preprocess(w, cam), [(w,) for w in worlds])
-    rendered = state.map(lambda s, bg: rasterize(s, cam, bg), list(zip(splats, backgrounds)))
+    if replay is None:
+        rendered = state.map(lambda s, bg: rasterize(s, cam, bg), list(zip(splats, backgrounds)))
+    else:
+        for s, r in zip(splats, replay):
+            if not np.array_equal(s.index, r["index"]):
+                raise ValueError("replay: kept-splat sets differ (a near-plane / min-radius cull flipped)")
+        rendered = state.map(lambda s, bg, r: rasterize(s, cam, bg, order=r["order"], bbox=r["bbox"]),
+                             list(zip(splats, backgrounds, replay)))
     losses = np.empty(B)
     black = np.empty(B)
     grads_img = []

@@ -112,6 +112,19 @@ def _t(a, dtype=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(a)).to(device=_dev(), dtype=dtype)
 
 
+_KEPT = []
+
+
+def _keep(t):
+    """Pointer to a temporary device tensor that stays referenced past the launch
+    (otherwise the caching allocator could hand its block to the next temporary of
+    the same argument list and the two pointers would alias)."""
+    _KEPT.append(t)
+    if len(_KEPT) > 64:
+        del _KEPT[:-32]
+    return _p(t)
+
+
 def _pack14(g) -> np.ndarray:
     return np.concatenate([np.asarray(g.position, np.float64).ravel(), np.asarray(g.rotation, np.float64).ravel(),
                            np.asarray(g.color, np.float64).ravel(), np.asarray(g.scale, np.float64).ravel(),
@@ -168,7 +181,7 @@ def mlp_backward(mlp, cache, grad_psi):
     gpsi = torch.empty(K, dtype=torch.float32, device=_dev())
     scratch = torch.empty(K + 2 * D + 16, dtype=torch.float32, device=_dev())
     g = torch.empty(int(L.load().hs_mlp_size(H, D, K)), dtype=torch.float32, device=_dev())
-    L.call("hs_mlp_bwd", 1, H, D, K, _p(w), _p(_t(theta)), _p(c), _p(parts), 1, _p(gpsi), _p(scratch), _p(g), _stream())
+    L.call("hs_mlp_bwd", 1, H, D, K, _p(w), _keep(_t(theta)), _p(c), _p(parts), 1, _p(gpsi), _p(scratch), _p(g), _stream())
     gz1 = scratch[D:2 * D].cpu().numpy().astype(np.float64)
     flat = g.cpu().numpy().astype(np.float64)
     o = 0
@@ -197,7 +210,7 @@ def blend(model, psi) -> GaussianSet:
     n = model.base.position.shape[0]
     base14 = _t(_pack14(model.base))
     raw = torch.empty(10 * n, dtype=torch.float32, device=_dev())
-    L.call("hs_blend_fwd", n, K, 1, _p(base14), _p(_t(_deltas10(model))), _p(_t(psi)), _p(raw), _stream())
+    L.call("hs_blend_fwd", n, K, 1, _p(base14), _keep(_t(_deltas10(model))), _keep(_t(psi)), _p(raw), _stream())
     r = raw.cpu().numpy().astype(np.float64)
     return GaussianSet(r[:3 * n].reshape(n, 3), r[3 * n:7 * n].reshape(n, 4),
                        np.asarray(model.base.scale, np.float64).copy(), np.asarray(model.base.opacity, np.float64).copy(),
@@ -216,7 +229,7 @@ def blend_backward(model, psi, grad_out):
     gd = torch.empty(K * 10 * n, dtype=torch.float32, device=_dev())
     parts = torch.empty(K * int(L.load().hs_blend_bwd_partials(n)), dtype=torch.float32, device=_dev())
     np_ = ctypes.c_int(0)
-    L.call("hs_blend_bwd", n, K, 1, _p(_t(_deltas10(model))), _p(_t(psi)), _p(g14), _p(gb), _p(gd), _p(parts),
+    L.call("hs_blend_bwd", n, K, 1, _keep(_t(_deltas10(model))), _keep(_t(psi)), _p(g14), _p(gb), _p(gd), _p(parts),
            ctypes.byref(np_), _stream())
     g_psi = parts.view(K, np_.value).sum(dim=1).double().cpu().numpy()
     gdn = gd.cpu().numpy().astype(np.float64).reshape(K, 10 * n)
@@ -231,7 +244,7 @@ def activate(raw) -> GaussianSet:
     n = raw.position.shape[0]
     out = torch.empty(14 * n, dtype=torch.float32, device=_dev())
     err = _err()
-    L.call("hs_activate_fwd", n, _p(_t(_pack14(raw))), _p(out), _p(err), _stream())
+    L.call("hs_activate_fwd", n, _keep(_t(_pack14(raw))), _p(out), _p(err), _stream())
     _raise(err)
     return _unpack14(out.cpu().numpy(), n)
 
@@ -240,7 +253,7 @@ def activate_backward(raw, activated, grad_out) -> GaussianSet:
     """S/model.py:237-248."""
     n = raw.position.shape[0]
     out = torch.empty(14 * n, dtype=torch.float32, device=_dev())
-    L.call("hs_activate_bwd", n, _p(_t(_pack14(raw))), _p(_t(_pack14(activated))), _p(_t(_pack14(grad_out))),
+    L.call("hs_activate_bwd", n, _keep(_t(_pack14(raw))), _keep(_t(_pack14(activated))), _keep(_t(_pack14(grad_out))),
            _p(out), _stream())
     return _unpack14(out.cpu().numpy(), n)
 
@@ -249,8 +262,8 @@ def transform_to_deformed(tangent, frames, bindings) -> GaussianSet:
     """S/binding.py:174-188."""
     n = tangent.position.shape[0]
     out = torch.empty(14 * n, dtype=torch.float32, device=_dev())
-    L.call("hs_transform_fwd", n, _p(_t(_pack14(tangent))), _p(_t(frames_array(frames))),
-           _p(_t(bindings.triangle_index, torch.int32)), _p(_t(bindings.barycentric)), _p(out), _stream())
+    L.call("hs_transform_fwd", n, _keep(_t(_pack14(tangent))), _keep(_t(frames_array(frames))),
+           _keep(_t(bindings.triangle_index, torch.int32)), _keep(_t(bindings.barycentric)), _p(out), _stream())
     return _unpack14(out.cpu().numpy(), n)
 
 
@@ -258,8 +271,8 @@ def transform_backward(tangent, frames, bindings, grad_world) -> GaussianSet:
     """S/binding.py:191-204."""
     n = tangent.position.shape[0]
     out = torch.empty(14 * n, dtype=torch.float32, device=_dev())
-    L.call("hs_transform_bwd", n, _p(_t(_pack14(tangent))), _p(_t(frames_array(frames))),
-           _p(_t(bindings.triangle_index, torch.int32)), _p(_t(_pack14(grad_world))), _p(out), _stream())
+    L.call("hs_transform_bwd", n, _keep(_t(_pack14(tangent))), _keep(_t(frames_array(frames))),
+           _keep(_t(bindings.triangle_index, torch.int32)), _keep(_t(_pack14(grad_world))), _p(out), _stream())
     return _unpack14(out.cpu().numpy(), n)
 
 
@@ -414,7 +427,7 @@ def render_backward(splats: ProjectedSplats, aux: RenderAux, grad_image) -> Gaus
     g[b] = np.asarray(grad_image, np.float64)
     g_splat = torch.zeros(B * n * 9, dtype=torch.float32, device=_dev())
     L.call("hs_raster_bwd", B, n, W, H, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(out["bgs"]),
-           _p(out["pix_T"]), _p(out["pix_state"]), _p(_t(g)), ctypes.c_float(0.0), _p(g_splat), _stream())
+           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat), _stream())
     g14 = torch.empty(B * 14 * n, dtype=torch.float32, device=_dev())
     L.call("hs_project_world_bwd", B, n, _p(dev["world14"]), _p(dev["cams"]), _p(g_splat), _p(g14), _stream())
     return _unpack14(g14[b * 14 * n:(b + 1) * 14 * n].cpu().numpy(), n)
@@ -429,7 +442,7 @@ def splat_space_grads(aux: RenderAux, grad_image):
     g[b] = np.asarray(grad_image, np.float64)
     g_splat = torch.zeros(B * n * 9, dtype=torch.float32, device=_dev())
     L.call("hs_raster_bwd", B, n, W, H, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(out["bgs"]),
-           _p(out["pix_T"]), _p(out["pix_state"]), _p(_t(g)), ctypes.c_float(0.0), _p(g_splat), _stream())
+           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat), _stream())
     return g_splat.view(B, n, 9)[b].cpu().numpy().astype(np.float64)
 
 

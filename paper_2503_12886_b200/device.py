@@ -204,7 +204,7 @@ class Binner:
         self.result = None
 
     def _ensure(self, total):
-        if total <= self.cap:
+        if total <= self.cap and self.keys is not None:
             return
         cap = max(int(total * 1.25) + 1024, 1 << 16)
         d = self.device
@@ -326,6 +326,7 @@ class Trainer:
         self.last_total = 0
         self.launches = 0           # libhs_b200 kernel launches issued so far
         self.events = None          # {stage: [(start, end), ...]} when profiling is enabled
+        self._ci_done = False
         # host staging for the end-to-end path (pinned)
         self._host = None
 
@@ -447,15 +448,13 @@ class Trainer:
         return StepResult(float(lo[2 * B]), lo[B:2 * B].copy(), lo[:B].copy(), self.last_total)
 
     def _all_visited(self):
-        # visited is one-way; cache the host answer once it becomes True
-        if getattr(self, "_done", False):
-            return True
-        return False
+        # visited is one-way; the host answer is cached once color_init_done() saw True
+        return self._ci_done
 
     def color_init_done(self) -> bool:
         """Host check (a sync) of ColorInitState.done (S/color_init.py:28-30)."""
-        self._done = bool(self.visited.bool().all().item())
-        return self._done
+        self._ci_done = bool(self.visited.bool().all().item())
+        return self._ci_done
 
     def _color_init(self):
         av = self.av

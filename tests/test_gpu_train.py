@@ -17,6 +17,7 @@ import torch
 import binning as BO
 import oracle as O
 from conftest import golden
+from gpu_helpers import normwise, replay_from_trainer
 
 pytestmark = pytest.mark.gpu
 ATTRS = ("position", "rotation", "scale", "opacity", "color")
@@ -30,10 +31,15 @@ def _cuda():
     build.build()
 
 
-def rel_fail_frac(a, b, rtol=1e-3, floor_frac=1e-6):
+def rel_fail_frac(a, b, rtol=1e-3, floor_frac=1e-6, scale=None):
+    """Fraction of entries failing |a-b| <= max(floor, rtol*max(|a|,|b|)); the floor is
+    floor_frac * max|b| of the tensor, or of `scale` (the whole gradient) when given --
+    needed where the exact gradient is 0 and both sides hold only roundoff (e.g. the
+    quaternion gradient of isotropic Gaussians at init, where R(q) cancels from Sigma)."""
     a = np.asarray(a, np.float64).ravel()
     b = np.asarray(b, np.float64).ravel()
-    floor = floor_frac * max(np.abs(b).max(initial=0.0), 1e-30)
+    ref = np.abs(b).max(initial=0.0) if scale is None else scale
+    floor = floor_frac * max(ref, 1e-30)
     diff = np.abs(a - b)
     bad = (diff > floor) & (diff > rtol * np.maximum(np.abs(a), np.abs(b)))
     return float(bad.mean()) if bad.size else 0.0, int(bad.sum())
@@ -64,18 +70,25 @@ def test_reference_fixture_steps():
         assert abs(res.loss - float(d[p + "loss"])) < 2e-5
         np.testing.assert_allclose(res.black_l1, d[p + "black"], atol=2e-5)
         gb, gd, gm = split_grads(tr.grads.cpu().numpy(), N, K, av.H, av.D)
+        gscale = max(np.abs(d[p + "g." + a]).max() for a in ATTRS)
         for a in ATTRS:
-            frac, nbad = rel_fail_frac(gb[a], d[p + "g." + a])
+            frac, nbad = rel_fail_frac(gb[a], d[p + "g." + a], scale=gscale)
             assert frac < 2e-3, (step, a, nbad)
         frac, nbad = rel_fail_frac(gd, d[p + "g_deltas"])
         assert frac < 2e-3, (step, "deltas", nbad)
         for k in gm:
             frac, nbad = rel_fail_frac(gm[k], d[p + "gmlp." + k], rtol=2e-3)
             assert frac < 5e-3, (step, k, nbad)
+        # Parameters after Adam: Adam's first steps map gradients at or below eps=1e-8
+        # (here the exactly-zero quaternion gradient of isotropic Gaussians, where fp32
+        # roundoff is ~1e-9 and fp64 roundoff ~1e-17) to updates up to lr*|g|/(|g|+eps),
+        # so the tolerance is a fraction of each group's learning rate.
         pb, pd, pm = av.split_host()
+        lrs = {"position": 8e-4, "rotation": 5e-3, "scale": 2.5e-2, "opacity": 0.25, "color": 1.25e-2}
         for a in ATTRS:
-            np.testing.assert_allclose(pb[a], d[p + "base." + a], rtol=1e-4, atol=5e-5)
-        np.testing.assert_allclose(pd, d[p + "deltas"], rtol=1e-4, atol=5e-5)
+            bad = np.abs(pb[a] - d[p + "base." + a]) > 0.05 * lrs[a] + 1e-4 * np.abs(d[p + "base." + a])
+            assert bad.mean() < 5e-3, (step, a, int(bad.sum()))
+        np.testing.assert_allclose(pd, d[p + "deltas"], rtol=1e-4, atol=0.05 * 2.5e-3)
         vis = tr.visited.cpu().numpy().astype(bool)
         assert (vis != d[p + "visited"]).sum() <= 2
     assert tr.visited.cpu().numpy().any()
@@ -98,9 +111,11 @@ def test_c1_step_vs_oracle():
                                  av.barycentric)
     B = 4
     tr = Trainer(dev, 256, 256, B)
+    tr.radius = torch.empty(B * dev.N, device="cuda")
     cams = np.tile(wl.camera.packed(), (B, 1))
     bgs = np.asarray(wl.backgrounds, np.float32).astype(np.float64)
     res = tr.step_from_host(wl.thetas, wl.targets, wl.frames, cams, bgs)
+    replay = replay_from_trainer(tr)
     # oracle on the same fp32-quantized inputs
     model = _oracle_model(wl)
     cam = O.Cam(*[float(x) for x in wl.camera.packed()[12:16]], wl.camera.packed()[:9].reshape(3, 3).astype(np.float64),
@@ -109,21 +124,64 @@ def test_c1_step_vs_oracle():
                        f[:, 13:].reshape(-1, 3, 3).astype(np.float64)) for f in wl.frames]
     state = O.State(model, cam, workers=4)
     images = wl.targets.astype(np.float64) / 255.0
-    loss, black = O.train_step(state, np.asarray(wl.thetas, np.float32).astype(np.float64), images, frames, bgs)
+    loss, black = O.train_step(state, np.asarray(wl.thetas, np.float32).astype(np.float64), images, frames, bgs,
+                               replay=replay)
     state.close()
     assert abs(res.loss - loss) < 1e-4 * max(loss, 1e-3)
     np.testing.assert_allclose(res.black_l1, black, rtol=1e-3, atol=1e-5)
     g_base, g_deltas, g_mlp = state.last_grads
     gb, gd, gm = split_grads(tr.grads.cpu().numpy(), dev.N, dev.K, dev.H, dev.D)
-    report = {}
+    # Normwise relative errors.  The remaining fp32-vs-fp64 decision flips (alpha
+    # cutoff, the L1 sign at |pred - target| ~ 1e-6) change whole per-pixel
+    # gradients, so entrywise checks on the cancellation-heavy reductions (g_psi,
+    # MLP) are not meaningful at this scale; the stage-wise blend/MLP adjoint fed
+    # the device's own g_raw is checked tightly in test_c1_blend_mlp_stagewise.
+    gscale = np.linalg.norm(g_base.position)
+    report = {a: normwise(gb[a], getattr(g_base, a), scale=gscale if a == "rotation" else None) for a in ATTRS}
+    report["deltas"] = normwise(gd, g_deltas)
+    report.update({"mlp." + k: normwise(gm[k], g_mlp[k]) for k in gm})
+    print("C1 normwise gradient errors:", report)
+    for k, e in report.items():
+        assert e < 2e-3, (k, e)
+    # entrywise on the base/delta gradients: rel 1e-3 with a 1e-6 * max floor
     for a in ATTRS:
-        report[a] = rel_fail_frac(gb[a], getattr(g_base, a))
-    report["deltas"] = rel_fail_frac(gd, g_deltas)
+        frac, nbad = rel_fail_frac(gb[a], getattr(g_base, a), scale=np.abs(g_base.position).max())
+        assert frac < 1e-3, (a, frac, nbad)
+    frac, nbad = rel_fail_frac(gd, g_deltas)
+    assert frac < 1e-3, ("deltas", frac, nbad)
+
+
+def test_c1_blend_mlp_stagewise():
+    """blend_bwd + mlp_bwd fed the device's own per-frame g_raw (C1 sizes)."""
+    from paper_2503_12886_b200 import synth
+    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    wl = synth.make_workload(141, 4, 256)
+    av = wl.avatar
+    dev = AvatarParams.from_host(O.GSet(*(av.base[a] for a in ATTRS)), av.deltas, av.mlp, av.tri_index,
+                                 av.barycentric)
+    B, n = 4, dev.N
+    tr = Trainer(dev, 256, 256, B, color_init=False)
+    tr.step_from_host(wl.thetas, wl.targets, wl.frames, np.tile(wl.camera.packed(), (B, 1)), wl.backgrounds)
+    model = _oracle_model(wl)
+    thetas = np.asarray(wl.thetas, np.float32).astype(np.float64)
+    graw = tr.g_raw14.view(B, 14 * n).cpu().numpy().astype(np.float64)
+    gpsi_dev = tr.gpsi.cpu().numpy().astype(np.float64)
+    g_base14 = np.zeros(14 * n)
+    g_deltas = np.zeros((dev.K, 10 * n))
+    acc = {k: np.zeros_like(v) for k, v in model.mlp.items()}
+    for b in range(B):
+        g = graw[b]
+        gr = O.GSet(g[:3 * n].reshape(n, 3), g[3 * n:7 * n].reshape(n, 4), g[10 * n:13 * n].reshape(n, 3),
+                    g[13 * n:], g[7 * n:10 * n].reshape(n, 3))
+        psi, cache = O.map_params(model.mlp, thetas[b])
+        _, _, gpsi = O.blend_backward(model, psi, gr, g_base14, g_deltas)
+        absum = np.abs(model.deltas * g[None, :10 * n]).sum(axis=1)
+        assert np.max(np.abs(gpsi - gpsi_dev[b]) / absum) < 1e-6
+        O.mlp_backward(model.mlp, cache, gpsi_dev[b], into=acc)
+    gb, gd, gm = split_grads(tr.grads.cpu().numpy(), n, dev.K, dev.H, dev.D)
+    assert normwise(gd, g_deltas) < 1e-6
     for k in gm:
-        report["mlp." + k] = rel_fail_frac(gm[k], g_mlp[k], rtol=5e-3)
-    print("C1 gradient mismatch fractions:", report)
-    for k, (frac, nbad) in report.items():
-        assert frac < 5e-3, (k, frac, nbad)
+        assert normwise(gm[k], acc[k]) < 1e-5, k
 
 
 def test_c2_full_size_properties():
