@@ -13,7 +13,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libhs_b200.so")
+LIB_PATH = os.environ.get("HS_B200_LIB") or os.path.join(PKG, "lib", "libhs_b200.so")
 
 HS_OK, HS_ERR_SHAPE, HS_ERR_NONFINITE, HS_ERR_ZERO_QUAT, HS_ERR_COLOR_INIT, HS_ERR_CUDA = range(6)
 HS_NO_ERROR = 0xFFFFFFFFFFFFFFFF

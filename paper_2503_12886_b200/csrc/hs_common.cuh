@@ -102,6 +102,55 @@ __host__ __device__ inline int bit_length_u32(uint32_t x) {
     return n;
 }
 
+// Warp reduce-scatter of S values: each round halves the slot count, exchanging
+// only the half the partner keeps (S=9: 12 shuffles instead of 45).  On return the
+// lane holds the warp total of value `idx`; exactly one lane per value has `issue`.
+template <int S, int R>
+struct ReduceScatter {
+    static __device__ __forceinline__ float run(const float *w, int lane, int &idx, int &cnt, int &dup) {
+        constexpr int O = 16 >> R;
+        if constexpr (R == 5) {
+            return w[0];
+        } else if constexpr (S == 1) {
+            const float t[1] = {w[0] + __shfl_xor_sync(0xffffffffu, w[0], O)};
+            dup |= O;
+            return ReduceScatter<1, R + 1>::run(t, lane, idx, cnt, dup);
+        } else {
+            constexpr int L = (S + 1) / 2;
+            const bool up = lane & O;
+            float nw[L];
+#pragma unroll
+            for (int s = 0; s < L; ++s) {
+                const float hi = (L + s < S) ? w[L + s] : 0.f;
+                const float lo = w[s];
+                nw[s] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, O);
+            }
+            if (up) {
+                idx += L;
+                cnt -= L;
+            } else {
+                cnt = min(cnt, L);
+            }
+            return ReduceScatter<L, R + 1>::run(nw, lane, idx, cnt, dup);
+        }
+    }
+};
+
+template <int S>
+__device__ __forceinline__ float reduce_scatter(const float (&v)[S], int lane, int &idx, bool &issue) {
+    int cnt = S, dup = 0;
+    idx = 0;
+    const float r = ReduceScatter<S, 0>::run(v, lane, idx, cnt, dup);
+    issue = cnt >= 1 && (lane & dup) == 0;
+    return r;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 }  // namespace hs
 
 #define HS_CHECK_STREAM(s) (reinterpret_cast<cudaStream_t>(s))

@@ -34,13 +34,22 @@ int check_launch(const char *what) {
 
 // ------------------------------------------------------------------- MLP
 
-// One CTA per frame.  S/model.py:130-142.
+// One CTA per frame.  S/model.py:130-142.  Each GEMV row is one warp-cooperative
+// dot product (lanes split the row: coalesced loads, many in flight).
+__device__ __forceinline__ float row_dot(const float *__restrict__ row, const float *__restrict__ x, int n, int lane) {
+    float acc = 0.f;
+#pragma unroll 4
+    for (int j = lane; j < n; j += 32) acc = fmaf(row[j], x[j], acc);
+    return warp_sum(acc);
+}
+
 __global__ void mlp_fwd_kernel(int H, int D, int K, const float *__restrict__ mlp,
                                const float *__restrict__ theta, float *__restrict__ cache,
                                float *__restrict__ psi, unsigned long long *err) {
     extern __shared__ float sm[];
     float *th = sm, *h1 = th + H, *h2 = h1 + D;
     const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const float *w1 = mlp, *b1 = w1 + D * H, *w2 = b1 + D, *b2 = w2 + D * D, *w3 = b2 + D, *b3 = w3 + K * D;
     for (int i = threadIdx.x; i < H; i += blockDim.x) {
         float t = theta[b * H + i];
@@ -49,52 +58,53 @@ __global__ void mlp_fwd_kernel(int H, int D, int K, const float *__restrict__ ml
     }
     __syncthreads();
     float *c = cache + (int64_t)b * 4 * D;
-    for (int i = threadIdx.x; i < D; i += blockDim.x) {
-        float acc = 0.f;
-        for (int j = 0; j < H; ++j) acc = fmaf(w1[i * H + j], th[j], acc);
-        float z = acc + b1[i];
-        float h = z > 0.f ? z : 0.f;
-        c[i] = z;
-        c[D + i] = h;
-        h1[i] = h;
+    for (int i = warp; i < D; i += nw) {
+        const float z = row_dot(w1 + (int64_t)i * H, th, H, lane) + b1[i];
+        if (lane == 0) {
+            const float h = z > 0.f ? z : 0.f;
+            c[i] = z;
+            c[D + i] = h;
+            h1[i] = h;
+        }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < D; i += blockDim.x) {
-        float acc = 0.f;
-        const float *row = w2 + (int64_t)i * D;
-        for (int j = 0; j < D; ++j) acc = fmaf(row[j], h1[j], acc);
-        float z = acc + b2[i];
-        float h = z > 0.f ? z : 0.f;
-        c[2 * D + i] = z;
-        c[3 * D + i] = h;
-        h2[i] = h;
+    for (int i = warp; i < D; i += nw) {
+        const float z = row_dot(w2 + (int64_t)i * D, h1, D, lane) + b2[i];
+        if (lane == 0) {
+            const float h = z > 0.f ? z : 0.f;
+            c[2 * D + i] = z;
+            c[3 * D + i] = h;
+            h2[i] = h;
+        }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        float acc = 0.f;
-        for (int j = 0; j < D; ++j) acc = fmaf(w3[k * D + j], h2[j], acc);
-        psi[b * K + k] = acc + b3[k];
+    for (int k = warp; k < K; k += nw) {
+        const float p = row_dot(w3 + (int64_t)k * D, h2, D, lane) + b3[k];
+        if (lane == 0) psi[b * K + k] = p;
     }
 }
 
 // Per frame: reduce the blend_bwd partials into g_psi (fixed order), then the
-// hidden-layer adjoints gz2, gz1 (S/model.py:151-160).
+// hidden-layer adjoints gz2 = relu'(z2) W3^T g_psi and gz1 = relu'(z1) W2^T gz2
+// (S/model.py:151-160).  The transposed GEMVs walk W rows (coalesced) with each
+// warp owning a slice of rows; warp partials are summed through shared memory.
 __global__ void mlp_bwd_frame_kernel(int H, int D, int K, const float *__restrict__ mlp,
                                      const float *__restrict__ cache,
                                      const float *__restrict__ partials, int P,
                                      float *__restrict__ gpsi, float *__restrict__ scratch) {
     extern __shared__ float sm[];
-    float *gp = sm, *gz2 = gp + K;
+    const int nw = blockDim.x >> 5;
+    float *gp = sm, *gz2 = gp + K, *part = gz2 + D;     // part: [nw][D]
     const int b = blockIdx.x;
     const int B = gridDim.x;
     const float *w2 = mlp + D * H + D, *w3 = w2 + D * D + D;
     const float *c = cache + (int64_t)b * 4 * D;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int k = warp; k < K; k += nw) {
         const float *row = partials + ((int64_t)b * K + k) * P;
         float s = 0.f;
         for (int p = lane; p < P; p += 32) s += row[p];
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        s = warp_sum(s);
         if (lane == 0) {
             gp[k] = s;
             gpsi[b * K + k] = s;
@@ -103,17 +113,27 @@ __global__ void mlp_bwd_frame_kernel(int H, int D, int K, const float *__restric
     __syncthreads();
     float *s_gz2 = scratch + (int64_t)b * D;             // [B][D]
     float *s_gz1 = scratch + (int64_t)B * D + (int64_t)b * D;
+    // gz2[j] = sum_k w3[k][j] gp[k]   (K rows of length D)
     for (int j = threadIdx.x; j < D; j += blockDim.x) {
         float acc = 0.f;
-        for (int k = 0; k < K; ++k) acc = fmaf(w3[k * D + j], gp[k], acc);
-        float g = c[2 * D + j] > 0.f ? acc : 0.f;
+#pragma unroll 4
+        for (int k = 0; k < K; ++k) acc = fmaf(w3[(int64_t)k * D + j], gp[k], acc);
+        const float g = c[2 * D + j] > 0.f ? acc : 0.f;
         gz2[j] = g;
         s_gz2[j] = g;
     }
     __syncthreads();
+    // gz1[j] = sum_i w2[i][j] gz2[i]: warp w sums rows i = w, w + nw, ...
+    for (int j = lane; j < D; j += 32) {
+        float acc = 0.f;
+#pragma unroll 4
+        for (int i = warp; i < D; i += nw) acc = fmaf(w2[(int64_t)i * D + j], gz2[i], acc);
+        part[warp * D + j] = acc;
+    }
+    __syncthreads();
     for (int j = threadIdx.x; j < D; j += blockDim.x) {
         float acc = 0.f;
-        for (int i = 0; i < D; ++i) acc = fmaf(w2[(int64_t)i * D + j], gz2[i], acc);
+        for (int w = 0; w < nw; ++w) acc += part[w * D + j];
         s_gz1[j] = c[j] > 0.f ? acc : 0.f;
     }
 }
@@ -218,109 +238,80 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
 }
 
 // Adjoint of blend, reduced over the frame batch in-kernel (S/model.py:188-216 +
-// the item-order sum of S/train.py:253-255).  A CTA owns a tile of kBE channels:
+// the item-order sum of S/train.py:253-255):
 //   g_base[e]     = sum_b g[b][e]                              (all 14N channels)
 //   g_delta[k][e] = sum_b psi[b][k] g[b][e]                    (10N blended channels)
-//   g_psi[b][k]   = sum_e delta[k][e] g[b][e]   -> one partial per tile (deterministic)
-// g and delta tiles are staged in shared memory; the g_psi contraction is register
-// blocked 4 (frames) x 4 (bases) per thread.
-constexpr int kBE = 512;
+//   g_psi[b][k]   = sum_e delta[k][e] g[b][e]   -> one partial per CTA (deterministic)
+// Each warp streams 32 consecutive channels at a time with the BP frame values in
+// registers (coalesced loads, no shared-memory staging); the g_psi products of a
+// basis k are reduce-scattered across the warp (16 values in 16 shuffles) and
+// accumulated per warp in shared memory, then summed over the CTA's warps.
 constexpr int kBT = 256;
 constexpr int kBMaxB = 16;
 constexpr int kBMaxK = 32;
+constexpr int kBBlocks = 592;   // persistent grid: 148 SMs x 4 CTAs
 
-__global__ void __launch_bounds__(kBT) blend_bwd_kernel(int64_t N, int K, int Bc, int b0, int Btot,
+template <int BP>
+__global__ void __launch_bounds__(kBT) blend_bwd_kernel(int64_t N, int K, int Bc, int b0,
                                                        const float *__restrict__ deltas,
                                                        const float *__restrict__ psi,
                                                        const float *__restrict__ g_raw,
                                                        float *__restrict__ g_base,
                                                        float *__restrict__ g_deltas,
-                                                       float *__restrict__ partials, int T10,
+                                                       float *__restrict__ partials, int P,
                                                        int accumulate) {
-    extern __shared__ float sm[];
-    const int Bp = (Bc + 3) & ~3, Kp = (K + 3) & ~3;
-    float *g_s = sm;                       // [Bp][kBE]
-    float *d_s = g_s + Bp * kBE;           // [Kp][kBE]
-    float *p_s = d_s + Kp * kBE;           // [Bc][K] psi
-    float *red = p_s + Bc * K;             // [slices][Bp][Kp]
+    __shared__ float p_s[kBMaxB * kBMaxK];
+    __shared__ float accw[kBT / 32][BP * kBMaxK];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < BP * K; i += kBT) {
+        const int b = i / K, k = i % K;
+        p_s[i] = b < Bc ? psi[(b0 + b) * K + k] : 0.f;
+    }
+    for (int i = lane; i < BP * K; i += 32) accw[warp][i] = 0.f;
+    __syncthreads();
     const int64_t E10 = 10 * N, E14 = 14 * N;
-    const int tile = blockIdx.x;
-    const int tid = threadIdx.x;
-    if (tile >= T10) {   // scale/opacity channels: only the base gradient
-        const int64_t e0 = E10 + (int64_t)(tile - T10) * kBE;
-        for (int i = tid; i < kBE; i += kBT) {
-            const int64_t e = e0 + i;
-            if (e >= E14) break;
-            float s = accumulate ? g_base[e] : 0.f;
-            for (int b = 0; b < Bc; ++b) s += g_raw[(int64_t)(b0 + b) * E14 + e];
-            g_base[e] = s;
-        }
-        return;
-    }
-    const int64_t e0 = (int64_t)tile * kBE;
-    const int cnt = (int)min((int64_t)kBE, E10 - e0);
-    for (int i = tid; i < Bc * K; i += kBT) p_s[i] = psi[(b0 + i / K) * K + i % K];
-    for (int b = 0; b < Bp; ++b)
-        for (int i = tid; i < kBE; i += kBT)
-            g_s[b * kBE + i] = (b < Bc && i < cnt) ? g_raw[(int64_t)(b0 + b) * E14 + e0 + i] : 0.f;
-    for (int k = 0; k < Kp; ++k)
-        for (int i = tid; i < kBE; i += kBT)
-            d_s[k * kBE + i] = (k < K && i < cnt) ? __ldcs(deltas + (int64_t)k * E10 + e0 + i) : 0.f;
-    __syncthreads();
-    // phase 1: base and delta gradients, coalesced writes
-    for (int i = tid; i < cnt; i += kBT) {
-        const int64_t e = e0 + i;
-        float gv[kBMaxB];
+    const int64_t chunks = (E14 + 31) / 32;
+    for (int64_t c = (int64_t)blockIdx.x * (kBT / 32) + warp; c < chunks; c += (int64_t)gridDim.x * (kBT / 32)) {
+        const int64_t e = c * 32 + lane;
+        const bool in = e < E14;
+        float g[BP];
         float s = 0.f;
 #pragma unroll
-        for (int b = 0; b < kBMaxB; ++b) {
-            gv[b] = b < Bc ? g_s[b * kBE + i] : 0.f;
-            s += gv[b];
+        for (int b = 0; b < BP; ++b) {
+            g[b] = (in && b < Bc) ? __ldcs(g_raw + (int64_t)(b0 + b) * E14 + e) : 0.f;
+            s += g[b];
         }
-        g_base[e] = accumulate ? g_base[e] + s : s;
+        if (in) g_base[e] = accumulate ? g_base[e] + s : s;
+        if (c * 32 >= E10) continue;                       // warp-uniform
+        const bool in10 = e < E10;
+#pragma unroll 4
         for (int k = 0; k < K; ++k) {
-            float acc = 0.f;
+            const float d = in10 ? __ldcs(deltas + (int64_t)k * E10 + e) : 0.f;
+            float gd = 0.f;
+            float v[BP];
 #pragma unroll
-            for (int b = 0; b < kBMaxB; ++b)
-                if (b < Bc) acc = fmaf(p_s[b * K + k], gv[b], acc);
-            float *o = g_deltas + (int64_t)k * E10 + e;
-            *o = accumulate ? *o + acc : acc;
-        }
-    }
-    // phase 2: g_psi partial over this tile, 4x4 register blocks
-    const int nbq = Bp / 4, nkq = Kp / 4, nsb = nbq * nkq;
-    const int slices = kBT / nsb;
-    const int sb = tid % nsb, sl = tid / nsb;
-    if (sl < slices) {
-        const int bq = sb / nkq, kq = sb % nkq;
-        const int span = (cnt + slices - 1) / slices;
-        const int i0 = sl * span, i1 = min(cnt, i0 + span);
-        float acc[4][4] = {};
-        for (int i = i0; i < i1; ++i) {
-            float gv[4], dv[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                gv[j] = g_s[(bq * 4 + j) * kBE + i];
-                dv[j] = d_s[(kq * 4 + j) * kBE + i];
+            for (int b = 0; b < BP; ++b) {
+                gd = fmaf(p_s[b * K + k], g[b], gd);
+                v[b] = d * g[b];
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int l = 0; l < 4; ++l) acc[j][l] = fmaf(gv[j], dv[l], acc[j][l]);
+            if (in10) {
+                float *o = g_deltas + (int64_t)k * E10 + e;
+                *o = accumulate ? *o + gd : gd;
+            }
+            int vi;
+            bool issue;
+            const float r = reduce_scatter(v, lane, vi, issue);
+            if (issue) accw[warp][k * BP + vi] += r;
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int l = 0; l < 4; ++l) red[(sl * Bp + bq * 4 + j) * Kp + kq * 4 + l] = acc[j][l];
     }
     __syncthreads();
-    for (int p = tid; p < Bc * K; p += kBT) {
-        const int b = p / K, k = p % K;
+    for (int i = tid; i < Bc * K; i += kBT) {
+        const int b = i / K, k = i % K;
         float s = 0.f;
-        for (int l = 0; l < slices; ++l) s += red[(l * Bp + b) * Kp + k];
-        partials[((int64_t)(b0 + b) * K + k) * T10 + tile] = s;
+#pragma unroll
+        for (int w = 0; w < kBT / 32; ++w) s += accw[w][k * BP + b];
+        partials[((int64_t)(b0 + b) * K + k) * P + blockIdx.x] = s;
     }
-    (void)Btot;
 }
 
 // ------------------------------------------------------------------ Adam
@@ -548,9 +539,8 @@ int hs_mlp_fwd(int B, int H, int D, int K, const float *mlp, const float *theta,
         set_error("hs_mlp_fwd: bad sizes B=%d H=%d D=%d K=%d", B, H, D, K);
         return HS_ERR_SHAPE;
     }
-    int threads = D < 128 ? 128 : (D > 1024 ? 1024 : ((D + 31) / 32) * 32);
     size_t smem = sizeof(float) * (H + 2 * D);
-    mlp_fwd_kernel<<<B, threads, smem, HS_CHECK_STREAM(stream)>>>(H, D, K, mlp, theta, cache, psi, err);
+    mlp_fwd_kernel<<<B, 256, smem, HS_CHECK_STREAM(stream)>>>(H, D, K, mlp, theta, cache, psi, err);
     return check_launch("hs_mlp_fwd");
 }
 
@@ -558,7 +548,7 @@ int hs_mlp_bwd(int B, int H, int D, int K, const float *mlp, const float *theta,
                const float *gpsi_partials, int num_partials, float *gpsi, float *scratch, float *g_mlp,
                void *stream) {
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    size_t smem = sizeof(float) * (K + D);
+    size_t smem = sizeof(float) * (K + D + 8 * D);
     mlp_bwd_frame_kernel<<<B, 256, smem, s>>>(H, D, K, mlp, cache, gpsi_partials, num_partials, gpsi, scratch);
     int64_t total = hs_mlp_size(H, D, K);
     mlp_bwd_weights_kernel<<<grid_for(total, 256), 256, 0, s>>>(B, H, D, K, theta, cache, gpsi, scratch, g_mlp);
@@ -589,7 +579,10 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
     return check_launch("hs_blend_fwd");
 }
 
-int hs_blend_bwd_partials(int64_t N) { return (int)((10 * N + kBE - 1) / kBE); }
+int hs_blend_bwd_partials(int64_t N) {
+    const int64_t warps = ((14 * N + 31) / 32 + (kBT / 32) - 1) / (kBT / 32);
+    return (int)std::min<int64_t>(kBBlocks, std::max<int64_t>(1, warps));
+}
 
 int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi, const float *g_raw14,
                  float *g_base14, float *g_deltas, float *gpsi_partials, int *num_partials, void *stream) {
@@ -598,20 +591,21 @@ int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
         return HS_ERR_SHAPE;
     }
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    const int T10 = hs_blend_bwd_partials(N);
-    const int T4 = (int)((4 * N + kBE - 1) / kBE);
-    const int Kp = (K + 3) & ~3;
+    const int P = hs_blend_bwd_partials(N);
     for (int b0 = 0; b0 < B; b0 += kBMaxB) {
         const int Bc = std::min(kBMaxB, B - b0);
-        const int Bp = (Bc + 3) & ~3;
-        const int nsb = (Bp / 4) * (Kp / 4);
-        const int slices = kBT / nsb;
-        size_t smem = sizeof(float) * ((size_t)(Bp + Kp) * kBE + Bc * K + (size_t)slices * Bp * Kp);
-        cudaFuncSetAttribute(blend_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        blend_bwd_kernel<<<T10 + T4, kBT, smem, s>>>(N, K, Bc, b0, B, deltas, psi, g_raw14, g_base14,
-                                                      g_deltas, gpsi_partials, T10, b0 > 0);
+        const int acc = b0 > 0;
+        if (Bc <= 4)
+            blend_bwd_kernel<4><<<P, kBT, 0, s>>>(N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
+                                                  gpsi_partials, P, acc);
+        else if (Bc <= 8)
+            blend_bwd_kernel<8><<<P, kBT, 0, s>>>(N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
+                                                  gpsi_partials, P, acc);
+        else
+            blend_bwd_kernel<16><<<P, kBT, 0, s>>>(N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
+                                                   gpsi_partials, P, acc);
     }
-    if (num_partials) *num_partials = T10;
+    if (num_partials) *num_partials = P;
     return check_launch("hs_blend_bwd");
 }
 

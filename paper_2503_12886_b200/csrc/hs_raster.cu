@@ -1,25 +1,37 @@
 // hs_raster.cu -- tile rasterizer (forward + adjoint) on sm_100a.
 //
-// One 256-thread CTA per (frame, 16x16 tile); one pixel per thread.  The
-// frame's depth-sorted key range for the tile is walked in chunks of 256 splat
-// records staged in shared memory (one coalesced gather per chunk, broadcast
-// reads in the inner loop).  Per pixel the math is exactly the reference's
-// front-to-back compositing (S/render.py:233-273): same bbox test, q / qmax and
-// alpha >= 1/255 cutoffs, no alpha clamp, termination at T < 1e-14 with the stop
-// index recorded for the adjoint.  Fused epilogue: background (:402), the L1
-// loss and its sign (S/metrics.py:10-22, :80-85, S/train.py:238-247), the black
-// background L1, and -- for colour init -- per-(frame, Gaussian) max blend weight
-// and the Eq. 3 weight sums (S/render.py:339-377) reduced across the warp with
-// shuffles before one atomic per warp.
+// One 256-thread CTA per (frame, 16x16 tile); one pixel per thread; each warp
+// owns an 8x4 pixel block of the tile.  The frame's depth-sorted key range for
+// the tile is walked in chunks of 256 splat records staged in shared memory (one
+// coalesced gather per chunk).  While staging, the loading thread also computes
+// which of the 8 warp blocks the splat can touch at all -- the intersection of
+// its integer pixel bbox with the exact extent of its alpha >= 1/255 ellipse
+// (q <= qmax), padded for rounding -- and each warp then iterates only over its
+// own splats (ballot-compacted bit lists).  Skipping a warp is exact: every pixel
+// of a skipped block fails the reference's bbox or q test anyway.
 //
-// The adjoint (S/render.py:276-336) walks the same range back to front per pixel
-// with the suffix recurrence, reduces the 9 per-splat gradients across each warp
-// with xor shuffles and issues one atomic per attribute per warp.
+// Per pixel the math is the reference's front-to-back compositing
+// (S/render.py:233-273): same bbox test, q / qmax and alpha >= 1/255 cutoffs, no
+// alpha clamp, termination at T < 1e-14 with the stop index recorded for the
+// adjoint.  Fused epilogue: background (:402), the L1 loss and its sign
+// (S/metrics.py:10-22, :80-85, S/train.py:238-247), the black-background L1, and
+// for colour init the per-(frame, Gaussian) max blend weight and Eq. 3 weight
+// sums (S/render.py:339-377) reduced across the warp before one atomic per value.
+//
+// The adjoint (S/render.py:276-336) walks the same lists back to front per pixel
+// with the suffix recurrence and reduces the 9 per-splat gradients across the
+// warp with a reduce-scatter (12 shuffles instead of 45) before the atomics.
 #include "hs_common.cuh"
 
 namespace hs {
 
+#ifndef HS_RASTER_MINB
+#define HS_RASTER_MINB 4             // resident CTAs per SM the register budget must allow
+#endif
+
 constexpr int kRT = kTile * kTile;   // 256 pixels / threads per CTA
+constexpr int kWarps = kRT / 32;     // 8 warps, each an 8x4 pixel block
+constexpr unsigned kFull = 0xffffffffu;
 
 struct RasterArgs {
     int B;
@@ -44,28 +56,65 @@ struct RasterArgs {
     float *g_splat;
 };
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
     return v;
+}
+
+// Pixel of thread `tid` in the tile: warp w covers cols (w & 1) * 8 .. +7 and
+// rows (w >> 1) * 4 .. +3; lane l is (col l & 7, row l >> 3) of that block.
+__device__ __forceinline__ void pixel_of(int tid, int tx, int ty, int &px, int &py) {
+    const int w = tid >> 5, l = tid & 31;
+    px = tx * kTile + (w & 1) * 8 + (l & 7);
+    py = ty * kTile + (w >> 1) * 4 + (l >> 3);
+}
+
+// Stage one splat record and compute its 8-bit warp-block mask.
+__device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, int tx, int ty, float4 &A, float4 &Bv,
+                                                float4 &Cv) {
+    const float4 *r = reinterpret_cast<const float4 *>(rec);
+    A = __ldg(r);
+    Bv = __ldg(r + 1);
+    Cv = __ldg(r + 2);
+    const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
+    int r0 = unpack_lo(rows), r1 = unpack_hi(rows), c0 = unpack_lo(cols), c1 = unpack_hi(cols);
+    // ellipse extent of q <= qmax: |dx| <= sqrt(qmax * c / det), |dy| <= sqrt(qmax * a / det)
+    const float a = A.z, b = A.w, c = Bv.x, qmax = Bv.z;
+    const float det = a * c - b * b;
+    if (qmax < 0.f) return 0u;
+    const float ex = sqrtf(qmax * c / det), ey = sqrtf(qmax * a / det);
+    if (det > 0.f && ex < 1e6f && ey < 1e6f) {
+        const float hx = ex * 1.001f + 1e-3f, hy = ey * 1.001f + 1e-3f;   // rounding margin
+        // pixel p passes |p + 0.5 - m| <= e  <=>  p in [m - e - 0.5, m + e - 0.5]
+        r0 = max(r0, (int)floorf(A.y - hy - 0.5f));
+        r1 = min(r1, (int)ceilf(A.y + hy - 0.5f));
+        c0 = max(c0, (int)floorf(A.x - hx - 0.5f));
+        c1 = min(c1, (int)ceilf(A.x + hx - 0.5f));
+    }
+    uint32_t mask = 0u;
+    const int bx = tx * kTile, by = ty * kTile;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const int x0 = bx + (w & 1) * 8, y0 = by + (w >> 1) * 4;
+        if (c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 3 && r1 >= y0) mask |= 1u << w;
+    }
+    return mask;
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
 //     3 max weight + weight sums for splats whose Gaussian is not yet visited.
 template <bool kLoss, bool kImage, int CI>
-__global__ void __launch_bounds__(kRT) raster_fwd_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a) {
     __shared__ float4 s_a[kRT], s_b[kRT], s_c[kRT];
     __shared__ uint32_t s_n[kRT];
-    __shared__ float red[2][kRT / 32];
-    const int tid = threadIdx.x;
+    __shared__ uint32_t s_mask[kRT];
+    __shared__ float red[2][kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x, b = blockIdx.y;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid / kTile);
+    int px, py;
+    pixel_of(tid, tx, ty, px, py);
     const bool inside = px < a.W && py < a.H;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
@@ -95,60 +144,67 @@ __global__ void __launch_bounds__(kRT) raster_fwd_kernel(RasterArgs a) {
     for (uint32_t c0 = start; c0 < end; c0 += kRT) {
         if (__syncthreads_count(!done) == 0) break;
         const uint32_t idx = c0 + tid;
+        uint32_t m = 0u;
         if (idx < end) {
             const uint32_t n = a.vals[idx];
-            const float4 *r = reinterpret_cast<const float4 *>(a.records + ((int64_t)b * a.N + n) * kRec);
-            s_a[tid] = __ldg(r);
-            s_b[tid] = __ldg(r + 1);
-            s_c[tid] = __ldg(r + 2);
+            float4 A, Bv, Cv;
+            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, tx, ty, A, Bv, Cv);
+            s_a[tid] = A;
+            s_b[tid] = Bv;
+            s_c[tid] = Cv;
             uint32_t flag = n;
             if (CI == 3 && a.visited[n]) flag |= 0x80000000u;   // visited: skip colour-init work
             s_n[tid] = flag;
         }
+        s_mask[tid] = m;
         __syncthreads();
         const int cnt = (int)min((uint32_t)kRT, end - c0);
-        for (int j = 0; j < cnt; ++j) {
-            float w = 0.f;
-            if (!done) {
-                const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
-                const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
-                if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) && px <= unpack_hi(cols)) {
-                    const float dx = fpx - A.x, dy = fpy - A.y;
-                    const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
-                    if (q <= Bv.z) {
-                        const float alpha = Bv.y * __expf(-0.5f * q);
-                        if (alpha >= kAlphaCutoff) {
-                            w = alpha * T;
-                            C[0] += w * Cv.y;
-                            C[1] += w * Cv.z;
-                            C[2] += w * Cv.w;
-                            T = T * (1.0f - alpha);
-                            if (T < kTermEps) {
-                                done = true;
-                                stop = c0 - start + (uint32_t)j + 1u;
+        if (!__all_sync(kFull, done)) {
+            for (int i = 0; i < (cnt + 31) / 32; ++i) {
+                uint32_t bits = __ballot_sync(kFull, (s_mask[i * 32 + lane] >> warp) & 1u);
+                while (bits) {
+                    const int j = i * 32 + __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    float w = 0.f;
+                    if (!done) {
+                        const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
+                        const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
+                        if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) &&
+                            px <= unpack_hi(cols)) {
+                            const float dx = fpx - A.x, dy = fpy - A.y;
+                            const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
+                            if (q <= Bv.z) {
+                                const float alpha = Bv.y * __expf(-0.5f * q);
+                                if (alpha >= kAlphaCutoff) {
+                                    w = alpha * T;
+                                    C[0] += w * Cv.y;
+                                    C[1] += w * Cv.z;
+                                    C[2] += w * Cv.w;
+                                    T = T * (1.0f - alpha);
+                                    if (T < kTermEps) {
+                                        done = true;
+                                        stop = c0 - start + (uint32_t)j + 1u;
+                                    }
+                                }
                             }
                         }
                     }
-                }
-            }
-            if (CI > 0) {
-                const uint32_t flag = s_n[j];
-                const bool want = CI != 3 || !(flag & 0x80000000u);
-                if (want && __any_sync(0xffffffffu, w > 0.f)) {
-                    const int64_t g = (int64_t)b * a.N + (flag & 0x7FFFFFFFu);
-                    const float wm = warp_max(w);
-                    if (CI >= 2) {
-                        const float s0 = warp_sum(w * ws_src[0]);
-                        const float s1 = warp_sum(w * ws_src[1]);
-                        const float s2 = warp_sum(w * ws_src[2]);
-                        const float sw = warp_sum(w);
-                        const int lane = tid & 31;
-                        if (lane < 4) {
-                            const float v = lane == 0 ? s0 : lane == 1 ? s1 : lane == 2 ? s2 : sw;
-                            atomicAdd(a.wsums + g * 4 + lane, v);
+                    if (CI > 0) {
+                        const uint32_t flag = s_n[j];
+                        const bool want = CI != 3 || !(flag & 0x80000000u);
+                        if (want && __any_sync(kFull, w > 0.f)) {
+                            const int64_t g = (int64_t)b * a.N + (flag & 0x7FFFFFFFu);
+                            const float wm = warp_max(w);
+                            if (CI >= 2) {
+                                const float v[4] = {w * ws_src[0], w * ws_src[1], w * ws_src[2], w};
+                                int vi;
+                                bool issue;
+                                const float s = reduce_scatter(v, lane, vi, issue);
+                                if (issue) atomicAdd(a.wsums + g * 4 + vi, s);
+                            }
+                            if (lane == 0) atomicMax(reinterpret_cast<int *>(a.maxw) + g, __float_as_int(wm));
                         }
                     }
-                    if ((tid & 31) == 0) atomicMax(reinterpret_cast<int *>(a.maxw) + g, __float_as_int(wm));
                 }
             }
         }
@@ -180,14 +236,14 @@ __global__ void __launch_bounds__(kRT) raster_fwd_kernel(RasterArgs a) {
     if (kLoss) {
         l1 = warp_sum(l1);
         black = warp_sum(black);
-        if ((tid & 31) == 0) {
-            red[0][tid >> 5] = l1;
-            red[1][tid >> 5] = black;
+        if (lane == 0) {
+            red[0][warp] = l1;
+            red[1][warp] = black;
         }
         __syncthreads();
         if (tid == 0) {
             float s0 = 0.f, s1 = 0.f;
-            for (int i = 0; i < kRT / 32; ++i) { s0 += red[0][i]; s1 += red[1][i]; }
+            for (int i = 0; i < kWarps; ++i) { s0 += red[0][i]; s1 += red[1][i]; }
             const int tiles = gridDim.x;
             a.loss_partials[((int64_t)b * tiles + tile) * 2] = s0;
             a.loss_partials[((int64_t)b * tiles + tile) * 2 + 1] = s1;
@@ -196,14 +252,16 @@ __global__ void __launch_bounds__(kRT) raster_fwd_kernel(RasterArgs a) {
 }
 
 template <bool kExplicitGrad>
-__global__ void __launch_bounds__(kRT) raster_bwd_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a) {
     __shared__ float4 s_a[kRT], s_b[kRT], s_c[kRT];
     __shared__ uint32_t s_n[kRT];
-    __shared__ uint32_t s_max[kRT / 32];
-    const int tid = threadIdx.x, lane = tid & 31;
+    __shared__ uint32_t s_mask[kRT];
+    __shared__ uint32_t s_max[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x, b = blockIdx.y;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid / kTile);
+    int px, py;
+    pixel_of(tid, tx, ty, px, py);
     const bool inside = px < a.W && py < a.H;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
@@ -233,75 +291,82 @@ __global__ void __launch_bounds__(kRT) raster_bwd_kernel(RasterArgs a) {
         suffix = Tf * (g[0] * a.bgs[3 * b] + g[1] * a.bgs[3 * b + 1] + g[2] * a.bgs[3 * b + 2]);
     }
     // last local index any pixel of the tile needs
-    const uint32_t wmax = __reduce_max_sync(0xffffffffu, stop);
-    if (lane == 0) s_max[tid >> 5] = wmax;
+    const uint32_t wmax = __reduce_max_sync(kFull, stop);
+    if (lane == 0) s_max[warp] = wmax;
     __syncthreads();
     uint32_t maxstop = 0;
 #pragma unroll
-    for (int i = 0; i < kRT / 32; ++i) maxstop = max(maxstop, s_max[i]);
+    for (int i = 0; i < kWarps; ++i) maxstop = max(maxstop, s_max[i]);
     const uint32_t last = start + maxstop;
 
     for (uint32_t c_end = last; c_end > start;) {
         const uint32_t c0 = c_end - start > (uint32_t)kRT ? c_end - kRT : start;
         const uint32_t idx = c0 + tid;
         __syncthreads();
+        uint32_t m = 0u;
         if (idx < c_end) {
             const uint32_t n = a.vals[idx];
-            const float4 *r = reinterpret_cast<const float4 *>(a.records + ((int64_t)b * a.N + n) * kRec);
-            s_a[tid] = __ldg(r);
-            s_b[tid] = __ldg(r + 1);
-            s_c[tid] = __ldg(r + 2);
+            float4 A, Bv, Cv;
+            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, tx, ty, A, Bv, Cv);
+            s_a[tid] = A;
+            s_b[tid] = Bv;
+            s_c[tid] = Cv;
             s_n[tid] = n;
         }
+        s_mask[tid] = m;
         __syncthreads();
-        for (int j = (int)(c_end - c0) - 1; j >= 0; --j) {
-            const uint32_t jl = c0 - start + (uint32_t)j;
-            float gv[9];
-            bool contrib = false;
-            if (jl < stop) {
-                const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
-                const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
-                if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) && px <= unpack_hi(cols)) {
-                    const float dx = fpx - A.x, dy = fpy - A.y;
-                    const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
-                    if (q <= Bv.z) {
-                        const float G = __expf(-0.5f * q);
-                        const float alpha = Bv.y * G;
-                        if (alpha >= kAlphaCutoff) {
-                            contrib = true;
-                            const float one_m = 1.0f - alpha;
-                            const float t_prior = t_rev / one_m;
-                            const float gw = g[0] * Cv.y + g[1] * Cv.z + g[2] * Cv.w;
-                            const float wgt = alpha * t_prior;
-                            gv[6] = wgt * g[0];
-                            gv[7] = wgt * g[1];
-                            gv[8] = wgt * g[2];
-                            const float d_alpha = t_prior * gw - suffix / one_m;
-                            gv[5] = G * d_alpha;
-                            const float dq = -0.5f * alpha * d_alpha;
-                            gv[2] = dq * dx * dx;
-                            gv[3] = 2.0f * dq * dx * dy;
-                            gv[4] = dq * dy * dy;
-                            gv[0] = -2.0f * dq * (A.z * dx + A.w * dy);
-                            gv[1] = -2.0f * dq * (A.w * dx + Bv.x * dy);
-                            suffix += wgt * gw;
-                            t_rev = t_prior;
+        const int cnt = (int)(c_end - c0);
+        for (int i = (cnt - 1) / 32; i >= 0; --i) {
+            uint32_t bits = __ballot_sync(kFull, (s_mask[i * 32 + lane] >> warp) & 1u);
+            while (bits) {
+                const int hb = 31 - __clz(bits);
+                bits &= ~(1u << hb);
+                const int j = i * 32 + hb;
+                const uint32_t jl = c0 - start + (uint32_t)j;
+                float gv[9];
+                bool contrib = false;
+                if (jl < stop) {
+                    const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
+                    const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
+                    if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) &&
+                        px <= unpack_hi(cols)) {
+                        const float dx = fpx - A.x, dy = fpy - A.y;
+                        const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
+                        if (q <= Bv.z) {
+                            const float G = __expf(-0.5f * q);
+                            const float alpha = Bv.y * G;
+                            if (alpha >= kAlphaCutoff) {
+                                contrib = true;
+                                const float one_m = 1.0f - alpha;
+                                const float t_prior = t_rev / one_m;
+                                const float gw = g[0] * Cv.y + g[1] * Cv.z + g[2] * Cv.w;
+                                const float wgt = alpha * t_prior;
+                                gv[6] = wgt * g[0];
+                                gv[7] = wgt * g[1];
+                                gv[8] = wgt * g[2];
+                                const float d_alpha = t_prior * gw - suffix / one_m;
+                                gv[5] = G * d_alpha;
+                                const float dq = -0.5f * alpha * d_alpha;
+                                gv[2] = dq * dx * dx;
+                                gv[3] = 2.0f * dq * dx * dy;
+                                gv[4] = dq * dy * dy;
+                                gv[0] = -2.0f * dq * (A.z * dx + A.w * dy);
+                                gv[1] = -2.0f * dq * (A.w * dx + Bv.x * dy);
+                                suffix += wgt * gw;
+                                t_rev = t_prior;
+                            }
                         }
                     }
                 }
-            }
-            if (__any_sync(0xffffffffu, contrib)) {
-                if (!contrib) {
+                if (__any_sync(kFull, contrib)) {
+                    if (!contrib) {
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) gv[k] = 0.f;
-                }
-#pragma unroll
-                for (int k = 0; k < 9; ++k) gv[k] = warp_sum(gv[k]);
-                if (lane < 9) {
-                    float v = gv[0];
-#pragma unroll
-                    for (int k = 1; k < 9; ++k) v = lane == k ? gv[k] : v;
-                    atomicAdd(a.g_splat + ((int64_t)b * a.N + s_n[j]) * kGS + lane, v);
+                        for (int k = 0; k < 9; ++k) gv[k] = 0.f;
+                    }
+                    int vi;
+                    bool issue;
+                    const float s = reduce_scatter(gv, lane, vi, issue);
+                    if (issue) atomicAdd(a.g_splat + ((int64_t)b * a.N + s_n[j]) * kGS + vi, s);
                 }
             }
         }

@@ -29,7 +29,7 @@ def test_pure_queries():
     assert lib.hs_scan_blocks(1000) == 4
     assert lib.hs_mlp_size(13, 128, 20) == 128 * 13 + 128 + 128 * 128 + 128 + 20 * 128 + 20
     assert lib.hs_sort_workspace_size(1 << 20) > 0
-    assert lib.hs_blend_bwd_partials(100) == (1000 + 511) // 512
+    assert 1 <= lib.hs_blend_bwd_partials(100) <= lib.hs_blend_bwd_partials(50176) <= 592
 
 
 def test_device_error_mapping():
