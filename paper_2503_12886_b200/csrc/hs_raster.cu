@@ -70,19 +70,65 @@ __device__ __forceinline__ void pixel_of(int tid, int tx, int ty, int &px, int &
     py = ty * kTile + (w >> 1) * 4 + (l >> 3);
 }
 
-// Stage one splat record and compute its 8-bit warp-block mask.
-__device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, int tx, int ty, float4 &A, float4 &Bv,
-                                                float4 &Cv) {
+// ---- staged splat layout (shared memory, 64 B per splat) -------------------
+//   p0: mx - 0.5, my - 0.5, k*a, 2k*b     with k = -0.5 log2(e), so that
+//       e2 = k*q = dx (k a dx + 2k b dy) + k c dy^2 and alpha = op * 2^e2;
+//       q <= qmax  <=>  e2 >= k*qmax  (k < 0)
+//   p1: k*c, k*qmax, opacity, gidx | visited << 31   (gidx = frame * N + n)
+//   p2: c_lo, c_hi, r_lo, r_hi  (the reference's pixel bbox, S/render.py:248-251)
+//   p3: colour r, g, b, 0
+// Forward and adjoint evaluate e2 / alpha through the same explicit-rounding
+// helpers, so both make identical pair decisions.
+constexpr float kK = -0.72134752044448170f;      // -0.5 * log2(e)
+constexpr float kMeanScale = -2.0f / kK;         // d q / d(k q) folded into g_mean
+constexpr int kStageBytes = 64;
+
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ int4 lds4i(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds1(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// e2 = k q(dx, dy), one rounding per operation (no contraction differences between kernels)
+__device__ __forceinline__ float splat_e2(float dx, float dy, float ka, float kb2, float kc) {
+    const float t = __fmaf_rn(kb2, dy, __fmul_rn(ka, dx));
+    return __fmaf_rn(__fmul_rn(kc, dy), dy, __fmul_rn(dx, t));
+}
+
+// Stage one splat record into shared memory and return its 8-bit warp-block mask:
+// warp w's 8x4 block can hold a contributing pixel only if it intersects the
+// integer bbox AND the extent of the q <= qmax ellipse (padded for rounding).
+__device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, uint32_t gflag, int tx, int ty,
+                                                uint32_t saddr) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
-    A = __ldg(r);
-    Bv = __ldg(r + 1);
-    Cv = __ldg(r + 2);
+    const float4 A = __ldg(r), Bv = __ldg(r + 1), Cv = __ldg(r + 2);
     const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
-    int r0 = unpack_lo(rows), r1 = unpack_hi(rows), c0 = unpack_lo(cols), c1 = unpack_hi(cols);
-    // ellipse extent of q <= qmax: |dx| <= sqrt(qmax * c / det), |dy| <= sqrt(qmax * a / det)
+    const int rl = unpack_lo(rows), rh = unpack_hi(rows), cl = unpack_lo(cols), ch = unpack_hi(cols);
     const float a = A.z, b = A.w, c = Bv.x, qmax = Bv.z;
-    const float det = a * c - b * b;
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "f"(A.x - 0.5f), "f"(A.y - 0.5f),
+                 "f"(kK * a), "f"(2.0f * kK * b));
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 16), "f"(kK * c), "f"(kK * qmax),
+                 "f"(Bv.y), "f"(__uint_as_float(gflag)));
+    asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 32), "r"(cl), "r"(ch), "r"(rl), "r"(rh));
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 48), "f"(Cv.y), "f"(Cv.z), "f"(Cv.w),
+                 "f"(0.f));
     if (qmax < 0.f) return 0u;
+    int r0 = rl, r1 = rh, c0 = cl, c1 = ch;
+    const float det = a * c - b * b;
     const float ex = sqrtf(qmax * c / det), ey = sqrtf(qmax * a / det);
     if (det > 0.f && ex < 1e6f && ey < 1e6f) {
         const float hx = ex * 1.001f + 1e-3f, hy = ey * 1.001f + 1e-3f;   // rounding margin
@@ -106,8 +152,7 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, i
 //     3 max weight + weight sums for splats whose Gaussian is not yet visited.
 template <bool kLoss, bool kImage, int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a) {
-    __shared__ float4 s_a[kRT], s_b[kRT], s_c[kRT];
-    __shared__ uint32_t s_n[kRT];
+    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
     __shared__ uint32_t s_mask[kRT];
     __shared__ float red[2][kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -118,8 +163,9 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
     const bool inside = px < a.W && py < a.H;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
-    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+    const float fpx = (float)px, fpy = (float)py;
     const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_stage);
 
     float tgt[3] = {0.f, 0.f, 0.f}, rgba_a = 0.f, rgb[3] = {0.f, 0.f, 0.f};
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
@@ -147,14 +193,9 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
         uint32_t m = 0u;
         if (idx < end) {
             const uint32_t n = a.vals[idx];
-            float4 A, Bv, Cv;
-            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, tx, ty, A, Bv, Cv);
-            s_a[tid] = A;
-            s_b[tid] = Bv;
-            s_c[tid] = Cv;
-            uint32_t flag = n;
-            if (CI == 3 && a.visited[n]) flag |= 0x80000000u;   // visited: skip colour-init work
-            s_n[tid] = flag;
+            uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
+            if (CI == 3 && a.visited[n]) gflag |= 0x80000000u;   // visited: skip colour-init work
+            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, tx, ty, sbase + tid * kStageBytes);
         }
         s_mask[tid] = m;
         __syncthreads();
@@ -165,21 +206,22 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
                 while (bits) {
                     const int j = i * 32 + __ffs(bits) - 1;
                     bits &= bits - 1u;
+                    const uint32_t ad = sbase + j * kStageBytes;
                     float w = 0.f;
                     if (!done) {
-                        const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
-                        const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
-                        if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) &&
-                            px <= unpack_hi(cols)) {
-                            const float dx = fpx - A.x, dy = fpy - A.y;
-                            const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
-                            if (q <= Bv.z) {
-                                const float alpha = Bv.y * __expf(-0.5f * q);
+                        const int4 bb = lds4i(ad + 32);
+                        if (px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w) {
+                            const float4 p0 = lds4(ad), p1 = lds4(ad + 16);
+                            const float dx = fpx - p0.x, dy = fpy - p0.y;
+                            const float e2 = splat_e2(dx, dy, p0.z, p0.w, p1.x);
+                            if (e2 >= p1.y) {
+                                const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
                                 if (alpha >= kAlphaCutoff) {
+                                    const float4 col = lds4(ad + 48);
                                     w = alpha * T;
-                                    C[0] += w * Cv.y;
-                                    C[1] += w * Cv.z;
-                                    C[2] += w * Cv.w;
+                                    C[0] += w * col.x;
+                                    C[1] += w * col.y;
+                                    C[2] += w * col.z;
                                     T = T * (1.0f - alpha);
                                     if (T < kTermEps) {
                                         done = true;
@@ -190,10 +232,10 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
                         }
                     }
                     if (CI > 0) {
-                        const uint32_t flag = s_n[j];
-                        const bool want = CI != 3 || !(flag & 0x80000000u);
+                        const uint32_t gf = lds1(ad + 28);
+                        const bool want = CI != 3 || !(gf & 0x80000000u);
                         if (want && __any_sync(kFull, w > 0.f)) {
-                            const int64_t g = (int64_t)b * a.N + (flag & 0x7FFFFFFFu);
+                            const int64_t g = gf & 0x7FFFFFFFu;
                             const float wm = warp_max(w);
                             if (CI >= 2) {
                                 const float v[4] = {w * ws_src[0], w * ws_src[1], w * ws_src[2], w};
@@ -253,8 +295,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
 
 template <bool kExplicitGrad>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a) {
-    __shared__ float4 s_a[kRT], s_b[kRT], s_c[kRT];
-    __shared__ uint32_t s_n[kRT];
+    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
     __shared__ uint32_t s_mask[kRT];
     __shared__ uint32_t s_max[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -266,8 +307,9 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     if (start >= end) return;
-    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+    const float fpx = (float)px, fpy = (float)py;
     const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_stage);
 
     float g[3] = {0.f, 0.f, 0.f};
     uint32_t stop = 0;
@@ -306,12 +348,8 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
         uint32_t m = 0u;
         if (idx < c_end) {
             const uint32_t n = a.vals[idx];
-            float4 A, Bv, Cv;
-            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, tx, ty, A, Bv, Cv);
-            s_a[tid] = A;
-            s_b[tid] = Bv;
-            s_c[tid] = Cv;
-            s_n[tid] = n;
+            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), tx, ty,
+                            sbase + tid * kStageBytes);
         }
         s_mask[tid] = m;
         __syncthreads();
@@ -323,35 +361,39 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
                 bits &= ~(1u << hb);
                 const int j = i * 32 + hb;
                 const uint32_t jl = c0 - start + (uint32_t)j;
+                const uint32_t ad = sbase + j * kStageBytes;
                 float gv[9];
                 bool contrib = false;
                 if (jl < stop) {
-                    const float4 A = s_a[j], Bv = s_b[j], Cv = s_c[j];
-                    const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
-                    if (py >= unpack_lo(rows) && py <= unpack_hi(rows) && px >= unpack_lo(cols) &&
-                        px <= unpack_hi(cols)) {
-                        const float dx = fpx - A.x, dy = fpy - A.y;
-                        const float q = A.z * dx * dx + 2.0f * A.w * dx * dy + Bv.x * dy * dy;
-                        if (q <= Bv.z) {
-                            const float G = __expf(-0.5f * q);
-                            const float alpha = Bv.y * G;
+                    const int4 bb = lds4i(ad + 32);
+                    if (px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w) {
+                        const float4 p0 = lds4(ad), p1 = lds4(ad + 16);
+                        const float dx = fpx - p0.x, dy = fpy - p0.y;
+                        const float e2 = splat_e2(dx, dy, p0.z, p0.w, p1.x);
+                        if (e2 >= p1.y) {
+                            const float G = ex2_approx(e2);
+                            const float alpha = __fmul_rn(p1.z, G);
                             if (alpha >= kAlphaCutoff) {
                                 contrib = true;
-                                const float one_m = 1.0f - alpha;
-                                const float t_prior = t_rev / one_m;
-                                const float gw = g[0] * Cv.y + g[1] * Cv.z + g[2] * Cv.w;
+                                const float4 col = lds4(ad + 48);
+                                const float inv = __fdividef(1.0f, 1.0f - alpha);
+                                const float t_prior = t_rev * inv;
+                                const float gw = g[0] * col.x + g[1] * col.y + g[2] * col.z;
                                 const float wgt = alpha * t_prior;
                                 gv[6] = wgt * g[0];
                                 gv[7] = wgt * g[1];
                                 gv[8] = wgt * g[2];
-                                const float d_alpha = t_prior * gw - suffix / one_m;
+                                const float d_alpha = t_prior * gw - suffix * inv;
                                 gv[5] = G * d_alpha;
                                 const float dq = -0.5f * alpha * d_alpha;
-                                gv[2] = dq * dx * dx;
-                                gv[3] = 2.0f * dq * dx * dy;
-                                gv[4] = dq * dy * dy;
-                                gv[0] = -2.0f * dq * (A.z * dx + A.w * dy);
-                                gv[1] = -2.0f * dq * (A.w * dx + Bv.x * dy);
+                                const float dqx = dq * dx, dqy = dq * dy;
+                                gv[2] = dqx * dx;
+                                gv[3] = 2.0f * dqx * dy;
+                                gv[4] = dqy * dy;
+                                // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
+                                const float hb2 = 0.5f * p0.w;
+                                gv[0] = kMeanScale * (p0.z * dqx + hb2 * dqy);
+                                gv[1] = kMeanScale * (hb2 * dqx + p1.x * dqy);
                                 suffix += wgt * gw;
                                 t_rev = t_prior;
                             }
@@ -366,7 +408,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
                     int vi;
                     bool issue;
                     const float s = reduce_scatter(gv, lane, vi, issue);
-                    if (issue) atomicAdd(a.g_splat + ((int64_t)b * a.N + s_n[j]) * kGS + vi, s);
+                    if (issue) atomicAdd(a.g_splat + (uint64_t)lds1(ad + 28) * kGS + vi, s);
                 }
             }
         }
