@@ -611,12 +611,15 @@ def frame_forward(model: Model, theta, frames: Frames):
     return world, FrameCtx(psi, cache, raw, act, frames)
 
 
-def frame_backward(model: Model, ctx: FrameCtx, grad_image, acc):
-    """S/train.py:152-161 with the item-order reduction (:253-255) accumulated into acc."""
+def frame_backward(model: Model, ctx: FrameCtx, grad_image):
+    """S/train.py:152-161: the full per-item adjoint chain (runs on a worker thread,
+    like the reference's map_items).  Returns (g_base14, g_deltas, g_mlp) of this item."""
     g_world = render_backward(ctx.splats, ctx.aux, grad_image)
     g_act = transform_backward(ctx.act, ctx.frames, model.tri_index, g_world)
     g_raw = activate_backward(ctx.raw, ctx.act, g_act)
-    return g_raw
+    g_base14, g_deltas, g_psi = blend_backward(model, ctx.psi, g_raw)
+    g_mlp = mlp_backward(model.mlp, ctx.cache, g_psi)
+    return g_base14, g_deltas, g_mlp
 
 
 class State:
@@ -643,10 +646,15 @@ class State:
             self.pool.shutdown()
 
 
-def train_step(state: State, thetas, images, frames_list, backgrounds, replay=None):
+def train_step(state: State, thetas, images, frames_list, backgrounds, replay=None, global_batch=None,
+               reduce_fn=None):
     """S/train.py:214-260.  images: (B, H, W, 4) straight RGBA in [0, 1].
     Returns (mean loss, black-bg L1 per item).  The summed gradients passed to
     Adam are kept on state.last_grads (g_base14, g_deltas, g_mlp).
+
+    ``global_batch`` / ``reduce_fn`` (checker extensions for the data-parallel
+    split): image gradients are scaled by 1/global_batch and the summed
+    gradients pass through ``reduce_fn`` (e.g. a gloo allreduce) before Adam.
 
     ``replay`` (checker extension): per frame a dict with ``order``
     (compositing order over the kept splats) and ``bbox`` (int pixel bbox per kept
@@ -680,18 +688,23 @@ def train_step(state: State, thetas, images, frames_list, backgrounds, replay=No
         target = composite_over(images[b], backgrounds[b])
         loss, gimg = l1_loss(image, target)
         losses[b] = loss
-        grads_img.append(gimg / B)
+        grads_img.append(gimg / (global_batch or B))
         bp = image - aux.transmittance[:, :, None] * _f64(backgrounds[b])[None, None, :]
         bt = _f64(images[b])[:, :, :3] * _f64(images[b])[:, :, 3:4]
         black[b] = float(np.mean(np.abs(bp - bt)))
-    g_raws = state.map(lambda c, g: frame_backward(model, c, g, None), list(zip(ctxs, grads_img)))
+    per_item = state.map(lambda c, g: frame_backward(model, c, g), list(zip(ctxs, grads_img)))
+    # ParamGradients reduction in item order (S/train.py:253-255)
     n = model.count
     g_base14 = np.zeros(14 * n)
     g_deltas = np.zeros((model.K, 10 * n))
     g_mlp = {k: np.zeros_like(v, dtype=np.float64) for k, v in model.mlp.items()}
-    for b in range(B):
-        _, _, g_psi = blend_backward(model, ctxs[b].psi, g_raws[b], g_base14, g_deltas)
-        mlp_backward(model.mlp, ctxs[b].cache, g_psi, into=g_mlp)
+    for gb, gd, gm in per_item:
+        g_base14 += gb
+        g_deltas += gd
+        for k in g_mlp:
+            g_mlp[k] += gm[k]
+    if reduce_fn is not None:          # cross-rank sum (multi-process checker)
+        g_base14, g_deltas, g_mlp = reduce_fn(g_base14, g_deltas, g_mlp)
     g_base = GSet(g_base14[:3 * n].reshape(n, 3), g_base14[3 * n:7 * n].reshape(n, 4),
                   g_base14[10 * n:13 * n].reshape(n, 3), g_base14[13 * n:], g_base14[7 * n:10 * n].reshape(n, 3))
     state.last_grads = (g_base.copy(), g_deltas.copy(), {k: v.copy() for k, v in g_mlp.items()})
