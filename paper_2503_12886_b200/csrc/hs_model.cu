@@ -246,13 +246,16 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
 // registers (coalesced loads, no shared-memory staging); the g_psi products of a
 // basis k are reduce-scattered across the warp (16 values in 16 shuffles) and
 // accumulated per warp in shared memory, then summed over the CTA's warps.
+#ifndef HS_BLEND_MINB
+#define HS_BLEND_MINB 3
+#endif
 constexpr int kBT = 256;
 constexpr int kBMaxB = 16;
 constexpr int kBMaxK = 32;
 constexpr int kBBlocks = 592;   // persistent grid: 148 SMs x 4 CTAs
 
 template <int BP>
-__global__ void __launch_bounds__(kBT) blend_bwd_kernel(int64_t N, int K, int Bc, int b0,
+__global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N, int K, int Bc, int b0,
                                                        const float *__restrict__ deltas,
                                                        const float *__restrict__ psi,
                                                        const float *__restrict__ g_raw,

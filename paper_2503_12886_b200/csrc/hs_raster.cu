@@ -1,14 +1,15 @@
 // hs_raster.cu -- tile rasterizer (forward + adjoint) on sm_100a.
 //
-// One 256-thread CTA per (frame, 16x16 tile); one pixel per thread; each warp
-// owns an 8x4 pixel block of the tile.  The frame's depth-sorted key range for
-// the tile is walked in chunks of 256 splat records staged in shared memory (one
-// coalesced gather per chunk).  While staging, the loading thread also computes
-// which of the 8 warp blocks the splat can touch at all -- the intersection of
-// its integer pixel bbox with the exact extent of its alpha >= 1/255 ellipse
-// (q <= qmax), padded for rounding -- and each warp then iterates only over its
-// own splats (ballot-compacted bit lists).  Skipping a warp is exact: every pixel
-// of a skipped block fails the reference's bbox or q test anyway.
+// One 128-thread CTA per (frame, 16x16 tile).  Each warp owns an 8x8 pixel block
+// and each lane two pixels of it (rows r and r+4 of one column), so the per-splat
+// overhead (list walk, shared loads, the warp reduction of the adjoint) is paid
+// once per 64 pixels.  Every warp walks the tile's depth-ordered key range on its
+// own, 32 splats per batch: each lane gathers one 48-byte record, pre-transforms it
+// into a 64-byte staged form in the warp's private shared slot and votes whether
+// the warp's 8x8 block can be touched at all -- the intersection of the splat's
+// integer pixel bbox with the exact extent of its alpha >= 1/255 ellipse (q <=
+// qmax), padded for rounding.  Skipping a block is exact: every pixel in it fails
+// the reference's bbox or q test anyway.  There is no CTA barrier in the loop.
 //
 // Per pixel the math is the reference's front-to-back compositing
 // (S/render.py:233-273): same bbox test, q / qmax and alpha >= 1/255 cutoffs, no
@@ -19,18 +20,19 @@
 // sums (S/render.py:339-377) reduced across the warp before one atomic per value.
 //
 // The adjoint (S/render.py:276-336) walks the same lists back to front per pixel
-// with the suffix recurrence and reduces the 9 per-splat gradients across the
-// warp with a reduce-scatter (12 shuffles instead of 45) before the atomics.
+// with the suffix recurrence; each lane first adds its two pixels' contributions,
+// then the 9 per-splat gradients are reduce-scattered across the warp (12 shuffles)
+// before one RED per value.
 #include "hs_common.cuh"
 
 namespace hs {
 
 #ifndef HS_RASTER_MINB
-#define HS_RASTER_MINB 4             // resident CTAs per SM the register budget must allow
+#define HS_RASTER_MINB 8             // resident CTAs per SM the register budget must allow
 #endif
 
-constexpr int kRT = kTile * kTile;   // 256 pixels / threads per CTA
-constexpr int kWarps = kRT / 32;     // 8 warps, each an 8x4 pixel block
+constexpr int kRT = 128;             // threads per CTA: 4 warps x (8x8 pixels, 2 per lane)
+constexpr int kWarps = kRT / 32;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct RasterArgs {
@@ -62,14 +64,6 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-// Pixel of thread `tid` in the tile: warp w covers cols (w & 1) * 8 .. +7 and
-// rows (w >> 1) * 4 .. +3; lane l is (col l & 7, row l >> 3) of that block.
-__device__ __forceinline__ void pixel_of(int tid, int tx, int ty, int &px, int &py) {
-    const int w = tid >> 5, l = tid & 31;
-    px = tx * kTile + (w & 1) * 8 + (l & 7);
-    py = ty * kTile + (w >> 1) * 4 + (l >> 3);
-}
-
 // ---- staged splat layout (shared memory, 64 B per splat) -------------------
 //   p0: mx - 0.5, my - 0.5, k*a, 2k*b     with k = -0.5 log2(e), so that
 //       e2 = k*q = dx (k a dx + 2k b dy) + k c dy^2 and alpha = op * 2^e2;
@@ -77,8 +71,8 @@ __device__ __forceinline__ void pixel_of(int tid, int tx, int ty, int &px, int &
 //   p1: k*c, k*qmax, opacity, gidx | visited << 31   (gidx = frame * N + n)
 //   p2: c_lo, c_hi, r_lo, r_hi  (the reference's pixel bbox, S/render.py:248-251)
 //   p3: colour r, g, b, 0
-// Forward and adjoint evaluate e2 / alpha through the same explicit-rounding
-// helpers, so both make identical pair decisions.
+// Forward and adjoint evaluate e2 / alpha with the same explicit-rounding
+// expression, so both make identical pair decisions.
 constexpr float kK = -0.72134752044448170f;      // -0.5 * log2(e)
 constexpr float kMeanScale = -2.0f / kK;         // d q / d(k q) folded into g_mean
 constexpr int kStageBytes = 64;
@@ -93,27 +87,28 @@ __device__ __forceinline__ int4 lds4i(uint32_t addr) {
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
-__device__ __forceinline__ uint32_t lds1(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// e2 = k q(dx, dy), one rounding per operation (no contraction differences between kernels)
-__device__ __forceinline__ float splat_e2(float dx, float dy, float ka, float kb2, float kc) {
-    const float t = __fmaf_rn(kb2, dy, __fmul_rn(ka, dx));
-    return __fmaf_rn(__fmul_rn(kc, dy), dy, __fmul_rn(dx, t));
+// e2 = k q(dx, dy) given kadx = k a dx; one rounding per operation
+__device__ __forceinline__ float splat_e2(float dx, float dy, float kadx, float kb2, float kc) {
+    return __fmaf_rn(__fmul_rn(kc, dy), dy, __fmul_rn(dx, __fmaf_rn(kb2, dy, kadx)));
 }
 
-// Stage one splat record into shared memory and return its 8-bit warp-block mask:
-// warp w's 8x4 block can hold a contributing pixel only if it intersects the
-// integer bbox AND the extent of the q <= qmax ellipse (padded for rounding).
-__device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, uint32_t gflag, int tx, int ty,
-                                                uint32_t saddr) {
+// Pixels of thread `tid`: warp w covers cols (w & 1) * 8 .. +7 and rows
+// (w >> 1) * 8 .. +7 of the tile; lane l holds column l & 7 and rows (l >> 3), +4.
+__device__ __forceinline__ void pixels_of(int tid, int tx, int ty, int &px, int &py0) {
+    const int w = tid >> 5, l = tid & 31;
+    px = tx * kTile + (w & 1) * 8 + (l & 7);
+    py0 = ty * kTile + (w >> 1) * 8 + (l >> 3);
+}
+
+// Stage one splat record into the lane's slot and vote whether the warp's 8x8 block
+// [x0, x0+7] x [y0, y0+7] can hold a contributing pixel.
+__device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
+                                            uint32_t saddr) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
     const float4 A = __ldg(r), Bv = __ldg(r + 1), Cv = __ldg(r + 2);
     const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
@@ -126,7 +121,7 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
     asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 32), "r"(cl), "r"(ch), "r"(rl), "r"(rh));
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 48), "f"(Cv.y), "f"(Cv.z), "f"(Cv.w),
                  "f"(0.f));
-    if (qmax < 0.f) return 0u;
+    if (!(qmax >= 0.f)) return false;
     int r0 = rl, r1 = rh, c0 = cl, c1 = ch;
     const float det = a * c - b * b;
     const float ex = sqrtf(qmax * c / det), ey = sqrtf(qmax * a / det);
@@ -138,14 +133,7 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
         c0 = max(c0, (int)floorf(A.x - hx - 0.5f));
         c1 = min(c1, (int)ceilf(A.x + hx - 0.5f));
     }
-    uint32_t mask = 0u;
-    const int bx = tx * kTile, by = ty * kTile;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        const int x0 = bx + (w & 1) * 8, y0 = by + (w >> 1) * 4;
-        if (c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 3 && r1 >= y0) mask |= 1u << w;
-    }
-    return mask;
+    return c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 7 && r1 >= y0;
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
@@ -153,126 +141,138 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
 template <bool kLoss, bool kImage, int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    __shared__ uint32_t s_mask[kRT];
     __shared__ float red[2][kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x, b = blockIdx.y;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    int px, py;
-    pixel_of(tid, tx, ty, px, py);
-    const bool inside = px < a.W && py < a.H;
+    int px, py0;
+    pixels_of(tid, tx, ty, px, py0);
+    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 8;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
-    const float fpx = (float)px, fpy = (float)py;
-    const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_stage);
-
-    float tgt[3] = {0.f, 0.f, 0.f}, rgba_a = 0.f, rgb[3] = {0.f, 0.f, 0.f};
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
-    if ((kLoss || CI >= 2) && inside && a.targets) {
-        const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
-        rgba_a = (float)t.w / 255.0f;
-        rgb[0] = (float)t.x / 255.0f;
-        rgb[1] = (float)t.y / 255.0f;
-        rgb[2] = (float)t.z / 255.0f;
+    const float fpx = (float)px;
+
+    int py[2];
+    bool inside[2], done[2];
+    int64_t pix[2];
+    float fpy[2], T[2], C[2][3], tgt[2][3], rgb[2][3], rgba_a[2], src[2][3];
+    uint32_t stop[2];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) tgt[c] = rgb[c] * rgba_a + (1.0f - rgba_a) * bg[c];
-    }
-    float ws_src[3] = {tgt[0], tgt[1], tgt[2]};
-    if (CI >= 2 && a.wsum_image && inside) {
+    for (int p = 0; p < 2; ++p) {
+        py[p] = py0 + 4 * p;
+        inside[p] = px < a.W && py[p] < a.H;
+        pix[p] = ((int64_t)b * a.H + (inside[p] ? py[p] : 0)) * a.W + (inside[p] ? px : 0);
+        fpy[p] = (float)py[p];
+        T[p] = 1.0f;
+        done[p] = !inside[p];
+        stop[p] = end - start;
+        rgba_a[p] = 0.f;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) ws_src[c] = a.wsum_image[pix * 3 + c];
+        for (int c = 0; c < 3; ++c) { C[p][c] = 0.f; tgt[p][c] = 0.f; rgb[p][c] = 0.f; }
+        if ((kLoss || CI >= 2) && inside[p] && a.targets) {
+            const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix[p]];
+            rgba_a[p] = (float)t.w / 255.0f;
+            rgb[p][0] = (float)t.x / 255.0f;
+            rgb[p][1] = (float)t.y / 255.0f;
+            rgb[p][2] = (float)t.z / 255.0f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) tgt[p][c] = rgb[p][c] * rgba_a[p] + (1.0f - rgba_a[p]) * bg[c];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) src[p][c] = tgt[p][c];
+        if (CI >= 2 && a.wsum_image && inside[p]) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) src[p][c] = a.wsum_image[pix[p] * 3 + c];
+        }
     }
 
-    float T = 1.0f, C[3] = {0.f, 0.f, 0.f};
-    uint32_t stop = end - start;
-    bool done = !inside;
-    for (uint32_t c0 = start; c0 < end; c0 += kRT) {
-        if (__syncthreads_count(!done) == 0) break;
-        const uint32_t idx = c0 + tid;
-        uint32_t m = 0u;
+    for (uint32_t c0 = start; c0 < end; c0 += 32) {
+        if (__all_sync(kFull, done[0] && done[1])) break;
+        const uint32_t idx = c0 + lane;
+        bool hit = false;
         if (idx < end) {
             const uint32_t n = a.vals[idx];
             uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
             if (CI == 3 && a.visited[n]) gflag |= 0x80000000u;   // visited: skip colour-init work
-            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, tx, ty, sbase + tid * kStageBytes);
+            hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, x0, y0, wbase + lane * kStageBytes);
         }
-        s_mask[tid] = m;
-        __syncthreads();
-        const int cnt = (int)min((uint32_t)kRT, end - c0);
-        if (!__all_sync(kFull, done)) {
-            for (int i = 0; i < (cnt + 31) / 32; ++i) {
-                uint32_t bits = __ballot_sync(kFull, (s_mask[i * 32 + lane] >> warp) & 1u);
-                while (bits) {
-                    const int j = i * 32 + __ffs(bits) - 1;
-                    bits &= bits - 1u;
-                    const uint32_t ad = sbase + j * kStageBytes;
-                    float w = 0.f;
-                    if (!done) {
-                        const int4 bb = lds4i(ad + 32);
-                        if (px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w) {
-                            const float4 p0 = lds4(ad), p1 = lds4(ad + 16);
-                            const float dx = fpx - p0.x, dy = fpy - p0.y;
-                            const float e2 = splat_e2(dx, dy, p0.z, p0.w, p1.x);
-                            if (e2 >= p1.y) {
-                                const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
-                                if (alpha >= kAlphaCutoff) {
-                                    const float4 col = lds4(ad + 48);
-                                    w = alpha * T;
-                                    C[0] += w * col.x;
-                                    C[1] += w * col.y;
-                                    C[2] += w * col.z;
-                                    T = T * (1.0f - alpha);
-                                    if (T < kTermEps) {
-                                        done = true;
-                                        stop = c0 - start + (uint32_t)j + 1u;
-                                    }
-                                }
+        uint32_t bits = __ballot_sync(kFull, hit);
+        __syncwarp();
+        while (bits) {
+            const int j = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            const uint32_t ad = wbase + j * kStageBytes;
+            const int4 bb = lds4i(ad + 32);
+            const float4 p0 = lds4(ad), p1 = lds4(ad + 16), col = lds4(ad + 48);
+            const bool inx = px >= bb.x && px <= bb.y;
+            const float dx = fpx - p0.x;
+            const float kadx = __fmul_rn(p0.z, dx);
+            float w[2] = {0.f, 0.f};
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (!done[p] && inx && py[p] >= bb.z && py[p] <= bb.w) {
+                    const float e2 = splat_e2(dx, fpy[p] - p0.y, kadx, p0.w, p1.x);
+                    if (e2 >= p1.y) {
+                        const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
+                        if (alpha >= kAlphaCutoff) {
+                            w[p] = alpha * T[p];
+                            C[p][0] += w[p] * col.x;
+                            C[p][1] += w[p] * col.y;
+                            C[p][2] += w[p] * col.z;
+                            T[p] = T[p] * (1.0f - alpha);
+                            if (T[p] < kTermEps) {
+                                done[p] = true;
+                                stop[p] = c0 - start + (uint32_t)j + 1u;
                             }
-                        }
-                    }
-                    if (CI > 0) {
-                        const uint32_t gf = lds1(ad + 28);
-                        const bool want = CI != 3 || !(gf & 0x80000000u);
-                        if (want && __any_sync(kFull, w > 0.f)) {
-                            const int64_t g = gf & 0x7FFFFFFFu;
-                            const float wm = warp_max(w);
-                            if (CI >= 2) {
-                                const float v[4] = {w * ws_src[0], w * ws_src[1], w * ws_src[2], w};
-                                int vi;
-                                bool issue;
-                                const float s = reduce_scatter(v, lane, vi, issue);
-                                if (issue) atomicAdd(a.wsums + g * 4 + vi, s);
-                            }
-                            if (lane == 0) atomicMax(reinterpret_cast<int *>(a.maxw) + g, __float_as_int(wm));
                         }
                     }
                 }
             }
+            if (CI > 0) {
+                const uint32_t gf = __float_as_uint(p1.w);
+                const bool want = CI != 3 || !(gf & 0x80000000u);
+                if (want && __any_sync(kFull, w[0] > 0.f || w[1] > 0.f)) {
+                    const int64_t g = gf & 0x7FFFFFFFu;
+                    const float wm = warp_max(fmaxf(w[0], w[1]));
+                    if (CI >= 2) {
+                        const float v[4] = {w[0] * src[0][0] + w[1] * src[1][0], w[0] * src[0][1] + w[1] * src[1][1],
+                                            w[0] * src[0][2] + w[1] * src[1][2], w[0] + w[1]};
+                        int vi;
+                        bool issue;
+                        const float s = reduce_scatter(v, lane, vi, issue);
+                        if (issue) atomicAdd(a.wsums + g * 4 + vi, s);
+                    }
+                    if (lane == 0) atomicMax(reinterpret_cast<int *>(a.maxw) + g, __float_as_int(wm));
+                }
+            }
         }
-        __syncthreads();
+        __syncwarp();
     }
 
     float l1 = 0.f, black = 0.f;
-    if (inside) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        if (!inside[p]) continue;
         float pred[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) pred[c] = C[c] + T * bg[c];
+        for (int c = 0; c < 3; ++c) pred[c] = C[p][c] + T[p] * bg[c];
         uint32_t signs = 0;
         if (kLoss) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float d = pred[c] - tgt[c];
+                const float d = pred[c] - tgt[p][c];
                 l1 += fabsf(d);
-                black += fabsf(C[c] - rgb[c] * rgba_a);
+                black += fabsf(C[p][c] - rgb[p][c] * rgba_a[p]);
                 signs |= (d > 0.f ? 1u : d < 0.f ? 2u : 0u) << (2 * c);
             }
         }
-        a.pix_T[pix] = T;
-        a.pix_state[pix] = stop | (signs << 26);
+        a.pix_T[pix[p]] = T[p];
+        a.pix_state[pix[p]] = stop[p] | (signs << 26);
         if (kImage) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) a.image[pix * 3 + c] = pred[c];
+            for (int c = 0; c < 3; ++c) a.image[pix[p] * 3 + c] = pred[c];
         }
     }
     if (kLoss) {
@@ -296,122 +296,120 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
 template <bool kExplicitGrad>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    __shared__ uint32_t s_mask[kRT];
-    __shared__ uint32_t s_max[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x, b = blockIdx.y;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    int px, py;
-    pixel_of(tid, tx, ty, px, py);
-    const bool inside = px < a.W && py < a.H;
+    int px, py0;
+    pixels_of(tid, tx, ty, px, py0);
+    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 8;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     if (start >= end) return;
-    const float fpx = (float)px, fpy = (float)py;
-    const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_stage);
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
+    const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
+    const float fpx = (float)px;
 
-    float g[3] = {0.f, 0.f, 0.f};
-    uint32_t stop = 0;
-    float t_rev = 0.f, suffix = 0.f;
-    if (inside) {
-        const uint32_t st = a.pix_state[pix];
-        stop = st & kStopMask;
-        const float Tf = a.pix_T[pix];
-        if (kExplicitGrad) {
+    int py[2];
+    float fpy[2], g[2][3], t_rev[2], suffix[2];
+    uint32_t stop[2];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) g[c] = a.grad_image[pix * 3 + c];
-        } else {
-            const uint32_t sg = st >> 26;
+    for (int p = 0; p < 2; ++p) {
+        py[p] = py0 + 4 * p;
+        fpy[p] = (float)py[p];
+        const bool inside = px < a.W && py[p] < a.H;
+        const int64_t pix = ((int64_t)b * a.H + (inside ? py[p] : 0)) * a.W + (inside ? px : 0);
+        g[p][0] = g[p][1] = g[p][2] = 0.f;
+        stop[p] = 0;
+        t_rev[p] = 0.f;
+        suffix[p] = 0.f;
+        if (inside) {
+            const uint32_t st = a.pix_state[pix];
+            stop[p] = st & kStopMask;
+            const float Tf = a.pix_T[pix];
+            if (kExplicitGrad) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const uint32_t s2 = (sg >> (2 * c)) & 3u;
-                g[c] = s2 == 1u ? a.grad_scale : s2 == 2u ? -a.grad_scale : 0.f;
+                for (int c = 0; c < 3; ++c) g[p][c] = a.grad_image[pix * 3 + c];
+            } else {
+                const uint32_t sg = st >> 26;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const uint32_t s2 = (sg >> (2 * c)) & 3u;
+                    g[p][c] = s2 == 1u ? a.grad_scale : s2 == 2u ? -a.grad_scale : 0.f;
+                }
             }
+            t_rev[p] = Tf;
+            suffix[p] = Tf * (g[p][0] * bg[0] + g[p][1] * bg[1] + g[p][2] * bg[2]);
         }
-        t_rev = Tf;
-        suffix = Tf * (g[0] * a.bgs[3 * b] + g[1] * a.bgs[3 * b + 1] + g[2] * a.bgs[3 * b + 2]);
     }
-    // last local index any pixel of the tile needs
-    const uint32_t wmax = __reduce_max_sync(kFull, stop);
-    if (lane == 0) s_max[warp] = wmax;
-    __syncthreads();
-    uint32_t maxstop = 0;
-#pragma unroll
-    for (int i = 0; i < kWarps; ++i) maxstop = max(maxstop, s_max[i]);
-    const uint32_t last = start + maxstop;
-
+    // this warp only needs the list up to its pixels' largest stop index
+    const uint32_t last = start + __reduce_max_sync(kFull, max(stop[0], stop[1]));
     for (uint32_t c_end = last; c_end > start;) {
-        const uint32_t c0 = c_end - start > (uint32_t)kRT ? c_end - kRT : start;
-        const uint32_t idx = c0 + tid;
-        __syncthreads();
-        uint32_t m = 0u;
+        const uint32_t c0 = c_end - start > 32u ? c_end - 32u : start;
+        const uint32_t idx = c0 + lane;
+        bool hit = false;
         if (idx < c_end) {
             const uint32_t n = a.vals[idx];
-            m = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), tx, ty,
-                            sbase + tid * kStageBytes);
+            hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0, y0,
+                              wbase + lane * kStageBytes);
         }
-        s_mask[tid] = m;
-        __syncthreads();
-        const int cnt = (int)(c_end - c0);
-        for (int i = (cnt - 1) / 32; i >= 0; --i) {
-            uint32_t bits = __ballot_sync(kFull, (s_mask[i * 32 + lane] >> warp) & 1u);
-            while (bits) {
-                const int hb = 31 - __clz(bits);
-                bits &= ~(1u << hb);
-                const int j = i * 32 + hb;
-                const uint32_t jl = c0 - start + (uint32_t)j;
-                const uint32_t ad = sbase + j * kStageBytes;
-                float gv[9];
-                bool contrib = false;
-                if (jl < stop) {
-                    const int4 bb = lds4i(ad + 32);
-                    if (px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w) {
-                        const float4 p0 = lds4(ad), p1 = lds4(ad + 16);
-                        const float dx = fpx - p0.x, dy = fpy - p0.y;
-                        const float e2 = splat_e2(dx, dy, p0.z, p0.w, p1.x);
-                        if (e2 >= p1.y) {
-                            const float G = ex2_approx(e2);
-                            const float alpha = __fmul_rn(p1.z, G);
-                            if (alpha >= kAlphaCutoff) {
-                                contrib = true;
-                                const float4 col = lds4(ad + 48);
-                                const float inv = __fdividef(1.0f, 1.0f - alpha);
-                                const float t_prior = t_rev * inv;
-                                const float gw = g[0] * col.x + g[1] * col.y + g[2] * col.z;
-                                const float wgt = alpha * t_prior;
-                                gv[6] = wgt * g[0];
-                                gv[7] = wgt * g[1];
-                                gv[8] = wgt * g[2];
-                                const float d_alpha = t_prior * gw - suffix * inv;
-                                gv[5] = G * d_alpha;
-                                const float dq = -0.5f * alpha * d_alpha;
-                                const float dqx = dq * dx, dqy = dq * dy;
-                                gv[2] = dqx * dx;
-                                gv[3] = 2.0f * dqx * dy;
-                                gv[4] = dqy * dy;
-                                // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
-                                const float hb2 = 0.5f * p0.w;
-                                gv[0] = kMeanScale * (p0.z * dqx + hb2 * dqy);
-                                gv[1] = kMeanScale * (hb2 * dqx + p1.x * dqy);
-                                suffix += wgt * gw;
-                                t_rev = t_prior;
-                            }
+        uint32_t bits = __ballot_sync(kFull, hit);
+        __syncwarp();
+        while (bits) {
+            const int j = 31 - __clz(bits);
+            bits &= ~(1u << j);
+            const uint32_t jl = c0 - start + (uint32_t)j;
+            const uint32_t ad = wbase + j * kStageBytes;
+            const int4 bb = lds4i(ad + 32);
+            const float4 p0 = lds4(ad), p1 = lds4(ad + 16), col = lds4(ad + 48);
+            const bool inx = px >= bb.x && px <= bb.y;
+            const float dx = fpx - p0.x;
+            const float kadx = __fmul_rn(p0.z, dx);
+            const float hb2 = 0.5f * p0.w;
+            float gv[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) gv[k] = 0.f;
+            bool contrib = false;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (jl < stop[p] && inx && py[p] >= bb.z && py[p] <= bb.w) {
+                    const float dy = fpy[p] - p0.y;
+                    const float e2 = splat_e2(dx, dy, kadx, p0.w, p1.x);
+                    if (e2 >= p1.y) {
+                        const float G = ex2_approx(e2);
+                        const float alpha = __fmul_rn(p1.z, G);
+                        if (alpha >= kAlphaCutoff) {
+                            contrib = true;
+                            const float inv = __fdividef(1.0f, 1.0f - alpha);
+                            const float t_prior = t_rev[p] * inv;
+                            const float gw = g[p][0] * col.x + g[p][1] * col.y + g[p][2] * col.z;
+                            const float wgt = alpha * t_prior;
+                            gv[6] += wgt * g[p][0];
+                            gv[7] += wgt * g[p][1];
+                            gv[8] += wgt * g[p][2];
+                            const float d_alpha = t_prior * gw - suffix[p] * inv;
+                            gv[5] += G * d_alpha;
+                            const float dq = -0.5f * alpha * d_alpha;
+                            const float dqx = dq * dx, dqy = dq * dy;
+                            gv[2] += dqx * dx;
+                            gv[3] += 2.0f * dqx * dy;
+                            gv[4] += dqy * dy;
+                            // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
+                            gv[0] += kMeanScale * (p0.z * dqx + hb2 * dqy);
+                            gv[1] += kMeanScale * (hb2 * dqx + p1.x * dqy);
+                            suffix[p] += wgt * gw;
+                            t_rev[p] = t_prior;
                         }
                     }
                 }
-                if (__any_sync(kFull, contrib)) {
-                    if (!contrib) {
-#pragma unroll
-                        for (int k = 0; k < 9; ++k) gv[k] = 0.f;
-                    }
-                    int vi;
-                    bool issue;
-                    const float s = reduce_scatter(gv, lane, vi, issue);
-                    if (issue) atomicAdd(a.g_splat + (uint64_t)lds1(ad + 28) * kGS + vi, s);
-                }
+            }
+            if (__any_sync(kFull, contrib)) {
+                int vi;
+                bool issue;
+                const float s = reduce_scatter(gv, lane, vi, issue);
+                if (issue) atomicAdd(a.g_splat + (uint64_t)(__float_as_uint(p1.w)) * kGS + vi, s);
             }
         }
+        __syncwarp();
         c_end = c0;
     }
 }
