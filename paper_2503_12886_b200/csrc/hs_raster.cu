@@ -27,11 +27,15 @@
 
 namespace hs {
 
+#ifndef HS_RASTER_PX
+#define HS_RASTER_PX 2               // pixels per lane (a warp owns an 8 x 4*PX block)
+#endif
 #ifndef HS_RASTER_MINB
-#define HS_RASTER_MINB 8             // resident CTAs per SM the register budget must allow
+#define HS_RASTER_MINB (16 / HS_RASTER_PX)   // resident CTAs per SM the register budget must allow
 #endif
 
-constexpr int kRT = 128;             // threads per CTA: 4 warps x (8x8 pixels, 2 per lane)
+constexpr int kPX = HS_RASTER_PX;
+constexpr int kRT = kTile * kTile / kPX;   // threads per CTA
 constexpr int kWarps = kRT / 32;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -98,15 +102,16 @@ __device__ __forceinline__ float splat_e2(float dx, float dy, float kadx, float 
 }
 
 // Pixels of thread `tid`: warp w covers cols (w & 1) * 8 .. +7 and rows
-// (w >> 1) * 8 .. +7 of the tile; lane l holds column l & 7 and rows (l >> 3), +4.
+// (w >> 1) * 4 kPX .. +4 kPX - 1 of the tile; lane l holds column l & 7 and rows
+// (l >> 3) + 4 p for p < kPX.
 __device__ __forceinline__ void pixels_of(int tid, int tx, int ty, int &px, int &py0) {
     const int w = tid >> 5, l = tid & 31;
     px = tx * kTile + (w & 1) * 8 + (l & 7);
-    py0 = ty * kTile + (w >> 1) * 8 + (l >> 3);
+    py0 = ty * kTile + (w >> 1) * 4 * kPX + (l >> 3);
 }
 
-// Stage one splat record into the lane's slot and vote whether the warp's 8x8 block
-// [x0, x0+7] x [y0, y0+7] can hold a contributing pixel.
+// Stage one splat record into the lane's slot and vote whether the warp's block
+// [x0, x0+7] x [y0, y0+4 kPX-1] can hold a contributing pixel.
 __device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
                                             uint32_t saddr) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
@@ -133,7 +138,7 @@ __device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint3
         c0 = max(c0, (int)floorf(A.x - hx - 0.5f));
         c1 = min(c1, (int)ceilf(A.x + hx - 0.5f));
     }
-    return c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 7 && r1 >= y0;
+    return c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 4 * kPX - 1 && r1 >= y0;
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
@@ -147,20 +152,20 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int px, py0;
     pixels_of(tid, tx, ty, px, py0);
-    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 8;
+    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 4 * kPX;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
     const float fpx = (float)px;
 
-    int py[2];
-    bool inside[2], done[2];
-    int64_t pix[2];
-    float fpy[2], T[2], C[2][3], tgt[2][3], rgb[2][3], rgba_a[2], src[2][3];
-    uint32_t stop[2];
+    int py[kPX];
+    bool inside[kPX], done[kPX];
+    int64_t pix[kPX];
+    float fpy[kPX], T[kPX], C[kPX][3], tgt[kPX][3], rgb[kPX][3], rgba_a[kPX], src[kPX][3];
+    uint32_t stop[kPX];
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < kPX; ++p) {
         py[p] = py0 + 4 * p;
         inside[p] = px < a.W && py[p] < a.H;
         pix[p] = ((int64_t)b * a.H + (inside[p] ? py[p] : 0)) * a.W + (inside[p] ? px : 0);
@@ -189,7 +194,10 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
     }
 
     for (uint32_t c0 = start; c0 < end; c0 += 32) {
-        if (__all_sync(kFull, done[0] && done[1])) break;
+        bool all_done = true;
+#pragma unroll
+        for (int p = 0; p < kPX; ++p) all_done = all_done && done[p];
+        if (__all_sync(kFull, all_done)) break;
         const uint32_t idx = c0 + lane;
         bool hit = false;
         if (idx < end) {
@@ -209,9 +217,11 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
             const bool inx = px >= bb.x && px <= bb.y;
             const float dx = fpx - p0.x;
             const float kadx = __fmul_rn(p0.z, dx);
-            float w[2] = {0.f, 0.f};
+            float w[kPX];
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
+            for (int p = 0; p < kPX; ++p) w[p] = 0.f;
+#pragma unroll
+            for (int p = 0; p < kPX; ++p) {
                 if (!done[p] && inx && py[p] >= bb.z && py[p] <= bb.w) {
                     const float e2 = splat_e2(dx, fpy[p] - p0.y, kadx, p0.w, p1.x);
                     if (e2 >= p1.y) {
@@ -233,12 +243,21 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
             if (CI > 0) {
                 const uint32_t gf = __float_as_uint(p1.w);
                 const bool want = CI != 3 || !(gf & 0x80000000u);
-                if (want && __any_sync(kFull, w[0] > 0.f || w[1] > 0.f)) {
+                float wmax = 0.f;
+#pragma unroll
+                for (int p = 0; p < kPX; ++p) wmax = fmaxf(wmax, w[p]);
+                if (want && __any_sync(kFull, wmax > 0.f)) {
                     const int64_t g = gf & 0x7FFFFFFFu;
-                    const float wm = warp_max(fmaxf(w[0], w[1]));
+                    const float wm = warp_max(wmax);
                     if (CI >= 2) {
-                        const float v[4] = {w[0] * src[0][0] + w[1] * src[1][0], w[0] * src[0][1] + w[1] * src[1][1],
-                                            w[0] * src[0][2] + w[1] * src[1][2], w[0] + w[1]};
+                        float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int p = 0; p < kPX; ++p) {
+                            v[0] += w[p] * src[p][0];
+                            v[1] += w[p] * src[p][1];
+                            v[2] += w[p] * src[p][2];
+                            v[3] += w[p];
+                        }
                         int vi;
                         bool issue;
                         const float s = reduce_scatter(v, lane, vi, issue);
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
 
     float l1 = 0.f, black = 0.f;
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < kPX; ++p) {
         if (!inside[p]) continue;
         float pred[3];
 #pragma unroll
@@ -301,7 +320,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int px, py0;
     pixels_of(tid, tx, ty, px, py0);
-    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 8;
+    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 4 * kPX;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     if (start >= end) return;
@@ -309,11 +328,11 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
     const float fpx = (float)px;
 
-    int py[2];
-    float fpy[2], g[2][3], t_rev[2], suffix[2];
-    uint32_t stop[2];
+    int py[kPX];
+    float fpy[kPX], g[kPX][3], t_rev[kPX], suffix[kPX];
+    uint32_t stop[kPX];
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < kPX; ++p) {
         py[p] = py0 + 4 * p;
         fpy[p] = (float)py[p];
         const bool inside = px < a.W && py[p] < a.H;
@@ -342,7 +361,10 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
         }
     }
     // this warp only needs the list up to its pixels' largest stop index
-    const uint32_t last = start + __reduce_max_sync(kFull, max(stop[0], stop[1]));
+    uint32_t smax = 0;
+#pragma unroll
+    for (int p = 0; p < kPX; ++p) smax = max(smax, stop[p]);
+    const uint32_t last = start + __reduce_max_sync(kFull, smax);
     for (uint32_t c_end = last; c_end > start;) {
         const uint32_t c0 = c_end - start > 32u ? c_end - 32u : start;
         const uint32_t idx = c0 + lane;
@@ -370,7 +392,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
             for (int k = 0; k < 9; ++k) gv[k] = 0.f;
             bool contrib = false;
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
+            for (int p = 0; p < kPX; ++p) {
                 if (jl < stop[p] && inx && py[p] >= bb.z && py[p] <= bb.w) {
                     const float dy = fpy[p] - p0.y;
                     const float e2 = splat_e2(dx, dy, kadx, p0.w, p1.x);
