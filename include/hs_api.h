@@ -110,15 +110,16 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height,
                           const float *raw10, const float *base14, const int32_t *tri_index,
                           const float *bary, const float *frames, const float *cameras,
                           float *records, float *depth, uint32_t *counts,
-                          uint32_t *block_sums, float *radius, unsigned long long *err,
-                          void *stream);
+                          uint32_t *block_sums, uint32_t *depth_range, float *radius,
+                          unsigned long long *err, void *stream);
 /* Projection of already-activated world Gaussians (compat preprocess).
  * radius (B*N, 0 for culled splats), x_cam (B*N*3) and cov_cam (B*N*9) are
  * optional outputs (NULL to skip) in both projection calls. */
 int hs_project_world_fwd(int B, int64_t N, int width, int height, const float *world14,
                          const float *cameras, float *records, float *depth,
-                         uint32_t *counts, uint32_t *block_sums, float *radius, float *x_cam,
-                         float *cov_cam, unsigned long long *err, void *stream);
+                         uint32_t *counts, uint32_t *block_sums, uint32_t *depth_range,
+                         float *radius, float *x_cam, float *cov_cam, unsigned long long *err,
+                         void *stream);
 /* Adjoint of hs_project_avatar_fwd (render.py:432-497 _preprocess_backward,
  * binding.py:191-204 transform_backward, model.py:237-248 activate_backward):
  * g_splat[B,N,9] -> g_raw14[B,14N] (written). */
@@ -133,20 +134,25 @@ int hs_project_world_bwd(int B, int64_t N, const float *world14, const float *ca
 /* ---- Binning (new; replaces render.py:221-223 + :380-386) */
 int hs_scan_blocks(int64_t num_items);  /* = ceil(num_items / 256) */
 /* Exclusive scan of block_sums -> block_offsets; summary[0] = total keys,
- * summary[1] = *err.  The caller copies summary to pinned host memory: the one
- * device->host read of a training step. */
+ * summary[1] = *err, summary[2] = depth_range[0] | depth_range[1] << 32 (float bits of
+ * the smallest / largest depth that emits keys; depth_range = {0xFFFFFFFF, 0} before
+ * the projection, optional).  The caller copies summary to pinned host memory: the
+ * one device->host read of a training step. */
 int hs_bin_scan(int num_blocks, const uint32_t *block_sums, uint32_t *block_offsets,
-                const unsigned long long *err, unsigned long long *summary, void *stream);
+                const unsigned long long *err, const uint32_t *depth_range,
+                unsigned long long *summary, void *stream);
 /* Writes keys/values in (frame, n, ty, tx) order. */
 int hs_bin_emit(int B, int64_t N, int width, int height, const float *records,
                 const float *depth, const uint32_t *counts, const uint32_t *block_offsets,
                 uint64_t *keys, uint32_t *values, void *stream);
 /* Bytes of scratch for hs_sort_pairs. */
 size_t hs_sort_workspace_size(int64_t num_keys);
-/* Stable LSD radix sort of (keys, values) over bits [0, key_bits).  Ping-pongs
- * between the (keys, values) and (keys_alt, values_alt) buffers; *result_in_alt
- * tells which pair holds the sorted output. */
-int hs_sort_pairs(int64_t num_keys, int key_bits, uint64_t *keys, uint32_t *values,
+/* Stable LSD radix sort (onesweep: one histogram kernel, then one decoupled
+ * look-back kernel per 8-bit pass) of (keys, values) by the key bits in bit_mask;
+ * digit windows outside the mask must be constant over the keys.  Ping-pongs
+ * between (keys, values) and (keys_alt, values_alt); *result_in_alt tells which
+ * pair holds the sorted output. */
+int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t *values,
                   uint64_t *keys_alt, uint32_t *values_alt, void *workspace,
                   size_t workspace_bytes, int *result_in_alt, void *stream);
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */

@@ -42,15 +42,15 @@ SIGNATURES = {
     "hs_blend_fwd": (_I, [_L, _I, _I, _P, _P, _P, _P, _P]),
     "hs_blend_bwd": (_I, [_L, _I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I), _P]),
     "hs_blend_bwd_partials": (_I, [_L]),
-    "hs_project_avatar_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "hs_project_world_fwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_project_avatar_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_project_world_fwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_project_avatar_bwd": (_I, [_I, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_project_world_bwd": (_I, [_I, _L, _P, _P, _P, _P, _P]),
     "hs_scan_blocks": (_I, [_L]),
-    "hs_bin_scan": (_I, [_I, _P, _P, _P, _P, _P]),
+    "hs_bin_scan": (_I, [_I, _P, _P, _P, _P, _P, _P]),
     "hs_bin_emit": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "hs_sort_workspace_size": (_Z, [_L]),
-    "hs_sort_pairs": (_I, [_L, _I, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
+    "hs_sort_pairs": (_I, [_L, ctypes.c_uint64, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges": (_I, [_L, _P, _P, _P]),
     "hs_raster_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_raster_bwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _F, _P, _P]),

@@ -302,10 +302,10 @@ def _project_batch(worlds, cameras):
     nb = int(L.load().hs_scan_blocks(B * n))
     dev["block_sums"] = torch.empty(nb, dtype=torch.int32, device=d)
     err = _err()
-    L.call("hs_project_world_fwd", B, n, W, H, _p(w14), _p(cams), _p(dev["records"]), _p(dev["depth"]),
-           _p(dev["counts"]), _p(dev["block_sums"]), _p(dev["radius"]), _p(dev["x_cam"]), _p(dev["cov_cam"]),
-           _p(err), _stream())
     binner = Binner(d)
+    L.call("hs_project_world_fwd", B, n, W, H, _p(w14), _p(cams), _p(dev["records"]), _p(dev["depth"]),
+           _p(dev["counts"]), _p(dev["block_sums"]), _p(binner.reset_depth_range()), _p(dev["radius"]),
+           _p(dev["x_cam"]), _p(dev["cov_cam"]), _p(err), _stream())
     total, code = binner.scan(dev["block_sums"], nb, err)
     L.raise_device_error(code)
     dev["binned"] = binner.bin(B, n, W, H, dev["records"], dev["depth"], dev["counts"], total)

@@ -7,6 +7,8 @@
 // step in one pass; oracle/binning.py is the bit-exact CPU restatement
 // (SURVEY Appendix B).  Stable sorting of keys emitted in Gaussian order makes
 // equal depth bits resolve to the lower index, the reference's tie-break.
+#include <algorithm>
+
 #include "hs_common.cuh"
 
 namespace hs {
@@ -18,6 +20,7 @@ namespace hs {
 __global__ void __launch_bounds__(1024) scan_kernel(int nb, const uint32_t *__restrict__ sums,
                                                     uint32_t *__restrict__ offs,
                                                     const unsigned long long *__restrict__ err,
+                                                    const uint32_t *__restrict__ depth_range,
                                                     unsigned long long *__restrict__ summary) {
     __shared__ unsigned long long warp_tot[32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -49,6 +52,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(int nb, const uint32_t *__re
     if (tid == 0) {
         summary[0] = warp_tot[(blockDim.x >> 5) - 1];
         summary[1] = err ? *err : HS_NO_ERROR;
+        summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
     }
 }
 
@@ -95,39 +99,50 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
 }
 
 // --------------------------------------------------------------- radix sort
+//
+// Stable LSD radix sort, onesweep style: one kernel computes the digit histograms
+// of every pass in a single read of the keys; each pass is then ONE kernel whose
+// CTAs take tile ids in launch order, rank their 2048 keys per digit (warp
+// match.any), publish per-digit counts and resolve their global digit offsets by
+// decoupled look-back over the predecessor tiles, and scatter through shared
+// memory so every digit run is written contiguously.  Only the 8-bit digit
+// windows that intersect `bit_mask` are sorted (digits that are constant across all
+// keys cannot change the order).
 
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per CTA
 constexpr int kRadix = 256;
+constexpr int kMaxPasses = 8;
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1u;
 
-// per-CTA digit histogram, stored digit-major: hist[d * tiles + tile]
-__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(int64_t n, int shift,
-                                                                  const uint64_t *__restrict__ keys,
-                                                                  uint32_t *__restrict__ hist, int tiles) {
-    __shared__ uint32_t h[kRadix];
-    h[threadIdx.x] = 0;
+struct PassShifts {
+    int shift[kMaxPasses];
+    int n;
+};
+
+__global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const uint64_t *__restrict__ keys,
+                                                             PassShifts ps, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[kMaxPasses][kRadix];
+    for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kSortTile;
-#pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const int64_t idx = base + i * kSortThreads + threadIdx.x;
-        if (idx < n) atomicAdd(&h[(uint32_t)(keys[idx] >> shift) & (kRadix - 1)], 1u);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        for (int p = 0; p < ps.n; ++p) atomicAdd(&h[p][(uint32_t)(k >> ps.shift[p]) & (kRadix - 1)], 1u);
     }
     __syncthreads();
-    hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];
+    for (int i = threadIdx.x; i < ps.n * kRadix; i += blockDim.x) {
+        const uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(hist + i, v);
+    }
 }
 
-// one CTA per digit: exclusive scan of that digit's row over the CTAs; totals[d]
-__global__ void __launch_bounds__(256) radix_rowscan_kernel(uint32_t *__restrict__ hist, int tiles,
-                                                            uint32_t *__restrict__ totals) {
-    __shared__ uint32_t warp_tot[8];
-    uint32_t *row = hist + (int64_t)blockIdx.x * tiles;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    uint32_t carry = 0;
-    for (int c0 = 0; c0 < tiles; c0 += 256) {
-        const int idx = c0 + tid;
-        const uint32_t v = idx < tiles ? row[idx] : 0u;
+// exclusive scan of each pass's 256 digit counts (one CTA, one thread per digit)
+__global__ void __launch_bounds__(kRadix) radix_digit_scan_kernel(int npass, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t warp_tot[kRadix / 32];
+    const int d = threadIdx.x, lane = d & 31, w = d >> 5;
+    for (int p = 0; p < npass; ++p) {
+        const uint32_t v = hist[p * kRadix + d];
         uint32_t incl = v;
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -135,54 +150,43 @@ __global__ void __launch_bounds__(256) radix_rowscan_kernel(uint32_t *__restrict
         }
         if (lane == 31) warp_tot[w] = incl;
         __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-        for (int k = 0; k < 8; ++k) {
-            if (k < w) wpre += warp_tot[k];
-            tot += warp_tot[k];
-        }
-        if (idx < tiles) row[idx] = carry + wpre + incl - v;
-        carry += tot;
+        uint32_t pre = 0;
+        for (int k = 0; k < w; ++k) pre += warp_tot[k];
+        hist[p * kRadix + d] = pre + incl - v;
         __syncthreads();
     }
-    if (tid == 0) totals[blockIdx.x] = carry;
 }
 
-// Stable scatter.  Keys are read warp-striped (warp w owns 256 consecutive keys,
-// item i of lane l is key w*256 + i*32 + l), ranked per warp with match.any,
-// staged digit-sorted in shared memory and written out as contiguous runs.
-__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(int64_t n, int shift,
-                                                                     const uint64_t *__restrict__ keys_in,
-                                                                     const uint32_t *__restrict__ vals_in,
-                                                                     uint64_t *__restrict__ keys_out,
-                                                                     uint32_t *__restrict__ vals_out,
-                                                                     const uint32_t *__restrict__ hist,
-                                                                     const uint32_t *__restrict__ totals,
-                                                                     int tiles) {
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(int64_t n, int shift,
+                                                                      const uint64_t *__restrict__ keys_in,
+                                                                      const uint32_t *__restrict__ vals_in,
+                                                                      uint64_t *__restrict__ keys_out,
+                                                                      uint32_t *__restrict__ vals_out,
+                                                                      const uint32_t *__restrict__ digit_base,
+                                                                      uint32_t *__restrict__ status,
+                                                                      uint32_t *__restrict__ counter) {
     __shared__ uint64_t s_keys[kSortTile];
     __shared__ uint32_t s_vals[kSortTile];
     __shared__ uint32_t warp_hist[kSortThreads / 32][kRadix];
     __shared__ uint32_t digit_off[kRadix];
     __shared__ uint32_t glob[kRadix];
     __shared__ uint32_t warp_tot[8];
+    __shared__ uint32_t s_tile;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int64_t base = (int64_t)blockIdx.x * kSortTile;
-
-    // global base of each digit: exclusive prefix of totals + this CTA's row offset
-    {
-        const uint32_t v = totals[tid];
-        uint32_t incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) warp_tot[w] = incl;
-        for (int k = 0; k < kSortThreads / 32; ++k) warp_hist[k][tid] = 0;
-        __syncthreads();
-        uint32_t wpre = 0;
-        for (int k = 0; k < w; ++k) wpre += warp_tot[k];
-        glob[tid] = wpre + incl - v + hist[(int64_t)tid * tiles + blockIdx.x];
-    }
+    if (tid == 0) s_tile = atomicAdd(counter, 1u);          // tile ids in launch order
+    for (int k = 0; k < kSortThreads / 32; ++k) warp_hist[k][tid] = 0;
     __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t base = (int64_t)tile * kSortTile;
 
     uint64_t k_reg[kSortItems];
     uint32_t v_reg[kSortItems];
@@ -194,6 +198,11 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(int64_t n, 
         const bool valid = idx < n;
         k_reg[i] = valid ? keys_in[idx] : 0ull;
         v_reg[i] = valid ? vals_in[idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int64_t idx = base + w * (32 * kSortItems) + i * 32 + lane;
+        const bool valid = idx < n;
         const uint32_t d = (uint32_t)(k_reg[i] >> shift) & (kRadix - 1);
         const uint32_t mask = __ballot_sync(0xffffffffu, valid);
         local[i] = 0;
@@ -208,7 +217,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(int64_t n, 
         }
     }
     __syncthreads();
-    // per digit: prefix over warps, then block-exclusive scan over digits
+    // per digit (thread tid = digit): prefix over warps, CTA count, block-exclusive scan
+    uint32_t cnt;
     {
         uint32_t run = 0;
 #pragma unroll
@@ -217,17 +227,37 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(int64_t n, 
             warp_hist[k][tid] = run;
             run += t;
         }
+        cnt = run;
         uint32_t incl = run;
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        __syncthreads();
         if (lane == 31) warp_tot[w] = incl;
         __syncthreads();
         uint32_t wpre = 0;
         for (int k = 0; k < w; ++k) wpre += warp_tot[k];
         digit_off[tid] = wpre + incl - run;
+    }
+    // decoupled look-back for digit `tid`
+    {
+        uint32_t *st = status + (size_t)tile * kRadix + tid;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st_relaxed(st, kFlagInc | cnt);
+        } else {
+            st_relaxed(st, kFlagAgg | cnt);
+            for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
+                uint32_t v;
+                do {
+                    v = ld_relaxed(status + (size_t)j * kRadix + tid);
+                } while (v == 0u);
+                excl += v & kCountMask;
+                if (v & kFlagInc) break;
+            }
+            st_relaxed(st, kFlagInc | (excl + cnt));
+        }
+        glob[tid] = digit_base[tid] + excl;
     }
     __syncthreads();
 #pragma unroll
@@ -241,8 +271,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(int64_t n, 
         }
     }
     __syncthreads();
-    const int cnt = (int)min((int64_t)kSortTile, n - base);
-    for (int j = tid; j < cnt; j += kSortThreads) {
+    const int cnt_tile = (int)min((int64_t)kSortTile, n - base);
+    for (int j = tid; j < cnt_tile; j += kSortThreads) {
         const uint64_t key = s_keys[j];
         const uint32_t d = (uint32_t)(key >> shift) & (kRadix - 1);
         const uint32_t p = glob[d] + (uint32_t)j - digit_off[d];
@@ -268,8 +298,9 @@ using namespace hs;
 extern "C" {
 
 int hs_bin_scan(int num_blocks, const uint32_t *block_sums, uint32_t *block_offsets, const unsigned long long *err,
-                unsigned long long *summary, void *stream) {
-    scan_kernel<<<1, 1024, 0, HS_CHECK_STREAM(stream)>>>(num_blocks, block_sums, block_offsets, err, summary);
+                const uint32_t *depth_range, unsigned long long *summary, void *stream) {
+    scan_kernel<<<1, 1024, 0, HS_CHECK_STREAM(stream)>>>(num_blocks, block_sums, block_offsets, err, depth_range,
+                                                         summary);
     return check_launch("hs_bin_scan");
 }
 
@@ -291,10 +322,12 @@ int hs_bin_emit(int B, int64_t N, int width, int height, const float *records, c
 
 size_t hs_sort_workspace_size(int64_t num_keys) {
     const int64_t tiles = (num_keys + kSortTile - 1) / kSortTile;
-    return sizeof(uint32_t) * ((size_t)kRadix * (size_t)(tiles > 0 ? tiles : 1) + kRadix);
+    // digit bases [8][256] + status [8][tiles][256] + tile counters [8]
+    return sizeof(uint32_t) * ((size_t)kMaxPasses * kRadix + (size_t)kMaxPasses * (size_t)(tiles > 0 ? tiles : 1) *
+                               kRadix + kMaxPasses);
 }
 
-int hs_sort_pairs(int64_t num_keys, int key_bits, uint64_t *keys, uint32_t *values, uint64_t *keys_alt,
+int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t *values, uint64_t *keys_alt,
                   uint32_t *values_alt, void *workspace, size_t workspace_bytes, int *result_in_alt,
                   void *stream) {
     if (result_in_alt) *result_in_alt = 0;
@@ -303,21 +336,34 @@ int hs_sort_pairs(int64_t num_keys, int key_bits, uint64_t *keys, uint32_t *valu
         set_error("hs_sort_pairs: workspace too small (%zu < %zu)", workspace_bytes, hs_sort_workspace_size(num_keys));
         return HS_ERR_SHAPE;
     }
-    if (num_keys > 0xFFFFFFFFll) {
+    if (num_keys > (int64_t)kCountMask) {
         set_error("hs_sort_pairs: too many keys");
         return HS_ERR_SHAPE;
     }
+    PassShifts ps{};
+    for (int sh = 0; sh < 64; sh += 8)
+        if ((bit_mask >> sh) & 0xFFull) ps.shift[ps.n++] = sh;
+    if (ps.n == 0) return HS_OK;
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const int tiles = (int)((num_keys + kSortTile - 1) / kSortTile);
     uint32_t *hist = reinterpret_cast<uint32_t *>(workspace);
-    uint32_t *totals = hist + (size_t)kRadix * tiles;
+    uint32_t *status = hist + (size_t)kMaxPasses * kRadix;
+    uint32_t *counters = status + (size_t)kMaxPasses * tiles * kRadix;
+    cudaMemsetAsync(workspace, 0,
+                    sizeof(uint32_t) * ((size_t)kMaxPasses * kRadix + (size_t)ps.n * tiles * kRadix), s);
+    cudaMemsetAsync(counters, 0, sizeof(uint32_t) * kMaxPasses, s);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const unsigned hgrid = (unsigned)std::min<int64_t>(grid_for(num_keys, 256 * 8), (int64_t)sms * 4);
+    radix_hist_all_kernel<<<hgrid, 256, 0, s>>>(num_keys, keys, ps, hist);
+    radix_digit_scan_kernel<<<1, kRadix, 0, s>>>(ps.n, hist);
     uint64_t *ki = keys, *ko = keys_alt;
     uint32_t *vi = values, *vo = values_alt;
     int alt = 0;
-    for (int shift = 0; shift < key_bits; shift += 8) {
-        radix_hist_kernel<<<tiles, kSortThreads, 0, s>>>(num_keys, shift, ki, hist, tiles);
-        radix_rowscan_kernel<<<kRadix, 256, 0, s>>>(hist, tiles, totals);
-        radix_scatter_kernel<<<tiles, kSortThreads, 0, s>>>(num_keys, shift, ki, vi, ko, vo, hist, totals, tiles);
+    for (int p = 0; p < ps.n; ++p) {
+        radix_onesweep_kernel<<<tiles, kSortThreads, 0, s>>>(num_keys, ps.shift[p], ki, vi, ko, vo,
+                                                             hist + (size_t)p * kRadix,
+                                                             status + (size_t)p * tiles * kRadix, counters + p);
         uint64_t *tk = ki; ki = ko; ko = tk;
         uint32_t *tv = vi; vi = vo; vo = tv;
         alt ^= 1;

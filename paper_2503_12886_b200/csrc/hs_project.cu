@@ -108,16 +108,35 @@ __device__ __forceinline__ uint32_t write_record(const Proj &p, float op, const 
     return (uint32_t)((r_hi / kTile - r_lo / kTile + 1) * (c_hi / kTile - c_lo / kTile + 1));
 }
 
-__device__ __forceinline__ void block_sum_store(uint32_t v, uint32_t *block_sums) {
-    __shared__ uint32_t warp_sums[32];
+// Per-256-item sum of tile counts (the key-offset scan input) and the range of the
+// float bits of the depths that emit keys: the radix sort skips digit windows that
+// are constant over [min, max] (positive floats order like their bit patterns).
+__device__ __forceinline__ void block_sum_store(uint32_t v, float depth, uint32_t *block_sums,
+                                                uint32_t *depth_range) {
+    __shared__ uint32_t warp_sums[32], warp_min[32], warp_max[32];
+    const uint32_t db = __float_as_uint(depth);
+    const uint32_t dmin = __reduce_min_sync(0xffffffffu, v ? db : 0xFFFFFFFFu);
+    const uint32_t dmax = __reduce_max_sync(0xffffffffu, v ? db : 0u);
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) warp_sums[w] = v;
+    if (lane == 0) {
+        warp_sums[w] = v;
+        warp_min[w] = dmin;
+        warp_max[w] = dmax;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t s = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += warp_sums[i];
+        uint32_t s = 0, mn = 0xFFFFFFFFu, mx = 0u;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            s += warp_sums[i];
+            mn = min(mn, warp_min[i]);
+            mx = max(mx, warp_max[i]);
+        }
         block_sums[blockIdx.x] = s;
+        if (depth_range && s) {
+            atomicMin(depth_range, mn);
+            atomicMax(depth_range + 1, mx);
+        }
     }
 }
 
@@ -194,10 +213,11 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     int B, int64_t N, int F, int W, int H, const float *__restrict__ raw10, const float *__restrict__ base14,
     const int32_t *__restrict__ tri, const float *__restrict__ bary, const float *__restrict__ frames,
     const float *__restrict__ cams, float *__restrict__ records, float *__restrict__ depth,
-    uint32_t *__restrict__ counts, uint32_t *__restrict__ block_sums, float *__restrict__ radius,
-    unsigned long long *err) {
+    uint32_t *__restrict__ counts, uint32_t *__restrict__ block_sums, uint32_t *__restrict__ depth_range,
+    float *__restrict__ radius, unsigned long long *err) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
+    float dz = 0.f;
     if (i < (int64_t)B * N) {
         const int b = (int)(i / N);
         const int64_t n = i - (int64_t)b * N;
@@ -210,19 +230,21 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
         if (!ok) p.valid = false;
         cnt = write_record(p, a.op, a.col, W, H, records + i * kRec);
         depth[i] = p.zc;
+        dz = p.zc;
         counts[i] = cnt;
         if (radius) radius[i] = p.valid ? p.rad : 0.f;
     }
-    block_sum_store(cnt, block_sums);
+    block_sum_store(cnt, dz, block_sums, depth_range);
 }
 
 __global__ void __launch_bounds__(256) project_world_fwd_kernel(
     int B, int64_t N, int W, int H, const float *__restrict__ world14, const float *__restrict__ cams,
     float *__restrict__ records, float *__restrict__ depth, uint32_t *__restrict__ counts,
-    uint32_t *__restrict__ block_sums, float *__restrict__ radius, float *__restrict__ x_cam,
-    float *__restrict__ cov_cam, unsigned long long *err) {
+    uint32_t *__restrict__ block_sums, uint32_t *__restrict__ depth_range, float *__restrict__ radius,
+    float *__restrict__ x_cam, float *__restrict__ cov_cam, unsigned long long *err) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
+    float dz = 0.f;
     if (i < (int64_t)B * N) {
         const int b = (int)(i / N);
         const int64_t n = i - (int64_t)b * N;
@@ -238,6 +260,7 @@ __global__ void __launch_bounds__(256) project_world_fwd_kernel(
         project_one(pw, q, s, cams + b * kCam, p);
         cnt = write_record(p, op, col, W, H, records + i * kRec);
         depth[i] = p.zc;
+        dz = p.zc;
         counts[i] = cnt;
         if (radius) radius[i] = p.valid ? p.rad : 0.f;
         if (x_cam) { x_cam[3 * i] = p.xc; x_cam[3 * i + 1] = p.yc; x_cam[3 * i + 2] = p.zc; }
@@ -248,7 +271,7 @@ __global__ void __launch_bounds__(256) project_world_fwd_kernel(
             for (int k = 0; k < 9; ++k) cov_cam[9 * i + k] = p.valid ? full[k] : 0.f;
         }
     }
-    block_sum_store(cnt, block_sums);
+    block_sum_store(cnt, dz, block_sums, depth_range);
 }
 
 // _preprocess_backward for one splat (S/render.py:444-490).  gs = g_splat (9 floats).
@@ -429,7 +452,8 @@ int hs_scan_blocks(int64_t num_items) { return (int)((num_items + kScanBlock - 1
 int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const float *raw10,
                           const float *base14, const int32_t *tri_index, const float *bary, const float *frames,
                           const float *cameras, float *records, float *depth, uint32_t *counts,
-                          uint32_t *block_sums, float *radius, unsigned long long *err, void *stream) {
+                          uint32_t *block_sums, uint32_t *depth_range, float *radius, unsigned long long *err,
+                          void *stream) {
     if (B < 1 || N < 1 || width < 1 || height < 1 || width > 32767 || height > 32767) {
         set_error("hs_project_avatar_fwd: bad sizes B=%d N=%lld %dx%d", B, (long long)N, width, height);
         return HS_ERR_SHAPE;
@@ -437,20 +461,22 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
     const int64_t items = (int64_t)B * N;
     project_avatar_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream)>>>(
         B, N, F, width, height, raw10, base14, tri_index, bary, frames, cameras, records, depth, counts,
-        block_sums, radius, err);
+        block_sums, depth_range, radius, err);
     return check_launch("hs_project_avatar_fwd");
 }
 
 int hs_project_world_fwd(int B, int64_t N, int width, int height, const float *world14, const float *cameras,
-                         float *records, float *depth, uint32_t *counts, uint32_t *block_sums, float *radius,
-                         float *x_cam, float *cov_cam, unsigned long long *err, void *stream) {
+                         float *records, float *depth, uint32_t *counts, uint32_t *block_sums,
+                         uint32_t *depth_range, float *radius, float *x_cam, float *cov_cam,
+                         unsigned long long *err, void *stream) {
     if (B < 1 || N < 1 || width < 1 || height < 1 || width > 32767 || height > 32767) {
         set_error("hs_project_world_fwd: bad sizes B=%d N=%lld %dx%d", B, (long long)N, width, height);
         return HS_ERR_SHAPE;
     }
     const int64_t items = (int64_t)B * N;
     project_world_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream)>>>(
-        B, N, width, height, world14, cameras, records, depth, counts, block_sums, radius, x_cam, cov_cam, err);
+        B, N, width, height, world14, cameras, records, depth, counts, block_sums, depth_range, radius, x_cam, cov_cam,
+        err);
     return check_launch("hs_project_world_fwd");
 }
 

@@ -197,9 +197,12 @@ class Binner:
         self.device = device
         self.cap = 0
         self.keys = self.vals = self.keys_alt = self.vals_alt = self.ws = None
-        self.summary_host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        self.summary_host = torch.empty(3, dtype=torch.int64, pin_memory=True)
         self.offsets = None
-        self.summary = torch.empty(2, dtype=torch.int64, device=device)
+        self.summary = torch.empty(3, dtype=torch.int64, device=device)
+        self.depth_range = torch.empty(2, dtype=torch.int32, device=device)
+        self.depth_bits = (0, 0)
+        self.passes = 0
         self.ranges = None
         self.result = None
 
@@ -216,16 +219,33 @@ class Binner:
         self.ws = torch.empty(ws, dtype=torch.uint8, device=d)
         self.cap = cap
 
+    def reset_depth_range(self):
+        """{0xFFFFFFFF, 0}: the projection atomically narrows it to the depths that emit keys."""
+        self.depth_range[0] = -1
+        self.depth_range[1] = 0
+        return self.depth_range
+
     def scan(self, block_sums, nblocks, err):
-        """Exclusive scan of the per-block tile counts + the step's single D2H read."""
+        """Exclusive scan of the per-block tile counts + the step's single D2H read
+        (key total, error word, depth-bit range)."""
         if self.offsets is None or self.offsets.numel() < nblocks:
             self.offsets = torch.empty(max(nblocks, 1), dtype=torch.int32, device=self.device)
-        L.call("hs_bin_scan", nblocks, _p(block_sums), _p(self.offsets), _p(err), _p(self.summary), _stream())
+        L.call("hs_bin_scan", nblocks, _p(block_sums), _p(self.offsets), _p(err), _p(self.depth_range),
+               _p(self.summary), _stream())
         self.summary_host.copy_(self.summary, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         total = int(self.summary_host[0])
         code = int(self.summary_host[1]) & 0xFFFFFFFFFFFFFFFF
+        dr = int(self.summary_host[2]) & 0xFFFFFFFFFFFFFFFF
+        self.depth_bits = (dr & 0xFFFFFFFF, dr >> 32)
         return total, code
+
+    def sort_mask(self, tile_bits, frame_bits):
+        """Key bits the sort must resolve: the frame/tile bits plus the depth bits below
+        the highest bit in which the smallest and largest emitted depth differ."""
+        lo, hi = self.depth_bits
+        depth_width = (lo ^ hi).bit_length() if lo <= hi else 32
+        return (((1 << (tile_bits + frame_bits)) - 1) << 32) | ((1 << depth_width) - 1)
 
     def bin(self, B, N, width, height, records, depth, counts, total):
         tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
@@ -240,7 +260,9 @@ class Binner:
             L.call("hs_bin_emit", B, N, width, height, _p(records), _p(depth), _p(counts), _p(self.offsets),
                    _p(self.keys), _p(self.vals), s)
             alt = ctypes.c_int(0)
-            L.call("hs_sort_pairs", total, 32 + tile_bits + frame_bits, _p(self.keys), _p(self.vals),
+            mask = self.sort_mask(tile_bits, frame_bits)
+            self.passes = sum(1 for sh in range(0, 64, 8) if (mask >> sh) & 0xFF)
+            L.call("hs_sort_pairs", total, ctypes.c_uint64(mask), _p(self.keys), _p(self.vals),
                    _p(self.keys_alt), _p(self.vals_alt), _p(self.ws), self.ws.numel(), ctypes.byref(alt), s)
             keys, vals = (self.keys_alt, self.vals_alt) if alt.value else (self.keys, self.vals)
             L.call("hs_tile_ranges", total, _p(keys), _p(ranges), s)
@@ -250,11 +272,12 @@ class Binner:
         return self.result
 
 
-def launches_binning(total, key_bits):
-    """Kernel launches issued by Binner.bin (for the bench's gpu_launches count)."""
+def launches_binning(total, passes):
+    """Kernel launches issued by Binner.bin (emit, histogram, digit scan, one per pass,
+    ranges) -- for the bench's gpu_launches count."""
     if not total:
         return 0
-    return 1 + 3 * ((key_bits + 7) // 8) + 1
+    return 1 + 2 + passes + 1
 
 
 # -------------------------------------------------------------------- trainer
@@ -374,7 +397,8 @@ class Trainer:
         F = frames.shape[-2] if frames.dim() == 3 else frames.numel() // (B * 22)
         self._call("project_fwd", "hs_project_avatar_fwd", B, N, F, self.W, self.H, _p(self.raw10), _p(av.base14),
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
-                   _p(self.counts), _p(self.block_sums), _p(self.radius), _p(self.err), s)
+                   _p(self.counts), _p(self.block_sums), _p(self.binner.reset_depth_range()), _p(self.radius),
+                   _p(self.err), s)
         m = self._mark("bin_scan+sync")
         total, code = self.binner.scan(self.block_sums, self.nblocks, self.err)
         self._done(m)
@@ -384,7 +408,7 @@ class Trainer:
         m = self._mark("bin_sort")
         res = self.binner.bin(B, N, self.W, self.H, self.records, self.depth, self.counts, total)
         self._done(m)
-        self.launches += launches_binning(total, 32 + self.tile_bits + self.frame_bits)
+        self.launches += launches_binning(total, self.binner.passes)
         return F, res
 
     def _cameras(self, cameras):

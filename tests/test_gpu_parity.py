@@ -163,6 +163,30 @@ def test_binning_bit_exact():
         np.testing.assert_array_equal(bbox[live], res["bbox"][0][live])
 
 
+@pytest.mark.parametrize("n", [200, 1000, 9000])
+def test_binning_bit_exact_crowded_tiles(n):
+    """One 16x16 tile holding 200 / 1000 / 9000 splats with many exact depth ties
+    (quantized positions): the stable sort must break ties by Gaussian index."""
+    from paper_2503_12886_b200 import compat as C
+    rng = np.random.default_rng(n)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=-1, keepdims=True)
+    pos = np.round(rng.uniform(-0.3, 0.3, (n, 3)) * 8) / 8          # few distinct depths -> ties
+    world = O.GSet(pos, q, rng.uniform(0.02, 0.06, (n, 3)), rng.uniform(0.3, 0.9, n), rng.uniform(0, 1, (n, 3)))
+    world = gq(world)
+    cam = O.Cam(24.0, 24.0, 8.0, 8.0, np.eye(3), np.array([0.0, 0.0, 2.0]), 16, 16)
+    sp = C.preprocess(world, cam)
+    dev = sp._dev["batch"]
+    rec, bbox = record_fields(dev)
+    rad = dev["radius"].cpu().numpy()[None]
+    res = BO.bin_batch(rec[None, :, 0:2], rad, dev["depth"].cpu().numpy()[None], rec[None, :, 5], rad > 0, 16, 16)
+    keys, vals, ranges, tile_bits, tiles = dev["binned"]
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), res["keys"])
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32), res["values"])
+    r = ranges.view(-1, 2).cpu().numpy().view(np.uint32)[:res["ranges"].shape[1]]
+    assert np.array_equal(r, res["ranges"][0])
+
+
 # --------------------------------------------------------------------- raster
 
 def test_rasterize_matches_oracle():
