@@ -109,6 +109,9 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
 // windows that intersect `bit_mask` are sorted (digits that are constant across all
 // keys cannot change the order).
 
+#ifndef HS_SORT_MINB
+#define HS_SORT_MINB 4
+#endif
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per CTA
@@ -126,9 +129,22 @@ __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const ui
     __shared__ uint32_t h[kMaxPasses][kRadix];
     for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = keys[i];
-        for (int p = 0; p < ps.n; ++p) atomicAdd(&h[p][(uint32_t)(k >> ps.shift[p]) & (kRadix - 1)], 1u);
+    // warp-uniform trip count so the digit counts can be aggregated per warp with
+    // match.any (the frame/tile digits are nearly constant within a warp)
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+        const int64_t i = i0 + lane;
+        const bool valid = i < n;
+        const uint64_t k = valid ? keys[i] : 0ull;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        for (int p = 0; p < ps.n; ++p) {
+            const uint32_t d = (uint32_t)(k >> ps.shift[p]) & (kRadix - 1);
+            if (valid) {
+                const uint32_t peers = __match_any_sync(vmask, d);
+                if ((peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+            }
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < ps.n * kRadix; i += blockDim.x) {
@@ -166,7 +182,7 @@ __device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(int64_t n, int shift,
+__global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_kernel(int64_t n, int shift,
                                                                       const uint64_t *__restrict__ keys_in,
                                                                       const uint32_t *__restrict__ vals_in,
                                                                       uint64_t *__restrict__ keys_out,
@@ -247,13 +263,23 @@ __global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(int64_t n,
             st_relaxed(st, kFlagInc | cnt);
         } else {
             st_relaxed(st, kFlagAgg | cnt);
-            for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
-                uint32_t v;
-                do {
-                    v = ld_relaxed(status + (size_t)j * kRadix + tid);
-                } while (v == 0u);
-                excl += v & kCountMask;
-                if (v & kFlagInc) break;
+            // windowed look-back: 8 predecessor words per round (independent loads),
+            // consumed in order until an inclusive prefix is found
+            int64_t j = (int64_t)tile - 1;
+            bool found = false;
+            while (!found) {
+                uint32_t v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    v[k] = (j - k >= 0) ? ld_relaxed(status + (size_t)(j - k) * kRadix + tid) : kFlagInc;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (found) break;
+                    if (v[k] == 0u) break;          // not published yet: retry from this tile
+                    excl += v[k] & kCountMask;
+                    if (v[k] & kFlagInc) found = true;
+                    --j;
+                }
             }
             st_relaxed(st, kFlagInc | (excl + cnt));
         }

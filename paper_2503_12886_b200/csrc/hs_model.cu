@@ -58,14 +58,17 @@ __global__ void mlp_fwd_kernel(int H, int D, int K, const float *__restrict__ ml
     }
     __syncthreads();
     float *c = cache + (int64_t)b * 4 * D;
-    for (int i = warp; i < D; i += nw) {
-        const float z = row_dot(w1 + (int64_t)i * H, th, H, lane) + b1[i];
-        if (lane == 0) {
-            const float h = z > 0.f ? z : 0.f;
-            c[i] = z;
-            c[D + i] = h;
-            h1[i] = h;
-        }
+    // layer 1 is narrow (H = 13): one thread per output row, loads issued back to back
+    for (int i = threadIdx.x; i < D; i += blockDim.x) {
+        const float *row = w1 + (int64_t)i * H;
+        float acc = 0.f;
+#pragma unroll 8
+        for (int j = 0; j < H; ++j) acc = fmaf(row[j], th[j], acc);
+        const float z = acc + b1[i];
+        const float h = z > 0.f ? z : 0.f;
+        c[i] = z;
+        c[D + i] = h;
+        h1[i] = h;
     }
     __syncthreads();
     for (int i = warp; i < D; i += nw) {
@@ -543,7 +546,7 @@ int hs_mlp_fwd(int B, int H, int D, int K, const float *mlp, const float *theta,
         return HS_ERR_SHAPE;
     }
     size_t smem = sizeof(float) * (H + 2 * D);
-    mlp_fwd_kernel<<<B, 256, smem, HS_CHECK_STREAM(stream)>>>(H, D, K, mlp, theta, cache, psi, err);
+    mlp_fwd_kernel<<<B, 1024, smem, HS_CHECK_STREAM(stream)>>>(H, D, K, mlp, theta, cache, psi, err);
     return check_launch("hs_mlp_fwd");
 }
 
@@ -551,8 +554,8 @@ int hs_mlp_bwd(int B, int H, int D, int K, const float *mlp, const float *theta,
                const float *gpsi_partials, int num_partials, float *gpsi, float *scratch, float *g_mlp,
                void *stream) {
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    size_t smem = sizeof(float) * (K + D + 8 * D);
-    mlp_bwd_frame_kernel<<<B, 256, smem, s>>>(H, D, K, mlp, cache, gpsi_partials, num_partials, gpsi, scratch);
+    size_t smem = sizeof(float) * (K + D + 32 * D);
+    mlp_bwd_frame_kernel<<<B, 1024, smem, s>>>(H, D, K, mlp, cache, gpsi_partials, num_partials, gpsi, scratch);
     int64_t total = hs_mlp_size(H, D, K);
     mlp_bwd_weights_kernel<<<grid_for(total, 256), 256, 0, s>>>(B, H, D, K, theta, cache, gpsi, scratch, g_mlp);
     return check_launch("hs_mlp_bwd");
@@ -567,8 +570,11 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const int64_t E = 10 * N;
     size_t smem = sizeof(float) * B * K;
-    const bool vec = (E % 4 == 0) && ((uintptr_t)base14 % 16 == 0) && ((uintptr_t)deltas % 16 == 0) &&
-                     ((uintptr_t)raw10 % 16 == 0);
+#ifndef HS_BLEND_VEC4
+#define HS_BLEND_VEC4 1
+#endif
+    const bool vec = HS_BLEND_VEC4 && (E % 4 == 0) && ((uintptr_t)base14 % 16 == 0) &&
+                     ((uintptr_t)deltas % 16 == 0) && ((uintptr_t)raw10 % 16 == 0);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     if (vec) {
@@ -576,7 +582,7 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
         unsigned grid = (unsigned)std::min<int64_t>(grid_for(nv, 256), (int64_t)sms * 8);
         blend_fwd_kernel<4, 16><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
     } else {
-        unsigned grid = (unsigned)std::min<int64_t>(grid_for(E, 256), (int64_t)sms * 8);
+        unsigned grid = (unsigned)std::min<int64_t>(grid_for(E, 256), (int64_t)sms * 16);
         blend_fwd_kernel<1, 16><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
     }
     return check_launch("hs_blend_fwd");

@@ -358,7 +358,10 @@ __device__ __forceinline__ void preprocess_bwd_one(const Proj &p, const float q[
     for (int j = 0; j < 3; ++j) g_pos[j] = gx * rc[j] + gy * rc[3 + j] + gz * rc[6 + j];
 }
 
-__global__ void __launch_bounds__(256) project_avatar_bwd_kernel(
+#ifndef HS_PBWD_MINB
+#define HS_PBWD_MINB 3
+#endif
+__global__ void __launch_bounds__(256, HS_PBWD_MINB) project_avatar_bwd_kernel(
     int B, int64_t N, int F, const float *__restrict__ raw10, const float *__restrict__ base14,
     const int32_t *__restrict__ tri, const float *__restrict__ bary, const float *__restrict__ frames,
     const float *__restrict__ cams, const float *__restrict__ g_splat, float *__restrict__ g_raw14) {
