@@ -180,6 +180,10 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const float *pix_T, const uint32_t *pix_state,
                   const float *grad_image, float grad_scale, float *g_splat, void *stream);
+/* Diagnostics: forward-raster counters [warp iterations, pixel tests, q <= qmax,
+ * alpha >= 1/255] accumulated when built with -DHS_RASTER_STATS (zeros otherwise);
+ * synchronous copy to host_out[4]. */
+int hs_raster_stats(unsigned long long *host_out, int reset);
 /* loss_out[b] = sum|pred-target| / (H*W*3), loss_out[B+b] = black-bg L1,
  * loss_out[2B] = mean over frames. */
 int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *loss_partials,

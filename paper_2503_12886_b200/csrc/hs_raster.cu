@@ -35,6 +35,10 @@ namespace hs {
 #endif
 
 constexpr int kPX = HS_RASTER_PX;
+
+// Optional instrumentation (-DHS_RASTER_STATS): forward-pass counts of warp
+// iterations and pixel tests, read with hs_raster_stats().
+__device__ unsigned long long g_raster_stats[4];
 constexpr int kRT = kTile * kTile / kPX;   // threads per CTA
 constexpr int kWarps = kRT / 32;
 constexpr unsigned kFull = 0xffffffffu;
@@ -110,9 +114,10 @@ __device__ __forceinline__ void pixels_of(int tid, int tx, int ty, int &px, int 
     py0 = ty * kTile + (w >> 1) * 4 * kPX + (l >> 3);
 }
 
-// Stage one splat record into the lane's slot and vote whether the warp's block
-// [x0, x0+7] x [y0, y0+4 kPX-1] can hold a contributing pixel.
-__device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
+// Stage one splat record into the lane's slot.  Returns bit 0: the warp's block
+// [x0, x0+7] x [y0, y0+4 kPX-1] can hold a contributing pixel; bit 1: the splat's
+// integer bbox covers the whole block (the per-pixel bbox test can be skipped).
+__device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
                                             uint32_t saddr) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
     const float4 A = __ldg(r), Bv = __ldg(r + 1), Cv = __ldg(r + 2);
@@ -126,7 +131,7 @@ __device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint3
     asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 32), "r"(cl), "r"(ch), "r"(rl), "r"(rh));
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 48), "f"(Cv.y), "f"(Cv.z), "f"(Cv.w),
                  "f"(0.f));
-    if (!(qmax >= 0.f)) return false;
+    if (!(qmax >= 0.f)) return 0u;
     int r0 = rl, r1 = rh, c0 = cl, c1 = ch;
     const float det = a * c - b * b;
     const float ex = sqrtf(qmax * c / det), ey = sqrtf(qmax * a / det);
@@ -138,7 +143,9 @@ __device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint3
         c0 = max(c0, (int)floorf(A.x - hx - 0.5f));
         c1 = min(c1, (int)ceilf(A.x + hx - 0.5f));
     }
-    return c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 4 * kPX - 1 && r1 >= y0;
+    const bool hit = c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 4 * kPX - 1 && r1 >= y0;
+    const bool full = cl <= x0 && ch >= x0 + 7 && rl <= y0 && rh >= y0 + 4 * kPX - 1;
+    return (uint32_t)hit | ((uint32_t)(hit && full) << 1);
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
@@ -193,39 +200,63 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
         }
     }
 
+#ifdef HS_RASTER_STATS
+    unsigned long long st_iter = 0, st_test = 0, st_q = 0, st_c = 0;
+#endif
     for (uint32_t c0 = start; c0 < end; c0 += 32) {
         bool all_done = true;
 #pragma unroll
         for (int p = 0; p < kPX; ++p) all_done = all_done && done[p];
         if (__all_sync(kFull, all_done)) break;
         const uint32_t idx = c0 + lane;
-        bool hit = false;
+        uint32_t code = 0u;
+        bool want = false;
         if (idx < end) {
             const uint32_t n = a.vals[idx];
-            uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
-            if (CI == 3 && a.visited[n]) gflag |= 0x80000000u;   // visited: skip colour-init work
-            hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, x0, y0, wbase + lane * kStageBytes);
+            const uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
+            code = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, x0, y0, wbase + lane * kStageBytes);
+            want = CI > 0 && (code & 1u) && (CI != 3 || !a.visited[n]);   // visited: no colour-init work
         }
-        uint32_t bits = __ballot_sync(kFull, hit);
+        uint32_t bits = __ballot_sync(kFull, code & 1u);
+        const uint32_t fullb = __ballot_sync(kFull, code & 2u);
+        const uint32_t wantb = __ballot_sync(kFull, want);
         __syncwarp();
         while (bits) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1u;
             const uint32_t ad = wbase + j * kStageBytes;
-            const int4 bb = lds4i(ad + 32);
             const float4 p0 = lds4(ad), p1 = lds4(ad + 16), col = lds4(ad + 48);
-            const bool inx = px >= bb.x && px <= bb.y;
+            bool inb[kPX];
+            if ((fullb >> j) & 1u) {                 // warp-uniform: bbox covers the block
+#pragma unroll
+                for (int p = 0; p < kPX; ++p) inb[p] = true;
+            } else {
+                const int4 bb = lds4i(ad + 32);
+                const bool inx = px >= bb.x && px <= bb.y;
+#pragma unroll
+                for (int p = 0; p < kPX; ++p) inb[p] = inx && py[p] >= bb.z && py[p] <= bb.w;
+            }
             const float dx = fpx - p0.x;
             const float kadx = __fmul_rn(p0.z, dx);
             float w[kPX];
 #pragma unroll
             for (int p = 0; p < kPX; ++p) w[p] = 0.f;
+#ifdef HS_RASTER_STATS
+            st_iter += (lane == 0);
+#endif
 #pragma unroll
             for (int p = 0; p < kPX; ++p) {
-                if (!done[p] && inx && py[p] >= bb.z && py[p] <= bb.w) {
+                if (!done[p] && inb[p]) {
                     const float e2 = splat_e2(dx, fpy[p] - p0.y, kadx, p0.w, p1.x);
+#ifdef HS_RASTER_STATS
+                    ++st_test;
+                    st_q += e2 >= p1.y;
+#endif
                     if (e2 >= p1.y) {
                         const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
+#ifdef HS_RASTER_STATS
+                        st_c += alpha >= kAlphaCutoff;
+#endif
                         if (alpha >= kAlphaCutoff) {
                             w[p] = alpha * T[p];
                             C[p][0] += w[p] * col.x;
@@ -240,14 +271,12 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
                     }
                 }
             }
-            if (CI > 0) {
-                const uint32_t gf = __float_as_uint(p1.w);
-                const bool want = CI != 3 || !(gf & 0x80000000u);
+            if (CI > 0 && ((wantb >> j) & 1u)) {
                 float wmax = 0.f;
 #pragma unroll
                 for (int p = 0; p < kPX; ++p) wmax = fmaxf(wmax, w[p]);
-                if (want && __any_sync(kFull, wmax > 0.f)) {
-                    const int64_t g = gf & 0x7FFFFFFFu;
+                if (__any_sync(kFull, wmax > 0.f)) {
+                    const int64_t g = __float_as_uint(p1.w);
                     const float wm = warp_max(wmax);
                     if (CI >= 2) {
                         float v[4] = {0.f, 0.f, 0.f, 0.f};
@@ -270,6 +299,12 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
         __syncwarp();
     }
 
+#ifdef HS_RASTER_STATS
+    atomicAdd(&g_raster_stats[0], st_iter);
+    atomicAdd(&g_raster_stats[1], st_test);
+    atomicAdd(&g_raster_stats[2], st_q);
+    atomicAdd(&g_raster_stats[3], st_c);
+#endif
     float l1 = 0.f, black = 0.f;
 #pragma unroll
     for (int p = 0; p < kPX; ++p) {
@@ -368,22 +403,31 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
     for (uint32_t c_end = last; c_end > start;) {
         const uint32_t c0 = c_end - start > 32u ? c_end - 32u : start;
         const uint32_t idx = c0 + lane;
-        bool hit = false;
+        uint32_t code = 0u;
         if (idx < c_end) {
             const uint32_t n = a.vals[idx];
-            hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0, y0,
-                              wbase + lane * kStageBytes);
+            code = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0, y0,
+                               wbase + lane * kStageBytes);
         }
-        uint32_t bits = __ballot_sync(kFull, hit);
+        uint32_t bits = __ballot_sync(kFull, code & 1u);
+        const uint32_t fullb = __ballot_sync(kFull, code & 2u);
         __syncwarp();
         while (bits) {
             const int j = 31 - __clz(bits);
             bits &= ~(1u << j);
             const uint32_t jl = c0 - start + (uint32_t)j;
             const uint32_t ad = wbase + j * kStageBytes;
-            const int4 bb = lds4i(ad + 32);
             const float4 p0 = lds4(ad), p1 = lds4(ad + 16), col = lds4(ad + 48);
-            const bool inx = px >= bb.x && px <= bb.y;
+            bool inb[kPX];
+            if ((fullb >> j) & 1u) {                 // warp-uniform: bbox covers the block
+#pragma unroll
+                for (int p = 0; p < kPX; ++p) inb[p] = true;
+            } else {
+                const int4 bb = lds4i(ad + 32);
+                const bool inx = px >= bb.x && px <= bb.y;
+#pragma unroll
+                for (int p = 0; p < kPX; ++p) inb[p] = inx && py[p] >= bb.z && py[p] <= bb.w;
+            }
             const float dx = fpx - p0.x;
             const float kadx = __fmul_rn(p0.z, dx);
             const float hb2 = 0.5f * p0.w;
@@ -393,7 +437,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
             bool contrib = false;
 #pragma unroll
             for (int p = 0; p < kPX; ++p) {
-                if (jl < stop[p] && inx && py[p] >= bb.z && py[p] <= bb.w) {
+                if (jl < stop[p] && inb[p]) {
                     const float dy = fpy[p] - p0.y;
                     const float e2 = splat_e2(dx, dy, kadx, p0.w, p1.x);
                     if (e2 >= p1.y) {
@@ -547,6 +591,15 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a);
     else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a);
     return check_launch("hs_raster_bwd");
+}
+
+int hs_raster_stats(unsigned long long *host_out, int reset) {
+    cudaMemcpyFromSymbol(host_out, g_raster_stats, sizeof(unsigned long long) * 4);
+    if (reset) {
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_raster_stats, z, sizeof(z));
+    }
+    return check_launch("hs_raster_stats");
 }
 
 int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *loss_partials, float *loss_out,

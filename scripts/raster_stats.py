@@ -1,0 +1,20 @@
+"""Forward-raster work counters on the C2 step (needs a -DHS_RASTER_STATS build)."""
+import ctypes, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from bench import CONFIGS, make_trainer
+from paper_2503_12886_b200 import _lib as L
+import torch
+tr, d, wl = make_trainer(CONFIGS["C2"])
+for _ in range(3):
+    tr.step(d["thetas"], d["targets"], d["frames"], d["cameras"], d["backgrounds"])
+torch.cuda.synchronize()
+buf = (ctypes.c_uint64 * 4)()
+L.load().hs_raster_stats(buf, 1)
+tr.step(d["thetas"], d["targets"], d["frames"], d["cameras"], d["backgrounds"])
+torch.cuda.synchronize()
+L.load().hs_raster_stats(buf, 1)
+it, test, q, c = list(buf)
+print(f"keys {tr.last_total}  warp-iters {it}  per key {it / tr.last_total:.2f}  pixel-tests {test} "
+      f"({test / max(it, 1):.1f} per iter of 64 slots)  q-pass {q} ({q / max(test, 1) * 100:.1f}%)  contrib {c} "
+      f"({c / max(test, 1) * 100:.1f}%)")
