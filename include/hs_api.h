@@ -168,6 +168,9 @@ enum {
     HS_RASTER_WSUMS = 16,        /* colour-init sums (sum w*target, sum w) for the same set */
     HS_RASTER_WSUMS_IMAGE = 32   /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
 };
+/* loss_partials holds B * num_tiles * HS_LOSS_PARTIALS_PER_TILE floats (an (L1,
+ * black L1) pair per 8x8 pixel block), reduced by hs_loss_reduce. */
+#define HS_LOSS_PARTIALS_PER_TILE 8
 int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const uint8_t *targets, const float *wsum_image,
@@ -181,8 +184,9 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
                   const float *backgrounds, const float *pix_T, const uint32_t *pix_state,
                   const float *grad_image, float grad_scale, float *g_splat, void *stream);
 /* Diagnostics: forward-raster counters [warp iterations, pixel tests, q <= qmax,
- * alpha >= 1/255] accumulated when built with -DHS_RASTER_STATS (zeros otherwise);
- * synchronous copy to host_out[4]. */
+ * alpha >= 1/255, iterations with no q pass, full-cover iterations, staged
+ * batches, 0] accumulated when built with -DHS_RASTER_STATS (zeros otherwise);
+ * synchronous copy to host_out[8]. */
 int hs_raster_stats(unsigned long long *host_out, int reset);
 /* loss_out[b] = sum|pred-target| / (H*W*3), loss_out[B+b] = black-bg L1,
  * loss_out[2B] = mean over frames. */

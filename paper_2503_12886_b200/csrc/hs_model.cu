@@ -179,6 +179,10 @@ __global__ void mlp_bwd_weights_kernel(int B, int H, int D, int K, const float *
 // thread owns VEC consecutive channels and keeps BC frames of accumulators, so
 // every delta element is read from HBM once per BC frames (once per step for
 // B <= BC).  S/model.py:165-185 (k ascending, psi == 0 skipped).
+#ifndef HS_BLEND_KB
+#define HS_BLEND_KB 4
+#endif
+constexpr int kKB = HS_BLEND_KB;
 template <int VEC, int BC>
 __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
                                                         const float *__restrict__ base,
@@ -206,21 +210,31 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
             for (int j = 0; j < BC; ++j)
 #pragma unroll
                 for (int c = 0; c < VEC; ++c) acc[j][c] = bv[c];
-            for (int k = 0; k < K; ++k) {
-                float dv[VEC];
-                if constexpr (VEC == 4) {
-                    float4 t = __ldcs(reinterpret_cast<const float4 *>(deltas + (int64_t)k * E + e));
-                    dv[0] = t.x; dv[1] = t.y; dv[2] = t.z; dv[3] = t.w;
-                } else {
-                    dv[0] = __ldcs(deltas + (int64_t)k * E + e);
+            // kKB bases per round: all their loads are issued before any use, so a
+            // thread keeps kKB * 16 B in flight instead of one dependent load per basis
+            for (int k0 = 0; k0 < K; k0 += kKB) {
+                float dv[kKB][VEC];
+#pragma unroll
+                for (int q = 0; q < kKB; ++q) {
+                    const int k = min(k0 + q, K - 1);
+                    if constexpr (VEC == 4) {
+                        float4 t = __ldcs(reinterpret_cast<const float4 *>(deltas + (int64_t)k * E + e));
+                        dv[q][0] = t.x; dv[q][1] = t.y; dv[q][2] = t.z; dv[q][3] = t.w;
+                    } else {
+                        dv[q][0] = __ldcs(deltas + (int64_t)k * E + e);
+                    }
                 }
 #pragma unroll
-                for (int j = 0; j < BC; ++j) {
-                    if (j < nb) {
-                        const float w = s_psi[(b0 + j) * K + k];
-                        if (w != 0.0f) {
+                for (int q = 0; q < kKB; ++q) {
+                    if (k0 + q < K) {
 #pragma unroll
-                            for (int c = 0; c < VEC; ++c) acc[j][c] = fmaf(w, dv[c], acc[j][c]);
+                        for (int j = 0; j < BC; ++j) {
+                            if (j < nb) {
+                                const float w = s_psi[(b0 + j) * K + k0 + q];
+#pragma unroll
+                                for (int c = 0; c < VEC; ++c)
+                                    acc[j][c] = w != 0.0f ? fmaf(w, dv[q][c], acc[j][c]) : acc[j][c];
+                            }
                         }
                     }
                 }
@@ -256,6 +270,10 @@ constexpr int kBT = 256;
 constexpr int kBMaxB = 16;
 constexpr int kBMaxK = 32;
 constexpr int kBBlocks = 592;   // persistent grid: 148 SMs x 4 CTAs
+#ifndef HS_BLEND_KBB
+#define HS_BLEND_KBB 8
+#endif
+constexpr int kKBB = HS_BLEND_KBB;  // delta loads in flight per lane
 
 template <int BP>
 __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N, int K, int Bc, int b0,
@@ -290,9 +308,16 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
         if (in) g_base[e] = accumulate ? g_base[e] + s : s;
         if (c * 32 >= E10) continue;                       // warp-uniform
         const bool in10 = e < E10;
-#pragma unroll 4
-        for (int k = 0; k < K; ++k) {
-            const float d = in10 ? __ldcs(deltas + (int64_t)k * E10 + e) : 0.f;
+        for (int k0 = 0; k0 < K; k0 += kKBB) {
+          float dk[kKBB];
+#pragma unroll
+          for (int q = 0; q < kKBB; ++q)     // issue the round's loads before any use
+              dk[q] = in10 ? __ldcs(deltas + (int64_t)min(k0 + q, K - 1) * E10 + e) : 0.f;
+#pragma unroll
+          for (int q = 0; q < kKBB; ++q) {
+            const int k = k0 + q;
+            if (k >= K) break;
+            const float d = dk[q];
             float gd = 0.f;
             float v[BP];
 #pragma unroll
@@ -308,6 +333,7 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
             bool issue;
             const float r = reduce_scatter(v, lane, vi, issue);
             if (issue) accw[warp][k * BP + vi] += r;
+          }
         }
     }
     __syncthreads();

@@ -30,17 +30,22 @@ namespace hs {
 #ifndef HS_RASTER_PX
 #define HS_RASTER_PX 2               // pixels per lane (a warp owns an 8 x 4*PX block)
 #endif
+#ifndef HS_RASTER_CTA_WARPS
+#define HS_RASTER_CTA_WARPS 1        // warps per CTA (each warp owns one 8 x 4*PX block)
+#endif
 #ifndef HS_RASTER_MINB
-#define HS_RASTER_MINB (16 / HS_RASTER_PX)   // resident CTAs per SM the register budget must allow
+#define HS_RASTER_MINB (64 / HS_RASTER_PX / HS_RASTER_CTA_WARPS)   // resident CTAs per SM the register budget must allow
 #endif
 
 constexpr int kPX = HS_RASTER_PX;
+constexpr int kCW = HS_RASTER_CTA_WARPS;
 
 // Optional instrumentation (-DHS_RASTER_STATS): forward-pass counts of warp
 // iterations and pixel tests, read with hs_raster_stats().
-__device__ unsigned long long g_raster_stats[4];
-constexpr int kRT = kTile * kTile / kPX;   // threads per CTA
-constexpr int kWarps = kRT / 32;
+__device__ unsigned long long g_raster_stats[8];
+constexpr int kBlocks = kTile * kTile / (32 * kPX);   // 8 x 4*PX pixel blocks per tile
+constexpr int kRT = 32 * kCW;                          // threads per CTA
+static_assert(kBlocks % kCW == 0, "CTA warps must divide the blocks of a tile");
 constexpr unsigned kFull = 0xffffffffu;
 
 struct RasterArgs {
@@ -105,11 +110,10 @@ __device__ __forceinline__ float splat_e2(float dx, float dy, float kadx, float 
     return __fmaf_rn(__fmul_rn(kc, dy), dy, __fmul_rn(dx, __fmaf_rn(kb2, dy, kadx)));
 }
 
-// Pixels of thread `tid`: warp w covers cols (w & 1) * 8 .. +7 and rows
-// (w >> 1) * 4 kPX .. +4 kPX - 1 of the tile; lane l holds column l & 7 and rows
+// Pixels of lane l in block w of a tile: block w covers cols (w & 1) * 8 .. +7 and
+// rows (w >> 1) * 4 kPX .. +4 kPX - 1; lane l holds column l & 7 and rows
 // (l >> 3) + 4 p for p < kPX.
-__device__ __forceinline__ void pixels_of(int tid, int tx, int ty, int &px, int &py0) {
-    const int w = tid >> 5, l = tid & 31;
+__device__ __forceinline__ void pixels_of(int w, int l, int tx, int ty, int &px, int &py0) {
     px = tx * kTile + (w & 1) * 8 + (l & 7);
     py0 = ty * kTile + (w >> 1) * 4 * kPX + (l >> 3);
 }
@@ -153,61 +157,59 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
 template <bool kLoss, bool kImage, int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    __shared__ float red[2][kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x, b = blockIdx.y;
+    const int gw = blockIdx.x * kCW + warp;              // block of the frame: tile * kBlocks + blk
+    const int tile = gw / kBlocks, blk = gw % kBlocks, b = blockIdx.y;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int px, py0;
-    pixels_of(tid, tx, ty, px, py0);
-    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 4 * kPX;
+    pixels_of(blk, lane, tx, ty, px, py0);
+    const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 4 * kPX;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
     const float fpx = (float)px;
 
-    int py[kPX];
-    bool inside[kPX], done[kPX];
-    int64_t pix[kPX];
-    float fpy[kPX], T[kPX], C[kPX][3], tgt[kPX][3], rgb[kPX][3], rgba_a[kPX], src[kPX][3];
+    // live state across the splat loop is kept small (T, C, stop, and the colour-init
+    // source only when needed); the target is re-read in the epilogue
+    float fpy[kPX], T[kPX], C[kPX][3], src[CI >= 2 ? kPX : 1][3];
     uint32_t stop[kPX];
+    bool live[kPX];
 #pragma unroll
     for (int p = 0; p < kPX; ++p) {
-        py[p] = py0 + 4 * p;
-        inside[p] = px < a.W && py[p] < a.H;
-        pix[p] = ((int64_t)b * a.H + (inside[p] ? py[p] : 0)) * a.W + (inside[p] ? px : 0);
-        fpy[p] = (float)py[p];
+        const int py = py0 + 4 * p;
+        const bool inside = px < a.W && py < a.H;
+        fpy[p] = (float)py;
         T[p] = 1.0f;
-        done[p] = !inside[p];
+        live[p] = inside;
         stop[p] = end - start;
-        rgba_a[p] = 0.f;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) { C[p][c] = 0.f; tgt[p][c] = 0.f; rgb[p][c] = 0.f; }
-        if ((kLoss || CI >= 2) && inside[p] && a.targets) {
-            const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix[p]];
-            rgba_a[p] = (float)t.w / 255.0f;
-            rgb[p][0] = (float)t.x / 255.0f;
-            rgb[p][1] = (float)t.y / 255.0f;
-            rgb[p][2] = (float)t.z / 255.0f;
+        for (int c = 0; c < 3; ++c) C[p][c] = 0.f;
+        if constexpr (CI >= 2) {
+            const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) tgt[p][c] = rgb[p][c] * rgba_a[p] + (1.0f - rgba_a[p]) * bg[c];
-        }
+            for (int c = 0; c < 3; ++c) src[p][c] = 0.f;
+            if (inside && a.wsum_image) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) src[p][c] = tgt[p][c];
-        if (CI >= 2 && a.wsum_image && inside[p]) {
+                for (int c = 0; c < 3; ++c) src[p][c] = a.wsum_image[pix * 3 + c];
+            } else if (inside && a.targets) {
+                const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
+                const float al = (float)t.w / 255.0f;
+                const float rgb[3] = {(float)t.x / 255.0f, (float)t.y / 255.0f, (float)t.z / 255.0f};
 #pragma unroll
-            for (int c = 0; c < 3; ++c) src[p][c] = a.wsum_image[pix[p] * 3 + c];
+                for (int c = 0; c < 3; ++c) src[p][c] = rgb[c] * al + (1.0f - al) * bg[c];
+            }
         }
     }
 
 #ifdef HS_RASTER_STATS
-    unsigned long long st_iter = 0, st_test = 0, st_q = 0, st_c = 0;
+    unsigned long long st_iter = 0, st_test = 0, st_q = 0, st_c = 0, st_empty = 0, st_full = 0, st_batches = 0;
 #endif
     for (uint32_t c0 = start; c0 < end; c0 += 32) {
-        bool all_done = true;
+        bool any_live = false;
 #pragma unroll
-        for (int p = 0; p < kPX; ++p) all_done = all_done && done[p];
-        if (__all_sync(kFull, all_done)) break;
+        for (int p = 0; p < kPX; ++p) any_live = any_live || live[p];
+        if (!__any_sync(kFull, any_live)) break;
         const uint32_t idx = c0 + lane;
         uint32_t code = 0u;
         bool want = false;
@@ -220,6 +222,9 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
         uint32_t bits = __ballot_sync(kFull, code & 1u);
         const uint32_t fullb = __ballot_sync(kFull, code & 2u);
         const uint32_t wantb = __ballot_sync(kFull, want);
+#ifdef HS_RASTER_STATS
+        st_batches += lane == 0;
+#endif
         __syncwarp();
         while (bits) {
             const int j = __ffs(bits) - 1;
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
                 const int4 bb = lds4i(ad + 32);
                 const bool inx = px >= bb.x && px <= bb.y;
 #pragma unroll
-                for (int p = 0; p < kPX; ++p) inb[p] = inx && py[p] >= bb.z && py[p] <= bb.w;
+                for (int p = 0; p < kPX; ++p) inb[p] = inx && py0 + 4 * p >= bb.z && py0 + 4 * p <= bb.w;
             }
             const float dx = fpx - p0.x;
             const float kadx = __fmul_rn(p0.z, dx);
@@ -243,34 +248,37 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
             for (int p = 0; p < kPX; ++p) w[p] = 0.f;
 #ifdef HS_RASTER_STATS
             st_iter += (lane == 0);
+            st_full += (lane == 0) && ((fullb >> j) & 1u);
+            bool anyq = false;
 #endif
+            // branch-free per pixel: alpha is evaluated for every slot and the
+            // update predicated on the reference's tests (bbox, q <= qmax, cutoff)
 #pragma unroll
             for (int p = 0; p < kPX; ++p) {
-                if (!done[p] && inb[p]) {
-                    const float e2 = splat_e2(dx, fpy[p] - p0.y, kadx, p0.w, p1.x);
+                const float e2 = splat_e2(dx, fpy[p] - p0.y, kadx, p0.w, p1.x);
+                const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
+                const bool ok = live[p] && inb[p] && e2 >= p1.y && alpha >= kAlphaCutoff;
 #ifdef HS_RASTER_STATS
-                    ++st_test;
-                    st_q += e2 >= p1.y;
+                st_test += live[p] && inb[p];
+                st_q += live[p] && inb[p] && e2 >= p1.y;
+                anyq = anyq || (live[p] && inb[p] && e2 >= p1.y);
+                st_c += ok;
 #endif
-                    if (e2 >= p1.y) {
-                        const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
-#ifdef HS_RASTER_STATS
-                        st_c += alpha >= kAlphaCutoff;
-#endif
-                        if (alpha >= kAlphaCutoff) {
-                            w[p] = alpha * T[p];
-                            C[p][0] += w[p] * col.x;
-                            C[p][1] += w[p] * col.y;
-                            C[p][2] += w[p] * col.z;
-                            T[p] = T[p] * (1.0f - alpha);
-                            if (T[p] < kTermEps) {
-                                done[p] = true;
-                                stop[p] = c0 - start + (uint32_t)j + 1u;
-                            }
-                        }
+                if (ok) {
+                    w[p] = alpha * T[p];
+                    C[p][0] += w[p] * col.x;
+                    C[p][1] += w[p] * col.y;
+                    C[p][2] += w[p] * col.z;
+                    T[p] = T[p] * (1.0f - alpha);
+                    if (T[p] < kTermEps) {
+                        live[p] = false;
+                        stop[p] = c0 - start + (uint32_t)j + 1u;
                     }
                 }
             }
+#ifdef HS_RASTER_STATS
+            st_empty += !__any_sync(kFull, anyq) && lane == 0;
+#endif
             if (CI > 0 && ((wantb >> j) & 1u)) {
                 float wmax = 0.f;
 #pragma unroll
@@ -304,45 +312,47 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
     atomicAdd(&g_raster_stats[1], st_test);
     atomicAdd(&g_raster_stats[2], st_q);
     atomicAdd(&g_raster_stats[3], st_c);
+    atomicAdd(&g_raster_stats[4], st_empty);
+    atomicAdd(&g_raster_stats[5], st_full);
+    atomicAdd(&g_raster_stats[6], st_batches);
 #endif
     float l1 = 0.f, black = 0.f;
 #pragma unroll
     for (int p = 0; p < kPX; ++p) {
-        if (!inside[p]) continue;
+        const int py = py0 + 4 * p;
+        if (px >= a.W || py >= a.H) continue;
+        const int64_t pix = ((int64_t)b * a.H + py) * a.W + px;
         float pred[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) pred[c] = C[p][c] + T[p] * bg[c];
         uint32_t signs = 0;
         if (kLoss) {
+            const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
+            const float al = (float)t.w / 255.0f;
+            const float rgb[3] = {(float)t.x / 255.0f, (float)t.y / 255.0f, (float)t.z / 255.0f};
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float d = pred[c] - tgt[p][c];
+                const float tgt = rgb[c] * al + (1.0f - al) * bg[c];
+                const float d = pred[c] - tgt;
                 l1 += fabsf(d);
-                black += fabsf(C[p][c] - rgb[p][c] * rgba_a[p]);
+                black += fabsf(C[p][c] - rgb[c] * al);
                 signs |= (d > 0.f ? 1u : d < 0.f ? 2u : 0u) << (2 * c);
             }
         }
-        a.pix_T[pix[p]] = T[p];
-        a.pix_state[pix[p]] = stop[p] | (signs << 26);
+        a.pix_T[pix] = T[p];
+        a.pix_state[pix] = stop[p] | (signs << 26);
         if (kImage) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) a.image[pix[p] * 3 + c] = pred[c];
+            for (int c = 0; c < 3; ++c) a.image[pix * 3 + c] = pred[c];
         }
     }
-    if (kLoss) {
+    if (kLoss) {            // per-block partials: no CTA barrier, warps retire independently
         l1 = warp_sum(l1);
         black = warp_sum(black);
         if (lane == 0) {
-            red[0][warp] = l1;
-            red[1][warp] = black;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            float s0 = 0.f, s1 = 0.f;
-            for (int i = 0; i < kWarps; ++i) { s0 += red[0][i]; s1 += red[1][i]; }
-            const int tiles = gridDim.x;
-            a.loss_partials[((int64_t)b * tiles + tile) * 2] = s0;
-            a.loss_partials[((int64_t)b * tiles + tile) * 2 + 1] = s1;
+            const int64_t o = ((int64_t)b * gridDim.x * kCW + gw) * 2;
+            a.loss_partials[o] = l1;
+            a.loss_partials[o + 1] = black;
         }
     }
 }
@@ -351,11 +361,12 @@ template <bool kExplicitGrad>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x, b = blockIdx.y;
+    const int gw = blockIdx.x * kCW + warp;
+    const int tile = gw / kBlocks, blk = gw % kBlocks, b = blockIdx.y;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int px, py0;
-    pixels_of(tid, tx, ty, px, py0);
-    const int x0 = tx * kTile + (warp & 1) * 8, y0 = ty * kTile + (warp >> 1) * 4 * kPX;
+    pixels_of(blk, lane, tx, ty, px, py0);
+    const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 4 * kPX;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     if (start >= end) return;
@@ -480,6 +491,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
     }
 }
 
+// partials[b][tiles * kBlocks][2] (one pair per pixel block)
 __global__ void loss_reduce_kernel(int B, int tiles, float inv_count, const float *__restrict__ partials,
                                    float *__restrict__ out) {
     __shared__ float red[2][32];
@@ -566,7 +578,7 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     a.maxw = maxw;
     a.wsums = wsums;
     a.loss_partials = loss_partials;
-    dim3 grid(tiles_x * tiles_y, B);
+    dim3 grid(tiles_x * tiles_y * (kBlocks / kCW), B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
     if (loss && img) launch_fwd_ci<true, true>(ci, grid, s, a);
     else if (loss) launch_fwd_ci<true, false>(ci, grid, s, a);
@@ -586,7 +598,7 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     a.grad_image = grad_image;
     a.grad_scale = grad_scale;
     a.g_splat = g_splat;
-    dim3 grid(tiles_x * tiles_y, B);
+    dim3 grid(tiles_x * tiles_y * (kBlocks / kCW), B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
     if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a);
     else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a);
@@ -594,9 +606,9 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
 }
 
 int hs_raster_stats(unsigned long long *host_out, int reset) {
-    cudaMemcpyFromSymbol(host_out, g_raster_stats, sizeof(unsigned long long) * 4);
+    cudaMemcpyFromSymbol(host_out, g_raster_stats, sizeof(unsigned long long) * 8);
     if (reset) {
-        const unsigned long long z[4] = {0, 0, 0, 0};
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(g_raster_stats, z, sizeof(z));
     }
     return check_launch("hs_raster_stats");
@@ -606,7 +618,8 @@ int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *los
                    void *stream) {
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const float inv = (float)(1.0 / ((double)width * height * 3.0));
-    loss_reduce_kernel<<<B, 256, 0, s>>>(B, num_tiles, inv, loss_partials, loss_out);
+    static_assert(HS_LOSS_PARTIALS_PER_TILE == 2 * kBlocks, "hs_api.h partial count");
+    loss_reduce_kernel<<<B, 256, 0, s>>>(B, num_tiles * kBlocks, inv, loss_partials, loss_out);
     loss_mean_kernel<<<1, 32, 0, s>>>(B, loss_out);
     return check_launch("hs_loss_reduce");
 }

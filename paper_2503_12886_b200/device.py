@@ -336,7 +336,7 @@ class Trainer:
         self.pix_state = torch.empty(B * self.H * self.W, dtype=torch.int32, device=d)
         self.maxw = torch.zeros(B * N, **f32)
         self.wsums = torch.zeros(B * N * 4, **f32)
-        self.loss_partials = torch.empty(B * self.tiles * 2, **f32)
+        self.loss_partials = torch.empty(B * self.tiles * L.LOSS_PARTIALS_PER_TILE, **f32)
         self.loss_out = torch.empty(2 * B + 1, **f32)
         self.g_splat = torch.empty(B * N * 9, **f32)
         self.g_raw14 = torch.empty(B * 14 * N, **f32)

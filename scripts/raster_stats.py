@@ -9,12 +9,13 @@ tr, d, wl = make_trainer(CONFIGS["C2"])
 for _ in range(3):
     tr.step(d["thetas"], d["targets"], d["frames"], d["cameras"], d["backgrounds"])
 torch.cuda.synchronize()
-buf = (ctypes.c_uint64 * 4)()
+buf = (ctypes.c_uint64 * 8)()
 L.load().hs_raster_stats(buf, 1)
 tr.step(d["thetas"], d["targets"], d["frames"], d["cameras"], d["backgrounds"])
 torch.cuda.synchronize()
 L.load().hs_raster_stats(buf, 1)
-it, test, q, c = list(buf)
+it, test, q, c, empty, full, batches, _ = list(buf)
 print(f"keys {tr.last_total}  warp-iters {it}  per key {it / tr.last_total:.2f}  pixel-tests {test} "
       f"({test / max(it, 1):.1f} per iter of 64 slots)  q-pass {q} ({q / max(test, 1) * 100:.1f}%)  contrib {c} "
-      f"({c / max(test, 1) * 100:.1f}%)")
+      f"({c / max(test, 1) * 100:.1f}%)  no-q iters {empty} ({empty / max(it, 1) * 100:.1f}%)  full-cover iters {full} "
+      f"({full / max(it, 1) * 100:.1f}%)  batches {batches}")
