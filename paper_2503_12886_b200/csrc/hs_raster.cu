@@ -1,15 +1,17 @@
 // hs_raster.cu -- tile rasterizer (forward + adjoint) on sm_100a.
 //
-// One 128-thread CTA per (frame, 16x16 tile).  Each warp owns an 8x8 pixel block
-// and each lane two pixels of it (rows r and r+4 of one column), so the per-splat
+// One warp (a one-warp CTA) per (frame, 16x16 tile, 8x8 pixel block): each lane
+// holds two pixels of the block (rows r and r+4 of one column), so the per-splat
 // overhead (list walk, shared loads, the warp reduction of the adjoint) is paid
-// once per 64 pixels.  Every warp walks the tile's depth-ordered key range on its
-// own, 32 splats per batch: each lane gathers one 48-byte record, pre-transforms it
+// once per 64 pixels.  The four warps of a tile walk its depth-ordered key range
+// independently, 32 splats per batch: each lane gathers one 48-byte record, pre-transforms it
 // into a 64-byte staged form in the warp's private shared slot and votes whether
-// the warp's 8x8 block can be touched at all -- the intersection of the splat's
-// integer pixel bbox with the exact extent of its alpha >= 1/255 ellipse (q <=
-// qmax), padded for rounding.  Skipping a block is exact: every pixel in it fails
-// the reference's bbox or q test anyway.  There is no CTA barrier in the loop.
+// the warp's 8x8 block can be touched at all: the splat's integer pixel bbox must
+// admit a pixel of the block and its alpha >= 1/255 ellipse (q <= qmax) must reach
+// the rectangle of those pixel centres (exact minimum of q over the rectangle,
+// padded for rounding).  Skipping a block is exact: every pixel in it fails the
+// reference's bbox or q test anyway.  Each CTA is a single warp, so there is no
+// CTA barrier and blocks retire independently.
 //
 // Per pixel the math is the reference's front-to-back compositing
 // (S/render.py:233-273): same bbox test, q / qmax and alpha >= 1/255 cutoffs, no
@@ -35,6 +37,10 @@ namespace hs {
 #endif
 #ifndef HS_RASTER_MINB
 #define HS_RASTER_MINB (64 / HS_RASTER_PX / HS_RASTER_CTA_WARPS)   // resident CTAs per SM the register budget must allow
+#endif
+
+#ifndef HS_RASTER_EXACT_CULL
+#define HS_RASTER_EXACT_CULL 1       // cull blocks with the exact ellipse-rectangle distance
 #endif
 
 constexpr int kPX = HS_RASTER_PX;
@@ -136,20 +142,29 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 48), "f"(Cv.y), "f"(Cv.z), "f"(Cv.w),
                  "f"(0.f));
     if (!(qmax >= 0.f)) return 0u;
-    int r0 = rl, r1 = rh, c0 = cl, c1 = ch;
-    const float det = a * c - b * b;
-    const float ex = sqrtf(qmax * c / det), ey = sqrtf(qmax * a / det);
-    if (det > 0.f && ex < 1e6f && ey < 1e6f) {
-        const float hx = ex * 1.001f + 1e-3f, hy = ey * 1.001f + 1e-3f;   // rounding margin
-        // pixel p passes |p + 0.5 - m| <= e  <=>  p in [m - e - 0.5, m + e - 0.5]
-        r0 = max(r0, (int)floorf(A.y - hy - 0.5f));
-        r1 = min(r1, (int)ceilf(A.y + hy - 0.5f));
-        c0 = max(c0, (int)floorf(A.x - hx - 0.5f));
-        c1 = min(c1, (int)ceilf(A.x + hx - 0.5f));
-    }
-    const bool hit = c0 <= x0 + 7 && c1 >= x0 && r0 <= y0 + 4 * kPX - 1 && r1 >= y0;
+    // pixels of the block the reference's bbox admits
+    const int xs = max(x0, cl), xe = min(x0 + 7, ch), ys = max(y0, rl), ye = min(y0 + 4 * kPX - 1, rh);
+    if (xs > xe || ys > ye) return 0u;
     const bool full = cl <= x0 && ch >= x0 + 7 && rl <= y0 && rh >= y0 + 4 * kPX - 1;
-    return (uint32_t)hit | ((uint32_t)(hit && full) << 1);
+    const float det = a * c - b * b;
+    if (HS_RASTER_EXACT_CULL && det > 0.f && a > 0.f && c > 0.f) {
+        // minimum of q(d) = a dx^2 + 2b dx dy + c dy^2 over the rectangle spanned by
+        // those pixel centres (d = centre - mean).  For a positive-definite q the
+        // minimiser is the mean if it lies inside, else on a rectangle edge facing it;
+        // the two candidate segments (x nearest the mean with the best y, and vice
+        // versa) are both inside the rectangle, so their minimum is the exact one.
+        const float dxlo = (float)xs + 0.5f - A.x, dxhi = (float)xe + 0.5f - A.x;
+        const float dylo = (float)ys + 0.5f - A.y, dyhi = (float)ye + 0.5f - A.y;
+        const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
+        const float dyv = fminf(fmaxf(-b * dxv / c, dylo), dyhi);
+        const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
+        const float dxh = fminf(fmaxf(-b * dyh / a, dxlo), dxhi);
+        const float qv = a * dxv * dxv + 2.f * b * dxv * dyv + c * dyv * dyv;
+        const float qh = a * dxh * dxh + 2.f * b * dxh * dyh + c * dyh * dyh;
+        // margin for the fp32 rounding of this bound and of the per-pixel q
+        if (fminf(qv, qh) * 0.999f - 1e-3f > qmax) return 0u;
+    }
+    return 1u | ((uint32_t)full << 1);
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
@@ -446,38 +461,37 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
 #pragma unroll
             for (int k = 0; k < 9; ++k) gv[k] = 0.f;
             bool contrib = false;
+            // branch-free per pixel: a slot failing the reference's tests runs the same
+            // instructions with alpha = G = 0, which leaves t_rev and suffix unchanged
+            // (1 / (1 - 0) == 1 exactly) and adds zeros to the gradients
 #pragma unroll
             for (int p = 0; p < kPX; ++p) {
-                if (jl < stop[p] && inb[p]) {
-                    const float dy = fpy[p] - p0.y;
-                    const float e2 = splat_e2(dx, dy, kadx, p0.w, p1.x);
-                    if (e2 >= p1.y) {
-                        const float G = ex2_approx(e2);
-                        const float alpha = __fmul_rn(p1.z, G);
-                        if (alpha >= kAlphaCutoff) {
-                            contrib = true;
-                            const float inv = __fdividef(1.0f, 1.0f - alpha);
-                            const float t_prior = t_rev[p] * inv;
-                            const float gw = g[p][0] * col.x + g[p][1] * col.y + g[p][2] * col.z;
-                            const float wgt = alpha * t_prior;
-                            gv[6] += wgt * g[p][0];
-                            gv[7] += wgt * g[p][1];
-                            gv[8] += wgt * g[p][2];
-                            const float d_alpha = t_prior * gw - suffix[p] * inv;
-                            gv[5] += G * d_alpha;
-                            const float dq = -0.5f * alpha * d_alpha;
-                            const float dqx = dq * dx, dqy = dq * dy;
-                            gv[2] += dqx * dx;
-                            gv[3] += 2.0f * dqx * dy;
-                            gv[4] += dqy * dy;
-                            // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
-                            gv[0] += kMeanScale * (p0.z * dqx + hb2 * dqy);
-                            gv[1] += kMeanScale * (hb2 * dqx + p1.x * dqy);
-                            suffix[p] += wgt * gw;
-                            t_rev[p] = t_prior;
-                        }
-                    }
-                }
+                const float dy = fpy[p] - p0.y;
+                const float e2 = splat_e2(dx, dy, kadx, p0.w, p1.x);
+                const float G0 = ex2_approx(e2);
+                const float alpha0 = __fmul_rn(p1.z, G0);
+                const bool ok = jl < stop[p] && inb[p] && e2 >= p1.y && alpha0 >= kAlphaCutoff;
+                contrib = contrib || ok;
+                const float G = ok ? G0 : 0.f, alpha = ok ? alpha0 : 0.f;
+                const float inv = __fdividef(1.0f, 1.0f - alpha);
+                const float t_prior = t_rev[p] * inv;
+                const float gw = g[p][0] * col.x + g[p][1] * col.y + g[p][2] * col.z;
+                const float wgt = alpha * t_prior;
+                gv[6] += wgt * g[p][0];
+                gv[7] += wgt * g[p][1];
+                gv[8] += wgt * g[p][2];
+                const float d_alpha = t_prior * gw - suffix[p] * inv;
+                gv[5] += G * d_alpha;
+                const float dq = -0.5f * alpha * d_alpha;
+                const float dqx = dq * dx, dqy = dq * dy;
+                gv[2] += dqx * dx;
+                gv[3] += 2.0f * dqx * dy;
+                gv[4] += dqy * dy;
+                // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
+                gv[0] += kMeanScale * (p0.z * dqx + hb2 * dqy);
+                gv[1] += kMeanScale * (hb2 * dqx + p1.x * dqy);
+                suffix[p] += wgt * gw;
+                t_rev[p] = t_prior;
             }
             if (__any_sync(kFull, contrib)) {
                 int vi;
