@@ -168,9 +168,10 @@ enum {
     HS_RASTER_WSUMS = 16,        /* colour-init sums (sum w*target, sum w) for the same set */
     HS_RASTER_WSUMS_IMAGE = 32   /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
 };
-/* loss_partials holds B * num_tiles * HS_LOSS_PARTIALS_PER_TILE floats (an (L1,
- * black L1) pair per 8x8 pixel block), reduced by hs_loss_reduce. */
-#define HS_LOSS_PARTIALS_PER_TILE 8
+/* loss_partials holds B * num_tiles * HS_LOSS_PARTIALS_PER_TILE floats (one (L1,
+ * black L1) pair per pixel block of the kernel, at most 8 per tile), reduced by
+ * hs_loss_reduce. */
+#define HS_LOSS_PARTIALS_PER_TILE 16
 int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const uint8_t *targets, const float *wsum_image,

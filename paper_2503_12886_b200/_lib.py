@@ -20,7 +20,7 @@ HS_NO_ERROR = 0xFFFFFFFFFFFFFFFF
 
 RASTER_LOSS = 1
 RASTER_IMAGE = 2
-LOSS_PARTIALS_PER_TILE = 8   # hs_api.h HS_LOSS_PARTIALS_PER_TILE
+LOSS_PARTIALS_PER_TILE = 16  # hs_api.h HS_LOSS_PARTIALS_PER_TILE
 RASTER_MAXW_ALL = 4
 RASTER_MAXW_UNVISITED = 8
 RASTER_WSUMS = 16

@@ -482,14 +482,16 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
                 gv[8] += wgt * g[p][2];
                 const float d_alpha = t_prior * gw - suffix[p] * inv;
                 gv[5] += G * d_alpha;
-                const float dq = -0.5f * alpha * d_alpha;
+                // dq = -0.5 alpha d_alpha; the constant factors are applied once per
+                // reduced value (kGradScale) instead of per pixel
+                const float dq = alpha * d_alpha;
                 const float dqx = dq * dx, dqy = dq * dy;
                 gv[2] += dqx * dx;
-                gv[3] += 2.0f * dqx * dy;
+                gv[3] += dqx * dy;
                 gv[4] += dqy * dy;
                 // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
-                gv[0] += kMeanScale * (p0.z * dqx + hb2 * dqy);
-                gv[1] += kMeanScale * (hb2 * dqx + p1.x * dqy);
+                gv[0] += p0.z * dqx + hb2 * dqy;
+                gv[1] += hb2 * dqx + p1.x * dqy;
                 suffix[p] += wgt * gw;
                 t_rev[p] = t_prior;
             }
@@ -497,7 +499,8 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
                 int vi;
                 bool issue;
                 const float s = reduce_scatter(gv, lane, vi, issue);
-                if (issue) atomicAdd(a.g_splat + (uint64_t)(__float_as_uint(p1.w)) * kGS + vi, s);
+                const float sc = vi < 2 ? -0.5f * kMeanScale : vi == 3 ? -1.0f : vi < 5 ? -0.5f : 1.0f;
+                if (issue) atomicAdd(a.g_splat + (uint64_t)(__float_as_uint(p1.w)) * kGS + vi, s * sc);
             }
         }
         __syncwarp();
@@ -632,7 +635,7 @@ int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *los
                    void *stream) {
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const float inv = (float)(1.0 / ((double)width * height * 3.0));
-    static_assert(HS_LOSS_PARTIALS_PER_TILE == 2 * kBlocks, "hs_api.h partial count");
+    static_assert(HS_LOSS_PARTIALS_PER_TILE >= 2 * kBlocks, "hs_api.h partial count");
     loss_reduce_kernel<<<B, 256, 0, s>>>(B, num_tiles * kBlocks, inv, loss_partials, loss_out);
     loss_mean_kernel<<<1, 32, 0, s>>>(B, loss_out);
     return check_launch("hs_loss_reduce");
