@@ -200,6 +200,21 @@ int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *los
 int hs_adam(int64_t N, int K, int64_t mlp_size, float *params, const float *grads,
             float *m, float *v, const float *lrs, int step, float beta1, float beta2,
             float eps, void *stream);
+/* The same update restricted to flat elements [begin, end) -- one call per
+ * allreduce bucket, so the update of bucket i overlaps the reduction of bucket
+ * i+1 -- optionally fused with the colour-init apply that the
+ * reference runs right after Adam (train.py:258-278; moments untouched):
+ *   ci_mode 0: none;
+ *   ci_mode 1: single rank -- hs_color_init semantics from maxw/wsums of B frames;
+ *   ci_mode 2: across ranks -- hs_color_apply semantics from packed/est4 (after
+ *              hs_color_pack/select and their two allreduces).
+ * With ci_mode != 0 a range that touches the base-colour segment [7N, 10N) must
+ * hold all of it.  Vectorised (float4) when N, begin and end are multiples of 4. */
+int hs_adam_fused(int64_t N, int K, int64_t mlp_size, float *params, const float *grads,
+                  float *m, float *v, const float *lrs, int step, float beta1, float beta2,
+                  float eps, int64_t begin, int64_t end, int ci_mode, int B, const float *maxw,
+                  const float *wsums, const int64_t *packed, const float *est4, float threshold,
+                  uint8_t *visited, int *n_init, unsigned long long *err, void *stream);
 
 /* ---- Colour init (train.py:263-278, color_init.py:45-80, model.py:260-263) */
 /* best frame = first argmax_b maxw[b,n]; need = !visited && best > threshold;

@@ -348,34 +348,144 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
 
 // ------------------------------------------------------------------ Adam
 
-// S/optim.py:28-40 over the whole flat parameter buffer; the learning rate of
-// each element comes from its group (S/train.py:184-199).
-__global__ void adam_kernel(int64_t total, int64_t N, int K, float *__restrict__ p,
-                            const float *__restrict__ g, float *__restrict__ m,
-                            float *__restrict__ v, float lr0, float lr1, float lr2, float lr3,
-                            float lr4, float lr5, float lr6, float lr7, float lr8, float b1,
-                            float b2, float inv_bc1, float inv_bc2, float eps) {
-    const int64_t base = 14 * N, dend = base + (int64_t)K * 10 * N;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        float lr;
-        if (i < base) {
-            lr = i < 3 * N ? lr0 : i < 7 * N ? lr1 : i < 10 * N ? lr2 : i < 13 * N ? lr3 : lr4;
-        } else if (i < dend) {
-            int64_t j = (i - base) % (10 * N);
-            lr = j < 3 * N ? lr5 : j < 7 * N ? lr6 : lr7;
+// S/optim.py:28-40, one update of the flat parameter buffer [base | deltas | mlp]:
+// a multi-tensor Adam whose learning rate comes from the element's group
+// (S/train.py:184-199: 5 base groups, 3 delta groups repeated per basis, the MLP).
+// Optionally restricted to [begin, end) so that it can run per allreduce bucket
+// as the buckets arrive, and optionally fused with the colour-init apply
+// (S/train.py:263-278, S/color_init.py:45-80, S/model.py:260-263): colour init
+// runs after Adam in the reference and leaves the moments alone, so the colour
+// segment's threads do the Adam update and then overwrite the parameter.
+struct AdamArgs {
+    int64_t N, begin, end;
+    int K;
+    float *p;
+    const float *g;
+    float *m, *v;
+    float lr[9];
+    float b1, b2, inv_bc1, inv_bc2, eps;
+    // colour init: mode 1 = local frames (maxw/wsums), 2 = reduced across ranks (packed/est4)
+    int B;
+    const float *maxw, *wsums;
+    const int64_t *packed;
+    const float *est4;
+    float thr;
+    uint8_t *visited;
+    int *n_init;
+    unsigned long long *err;
+};
+
+__device__ __forceinline__ float adam_lr(const AdamArgs &a, int64_t i) {
+    const int64_t N = a.N, base = 14 * N, dend = base + (int64_t)a.K * 10 * N;
+    if (i < base) return i < 3 * N ? a.lr[0] : i < 7 * N ? a.lr[1] : i < 10 * N ? a.lr[2] : i < 13 * N ? a.lr[3] : a.lr[4];
+    if (i < dend) {
+        const int64_t j = (i - base) % (10 * N);
+        return j < 3 * N ? a.lr[5] : j < 7 * N ? a.lr[6] : a.lr[7];
+    }
+    return a.lr[8];
+}
+
+__device__ __forceinline__ float adam_one(const AdamArgs &a, float lr, float p, float gi, float &mi, float &vi) {
+    mi = mi * a.b1;
+    mi = mi + (1.0f - a.b1) * gi;
+    vi = vi * a.b2;
+    vi = vi + (1.0f - a.b2) * (gi * gi);
+    const float mh = mi * a.inv_bc1, vh = vi * a.inv_bc2;
+    return p - lr * mh / (sqrtf(vh) + a.eps);
+}
+
+__device__ __forceinline__ float logit_clip(float e) {
+    const float q = fminf(fmaxf(e, 1e-4f), 1.0f - 1e-4f);
+    return logf(q) - log1pf(-q);
+}
+
+template <int CI, bool kVec>
+__global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
+    const int64_t N = a.N, c0 = 7 * N, c1 = 10 * N;      // base colour segment
+    // element ranges of the generic update: [begin, end) minus the colour segment when fused
+    int64_t lo0 = a.begin, hi0 = a.end, lo1 = 0, hi1 = 0;
+    if (CI && a.begin <= c0 && a.end >= c1) {
+        hi0 = c0;
+        lo1 = c1;
+        hi1 = a.end;
+    }
+    constexpr int W = kVec ? 4 : 1;
+    const int64_t n0 = (hi0 - lo0) / W, n1 = (hi1 - lo1) / W;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n0 + n1; t += stride) {
+        const int64_t i = t < n0 ? lo0 + t * W : lo1 + (t - n0) * W;
+        const float lr = adam_lr(a, i);      // group boundaries are multiples of N (N % 4 == 0 when kVec)
+        if constexpr (kVec) {
+            const float4 gv = __ldcs(reinterpret_cast<const float4 *>(a.g + i));
+            float4 mv = __ldcs(reinterpret_cast<const float4 *>(a.m + i));
+            float4 vv = __ldcs(reinterpret_cast<const float4 *>(a.v + i));
+            float4 pv = *reinterpret_cast<const float4 *>(a.p + i);
+            pv.x = adam_one(a, lr, pv.x, gv.x, mv.x, vv.x);
+            pv.y = adam_one(a, lr, pv.y, gv.y, mv.y, vv.y);
+            pv.z = adam_one(a, lr, pv.z, gv.z, mv.z, vv.z);
+            pv.w = adam_one(a, lr, pv.w, gv.w, mv.w, vv.w);
+            __stcs(reinterpret_cast<float4 *>(a.m + i), mv);
+            __stcs(reinterpret_cast<float4 *>(a.v + i), vv);
+            *reinterpret_cast<float4 *>(a.p + i) = pv;
         } else {
-            lr = lr8;
+            float mi = a.m[i], vi = a.v[i];
+            a.p[i] = adam_one(a, lr, a.p[i], a.g[i], mi, vi);
+            a.m[i] = mi;
+            a.v[i] = vi;
         }
-        const float gi = g[i];
-        float mi = m[i] * b1;
-        mi = mi + (1.0f - b1) * gi;
-        float vi = v[i] * b2;
-        vi = vi + (1.0f - b2) * (gi * gi);
-        m[i] = mi;
-        v[i] = vi;
-        const float mh = mi * inv_bc1, vh = vi * inv_bc2;
-        p[i] = p[i] - lr * mh / (sqrtf(vh) + eps);
+    }
+    if (!CI || hi1 == 0) return;
+    // colour segment: one thread per Gaussian (its 3 channels), Adam then colour init
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += stride) {
+        float col[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int64_t i = c0 + 3 * n + c;
+            float mi = a.m[i], vi = a.v[i];
+            col[c] = adam_one(a, a.lr[2], a.p[i], a.g[i], mi, vi);
+            a.m[i] = mi;
+            a.v[i] = vi;
+        }
+        bool init = false;
+        float est[3];
+        if (!a.visited[n]) {
+            if (CI == 1) {
+                int best = 0;
+                float bw = a.maxw[n];
+                for (int b = 1; b < a.B; ++b) {
+                    const float w = a.maxw[(int64_t)b * N + n];
+                    if (w > bw) { bw = w; best = b; }   // first max wins (np.argmax)
+                }
+                if (bw > a.thr) {
+                    const float4 sm = reinterpret_cast<const float4 *>(a.wsums)[(int64_t)best * N + n];
+                    if (sm.w <= 0.f) {
+                        atomicMin(a.err, err_code(2, best, 0, n));
+                    } else {
+                        init = true;
+                        est[0] = sm.x / sm.w;
+                        est[1] = sm.y / sm.w;
+                        est[2] = sm.z / sm.w;
+                    }
+                }
+            } else {
+                const float w = __uint_as_float((uint32_t)((unsigned long long)a.packed[n] >> 32));
+                const float4 e = reinterpret_cast<const float4 *>(a.est4)[n];
+                if (w > a.thr && e.w > 0.f) {
+                    init = true;
+                    est[0] = e.x;
+                    est[1] = e.y;
+                    est[2] = e.z;
+                }
+            }
+        }
+        if (init) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) col[c] = logit_clip(est[c]);
+            a.visited[n] = 1;
+            if (a.n_init) atomicAdd(a.n_init, 1);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) a.p[c0 + 3 * n + c] = col[c];
     }
 }
 
@@ -644,22 +754,82 @@ int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
     return check_launch("hs_blend_bwd");
 }
 
-int hs_adam(int64_t N, int K, int64_t mlp_size, float *params, const float *grads, float *m, float *v,
-            const float *lrs, int step, float beta1, float beta2, float eps, void *stream) {
+int hs_adam_fused(int64_t N, int K, int64_t mlp_size, float *params, const float *grads, float *m, float *v,
+                  const float *lrs, int step, float beta1, float beta2, float eps, int64_t begin, int64_t end,
+                  int ci_mode, int B, const float *maxw, const float *wsums, const int64_t *packed,
+                  const float *est4, float threshold, uint8_t *visited, int *n_init, unsigned long long *err,
+                  void *stream) {
+    const int64_t total = 14 * N + (int64_t)K * 10 * N + mlp_size;
     if (step < 1) {
         set_error("hs_adam: step must be >= 1");
         return HS_ERR_SHAPE;
     }
-    const int64_t total = 14 * N + (int64_t)K * 10 * N + mlp_size;
-    const double bc1 = 1.0 - std::pow((double)beta1, step);
-    const double bc2 = 1.0 - std::pow((double)beta2, step);
+    if (begin < 0 || end > total || begin > end) {
+        set_error("hs_adam: range [%lld, %lld) outside [0, %lld)", (long long)begin, (long long)end,
+                  (long long)total);
+        return HS_ERR_SHAPE;
+    }
+    const int64_t c0 = 7 * N, c1 = 10 * N;
+    const bool has_colour = begin <= c0 && end >= c1;
+    if (ci_mode != 0 && !has_colour && begin < c1 && end > c0) {
+        set_error("hs_adam: a colour-init bucket must hold the whole colour segment [%lld, %lld)", (long long)c0,
+                  (long long)c1);
+        return HS_ERR_SHAPE;
+    }
+    if (ci_mode < 0 || ci_mode > 2 || (ci_mode && has_colour && (!visited || (ci_mode == 1 && (!maxw || !wsums || !err || B < 1)) ||
+                                                                 (ci_mode == 2 && (!packed || !est4))))) {
+        set_error("hs_adam: colour-init mode %d needs a buffer that is NULL", ci_mode);
+        return HS_ERR_SHAPE;
+    }
+    if (end == begin) return HS_OK;
+    AdamArgs a{};
+    a.N = N;
+    a.K = K;
+    a.begin = begin;
+    a.end = end;
+    a.p = params;
+    a.g = grads;
+    a.m = m;
+    a.v = v;
+    for (int i = 0; i < 9; ++i) a.lr[i] = lrs[i];
+    a.b1 = beta1;
+    a.b2 = beta2;
+    a.inv_bc1 = (float)(1.0 / (1.0 - std::pow((double)beta1, step)));
+    a.inv_bc2 = (float)(1.0 / (1.0 - std::pow((double)beta2, step)));
+    a.eps = eps;
+    a.B = B;
+    a.maxw = maxw;
+    a.wsums = wsums;
+    a.packed = packed;
+    a.est4 = est4;
+    a.thr = threshold;
+    a.visited = visited;
+    a.n_init = n_init;
+    a.err = err;
+    const int ci = has_colour ? ci_mode : 0;
+    const bool vec = N % 4 == 0 && begin % 4 == 0 && end % 4 == 0 && (uintptr_t)params % 16 == 0 &&
+                     (uintptr_t)grads % 16 == 0 && (uintptr_t)m % 16 == 0 && (uintptr_t)v % 16 == 0;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    unsigned grid = (unsigned)std::min<int64_t>(grid_for(total, 256), (int64_t)sms * 16);
-    adam_kernel<<<grid, 256, 0, HS_CHECK_STREAM(stream)>>>(
-        total, N, K, params, grads, m, v, lrs[0], lrs[1], lrs[2], lrs[3], lrs[4], lrs[5], lrs[6], lrs[7],
-        lrs[8], beta1, beta2, (float)(1.0 / bc1), (float)(1.0 / bc2), eps);
+    const unsigned grid = (unsigned)std::min<int64_t>(grid_for((end - begin) / (vec ? 4 : 1), 256), (int64_t)sms * 8);
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    if (vec) {
+        if (ci == 0) adam_kernel<0, true><<<grid, 256, 0, s>>>(a);
+        else if (ci == 1) adam_kernel<1, true><<<grid, 256, 0, s>>>(a);
+        else adam_kernel<2, true><<<grid, 256, 0, s>>>(a);
+    } else {
+        if (ci == 0) adam_kernel<0, false><<<grid, 256, 0, s>>>(a);
+        else if (ci == 1) adam_kernel<1, false><<<grid, 256, 0, s>>>(a);
+        else adam_kernel<2, false><<<grid, 256, 0, s>>>(a);
+    }
     return check_launch("hs_adam");
+}
+
+int hs_adam(int64_t N, int K, int64_t mlp_size, float *params, const float *grads, float *m, float *v,
+            const float *lrs, int step, float beta1, float beta2, float eps, void *stream) {
+    const int64_t total = 14 * N + (int64_t)K * 10 * N + mlp_size;
+    return hs_adam_fused(N, K, mlp_size, params, grads, m, v, lrs, step, beta1, beta2, eps, 0, total, 0, 0, nullptr,
+                         nullptr, nullptr, nullptr, 0.f, nullptr, nullptr, nullptr, stream);
 }
 
 int hs_color_init(int B, int64_t N, const float *maxw, const float *wsums, float threshold,

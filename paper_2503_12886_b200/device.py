@@ -331,7 +331,7 @@ class Trainer:
         self.counts = torch.empty(B * N, dtype=torch.int32, device=d)
         self.nblocks = int(L.load().hs_scan_blocks(B * N))
         self.block_sums = torch.empty(self.nblocks, dtype=torch.int32, device=d)
-        self.err = torch.empty(1, dtype=torch.int64, device=d)
+        self.err = torch.full((1,), -1, dtype=torch.int64, device=d)
         self.pix_T = torch.empty(B * self.H * self.W, **f32)
         self.pix_state = torch.empty(B * self.H * self.W, dtype=torch.int32, device=d)
         self.maxw = torch.zeros(B * N, **f32)
@@ -350,6 +350,8 @@ class Trainer:
         self.launches = 0           # libhs_b200 kernel launches issued so far
         self.events = None          # {stage: [(start, end), ...]} when profiling is enabled
         self._ci_done = False
+        self._comm = None
+        self._bucket_events = []
         # host staging for the end-to-end path (pinned)
         self._host = None
 
@@ -389,7 +391,6 @@ class Trainer:
         av = self.av
         N, K, B = av.N, av.K, self.B
         s = _stream()
-        self.err.fill_(-1)
         self._call("mlp_fwd", "hs_mlp_fwd", B, av.H, av.D, K, _p(av.mlp), _p(thetas), _p(self.cache), _p(self.psi),
                    _p(self.err), s)
         self._call("blend_fwd", "hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(self.psi),
@@ -403,6 +404,9 @@ class Trainer:
         total, code = self.binner.scan(self.block_sums, self.nblocks, self.err)
         self._done(m)
         self.launches += 1
+        # the error word also carries a colour-init failure of the previous step's
+        # fused Adam (read here, at the step's one host sync); reset after reading
+        self.err.fill_(-1)
         L.raise_device_error(code, self.frame_offset)
         self.last_total = total
         m = self._mark("bin_sort")
@@ -423,6 +427,7 @@ class Trainer:
         av = self.av
         N, K, B = av.N, av.K, self.B
         cameras = self._cameras(cameras)
+        self._bucket_events = []
         F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras)
         s = _stream()
         ci = self.color_init and not self._all_visited()
@@ -434,6 +439,8 @@ class Trainer:
         self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                    _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
                    _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials), s)
+        if ci and self.pg is not None:
+            self._color_collectives()       # on the comm stream, overlapping the backward
         self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
                    _p(self.loss_out), s, kernels=2)
         # backward: d loss_b / d pred = sign / (H W 3) / B_global  (S/metrics.py:19-22, S/train.py:244)
@@ -448,22 +455,65 @@ class Trainer:
         self._call("blend_bwd", "hs_blend_bwd", N, K, B, _p(av.deltas), _p(self.psi), _p(self.g_raw14),
                    _p(self.grads), _p(self.grads[14 * N:]), _p(self.gpsi_partials), ctypes.byref(nparts), s,
                    kernels=(B + 15) // 16)
+        buckets = self.buckets()
+        if self.pg is not None:           # base + delta buckets reduce while mlp_bwd runs
+            self._allreduce_buckets(buckets[:-1])
         self._call("mlp_bwd", "hs_mlp_bwd", B, av.H, av.D, K, _p(av.mlp), _p(thetas), _p(self.cache),
                    _p(self.gpsi_partials), nparts.value, _p(self.gpsi), _p(self.mlp_scratch),
                    _p(self.grads[14 * N + 10 * K * N:]), s, kernels=2)
         if self.pg is not None:
-            import torch.distributed as dist
-            m = self._mark("allreduce")
-            dist.all_reduce(self.grads, op=dist.ReduceOp.SUM, group=self.pg)
-            self._done(m)
+            self._allreduce_buckets(buckets[-1:])
         self.step_count += 1
-        self._call("adam", "hs_adam", N, K, av.mlp_size, _p(av.params), _p(self.grads), _p(self.m), _p(self.v),
-                   self.lrs, self.step_count, ADAM_BETAS[0], ADAM_BETAS[1], ADAM_EPS, s)
-        if ci:
-            m = self._mark("color_init")
-            self._color_init()
-            self._done(m)
+        # multi-tensor Adam per bucket (each waits only for its own reduction), colour
+        # init fused into the bucket holding the base colours
+        ci_mode = (2 if self.pg is not None else 1) if ci else 0
+        m = self._mark("adam")
+        for i, (lo, hi) in enumerate(buckets):
+            if self.pg is not None:
+                s_cur = torch.cuda.current_stream()
+                s_cur.wait_event(self._bucket_events[i])
+            L.call("hs_adam_fused", N, K, av.mlp_size, _p(av.params), _p(self.grads), _p(self.m), _p(self.v),
+                   self.lrs, self.step_count, ADAM_BETAS[0], ADAM_BETAS[1], ADAM_EPS, lo, hi, ci_mode, B,
+                   _p(self.maxw), _p(self.wsums), _p(self.packed), _p(self.est4), ctypes.c_float(self.threshold),
+                   _p(self.visited), _p(self.n_init), _p(self.err), s)
+            self.launches += 1
+        self._done(m)
         return self.loss_out
+
+    def buckets(self):
+        """Flat-gradient buckets [lo, hi): the base block (holds the colour segment
+        that colour init writes), the deltas in 4 basis groups, then the MLP (which
+        is produced last, by mlp_bwd).  Boundaries are multiples of N (float4 Adam)."""
+        av = self.av
+        N, K = av.N, av.K
+        out = [(0, 14 * N)]
+        per = max(1, -(-K // 4))
+        for k0 in range(0, K, per):
+            out.append((14 * N + 10 * N * k0, 14 * N + 10 * N * min(K, k0 + per)))
+        out.append((14 * N + 10 * K * N, av.size))
+        return out
+
+    def _comm_stream(self):
+        if self._comm is None:
+            self._comm = torch.cuda.Stream(device=self.av.device)
+        return self._comm
+
+    def _allreduce_buckets(self, buckets):
+        """Allreduce-sum each bucket on the comm stream after the work enqueued so far
+        on the compute stream; records one event per bucket for its Adam launch."""
+        import torch.distributed as dist
+        comm = self._comm_stream()
+        ready = torch.cuda.Event()
+        ready.record()
+        m = self._mark("allreduce")
+        with torch.cuda.stream(comm):
+            comm.wait_event(ready)
+            for lo, hi in buckets:
+                dist.all_reduce(self.grads[lo:hi], op=dist.ReduceOp.SUM, group=self.pg)
+                ev = torch.cuda.Event()
+                ev.record(comm)
+                self._bucket_events.append(ev)
+        self._done(m)
 
     def result(self) -> StepResult:
         """Host copy of the last step's losses (a device->host read)."""
@@ -480,23 +530,26 @@ class Trainer:
         self._ci_done = bool(self.visited.bool().all().item())
         return self._ci_done
 
-    def _color_init(self):
-        av = self.av
-        s = _stream()
-        if self.pg is None:
-            L.call("hs_color_init", self.B, av.N, _p(self.maxw), _p(self.wsums), ctypes.c_float(self.threshold),
-                   _p(self.visited), _p(av.params), _p(self.n_init), _p(self.err), s)
-            self.launches += 1
-            return
-        self.launches += 3
+    def _color_collectives(self):
+        """Multi-GPU colour-init exchange on the comm stream right after
+        the forward raster: pack -> allreduce-MAX -> select -> allreduce-SUM.  The
+        apply is fused into the Adam launch of the base bucket."""
         import torch.distributed as dist
-        L.call("hs_color_pack", self.B, av.N, self.frame_offset, _p(self.maxw), _p(self.visited), _p(self.packed), s)
-        dist.all_reduce(self.packed, op=dist.ReduceOp.MAX, group=self.pg)
-        L.call("hs_color_select", self.B, av.N, self.frame_offset, _p(self.packed), _p(self.wsums), _p(self.est4),
-               _p(self.err), s)
-        dist.all_reduce(self.est4, op=dist.ReduceOp.SUM, group=self.pg)
-        L.call("hs_color_apply", av.N, _p(self.packed), _p(self.est4), ctypes.c_float(self.threshold),
-               _p(self.visited), _p(av.params), _p(self.n_init), s)
+        av = self.av
+        comm = self._comm_stream()
+        ready = torch.cuda.Event()
+        ready.record()
+        with torch.cuda.stream(comm):
+            comm.wait_event(ready)
+            cs = ctypes.c_void_p(comm.cuda_stream)
+            L.call("hs_color_pack", self.B, av.N, self.frame_offset, _p(self.maxw), _p(self.visited),
+                   _p(self.packed), cs)
+            dist.all_reduce(self.packed, op=dist.ReduceOp.MAX, group=self.pg)
+            L.call("hs_color_select", self.B, av.N, self.frame_offset, _p(self.packed), _p(self.wsums),
+                   _p(self.est4), _p(self.err), cs)
+            dist.all_reduce(self.est4, op=dist.ReduceOp.SUM, group=self.pg)
+        self.launches += 2
+
 
     # ------------------------------------------------------------------ render
     def render(self, thetas, frames, cameras, backgrounds, out=None):
