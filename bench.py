@@ -6,7 +6,8 @@
 Workload (BASELINE.json configs[1], "paper default"): synthetic head avatar,
 20 blendshapes, 50,176 Gaussians (UV 224), 512x512, batch 16 frames per GPU,
 random-init weights perturbed per SURVEY §8d, synthetic u8 RGBA targets.  A step
-is one full ``train_step`` (S/train.py:214-260): MLP, blend, projection, tile
+is one full ``train_step`` (S/train.py:214-260): mesh frames from theta (device
+rig), MLP, blend, projection, tile
 binning + radix sort (one host sync), forward compositing with the fused L1
 loss, the full adjoint chain, the gradient reduction (NCCL allreduce for N>1),
 the multi-group Adam update and the colour-initialisation estimate.
@@ -115,6 +116,7 @@ def stage_bytes(B, N, K, H, D, W, Hh, keys, params, color_init=True, passes=6):
     out = {
         "mlp_fwd": 4 * (H * D + D * D + K * D + B * (H + 4 * D + K)),
         "blend_fwd": 4 * (10 * N * K + 10 * N + B * 10 * N),
+        "rig_frames": B * 1024 * 22 * 4 + 561 * 11 * 3 * 8,
         "project_fwd": B * N * (40 + rec + 4 + 4) + N * 32 + B * 1024 * 22 * 4,
         "bin_sort": keys * (12 + 8 + passes * 24 + 8),   # emit, histogram, passes, ranges
         "raster_fwd": keys * (4 + rec) + B * HW * (4 + 4 + 4) + (B * N * 20 if color_init else 0),
@@ -138,14 +140,16 @@ CONFIGS = {
 def make_trainer(cfg, rank=0, world=1, pg=None):
     import torch
     from paper_2503_12886_b200 import synth
-    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     wl = synth.make_workload(cfg["uv"], cfg["batch"], cfg["size"], distinct_frames=min(cfg["batch"], 8),
                              frames_seed=1 + rank)
     av = wl.avatar
     dev = AvatarParams.from_host(type("G", (), {a: av.base[a] for a in av.base})(), av.deltas, av.mlp,
                                  av.tri_index, av.barycentric)
     B = cfg["batch"]
-    tr = Trainer(dev, cfg["size"], cfg["size"], B, process_group=pg, global_batch=B * world, frame_offset=B * rank)
+    # mesh frames come from theta on the device (hs_rig_frames) inside every step
+    tr = Trainer(dev, cfg["size"], cfg["size"], B, process_group=pg, global_batch=B * world, frame_offset=B * rank,
+                 rig=DeviceRig(wl.rig))
     d = {
         "thetas": torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda(),
         "targets": torch.from_numpy(wl.targets).cuda(),
@@ -242,7 +246,7 @@ def run_b200(args, cfg):
         torch.cuda.synchronize()
 
     def step():
-        tr.step(d["thetas"], d["targets"], d["frames"], d["cameras"], d["backgrounds"])
+        tr.step(d["thetas"], d["targets"], None, d["cameras"], d["backgrounds"])
 
     clocks = ClockSampler(dev_index)
     clocks.start()                      # sampled through warm-up + timed region (>= 1 s of load)
@@ -276,14 +280,14 @@ def run_b200(args, cfg):
     # ---- end-to-end through the host API (pinned H2D inputs, D2H losses) every step
     h = {k: v.cpu().numpy() for k, v in d.items()}
     for _ in range(2):
-        tr.step_from_host(h["thetas"], h["targets"], h["frames"], h["cameras"], h["backgrounds"])
+        tr.step_from_host(h["thetas"], h["targets"], None, h["cameras"], h["backgrounds"])
     barrier()
     e2e_ms = 0.0
     for _ in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        tr.step_from_host(h["thetas"], h["targets"], h["frames"], h["cameras"], h["backgrounds"])
+        tr.step_from_host(h["thetas"], h["targets"], None, h["cameras"], h["backgrounds"])
         e2e_ms += (time.perf_counter() - t0) * 1000.0
     t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -315,7 +319,8 @@ def run_b200(args, cfg):
                        "frames_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world}",
                        "l2": "256 MiB buffer written between timed steps (outside the CUDA events); "
                              "per-step working set ~0.4 GB also exceeds L2",
-                       "keys_per_step": tr.last_total, "colour_init": "active (unvisited Gaussians)"},
+                       "keys_per_step": tr.last_total, "colour_init": "active (unvisited Gaussians)",
+                       "mesh_frames": "computed from theta on the device every step (hs_rig_frames)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
@@ -326,7 +331,7 @@ def run_b200(args, cfg):
                               "frac": step_bytes / (ms / 1000.0) / 1e9 / peak},
             "stages_ms": {k: round(v, 4) for k, v in per_step.items()},
             "clocks": clk,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": tr.h2d_bytes(F),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": tr.h2d_bytes(F, frames=False),
                     "d2h_bytes_per_step": tr.d2h_bytes()},
             "gpu_launches": launches,
         }
@@ -359,14 +364,14 @@ def render_fps(args):
     """Render-only FPS (BASELINE configs[2]: 100,489 Gaussians, 512^2, batch 64), device-resident."""
     import torch
     from paper_2503_12886_b200 import synth
-    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     wl = synth.make_workload(317, 64, 512, distinct_frames=8)
     av = wl.avatar
     dev = AvatarParams.from_host(type("G", (), {a: av.base[a] for a in av.base})(), av.deltas, av.mlp,
                                  av.tri_index, av.barycentric)
-    tr = Trainer(dev, 512, 512, 64, color_init=False)
+    tr = Trainer(dev, 512, 512, 64, color_init=False, rig=DeviceRig(wl.rig))
     th = torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda()
-    fr = torch.from_numpy(wl.frames).cuda()
+    fr = None                                   # mesh frames from theta on the device (unseen theta)
     cams = torch.from_numpy(np.tile(wl.camera.packed(), (64, 1))).cuda()
     bg = torch.zeros(64, 3, device="cuda")
     out = torch.empty(64, 512, 512, 3, device="cuda")
@@ -381,7 +386,8 @@ def render_fps(args):
     e.record()
     e.synchronize()
     ms = s.elapsed_time(e) / reps
-    return {"metric": "render FPS (MLP + blend + transform + project + bin/sort + composite)", "value": 64 / (ms / 1000.0),
+    return {"metric": "render FPS (rig + MLP + blend + transform + project + bin/sort + composite)",
+            "value": 64 / (ms / 1000.0),
             "unit": "frames/s", "ms_per_batch": ms, "config": "20 bases, 100,489 Gaussians, 512x512, batch 64",
             "keys_per_batch": tr.last_total}
 

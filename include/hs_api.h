@@ -68,7 +68,9 @@ enum {
  *   bits 40-61 frame, bits 32-39 attribute, bits 0-31 Gaussian index
  * stage 0 attributes: 0 non-finite theta (model.py:135-136), 1 zero-norm quat (model.py:224-227)
  * stage 1 attributes: 0 position, 1 rotation, 2 scale, 3 opacity, 4 color (render.py:204-208)
- * stage 2 attribute 0: colour-init eligibility inconsistency (color_init.py:59-63) */
+ * stage 2 attribute 0: colour-init eligibility inconsistency (color_init.py:59-63)
+ * stage 3 attributes: 0 degenerate UV triangle, 1 degenerate 3D triangle (binding.py:104-109);
+ *         the index field holds the face */
 #define HS_NO_ERROR 0xFFFFFFFFFFFFFFFFull
 
 const char *hs_last_error(void);
@@ -236,6 +238,20 @@ int hs_color_select(int B, int64_t N, int frame_offset, const int64_t *packed, c
                     float *est4, unsigned long long *err, void *stream);
 int hs_color_apply(int64_t N, const int64_t *packed, const float *est4, float threshold,
                    uint8_t *visited, float *params, int *n_init, void *stream);
+
+/* ---- Device rig + tangent frames -------------------------
+ * rig.py:57-66 rig_evaluate, quatmath.py:152-161 axis_angle_to_matrix,
+ * binding.py:67-115 mesh_frames (_tbn_batch, polar_rotation), quatmath.py:105-149
+ * matrix_to_quat.  frames[B][F][22] fp32 = [TBN 3x3 row-major (columns T, B, N) |
+ * quaternion of its polar rotation factor (wxyz, unnormalised) | triangle
+ * vertices 3x3], the layout hs_project_avatar_fwd reads.  Rig data in fp64
+ * (base_vertices V x 3, expr_bases E x V x 3, uv_coords V x 2), faces int32 F x 3,
+ * theta B x (E + 3) fp32 (expressions, then the axis-angle pose).  With
+ * `vertices` (B x V x 3 fp64) non-NULL, theta is ignored and only mesh_frames
+ * runs.  Degenerate triangles set a stage-3 error code in *err (face index). */
+int hs_rig_frames(int B, int V, int F, int E, const double *base_vertices, const double *expr_bases,
+                  const int32_t *faces, const double *uv_coords, const float *theta,
+                  const double *vertices, float *frames, unsigned long long *err, void *stream);
 
 /* ---- Elementwise compat ops (model.py:219-248, binding.py:174-204) ------- */
 int hs_activate_fwd(int64_t N, const float *raw14, float *act14, unsigned long long *err, void *stream);

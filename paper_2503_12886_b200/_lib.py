@@ -58,6 +58,7 @@ SIGNATURES = {
     "hs_loss_reduce": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "hs_raster_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_adam": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _P]),
+    "hs_rig_frames": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_adam_fused": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _L, _L, _I, _I, _P, _P,
                            _P, _P, _F, _P, _P, _P, _P]),
     "hs_color_init": (_I, [_I, _L, _P, _P, _F, _P, _P, _P, _P, _P]),
@@ -123,6 +124,10 @@ def call(name: str, *args):
 ATTR_NAMES = ("position", "rotation", "scale", "opacity", "color")
 
 
+class DegenerateTriangleError(ValueError):
+    """S/binding.py:21-22."""
+
+
 def raise_device_error(code: int, item_base: int = 0):
     """Map the device error word (hs_api.h) to the reference's exception."""
     if code == HS_NO_ERROR:
@@ -137,5 +142,7 @@ def raise_device_error(code: int, item_base: int = 0):
         raise FloatingPointError(f"zero-norm quaternion at Gaussian index {n}")    # S/model.py:226-227
     if stage == 1:
         raise FloatingPointError(f"non-finite {ATTR_NAMES[attr]} at Gaussian index {n}")  # S/render.py:208
+    if stage == 3:                                                                 # S/binding.py:104-109
+        raise DegenerateTriangleError(f"degenerate {'UV' if attr == 0 else '3D'} triangle at face {n}")
     raise RuntimeError(f"Gaussian {n} exceeds the weight threshold but accumulated zero total weight "
                        f"(frame {frame + item_base})")                             # S/color_init.py:59-63

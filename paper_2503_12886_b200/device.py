@@ -9,10 +9,11 @@ between the projection and rasterization stages (PAPER.md:156,
 S/scheduler.py:64-72).
 
 Step (N Gaussians, K bases, B frames):
-  mlp_fwd -> blend_fwd -> project_avatar_fwd (+ tile counts) -> bin_scan -> [sync]
+  [rig_frames: theta -> mesh frames, when the Trainer holds a DeviceRig]
+  -> mlp_fwd -> blend_fwd -> project_avatar_fwd (+ tile counts) -> bin_scan -> [sync]
   -> bin_emit -> sort_pairs -> tile_ranges -> raster_fwd (+ L1 loss, colour-init
   sums) -> loss_reduce -> raster_bwd -> project_avatar_bwd -> blend_bwd -> mlp_bwd
-  -> [allreduce of the flat gradient, multi-GPU] -> adam -> colour init.
+  -> [bucketed allreduce of the flat gradient, multi-GPU] -> Adam + colour init.
 """
 
 from __future__ import annotations
@@ -189,6 +190,54 @@ def split_flat(flat, N, K, H, D):
 
 # -------------------------------------------------------------------- binning
 
+class DeviceRig:
+    """Device copy of the head rig (S/rig.py:18-54 ParametricHeadRig) that turns
+    rig parameters into mesh frames on the GPU (hs_rig_frames):
+    rig_evaluate (S/rig.py:57-66) + mesh_frames (S/binding.py:67-115).
+
+    ``rig`` is any object with base_vertices (V,3), faces (F,3), uv_coords (V,2) and
+    expr_bases (E,V,3) -- the reference's rig or synth.HeadRig."""
+
+    def __init__(self, rig, device="cuda"):
+        require_cuda()
+        f64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(device)
+        self.base = f64(rig.base_vertices)
+        self.bases = f64(rig.expr_bases)
+        self.uv = f64(rig.uv_coords)
+        self.faces = torch.from_numpy(np.ascontiguousarray(rig.faces, np.int32)).to(device)
+        self.V, self.F, self.E = self.base.shape[0], self.faces.shape[0], self.bases.shape[0]
+        if self.bases.shape[1:] != (self.V, 3) or self.uv.shape != (self.V, 2):
+            raise ValueError("rig arrays have inconsistent shapes")
+        self.err = torch.full((1,), -1, dtype=torch.int64, device=device)
+        self.device = device
+
+    @property
+    def param_dim(self):
+        return self.E + 3
+
+    def frames(self, thetas=None, vertices=None, out=None, err=None):
+        """(B, F, 22) fp32 frames of thetas (B, E+3) fp32 or of vertices (B, V, 3) fp64.
+        With err=None the call checks the error word (a host sync) and raises the
+        reference's DegenerateTriangleError; with a caller err word it is async."""
+        src = thetas if vertices is None else vertices
+        if src is None:
+            raise ValueError("need thetas or vertices")
+        B = src.shape[0]
+        if vertices is None and thetas.shape[-1] != self.param_dim:
+            raise ValueError(f"theta has shape {tuple(thetas.shape)}, rig expects (B, {self.param_dim})")
+        if out is None:
+            out = torch.empty(B, self.F, 22, dtype=torch.float32, device=self.device)
+        check = err is None
+        if check:
+            err = self.err
+            err.fill_(-1)
+        L.call("hs_rig_frames", B, self.V, self.F, self.E, _p(self.base), _p(self.bases), _p(self.faces),
+               _p(self.uv), _p(thetas), _p(vertices), _p(out), _p(err), _stream())
+        if check:
+            L.raise_device_error(int(err.item()) & 0xFFFFFFFFFFFFFFFF)
+        return out
+
+
 class Binner:
     """Batched tile binning shared by training, rendering and the compat path:
     project-stage outputs -> (keys, values, ranges) with one host read."""
@@ -300,9 +349,10 @@ class Trainer:
     """
 
     def __init__(self, avatar: AvatarParams, width, height, batch, lrs=None, color_init=True, threshold=0.1,
-                 process_group=None, global_batch=None, frame_offset=0):
+                 process_group=None, global_batch=None, frame_offset=0, rig: DeviceRig = None):
         require_cuda()
         self.av = avatar
+        self.rig = rig              # DeviceRig: frames computed from theta on device
         self.W, self.H = int(width), int(height)
         self.B = int(batch)
         self.global_batch = int(global_batch or batch)
@@ -352,8 +402,14 @@ class Trainer:
         self._ci_done = False
         self._comm = None
         self._bucket_events = []
+        self._rig_frames = None
+        self._last_frames = None
+        self._copy = None               # H2D copy stream of step_from_host
+        self._targets_ready = None
+        self._registered = {}           # page-locked caller arrays
+        self._staging = {}
+        self._dev_in = {}
         # host staging for the end-to-end path (pinned)
-        self._host = None
 
     # --------------------------------------------------------------- profiling
     def enable_profiling(self, on=True):
@@ -387,10 +443,24 @@ class Trainer:
         self.launches += kernels
 
     # ------------------------------------------------------------------ forward
+    def _frames(self, thetas, frames):
+        if frames is not None:
+            return frames
+        if self.rig is None:
+            raise ValueError("frames is None and the Trainer has no DeviceRig")
+        if self._rig_frames is None:
+            self._rig_frames = torch.empty(self.B, self.rig.F, 22, dtype=torch.float32, device=self.av.device)
+        m = self._mark("rig_frames")
+        self.rig.frames(thetas, out=self._rig_frames, err=self.err)     # errors surface at the scan read
+        self._done(m)
+        self.launches += 1
+        return self._rig_frames
+
     def _forward_project(self, thetas, frames, cameras):
         av = self.av
         N, K, B = av.N, av.K, self.B
         s = _stream()
+        frames = self._frames(thetas, frames)
         self._call("mlp_fwd", "hs_mlp_fwd", B, av.H, av.D, K, _p(av.mlp), _p(thetas), _p(self.cache), _p(self.psi),
                    _p(self.err), s)
         self._call("blend_fwd", "hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(self.psi),
@@ -409,6 +479,7 @@ class Trainer:
         self.err.fill_(-1)
         L.raise_device_error(code, self.frame_offset)
         self.last_total = total
+        self._last_frames = frames
         m = self._mark("bin_sort")
         res = self.binner.bin(B, N, self.W, self.H, self.records, self.depth, self.counts, total)
         self._done(m)
@@ -422,13 +493,15 @@ class Trainer:
 
     # --------------------------------------------------------------------- step
     def step(self, thetas, targets, frames, cameras, backgrounds) -> StepResult:
-        """thetas (B,H) f32, targets (B,H,W,4) u8 straight RGBA, frames (B,F,22) f32,
+        """thetas (B,H) f32, targets (B,H,W,4) u8 straight RGBA, frames (B,F,22) f32
+        (or None: computed from thetas by the Trainer's DeviceRig),
         cameras (B,16) or (16,) f32, backgrounds (B,3) f32 -- all on the device."""
         av = self.av
         N, K, B = av.N, av.K, self.B
         cameras = self._cameras(cameras)
         self._bucket_events = []
         F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras)
+        frames = self._last_frames
         s = _stream()
         ci = self.color_init and not self._all_visited()
         flags = L.RASTER_LOSS
@@ -436,6 +509,9 @@ class Trainer:
             flags |= L.RASTER_MAXW_UNVISITED | L.RASTER_WSUMS
             self.maxw.zero_()
             self.wsums.zero_()
+        if self._targets_ready is not None:     # step_from_host: targets arrive on the copy stream
+            torch.cuda.current_stream().wait_event(self._targets_ready)
+            self._targets_ready = None
         self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                    _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
                    _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials), s)
@@ -566,32 +642,94 @@ class Trainer:
         return out
 
     # -------------------------------------------------------------- end to end
+    def _host_view(self, name, arr, dtype):
+        """A CPU tensor over the caller's host array that the GPU can DMA from.
+
+        Conforming arrays (C-contiguous, right dtype) are page-locked in place once
+        (cudaHostRegister) and cached by address, so a caller cycling through a few
+        frame buffers pays no host copy per step; anything else is copied into a
+        pinned staging buffer."""
+        a = np.asarray(arr)
+        if a.dtype == dtype and a.flags.c_contiguous and a.nbytes >= (1 << 16):
+            key = (a.__array_interface__["data"][0], a.nbytes)
+            hit = self._registered.get(key)
+            if hit is None:
+                t = torch.from_numpy(a)
+                rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), a.nbytes, 0)
+                if int(rc) == 0:
+                    if len(self._registered) >= 32:          # bounded: drop the oldest
+                        old_key, (old_a, old_t) = next(iter(self._registered.items()))
+                        torch.cuda.synchronize()
+                        torch.cuda.cudart().cudaHostUnregister(old_t.data_ptr())
+                        del self._registered[old_key]
+                    hit = self._registered[key] = (a, t)     # keeps the array alive
+            if hit is not None:
+                return hit[1]
+        a = np.ascontiguousarray(a, dtype)
+        st = self._staging.get(name)
+        if st is None or st.shape != a.shape:
+            st = self._staging[name] = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+        st.numpy()[...] = a
+        return st
+
+    def _device_buf(self, name, host):
+        d = self._dev_in.get(name)
+        if d is None or d.shape != host.shape or d.dtype != host.dtype:
+            d = self._dev_in[name] = torch.empty(host.shape, dtype=host.dtype, device=self.av.device)
+        return d
+
     def step_from_host(self, thetas, targets, frames, cameras, backgrounds):
-        """End-to-end step through host buffers (numpy): pinned staging, H2D copies,
-        the device step, and the D2H read of the losses.  Returns StepResult."""
-        arrays = {"thetas": np.asarray(thetas, np.float32), "targets": np.asarray(targets, np.uint8),
-                  "frames": np.asarray(frames, np.float32), "cameras": np.asarray(cameras, np.float32),
-                  "backgrounds": np.asarray(backgrounds, np.float32)}
-        if self._host is None or any(self._host[k][0].shape != v.shape for k, v in arrays.items()):
-            self._host = {k: (torch.empty(v.shape, dtype=torch.from_numpy(v).dtype, pin_memory=True),
-                              torch.empty(v.shape, dtype=torch.from_numpy(v).dtype, device=self.av.device))
-                          for k, v in arrays.items()}
+        """End-to-end step through host buffers (numpy): H2D copies, the device step
+        and the D2H read of the losses.  Returns StepResult.
+
+        The small inputs go first on the compute stream; the targets (the bulk of the
+        bytes) go on a copy stream and only the forward raster waits for them, so
+        their transfer overlaps the MLP, blend, projection and sort.  frames may be
+        None when the Trainer holds a DeviceRig (mesh frames computed from theta)."""
+        if self._copy is None:
+            self._copy = torch.cuda.Stream(device=self.av.device)
             self._loss_host = torch.empty(2 * self.B + 1, dtype=torch.float32, pin_memory=True)
+        small = {"thetas": (thetas, np.float32), "cameras": (cameras, np.float32),
+                 "backgrounds": (backgrounds, np.float32)}
+        if frames is not None:
+            small["frames"] = (frames, np.float32)
         dev = {}
-        for k, v in arrays.items():
-            h, d = self._host[k]
-            h.numpy()[...] = v
+        for k, (v, dt) in small.items():
+            h = self._host_view(k, v, dt)
+            d = self._device_buf(k, h)
             d.copy_(h, non_blocking=True)
             dev[k] = d
-        self.step(dev["thetas"], dev["targets"], dev["frames"], dev["cameras"], dev["backgrounds"])
+        h = self._host_view("targets", targets, np.uint8)
+        d = self._device_buf("targets", h)
+        self._copy.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self._copy):
+            d.copy_(h, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self._copy)
+        self._targets_ready = ready
+        self.step(dev["thetas"], d, dev.get("frames"), dev["cameras"], dev["backgrounds"])
         self._loss_host.copy_(self.loss_out, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         lo = self._loss_host.numpy()
         B = self.B
         return StepResult(float(lo[2 * B]), lo[B:2 * B].copy(), lo[:B].copy(), self.last_total)
 
-    def h2d_bytes(self, F):
-        return self.B * (self.av.H * 4 + self.H * self.W * 4 + F * 22 * 4 + 16 * 4 + 3 * 4)
+    def close(self):
+        """Unregister the page-locked caller arrays of step_from_host."""
+        if self._registered:
+            torch.cuda.synchronize()
+            for a, t in self._registered.values():
+                torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
+            self._registered.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def h2d_bytes(self, F, frames=True):
+        return self.B * (self.av.H * 4 + self.H * self.W * 4 + (F * 22 * 4 if frames else 0) + 16 * 4 + 3 * 4)
 
     def d2h_bytes(self):
         return (2 * self.B + 1) * 4

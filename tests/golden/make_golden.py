@@ -21,6 +21,8 @@ Fixtures (all float64 unless stated):
   train.npz    two reference train_step calls on a tiny synthetic avatar with the
                summed ParamGradients captured at Optimizer.step (S/train.py:214-278)
   counts.json  bind_gaussians counts at uv 141/224/317
+  rig.npz      rig_evaluate + mesh_frames on a theta batch, DegenerateTriangleError
+               messages                                    (S/rig.py:57-66, S/binding.py:67-115)
 """
 
 from __future__ import annotations
@@ -286,16 +288,70 @@ def make_train(out):
     out["train"] = d
 
 
+def make_rig(out):
+    """rig.npz: rig_evaluate + mesh_frames for a batch of theta (incl. a zero pose,
+    which takes the identity branch of axis_angle_to_matrix, and a large pose), and
+    the DegenerateTriangleError messages of a collapsed UV and a collapsed 3D face."""
+    from headsplat.binding import DegenerateTriangleError, mesh_frames
+    from headsplat.rig import ParametricHeadRig, build_head_rig, rig_evaluate
+    rig = build_head_rig()
+    rng = np.random.default_rng(9)
+    th = rng.normal(0.0, 0.3, (5, rig.param_dim))
+    th[1, -3:] = 0.0                                     # identity pose
+    th[2, -3:] = [2.5, -1.0, 0.7]                        # large rotation
+    th[3, :-3] *= 4.0                                    # strong expressions
+    verts = np.stack([rig_evaluate(rig, t) for t in th])
+    frames = [mesh_frames(rig, v) for v in verts]
+    d = {"theta": th, "verts": verts,
+         "frames.rotation": np.stack([f.rotation for f in frames]),
+         "frames.quat": np.stack([f.quat for f in frames]),
+         "frames.tri_vertices": np.stack([f.tri_vertices for f in frames])}
+    # degenerate UV: give vertex faces[37][1] the UV of faces[37][0]
+    uv = rig.uv_coords.copy()
+    f37 = rig.faces[37]
+    uv[f37[1]] = uv[f37[0]]
+    bad = ParametricHeadRig(rig.base_vertices, rig.faces, uv, rig.expr_bases)
+    try:
+        mesh_frames(bad, rig_evaluate(bad, th[0]))
+        msg = ""
+    except DegenerateTriangleError as e:
+        msg = str(e)
+    d["bad_uv.uv_coords"], d["bad_uv.message"] = uv, np.array(msg)
+    # degenerate 3D: collapse the vertices of face 300 onto one point
+    v3 = rig.base_vertices.copy()
+    eb = rig.expr_bases.copy()
+    f300 = rig.faces[300]
+    v3[f300[1]] = v3[f300[2]] = v3[f300[0]]
+    eb[:, f300[1]] = eb[:, f300[2]] = eb[:, f300[0]]
+    bad3 = ParametricHeadRig(v3, rig.faces, rig.uv_coords, eb)
+    try:
+        mesh_frames(bad3, rig_evaluate(bad3, th[0]))
+        msg = ""
+    except DegenerateTriangleError as e:
+        msg = str(e)
+    d["bad_3d.base_vertices"], d["bad_3d.expr_bases"], d["bad_3d.message"] = v3, eb, np.array(msg)
+    out["rig"] = d
+
+
 def main():
     hs = _ref()
     import numba
     out = {}
+    only = set(sys.argv[1:])            # e.g. `make_golden.py rig` regenerates rig.npz only
+    if only:
+        for name in only:
+            globals()[f"make_{name}"](out)
+        for name, d in out.items():
+            np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+            print(name, os.path.getsize(os.path.join(HERE, f"{name}.npz")))
+        return
     counts = {"numpy": np.__version__, "numba": numba.__version__, "headsplat": getattr(hs, "__version__", "0.1.0")}
     make_model(out)
     make_binding(out, counts)
     make_render(out)
     make_color(out)
     make_train(out)
+    make_rig(out)
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     with open(os.path.join(HERE, "counts.json"), "w") as f:

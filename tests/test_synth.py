@@ -47,3 +47,17 @@ def test_init_avatar_matches_reference_train_fixture():
     np.testing.assert_array_equal(av.base["scale"], d["base0.scale"])
     for k in ("w1", "w2", "b1"):
         np.testing.assert_array_equal(av.mlp[k], d["mlp0." + k])
+
+
+def test_rig_batch_matches_reference():
+    """rig.npz: identity pose, large rotation and strong expressions (S/rig.py:57-66,
+    S/binding.py:67-115) -- the restatement the device rig is also checked against."""
+    d = golden("rig")
+    rig = synth.build_head_rig()
+    for b, th in enumerate(d["theta"]):
+        v = synth.rig_evaluate(rig, th)
+        np.testing.assert_allclose(v, d["verts"][b], rtol=0, atol=1e-13)
+        mf = synth.mesh_frames(rig, v)
+        np.testing.assert_allclose(mf.rotation, d["frames.rotation"][b], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(mf.quat, d["frames.quat"][b], rtol=0, atol=1e-11)
+        np.testing.assert_allclose(mf.tri_vertices, d["frames.tri_vertices"][b], rtol=0, atol=1e-13)
