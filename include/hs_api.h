@@ -253,6 +253,13 @@ int hs_rig_frames(int B, int V, int F, int E, const double *base_vertices, const
                   const int32_t *faces, const double *uv_coords, const float *theta,
                   const double *vertices, float *frames, unsigned long long *err, void *stream);
 
+/* ---- Device frame pool (stream.py:27-86) -------------------
+ * out[r] = pool[slots[r]] for num_rows rows of row_bytes bytes each: the online
+ * step gathers its sampled frames (u8 RGBA images, thetas) from the HBM-resident
+ * pool into the step's contiguous buffers.  slots is a device int32 array. */
+int hs_gather_rows(int num_rows, int64_t row_bytes, const int32_t *slots, const void *pool, void *out,
+                   void *stream);
+
 /* ---- Elementwise compat ops (model.py:219-248, binding.py:174-204) ------- */
 int hs_activate_fwd(int64_t N, const float *raw14, float *act14, unsigned long long *err, void *stream);
 int hs_activate_bwd(int64_t N, const float *raw14, const float *act14, const float *g_act14,

@@ -21,6 +21,7 @@ Fixtures (all float64 unless stated):
   train.npz    two reference train_step calls on a tiny synthetic avatar with the
                summed ParamGradients captured at Optimizer.step (S/train.py:214-278)
   counts.json  bind_gaussians counts at uv 141/224/317
+  pools.npz    SamplePools / sample_batch bookkeeping        (S/stream.py:27-86)
   rig.npz      rig_evaluate + mesh_frames on a theta batch, DegenerateTriangleError
                messages                                    (S/rig.py:57-66, S/binding.py:67-115)
 """
@@ -333,6 +334,37 @@ def make_rig(out):
     out["rig"] = d
 
 
+def make_pools(out):
+    """pools.npz: S/stream.py SamplePools / sample_batch driven by a seeded rng --
+    pool contents (frame indices) after every ingest and the batch picks, for the
+    three sampling modes of run_online (full, no_global, no_local)."""
+    from headsplat.stream import SamplePools, sample_batch
+
+    class _S:                     # process_frame / sample_batch only read .index
+        def __init__(self, i):
+            self.index = i
+
+    d = {}
+    for mode, (lc, gc, keep) in {"full": (5, 12, True), "no_global": (5, 12, False),
+                                 "no_local": (1, 12, True)}.items():
+        rng = np.random.default_rng(3)
+        pools = SamplePools(lc, gc, keep_evicted=keep)
+        local, glob, picks, counters = [], [], [], []
+        for i in range(1, 81):
+            pools.process_frame(_S(i), rng)
+            local.append([s.index for s in pools.local] + [0] * (lc - len(pools.local)))
+            glob.append([s.index for s in pools.global_pool] + [0] * (gc - len(pools.global_pool)))
+            counters.append([pools.evictions, pools.discarded, pools.reservoir_inserts])
+            if i % 3 == 0:
+                picks.append([s.index for s in sample_batch(pools, 8, 0.7 if mode == "full" else 1.0, rng)])
+                rng.uniform(0.0, 1.0, size=(8, 3))       # the step's backgrounds (S/stream.py:140)
+        d[f"{mode}.local"] = np.array(local)
+        d[f"{mode}.global"] = np.array(glob)
+        d[f"{mode}.picks"] = np.array(picks)
+        d[f"{mode}.counters"] = np.array(counters)
+    out["pools"] = d
+
+
 def main():
     hs = _ref()
     import numba
@@ -352,6 +384,7 @@ def main():
     make_color(out)
     make_train(out)
     make_rig(out)
+    make_pools(out)
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     with open(os.path.join(HERE, "counts.json"), "w") as f:
