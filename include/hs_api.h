@@ -260,6 +260,17 @@ int hs_rig_frames(int B, int V, int F, int E, const double *base_vertices, const
 int hs_gather_rows(int num_rows, int64_t row_bytes, const int32_t *slots, const void *pool, void *out,
                    void *stream);
 
+/* ---- Evaluation metrics (train.py:342-360, metrics.py:25-85) ----
+ * For each frame b of pred (B,H,W,3 fp32) against target_rgba (B,H,W,4 u8)
+ * composited over black, accumulates in fp64 (written, not accumulated):
+ *   sums[5b + 0] = sum (pred - target)^2        -> psnr = 10 log10(3HW / sum), cap 99
+ *   sums[5b + 1] = sum |pred - target|          -> l1 = sum / (3HW)
+ *   sums[5b + 2 + c] = sum of the SSIM map of channel c over the (H-10)(W-10)
+ *                      valid positions (Gaussian window 11, sigma 1.5, k1 .01, k2 .03)
+ * H, W >= 11. */
+int hs_image_metrics(int B, int H, int W, const float *pred, const uint8_t *target_rgba, double *sums,
+                     void *stream);
+
 /* ---- Elementwise compat ops (model.py:219-248, binding.py:174-204) ------- */
 int hs_activate_fwd(int64_t N, const float *raw14, float *act14, unsigned long long *err, void *stream);
 int hs_activate_bwd(int64_t N, const float *raw14, const float *act14, const float *g_act14,

@@ -21,6 +21,9 @@ Fixtures (all float64 unless stated):
   train.npz    two reference train_step calls on a tiny synthetic avatar with the
                summed ParamGradients captured at Optimizer.step (S/train.py:214-278)
   counts.json  bind_gaussians counts at uv 141/224/317
+  io.npz       save_model bytes, a synth_generate sequence + load_sequence/evaluate,
+               psnr/ssim/l1 values                 (S/model_io.py, S/dataset.py:175-275,
+                                                    S/metrics.py:25-85, S/train.py:342-360)
   pools.npz    SamplePools / sample_batch bookkeeping        (S/stream.py:27-86)
   rig.npz      rig_evaluate + mesh_frames on a theta batch, DegenerateTriangleError
                messages                                    (S/rig.py:57-66, S/binding.py:67-115)
@@ -365,6 +368,73 @@ def make_pools(out):
     out["pools"] = d
 
 
+def make_io(out):
+    """io.npz: (1) a reference save_model file of a small perturbed avatar with random
+    visited flags (bytes + arrays); (2) a reference synth_generate sequence (3 frames,
+    48^2) as the raw files (params.json, rig.json, PNG bytes, gt_model.bin) with the
+    reference load_sequence / evaluate(gt model) results; (3) psnr / ssim / l1 of
+    random image pairs (S/metrics.py:25-85)."""
+    import tempfile
+    from pathlib import Path
+    from headsplat.color_init import ColorInitState
+    from headsplat.dataset import SynthConfig, load_sequence, synth_generate
+    from headsplat.metrics import composite_over, psnr, ssim
+    from headsplat.model_io import load_model, save_model
+    from headsplat.rig import build_head_rig
+    from headsplat.train import TrainConfig, evaluate, init_avatar
+    rng = np.random.default_rng(21)
+    d = {}
+    rig = build_head_rig()
+    model = init_avatar(rig, TrainConfig(uv_resolution=18, num_blendshapes=3, hidden_dim=8))
+    n = model.count
+    for x in model.deltas:
+        x.position[:] = rng.normal(0, 0.002, (n, 3))
+        x.rotation[:] = rng.normal(0, 0.02, (n, 4))
+        x.color[:] = rng.normal(0, 0.1, (n, 3))
+    model.base.opacity[:] = rng.uniform(-2, 2, n)
+    for nm in ("w1", "b1", "w2", "b2", "w3", "b3"):
+        getattr(model.mlp, nm)[...] = rng.normal(0, 0.3, getattr(model.mlp, nm).shape)
+    vis = rng.uniform(size=n) < 0.4
+    with tempfile.TemporaryDirectory() as td:
+        save_model(model, ColorInitState(vis.copy()), Path(td) / "m.bin")
+        d["model.bytes"] = np.frombuffer((Path(td) / "m.bin").read_bytes(), np.uint8).copy()
+        seq_dir = Path(td) / "seq"
+        synth_generate(seq_dir, SynthConfig(frames=3, image_size=48, uv_resolution=16, hidden_dim=16), seed=4)
+        d["seq.params"] = np.array((seq_dir / "params.json").read_text())
+        d["seq.rig"] = np.array((seq_dir / "rig.json").read_text())
+        for i in range(3):
+            d[f"seq.png{i}"] = np.frombuffer((seq_dir / "frames" / f"{i:06d}.png").read_bytes(), np.uint8).copy()
+        d["seq.gt_model"] = np.frombuffer((seq_dir / "gt_model.bin").read_bytes(), np.uint8).copy()
+        ds = load_sequence(seq_dir)
+        d["seq.thetas"] = ds.thetas
+        d["seq.images"] = np.stack(ds.images)
+        gt, _ = load_model(seq_dir / "gt_model.bin")
+        ev = evaluate(gt, ds)
+        d["seq.eval"] = np.array([[f["psnr"], f["ssim"], f["l1"]] for f in ev["frames"]])
+    d.update({f"model.{k}": v for k, v in gset_arrays("base", model.base).items()})
+    d["model.deltas"] = np.stack([np.concatenate([x.position.ravel(), x.rotation.ravel(), x.color.ravel()])
+                                  for x in model.deltas])
+    for nm in ("w1", "b1", "w2", "b2", "w3", "b3"):
+        d[f"model.mlp.{nm}"] = getattr(model.mlp, nm).copy()
+    d["model.tri_index"] = model.bindings.triangle_index
+    d["model.barycentric"] = model.bindings.barycentric
+    d["model.visited"] = vis
+    preds, tgts, vals = [], [], []
+    for i in range(3):
+        h, w = (24, 40) if i < 2 else (11, 11)
+        t = rng.integers(0, 256, (h, w, 4)).astype(np.uint8)
+        if i == 0:
+            pred = composite_over(t / 255.0, np.zeros(3)).astype(np.float32)
+            pred[3, 4, 1] += np.float32(0.25)
+        else:
+            pred = rng.uniform(0, 1, (h, w, 3)).astype(np.float32)
+        tb = composite_over(t / 255.0, np.zeros(3))
+        p64 = pred.astype(np.float64)
+        d[f"metrics{i}.pred"], d[f"metrics{i}.target"] = pred, t
+        d[f"metrics{i}.values"] = np.array([psnr(p64, tb), ssim(p64, tb), float(np.mean(np.abs(p64 - tb)))])
+    out["io"] = d
+
+
 def main():
     hs = _ref()
     import numba
@@ -385,6 +455,7 @@ def main():
     make_train(out)
     make_rig(out)
     make_pools(out)
+    make_io(out)
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     with open(os.path.join(HERE, "counts.json"), "w") as f:
