@@ -278,6 +278,48 @@ def transform_backward(tangent, frames, bindings, grad_world) -> GaussianSet:
 
 # --------------------------------------------------------------------- render
 
+@dataclass
+class MeshFrames:
+    """S/binding.py:47-53."""
+    rotation: np.ndarray       # (F, 3, 3), columns T, B, N
+    quat: np.ndarray           # (F, 4)
+    tri_vertices: np.ndarray   # (F, 3, 3)
+
+
+_RIGS = {}
+
+
+def _device_rig(rig):
+    from .device import DeviceRig
+    key = id(rig)
+    hit = _RIGS.get(key)
+    if hit is None or hit[0] is not rig:
+        hit = _RIGS[key] = (rig, DeviceRig(rig, _dev()))
+    return hit[1]
+
+
+def mesh_frames(rig, vertices) -> MeshFrames:
+    """S/binding.py:67-78 on the device (hs_rig_frames; fp64 TBN / polar / quaternion,
+    returned through fp32).  Raises the reference's DegenerateTriangleError
+    (a ValueError) naming the first bad face."""
+    v = torch.from_numpy(np.ascontiguousarray(vertices, np.float64)[None]).to(_dev())
+    out = _device_rig(rig).frames(vertices=v)[0].cpu().numpy().astype(np.float64)
+    F = out.shape[0]
+    return MeshFrames(out[:, :9].reshape(F, 3, 3), out[:, 9:13].copy(), out[:, 13:].reshape(F, 3, 3))
+
+
+def rig_mesh_frames(rig, theta) -> MeshFrames:
+    """mesh_frames(rig, rig_evaluate(rig, theta)) in one device call (S/rig.py:57-66 +
+    S/binding.py:67-78); theta is taken in fp32."""
+    theta = np.asarray(theta, np.float64)
+    if theta.shape != (rig.num_expressions + 3,) and theta.shape != (getattr(rig, "param_dim", -1),):
+        raise ValueError(f"theta has shape {theta.shape}, rig expects ({rig.num_expressions + 3},)")
+    t = torch.from_numpy(theta.astype(np.float32)[None]).to(_dev())
+    out = _device_rig(rig).frames(t)[0].cpu().numpy().astype(np.float64)
+    F = out.shape[0]
+    return MeshFrames(out[:, :9].reshape(F, 3, 3), out[:, 9:13].copy(), out[:, 13:].reshape(F, 3, 3))
+
+
 def _check_camera(camera):
     if camera.fx <= 0 or camera.fy <= 0:
         raise ValueError("focal lengths must be positive")

@@ -140,3 +140,23 @@ def test_step_and_render_on_device_frames():
         r = b.step_from_host(h["thetas"], h["targets"], None, h["cameras"], h["backgrounds"])
         assert np.isfinite(r.loss)
     b.close()
+
+
+def test_compat_mesh_frames_drop_in():
+    """compat.mesh_frames / rig_mesh_frames: the reference signatures (S/binding.py:67,
+    S/rig.py:57) returning MeshFrames-shaped float64 arrays."""
+    from paper_2503_12886_b200 import _lib as L
+    from paper_2503_12886_b200 import compat
+    d = golden("rig")
+    rig = _ref_rig()
+    rig.num_expressions = rig.expr_bases.shape[0]
+    for b in (0, 2):
+        mf = compat.mesh_frames(rig, d["verts"][b])
+        np.testing.assert_allclose(mf.rotation, d["frames.rotation"][b], rtol=2e-6, atol=2e-6)
+        np.testing.assert_allclose(mf.quat, d["frames.quat"][b], rtol=2e-6, atol=2e-6)
+        mf2 = compat.rig_mesh_frames(rig, d["theta"][b])
+        np.testing.assert_allclose(mf2.tri_vertices, d["frames.tri_vertices"][b], rtol=2e-6, atol=2e-6)
+    bad = _ref_rig()
+    bad.uv_coords = d["bad_uv.uv_coords"]
+    with pytest.raises(L.DegenerateTriangleError, match=str(d["bad_uv.message"])):
+        compat.mesh_frames(bad, d["verts"][0])
