@@ -161,7 +161,10 @@ int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t 
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);
 
 /* ---- Raster (render.py:233-273 _composite_kernel, :339-377 _weight_sums_kernel,
- *      metrics.py:10-22 l1_loss, :80-85 composite_over, train.py:238-247) ---- */
+ *      metrics.py:10-22 l1_loss, :80-85 composite_over, train.py:238-247) ----
+ * The raster kernels are persistent and share a per-process work counter: within
+ * one process, hs_raster_fwd / hs_raster_bwd launches must be ordered (same stream
+ * or synchronised), not concurrent on different streams. */
 enum {
     HS_RASTER_LOSS = 1,          /* fused L1 loss vs targets (u8 RGBA) composited over bg */
     HS_RASTER_IMAGE = 2,         /* write image[B,H,W,3] */
@@ -186,10 +189,11 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const float *pix_T, const uint32_t *pix_state,
                   const float *grad_image, float grad_scale, float *g_splat, void *stream);
-/* Diagnostics: forward-raster counters [warp iterations, pixel tests, q <= qmax,
- * alpha >= 1/255, iterations with no q pass, full-cover iterations, staged
- * batches, 0] accumulated when built with -DHS_RASTER_STATS (zeros otherwise);
- * synchronous copy to host_out[8]. */
+/* Diagnostics: raster counters accumulated when built with -DHS_RASTER_STATS (zeros
+ * otherwise); synchronous copy to host_out[16]:
+ *   forward [warp iterations, pixel tests, q <= qmax, alpha >= 1/255, iterations with
+ *   no q pass, full-cover iterations, staged batches, 0], adjoint iterations by the
+ *   number of contributing lanes [0, 1, 2, 3-4, 5-8, 9-16, 17-32, 0]. */
 int hs_raster_stats(unsigned long long *host_out, int reset);
 /* loss_out[b] = sum|pred-target| / (H*W*3), loss_out[B+b] = black-bg L1,
  * loss_out[2B] = mean over frames. */

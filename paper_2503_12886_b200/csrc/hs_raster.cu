@@ -25,6 +25,8 @@
 // with the suffix recurrence; each lane first adds its two pixels' contributions,
 // then the 9 per-splat gradients are reduce-scattered across the warp (12 shuffles)
 // before one RED per value.
+#include <algorithm>
+
 #include "hs_common.cuh"
 
 namespace hs {
@@ -48,7 +50,7 @@ constexpr int kCW = HS_RASTER_CTA_WARPS;
 
 // Optional instrumentation (-DHS_RASTER_STATS): forward-pass counts of warp
 // iterations and pixel tests, read with hs_raster_stats().
-__device__ unsigned long long g_raster_stats[8];
+__device__ unsigned long long g_raster_stats[16];
 constexpr int kBlocks = kTile * kTile / (32 * kPX);   // 8 x 4*PX pixel blocks per tile
 constexpr int kRT = 32 * kCW;                          // threads per CTA
 static_assert(kBlocks % kCW == 0, "CTA warps must divide the blocks of a tile");
@@ -170,18 +172,16 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
 //     3 max weight + weight sums for splats whose Gaussian is not yet visited.
 template <bool kLoss, bool kImage, int CI>
-__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a) {
-    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int gw = blockIdx.x * kCW + warp;              // block of the frame: tile * kBlocks + blk
-    const int tile = gw / kBlocks, blk = gw % kBlocks, b = blockIdx.y;
+__device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int gw, int nblk, int lane,
+                                                 uint32_t wbase) {
+    // gw = tile * kBlocks + blk: the pixel block of frame b this warp composites
+    const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int px, py0;
     pixels_of(blk, lane, tx, ty, px, py0);
     const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 4 * kPX;
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
-    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
     const float fpx = (float)px;
 
@@ -365,19 +365,61 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
         l1 = warp_sum(l1);
         black = warp_sum(black);
         if (lane == 0) {
-            const int64_t o = ((int64_t)b * gridDim.x * kCW + gw) * 2;
+            const int64_t o = ((int64_t)b * nblk + gw) * 2;
             a.loss_partials[o] = l1;
             a.loss_partials[o + 1] = black;
         }
     }
 }
 
-template <bool kExplicitGrad>
-__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a) {
+// Work distribution (HS_RASTER_PERSIST, default): a persistent grid of resident
+// one-warp CTAs where every warp pulls (frame, block) items from a global counter
+// (frame-major, tile order), so short and long blocks mix freely and no CTA launch
+// happens per block (-8 % raster time vs one CTA per block).  The last warp to
+// finish resets the counters for the next launch, so raster launches of one process
+// must not run concurrently on different streams (hs_api.h).  HS_RASTER_PERSIST=0:
+// one CTA per block.
+#ifndef HS_RASTER_PERSIST
+#define HS_RASTER_PERSIST 1
+#endif
+__device__ unsigned int g_raster_work[4];   // [fwd next, fwd done, bwd next, bwd done]
+
+template <typename F>
+__device__ __forceinline__ void for_each_block(int B, int nblk, int lane, int warp, unsigned int *work, F &&fn) {
+    if (!HS_RASTER_PERSIST) {
+        fn((int)blockIdx.y, (int)blockIdx.x * kCW + warp);
+        return;
+    }
+    const int total = B * nblk;
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(work, 1u);
+        item = __shfl_sync(kFull, item, 0);
+        if (item >= total) break;
+        fn(item / nblk, item % nblk);
+        __syncwarp();
+    }
+    if (lane == 0) {
+        const unsigned int warps = gridDim.x * gridDim.y * kCW;
+        if (atomicAdd(work + 1, 1u) == warps - 1) {
+            work[0] = 0u;
+            work[1] = 0u;
+        }
+    }
+}
+
+template <bool kLoss, bool kImage, int CI>
+__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a, int nblk) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int gw = blockIdx.x * kCW + warp;
-    const int tile = gw / kBlocks, blk = gw % kBlocks, b = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
+    for_each_block(a.B, nblk, lane, warp, g_raster_work,
+                   [&](int b, int gw) { raster_fwd_block<kLoss, kImage, CI>(a, b, gw, nblk, lane, wbase); });
+}
+
+template <bool kExplicitGrad>
+__device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int gw, int lane, uint32_t wbase) {
+    const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int px, py0;
     pixels_of(blk, lane, tx, ty, px, py0);
@@ -385,7 +427,6 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     if (start >= end) return;
-    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
     const float fpx = (float)px;
 
@@ -495,6 +536,15 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
                 suffix[p] += wgt * gw;
                 t_rev[p] = t_prior;
             }
+#ifdef HS_RASTER_STATS
+            {
+                const int nc = __popc(__ballot_sync(kFull, contrib));
+                if (lane == 0) {
+                    const int bin = nc == 0 ? 0 : nc == 1 ? 1 : nc == 2 ? 2 : nc <= 4 ? 3 : nc <= 8 ? 4 : nc <= 16 ? 5 : 6;
+                    atomicAdd(&g_raster_stats[8 + bin], 1ull);
+                }
+            }
+#endif
             if (__any_sync(kFull, contrib)) {
                 int vi;
                 bool issue;
@@ -506,6 +556,15 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
         __syncwarp();
         c_end = c0;
     }
+}
+
+template <bool kExplicitGrad>
+__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a, int nblk) {
+    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
+    for_each_block(a.B, nblk, lane, warp, g_raster_work + 2,
+                   [&](int b, int gw) { raster_bwd_block<kExplicitGrad>(a, b, gw, lane, wbase); });
 }
 
 // partials[b][tiles * kBlocks][2] (one pair per pixel block)
@@ -555,13 +614,23 @@ static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records
 }
 
 template <bool L, bool I>
-static void launch_fwd_ci(int ci, dim3 grid, cudaStream_t s, const RasterArgs &a) {
+static void launch_fwd_ci(int ci, dim3 grid, int nblk, cudaStream_t s, const RasterArgs &a) {
     switch (ci) {
-        case 0: raster_fwd_kernel<L, I, 0><<<grid, kRT, 0, s>>>(a); break;
-        case 1: raster_fwd_kernel<L, I, 1><<<grid, kRT, 0, s>>>(a); break;
-        case 2: raster_fwd_kernel<L, I, 2><<<grid, kRT, 0, s>>>(a); break;
-        default: raster_fwd_kernel<L, I, 3><<<grid, kRT, 0, s>>>(a); break;
+        case 0: raster_fwd_kernel<L, I, 0><<<grid, kRT, 0, s>>>(a, nblk); break;
+        case 1: raster_fwd_kernel<L, I, 1><<<grid, kRT, 0, s>>>(a, nblk); break;
+        case 2: raster_fwd_kernel<L, I, 2><<<grid, kRT, 0, s>>>(a, nblk); break;
+        default: raster_fwd_kernel<L, I, 3><<<grid, kRT, 0, s>>>(a, nblk); break;
     }
+}
+
+// grid of the raster kernels: one CTA per kCW blocks, or a persistent grid of
+// resident CTAs (HS_RASTER_PERSIST)
+static dim3 raster_grid(int nblk, int B) {
+    if (!HS_RASTER_PERSIST) return dim3(nblk / kCW, B);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t want = (int64_t)sms * HS_RASTER_MINB, items = (int64_t)nblk * B / kCW;
+    return dim3((unsigned)std::max<int64_t>(1, std::min(want, items)), 1);
 }
 
 }  // namespace hs
@@ -595,12 +664,13 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     a.maxw = maxw;
     a.wsums = wsums;
     a.loss_partials = loss_partials;
-    dim3 grid(tiles_x * tiles_y * (kBlocks / kCW), B);
+    const int nblk = tiles_x * tiles_y * kBlocks;
+    const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    if (loss && img) launch_fwd_ci<true, true>(ci, grid, s, a);
-    else if (loss) launch_fwd_ci<true, false>(ci, grid, s, a);
-    else if (img) launch_fwd_ci<false, true>(ci, grid, s, a);
-    else launch_fwd_ci<false, false>(ci, grid, s, a);
+    if (loss && img) launch_fwd_ci<true, true>(ci, grid, nblk, s, a);
+    else if (loss) launch_fwd_ci<true, false>(ci, grid, nblk, s, a);
+    else if (img) launch_fwd_ci<false, true>(ci, grid, nblk, s, a);
+    else launch_fwd_ci<false, false>(ci, grid, nblk, s, a);
     return check_launch("hs_raster_fwd");
 }
 
@@ -615,17 +685,18 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     a.grad_image = grad_image;
     a.grad_scale = grad_scale;
     a.g_splat = g_splat;
-    dim3 grid(tiles_x * tiles_y * (kBlocks / kCW), B);
+    const int nblk = tiles_x * tiles_y * kBlocks;
+    const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a);
-    else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a);
+    if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a, nblk);
+    else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a, nblk);
     return check_launch("hs_raster_bwd");
 }
 
 int hs_raster_stats(unsigned long long *host_out, int reset) {
-    cudaMemcpyFromSymbol(host_out, g_raster_stats, sizeof(unsigned long long) * 8);
+    cudaMemcpyFromSymbol(host_out, g_raster_stats, sizeof(unsigned long long) * 16);
     if (reset) {
-        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const unsigned long long z[16] = {};
         cudaMemcpyToSymbol(g_raster_stats, z, sizeof(z));
     }
     return check_launch("hs_raster_stats");
