@@ -121,6 +121,8 @@ def stage_bytes(B, N, K, H, D, W, Hh, keys, params, color_init=True, passes=6):
         "bin_sort": keys * (12 + 8 + passes * 24 + 8),   # emit, histogram, passes, ranges
         "raster_fwd": keys * (4 + rec) + B * HW * (4 + 4 + 4) + (B * N * 20 if color_init else 0),
         "raster_bwd": keys * (4 + rec) + B * HW * 8 + B * N * 36,
+        # fused forward + adjoint: both key walks, targets once, no per-pixel state round trip
+        "raster": 2 * keys * (4 + rec) + B * HW * 4 + B * N * 36 + (B * N * 20 if color_init else 0),
         "project_bwd": B * N * (36 + 40 + 56) + N * 32 + B * 1024 * 22 * 4,
         "blend_bwd": 4 * (B * 14 * N + 2 * 10 * N * K + 14 * N),
         "adam": 28 * params,

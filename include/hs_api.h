@@ -189,6 +189,16 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const float *pix_T, const uint32_t *pix_state,
                   const float *grad_image, float grad_scale, float *g_splat, void *stream);
+/* Training-step raster: hs_raster_fwd (HS_RASTER_LOSS plus the colour-init flags)
+ * and hs_raster_bwd with the L1 gradient sign(pred - target) * grad_scale, fused per
+ * pixel block -- T, stop and the gradient stay in registers and the adjoint reuses
+ * the forward's per-batch hit masks.  pix_T / pix_state are written only when
+ * non-NULL.  g_splat must be zero-filled; loss_partials as hs_raster_fwd. */
+int hs_raster_train(int B, int64_t N, int width, int height, int flags, const float *records,
+                    const uint32_t *values, const uint32_t *ranges, int tile_bits,
+                    const float *backgrounds, const uint8_t *targets, const uint8_t *visited,
+                    float *maxw, float *wsums, float *loss_partials, float grad_scale, float *g_splat,
+                    float *pix_T, uint32_t *pix_state, void *stream);
 /* Diagnostics: raster counters accumulated when built with -DHS_RASTER_STATS (zeros
  * otherwise); synchronous copy to host_out[16]:
  *   forward [warp iterations, pixel tests, q <= qmax, alpha >= 1/255, iterations with

@@ -129,6 +129,7 @@ __device__ __forceinline__ void pixels_of(int w, int l, int tx, int ty, int &px,
 // Stage one splat record into the lane's slot.  Returns bit 0: the warp's block
 // [x0, x0+7] x [y0, y0+4 kPX-1] can hold a contributing pixel; bit 1: the splat's
 // integer bbox covers the whole block (the per-pixel bbox test can be skipped).
+template <bool kCull = true>
 __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
                                             uint32_t saddr) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
@@ -143,6 +144,7 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
     asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 32), "r"(cl), "r"(ch), "r"(rl), "r"(rh));
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 48), "f"(Cv.y), "f"(Cv.z), "f"(Cv.w),
                  "f"(0.f));
+    if (!kCull) return 0u;
     if (!(qmax >= 0.f)) return 0u;
     // pixels of the block the reference's bbox admits
     const int xs = max(x0, cl), xe = min(x0 + 7, ch), ys = max(y0, rl), ye = min(y0 + 4 * kPX - 1, rh);
@@ -171,9 +173,17 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
 //     3 max weight + weight sums for splats whose Gaussian is not yet visited.
-template <bool kLoss, bool kImage, int CI>
+constexpr int kMaskBatches = 64;     // per-warp hit masks kept from the forward for the fused adjoint
+
+template <bool kExplicitGrad>
+__device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
+                                                uint32_t start, uint32_t last, const float (&g)[kPX][3],
+                                                float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
+                                                int lane, uint32_t wbase, const uint2 *masks);
+
+template <bool kLoss, bool kImage, int CI, bool kTrain = false>
 __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int gw, int nblk, int lane,
-                                                 uint32_t wbase) {
+                                                 uint32_t wbase, uint2 *masks = nullptr) {
     // gw = tile * kBlocks + blk: the pixel block of frame b this warp composites
     const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -237,6 +247,10 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         uint32_t bits = __ballot_sync(kFull, code & 1u);
         const uint32_t fullb = __ballot_sync(kFull, code & 2u);
         const uint32_t wantb = __ballot_sync(kFull, want);
+        if (kTrain && lane == 0) {
+            const uint32_t k = (c0 - start) >> 5;
+            if (k < (uint32_t)kMaskBatches) masks[k] = make_uint2(bits, fullb);
+        }
 #ifdef HS_RASTER_STATS
         st_batches += lane == 0;
 #endif
@@ -332,9 +346,14 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     atomicAdd(&g_raster_stats[6], st_batches);
 #endif
     float l1 = 0.f, black = 0.f;
+    float g[kTrain ? kPX : 1][3];            // fused adjoint: the L1 gradient of each pixel
 #pragma unroll
     for (int p = 0; p < kPX; ++p) {
         const int py = py0 + 4 * p;
+        if (kTrain) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[p][c] = 0.f;
+        }
         if (px >= a.W || py >= a.H) continue;
         const int64_t pix = ((int64_t)b * a.H + py) * a.W + px;
         float pred[3];
@@ -352,10 +371,13 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                 l1 += fabsf(d);
                 black += fabsf(C[p][c] - rgb[c] * al);
                 signs |= (d > 0.f ? 1u : d < 0.f ? 2u : 0u) << (2 * c);
+                if (kTrain) g[p][c] = d > 0.f ? a.grad_scale : d < 0.f ? -a.grad_scale : 0.f;
             }
         }
-        a.pix_T[pix] = T[p];
-        a.pix_state[pix] = stop[p] | (signs << 26);
+        if (!kTrain || a.pix_T) {
+            a.pix_T[pix] = T[p];
+            a.pix_state[pix] = stop[p] | (signs << 26);
+        }
         if (kImage) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) a.image[pix * 3 + c] = pred[c];
@@ -370,6 +392,24 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             a.loss_partials[o + 1] = black;
         }
     }
+    if constexpr (kTrain) {
+        // the adjoint of this block right away: T, stop and the loss gradient are in
+        // registers and the forward's hit masks are in shared memory
+        if (start >= end) return;
+        float t_rev[kPX], suffix[kPX];
+        uint32_t smax = 0;
+#pragma unroll
+        for (int p = 0; p < kPX; ++p) {
+            const bool inside = px < a.W && py0 + 4 * p < a.H;
+            if (!inside) stop[p] = 0;
+            t_rev[p] = inside ? T[p] : 0.f;
+            suffix[p] = inside ? T[p] * (g[p][0] * bg[0] + g[p][1] * bg[1] + g[p][2] * bg[2]) : 0.f;
+            smax = max(smax, stop[p]);
+        }
+        const uint32_t last = start + __reduce_max_sync(kFull, smax);
+        __syncwarp();
+        raster_bwd_loop<false>(a, b, px, py0, x0, y0, start, last, g, t_rev, suffix, stop, lane, wbase, masks);
+    }
 }
 
 // Work distribution (HS_RASTER_PERSIST, default): a persistent grid of resident
@@ -382,7 +422,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
 #ifndef HS_RASTER_PERSIST
 #define HS_RASTER_PERSIST 1
 #endif
-__device__ unsigned int g_raster_work[4];   // [fwd next, fwd done, bwd next, bwd done]
+__device__ unsigned int g_raster_work[6];   // [fwd next, done, bwd next, done, train next, done]
 
 template <typename F>
 __device__ __forceinline__ void for_each_block(int B, int nblk, int lane, int warp, unsigned int *work, F &&fn) {
@@ -428,17 +468,14 @@ __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int
     const uint32_t start = rg.x, end = rg.y;
     if (start >= end) return;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
-    const float fpx = (float)px;
 
-    int py[kPX];
-    float fpy[kPX], g[kPX][3], t_rev[kPX], suffix[kPX];
+    float g[kPX][3], t_rev[kPX], suffix[kPX];
     uint32_t stop[kPX];
 #pragma unroll
     for (int p = 0; p < kPX; ++p) {
-        py[p] = py0 + 4 * p;
-        fpy[p] = (float)py[p];
-        const bool inside = px < a.W && py[p] < a.H;
-        const int64_t pix = ((int64_t)b * a.H + (inside ? py[p] : 0)) * a.W + (inside ? px : 0);
+        const int py = py0 + 4 * p;
+        const bool inside = px < a.W && py < a.H;
+        const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
         g[p][0] = g[p][1] = g[p][2] = 0.f;
         stop[p] = 0;
         t_rev[p] = 0.f;
@@ -467,17 +504,52 @@ __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int
 #pragma unroll
     for (int p = 0; p < kPX; ++p) smax = max(smax, stop[p]);
     const uint32_t last = start + __reduce_max_sync(kFull, smax);
-    for (uint32_t c_end = last; c_end > start;) {
-        const uint32_t c0 = c_end - start > 32u ? c_end - 32u : start;
+    raster_bwd_loop<kExplicitGrad>(a, b, px, py0, x0, y0, start, last, g, t_rev, suffix, stop, lane, wbase, nullptr);
+}
+
+// Back-to-front walk of [start, last) in the forward's 32-key batches.  With the
+// forward's hit masks (fused kernel) a batch is staged only by its hit lanes and
+// skipped when empty; otherwise each batch is staged and culled again.
+template <bool kExplicitGrad>
+__device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
+                                                uint32_t start, uint32_t last, const float (&g)[kPX][3],
+                                                float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
+                                                int lane, uint32_t wbase, const uint2 *masks) {
+    const float fpx = (float)px;
+    int py[kPX];
+    float fpy[kPX];
+#pragma unroll
+    for (int p = 0; p < kPX; ++p) {
+        py[p] = py0 + 4 * p;
+        fpy[p] = (float)py[p];
+    }
+    if (last <= start) return;
+    for (int k = (int)((last - 1 - start) >> 5); k >= 0; --k) {
+        const uint32_t c0 = start + 32u * (uint32_t)k;
+        const uint32_t c_end = min(c0 + 32u, last);
+        const uint32_t live_lanes = c_end - c0 >= 32u ? kFull : (1u << (c_end - c0)) - 1u;
+        uint32_t bits, fullb;
         const uint32_t idx = c0 + lane;
-        uint32_t code = 0u;
-        if (idx < c_end) {
-            const uint32_t n = a.vals[idx];
-            code = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0, y0,
-                               wbase + lane * kStageBytes);
+        if (masks != nullptr && k < kMaskBatches) {
+            const uint2 m = masks[k];
+            bits = m.x & live_lanes;
+            fullb = m.y;
+            if (bits == 0u) continue;                      // warp-uniform
+            if ((bits >> lane) & 1u) {
+                const uint32_t n = a.vals[idx];
+                stage_splat<false>(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
+                                   y0, wbase + lane * kStageBytes);
+            }
+        } else {
+            uint32_t code = 0u;
+            if (idx < c_end) {
+                const uint32_t n = a.vals[idx];
+                code = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
+                                   y0, wbase + lane * kStageBytes);
+            }
+            bits = __ballot_sync(kFull, code & 1u);
+            fullb = __ballot_sync(kFull, code & 2u);
         }
-        uint32_t bits = __ballot_sync(kFull, code & 1u);
-        const uint32_t fullb = __ballot_sync(kFull, code & 2u);
         __syncwarp();
         while (bits) {
             const int j = 31 - __clz(bits);
@@ -554,8 +626,22 @@ __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int
             }
         }
         __syncwarp();
-        c_end = c0;
     }
+}
+
+
+// Training step: forward (L1 loss, colour-init sums) and adjoint of each pixel block in
+// one pass -- no per-pixel state round trip through HBM, and the adjoint reuses the
+// forward's per-batch hit masks.
+template <int CI>
+__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
+    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
+    __shared__ uint2 s_masks[kCW][kMaskBatches];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
+    for_each_block(a.B, nblk, lane, warp, g_raster_work + 4, [&](int b, int gw) {
+        raster_fwd_block<true, false, CI, true>(a, b, gw, nblk, lane, wbase, s_masks[warp]);
+    });
 }
 
 template <bool kExplicitGrad>
@@ -691,6 +777,42 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a, nblk);
     else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a, nblk);
     return check_launch("hs_raster_bwd");
+}
+
+int hs_raster_train(int B, int64_t N, int width, int height, int flags, const float *records, const uint32_t *values,
+                    const uint32_t *ranges, int tile_bits, const float *backgrounds, const uint8_t *targets,
+                    const uint8_t *visited, float *maxw, float *wsums, float *loss_partials, float grad_scale,
+                    float *g_splat, float *pix_T, uint32_t *pix_state, void *stream) {
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    int ci = 0;
+    if (flags & HS_RASTER_MAXW_UNVISITED) ci = 3;
+    else if ((flags & HS_RASTER_MAXW_ALL) && (flags & HS_RASTER_WSUMS)) ci = 2;
+    else if (flags & HS_RASTER_MAXW_ALL) ci = 1;
+    if (!targets || !loss_partials || !g_splat || (ci && !maxw) || (ci >= 2 && !wsums) || (ci == 3 && !visited) ||
+        (flags & (HS_RASTER_IMAGE | HS_RASTER_WSUMS_IMAGE)) || (!pix_T != !pix_state)) {
+        set_error("hs_raster_train: flags 0x%x / buffers not supported (needs targets, loss_partials, g_splat)", flags);
+        return HS_ERR_SHAPE;
+    }
+    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds);
+    a.targets = targets;
+    a.visited = visited;
+    a.maxw = maxw;
+    a.wsums = wsums;
+    a.loss_partials = loss_partials;
+    a.grad_scale = grad_scale;
+    a.g_splat = g_splat;
+    a.pix_T = pix_T;
+    a.pix_state = pix_state;
+    const int nblk = tiles_x * tiles_y * kBlocks;
+    const dim3 grid = raster_grid(nblk, B);
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    switch (ci) {
+        case 0: raster_train_kernel<0><<<grid, kRT, 0, s>>>(a, nblk); break;
+        case 1: raster_train_kernel<1><<<grid, kRT, 0, s>>>(a, nblk); break;
+        case 2: raster_train_kernel<2><<<grid, kRT, 0, s>>>(a, nblk); break;
+        default: raster_train_kernel<3><<<grid, kRT, 0, s>>>(a, nblk); break;
+    }
+    return check_launch("hs_raster_train");
 }
 
 int hs_raster_stats(unsigned long long *host_out, int reset) {

@@ -353,6 +353,7 @@ class Trainer:
         require_cuda()
         self.av = avatar
         self.rig = rig              # DeviceRig: frames computed from theta on device
+        self.fused_raster = True    # hs_raster_train (False: hs_raster_fwd + hs_raster_bwd)
         self.W, self.H = int(width), int(height)
         self.B = int(batch)
         self.global_batch = int(global_batch or batch)
@@ -512,19 +513,30 @@ class Trainer:
         if self._targets_ready is not None:     # step_from_host: targets arrive on the copy stream
             torch.cuda.current_stream().wait_event(self._targets_ready)
             self._targets_ready = None
-        self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
-                   _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
-                   _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials), s)
-        if ci and self.pg is not None:
-            self._color_collectives()       # on the comm stream, overlapping the backward
-        self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
-                   _p(self.loss_out), s, kernels=2)
-        # backward: d loss_b / d pred = sign / (H W 3) / B_global  (S/metrics.py:19-22, S/train.py:244)
+        # d loss_b / d pred = sign / (H W 3) / B_global  (S/metrics.py:19-22, S/train.py:244)
         grad_scale = 1.0 / (self.H * self.W * 3.0) / self.global_batch
         self.g_splat.zero_()
-        self._call("raster_bwd", "hs_raster_bwd", B, N, self.W, self.H, _p(self.records), _p(vals), _p(ranges),
-                   tile_bits, _p(backgrounds), _p(self.pix_T), _p(self.pix_state), None, ctypes.c_float(grad_scale),
-                   _p(self.g_splat), s)
+        if self.fused_raster:
+            # forward + adjoint of every pixel block in one pass (hs_raster_train)
+            self._call("raster", "hs_raster_train", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
+                       _p(ranges), tile_bits, _p(backgrounds), _p(targets), _p(self.visited), _p(self.maxw),
+                       _p(self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale), _p(self.g_splat), None,
+                       None, s)
+            if ci and self.pg is not None:
+                self._color_collectives()   # on the comm stream, overlapping the rest of the backward
+            self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
+                       _p(self.loss_out), s, kernels=2)
+        else:
+            self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
+                       _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
+                       _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials), s)
+            if ci and self.pg is not None:
+                self._color_collectives()   # on the comm stream, overlapping the backward
+            self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
+                       _p(self.loss_out), s, kernels=2)
+            self._call("raster_bwd", "hs_raster_bwd", B, N, self.W, self.H, _p(self.records), _p(vals),
+                       _p(ranges), tile_bits, _p(backgrounds), _p(self.pix_T), _p(self.pix_state), None,
+                       ctypes.c_float(grad_scale), _p(self.g_splat), s)
         self._call("project_bwd", "hs_project_avatar_bwd", B, N, F, _p(self.raw10), _p(av.base14), _p(av.tri_index),
                    _p(av.barycentric), _p(frames), _p(cameras), _p(self.g_splat), _p(self.g_raw14), s)
         nparts = ctypes.c_int(0)

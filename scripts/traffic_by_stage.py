@@ -8,7 +8,7 @@ import json
 import subprocess
 import sys
 
-STAGE = [("raster_bwd", "raster_bwd_kernel"), ("raster_fwd", "raster_fwd_kernel"), ("blend_bwd", "blend_bwd_kernel"),
+STAGE = [("raster", "raster_train_kernel"), ("raster_bwd", "raster_bwd_kernel"), ("raster_fwd", "raster_fwd_kernel"), ("blend_bwd", "blend_bwd_kernel"),
          ("blend_fwd", "blend_fwd_kernel"), ("project_fwd", "project_avatar_fwd"),
          ("project_bwd", "project_avatar_bwd"), ("adam", "adam_kernel"), ("mlp_fwd", "mlp_fwd_kernel"),
          ("rig_frames", "rig_frames_kernel"),
@@ -35,7 +35,7 @@ if not any("raster_bwd" in k for k, _ in step):
     # capture starts mid-step: the forward half from the last rig_frames onwards, the
     # backward half (after the previous step's forward raster) from before it
     head = seq[:lo]
-    rf = max((i for i, (k, _) in enumerate(head) if "raster_fwd" in k), default=-1)
+    rf = max((i for i, (k, _) in enumerate(head) if "raster_fwd" in k or "raster_train" in k), default=-1)
     step = seq[lo:] + head[rf + 1:]
 res = {}
 for name, pat in STAGE:
