@@ -113,7 +113,10 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
 #define HS_SORT_MINB 4
 #endif
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;
+#ifndef HS_SORT_ITEMS
+#define HS_SORT_ITEMS 8
+#endif
+constexpr int kSortItems = HS_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per CTA
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;

@@ -108,6 +108,13 @@ __device__ __forceinline__ int4 lds4i(uint32_t addr) {
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
+// 1/x for x in (0, 1] (x = 1 - alpha, alpha < 1): the MUFU reciprocal without the
+// denormal-range fix-up __fdividef adds (same result for normal x)
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -586,7 +593,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
                 const bool ok = jl < stop[p] && inb[p] && e2 >= p1.y && alpha0 >= kAlphaCutoff;
                 contrib = contrib || ok;
                 const float G = ok ? G0 : 0.f, alpha = ok ? alpha0 : 0.f;
-                const float inv = __fdividef(1.0f, 1.0f - alpha);
+                const float inv = rcp_approx(1.0f - alpha);
                 const float t_prior = t_rev[p] * inv;
                 const float gw = g[p][0] * col.x + g[p][1] * col.y + g[p][2] * col.z;
                 const float wgt = alpha * t_prior;
