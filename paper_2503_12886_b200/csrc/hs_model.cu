@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
         } else {
             bv[0] = base[e];
         }
-        for (int b0 = 0; b0 < B; b0 += BC) {
+        for (int b0 = blockIdx.y * BC; b0 < B; b0 += BC * gridDim.y) {
             const int nb = min(BC, B - b0);
             float acc[BC][VEC];
 #pragma unroll
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
                 for (int q = 0; q < kKB; ++q) {
                     const int k = min(k0 + q, K - 1);
                     if constexpr (VEC == 4) {
-                        float4 t = __ldcs(reinterpret_cast<const float4 *>(deltas + (int64_t)k * E + e));
+                        float4 t = __ldg(reinterpret_cast<const float4 *>(deltas + (int64_t)k * E + e));
                         dv[q][0] = t.x; dv[q][1] = t.y; dv[q][2] = t.z; dv[q][3] = t.w;
                     } else {
                         dv[q][0] = __ldcs(deltas + (int64_t)k * E + e);
@@ -713,10 +713,16 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
                      ((uintptr_t)deltas % 16 == 0) && ((uintptr_t)raw10 % 16 == 0);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+#ifndef HS_BLEND_BC
+#define HS_BLEND_BC 4
+#endif
     if (vec) {
+        // grid.y splits the frames into chunks of HS_BLEND_BC: few accumulators per
+        // thread (occupancy) while the 40 MB of deltas stay L2-resident across chunks
         int64_t nv = E / 4;
-        unsigned grid = (unsigned)std::min<int64_t>(grid_for(nv, 256), (int64_t)sms * 8);
-        blend_fwd_kernel<4, 16><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
+        const unsigned gy = (unsigned)((B + HS_BLEND_BC - 1) / HS_BLEND_BC);
+        const dim3 grid((unsigned)grid_for(nv, 256), gy);
+        blend_fwd_kernel<4, HS_BLEND_BC><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
     } else {
         unsigned grid = (unsigned)std::min<int64_t>(grid_for(E, 256), (int64_t)sms * 16);
         blend_fwd_kernel<1, 16><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
