@@ -157,6 +157,9 @@ size_t hs_sort_workspace_size(int64_t num_keys);
 int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t *values,
                   uint64_t *keys_alt, uint32_t *values_alt, void *workspace,
                   size_t workspace_bytes, int *result_in_alt, void *stream);
+/* Diagnostics (-DHS_BIN_STATS builds; zeros otherwise): [keys emitted, keys whose
+ * splat provably contributes to no pixel of the tile]; synchronous copy to host_out[2]. */
+int hs_bin_stats(unsigned long long *host_out, int reset);
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);
 

@@ -58,6 +58,10 @@ __global__ void __launch_bounds__(1024) scan_kernel(int nb, const uint32_t *__re
 
 // ------------------------------------------------------------------ emission
 
+#ifdef HS_BIN_STATS
+__device__ unsigned long long g_bin_stats[2];
+#endif
+
 // Same 256-item partition as the projection kernel: block-local exclusive scan of
 // the tile counts plus the block offset gives each (frame, Gaussian) its slot.
 __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int tiles_x, int tile_bits,
@@ -95,6 +99,29 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
             keys[pos] = hi | ((uint64_t)(ty * tiles_x + tx) << 32);
             vals[pos] = n;
             ++pos;
+#ifdef HS_BIN_STATS
+            {   // would the exact ellipse-rectangle test cull this (splat, tile) key?
+                const float mx = rec[0], my = rec[1], a = rec[2], bb = rec[3], c = rec[4], qmax = rec[6];
+                const int rl = unpack_lo(rows), rh = unpack_hi(rows), cl = unpack_lo(cols), ch = unpack_hi(cols);
+                const int xs = max(tx * kTile, cl), xe = min(tx * kTile + kTile - 1, ch);
+                const int ys = max(ty * kTile, rl), ye = min(ty * kTile + kTile - 1, rh);
+                bool cull = xs > xe || ys > ye || !(qmax >= 0.f);
+                const float det = a * c - bb * bb;
+                if (!cull && det > 0.f && a > 0.f && c > 0.f) {
+                    const float dxlo = (float)xs + 0.5f - mx, dxhi = (float)xe + 0.5f - mx;
+                    const float dylo = (float)ys + 0.5f - my, dyhi = (float)ye + 0.5f - my;
+                    const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
+                    const float dyv = fminf(fmaxf(-bb * dxv / c, dylo), dyhi);
+                    const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
+                    const float dxh = fminf(fmaxf(-bb * dyh / a, dxlo), dxhi);
+                    const float qv = a * dxv * dxv + 2.f * bb * dxv * dyv + c * dyv * dyv;
+                    const float qh = a * dxh * dxh + 2.f * bb * dxh * dyh + c * dyh * dyh;
+                    cull = fminf(qv, qh) * 0.999f - 1e-3f > qmax;
+                }
+                atomicAdd(&g_bin_stats[0], 1ull);
+                if (cull) atomicAdd(&g_bin_stats[1], 1ull);
+            }
+#endif
         }
 }
 
@@ -399,6 +426,20 @@ int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t 
     }
     if (result_in_alt) *result_in_alt = alt;
     return check_launch("hs_sort_pairs");
+}
+
+int hs_bin_stats(unsigned long long *host_out, int reset) {
+#ifdef HS_BIN_STATS
+    cudaMemcpyFromSymbol(host_out, g_bin_stats, sizeof(unsigned long long) * 2);
+    if (reset) {
+        const unsigned long long z[2] = {0, 0};
+        cudaMemcpyToSymbol(g_bin_stats, z, sizeof(z));
+    }
+#else
+    host_out[0] = host_out[1] = 0;
+    (void)reset;
+#endif
+    return check_launch("hs_bin_stats");
 }
 
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream) {
