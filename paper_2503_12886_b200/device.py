@@ -556,6 +556,8 @@ class Trainer:
         # init fused into the bucket holding the base colours
         ci_mode = (2 if self.pg is not None else 1) if ci else 0
         m = self._mark("adam")
+        if self.pg is None:                 # one rank: nothing to overlap, one launch
+            buckets = [(0, av.size)]
         for i, (lo, hi) in enumerate(buckets):
             if self.pg is not None:
                 s_cur = torch.cuda.current_stream()
