@@ -39,6 +39,15 @@ __device__ __forceinline__ float sigmoidf_ref(float x) {
     return ex / (1.0f + ex);
 }
 
+// The same two-branch sigmoid with the MUFU exp / reciprocal (a few ulp): the
+// projection's activations feed only tolerance-checked values (the key list is built
+// from the device's own fp32 projection, so binning stays bit-exact against it).
+__device__ __forceinline__ float sigmoid_fast(float x) {
+    if (x >= 0.0f) return __fdividef(1.0f, 1.0f + __expf(-x));
+    const float ex = __expf(x);
+    return __fdividef(ex, 1.0f + ex);
+}
+
 // S/quatmath.py:28-40 Hamilton product a (x) b
 __device__ __forceinline__ void quat_mul(const float a[4], const float b[4], float o[4]) {
     o[0] = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];

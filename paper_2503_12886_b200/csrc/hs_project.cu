@@ -52,7 +52,7 @@ __device__ __forceinline__ void project_one(const float pw[3], const float q[4],
     const float c12 = s0 * m[3] * m[6] + s1 * m[4] * m[7] + s2 * m[5] * m[8];
     const float c22 = s0 * m[6] * m[6] + s1 * m[7] * m[7] + s2 * m[8] * m[8];
     p.cov[0] = c00; p.cov[1] = c01; p.cov[2] = c02; p.cov[3] = c11; p.cov[4] = c12; p.cov[5] = c22;
-    const float inv_z = 1.0f / p.zc;
+    const float inv_z = __fdividef(1.0f, p.zc);
     p.j00 = fx * inv_z;
     p.j02 = -fx * p.xc * inv_z * inv_z;
     p.j11 = fy * inv_z;
@@ -67,12 +67,12 @@ __device__ __forceinline__ void project_one(const float pw[3], const float q[4],
     const float lam = mid + sqrtf(disc);
     p.rad = lam > 0.0f ? 3.0f * sqrtf(lam) : 0.0f;
     if (!(p.det > 0.0f) || !(p.rad >= kMinRadius)) return;
-    const float inv_det = 1.0f / p.det;
+    const float inv_det = __fdividef(1.0f, p.det);
     p.ca = p.s11 * inv_det;
     p.cb = -p.s01 * inv_det;
     p.cc = p.s00 * inv_det;
-    p.mx = fx * p.xc / p.zc + cx;
-    p.my = fy * p.yc / p.zc + cy;
+    p.mx = fx * p.xc * inv_z + cx;
+    p.my = fy * p.yc * inv_z + cy;
     p.valid = true;
 }
 
@@ -173,13 +173,14 @@ __device__ __forceinline__ bool avatar_world(int64_t N, int b, int64_t n, int F,
     const float nrm = sqrtf(a.qraw[0] * a.qraw[0] + a.qraw[1] * a.qraw[1] + a.qraw[2] * a.qraw[2] +
                             a.qraw[3] * a.qraw[3]);
     const bool ok = nrm >= 1e-30f;
+    const float rn = __fdividef(1.0f, nrm);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) a.qn[c] = a.qraw[c] / nrm;
+    for (int c = 0; c < 4; ++c) a.qn[c] = a.qraw[c] * rn;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) a.s[c] = expf(sr[c]);
-    a.op = sigmoidf_ref(opr);
+    for (int c = 0; c < 3; ++c) a.s[c] = __expf(sr[c]);
+    a.op = sigmoid_fast(opr);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) a.col[c] = sigmoidf_ref(colr[c]);
+    for (int c = 0; c < 3; ++c) a.col[c] = sigmoid_fast(colr[c]);
     // transform (S/binding.py:174-188)
     const float *fr = frames + ((int64_t)b * F + __ldg(tri + n)) * kFrame;
     a.R = fr;
@@ -192,8 +193,9 @@ __device__ __forceinline__ bool avatar_world(int64_t N, int b, int64_t n, int F,
     for (int c = 0; c < 4; ++c) a.qf[c] = fr[9 + c];
     quat_mul(a.qf, a.qn, a.qr);
     const float n2 = sqrtf(a.qr[0] * a.qr[0] + a.qr[1] * a.qr[1] + a.qr[2] * a.qr[2] + a.qr[3] * a.qr[3]);
+    const float rn2 = __fdividef(1.0f, n2);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) a.qw[c] = a.qr[c] / n2;
+    for (int c = 0; c < 4; ++c) a.qw[c] = a.qr[c] * rn2;
     return ok;
 }
 
@@ -281,7 +283,7 @@ __device__ __forceinline__ void preprocess_bwd_one(const Proj &p, const float q[
                                                    float g_pos[3], float g_q[4], float g_s[3]) {
     const float *rc = cam;
     const float fx = cam[12], fy = cam[13];
-    const float inv_z = 1.0f / p.zc;
+    const float inv_z = __fdividef(1.0f, p.zc);
     const float ca = p.ca, cb = p.cb, cc = p.cc;
     const float ga = gs[2], gb = 0.5f * gs[3], gc = gs[4];
     const float g00 = -(ca * (ca * ga + cb * gb) + cb * (ca * gb + cb * gc));
