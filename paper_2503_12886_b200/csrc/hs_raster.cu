@@ -431,6 +431,39 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
 #endif
 __device__ unsigned int g_raster_work[6];   // [fwd next, done, bwd next, done, train next, done]
 
+// Longest-first item order (HS_RASTER_LPT): tiles bucketed by the bit length of their
+// key count, heaviest bucket first, so the long tiles start early and the persistent
+// grid's tail is made of short items.  One small CTA per launch builds it.
+#ifndef HS_RASTER_LPT
+#define HS_RASTER_LPT 1
+#endif
+constexpr int kMaxOrder = 1 << 20;
+__device__ uint32_t g_tile_order[kMaxOrder];
+
+__global__ void __launch_bounds__(1024) tile_order_kernel(int total_tiles, int tile_bits, int tiles,
+                                                          const uint32_t *__restrict__ ranges) {
+    __shared__ uint32_t hist[33], cursor[33];
+    if (threadIdx.x < 33) hist[threadIdx.x] = 0;
+    __syncthreads();
+    auto bucket = [&](int t) {
+        const int b = t / tiles, tile = t % tiles;
+        const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[((int64_t)b << tile_bits) + tile];
+        const uint32_t len = rg.y - rg.x;
+        return 32 - __clz(len);          // 0 (empty) .. 32, heavier = larger
+    };
+    for (int t = threadIdx.x; t < total_tiles; t += blockDim.x) atomicAdd(&hist[bucket(t)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int k = 32; k >= 0; --k) {
+            cursor[k] = run;
+            run += hist[k];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < total_tiles; t += blockDim.x) g_tile_order[atomicAdd(&cursor[bucket(t)], 1u)] = t;
+}
+
 template <typename F>
 __device__ __forceinline__ void for_each_block(int B, int nblk, int lane, int warp, unsigned int *work, F &&fn) {
     if (!HS_RASTER_PERSIST) {
@@ -438,12 +471,19 @@ __device__ __forceinline__ void for_each_block(int B, int nblk, int lane, int wa
         return;
     }
     const int total = B * nblk;
+    const bool lpt = HS_RASTER_LPT && total / kBlocks <= kMaxOrder;
+    const int tiles = nblk / kBlocks;
     for (;;) {
         int item = 0;
         if (lane == 0) item = (int)atomicAdd(work, 1u);
         item = __shfl_sync(kFull, item, 0);
         if (item >= total) break;
-        fn(item / nblk, item % nblk);
+        if (lpt) {
+            const uint32_t bt = g_tile_order[item / kBlocks];
+            fn((int)(bt / tiles), (int)(bt % tiles) * kBlocks + item % kBlocks);
+        } else {
+            fn(item / nblk, item % nblk);
+        }
         __syncwarp();
     }
     if (lane == 0) {
@@ -718,6 +758,12 @@ static void launch_fwd_ci(int ci, dim3 grid, int nblk, cudaStream_t s, const Ras
 
 // grid of the raster kernels: one CTA per kCW blocks, or a persistent grid of
 // resident CTAs (HS_RASTER_PERSIST)
+static void launch_tile_order(int B, int nblk, int tile_bits, const uint32_t *ranges, cudaStream_t s) {
+    const int tiles = nblk / kBlocks;
+    if (HS_RASTER_PERSIST && HS_RASTER_LPT && B * tiles <= kMaxOrder)
+        tile_order_kernel<<<1, 1024, 0, s>>>(B * tiles, tile_bits, tiles, ranges);
+}
+
 static dim3 raster_grid(int nblk, int B) {
     if (!HS_RASTER_PERSIST) return dim3(nblk / kCW, B);
     int sms = 148;
@@ -760,6 +806,7 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
+    launch_tile_order(B, nblk, tile_bits, ranges, s);
     if (loss && img) launch_fwd_ci<true, true>(ci, grid, nblk, s, a);
     else if (loss) launch_fwd_ci<true, false>(ci, grid, nblk, s, a);
     else if (img) launch_fwd_ci<false, true>(ci, grid, nblk, s, a);
@@ -781,6 +828,7 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
+    launch_tile_order(B, nblk, tile_bits, ranges, s);
     if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a, nblk);
     else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a, nblk);
     return check_launch("hs_raster_bwd");
@@ -813,6 +861,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
+    launch_tile_order(B, nblk, tile_bits, ranges, s);
     switch (ci) {
         case 0: raster_train_kernel<0><<<grid, kRT, 0, s>>>(a, nblk); break;
         case 1: raster_train_kernel<1><<<grid, kRT, 0, s>>>(a, nblk); break;
