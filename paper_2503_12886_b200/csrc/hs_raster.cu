@@ -437,25 +437,32 @@ __device__ unsigned int g_raster_work[6];   // [fwd next, done, bwd next, done, 
 #ifndef HS_RASTER_LPT
 #define HS_RASTER_LPT 1
 #endif
+#ifndef HS_RASTER_LPT_SUB
+#define HS_RASTER_LPT_SUB 2
+#endif
 constexpr int kMaxOrder = 1 << 20;
 __device__ uint32_t g_tile_order[kMaxOrder];
 
 __global__ void __launch_bounds__(1024) tile_order_kernel(int total_tiles, int tile_bits, int tiles,
                                                           const uint32_t *__restrict__ ranges) {
-    __shared__ uint32_t hist[33], cursor[33];
-    if (threadIdx.x < 33) hist[threadIdx.x] = 0;
+    constexpr int kSub = HS_RASTER_LPT_SUB;         // sub-buckets per octave
+    constexpr int kNB = 33 << kSub;
+    __shared__ uint32_t hist[kNB], cursor[kNB];
+    for (int i = threadIdx.x; i < kNB; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     auto bucket = [&](int t) {
         const int b = t / tiles, tile = t % tiles;
         const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[((int64_t)b << tile_bits) + tile];
         const uint32_t len = rg.y - rg.x;
-        return 32 - __clz(len);          // 0 (empty) .. 32, heavier = larger
+        const int bl = 32 - __clz(len);            // 0 (empty) .. 32
+        const uint32_t sub = bl > kSub ? (len >> (bl - 1 - kSub)) & ((1u << kSub) - 1u) : 0u;
+        return (bl << kSub) | (int)sub;            // log-linear: heavier = larger
     };
     for (int t = threadIdx.x; t < total_tiles; t += blockDim.x) atomicAdd(&hist[bucket(t)], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t run = 0;
-        for (int k = 32; k >= 0; --k) {
+        for (int k = kNB - 1; k >= 0; --k) {
             cursor[k] = run;
             run += hist[k];
         }
