@@ -38,7 +38,7 @@ namespace hs {
 #define HS_RASTER_CTA_WARPS 1        // warps per CTA (each warp owns one 8 x 4*PX block)
 #endif
 #ifndef HS_RASTER_MINB
-#define HS_RASTER_MINB (64 / HS_RASTER_PX / HS_RASTER_CTA_WARPS)   // resident CTAs per SM the register budget must allow
+#define HS_RASTER_MINB (56 / HS_RASTER_PX / HS_RASTER_CTA_WARPS)   // resident CTAs per SM (28 one-warp CTAs: 72 registers)
 #endif
 
 #ifndef HS_RASTER_EXACT_CULL
