@@ -160,6 +160,29 @@ int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t 
 /* Diagnostics (-DHS_BIN_STATS builds; zeros otherwise): [keys emitted, keys whose
  * splat provably contributes to no pixel of the tile]; synchronous copy to host_out[2]. */
 int hs_bin_stats(unsigned long long *host_out, int reset);
+/* ---- Two-level binning (the training path): the same per-tile lists with 32-bit
+ * sort keys.
+ * hs_depth_order: stable sort of the B*N (frame, Gaussian) items by their float depth
+ *   bits -> order[j] = item index (ties to the lower index).  Always 4 passes; the
+ *   8-bit windows that depth_range ({min, max} emitted depth bits, written by the
+ *   projection) shows constant copy through, so no host read is needed -- it can run
+ *   while the host waits for hs_bin_scan.  keys_a/keys_b/order_alt are scratch (B*N),
+ *   workspace hs_sort_workspace_size(B*N) bytes.
+ * hs_bin_emit_sorted: each item in depth order writes its tiles' 32-bit keys
+ *   frame << tile_bits | tile and values n (block sums + scan + emission); block_sums /
+ *   block_offsets hold hs_scan_blocks(B*N) words.
+ * hs_sort_pairs32: hs_sort_pairs for 32-bit keys (frame/tile bits only: 2 passes).
+ * hs_tile_ranges32: ranges from the sorted 32-bit keys (zero-filled by the caller). */
+int hs_depth_order(int64_t num_items, const float *depth, const uint32_t *depth_range, uint32_t *order,
+                   uint32_t *order_alt, uint32_t *keys_a, uint32_t *keys_b, void *workspace,
+                   size_t workspace_bytes, void *stream);
+int hs_bin_emit_sorted(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
+                       const uint32_t *order, uint32_t *block_sums, uint32_t *block_offsets, uint32_t *keys,
+                       uint32_t *values, void *stream);
+int hs_sort_pairs32(int64_t num_keys, uint32_t bit_mask, uint32_t *keys, uint32_t *values,
+                    uint32_t *keys_alt, uint32_t *values_alt, void *workspace, size_t workspace_bytes,
+                    int *result_in_alt, void *stream);
+int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, void *stream);
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);
 

@@ -57,6 +57,10 @@ SIGNATURES = {
     "hs_raster_bwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _F, _P, _P]),
     "hs_loss_reduce": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "hs_raster_train": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P]),
+    "hs_depth_order": (_I, [_L, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "hs_bin_emit_sorted": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_sort_pairs32": (_I, [_L, ctypes.c_uint32, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
+    "hs_tile_ranges32": (_I, [_L, _P, _P, _P]),
     "hs_bin_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_raster_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_adam": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _P]),

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(int nb, const uint32_t *__re
         offs[i] = (uint32_t)run;
         run += sums[i];
     }
-    if (tid == 0) {
+    if (tid == 0 && summary) {
         summary[0] = warp_tot[(blockDim.x >> 5) - 1];
         summary[1] = err ? *err : HS_NO_ERROR;
         summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
@@ -125,6 +125,79 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
         }
 }
 
+// ---------------------------------------------------- two-level binning
+//
+// Same lists, fewer key bits per sort pass: the (frame, Gaussian) items are first
+// sorted by depth alone (32-bit keys over B*N items -- the float depth bits, stable,
+// ties to the lower frame-major index), then each item emits its tiles in that
+// order with 32-bit (frame, tile) keys, and a stable 2-pass sort by (frame, tile)
+// leaves every tile's list in depth order with ties to the lower Gaussian index --
+// the lists the one-level (frame, tile, depth) sort produces.
+
+// per 256 sorted items: sum of their tile counts (the emission-offset scan input)
+__global__ void __launch_bounds__(kScanBlock) sorted_block_sums_kernel(int64_t items, const uint32_t *__restrict__ order,
+                                                                       const uint32_t *__restrict__ counts,
+                                                                       uint32_t *__restrict__ block_sums) {
+    const int64_t j = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+    uint32_t v = j < items ? counts[order[j]] : 0u;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __shared__ uint32_t ws[kScanBlock / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < kScanBlock / 32; ++k) t += ws[k];
+        block_sums[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kScanBlock) emit_sorted_kernel(int64_t items, int64_t N, int tiles_x, int tile_bits,
+                                                                 const float *__restrict__ records,
+                                                                 const uint32_t *__restrict__ order,
+                                                                 const uint32_t *__restrict__ counts,
+                                                                 const uint32_t *__restrict__ offs,
+                                                                 uint32_t *__restrict__ keys,
+                                                                 uint32_t *__restrict__ vals) {
+    __shared__ uint32_t warp_tot[kScanBlock / 32];
+    const int64_t j = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+    const bool in = j < items;
+    const uint32_t i = in ? order[j] : 0u;
+    const uint32_t cnt = in ? counts[i] : 0u;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int k = 0; k < w; ++k) wpre += warp_tot[k];
+    if (!in || cnt == 0) return;
+    uint32_t pos = offs[blockIdx.x] + wpre + incl - cnt;
+    const uint32_t b = (uint32_t)(i / N);
+    const uint32_t n = (uint32_t)(i - (int64_t)b * N);
+    const float *rec = records + (int64_t)i * kRec;
+    const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);
+    const int ty0 = unpack_lo(rows) / kTile, ty1 = unpack_hi(rows) / kTile;
+    const int tx0 = unpack_lo(cols) / kTile, tx1 = unpack_hi(cols) / kTile;
+    const uint32_t hi = b << tile_bits;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            keys[pos] = hi | (uint32_t)(ty * tiles_x + tx);
+            vals[pos] = n;
+            ++pos;
+        }
+}
+
+__global__ void tile_ranges32_kernel(int64_t n, const uint32_t *__restrict__ keys, uint32_t *__restrict__ ranges) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = keys[i];
+    if (i == 0 || keys[i - 1] != t) ranges[2 * (uint64_t)t] = (uint32_t)i;
+    if (i == n - 1 || keys[i + 1] != t) ranges[2 * (uint64_t)t + 1] = (uint32_t)(i + 1);
+}
+
 // --------------------------------------------------------------- radix sort
 //
 // Stable LSD radix sort, onesweep style: one kernel computes the digit histograms
@@ -154,7 +227,8 @@ struct PassShifts {
     int n;
 };
 
-__global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const uint64_t *__restrict__ keys,
+template <typename KT>
+__global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const KT *__restrict__ keys,
                                                              PassShifts ps, uint32_t *__restrict__ hist) {
     __shared__ uint32_t h[kMaxPasses][kRadix];
     for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
@@ -166,7 +240,7 @@ __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const ui
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
         const int64_t i = i0 + lane;
         const bool valid = i < n;
-        const uint64_t k = valid ? keys[i] : 0ull;
+        const uint64_t k = valid ? (uint64_t)keys[i] : 0ull;
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
         for (int p = 0; p < ps.n; ++p) {
             const uint32_t d = (uint32_t)(k >> ps.shift[p]) & (kRadix - 1);
@@ -203,6 +277,16 @@ __global__ void __launch_bounds__(kRadix) radix_digit_scan_kernel(int npass, uin
     }
 }
 
+// Bits of the float depth keys that can differ among key-emitting splats: every bit at
+// or below the highest bit in which the smallest and largest emitted depth differ
+// (depth_range = {min, max} float bits; none emitted -> min > max -> 0).
+__device__ __forceinline__ uint32_t depth_live_bits(const uint32_t *depth_range) {
+    const uint32_t lo = depth_range[0], hi = depth_range[1];
+    if (lo > hi) return 0u;
+    const uint32_t diff = lo ^ hi;
+    return diff ? (0xFFFFFFFFu >> __clz(diff)) : 0u;
+}
+
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -212,15 +296,29 @@ __device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// vals_in == nullptr: the values are the input positions (an implicit iota).
+// live_bits != nullptr: a device word of the key bits that may vary (the depth sort
+// decides this on the device, before the step's host read): a pass whose 8-bit window
+// holds none of them copies its input unchanged (same order, parity kept).
+template <typename KT>
 __global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_kernel(int64_t n, int shift,
-                                                                      const uint64_t *__restrict__ keys_in,
+                                                                      const KT *__restrict__ keys_in,
                                                                       const uint32_t *__restrict__ vals_in,
-                                                                      uint64_t *__restrict__ keys_out,
+                                                                      KT *__restrict__ keys_out,
                                                                       uint32_t *__restrict__ vals_out,
                                                                       const uint32_t *__restrict__ digit_base,
                                                                       uint32_t *__restrict__ status,
-                                                                      uint32_t *__restrict__ counter) {
-    __shared__ uint64_t s_keys[kSortTile];
+                                                                      uint32_t *__restrict__ counter,
+                                                                      const uint32_t *__restrict__ live_bits) {
+    if (live_bits && ((depth_live_bits(live_bits) >> shift) & (kRadix - 1)) == 0u) {
+        for (int64_t i = blockIdx.x * (int64_t)kSortTile + threadIdx.x; i < n && i < (blockIdx.x + 1) * (int64_t)kSortTile;
+             i += kSortThreads) {
+            keys_out[i] = keys_in[i];
+            vals_out[i] = vals_in ? vals_in[i] : (uint32_t)i;
+        }
+        return;
+    }
+    __shared__ KT s_keys[kSortTile];
     __shared__ uint32_t s_vals[kSortTile];
     __shared__ uint32_t warp_hist[kSortThreads / 32][kRadix];
     __shared__ uint32_t digit_off[kRadix];
@@ -234,7 +332,7 @@ __global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_ker
     const uint32_t tile = s_tile;
     const int64_t base = (int64_t)tile * kSortTile;
 
-    uint64_t k_reg[kSortItems];
+    KT k_reg[kSortItems];
     uint32_t v_reg[kSortItems];
     uint32_t local[kSortItems];
     const uint32_t lt = (1u << lane) - 1u;
@@ -242,8 +340,8 @@ __global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_ker
     for (int i = 0; i < kSortItems; ++i) {
         const int64_t idx = base + w * (32 * kSortItems) + i * 32 + lane;
         const bool valid = idx < n;
-        k_reg[i] = valid ? keys_in[idx] : 0ull;
-        v_reg[i] = valid ? vals_in[idx] : 0u;
+        k_reg[i] = valid ? keys_in[idx] : (KT)0;
+        v_reg[i] = valid ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
     }
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
@@ -329,7 +427,7 @@ __global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_ker
     __syncthreads();
     const int cnt_tile = (int)min((int64_t)kSortTile, n - base);
     for (int j = tid; j < cnt_tile; j += kSortThreads) {
-        const uint64_t key = s_keys[j];
+        const KT key = s_keys[j];
         const uint32_t d = (uint32_t)(key >> shift) & (kRadix - 1);
         const uint32_t p = glob[d] + (uint32_t)j - digit_off[d];
         keys_out[p] = key;
@@ -383,24 +481,28 @@ size_t hs_sort_workspace_size(int64_t num_keys) {
                                kRadix + kMaxPasses);
 }
 
-int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t *values, uint64_t *keys_alt,
-                  uint32_t *values_alt, void *workspace, size_t workspace_bytes, int *result_in_alt,
-                  void *stream) {
+}  // extern "C"
+
+template <typename KT>
+static int sort_pairs_impl(const char *what, int64_t num_keys, uint64_t bit_mask, const KT *keys_in,
+                           const uint32_t *values_in, KT *keys, uint32_t *values, KT *keys_alt,
+                           uint32_t *values_alt, void *workspace,
+                           size_t workspace_bytes, int *result_in_alt, const uint32_t *depth_range,
+                           cudaStream_t s) {
     if (result_in_alt) *result_in_alt = 0;
     if (num_keys <= 0) return HS_OK;
     if (workspace_bytes < hs_sort_workspace_size(num_keys)) {
-        set_error("hs_sort_pairs: workspace too small (%zu < %zu)", workspace_bytes, hs_sort_workspace_size(num_keys));
+        set_error("%s: workspace too small (%zu < %zu)", what, workspace_bytes, hs_sort_workspace_size(num_keys));
         return HS_ERR_SHAPE;
     }
     if (num_keys > (int64_t)kCountMask) {
-        set_error("hs_sort_pairs: too many keys");
+        set_error("%s: too many keys", what);
         return HS_ERR_SHAPE;
     }
     PassShifts ps{};
-    for (int sh = 0; sh < 64; sh += 8)
+    for (int sh = 0; sh < (int)(8 * sizeof(KT)); sh += 8)
         if ((bit_mask >> sh) & 0xFFull) ps.shift[ps.n++] = sh;
     if (ps.n == 0) return HS_OK;
-    cudaStream_t s = HS_CHECK_STREAM(stream);
     const int tiles = (int)((num_keys + kSortTile - 1) / kSortTile);
     uint32_t *hist = reinterpret_cast<uint32_t *>(workspace);
     uint32_t *status = hist + (size_t)kMaxPasses * kRadix;
@@ -411,21 +513,90 @@ int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t 
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const unsigned hgrid = (unsigned)std::min<int64_t>(grid_for(num_keys, 256 * 8), (int64_t)sms * 4);
-    radix_hist_all_kernel<<<hgrid, 256, 0, s>>>(num_keys, keys, ps, hist);
+    radix_hist_all_kernel<KT><<<hgrid, 256, 0, s>>>(num_keys, keys_in, ps, hist);
     radix_digit_scan_kernel<<<1, kRadix, 0, s>>>(ps.n, hist);
-    uint64_t *ki = keys, *ko = keys_alt;
-    uint32_t *vi = values, *vo = values_alt;
-    int alt = 0;
+    // pass 0 reads keys_in (values implicit when values_in is null), then ping-pong;
+    // the caller passes (keys, values) as pass 0's source when they are the input
+    const KT *ki = keys_in;
+    const uint32_t *vi = values_in;
+    KT *ko = keys_alt;
+    uint32_t *vo = values_alt;
+    int alt = 1;
     for (int p = 0; p < ps.n; ++p) {
-        radix_onesweep_kernel<<<tiles, kSortThreads, 0, s>>>(num_keys, ps.shift[p], ki, vi, ko, vo,
-                                                             hist + (size_t)p * kRadix,
-                                                             status + (size_t)p * tiles * kRadix, counters + p);
-        uint64_t *tk = ki; ki = ko; ko = tk;
-        uint32_t *tv = vi; vi = vo; vo = tv;
+        radix_onesweep_kernel<KT><<<tiles, kSortThreads, 0, s>>>(num_keys, ps.shift[p], ki, vi, ko, vo,
+                                                                 hist + (size_t)p * kRadix,
+                                                                 status + (size_t)p * tiles * kRadix, counters + p,
+                                                                 depth_range);
+        ki = ko;
+        vi = vo;
+        ko = alt ? keys : keys_alt;
+        vo = alt ? values : values_alt;
         alt ^= 1;
     }
-    if (result_in_alt) *result_in_alt = alt;
-    return check_launch("hs_sort_pairs");
+    if (result_in_alt) *result_in_alt = alt ^ 1;
+    return check_launch(what);
+}
+
+extern "C" {
+
+int hs_sort_pairs(int64_t num_keys, uint64_t bit_mask, uint64_t *keys, uint32_t *values, uint64_t *keys_alt,
+                  uint32_t *values_alt, void *workspace, size_t workspace_bytes, int *result_in_alt,
+                  void *stream) {
+    return sort_pairs_impl<uint64_t>("hs_sort_pairs", num_keys, bit_mask, keys, values, keys, values, keys_alt,
+                                     values_alt, workspace, workspace_bytes, result_in_alt, nullptr,
+                                     HS_CHECK_STREAM(stream));
+}
+
+int hs_sort_pairs32(int64_t num_keys, uint32_t bit_mask, uint32_t *keys, uint32_t *values, uint32_t *keys_alt,
+                    uint32_t *values_alt, void *workspace, size_t workspace_bytes, int *result_in_alt,
+                    void *stream) {
+    return sort_pairs_impl<uint32_t>("hs_sort_pairs32", num_keys, bit_mask, keys, values, keys, values, keys_alt,
+                                     values_alt, workspace, workspace_bytes, result_in_alt, nullptr,
+                                     HS_CHECK_STREAM(stream));
+}
+
+int hs_depth_order(int64_t num_items, const float *depth, const uint32_t *depth_range, uint32_t *order,
+                   uint32_t *order_alt, uint32_t *keys_a, uint32_t *keys_b, void *workspace, size_t workspace_bytes,
+                   void *stream) {
+    if (num_items <= 0) return HS_OK;
+    // 4 passes over the depth bits; windows that the device-side depth range shows to be
+    // constant copy through, so the result lands in `order` without a host read
+    int alt = 0;
+    const int rc = sort_pairs_impl<uint32_t>("hs_depth_order", num_items, 0xFFFFFFFFull,
+                                             reinterpret_cast<const uint32_t *>(depth), nullptr, keys_b, order,
+                                             keys_a, order_alt, workspace, workspace_bytes, &alt, depth_range,
+                                             HS_CHECK_STREAM(stream));
+    if (rc == HS_OK && alt) {
+        set_error("hs_depth_order: internal parity error");
+        return HS_ERR_CUDA;
+    }
+    return rc;
+}
+
+int hs_bin_emit_sorted(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
+                       const uint32_t *order, uint32_t *block_sums, uint32_t *block_offsets, uint32_t *keys,
+                       uint32_t *values, void *stream) {
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
+    const int frame_bits = bit_length_u32((uint32_t)(B - 1));
+    if (tile_bits + frame_bits > 32) {
+        set_error("hs_bin_emit_sorted: frame/tile key bits %d + %d exceed 32", frame_bits, tile_bits);
+        return HS_ERR_SHAPE;
+    }
+    const int64_t items = (int64_t)B * N;
+    const int nb = hs_scan_blocks(items);
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    sorted_block_sums_kernel<<<nb, kScanBlock, 0, s>>>(items, order, counts, block_sums);
+    scan_kernel<<<1, 1024, 0, s>>>(nb, block_sums, block_offsets, nullptr, nullptr, nullptr);
+    emit_sorted_kernel<<<nb, kScanBlock, 0, s>>>(items, N, tiles_x, tile_bits, records, order, counts, block_offsets,
+                                                 keys, values);
+    return check_launch("hs_bin_emit_sorted");
+}
+
+int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, void *stream) {
+    if (num_keys <= 0) return HS_OK;
+    tile_ranges32_kernel<<<grid_for(num_keys, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(num_keys, keys, ranges);
+    return check_launch("hs_tile_ranges32");
 }
 
 int hs_bin_stats(unsigned long long *host_out, int reset) {

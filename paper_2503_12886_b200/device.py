@@ -254,6 +254,8 @@ class Binner:
         self.passes = 0
         self.ranges = None
         self.result = None
+        self.order = None
+        self._ordered = None
 
     def _ensure(self, total):
         if total <= self.cap and self.keys is not None:
@@ -274,15 +276,21 @@ class Binner:
         self.depth_range[1] = 0
         return self.depth_range
 
-    def scan(self, block_sums, nblocks, err):
+    def scan(self, block_sums, nblocks, err, overlap=None):
         """Exclusive scan of the per-block tile counts + the step's single D2H read
-        (key total, error word, depth-bit range)."""
+        (key total, error word, depth-bit range).  ``overlap`` (a callable) enqueues
+        work that needs no host answer after the read: the host then waits on the
+        read's event only, while the GPU runs that work."""
         if self.offsets is None or self.offsets.numel() < nblocks:
             self.offsets = torch.empty(max(nblocks, 1), dtype=torch.int32, device=self.device)
         L.call("hs_bin_scan", nblocks, _p(block_sums), _p(self.offsets), _p(err), _p(self.depth_range),
                _p(self.summary), _stream())
         self.summary_host.copy_(self.summary, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        ready = torch.cuda.Event()
+        ready.record()
+        if overlap is not None:
+            overlap()
+        ready.synchronize()
         total = int(self.summary_host[0])
         code = int(self.summary_host[1]) & 0xFFFFFFFFFFFFFFFF
         dr = int(self.summary_host[2]) & 0xFFFFFFFFFFFFFFFF
@@ -296,7 +304,26 @@ class Binner:
         depth_width = (lo ^ hi).bit_length() if lo <= hi else 32
         return (((1 << (tile_bits + frame_bits)) - 1) << 32) | ((1 << depth_width) - 1)
 
+    def depth_order(self, B, N, depth):
+        """Two-level binning, stage 1 (hs_depth_order): the (frame, Gaussian) items in
+        stable depth order.  Needs only the projection's outputs (no host read), so it
+        is enqueued before the scan and runs while the host waits for the key total."""
+        items = B * N
+        d = self.device
+        if self.order is None or self.order.numel() < items:
+            mk = lambda: torch.empty(items, dtype=torch.int32, device=d)
+            self.order, self.order_alt, self.dkeys_a, self.dkeys_b = mk(), mk(), mk(), mk()
+            self.dws = torch.empty(int(L.load().hs_sort_workspace_size(items)), dtype=torch.uint8, device=d)
+            nb = int(L.load().hs_scan_blocks(items))
+            self.sblock_sums = torch.empty(nb, dtype=torch.int32, device=d)
+            self.sblock_offs = torch.empty(nb, dtype=torch.int32, device=d)
+        L.call("hs_depth_order", items, _p(depth), _p(self.depth_range), _p(self.order), _p(self.order_alt),
+               _p(self.dkeys_a), _p(self.dkeys_b), _p(self.dws), self.dws.numel(), _stream())
+        self._ordered = (B, N)
+
     def bin(self, B, N, width, height, records, depth, counts, total):
+        if self._ordered == (B, N):
+            return self._bin_two_level(B, N, width, height, records, counts, total)
         tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
         self._ensure(total)
         s = _stream()
@@ -320,13 +347,42 @@ class Binner:
         self.result = (keys[:total], vals[:total], ranges, tile_bits, tiles)
         return self.result
 
+    def _bin_two_level(self, B, N, width, height, records, counts, total):
+        """Stage 2: emission in depth order with 32-bit (frame, tile) keys and a stable
+        sort of those keys alone (frame + tile bits: 2 passes at C2) -- the same
+        per-tile lists as the one-level (frame, tile, depth) sort."""
+        self._ordered = None
+        tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
+        self._ensure(total)
+        s = _stream()
+        nr = B << tile_bits
+        if self.ranges is None or self.ranges.numel() < 2 * nr:
+            self.ranges = torch.empty(2 * nr, dtype=torch.int32, device=self.device)
+        ranges = self.ranges[:2 * nr]
+        ranges.zero_()
+        k32, k32_alt = self.keys.view(torch.int32), self.keys_alt.view(torch.int32)
+        if total:
+            L.call("hs_bin_emit_sorted", B, N, width, height, _p(records), _p(counts), _p(self.order),
+                   _p(self.sblock_sums), _p(self.sblock_offs), _p(k32), _p(self.vals), s)
+            alt = ctypes.c_int(0)
+            mask = (1 << (tile_bits + frame_bits)) - 1
+            self.passes = sum(1 for sh in range(0, 32, 8) if (mask >> sh) & 0xFF)
+            L.call("hs_sort_pairs32", total, ctypes.c_uint32(mask), _p(k32), _p(self.vals), _p(k32_alt),
+                   _p(self.vals_alt), _p(self.ws), self.ws.numel(), ctypes.byref(alt), s)
+            keys, vals = (k32_alt, self.vals_alt) if alt.value else (k32, self.vals)
+            L.call("hs_tile_ranges32", total, _p(keys), _p(ranges), s)
+        else:
+            keys, vals = k32, self.vals
+        self.result = (keys[:total], vals[:total], ranges, tile_bits, tiles)
+        return self.result
 
-def launches_binning(total, passes):
-    """Kernel launches issued by Binner.bin (emit, histogram, digit scan, one per pass,
-    ranges) -- for the bench's gpu_launches count."""
+
+def launches_binning(total, passes, two_level=False):
+    """Kernel launches issued by Binner.bin (emit (3 for the sorted emission), histogram,
+    digit scan, one per pass, ranges) -- for the bench's gpu_launches count."""
     if not total:
         return 0
-    return 1 + 2 + passes + 1
+    return (3 if two_level else 1) + 2 + passes + 1
 
 
 # -------------------------------------------------------------------- trainer
@@ -354,6 +410,7 @@ class Trainer:
         self.av = avatar
         self.rig = rig              # DeviceRig: frames computed from theta on device
         self.fused_raster = True    # hs_raster_train (False: hs_raster_fwd + hs_raster_bwd)
+        self.two_level_binning = True   # depth order + 32-bit tile sort (False: one 64-bit sort)
         self.W, self.H = int(width), int(height)
         self.B = int(batch)
         self.global_batch = int(global_batch or batch)
@@ -471,8 +528,13 @@ class Trainer:
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
                    _p(self.counts), _p(self.block_sums), _p(self.binner.reset_depth_range()), _p(self.radius),
                    _p(self.err), s)
+        overlap = None
+        if self.two_level_binning:
+            def overlap():      # the depth order runs while the host waits for the key total
+                self.binner.depth_order(B, N, self.depth)
+            self.launches += 7
         m = self._mark("bin_scan+sync")
-        total, code = self.binner.scan(self.block_sums, self.nblocks, self.err)
+        total, code = self.binner.scan(self.block_sums, self.nblocks, self.err, overlap)
         self._done(m)
         self.launches += 1
         # the error word also carries a colour-init failure of the previous step's
@@ -484,7 +546,7 @@ class Trainer:
         m = self._mark("bin_sort")
         res = self.binner.bin(B, N, self.W, self.H, self.records, self.depth, self.counts, total)
         self._done(m)
-        self.launches += launches_binning(total, self.binner.passes)
+        self.launches += launches_binning(total, self.binner.passes, self.two_level_binning)
         return F, res
 
     def _cameras(self, cameras):

@@ -144,6 +144,19 @@ def test_preprocess_nonfinite_raises_with_index():
 
 # --------------------------------------------------------------------- binning
 
+def check_two_level(dev, res, tag=""):
+    """Two-level binning (depth order, then 32-bit (frame, tile) keys; the training
+    path) on the same projection: the same lists and ranges as the oracle."""
+    bn = dev["binner"]          # its depth range is the projection's
+    bn.depth_order(dev["B"], dev["N"], dev["depth"])
+    keys, vals, ranges, tile_bits, tiles = bn.bin(dev["B"], dev["N"], dev["W"], dev["H"], dev["records"],
+                                                  dev["depth"], dev["counts"], dev["total"])
+    k = keys.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(k, res["keys"] >> np.uint64(32)), tag
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32), res["values"]), tag
+    r = ranges.view(-1, 2).cpu().numpy().view(np.uint32)[:res["ranges"].shape[1]]
+    assert np.array_equal(r, res["ranges"][0]), tag
+
 def test_binning_bit_exact():
     from paper_2503_12886_b200 import compat as C
     for s, p, d, world, cam in scenes():
@@ -161,6 +174,7 @@ def test_binning_bit_exact():
         assert np.array_equal(r, res["ranges"][0]), s
         live = (rad[0] > 0) & (rec[:, 5] >= np.float32(1 / 255))
         np.testing.assert_array_equal(bbox[live], res["bbox"][0][live])
+        check_two_level(dev, res, s)
 
 
 @pytest.mark.parametrize("n", [200, 1000, 9000])
@@ -185,6 +199,7 @@ def test_binning_bit_exact_crowded_tiles(n):
     assert np.array_equal(vals.cpu().numpy().view(np.uint32), res["values"])
     r = ranges.view(-1, 2).cpu().numpy().view(np.uint32)[:res["ranges"].shape[1]]
     assert np.array_equal(r, res["ranges"][0])
+    check_two_level(dev, res, n)
 
 
 # --------------------------------------------------------------------- raster
