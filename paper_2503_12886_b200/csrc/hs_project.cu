@@ -216,11 +216,20 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     const int32_t *__restrict__ tri, const float *__restrict__ bary, const float *__restrict__ frames,
     const float *__restrict__ cams, float *__restrict__ records, float *__restrict__ depth,
     uint32_t *__restrict__ counts, uint32_t *__restrict__ block_sums, uint32_t *__restrict__ depth_range,
-    float *__restrict__ radius, unsigned long long *err) {
+    float *__restrict__ radius, float *__restrict__ zero_gsplat, float *__restrict__ zero_maxw,
+    float *__restrict__ zero_wsums, unsigned long long *err) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
     float dz = 0.f;
     if (i < (int64_t)B * N) {
+        // the step's per-(frame, splat) accumulators, zeroed here instead of by
+        // separate fills: the raster adds into them with atomics
+        if (zero_gsplat) {
+#pragma unroll
+            for (int k = 0; k < kGS; ++k) zero_gsplat[i * kGS + k] = 0.f;
+        }
+        if (zero_maxw) zero_maxw[i] = 0.f;
+        if (zero_wsums) reinterpret_cast<float4 *>(zero_wsums)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         const int b = (int)(i / N);
         const int64_t n = i - (int64_t)b * N;
         AvatarWorld a;
@@ -457,8 +466,8 @@ int hs_scan_blocks(int64_t num_items) { return (int)((num_items + kScanBlock - 1
 int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const float *raw10,
                           const float *base14, const int32_t *tri_index, const float *bary, const float *frames,
                           const float *cameras, float *records, float *depth, uint32_t *counts,
-                          uint32_t *block_sums, uint32_t *depth_range, float *radius, unsigned long long *err,
-                          void *stream) {
+                          uint32_t *block_sums, uint32_t *depth_range, float *radius, float *zero_gsplat,
+                          float *zero_maxw, float *zero_wsums, unsigned long long *err, void *stream) {
     if (B < 1 || N < 1 || width < 1 || height < 1 || width > 32767 || height > 32767) {
         set_error("hs_project_avatar_fwd: bad sizes B=%d N=%lld %dx%d", B, (long long)N, width, height);
         return HS_ERR_SHAPE;
@@ -466,7 +475,7 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
     const int64_t items = (int64_t)B * N;
     project_avatar_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream)>>>(
         B, N, F, width, height, raw10, base14, tri_index, bary, frames, cameras, records, depth, counts,
-        block_sums, depth_range, radius, err);
+        block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, err);
     return check_launch("hs_project_avatar_fwd");
 }
 

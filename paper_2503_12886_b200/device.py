@@ -514,7 +514,7 @@ class Trainer:
         self.launches += 1
         return self._rig_frames
 
-    def _forward_project(self, thetas, frames, cameras):
+    def _forward_project(self, thetas, frames, cameras, zero=(None, None, None)):
         av = self.av
         N, K, B = av.N, av.K, self.B
         s = _stream()
@@ -527,7 +527,7 @@ class Trainer:
         self._call("project_fwd", "hs_project_avatar_fwd", B, N, F, self.W, self.H, _p(self.raw10), _p(av.base14),
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
                    _p(self.counts), _p(self.block_sums), _p(self.binner.reset_depth_range()), _p(self.radius),
-                   _p(self.err), s)
+                   *(_p(z) for z in zero), _p(self.err), s)
         overlap = None
         if self.two_level_binning:
             def overlap():      # the depth order runs while the host waits for the key total
@@ -563,21 +563,20 @@ class Trainer:
         N, K, B = av.N, av.K, self.B
         cameras = self._cameras(cameras)
         self._bucket_events = []
-        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras)
+        ci = self.color_init and not self._all_visited()
+        # the raster's accumulators are zero-filled by the projection pass
+        zero = (self.g_splat, self.maxw if ci else None, self.wsums if ci else None)
+        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero)
         frames = self._last_frames
         s = _stream()
-        ci = self.color_init and not self._all_visited()
         flags = L.RASTER_LOSS
         if ci:
             flags |= L.RASTER_MAXW_UNVISITED | L.RASTER_WSUMS
-            self.maxw.zero_()
-            self.wsums.zero_()
         if self._targets_ready is not None:     # step_from_host: targets arrive on the copy stream
             torch.cuda.current_stream().wait_event(self._targets_ready)
             self._targets_ready = None
         # d loss_b / d pred = sign / (H W 3) / B_global  (S/metrics.py:19-22, S/train.py:244)
         grad_scale = 1.0 / (self.H * self.W * 3.0) / self.global_batch
-        self.g_splat.zero_()
         if self.fused_raster:
             # forward + adjoint of every pixel block in one pass (hs_raster_train)
             self._call("raster", "hs_raster_train", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
