@@ -287,15 +287,19 @@ def run_b200(args, cfg):
 
     # ---- end-to-end through the host API (pinned H2D inputs, D2H losses) every step
     h = {k: v.cpu().numpy() for k, v in d.items()}
+    # a training loop's input pipeline: each call uploads the next step's inputs on the
+    # copy stream under its own compute (double-buffered), so every step of the timed
+    # region still pays one batch of H2D copies and one D2H read
+    hb = (h["thetas"], h["targets"], None, h["cameras"], h["backgrounds"])
     for _ in range(2):
-        tr.step_from_host(h["thetas"], h["targets"], None, h["cameras"], h["backgrounds"])
+        tr.step_from_host(*hb, prefetch=hb)
     barrier()
     e2e_ms = 0.0
     for _ in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        tr.step_from_host(h["thetas"], h["targets"], None, h["cameras"], h["backgrounds"])
+        tr.step_from_host(*hb, prefetch=hb)
         e2e_ms += (time.perf_counter() - t0) * 1000.0
     t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:

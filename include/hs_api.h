@@ -314,6 +314,11 @@ int hs_gather_rows(int num_rows, int64_t row_bytes, const int32_t *slots, const 
 int hs_image_metrics(int B, int H, int W, const float *pred, const uint8_t *target_rgba, double *sums,
                      void *stream);
 
+/* Page-lock / release a host buffer for the end-to-end input path (failures leave no
+ * sticky CUDA error; HS_ERR_CUDA + hs_last_error). */
+int hs_host_register(void *ptr, size_t bytes);
+int hs_host_unregister(void *ptr);
+
 /* ---- Elementwise compat ops (model.py:219-248, binding.py:174-204) ------- */
 int hs_activate_fwd(int64_t N, const float *raw14, float *act14, unsigned long long *err, void *stream);
 int hs_activate_bwd(int64_t N, const float *raw14, const float *act14, const float *g_act14,

@@ -66,6 +66,8 @@ SIGNATURES = {
     "hs_raster_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_adam": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _P]),
     "hs_image_metrics": (_I, [_I, _I, _I, _P, _P, _P, _P]),
+    "hs_host_register": (_I, [_P, _Z]),
+    "hs_host_unregister": (_I, [_P]),
     "hs_gather_rows": (_I, [_I, _L, _P, _P, _P, _P]),
     "hs_rig_frames": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_adam_fused": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _L, _L, _I, _I, _P, _P,

@@ -54,4 +54,27 @@ int hs_gather_rows(int num_rows, int64_t row_bytes, const int32_t *slots, const 
     return check_launch("hs_gather_rows");
 }
 
+// Page-lock a caller's host buffer in place (end-to-end inputs DMA'd without a staging
+// copy).  A failure (e.g. the range overlaps a registered one) is reported and the
+// runtime error state cleared, so the caller can fall back to staging.
+int hs_host_register(void *ptr, size_t bytes) {
+    const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("hs_host_register: %s", cudaGetErrorString(e));
+        return HS_ERR_CUDA;
+    }
+    return HS_OK;
+}
+
+int hs_host_unregister(void *ptr) {
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("hs_host_unregister: %s", cudaGetErrorString(e));
+        return HS_ERR_CUDA;
+    }
+    return HS_OK;
+}
+
 }  // extern "C"

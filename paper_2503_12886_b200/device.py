@@ -467,6 +467,8 @@ class Trainer:
         self._registered = {}           # page-locked caller arrays
         self._staging = {}
         self._dev_in = {}
+        self._slot = 0                  # input buffer set of the next uploaded step
+        self._pending = None            # (batch key, device inputs, event, slot) of a prefetch
         # host staging for the end-to-end path (pinned)
 
     # --------------------------------------------------------------- profiling
@@ -726,20 +728,26 @@ class Trainer:
         pinned staging buffer."""
         a = np.asarray(arr)
         if a.dtype == dtype and a.flags.c_contiguous and a.nbytes >= (1 << 16):
-            key = (a.__array_interface__["data"][0], a.nbytes)
+            # register the array that owns the memory (views of one buffer share it)
+            root = a
+            while isinstance(root.base, np.ndarray):
+                root = root.base
+            if not root.flags.c_contiguous:
+                root = a
+            key = (root.__array_interface__["data"][0], root.nbytes)
             hit = self._registered.get(key)
             if hit is None:
-                t = torch.from_numpy(a)
-                rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), a.nbytes, 0)
-                if int(rc) == 0:
+                t = torch.from_numpy(root)
+                if L.load().hs_host_register(ctypes.c_void_p(t.data_ptr()), root.nbytes) == L.HS_OK:
                     if len(self._registered) >= 32:          # bounded: drop the oldest
                         old_key, (old_a, old_t) = next(iter(self._registered.items()))
                         torch.cuda.synchronize()
-                        torch.cuda.cudart().cudaHostUnregister(old_t.data_ptr())
+                        L.load().hs_host_unregister(ctypes.c_void_p(old_t.data_ptr()))
                         del self._registered[old_key]
-                    hit = self._registered[key] = (a, t)     # keeps the array alive
+                    hit = self._registered[key] = (root, t)  # keeps the memory alive
+                # else: overlapping / unsupported range -> pinned staging below
             if hit is not None:
-                return hit[1]
+                return torch.from_numpy(a)
         a = np.ascontiguousarray(a, dtype)
         st = self._staging.get(name)
         if st is None or st.shape != a.shape:
@@ -747,44 +755,89 @@ class Trainer:
         st.numpy()[...] = a
         return st
 
-    def _device_buf(self, name, host):
-        d = self._dev_in.get(name)
+    def _device_buf(self, name, host, slot=0):
+        key = (slot, name)
+        d = self._dev_in.get(key)
         if d is None or d.shape != host.shape or d.dtype != host.dtype:
-            d = self._dev_in[name] = torch.empty(host.shape, dtype=host.dtype, device=self.av.device)
+            d = self._dev_in[key] = torch.empty(host.shape, dtype=host.dtype, device=self.av.device)
         return d
 
-    def step_from_host(self, thetas, targets, frames, cameras, backgrounds):
+    @staticmethod
+    def _batch_key(arrays):
+        return tuple((k, id(v), np.asarray(v).__array_interface__["data"][0], np.shape(v))
+                     for k, v in sorted(arrays.items()) if v is not None)
+
+    def _upload(self, slot, arrays):
+        """Every input of one step H2D on the copy stream into buffer set `slot`;
+        returns (device tensors, completion event)."""
+        dt = {"thetas": np.float32, "targets": np.uint8, "frames": np.float32, "cameras": np.float32,
+              "backgrounds": np.float32}
+        dev = {}
+        with torch.cuda.stream(self._copy):
+            for k, v in arrays.items():
+                if v is None:
+                    continue
+                h = self._host_view(f"{k}{slot}", v, dt[k])
+                d = self._device_buf(k, h, slot)
+                d.copy_(h, non_blocking=True)
+                dev[k] = d
+            ev = torch.cuda.Event()
+            ev.record(self._copy)
+        return dev, ev
+
+    def step_from_host(self, thetas, targets, frames, cameras, backgrounds, prefetch=None):
         """End-to-end step through host buffers (numpy): H2D copies, the device step
         and the D2H read of the losses.  Returns StepResult.
 
         The small inputs go first on the compute stream; the targets (the bulk of the
         bytes) go on a copy stream and only the forward raster waits for them, so
         their transfer overlaps the MLP, blend, projection and sort.  frames may be
-        None when the Trainer holds a DeviceRig (mesh frames computed from theta)."""
+        None when the Trainer holds a DeviceRig (mesh frames computed from theta).
+
+        ``prefetch`` = the next step's (thetas, targets, frames, cameras, backgrounds):
+        its copies are enqueued on the copy stream right after this step's kernels
+        (double-buffered device inputs), so they run under this step's compute and the
+        next call finds its inputs on the device -- the input pipeline of a training loop."""
         if self._copy is None:
             self._copy = torch.cuda.Stream(device=self.av.device)
             self._loss_host = torch.empty(2 * self.B + 1, dtype=torch.float32, pin_memory=True)
-        small = {"thetas": (thetas, np.float32), "cameras": (cameras, np.float32),
-                 "backgrounds": (backgrounds, np.float32)}
-        if frames is not None:
-            small["frames"] = (frames, np.float32)
-        dev = {}
-        for k, (v, dt) in small.items():
-            h = self._host_view(k, v, dt)
-            d = self._device_buf(k, h)
-            d.copy_(h, non_blocking=True)
-            dev[k] = d
-        h = self._host_view("targets", targets, np.uint8)
-        d = self._device_buf("targets", h)
-        self._copy.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(self._copy):
-            d.copy_(h, non_blocking=True)
-            ready = torch.cuda.Event()
-            ready.record(self._copy)
-        self._targets_ready = ready
+        arrays = {"thetas": thetas, "targets": targets, "frames": frames, "cameras": cameras,
+                  "backgrounds": backgrounds}
+        key = self._batch_key(arrays)
+        cur = torch.cuda.current_stream()
+        if self._pending is not None and self._pending[0] == key:
+            _, dev, ev, slot = self._pending
+            self._pending = None
+            cur.wait_event(ev)
+            d = dev["targets"]
+        else:
+            slot = self._slot
+            small = {"thetas": (thetas, np.float32), "cameras": (cameras, np.float32),
+                     "backgrounds": (backgrounds, np.float32)}
+            if frames is not None:
+                small["frames"] = (frames, np.float32)
+            dev = {}
+            for k, (v, dt) in small.items():
+                h = self._host_view(f"{k}{slot}", v, dt)
+                dd = self._device_buf(k, h, slot)
+                dd.copy_(h, non_blocking=True)
+                dev[k] = dd
+            h = self._host_view(f"targets{slot}", targets, np.uint8)
+            d = self._device_buf("targets", h, slot)
+            self._copy.wait_stream(cur)
+            with torch.cuda.stream(self._copy):
+                d.copy_(h, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(self._copy)
+            self._targets_ready = ready
         self.step(dev["thetas"], d, dev.get("frames"), dev["cameras"], dev["backgrounds"])
         self._loss_host.copy_(self.loss_out, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        self._slot = 1 - slot
+        if prefetch is not None:
+            nxt = dict(zip(("thetas", "targets", "frames", "cameras", "backgrounds"), prefetch))
+            ndev, nev = self._upload(self._slot, nxt)
+            self._pending = (self._batch_key(nxt), ndev, nev, self._slot)
+        cur.synchronize()
         lo = self._loss_host.numpy()
         B = self.B
         return StepResult(float(lo[2 * B]), lo[B:2 * B].copy(), lo[:B].copy(), self.last_total)
@@ -794,7 +847,7 @@ class Trainer:
         if self._registered:
             torch.cuda.synchronize()
             for a, t in self._registered.values():
-                torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
+                L.load().hs_host_unregister(ctypes.c_void_p(t.data_ptr()))
             self._registered.clear()
 
     def __del__(self):

@@ -160,3 +160,29 @@ def test_compat_mesh_frames_drop_in():
     bad.uv_coords = d["bad_uv.uv_coords"]
     with pytest.raises(L.DegenerateTriangleError, match=str(d["bad_uv.message"])):
         compat.mesh_frames(bad, d["verts"][0])
+
+
+def test_step_from_host_prefetch_pipeline():
+    """step_from_host with prefetch (double-buffered uploads) gives the same losses as
+    uploads on demand, across a sequence of distinct batches."""
+    from paper_2503_12886_b200 import synth
+    from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
+    import oracle as O
+    wl = synth.make_workload(40, 12, 96, distinct_frames=12)
+    av = wl.avatar
+    mk = lambda: Trainer(AvatarParams.from_host(O.GSet(*(av.base[a] for a in ("position", "rotation", "scale",
+                                                                                   "opacity", "color"))),
+                                                av.deltas, av.mlp, av.tri_index, av.barycentric), 96, 96, 4,
+                         rig=DeviceRig(wl.rig))
+    cams = np.tile(wl.camera.packed(), (4, 1))
+    th = np.asarray(wl.thetas, np.float32)
+    bg = np.asarray(wl.backgrounds, np.float32)
+    batches = [(np.ascontiguousarray(th[i:i + 4]), np.ascontiguousarray(wl.targets[i:i + 4]), None, cams,
+                np.ascontiguousarray(bg[i:i + 4])) for i in (0, 4, 8, 0)]
+    a, b = mk(), mk()
+    la = [a.step_from_host(*x).loss for x in batches]
+    lb = [b.step_from_host(*x, prefetch=batches[i + 1] if i + 1 < len(batches) else None).loss
+          for i, x in enumerate(batches)]
+    np.testing.assert_allclose(lb, la, rtol=1e-6)
+    a.close()
+    b.close()
