@@ -227,6 +227,9 @@ struct PassShifts {
     int n;
 };
 
+#ifndef HS_HIST32_PLAIN_BELOW
+#define HS_HIST32_PLAIN_BELOW 16   // depth-order histogram: plain atomics for the two low windows
+#endif
 template <typename KT>
 __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const KT *__restrict__ keys,
                                                              PassShifts ps, uint32_t *__restrict__ hist) {
@@ -244,7 +247,12 @@ __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const KT
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
         for (int p = 0; p < ps.n; ++p) {
             const uint32_t d = (uint32_t)(k >> ps.shift[p]) & (kRadix - 1);
-            if (valid) {
+            if (!valid) continue;
+            if (sizeof(KT) == 4 && ps.shift[p] < HS_HIST32_PLAIN_BELOW) {
+                // the low depth-mantissa digits of the depth order are close to random
+                // across neighbouring items: plain shared atomics beat the match
+                atomicAdd(&h[p][d], 1u);
+            } else {
                 const uint32_t peers = __match_any_sync(vmask, d);
                 if ((peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
             }
