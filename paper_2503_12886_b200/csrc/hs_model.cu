@@ -269,7 +269,10 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
 constexpr int kBT = 256;
 constexpr int kBMaxB = 16;
 constexpr int kBMaxK = 32;
-constexpr int kBBlocks = 592;   // persistent grid: 148 SMs x 4 CTAs
+#ifndef HS_BLEND_BLOCKS
+#define HS_BLEND_BLOCKS 444          // one wave at 3 CTAs per SM (148 x 3)
+#endif
+constexpr int kBBlocks = HS_BLEND_BLOCKS;   // persistent grid
 #ifndef HS_BLEND_KBB
 #define HS_BLEND_KBB 8
 #endif
