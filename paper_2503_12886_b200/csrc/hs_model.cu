@@ -820,7 +820,11 @@ int hs_adam_fused(int64_t N, int K, int64_t mlp_size, float *params, const float
                      (uintptr_t)grads % 16 == 0 && (uintptr_t)m % 16 == 0 && (uintptr_t)v % 16 == 0;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const unsigned grid = (unsigned)std::min<int64_t>(grid_for((end - begin) / (vec ? 4 : 1), 256), (int64_t)sms * 8);
+#ifndef HS_ADAM_CTAS_PER_SM
+#define HS_ADAM_CTAS_PER_SM 8
+#endif
+    const unsigned grid = (unsigned)std::min<int64_t>(grid_for((end - begin) / (vec ? 4 : 1), 256),
+                                                      (int64_t)sms * HS_ADAM_CTAS_PER_SM);
     cudaStream_t s = HS_CHECK_STREAM(stream);
     if (vec) {
         if (ci == 0) adam_kernel<0, true><<<grid, 256, 0, s>>>(a);
