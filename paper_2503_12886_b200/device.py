@@ -461,6 +461,8 @@ class Trainer:
         self._comm = None
         self._bucket_events = []
         self._rig_frames = None
+        self._rig_event = None
+        self._side = None               # side stream: the rig runs concurrently with mlp_fwd + blend_fwd
         self._last_frames = None
         self._copy = None               # H2D copy stream of step_from_host
         self._targets_ready = None
@@ -510,11 +512,24 @@ class Trainer:
             raise ValueError("frames is None and the Trainer has no DeviceRig")
         if self._rig_frames is None:
             self._rig_frames = torch.empty(self.B, self.rig.F, 22, dtype=torch.float32, device=self.av.device)
-        m = self._mark("rig_frames")
-        self.rig.frames(thetas, out=self._rig_frames, err=self.err)     # errors surface at the scan read
-        self._done(m)
+        # the rig depends on theta only: it runs on a side stream concurrently with
+        # mlp_fwd + blend_fwd, and project_fwd waits for it
+        side = self._side_stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            m = self._mark("rig_frames")
+            self.rig.frames(thetas, out=self._rig_frames, err=self.err)     # errors surface at the scan read
+            self._done(m)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        self._rig_event = ev
         self.launches += 1
         return self._rig_frames
+
+    def _side_stream(self):
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.av.device)
+        return self._side
 
     def _forward_project(self, thetas, frames, cameras, zero=(None, None, None)):
         av = self.av
@@ -526,6 +541,9 @@ class Trainer:
         self._call("blend_fwd", "hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(self.psi),
                    _p(self.raw10), s)
         F = frames.shape[-2] if frames.dim() == 3 else frames.numel() // (B * 22)
+        if self._rig_event is not None:
+            torch.cuda.current_stream().wait_event(self._rig_event)
+            self._rig_event = None
         self._call("project_fwd", "hs_project_avatar_fwd", B, N, F, self.W, self.H, _p(self.raw10), _p(av.base14),
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
                    _p(self.counts), _p(self.block_sums), _p(self.binner.reset_depth_range()), _p(self.radius),
