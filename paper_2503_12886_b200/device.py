@@ -462,7 +462,8 @@ class Trainer:
         self._bucket_events = []
         self._rig_frames = None
         self._rig_event = None
-        self._side = None               # side stream: the rig runs concurrently with mlp_fwd + blend_fwd
+        self._side = None               # side stream: rig || mlp_fwd + blend_fwd, loss || backward,
+        self._side_events = []          # base/delta Adam || mlp_bwd
         self._last_frames = None
         self._copy = None               # H2D copy stream of step_from_host
         self._targets_ready = None
@@ -605,8 +606,15 @@ class Trainer:
                        None, s)
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the rest of the backward
-            self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
-                       _p(self.loss_out), s, kernels=2)
+            # the loss is only read after the step: reduce it on the side stream
+            side = self._side_stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
+                           _p(self.loss_out), _stream(), kernels=2)
+                loss_ev = torch.cuda.Event()
+                loss_ev.record(side)
+            self._side_events.append(loss_ev)
         else:
             self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
@@ -625,31 +633,50 @@ class Trainer:
                    _p(self.grads), _p(self.grads[14 * N:]), _p(self.gpsi_partials), ctypes.byref(nparts), s,
                    kernels=(B + 15) // 16)
         buckets = self.buckets()
+        ci_mode = (2 if self.pg is not None else 1) if ci else 0
+        self.step_count += 1
         if self.pg is not None:           # base + delta buckets reduce while mlp_bwd runs
             self._allreduce_buckets(buckets[:-1])
+        else:
+            # one rank: Adam on base + deltas (+ colour init) needs only blend_bwd's output;
+            # it runs on the side stream while mlp_bwd runs
+            side = self._side_stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                m = self._mark("adam")
+                self._adam(0, 14 * N + 10 * K * N, ci_mode, _stream())
+                self._done(m)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            self._side_events.append(ev)
         self._call("mlp_bwd", "hs_mlp_bwd", B, av.H, av.D, K, _p(av.mlp), _p(thetas), _p(self.cache),
                    _p(self.gpsi_partials), nparts.value, _p(self.gpsi), _p(self.mlp_scratch),
                    _p(self.grads[14 * N + 10 * K * N:]), s, kernels=2)
         if self.pg is not None:
             self._allreduce_buckets(buckets[-1:])
-        self.step_count += 1
-        # multi-tensor Adam per bucket (each waits only for its own reduction), colour
-        # init fused into the bucket holding the base colours
-        ci_mode = (2 if self.pg is not None else 1) if ci else 0
-        m = self._mark("adam")
-        if self.pg is None:                 # one rank: nothing to overlap, one launch
-            buckets = [(0, av.size)]
-        for i, (lo, hi) in enumerate(buckets):
-            if self.pg is not None:
-                s_cur = torch.cuda.current_stream()
-                s_cur.wait_event(self._bucket_events[i])
-            L.call("hs_adam_fused", N, K, av.mlp_size, _p(av.params), _p(self.grads), _p(self.m), _p(self.v),
-                   self.lrs, self.step_count, ADAM_BETAS[0], ADAM_BETAS[1], ADAM_EPS, lo, hi, ci_mode, B,
-                   _p(self.maxw), _p(self.wsums), _p(self.packed), _p(self.est4), ctypes.c_float(self.threshold),
-                   _p(self.visited), _p(self.n_init), _p(self.err), s)
-            self.launches += 1
-        self._done(m)
+            # multi-tensor Adam per bucket (each waits only for its own reduction), colour
+            # init fused into the bucket holding the base colours
+            m = self._mark("adam")
+            for i, (lo, hi) in enumerate(buckets):
+                torch.cuda.current_stream().wait_event(self._bucket_events[i])
+                self._adam(lo, hi, ci_mode, s)
+            self._done(m)
+        else:
+            m = self._mark("adam_mlp")
+            self._adam(14 * N + 10 * K * N, av.size, 0, s)
+            self._done(m)
+        for ev in self._side_events:      # the step ends when the side-stream work has
+            torch.cuda.current_stream().wait_event(ev)
+        self._side_events = []
         return self.loss_out
+
+    def _adam(self, lo, hi, ci_mode, stream):
+        av = self.av
+        L.call("hs_adam_fused", av.N, av.K, av.mlp_size, _p(av.params), _p(self.grads), _p(self.m), _p(self.v),
+               self.lrs, self.step_count, ADAM_BETAS[0], ADAM_BETAS[1], ADAM_EPS, lo, hi, ci_mode, self.B,
+               _p(self.maxw), _p(self.wsums), _p(self.packed), _p(self.est4), ctypes.c_float(self.threshold),
+               _p(self.visited), _p(self.n_init), _p(self.err), stream)
+        self.launches += 1
 
     def buckets(self):
         """Flat-gradient buckets [lo, hi): the base block (holds the colour segment
