@@ -167,9 +167,9 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
         const float dxlo = (float)xs + 0.5f - A.x, dxhi = (float)xe + 0.5f - A.x;
         const float dylo = (float)ys + 0.5f - A.y, dyhi = (float)ye + 0.5f - A.y;
         const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
-        const float dyv = fminf(fmaxf(-b * dxv / c, dylo), dyhi);
+        const float dyv = fminf(fmaxf(__fdividef(-b * dxv, c), dylo), dyhi);   // (margin covers the approx.)
         const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
-        const float dxh = fminf(fmaxf(-b * dyh / a, dxlo), dxhi);
+        const float dxh = fminf(fmaxf(__fdividef(-b * dyh, a), dxlo), dxhi);
         const float qv = a * dxv * dxv + 2.f * b * dxv * dyv + c * dyv * dyv;
         const float qh = a * dxh * dxh + 2.f * b * dxh * dyh + c * dyh * dyh;
         // margin for the fp32 rounding of this bound and of the per-pixel q
