@@ -320,6 +320,12 @@ def run_b200(args, cfg):
                 traffic = json.load(f).get(dom)
         except Exception:
             pass
+        issue = None                     # the bound that actually limits the rasterizer
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_issue.json")) as f:
+                issue = json.load(f).get(dom)
+        except Exception:
+            pass
         step_bytes = sum(sb.values())
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -335,7 +341,8 @@ def run_b200(args, cfg):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                          else "fallback (B200_PROFILING.md)",
-                         "algorithmic_bytes_per_launch": sb[dom]},
+                         "algorithmic_bytes_per_launch": sb[dom],
+                         "issue_bound": issue},
             "step_roofline": {"algorithmic_bytes_per_step": step_bytes,
                               "achieved_gbs": step_bytes / (ms / 1000.0) / 1e9,
                               "frac": step_bytes / (ms / 1000.0) / 1e9 / peak},
