@@ -553,7 +553,7 @@ class Trainer:
         if self.two_level_binning:
             def overlap():      # the depth order runs while the host waits for the key total
                 self.binner.depth_order(B, N, self.depth)
-            self.launches += 7
+            self.launches += 6        # depth order: histogram, digit scan, 4 passes
         m = self._mark("bin_scan+sync")
         total, code = self.binner.scan(self.block_sums, self.nblocks, self.err, overlap)
         self._done(m)
@@ -603,7 +603,7 @@ class Trainer:
             self._call("raster", "hs_raster_train", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), _p(self.visited), _p(self.maxw),
                        _p(self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale), _p(self.g_splat), None,
-                       None, s)
+                       None, s, kernels=2)      # tile order + the fused raster
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the rest of the backward
             # the loss is only read after the step: reduce it on the side stream
