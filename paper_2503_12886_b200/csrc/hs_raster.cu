@@ -135,7 +135,9 @@ __device__ __forceinline__ void pixels_of(int w, int l, int tx, int ty, int &px,
 
 // Stage one splat record into the lane's slot.  Returns bit 0: the warp's block
 // [x0, x0+7] x [y0, y0+4 kPX-1] can hold a contributing pixel; bit 1: the splat's
-// integer bbox covers the whole block (the per-pixel bbox test can be skipped).
+// integer bbox covers the whole block (the per-pixel bbox test can be skipped);
+// bit 2+p: row group p (every lane's p-th pixel) can hold one -- a group the splat
+// cannot reach is skipped by the whole warp.
 template <bool kCull = true>
 __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
                                             uint32_t saddr) {
@@ -153,29 +155,41 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
                  "f"(0.f));
     if (!kCull) return 0u;
     if (!(qmax >= 0.f)) return 0u;
-    // pixels of the block the reference's bbox admits
-    const int xs = max(x0, cl), xe = min(x0 + 7, ch), ys = max(y0, rl), ye = min(y0 + 4 * kPX - 1, rh);
-    if (xs > xe || ys > ye) return 0u;
+    // columns of the block the reference's bbox admits
+    const int xs = max(x0, cl), xe = min(x0 + 7, ch);
+    if (xs > xe) return 0u;
     const bool full = cl <= x0 && ch >= x0 + 7 && rl <= y0 && rh >= y0 + 4 * kPX - 1;
     const float det = a * c - b * b;
-    if (HS_RASTER_EXACT_CULL && det > 0.f && a > 0.f && c > 0.f) {
-        // minimum of q(d) = a dx^2 + 2b dx dy + c dy^2 over the rectangle spanned by
-        // those pixel centres (d = centre - mean).  For a positive-definite q the
-        // minimiser is the mean if it lies inside, else on a rectangle edge facing it;
-        // the two candidate segments (x nearest the mean with the best y, and vice
-        // versa) are both inside the rectangle, so their minimum is the exact one.
-        const float dxlo = (float)xs + 0.5f - A.x, dxhi = (float)xe + 0.5f - A.x;
-        const float dylo = (float)ys + 0.5f - A.y, dyhi = (float)ye + 0.5f - A.y;
-        const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
-        const float dyv = fminf(fmaxf(__fdividef(-b * dxv, c), dylo), dyhi);   // (margin covers the approx.)
-        const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
-        const float dxh = fminf(fmaxf(__fdividef(-b * dyh, a), dxlo), dxhi);
-        const float qv = a * dxv * dxv + 2.f * b * dxv * dyv + c * dyv * dyv;
-        const float qh = a * dxh * dxh + 2.f * b * dxh * dyh + c * dyh * dyh;
-        // margin for the fp32 rounding of this bound and of the per-pixel q
-        if (fminf(qv, qh) * 0.999f - 1e-3f > qmax) return 0u;
+    const bool exact = HS_RASTER_EXACT_CULL && det > 0.f && a > 0.f && c > 0.f;
+    const float dxlo = (float)xs + 0.5f - A.x, dxhi = (float)xe + 0.5f - A.x;
+    const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
+    const float dyv0 = __fdividef(-b * dxv, c);                 // (margin covers the approx.)
+    uint32_t groups = 0u;
+#pragma unroll
+    for (int p = 0; p < kPX; ++p) {
+        // row group p (the lanes' p-th pixels: rows y0 + 4p .. y0 + 4p + 3)
+        const int ys = max(y0 + 4 * p, rl), ye = min(y0 + 4 * p + 3, rh);
+        if (ys > ye) continue;
+        bool hit = true;
+        if (exact) {
+            // minimum of q(d) = a dx^2 + 2b dx dy + c dy^2 over the rectangle spanned
+            // by those pixel centres (d = centre - mean).  For a positive-definite q the
+            // minimiser is the mean if it lies inside, else on a rectangle edge facing
+            // it; the two candidate segments (x nearest the mean with the best y, and
+            // vice versa) are both inside the rectangle, so their minimum is exact.
+            const float dylo = (float)ys + 0.5f - A.y, dyhi = (float)ye + 0.5f - A.y;
+            const float dyv = fminf(fmaxf(dyv0, dylo), dyhi);
+            const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
+            const float dxh = fminf(fmaxf(__fdividef(-b * dyh, a), dxlo), dxhi);
+            const float qv = a * dxv * dxv + 2.f * b * dxv * dyv + c * dyv * dyv;
+            const float qh = a * dxh * dxh + 2.f * b * dxh * dyh + c * dyh * dyh;
+            // margin for the fp32 rounding of this bound and of the per-pixel q
+            hit = !(fminf(qv, qh) * 0.999f - 1e-3f > qmax);
+        }
+        if (hit) groups |= 4u << p;
     }
-    return 1u | ((uint32_t)full << 1);
+    if (!groups) return 0u;
+    return 1u | ((uint32_t)full << 1) | groups;
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
@@ -186,11 +200,11 @@ template <bool kExplicitGrad>
 __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
                                                 uint32_t start, uint32_t last, const float (&g)[kPX][3],
                                                 float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
-                                                int lane, uint32_t wbase, const uint2 *masks);
+                                                int lane, uint32_t wbase, const uint4 *masks);
 
 template <bool kLoss, bool kImage, int CI, bool kTrain = false>
 __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int gw, int nblk, int lane,
-                                                 uint32_t wbase, uint2 *masks = nullptr) {
+                                                 uint32_t wbase, uint4 *masks = nullptr) {
     // gw = tile * kBlocks + blk: the pixel block of frame b this warp composites
     const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -254,9 +268,13 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         uint32_t bits = __ballot_sync(kFull, code & 1u);
         const uint32_t fullb = __ballot_sync(kFull, code & 2u);
         const uint32_t wantb = __ballot_sync(kFull, want);
+        uint32_t grpb[kPX];
+#pragma unroll
+        for (int p = 0; p < kPX; ++p) grpb[p] = __ballot_sync(kFull, code & (4u << p));
         if (kTrain && lane == 0) {
             const uint32_t k = (c0 - start) >> 5;
-            if (k < (uint32_t)kMaskBatches) masks[k] = make_uint2(bits, fullb);
+            if (k < (uint32_t)kMaskBatches)
+                masks[k] = make_uint4(bits, fullb, grpb[0], kPX > 1 ? grpb[kPX > 1 ? 1 : 0] : 0u);
         }
 #ifdef HS_RASTER_STATS
         st_batches += lane == 0;
@@ -291,6 +309,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             // update predicated on the reference's tests (bbox, q <= qmax, cutoff)
 #pragma unroll
             for (int p = 0; p < kPX; ++p) {
+                if (!((grpb[p] >> j) & 1u)) continue;          // warp-uniform: group out of reach
                 const float e2 = splat_e2(dx, fpy[p] - p0.y, kadx, p0.w, p1.x);
                 const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
                 const bool ok = live[p] && inb[p] && e2 >= p1.y && alpha >= kAlphaCutoff;
@@ -568,7 +587,7 @@ template <bool kExplicitGrad>
 __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
                                                 uint32_t start, uint32_t last, const float (&g)[kPX][3],
                                                 float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
-                                                int lane, uint32_t wbase, const uint2 *masks) {
+                                                int lane, uint32_t wbase, const uint4 *masks) {
     const float fpx = (float)px;
     int py[kPX];
     float fpy[kPX];
@@ -582,12 +601,14 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
         const uint32_t c0 = start + 32u * (uint32_t)k;
         const uint32_t c_end = min(c0 + 32u, last);
         const uint32_t live_lanes = c_end - c0 >= 32u ? kFull : (1u << (c_end - c0)) - 1u;
-        uint32_t bits, fullb;
+        uint32_t bits, fullb, grpb[kPX];
         const uint32_t idx = c0 + lane;
-        if (masks != nullptr && k < kMaskBatches) {
-            const uint2 m = masks[k];
+        if (masks != nullptr && k < kMaskBatches && kPX <= 2) {
+            const uint4 m = masks[k];
             bits = m.x & live_lanes;
             fullb = m.y;
+            grpb[0] = m.z;
+            if (kPX > 1) grpb[kPX > 1 ? 1 : 0] = m.w;
             if (bits == 0u) continue;                      // warp-uniform
             if ((bits >> lane) & 1u) {
                 const uint32_t n = a.vals[idx];
@@ -603,6 +624,8 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
             }
             bits = __ballot_sync(kFull, code & 1u);
             fullb = __ballot_sync(kFull, code & 2u);
+#pragma unroll
+            for (int p = 0; p < kPX; ++p) grpb[p] = __ballot_sync(kFull, code & (4u << p));
         }
         __syncwarp();
         while (bits) {
@@ -633,6 +656,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
             // (1 / (1 - 0) == 1 exactly) and adds zeros to the gradients
 #pragma unroll
             for (int p = 0; p < kPX; ++p) {
+                if (!((grpb[p] >> j) & 1u)) continue;          // warp-uniform: group out of reach
                 const float dy = fpy[p] - p0.y;
                 const float e2 = splat_e2(dx, dy, kadx, p0.w, p1.x);
                 const float G0 = ex2_approx(e2);
@@ -690,7 +714,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
 template <int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    __shared__ uint2 s_masks[kCW][kMaskBatches];
+    __shared__ uint4 s_masks[kCW][kMaskBatches];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
     for_each_block(a.B, nblk, lane, warp, g_raster_work + 4, [&](int b, int gw) {
