@@ -195,16 +195,17 @@ __device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, u
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
 //     3 max weight + weight sums for splats whose Gaussian is not yet visited.
 constexpr int kMaskBatches = 64;     // per-warp hit masks kept from the forward for the fused adjoint
+constexpr int kMaskWords = 2 + kPX;  // per batch: hit, full-cover, one per row group
 
 template <bool kExplicitGrad>
 __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
                                                 uint32_t start, uint32_t last, const float (&g)[kPX][3],
                                                 float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
-                                                int lane, uint32_t wbase, const uint4 *masks);
+                                                int lane, uint32_t wbase, const uint32_t *masks);
 
 template <bool kLoss, bool kImage, int CI, bool kTrain = false>
 __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int gw, int nblk, int lane,
-                                                 uint32_t wbase, uint4 *masks = nullptr) {
+                                                 uint32_t wbase, uint32_t *masks = nullptr) {
     // gw = tile * kBlocks + blk: the pixel block of frame b this warp composites
     const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -274,7 +275,13 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         if (kTrain && lane == 0) {
             const uint32_t k = (c0 - start) >> 5;
             if (k < (uint32_t)kMaskBatches)
-                masks[k] = make_uint4(bits, fullb, grpb[0], kPX > 1 ? grpb[kPX > 1 ? 1 : 0] : 0u);
+            {
+                uint32_t *m = masks + k * kMaskWords;
+                m[0] = bits;
+                m[1] = fullb;
+#pragma unroll
+                for (int p = 0; p < kPX; ++p) m[2 + p] = grpb[p];
+            }
         }
 #ifdef HS_RASTER_STATS
         st_batches += lane == 0;
@@ -587,7 +594,7 @@ template <bool kExplicitGrad>
 __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
                                                 uint32_t start, uint32_t last, const float (&g)[kPX][3],
                                                 float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
-                                                int lane, uint32_t wbase, const uint4 *masks) {
+                                                int lane, uint32_t wbase, const uint32_t *masks) {
     const float fpx = (float)px;
     int py[kPX];
     float fpy[kPX];
@@ -603,12 +610,12 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
         const uint32_t live_lanes = c_end - c0 >= 32u ? kFull : (1u << (c_end - c0)) - 1u;
         uint32_t bits, fullb, grpb[kPX];
         const uint32_t idx = c0 + lane;
-        if (masks != nullptr && k < kMaskBatches && kPX <= 2) {
-            const uint4 m = masks[k];
-            bits = m.x & live_lanes;
-            fullb = m.y;
-            grpb[0] = m.z;
-            if (kPX > 1) grpb[kPX > 1 ? 1 : 0] = m.w;
+        if (masks != nullptr && k < kMaskBatches) {
+            const uint32_t *m = masks + k * kMaskWords;
+            bits = m[0] & live_lanes;
+            fullb = m[1];
+#pragma unroll
+            for (int p = 0; p < kPX; ++p) grpb[p] = m[2 + p];
             if (bits == 0u) continue;                      // warp-uniform
             if ((bits >> lane) & 1u) {
                 const uint32_t n = a.vals[idx];
@@ -714,7 +721,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
 template <int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    __shared__ uint4 s_masks[kCW][kMaskBatches];
+    __shared__ uint32_t s_masks[kCW][kMaskBatches * kMaskWords];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
     for_each_block(a.B, nblk, lane, warp, g_raster_work + 4, [&](int b, int gw) {
