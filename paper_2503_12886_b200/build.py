@@ -9,6 +9,7 @@ the GPU box.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -47,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, extra=())
     if not force and not extra and out is None and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj" if not extra else "obj_" + str(abs(hash(tuple(extra)))))
+    objdir = os.path.join(LIBDIR, "obj" if not extra else "obj_" + hashlib.sha1(" ".join(extra).encode()).hexdigest()[:12])
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -62,6 +63,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, extra=())
         logs.append(f"== {src}\n{out}")
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{out}")
+    os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
     tmp = target + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)

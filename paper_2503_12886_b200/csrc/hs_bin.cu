@@ -173,21 +173,23 @@ __global__ void __launch_bounds__(kScanBlock) emit_sorted_kernel(int64_t items, 
     __syncthreads();
     uint32_t wpre = 0;
     for (int k = 0; k < w; ++k) wpre += warp_tot[k];
-    if (!in || cnt == 0) return;
-    uint32_t pos = offs[blockIdx.x] + wpre + incl - cnt;
-    const uint32_t b = (uint32_t)(i / N);
-    const uint32_t n = (uint32_t)(i - (int64_t)b * N);
-    const float *rec = records + (int64_t)i * kRec;
-    const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);
-    const int ty0 = unpack_lo(rows) / kTile, ty1 = unpack_hi(rows) / kTile;
-    const int tx0 = unpack_lo(cols) / kTile, tx1 = unpack_hi(cols) / kTile;
-    const uint32_t hi = b << tile_bits;
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            keys[pos] = hi | (uint32_t)(ty * tiles_x + tx);
-            vals[pos] = n;
-            ++pos;
-        }
+    if (in && cnt) {
+        uint32_t pos = offs[blockIdx.x] + wpre + incl - cnt;
+        const uint32_t b = (uint32_t)(i / N);
+        const uint32_t n = (uint32_t)(i - (int64_t)b * N);
+        const float *rec = records + (int64_t)i * kRec;
+        const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);
+        const int ty0 = unpack_lo(rows) / kTile, ty1 = unpack_hi(rows) / kTile;
+        const int tx0 = unpack_lo(cols) / kTile, tx1 = unpack_hi(cols) / kTile;
+        const uint32_t hi = b << tile_bits;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) {
+                const uint32_t key = hi | (uint32_t)(ty * tiles_x + tx);
+                keys[pos] = key;
+                vals[pos] = n;
+                ++pos;
+            }
+    }
 }
 
 __global__ void tile_ranges32_kernel(int64_t n, const uint32_t *__restrict__ keys, uint32_t *__restrict__ ranges) {
@@ -219,16 +221,24 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = HS_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per CTA
 constexpr int kRadix = 256;
+#ifndef HS_LOOKBACK
+#define HS_LOOKBACK 8
+#endif
+constexpr int kLookback = HS_LOOKBACK;
 constexpr int kMaxPasses = 8;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1u;
 
 struct PassShifts {
     int shift[kMaxPasses];
     int n;
+    int plain_below;   // windows below this shift count with plain shared atomics
 };
 
 #ifndef HS_HIST32_PLAIN_BELOW
 #define HS_HIST32_PLAIN_BELOW 16   // depth-order histogram: plain atomics for the two low windows
+#endif
+#ifndef HS_TILE_PLAIN_BELOW
+#define HS_TILE_PLAIN_BELOW 16     // tile sort: plain atomics for both windows (measured best)
 #endif
 template <typename KT>
 __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const KT *__restrict__ keys,
@@ -248,9 +258,9 @@ __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const KT
         for (int p = 0; p < ps.n; ++p) {
             const uint32_t d = (uint32_t)(k >> ps.shift[p]) & (kRadix - 1);
             if (!valid) continue;
-            if (sizeof(KT) == 4 && ps.shift[p] < HS_HIST32_PLAIN_BELOW) {
-                // the low depth-mantissa digits of the depth order are close to random
-                // across neighbouring items: plain shared atomics beat the match
+            if (ps.shift[p] < ps.plain_below) {
+                // digits close to random across neighbouring keys (the low depth-mantissa
+                // bytes, the tile's low byte): plain shared atomics beat the match
                 atomicAdd(&h[p][d], 1u);
             } else {
                 const uint32_t peers = __match_any_sync(vmask, d);
@@ -399,17 +409,17 @@ __global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_ker
             st_relaxed(st, kFlagInc | cnt);
         } else {
             st_relaxed(st, kFlagAgg | cnt);
-            // windowed look-back: 8 predecessor words per round (independent loads),
-            // consumed in order until an inclusive prefix is found
+            // windowed look-back: kLookback predecessor words per round (independent
+            // loads), consumed in order until an inclusive prefix is found
             int64_t j = (int64_t)tile - 1;
             bool found = false;
             while (!found) {
-                uint32_t v[8];
+                uint32_t v[kLookback];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < kLookback; ++k)
                     v[k] = (j - k >= 0) ? ld_relaxed(status + (size_t)(j - k) * kRadix + tid) : kFlagInc;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
+                for (int k = 0; k < kLookback; ++k) {
                     if (found) break;
                     if (v[k] == 0u) break;          // not published yet: retry from this tile
                     excl += v[k] & kCountMask;
@@ -496,7 +506,7 @@ static int sort_pairs_impl(const char *what, int64_t num_keys, uint64_t bit_mask
                            const uint32_t *values_in, KT *keys, uint32_t *values, KT *keys_alt,
                            uint32_t *values_alt, void *workspace,
                            size_t workspace_bytes, int *result_in_alt, const uint32_t *depth_range,
-                           cudaStream_t s) {
+                           cudaStream_t s, int plain_below = 0) {
     if (result_in_alt) *result_in_alt = 0;
     if (num_keys <= 0) return HS_OK;
     if (workspace_bytes < hs_sort_workspace_size(num_keys)) {
@@ -508,6 +518,7 @@ static int sort_pairs_impl(const char *what, int64_t num_keys, uint64_t bit_mask
         return HS_ERR_SHAPE;
     }
     PassShifts ps{};
+    ps.plain_below = plain_below;
     for (int sh = 0; sh < (int)(8 * sizeof(KT)); sh += 8)
         if ((bit_mask >> sh) & 0xFFull) ps.shift[ps.n++] = sh;
     if (ps.n == 0) return HS_OK;
@@ -520,7 +531,10 @@ static int sort_pairs_impl(const char *what, int64_t num_keys, uint64_t bit_mask
     cudaMemsetAsync(counters, 0, sizeof(uint32_t) * kMaxPasses, s);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const unsigned hgrid = (unsigned)std::min<int64_t>(grid_for(num_keys, 256 * 8), (int64_t)sms * 4);
+#ifndef HS_HIST_CTAS_PER_SM
+#define HS_HIST_CTAS_PER_SM 4
+#endif
+    const unsigned hgrid = (unsigned)std::min<int64_t>(grid_for(num_keys, 256 * 8), (int64_t)sms * HS_HIST_CTAS_PER_SM);
     radix_hist_all_kernel<KT><<<hgrid, 256, 0, s>>>(num_keys, keys_in, ps, hist);
     radix_digit_scan_kernel<<<1, kRadix, 0, s>>>(ps.n, hist);
     // pass 0 reads keys_in (values implicit when values_in is null), then ping-pong;
@@ -560,7 +574,7 @@ int hs_sort_pairs32(int64_t num_keys, uint32_t bit_mask, uint32_t *keys, uint32_
                     void *stream) {
     return sort_pairs_impl<uint32_t>("hs_sort_pairs32", num_keys, bit_mask, keys, values, keys, values, keys_alt,
                                      values_alt, workspace, workspace_bytes, result_in_alt, nullptr,
-                                     HS_CHECK_STREAM(stream));
+                                     HS_CHECK_STREAM(stream), HS_TILE_PLAIN_BELOW);
 }
 
 int hs_depth_order(int64_t num_items, const float *depth, const uint32_t *depth_range, uint32_t *order,
@@ -573,7 +587,7 @@ int hs_depth_order(int64_t num_items, const float *depth, const uint32_t *depth_
     const int rc = sort_pairs_impl<uint32_t>("hs_depth_order", num_items, 0xFFFFFFFFull,
                                              reinterpret_cast<const uint32_t *>(depth), nullptr, keys_b, order,
                                              keys_a, order_alt, workspace, workspace_bytes, &alt, depth_range,
-                                             HS_CHECK_STREAM(stream));
+                                             HS_CHECK_STREAM(stream), HS_HIST32_PLAIN_BELOW);
     if (rc == HS_OK && alt) {
         set_error("hs_depth_order: internal parity error");
         return HS_ERR_CUDA;
