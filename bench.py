@@ -119,6 +119,9 @@ def stage_bytes(B, N, K, H, D, W, Hh, keys, params, color_init=True, passes=6):
         "rig_frames": B * 1024 * 22 * 4 + 561 * 11 * 3 * 8,
         "project_fwd": B * N * (40 + rec + 4 + 4) + N * 32 + B * 1024 * 22 * 4,
         "bin_sort": keys * (12 + 8 + passes * 24 + 8),   # emit, histogram, passes, ranges
+        # tile-major: count + scatter read the bbox words, scatter writes key + value,
+        # the list sort reads value + depth and writes the value
+        "bin_tiles": keys * (8 + 12) + B * N * 2 * (8 + 4),
         "raster_fwd": keys * (4 + rec) + B * HW * (4 + 4 + 4) + (B * N * 20 if color_init else 0),
         "raster_bwd": keys * (4 + rec) + B * HW * 8 + B * N * 36,
         # fused forward + adjoint: both key walks, targets once, no per-pixel state round trip

@@ -186,6 +186,29 @@ int hs_sort_pairs32(int64_t num_keys, uint32_t bit_mask, uint32_t *keys, uint32_
                     uint32_t *keys_alt, uint32_t *values_alt, void *workspace, size_t workspace_bytes,
                     int *result_in_alt, void *stream);
 int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, void *stream);
+
+/* ---- Tile-major binning (the training path; same lists as the sorts above)
+ * hs_tile_count: each (frame, splat) with counts[i] > 0 adds one to every tile of its
+ *   pixel bbox in tile_counts [B << tile_bits] (zero on entry; hs_tile_scan re-zeroes it).
+ * hs_tile_scan: ranges [2 * (B << tile_bits)] (every entry written), scatter cursors
+ *   [B << tile_bits], the segment lists by length class (lists [3 * (B << tile_bits)],
+ *   list_counts [8]) and
+ *   summary [4] = {key total, error word, depth range as hs_bin_scan, longest list}.
+ * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
+ *   list in (depth, Gaussian index) order -- the reference order.  Skipped on the device
+ *   when summary[0] > capacity (grow the buffers, reset the cursors to the range starts
+ *   and call again).  Lists longer than hs_tile_sort_cap() are scattered but NOT sorted:
+ *   when summary[3] exceeds the cap, bin that step with the two-level sort instead. */
+int hs_tile_sort_cap(void);
+int hs_tile_count(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
+                  uint32_t *tile_counts, void *stream);
+int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,
+                 uint32_t *lists, uint32_t *list_counts, const unsigned long long *err,
+                 const uint32_t *depth_range, unsigned long long *summary, void *stream);
+int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
+                 const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
+                 uint32_t *list_counts, const unsigned long long *summary, uint64_t capacity,
+                 uint32_t *keys, uint32_t *values, void *stream);
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);
 

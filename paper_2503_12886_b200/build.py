@@ -20,7 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libhs_b200.so")
-SOURCES = ["hs_model.cu", "hs_project.cu", "hs_bin.cu", "hs_raster.cu", "hs_rig.cu", "hs_pool.cu", "hs_metrics.cu"]
+SOURCES = ["hs_model.cu", "hs_project.cu", "hs_bin.cu", "hs_tiles.cu", "hs_raster.cu", "hs_rig.cu", "hs_pool.cu", "hs_metrics.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]

@@ -1,0 +1,598 @@
+// hs_tiles.cu -- tile-major binning on sm_100a (the training path's binner).
+//
+// The per-(frame, tile) lists the reference order implies (S/render.py:221-223:
+// a stable depth argsort per frame, then the splats covering each tile in that
+// order) are built tile-first instead of by a global key sort:
+//
+//   hs_tile_count  every (frame, splat) adds one to each tile of its pixel bbox
+//   hs_tile_scan   one CTA: exclusive scan of the counts -> ranges + scatter cursors,
+//                  the segments sorted into three lists by length, and the step's
+//                  single device->host summary (key total, error word, depth range,
+//                  longest list)
+//   hs_tile_fill   scatter (an atomic cursor per tile, arrival order), then each list
+//                  sorted by the 64-bit key (depth bits << 32 | Gaussian index): a
+//                  register bitonic sort per warp up to 32 entries, a shared-memory
+//                  bitonic sort per warp up to kWarpCap, per CTA up to kCtaCap
+//
+// Sorting each list by (depth bits, index) is exactly the reference's order: positive
+// float depths compare like their bit patterns and the stable argsort breaks ties by
+// the lower index (oracle/binning.py).  Lists longer than kCtaCap are left to the
+// caller, which sees the longest length in the summary and falls back to the global
+// two-level sort (hs_depth_order + hs_bin_emit_sorted + hs_sort_pairs32) for that step.
+#include <algorithm>
+
+#include "hs_common.cuh"
+
+namespace hs {
+
+constexpr int kWarpShort = 256;       // warp-sorted lists up to this length go last
+constexpr int kWarpCap = 1024;        // longest list one warp sorts in shared memory
+constexpr int kCtaCap = 8192;         // longest list one CTA sorts in shared memory
+constexpr int kCtaSortThreads = 512;
+constexpr int kWarpSortWarps = 4;     // warps per CTA of the warp-level sort
+
+// ------------------------------------------------------------------- count
+
+// A CTA covers kTileItems consecutive (frame, Gaussian) items -- neighbours on the
+// UV grid, so they hit few, shared tiles.  Items of the CTA's first frame count
+// into a shared-memory histogram over that frame's tiles (flushed with one global
+// atomic per touched tile); items past a frame boundary, or every item when the
+// frame has too many tiles for shared memory, add to the global counters directly.
+constexpr int kTileItems = 1024;
+constexpr int kTileThreads = 256;
+constexpr int kTileSmemBins = 12288;   // tiles per frame the shared histogram holds (48 KB)
+
+struct TileBox {
+    int ty0, ty1, tx0, tx1;
+};
+
+__device__ __forceinline__ TileBox tile_box(const float *__restrict__ records, int64_t i) {
+    const float *rec = records + i * kRec;
+    const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);
+    return {unpack_lo(rows) / kTile, unpack_hi(rows) / kTile, unpack_lo(cols) / kTile, unpack_hi(cols) / kTile};
+}
+
+__global__ void __launch_bounds__(kTileThreads) tile_count_kernel(int64_t items, int64_t N, int tiles_x, int tiles,
+                                                                  int tile_bits, const float *__restrict__ records,
+                                                                  const uint32_t *__restrict__ counts,
+                                                                  uint32_t *__restrict__ tile_counts) {
+    extern __shared__ uint32_t hist[];
+    const int64_t i0 = blockIdx.x * (int64_t)kTileItems;
+    const int64_t b0 = i0 / N;
+    const bool shared = tiles <= kTileSmemBins;
+    if (shared)
+        for (int t = threadIdx.x; t < tiles; t += kTileThreads) hist[t] = 0u;
+    __syncthreads();
+    for (int k = threadIdx.x; k < kTileItems; k += kTileThreads) {
+        const int64_t i = i0 + k;
+        if (i >= items || counts[i] == 0u) continue;
+        const int64_t b = i / N;
+        const TileBox bx = tile_box(records, i);
+        uint32_t *dst = (shared && b == b0) ? hist : tile_counts + ((size_t)b << tile_bits);
+        for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
+            for (int tx = bx.tx0; tx <= bx.tx1; ++tx) atomicAdd(dst + ty * tiles_x + tx, 1u);
+    }
+    if (!shared) return;
+    __syncthreads();
+    uint32_t *row = tile_counts + ((size_t)b0 << tile_bits);
+    for (int t = threadIdx.x; t < tiles; t += kTileThreads) {
+        const uint32_t c = hist[t];
+        if (c) atomicAdd(row + t, c);
+    }
+}
+
+// -------------------------------------------------------------------- scan
+
+// List classes (list_counts[c]): 0 = 2..kWarpShort entries and 1 = ..kWarpCap (one
+// warp each; class 1 from the back of `lists`, sorted first), 2 = ..kCtaCap (one CTA
+// each, from lists + nseg), 3 = longer (counted only: the caller's fallback).
+constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 16;          // segments per thread and round: tid + k * kScanThreads
+
+__global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint32_t *__restrict__ tile_counts,
+                                                                 uint32_t *__restrict__ ranges,
+                                                                 uint32_t *__restrict__ cursor,
+                                                                 uint32_t *__restrict__ lists,
+                                                                 uint32_t *__restrict__ list_counts,
+                                                                 const unsigned long long *__restrict__ err,
+                                                                 const uint32_t *__restrict__ depth_range,
+                                                                 unsigned long long *__restrict__ summary) {
+    __shared__ uint32_t wt[kScanPer][kScanThreads / 32];   // per k: inclusive scan over warps
+    __shared__ uint32_t s_cnt[4], s_max;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid < 4) s_cnt[tid] = 0u;
+    if (tid == 0) s_max = 0u;
+    uint32_t carry = 0, mx = 0;
+    for (int base = 0; base < nseg; base += kScanThreads * kScanPer) {
+        uint32_t c[kScanPer], incl[kScanPer];
+#pragma unroll
+        for (int k = 0; k < kScanPer; ++k) {
+            const int i = base + k * kScanThreads + tid;
+            c[k] = i < nseg ? tile_counts[i] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kScanPer; ++k) {
+            mx = max(mx, c[k]);
+            uint32_t v = c[k];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
+            }
+            incl[k] = v;
+            if (lane == 31) wt[k][w] = v;
+        }
+        __syncthreads();
+        if (w < kScanPer) {
+            uint32_t v = wt[w][lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
+            }
+            wt[w][lane] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kScanPer; ++k) {
+            const int i = base + k * kScanThreads + tid;
+            const uint32_t run = carry + (w > 0 ? wt[k][w - 1] : 0u) + incl[k] - c[k];
+            carry += wt[k][kScanThreads / 32 - 1];
+            if (i < nseg) {
+                // empty lists: (0, 0), as the sorts leave them
+                reinterpret_cast<uint2 *>(ranges)[i] = c[k] ? make_uint2(run, run + c[k]) : make_uint2(0u, 0u);
+                cursor[i] = run;
+                if (c[k]) tile_counts[i] = 0u;       // ready for the next step's count
+            }
+            // list appends: one shared atomic per warp and class
+            const int cls = c[k] < 2u ? -1 : c[k] <= (uint32_t)kWarpShort ? 0 : c[k] <= (uint32_t)kWarpCap ? 1
+                          : c[k] <= (uint32_t)kCtaCap ? 2 : 3;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t m = __ballot_sync(0xffffffffu, cls == q);
+                if (!m) continue;
+                const int leader = __ffs(m) - 1;
+                uint32_t first = 0;
+                if (lane == leader) first = atomicAdd(&s_cnt[q], (uint32_t)__popc(m));
+                first = __shfl_sync(0xffffffffu, first, leader);
+                const uint32_t r = first + __popc(m & ((1u << lane) - 1u));
+                if (cls == q) {
+                    if (q == 0) lists[r] = (uint32_t)i;
+                    else if (q == 1) lists[nseg - 1 - r] = (uint32_t)i;
+                    else if (q == 2) lists[nseg + r] = (uint32_t)i;
+                }
+            }
+        }
+        __syncthreads();   // wt is rewritten by the next round
+    }
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(&s_max, mx);
+    __syncthreads();
+    if (tid < 4) list_counts[tid] = s_cnt[tid];
+    if (tid == 4) list_counts[4] = 0u;                 // the fill's 64-bit fallback count
+    if (tid == 0) {
+        summary[0] = carry;
+        summary[1] = err ? *err : HS_NO_ERROR;
+        summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
+        summary[3] = s_max;
+    }
+}
+
+// ----------------------------------------------------------------- scatter
+
+// Same CTA partition as the count: the shared histogram of the CTA's first frame
+// reserves one block of slots per touched tile (one global atomic each), then the
+// items take slots inside their block with shared atomics.  Slot order inside a list
+// is arbitrary; the list sort below fixes it.
+__global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t items, int64_t N, int tiles_x, int tiles,
+                                                                    int tile_bits, const float *__restrict__ records,
+                                                                    const uint32_t *__restrict__ counts,
+                                                                    uint32_t *__restrict__ cursor, uint64_t capacity,
+                                                                    const unsigned long long *__restrict__ summary,
+                                                                    uint32_t *__restrict__ keys,
+                                                                    uint32_t *__restrict__ vals) {
+    extern __shared__ uint32_t hist[];
+    if (summary[0] > capacity) return;               // the caller grows the buffers and re-runs
+    const int64_t i0 = blockIdx.x * (int64_t)kTileItems;
+    const int64_t b0 = i0 / N;
+    const bool shared = tiles <= kTileSmemBins;
+    if (shared) {
+        for (int t = threadIdx.x; t < tiles; t += kTileThreads) hist[t] = 0u;
+        __syncthreads();
+        for (int k = threadIdx.x; k < kTileItems; k += kTileThreads) {
+            const int64_t i = i0 + k;
+            if (i >= items || counts[i] == 0u || i / N != b0) continue;
+            const TileBox bx = tile_box(records, i);
+            for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
+                for (int tx = bx.tx0; tx <= bx.tx1; ++tx) atomicAdd(hist + ty * tiles_x + tx, 1u);
+        }
+        __syncthreads();
+        uint32_t *row = cursor + ((size_t)b0 << tile_bits);
+        for (int t = threadIdx.x; t < tiles; t += kTileThreads) {
+            const uint32_t c = hist[t];
+            if (c) hist[t] = atomicAdd(row + t, c);  // the block's first slot
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < kTileItems; k += kTileThreads) {
+        const int64_t i = i0 + k;
+        if (i >= items || counts[i] == 0u) continue;
+        const int64_t b = i / N;
+        const uint32_t n = (uint32_t)(i - b * N);
+        const TileBox bx = tile_box(records, i);
+        const bool local = shared && b == b0;
+        const uint32_t hi = (uint32_t)b << tile_bits;
+        for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
+            for (int tx = bx.tx0; tx <= bx.tx1; ++tx) {
+                const uint32_t t = (uint32_t)(ty * tiles_x + tx);
+                const uint32_t pos = atomicAdd(local ? hist + t : cursor + (hi | t), 1u);
+                keys[pos] = hi | t;
+                vals[pos] = n;
+            }
+    }
+}
+
+// -------------------------------------------------------------------- sort
+
+__device__ __forceinline__ unsigned long long sort_key(const float *__restrict__ depth, int64_t frame_base,
+                                                       uint32_t n) {
+    return ((unsigned long long)__float_as_uint(depth[frame_base + n]) << 32) | n;
+}
+
+// bitonic compare-exchange network over P (a power of two) keys in shared memory,
+// `threads` cooperating threads with index t (one warp, or the whole CTA)
+template <bool kCta>
+__device__ __forceinline__ void bitonic_smem(unsigned long long *s, int P, int t, int threads) {
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int q = t; q < (P >> 1); q += threads) {
+                const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+                const int l = i + j;
+                const unsigned long long a = s[i], c = s[l];
+                if ((a > c) == ((i & k) == 0)) {
+                    s[i] = c;
+                    s[l] = a;
+                }
+            }
+            if (kCta) __syncthreads();
+            else __syncwarp();
+        }
+}
+
+// Register bitonic sort of one list by one warp: E keys per lane, key q = e * 32 +
+// lane (padding ~0 sorts last).  Strides below 32 exchange across lanes with
+// shuffles; strides of 32 and up swap registers of the same lane.  The stage loops
+// stay rolled (small code: the kernels run out of the instruction cache otherwise).
+template <int E, int JE, typename K>
+__device__ __forceinline__ void swap_regs(K (&key)[E], int k) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e & JE) continue;
+        const bool up = ((e * 32) & k) == 0;     // k >= 64 here: lane bits do not matter
+        const K a = key[e], b = key[e | JE];
+        const bool sw = (a > b) == up;
+        key[e] = sw ? b : a;
+        key[e | JE] = sw ? a : b;
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void sort_list_warp(const float *__restrict__ depth, int64_t fb, uint32_t start,
+                                               uint32_t len, uint32_t *__restrict__ vals, int lane) {
+    constexpr int P = 32 * E;
+    unsigned long long key[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t q = (uint32_t)(e * 32 + lane);
+        key[e] = q < len ? sort_key(depth, fb, vals[start + q]) : ~0ull;
+    }
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int je = j >> 5;
+                if (E >= 32 && je == 16) swap_regs<E, (E >= 32 ? 16 : 0)>(key, k);
+                else if (E >= 16 && je == 8) swap_regs<E, (E >= 16 ? 8 : 0)>(key, k);
+                else if (E >= 8 && je == 4) swap_regs<E, (E >= 8 ? 4 : 0)>(key, k);
+                else if (E >= 4 && je == 2) swap_regs<E, (E >= 4 ? 2 : 0)>(key, k);
+                else if (E >= 2 && je == 1) swap_regs<E, (E >= 2 ? 1 : 0)>(key, k);
+            } else {
+                const bool lower = (lane & j) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const bool up = k >= 32 ? ((e * 32) & k) == 0 : (lane & k) == 0;
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, key[e], j);
+                    const unsigned long long lo = key[e] < o ? key[e] : o, hi = key[e] < o ? o : key[e];
+                    key[e] = (lower == up) ? lo : hi;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t q = (uint32_t)(e * 32 + lane);
+        if (q < len) vals[start + q] = (uint32_t)key[e];
+    }
+}
+
+// The common case in 32-bit keys: ((depth bits - the list's smallest) >> sh) << IB |
+// slot, slot = the entry's position in the unsorted list, whose full 64-bit key
+// (depth bits << 32 | index) waits in shared memory; sh drops just enough low depth
+// bits to fit.  Entries left next to each other with equal 32-bit depth fields (exact
+// depth ties, or depths that differ only in the dropped bits) are then put in full-key
+// order by odd-even transposition over the sorted slots.  Returns false -- `vals`
+// untouched -- when that does not settle within kFixRounds rounds (long runs of equal
+// depths); the caller then sorts the list with 64-bit keys.
+constexpr int kFixRounds = 32;
+
+template <int E>
+__device__ __forceinline__ bool sort_list_warp32(const float *__restrict__ depth, int64_t fb, uint32_t start,
+                                                 uint32_t len, uint32_t *__restrict__ vals, int lane,
+                                                 unsigned long long *__restrict__ s_k64,
+                                                 uint32_t *__restrict__ s_q) {
+    constexpr int P = 32 * E;
+    constexpr int IB = E == 1 ? 5 : E == 2 ? 6 : E == 4 ? 7 : E == 8 ? 8 : E == 16 ? 9 : 10;
+    constexpr uint32_t kSlot = (1u << IB) - 1u;
+    uint32_t key[E];
+    uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t q = (uint32_t)(e * 32 + lane);
+        key[e] = 0xFFFFFFFFu;
+        if (q < len) {
+            const uint32_t n = vals[start + q];
+            key[e] = __float_as_uint(depth[fb + n]);
+            s_k64[q] = ((unsigned long long)key[e] << 32) | n;
+            dmin = min(dmin, key[e]);
+            dmax = max(dmax, key[e]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    const int span = 32 - __clz(dmax - dmin);
+    const int sh = max(0, span - (31 - IB));           // real keys stay below 2^31
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t q = (uint32_t)(e * 32 + lane);
+        if (q < len) key[e] = (((key[e] - dmin) >> sh) << IB) | q;
+    }
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int je = j >> 5;
+                if (E >= 32 && je == 16) swap_regs<E, (E >= 32 ? 16 : 0)>(key, k);
+                else if (E >= 16 && je == 8) swap_regs<E, (E >= 16 ? 8 : 0)>(key, k);
+                else if (E >= 8 && je == 4) swap_regs<E, (E >= 8 ? 4 : 0)>(key, k);
+                else if (E >= 4 && je == 2) swap_regs<E, (E >= 4 ? 2 : 0)>(key, k);
+                else if (E >= 2 && je == 1) swap_regs<E, (E >= 2 ? 1 : 0)>(key, k);
+            } else {
+                const bool lower = (lane & j) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const bool up = k >= 32 ? ((e * 32) & k) == 0 : (lane & k) == 0;
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, key[e], j);
+                    // keep the smaller key when this slot's half runs ascending
+                    key[e] = ((key[e] < o) == (lower == up)) ? key[e] : o;
+                }
+            }
+        }
+    }
+    // neighbours with equal depth fields?
+    bool tie = false;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        uint32_t prev = __shfl_up_sync(0xffffffffu, key[e], 1);
+        if (e > 0) {
+            const uint32_t wrap = __shfl_sync(0xffffffffu, key[e > 0 ? e - 1 : 0], 31);
+            if (lane == 0) prev = wrap;
+        }
+        const uint32_t q = (uint32_t)(e * 32 + lane);
+        if (q > 0 && q < len && (prev >> IB) == (key[e] >> IB)) tie = true;
+    }
+    __syncwarp();
+    if (!__any_sync(0xffffffffu, tie)) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint32_t q = (uint32_t)(e * 32 + lane);
+            if (q < len) vals[start + q] = (uint32_t)s_k64[key[e] & kSlot];
+        }
+        return true;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const uint32_t q = (uint32_t)(e * 32 + lane);
+        if (q < len) s_q[q] = key[e];
+    }
+    __syncwarp();
+    int quiet = 0;
+    for (int round = 0; round < kFixRounds && quiet < 2; ++round) {
+        bool swapped = false;
+        for (uint32_t i = 2 * (uint32_t)lane + (round & 1); i + 1 < len; i += 64) {
+            const uint32_t a = s_q[i], b = s_q[i + 1];
+            if ((a >> IB) == (b >> IB) && s_k64[a & kSlot] > s_k64[b & kSlot]) {
+                s_q[i] = b;
+                s_q[i + 1] = a;
+                swapped = true;
+            }
+        }
+        __syncwarp();
+        quiet = __any_sync(0xffffffffu, swapped) ? 0 : quiet + 1;
+    }
+    if (quiet < 2) return false;
+    for (uint32_t q = lane; q < len; q += 32) vals[start + q] = (uint32_t)s_k64[s_q[q] & kSlot];
+    return true;
+}
+
+// lists the 32-bit sort declines go to lists[2 * nseg + ...] (count list_counts[4])
+template <int E>
+__device__ __forceinline__ void sort_list(const float *__restrict__ depth, int64_t fb, uint32_t start,
+                                          uint32_t len, uint32_t *__restrict__ vals, int lane,
+                                          unsigned long long *__restrict__ s_k64, uint32_t *__restrict__ s_q,
+                                          uint32_t seg, uint32_t *__restrict__ wide, uint32_t *__restrict__ n_wide) {
+    if (!sort_list_warp32<E>(depth, fb, start, len, vals, lane, s_k64, s_q) && lane == 0)
+        wide[atomicAdd(n_wide, 1u)] = seg;
+    __syncwarp();
+}
+
+// One warp per list: kLong = class 1 (kWarpShort+1..kWarpCap entries, from the back
+// of `lists`), else class 0 (2..kWarpShort).
+#ifndef HS_LONG_SORT_MINB
+#define HS_LONG_SORT_MINB 4
+#endif
+template <bool kLong>
+__global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB : 8) tile_sort_warp_kernel(
+    int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
+    uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, uint64_t capacity,
+    const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
+    __shared__ unsigned long long s_k64_all[kWarpSortWarps][kLong ? kWarpCap : kWarpShort];
+    __shared__ uint32_t s_q_all[kWarpSortWarps][kLong ? kWarpCap : kWarpShort];
+    uint32_t *wide = lists + 2 * (size_t)nseg;
+    if (summary[0] > capacity) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long *s_k64 = s_k64_all[w];
+    uint32_t *s_q = s_q_all[w];
+    const uint32_t count = list_counts[kLong ? 1 : 0];
+    const uint32_t stride = gridDim.x * kWarpSortWarps;
+    for (uint32_t e = blockIdx.x * kWarpSortWarps + w; e < count; e += stride) {
+        const uint32_t seg = kLong ? lists[nseg - 1 - e] : lists[e];
+        const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
+        const uint32_t start = rg.x, len = rg.y - rg.x;
+        const int64_t fb = (int64_t)(seg >> tile_bits) * N;
+        if (kLong) {
+            if (len <= 512u) sort_list<16>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
+            else sort_list<32>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
+        } else {
+            if (len <= 32u) sort_list<1>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
+            else if (len <= 64u) sort_list<2>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
+            else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
+            else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
+        }
+    }
+}
+
+// 64-bit keys (depth bits << 32 | index) for the lists the 32-bit sort declined
+__global__ void __launch_bounds__(32 * kWarpSortWarps) tile_sort_wide_kernel(
+    int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
+    const uint32_t *__restrict__ lists, const uint32_t *__restrict__ list_counts, uint64_t capacity,
+    const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
+    if (summary[0] > capacity) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t count = list_counts[4];
+    const uint32_t stride = gridDim.x * kWarpSortWarps;
+    for (uint32_t e = blockIdx.x * kWarpSortWarps + w; e < count; e += stride) {
+        const uint32_t seg = lists[2 * (size_t)nseg + e];
+        const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
+        const uint32_t start = rg.x, len = rg.y - rg.x;
+        const int64_t fb = (int64_t)(seg >> tile_bits) * N;
+        if (len <= 32u) sort_list_warp<1>(depth, fb, start, len, vals, lane);
+        else if (len <= 64u) sort_list_warp<2>(depth, fb, start, len, vals, lane);
+        else if (len <= 128u) sort_list_warp<4>(depth, fb, start, len, vals, lane);
+        else if (len <= 256u) sort_list_warp<8>(depth, fb, start, len, vals, lane);
+        else if (len <= 512u) sort_list_warp<16>(depth, fb, start, len, vals, lane);
+        else sort_list_warp<32>(depth, fb, start, len, vals, lane);
+    }
+}
+
+// one CTA per list of kWarpCap+1..kCtaCap entries
+__global__ void __launch_bounds__(kCtaSortThreads) tile_sort_cta_kernel(
+    int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
+    const uint32_t *__restrict__ lists, const uint32_t *__restrict__ list_counts, uint64_t capacity,
+    const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
+    extern __shared__ unsigned long long s_keys[];
+    if (summary[0] > capacity) return;
+    const uint32_t count = list_counts[2];
+    for (uint32_t e = blockIdx.x; e < count; e += gridDim.x) {
+        const uint32_t seg = lists[nseg + e];
+        const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
+        const uint32_t start = rg.x, len = rg.y - rg.x;
+        const int64_t fb = (int64_t)(seg >> tile_bits) * N;
+        int P = 2 * kWarpCap;
+        while (P < (int)len) P <<= 1;
+        for (int q = threadIdx.x; q < P; q += kCtaSortThreads)
+            s_keys[q] = q < (int)len ? sort_key(depth, fb, vals[start + q]) : ~0ull;
+        __syncthreads();
+        bitonic_smem<true>(s_keys, P, threadIdx.x, kCtaSortThreads);
+        for (int q = threadIdx.x; q < (int)len; q += kCtaSortThreads) vals[start + q] = (uint32_t)s_keys[q];
+        __syncthreads();
+    }
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" {
+
+int hs_tile_sort_cap(void) { return kCtaCap; }
+
+int hs_tile_count(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
+                  uint32_t *tile_counts, void *stream) {
+    const int64_t items = (int64_t)B * N;
+    if (items <= 0) return HS_OK;
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
+    if (tile_bits + bit_length_u32((uint32_t)(B - 1)) > 31) {
+        set_error("hs_tile_count: frame/tile bits exceed 31");
+        return HS_ERR_SHAPE;
+    }
+    const int tiles = tiles_x * tiles_y;
+    const size_t smem = tiles <= kTileSmemBins ? sizeof(uint32_t) * tiles : 0;
+    tile_count_kernel<<<grid_for(items, kTileItems), kTileThreads, smem, HS_CHECK_STREAM(stream)>>>(
+        items, N, tiles_x, tiles, tile_bits, records, counts, tile_counts);
+    return check_launch("hs_tile_count");
+}
+
+int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,
+                 uint32_t *lists, uint32_t *list_counts, const unsigned long long *err,
+                 const uint32_t *depth_range, unsigned long long *summary, void *stream) {
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
+    const int64_t nseg = (int64_t)B << tile_bits;
+    if (B <= 0 || nseg > (1ll << 30)) {
+        set_error("hs_tile_scan: bad segment count");
+        return HS_ERR_SHAPE;
+    }
+    tile_scan_kernel<<<1, 1024, 0, HS_CHECK_STREAM(stream)>>>((int)nseg, tile_counts, ranges, cursor, lists,
+                                                              list_counts, err, depth_range, summary);
+    return check_launch("hs_tile_scan");
+}
+
+int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
+                 const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
+                 uint32_t *list_counts, const unsigned long long *summary, uint64_t capacity,
+                 uint32_t *keys, uint32_t *values, void *stream) {
+    const int64_t items = (int64_t)B * N;
+    if (items <= 0) return HS_OK;
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
+    const int nseg = B << tile_bits;
+    const int tiles = tiles_x * tiles_y;
+    const size_t tsmem = tiles <= kTileSmemBins ? sizeof(uint32_t) * tiles : 0;
+    tile_scatter_kernel<<<grid_for(items, kTileItems), kTileThreads, tsmem, s>>>(
+        items, N, tiles_x, tiles, tile_bits, records, counts, cursor, capacity, summary, keys, values);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    static bool attr = false;
+    const int csmem = kCtaCap * (int)sizeof(unsigned long long);
+    if (!attr) {
+        cudaFuncSetAttribute(tile_sort_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
+        attr = true;
+    }
+    // the long lists first (fewer, longer: their tail overlaps nothing otherwise)
+    tile_sort_warp_kernel<true><<<(unsigned)sms * 8, 32 * kWarpSortWarps, 0, s>>>(
+        N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
+    tile_sort_warp_kernel<false><<<(unsigned)sms * 16, 32 * kWarpSortWarps, 0, s>>>(
+        N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
+    tile_sort_wide_kernel<<<(unsigned)sms * 4, 32 * kWarpSortWarps, 0, s>>>(
+        N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
+    tile_sort_cta_kernel<<<(unsigned)sms * 2, kCtaSortThreads, csmem, s>>>(N, tile_bits, nseg, depth, ranges, lists,
+                                                                          list_counts, capacity, summary, values);
+    return check_launch("hs_tile_fill");
+}
+
+}  // extern "C"

@@ -246,9 +246,9 @@ class Binner:
         self.device = device
         self.cap = 0
         self.keys = self.vals = self.keys_alt = self.vals_alt = self.ws = None
-        self.summary_host = torch.empty(3, dtype=torch.int64, pin_memory=True)
+        self.summary_host = torch.empty(4, dtype=torch.int64, pin_memory=True)
         self.offsets = None
-        self.summary = torch.empty(3, dtype=torch.int64, device=device)
+        self.summary = torch.empty(4, dtype=torch.int64, device=device)
         self.depth_range = torch.empty(2, dtype=torch.int32, device=device)
         self.depth_bits = (0, 0)
         self.passes = 0
@@ -256,6 +256,9 @@ class Binner:
         self.result = None
         self.order = None
         self._ordered = None
+        self.tile_counts = None
+        self.mode = None             # how the last bin() built its lists
+        self.longest = 0             # longest (frame, tile) list of the last tile-major binning
 
     def _ensure(self, total):
         if total <= self.cap and self.keys is not None:
@@ -377,6 +380,79 @@ class Binner:
         return self.result
 
 
+    def bin_tiles(self, B, N, width, height, records, depth, counts, err):
+        """Tile-major binning (hs_tile_count / hs_tile_scan / hs_tile_fill) with the
+        step's single host read: the scatter and the per-list sorts are enqueued before
+        the host waits, sized by the previous step's capacity; a step that needs more
+        re-runs them on grown buffers.  Lists longer than hs_tile_sort_cap() fall back to
+        the two-level sort for that step.  Returns (key total, error word)."""
+        tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
+        nseg = B << tile_bits
+        d = self.device
+        if self.tile_counts is None or self.tile_counts.numel() < nseg:
+            self.tile_counts = torch.zeros(nseg, dtype=torch.int32, device=d)
+            self.cursor = torch.empty(nseg, dtype=torch.int32, device=d)
+            self.lists = torch.empty(3 * nseg, dtype=torch.int32, device=d)
+            self.list_counts = torch.empty(8, dtype=torch.int32, device=d)
+        if self.ranges is None or self.ranges.numel() < 2 * nseg:
+            self.ranges = torch.empty(2 * nseg, dtype=torch.int32, device=d)
+        ranges = self.ranges[:2 * nseg]
+        s = _stream()
+        L.call("hs_tile_count", B, N, width, height, _p(records), _p(counts), _p(self.tile_counts), s)
+        L.call("hs_tile_scan", B, width, height, _p(self.tile_counts), _p(ranges), _p(self.cursor), _p(self.lists),
+               _p(self.list_counts), _p(err), _p(self.depth_range), _p(self.summary), s)
+        self.summary_host.copy_(self.summary, non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record()
+        if self.keys is None:
+            self._ensure(4 * B * N)         # a first guess; grown below when short
+
+        def fill():
+            L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(depth), _p(ranges),
+                   _p(self.cursor), _p(self.lists), _p(self.list_counts), _p(self.summary), self.cap,
+                   _p(self.keys), _p(self.vals), s)
+        fill()
+        ready.synchronize()
+        total = int(self.summary_host[0])
+        code = int(self.summary_host[1]) & 0xFFFFFFFFFFFFFFFF
+        dr = int(self.summary_host[2]) & 0xFFFFFFFFFFFFFFFF
+        self.depth_bits = (dr & 0xFFFFFFFF, dr >> 32)
+        self.longest = int(self.summary_host[3])
+        self.mode = "tiles"
+        if total > self.cap:
+            self._ensure(total)
+            self.cursor[:nseg].copy_(ranges.view(-1, 2)[:, 0])
+            fill()
+        if self.longest > tile_sort_cap():
+            # a list too long to sort in shared memory: the global two-level sort
+            self.depth_order(B, N, depth)
+            self._bin_two_level(B, N, width, height, records, counts, total)
+            self.mode = "two_level"
+            return total, code
+        k32 = self.keys.view(torch.int32)
+        self.result = (k32[:total], self.vals[:total], ranges, tile_bits, tiles)
+        return total, code
+
+
+_SORT_CAP = None
+
+
+def tile_sort_cap():
+    global _SORT_CAP
+    if _SORT_CAP is None:
+        _SORT_CAP = int(L.load().hs_tile_sort_cap())
+    return _SORT_CAP
+
+
+def launches_tiles(binner):
+    """Kernel launches issued by Binner.bin_tiles: count, scan, scatter, the two list
+    sorts (+ the two-level fallback's)."""
+    n = 5
+    if binner.mode == "two_level":
+        n += 6 + launches_binning(1, binner.passes, True)
+    return n
+
+
 def launches_binning(total, passes, two_level=False):
     """Kernel launches issued by Binner.bin (emit (3 for the sorted emission), histogram,
     digit scan, one per pass, ranges) -- for the bench's gpu_launches count."""
@@ -411,6 +487,7 @@ class Trainer:
         self.rig = rig              # DeviceRig: frames computed from theta on device
         self.fused_raster = True    # hs_raster_train (False: hs_raster_fwd + hs_raster_bwd)
         self.two_level_binning = True   # depth order + 32-bit tile sort (False: one 64-bit sort)
+        self.tile_binning = True        # tile-major binning (the two flags above: its fallback / off)
         self.W, self.H = int(width), int(height)
         self.B = int(batch)
         self.global_batch = int(global_batch or batch)
@@ -549,6 +626,17 @@ class Trainer:
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
                    _p(self.counts), _p(self.block_sums), _p(self.binner.reset_depth_range()), _p(self.radius),
                    *(_p(z) for z in zero), _p(self.err), s)
+        if self.tile_binning:
+            m = self._mark("bin_tiles")
+            total, code = self.binner.bin_tiles(B, N, self.W, self.H, self.records, self.depth, self.counts,
+                                                self.err)
+            self._done(m)
+            self.launches += launches_tiles(self.binner)
+            self.err.fill_(-1)
+            L.raise_device_error(code, self.frame_offset)
+            self.last_total = total
+            self._last_frames = frames
+            return F, self.binner.result
         overlap = None
         if self.two_level_binning:
             def overlap():      # the depth order runs while the host waits for the key total

@@ -157,6 +157,28 @@ def check_two_level(dev, res, tag=""):
     r = ranges.view(-1, 2).cpu().numpy().view(np.uint32)[:res["ranges"].shape[1]]
     assert np.array_equal(r, res["ranges"][0]), tag
 
+def check_tiles(dev, res, tag="", regrow=False):
+    """Tile-major binning (count, scan, scatter, per-list sort; the training path) on
+    the same projection: the same lists and ranges as the oracle.  regrow: start from
+    a capacity of one key, so the device skips the fill and the host re-runs it."""
+    import torch
+    bn = dev["binner"]
+    if regrow:
+        bn._ensure(1)
+        bn.cap = 1
+    err = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    total, code = bn.bin_tiles(dev["B"], dev["N"], dev["W"], dev["H"], dev["records"], dev["depth"],
+                               dev["counts"], err)
+    assert total == res["keys"].size, tag
+    keys, vals, ranges, tile_bits, tiles = bn.result
+    k = keys.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(k, res["keys"] >> np.uint64(32)), tag
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32), res["values"]), tag
+    r = ranges.view(-1, 2).cpu().numpy().view(np.uint32)[:res["ranges"].shape[1]]
+    assert np.array_equal(r, res["ranges"][0]), tag
+    return bn.mode
+
+
 def test_binning_bit_exact():
     from paper_2503_12886_b200 import compat as C
     for s, p, d, world, cam in scenes():
@@ -175,6 +197,8 @@ def test_binning_bit_exact():
         live = (rad[0] > 0) & (rec[:, 5] >= np.float32(1 / 255))
         np.testing.assert_array_equal(bbox[live], res["bbox"][0][live])
         check_two_level(dev, res, s)
+        check_tiles(dev, res, s)
+        check_tiles(dev, res, s, regrow=True)
 
 
 @pytest.mark.parametrize("n", [200, 1000, 9000])
@@ -200,6 +224,8 @@ def test_binning_bit_exact_crowded_tiles(n):
     r = ranges.view(-1, 2).cpu().numpy().view(np.uint32)[:res["ranges"].shape[1]]
     assert np.array_equal(r, res["ranges"][0])
     check_two_level(dev, res, n)
+    # lists past the shared-memory sort's cap take the two-level fallback
+    assert check_tiles(dev, res, n) == ("two_level" if n > 8192 else "tiles")
 
 
 # --------------------------------------------------------------------- raster
