@@ -223,8 +223,15 @@ enum {
     HS_RASTER_MAXW_ALL = 4,      /* max blend weight per (frame, Gaussian) */
     HS_RASTER_MAXW_UNVISITED = 8,/* same, only for Gaussians with visited[n] == 0 */
     HS_RASTER_WSUMS = 16,        /* colour-init sums (sum w*target, sum w) for the same set */
-    HS_RASTER_WSUMS_IMAGE = 32   /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
+    HS_RASTER_WSUMS_IMAGE = 32,  /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
+    HS_RASTER_ORDER_READY = 64   /* hs_raster_train: the tile order hs_raster_tile_order built for these
+                                    ranges is in place (the call then skips building it) */
 };
+/* The persistent raster's longest-list-first tile order for these ranges; lets a caller
+ * build it off the critical path (e.g. on a side stream while the lists are sorted) and
+ * pass HS_RASTER_ORDER_READY.  Shares process-wide state with the raster launches:
+ * order it before the raster that uses it and after the raster that used the last one. */
+int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, int tile_bits, void *stream);
 /* loss_partials holds B * num_tiles * HS_LOSS_PARTIALS_PER_TILE floats (one (L1,
  * black L1) pair per pixel block of the kernel, at most 8 per tile), reduced by
  * hs_loss_reduce. */

@@ -25,6 +25,7 @@ RASTER_MAXW_ALL = 4
 RASTER_MAXW_UNVISITED = 8
 RASTER_WSUMS = 16
 RASTER_WSUMS_IMAGE = 32
+RASTER_ORDER_READY = 64
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -63,6 +64,7 @@ SIGNATURES = {
     "hs_sort_pairs32": (_I, [_L, ctypes.c_uint32, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges32": (_I, [_L, _P, _P, _P]),
     "hs_tile_sort_cap": (_I, []),
+    "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P]),
     "hs_tile_count": (_I, [_I, _L, _I, _I, _P, _P, _P, _P]),
     "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint64, _P, _P, _P]),

@@ -816,6 +816,12 @@ using namespace hs;
 
 extern "C" {
 
+int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, int tile_bits, void *stream) {
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    launch_tile_order(B, tiles_x * tiles_y * kBlocks, tile_bits, ranges, HS_CHECK_STREAM(stream));
+    return check_launch("hs_raster_tile_order");
+}
+
 int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records, const uint32_t *values,
                   const uint32_t *ranges, int tile_bits, const float *backgrounds, const uint8_t *targets,
                   const float *wsum_image, const uint8_t *visited, float *pix_T, uint32_t *pix_state, float *image,
@@ -899,7 +905,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    launch_tile_order(B, nblk, tile_bits, ranges, s);
+    if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, s);
     switch (ci) {
         case 0: raster_train_kernel<0><<<grid, kRT, 0, s>>>(a, nblk); break;
         case 1: raster_train_kernel<1><<<grid, kRT, 0, s>>>(a, nblk); break;

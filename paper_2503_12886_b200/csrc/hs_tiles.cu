@@ -98,13 +98,15 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                                                                  const uint32_t *__restrict__ depth_range,
                                                                  unsigned long long *__restrict__ summary) {
     __shared__ uint32_t wt[kScanPer][kScanThreads / 32];   // per k: inclusive scan over warps
-    __shared__ uint32_t s_cnt[4], s_max;
+    __shared__ uint32_t wq[4][kScanThreads / 32];           // per class: warp slot bases
+    __shared__ uint32_t qcarry[4], qtot[4], s_max;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    if (tid < 4) s_cnt[tid] = 0u;
+    if (tid < 4) qcarry[tid] = 0u;
     if (tid == 0) s_max = 0u;
     uint32_t carry = 0, mx = 0;
     for (int base = 0; base < nseg; base += kScanThreads * kScanPer) {
-        uint32_t c[kScanPer], incl[kScanPer];
+        uint32_t c[kScanPer], incl[kScanPer], nq[4] = {0u, 0u, 0u, 0u};
+        int cls[kScanPer];
 #pragma unroll
         for (int k = 0; k < kScanPer; ++k) {
             const int i = base + k * kScanThreads + tid;
@@ -142,31 +144,51 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                 cursor[i] = run;
                 if (c[k]) tile_counts[i] = 0u;       // ready for the next step's count
             }
-            // list appends: one shared atomic per warp and class
-            const int cls = c[k] < 2u ? -1 : c[k] <= (uint32_t)kWarpShort ? 0 : c[k] <= (uint32_t)kWarpCap ? 1
-                          : c[k] <= (uint32_t)kCtaCap ? 2 : 3;
+            cls[k] = c[k] < 2u ? -1 : c[k] <= (uint32_t)kWarpShort ? 0 : c[k] <= (uint32_t)kWarpCap ? 1
+                   : c[k] <= (uint32_t)kCtaCap ? 2 : 3;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t m = __ballot_sync(0xffffffffu, cls == q);
-                if (!m) continue;
-                const int leader = __ffs(m) - 1;
-                uint32_t first = 0;
-                if (lane == leader) first = atomicAdd(&s_cnt[q], (uint32_t)__popc(m));
-                first = __shfl_sync(0xffffffffu, first, leader);
-                const uint32_t r = first + __popc(m & ((1u << lane) - 1u));
-                if (cls == q) {
+            for (int q = 0; q < 4; ++q) nq[q] += __popc(__ballot_sync(0xffffffffu, cls[k] == q));
+        }
+        // list slots: per class, an exclusive scan of the warps' counts (deterministic)
+        if (lane < 4) wq[lane][w] = lane == 0 ? nq[0] : lane == 1 ? nq[1] : lane == 2 ? nq[2] : nq[3];
+        __syncthreads();
+        if (w < 4) {
+            const uint32_t v = wq[w][lane];
+            uint32_t x = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += t;
+            }
+            wq[w][lane] = qcarry[w] + x - v;
+            if (lane == 31) qtot[w] = x;
+        }
+        __syncthreads();
+        uint32_t slot[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) slot[q] = wq[q][w];
+#pragma unroll
+        for (int k = 0; k < kScanPer; ++k) {
+            const int i = base + k * kScanThreads + tid;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const uint32_t m = __ballot_sync(0xffffffffu, cls[k] == q);
+                if (cls[k] == q) {
+                    const uint32_t r = slot[q] + __popc(m & ((1u << lane) - 1u));
                     if (q == 0) lists[r] = (uint32_t)i;
                     else if (q == 1) lists[nseg - 1 - r] = (uint32_t)i;
-                    else if (q == 2) lists[nseg + r] = (uint32_t)i;
+                    else lists[nseg + r] = (uint32_t)i;
                 }
+                slot[q] += __popc(m);
             }
         }
-        __syncthreads();   // wt is rewritten by the next round
+        __syncthreads();   // wt / wq are rewritten by the next round
+        if (tid < 4) qcarry[tid] += qtot[tid];
+        __syncthreads();
     }
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) atomicMax(&s_max, mx);
     __syncthreads();
-    if (tid < 4) list_counts[tid] = s_cnt[tid];
+    if (tid < 4) list_counts[tid] = qcarry[tid];
     if (tid == 4) list_counts[4] = 0u;                 // the fill's 64-bit fallback count
     if (tid == 0) {
         summary[0] = carry;
@@ -324,12 +346,40 @@ __device__ __forceinline__ void sort_list_warp(const float *__restrict__ depth, 
 // depths); the caller then sorts the list with 64-bit keys.
 constexpr int kFixRounds = 32;
 
+// ascending bitonic network over the 32 * E 32-bit keys of a warp (key q = e * 32 + lane)
+template <int E>
+__device__ __forceinline__ void bitonic_u32(uint32_t (&key)[E], int lane) {
+    constexpr int P = 32 * E;
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int je = j >> 5;
+                if (E >= 32 && je == 16) swap_regs<E, (E >= 32 ? 16 : 0)>(key, k);
+                else if (E >= 16 && je == 8) swap_regs<E, (E >= 16 ? 8 : 0)>(key, k);
+                else if (E >= 8 && je == 4) swap_regs<E, (E >= 8 ? 4 : 0)>(key, k);
+                else if (E >= 4 && je == 2) swap_regs<E, (E >= 4 ? 2 : 0)>(key, k);
+                else if (E >= 2 && je == 1) swap_regs<E, (E >= 2 ? 1 : 0)>(key, k);
+            } else {
+                const bool lower = (lane & j) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const bool up = k >= 32 ? ((e * 32) & k) == 0 : (lane & k) == 0;
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, key[e], j);
+                    // keep the smaller key when this slot's half runs ascending
+                    key[e] = ((key[e] < o) == (lower == up)) ? key[e] : o;
+                }
+            }
+        }
+    }
+}
+
 template <int E>
 __device__ __forceinline__ bool sort_list_warp32(const float *__restrict__ depth, int64_t fb, uint32_t start,
                                                  uint32_t len, uint32_t *__restrict__ vals, int lane,
                                                  unsigned long long *__restrict__ s_k64,
                                                  uint32_t *__restrict__ s_q) {
-    constexpr int P = 32 * E;
     constexpr int IB = E == 1 ? 5 : E == 2 ? 6 : E == 4 ? 7 : E == 8 ? 8 : E == 16 ? 9 : 10;
     constexpr uint32_t kSlot = (1u << IB) - 1u;
     uint32_t key[E];
@@ -358,29 +408,7 @@ __device__ __forceinline__ bool sort_list_warp32(const float *__restrict__ depth
         const uint32_t q = (uint32_t)(e * 32 + lane);
         if (q < len) key[e] = (((key[e] - dmin) >> sh) << IB) | q;
     }
-#pragma unroll 1
-    for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll 1
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-                const int je = j >> 5;
-                if (E >= 32 && je == 16) swap_regs<E, (E >= 32 ? 16 : 0)>(key, k);
-                else if (E >= 16 && je == 8) swap_regs<E, (E >= 16 ? 8 : 0)>(key, k);
-                else if (E >= 8 && je == 4) swap_regs<E, (E >= 8 ? 4 : 0)>(key, k);
-                else if (E >= 4 && je == 2) swap_regs<E, (E >= 4 ? 2 : 0)>(key, k);
-                else if (E >= 2 && je == 1) swap_regs<E, (E >= 2 ? 1 : 0)>(key, k);
-            } else {
-                const bool lower = (lane & j) == 0;
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const bool up = k >= 32 ? ((e * 32) & k) == 0 : (lane & k) == 0;
-                    const uint32_t o = __shfl_xor_sync(0xffffffffu, key[e], j);
-                    // keep the smaller key when this slot's half runs ascending
-                    key[e] = ((key[e] < o) == (lower == up)) ? key[e] : o;
-                }
-            }
-        }
-    }
+    bitonic_u32<E>(key, lane);
     // neighbours with equal depth fields?
     bool tie = false;
 #pragma unroll
@@ -471,6 +499,129 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB
             else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
             else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
         }
+    }
+}
+
+// Lists of kWarpShort+1..kWarpCap entries: one CTA of kLongWarps warps per list.
+// Each warp sorts a run of kWarpShort entries in registers (the 32-bit keys of
+// sort_list_warp32, on the list-wide depth offset and shift, 10 slot bits); every key
+// then finds its merged position by binary search in the other runs (keys are unique),
+// and the equal-depth-field fix-up runs over the merged list.  Lists the fix-up does
+// not settle go to the 64-bit fallback.
+constexpr int kLongWarps = kWarpCap / kWarpShort;
+
+__global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
+    int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
+    uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, uint64_t capacity,
+    const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
+    constexpr int E = kWarpShort / 32, IB = 10;
+    constexpr uint32_t kSlot = (1u << IB) - 1u;
+    __shared__ unsigned long long s_k64[kWarpCap];
+    __shared__ uint32_t s_run[kWarpCap], s_out[kWarpCap];
+    __shared__ uint32_t s_min[kLongWarps], s_max[kLongWarps];
+    __shared__ int s_flag;
+    if (summary[0] > capacity) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t count = list_counts[1];
+    uint32_t *wide = lists + 2 * (size_t)nseg;
+    for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+        const uint32_t seg = lists[nseg - 1 - li];
+        const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
+        const uint32_t start = rg.x, len = rg.y - rg.x;
+        const int64_t fb = (int64_t)(seg >> tile_bits) * N;
+        uint32_t key[E];
+        uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint32_t q = (uint32_t)(w * kWarpShort + e * 32 + lane);
+            key[e] = 0xFFFFFFFFu;
+            if (q < len) {
+                const uint32_t n = vals[start + q];
+                key[e] = __float_as_uint(depth[fb + n]);
+                s_k64[q] = ((unsigned long long)key[e] << 32) | n;
+                dmin = min(dmin, key[e]);
+                dmax = max(dmax, key[e]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+            dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        }
+        if (lane == 0) {
+            s_min[w] = dmin;
+            s_max[w] = dmax;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < kLongWarps; ++v) {
+            dmin = min(dmin, s_min[v]);
+            dmax = max(dmax, s_max[v]);
+        }
+        const int sh = max(0, (32 - __clz(dmax - dmin)) - (31 - IB));
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint32_t q = (uint32_t)(w * kWarpShort + e * 32 + lane);
+            if (q < len) key[e] = (((key[e] - dmin) >> sh) << IB) | q;
+        }
+        bitonic_u32<E>(key, lane);
+#pragma unroll
+        for (int e = 0; e < E; ++e) s_run[w * kWarpShort + e * 32 + lane] = key[e];
+        __syncthreads();
+        // merged position: own rank + the keys below it in every other run (runs past
+        // the list's end hold padding only and count nothing)
+        const int runs = (int)((len + kWarpShort - 1) / kWarpShort);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint32_t x = key[e];
+            if (x == 0xFFFFFFFFu) continue;          // padding (real keys stay below 2^31)
+            uint32_t pos = (uint32_t)(e * 32 + lane);
+            for (int v = 0; v < runs; ++v) {
+                if (v == w) continue;
+                const uint32_t *r = s_run + v * kWarpShort;
+                int lo = 0, hi = kWarpShort;         // count of r[] < x
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (r[mid] < x) lo = mid + 1;
+                    else hi = mid;
+                }
+                pos += (uint32_t)lo;
+            }
+            if (pos < len) s_out[pos] = x;
+        }
+        __syncthreads();
+        // equal depth fields next to each other: odd-even transposition on full keys
+        if (threadIdx.x == 0) s_flag = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x + 1; i < len; i += blockDim.x)
+            if ((s_out[i - 1] >> IB) == (s_out[i] >> IB)) s_flag = 1;
+        __syncthreads();
+        bool ok = true;
+        if (s_flag) {
+            int quiet = 0;
+            for (int round = 0; round < kFixRounds && quiet < 2; ++round) {
+                __syncthreads();
+                if (threadIdx.x == 0) s_flag = 0;
+                __syncthreads();
+                for (uint32_t i = 2 * threadIdx.x + (round & 1); i + 1 < len; i += 2 * blockDim.x) {
+                    const uint32_t a = s_out[i], b = s_out[i + 1];
+                    if ((a >> IB) == (b >> IB) && s_k64[a & kSlot] > s_k64[b & kSlot]) {
+                        s_out[i] = b;
+                        s_out[i + 1] = a;
+                        s_flag = 1;
+                    }
+                }
+                __syncthreads();
+                quiet = s_flag ? 0 : quiet + 1;
+            }
+            ok = quiet >= 2;
+        }
+        if (ok) {
+            for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) vals[start + q] = (uint32_t)s_k64[s_out[q] & kSlot];
+        } else if (threadIdx.x == 0) {
+            wide[atomicAdd(list_counts + 4, 1u)] = seg;
+        }
+        __syncthreads();
     }
 }
 
@@ -584,7 +735,7 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
         attr = true;
     }
     // the long lists first (fewer, longer: their tail overlaps nothing otherwise)
-    tile_sort_warp_kernel<true><<<(unsigned)sms * 8, 32 * kWarpSortWarps, 0, s>>>(
+    tile_sort_long_kernel<<<(unsigned)sms * 8, 32 * kLongWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     tile_sort_warp_kernel<false><<<(unsigned)sms * 16, 32 * kWarpSortWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);

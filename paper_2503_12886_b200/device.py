@@ -257,6 +257,7 @@ class Binner:
         self.order = None
         self._ordered = None
         self.tile_counts = None
+        self.order_ready = False
         self.mode = None             # how the last bin() built its lists
         self.longest = 0             # longest (frame, tile) list of the last tile-major binning
 
@@ -380,12 +381,13 @@ class Binner:
         return self.result
 
 
-    def bin_tiles(self, B, N, width, height, records, depth, counts, err):
+    def bin_tiles(self, B, N, width, height, records, depth, counts, err, after_scan=None):
         """Tile-major binning (hs_tile_count / hs_tile_scan / hs_tile_fill) with the
         step's single host read: the scatter and the per-list sorts are enqueued before
         the host waits, sized by the previous step's capacity; a step that needs more
         re-runs them on grown buffers.  Lists longer than hs_tile_sort_cap() fall back to
-        the two-level sort for that step.  Returns (key total, error word)."""
+        the two-level sort for that step.  ``after_scan(ranges, tile_bits)`` enqueues work
+        that needs only the ranges (the raster's tile order).  Returns (key total, error word)."""
         tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
         nseg = B << tile_bits
         d = self.device
@@ -404,6 +406,9 @@ class Binner:
         self.summary_host.copy_(self.summary, non_blocking=True)
         ready = torch.cuda.Event()
         ready.record()
+        self.order_ready = False
+        if after_scan is not None:
+            self.order_ready = after_scan(ranges, tile_bits)
         if self.keys is None:
             self._ensure(4 * B * N)         # a first guess; grown below when short
 
@@ -425,6 +430,8 @@ class Binner:
             fill()
         if self.longest > tile_sort_cap():
             # a list too long to sort in shared memory: the global two-level sort
+            # (whose ranges replace the ones the tile order was built from)
+            self.order_ready = False
             self.depth_order(B, N, depth)
             self._bin_two_level(B, N, width, height, records, counts, total)
             self.mode = "two_level"
@@ -539,6 +546,7 @@ class Trainer:
         self._bucket_events = []
         self._rig_frames = None
         self._rig_event = None
+        self._order_event = None
         self._side = None               # side stream: rig || mlp_fwd + blend_fwd, loss || backward,
         self._side_events = []          # base/delta Adam || mlp_bwd
         self._last_frames = None
@@ -604,12 +612,25 @@ class Trainer:
         self.launches += 1
         return self._rig_frames
 
+    def _tile_order(self, ranges, tile_bits):
+        """The raster's longest-first tile order, built on the side stream while the
+        lists are scattered and sorted; the raster waits for ``_order_event``."""
+        side = self._side_stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            L.call("hs_raster_tile_order", self.B, self.W, self.H, _p(ranges), tile_bits, _stream())
+            ev = torch.cuda.Event()
+            ev.record(side)
+        self._order_event = ev
+        self.launches += 1
+        return True
+
     def _side_stream(self):
         if self._side is None:
             self._side = torch.cuda.Stream(device=self.av.device)
         return self._side
 
-    def _forward_project(self, thetas, frames, cameras, zero=(None, None, None)):
+    def _forward_project(self, thetas, frames, cameras, zero=(None, None, None), order=False):
         av = self.av
         N, K, B = av.N, av.K, self.B
         s = _stream()
@@ -629,7 +650,7 @@ class Trainer:
         if self.tile_binning:
             m = self._mark("bin_tiles")
             total, code = self.binner.bin_tiles(B, N, self.W, self.H, self.records, self.depth, self.counts,
-                                                self.err)
+                                                self.err, self._tile_order if order else None)
             self._done(m)
             self.launches += launches_tiles(self.binner)
             self.err.fill_(-1)
@@ -675,7 +696,9 @@ class Trainer:
         ci = self.color_init and not self._all_visited()
         # the raster's accumulators are zero-filled by the projection pass
         zero = (self.g_splat, self.maxw if ci else None, self.wsums if ci else None)
-        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero)
+        self._order_event = None
+        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero,
+                                                                          order=self.fused_raster)
         frames = self._last_frames
         s = _stream()
         flags = L.RASTER_LOSS
@@ -688,10 +711,16 @@ class Trainer:
         grad_scale = 1.0 / (self.H * self.W * 3.0) / self.global_batch
         if self.fused_raster:
             # forward + adjoint of every pixel block in one pass (hs_raster_train)
+            kernels = 2                         # tile order + the fused raster
+            if self._order_event is not None:   # built on the side stream (see _tile_order)
+                torch.cuda.current_stream().wait_event(self._order_event)
+                if self.binner.mode == "tiles" and self.binner.order_ready:
+                    flags |= L.RASTER_ORDER_READY
+                    kernels = 1                 # (the order was counted in _tile_order)
             self._call("raster", "hs_raster_train", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), _p(self.visited), _p(self.maxw),
                        _p(self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale), _p(self.g_splat), None,
-                       None, s, kernels=2)      # tile order + the fused raster
+                       None, s, kernels=kernels)
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the rest of the backward
             # the loss is only read after the step: reduce it on the side stream
