@@ -285,14 +285,14 @@ __device__ __forceinline__ void bitonic_smem(unsigned long long *s, int P, int t
 // stay rolled (small code: the kernels run out of the instruction cache otherwise).
 template <int E, int JE, typename K>
 __device__ __forceinline__ void swap_regs(K (&key)[E], int k) {
+    const int kd = k >> 5;                       // k >= 64 here: lane bits do not matter
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         if (e & JE) continue;
-        const bool up = ((e * 32) & k) == 0;     // k >= 64 here: lane bits do not matter
+        const bool up = (e & kd) == 0;
         const K a = key[e], b = key[e | JE];
-        const bool sw = (a > b) == up;
-        key[e] = sw ? b : a;
-        key[e | JE] = sw ? a : b;
+        key[e] = up ? min(a, b) : max(a, b);
+        key[e | JE] = up ? max(a, b) : min(a, b);
     }
 }
 
@@ -363,12 +363,15 @@ __device__ __forceinline__ void bitonic_u32(uint32_t (&key)[E], int lane) {
                 else if (E >= 2 && je == 1) swap_regs<E, (E >= 2 ? 1 : 0)>(key, k);
             } else {
                 const bool lower = (lane & j) == 0;
+                // this slot keeps the smaller key when its half runs ascending: the
+                // direction bit is the lane's (k < 32) or the register's (k >= 32)
+                const int kd = k >> 5;
+                const bool lane_up = (lane & k) == 0;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    const bool up = k >= 32 ? ((e * 32) & k) == 0 : (lane & k) == 0;
+                    const bool up = kd ? (e & kd) == 0 : lane_up;
                     const uint32_t o = __shfl_xor_sync(0xffffffffu, key[e], j);
-                    // keep the smaller key when this slot's half runs ascending
-                    key[e] = ((key[e] < o) == (lower == up)) ? key[e] : o;
+                    key[e] = (lower == up) ? min(key[e], o) : max(key[e], o);
                 }
             }
         }
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
             const uint32_t q = (uint32_t)(w * kWarpShort + e * 32 + lane);
             if (q < len) key[e] = (((key[e] - dmin) >> sh) << IB) | q;
         }
-        bitonic_u32<E>(key, lane);
+        if (w * kWarpShort < (int)len) bitonic_u32<E>(key, lane);   // (runs past the end: padding)
 #pragma unroll
         for (int e = 0; e < E; ++e) s_run[w * kWarpShort + e * 32 + lane] = key[e];
         __syncthreads();
@@ -578,14 +581,13 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
             uint32_t pos = (uint32_t)(e * 32 + lane);
             for (int v = 0; v < runs; ++v) {
                 if (v == w) continue;
-                const uint32_t *r = s_run + v * kWarpShort;
-                int lo = 0, hi = kWarpShort;         // count of r[] < x
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (r[mid] < x) lo = mid + 1;
-                    else hi = mid;
-                }
-                pos += (uint32_t)lo;
+                // count of run v's keys below x: a branch-free search over its kWarpShort keys
+                int lo = v * kWarpShort;
+#pragma unroll
+                for (int step = kWarpShort / 2; step > 0; step >>= 1)
+                    if (s_run[lo + step - 1] < x) lo += step;
+                if (s_run[lo] < x) ++lo;
+                pos += (uint32_t)(lo - v * kWarpShort);
             }
             if (pos < len) s_out[pos] = x;
         }

@@ -1,5 +1,5 @@
 """Fraction of (splat, tile) keys the exact ellipse-rectangle test would cull at
-emission (needs a -DHS_BIN_STATS build)."""
+emission (needs a -DHS_BIN_STATS build: HS_B200_LIB=... python scripts/bin_stats.py)."""
 import ctypes
 import os
 import sys
@@ -12,6 +12,7 @@ from bench import CONFIGS, make_trainer  # noqa: E402
 from paper_2503_12886_b200 import _lib as L  # noqa: E402
 
 tr, d, wl = make_trainer(CONFIGS["C2"])
+tr.tile_binning = tr.two_level_binning = False     # the counters live in the one-level emission
 buf = (ctypes.c_uint64 * 2)()
 for _ in range(3):
     tr.step(d["thetas"], d["targets"], None, d["cameras"], d["backgrounds"])
