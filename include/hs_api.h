@@ -191,9 +191,9 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  * hs_tile_count: each (frame, splat) with counts[i] > 0 adds one to every tile of its
  *   pixel bbox in tile_counts [B << tile_bits] (zero on entry; hs_tile_scan re-zeroes it).
  * hs_tile_scan: ranges [2 * (B << tile_bits)] (every entry written), scatter cursors
- *   [B << tile_bits], the segment lists by length class (lists [3 * (B << tile_bits)],
- *   list_counts [8]) and
- *   summary [4] = {key total, error word, depth range as hs_bin_scan, longest list}.
+ *   [B << tile_bits], summary [4] = {key total, error word, depth range as hs_bin_scan,
+ *   longest list}, and in lists [2 * (B << tile_bits)] / list_counts [8] the lists the
+ *   fill sorts per CTA (the rest of lists is the fill's scratch).
  * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
  *   list in (depth, Gaussian index) order -- the reference order.  Skipped on the device
  *   when summary[0] > capacity (grow the buffers, reset the cursors to the range starts

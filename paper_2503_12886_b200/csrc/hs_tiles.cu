@@ -5,10 +5,9 @@
 // order) are built tile-first instead of by a global key sort:
 //
 //   hs_tile_count  every (frame, splat) adds one to each tile of its pixel bbox
-//   hs_tile_scan   one CTA: exclusive scan of the counts -> ranges + scatter cursors,
-//                  the segments sorted into three lists by length, and the step's
-//                  single device->host summary (key total, error word, depth range,
-//                  longest list)
+//   hs_tile_scan   one CTA: exclusive scan of the counts -> ranges + scatter cursors
+//                  and the step's single device->host summary (key total, error word,
+//                  depth range, longest list)
 //   hs_tile_fill   scatter (an atomic cursor per tile, arrival order), then each list
 //                  sorted by the 64-bit key (depth bits << 32 | Gaussian index): a
 //                  register bitonic sort per warp up to 32 entries, a shared-memory
@@ -83,9 +82,9 @@ __global__ void __launch_bounds__(kTileThreads) tile_count_kernel(int64_t items,
 
 // -------------------------------------------------------------------- scan
 
-// List classes (list_counts[c]): 0 = 2..kWarpShort entries and 1 = ..kWarpCap (one
-// warp each; class 1 from the back of `lists`, sorted first), 2 = ..kCtaCap (one CTA
-// each, from lists + nseg), 3 = longer (counted only: the caller's fallback).
+// One CTA: the exclusive scan of the per-(frame, tile) counts -> ranges, scatter
+// cursors, the key total and the longest list; resets the fill's counters.  (The list
+// sorts stride over all segments and pick their length class themselves.)
 constexpr int kScanThreads = 1024;
 constexpr int kScanPer = 16;          // segments per thread and round: tid + k * kScanThreads
 
@@ -98,15 +97,13 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                                                                  const uint32_t *__restrict__ depth_range,
                                                                  unsigned long long *__restrict__ summary) {
     __shared__ uint32_t wt[kScanPer][kScanThreads / 32];   // per k: inclusive scan over warps
-    __shared__ uint32_t wq[4][kScanThreads / 32];           // per class: warp slot bases
-    __shared__ uint32_t qcarry[4], qtot[4], s_max;
+    __shared__ uint32_t s_max, s_big[2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    if (tid < 4) qcarry[tid] = 0u;
-    if (tid == 0) s_max = 0u;
+    if (tid == 0) s_max = s_big[0] = s_big[1] = 0u;
+    __syncthreads();
     uint32_t carry = 0, mx = 0;
     for (int base = 0; base < nseg; base += kScanThreads * kScanPer) {
-        uint32_t c[kScanPer], incl[kScanPer], nq[4] = {0u, 0u, 0u, 0u};
-        int cls[kScanPer];
+        uint32_t c[kScanPer], incl[kScanPer];
 #pragma unroll
         for (int k = 0; k < kScanPer; ++k) {
             const int i = base + k * kScanThreads + tid;
@@ -144,52 +141,30 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                 cursor[i] = run;
                 if (c[k]) tile_counts[i] = 0u;       // ready for the next step's count
             }
-            cls[k] = c[k] < 2u ? -1 : c[k] <= (uint32_t)kWarpShort ? 0 : c[k] <= (uint32_t)kWarpCap ? 1
-                   : c[k] <= (uint32_t)kCtaCap ? 2 : 3;
+            // the CTA-sorted lists, one shared atomic per warp: kWarpShort+1..kWarpCap
+            // entries from the front of lists, kWarpCap+1..kCtaCap from the back
 #pragma unroll
-            for (int q = 0; q < 4; ++q) nq[q] += __popc(__ballot_sync(0xffffffffu, cls[k] == q));
-        }
-        // list slots: per class, an exclusive scan of the warps' counts (deterministic)
-        if (lane < 4) wq[lane][w] = lane == 0 ? nq[0] : lane == 1 ? nq[1] : lane == 2 ? nq[2] : nq[3];
-        __syncthreads();
-        if (w < 4) {
-            const uint32_t v = wq[w][lane];
-            uint32_t x = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += t;
-            }
-            wq[w][lane] = qcarry[w] + x - v;
-            if (lane == 31) qtot[w] = x;
-        }
-        __syncthreads();
-        uint32_t slot[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) slot[q] = wq[q][w];
-#pragma unroll
-        for (int k = 0; k < kScanPer; ++k) {
-            const int i = base + k * kScanThreads + tid;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                const uint32_t m = __ballot_sync(0xffffffffu, cls[k] == q);
-                if (cls[k] == q) {
-                    const uint32_t r = slot[q] + __popc(m & ((1u << lane) - 1u));
-                    if (q == 0) lists[r] = (uint32_t)i;
-                    else if (q == 1) lists[nseg - 1 - r] = (uint32_t)i;
-                    else lists[nseg + r] = (uint32_t)i;
+            for (int q = 0; q < 2; ++q) {
+                const bool big = q == 0 ? c[k] > (uint32_t)kWarpShort && c[k] <= (uint32_t)kWarpCap
+                                        : c[k] > (uint32_t)kWarpCap && c[k] <= (uint32_t)kCtaCap;
+                const uint32_t m = __ballot_sync(0xffffffffu, big);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    uint32_t first = 0;
+                    if (lane == leader) first = atomicAdd(&s_big[q], (uint32_t)__popc(m));
+                    first = __shfl_sync(0xffffffffu, first, leader);
+                    const uint32_t r = first + __popc(m & ((1u << lane) - 1u));
+                    if (big) lists[q == 0 ? r : nseg - 1 - r] = (uint32_t)i;
                 }
-                slot[q] += __popc(m);
             }
         }
-        __syncthreads();   // wt / wq are rewritten by the next round
-        if (tid < 4) qcarry[tid] += qtot[tid];
-        __syncthreads();
+        __syncthreads();   // wt is rewritten by the next round
     }
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) atomicMax(&s_max, mx);
     __syncthreads();
-    if (tid < 4) list_counts[tid] = qcarry[tid];
-    if (tid == 4) list_counts[4] = 0u;                 // the fill's 64-bit fallback count
+    // [1] / [2]: the long / longer lists, [4]: the fallback's count
+    if (tid < 8) list_counts[tid] = tid == 1 ? s_big[0] : tid == 2 ? s_big[1] : 0u;
     if (tid == 0) {
         summary[0] = carry;
         summary[1] = err ? *err : HS_NO_ERROR;
@@ -458,7 +433,7 @@ __device__ __forceinline__ bool sort_list_warp32(const float *__restrict__ depth
     return true;
 }
 
-// lists the 32-bit sort declines go to lists[2 * nseg + ...] (count list_counts[4])
+// lists the 32-bit sort declines go to lists[nseg + ...] (count list_counts[4])
 template <int E>
 __device__ __forceinline__ void sort_list(const float *__restrict__ depth, int64_t fb, uint32_t start,
                                           uint32_t len, uint32_t *__restrict__ vals, int lane,
@@ -481,17 +456,24 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
     __shared__ unsigned long long s_k64_all[kWarpSortWarps][kLong ? kWarpCap : kWarpShort];
     __shared__ uint32_t s_q_all[kWarpSortWarps][kLong ? kWarpCap : kWarpShort];
-    uint32_t *wide = lists + 2 * (size_t)nseg;
+    uint32_t *wide = lists + nseg;
     if (summary[0] > capacity) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned long long *s_k64 = s_k64_all[w];
     uint32_t *s_q = s_q_all[w];
-    const uint32_t count = list_counts[kLong ? 1 : 0];
+    // warp g takes segments g + j * stride; 32 candidates are read at once (one per lane)
     const uint32_t stride = gridDim.x * kWarpSortWarps;
-    for (uint32_t e = blockIdx.x * kWarpSortWarps + w; e < count; e += stride) {
-        const uint32_t seg = kLong ? lists[nseg - 1 - e] : lists[e];
-        const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
-        const uint32_t start = rg.x, len = rg.y - rg.x;
+    for (uint32_t base = blockIdx.x * kWarpSortWarps + w; base < (uint32_t)nseg; base += 32 * stride) {
+      const uint32_t seg_l = base + lane * stride;
+      const uint2 rg_l = seg_l < (uint32_t)nseg ? reinterpret_cast<const uint2 *>(ranges)[seg_l] : make_uint2(0u, 0u);
+      const uint32_t len_l = rg_l.y - rg_l.x;
+      uint32_t pick = __ballot_sync(0xffffffffu, kLong ? (len_l > (uint32_t)kWarpShort && len_l <= (uint32_t)kWarpCap)
+                                                        : (len_l >= 2u && len_l <= (uint32_t)kWarpShort));
+      while (pick) {
+        const int b = __ffs(pick) - 1;
+        pick &= pick - 1u;
+        const uint32_t seg = base + b * stride;
+        const uint32_t start = __shfl_sync(0xffffffffu, rg_l.x, b), len = __shfl_sync(0xffffffffu, len_l, b);
         const int64_t fb = (int64_t)(seg >> tile_bits) * N;
         if (kLong) {
             if (len <= 512u) sort_list<16>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
@@ -502,6 +484,7 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB
             else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
             else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
         }
+      }
     }
 }
 
@@ -525,10 +508,12 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
     __shared__ int s_flag;
     if (summary[0] > capacity) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t count = list_counts[1];
-    uint32_t *wide = lists + 2 * (size_t)nseg;
-    for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
-        const uint32_t seg = lists[nseg - 1 - li];
+    uint32_t *wide = lists + nseg;
+    // the lists longer than kWarpShort, collected by the scan: CTA c takes c + j * gridDim.x
+    const uint32_t nbig = list_counts[1];
+    for (uint32_t li = blockIdx.x; li < nbig; li += gridDim.x) {
+      {
+        const uint32_t seg = lists[li];
         const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
         const uint32_t start = rg.x, len = rg.y - rg.x;
         const int64_t fb = (int64_t)(seg >> tile_bits) * N;
@@ -624,6 +609,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
             wide[atomicAdd(list_counts + 4, 1u)] = seg;
         }
         __syncthreads();
+      }
     }
 }
 
@@ -637,7 +623,7 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps) tile_sort_wide_kernel(
     const uint32_t count = list_counts[4];
     const uint32_t stride = gridDim.x * kWarpSortWarps;
     for (uint32_t e = blockIdx.x * kWarpSortWarps + w; e < count; e += stride) {
-        const uint32_t seg = lists[2 * (size_t)nseg + e];
+        const uint32_t seg = lists[nseg + e];
         const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
         const uint32_t start = rg.x, len = rg.y - rg.x;
         const int64_t fb = (int64_t)(seg >> tile_bits) * N;
@@ -657,9 +643,10 @@ __global__ void __launch_bounds__(kCtaSortThreads) tile_sort_cta_kernel(
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
     extern __shared__ unsigned long long s_keys[];
     if (summary[0] > capacity) return;
-    const uint32_t count = list_counts[2];
-    for (uint32_t e = blockIdx.x; e < count; e += gridDim.x) {
-        const uint32_t seg = lists[nseg + e];
+    const uint32_t nbig = list_counts[2];
+    for (uint32_t li = blockIdx.x; li < nbig; li += gridDim.x) {
+      {
+        const uint32_t seg = lists[nseg - 1 - li];
         const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
         const uint32_t start = rg.x, len = rg.y - rg.x;
         const int64_t fb = (int64_t)(seg >> tile_bits) * N;
@@ -671,6 +658,7 @@ __global__ void __launch_bounds__(kCtaSortThreads) tile_sort_cta_kernel(
         bitonic_smem<true>(s_keys, P, threadIdx.x, kCtaSortThreads);
         for (int q = threadIdx.x; q < (int)len; q += kCtaSortThreads) vals[start + q] = (uint32_t)s_keys[q];
         __syncthreads();
+      }
     }
 }
 

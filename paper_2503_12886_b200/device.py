@@ -394,15 +394,15 @@ class Binner:
         if self.tile_counts is None or self.tile_counts.numel() < nseg:
             self.tile_counts = torch.zeros(nseg, dtype=torch.int32, device=d)
             self.cursor = torch.empty(nseg, dtype=torch.int32, device=d)
-            self.lists = torch.empty(3 * nseg, dtype=torch.int32, device=d)
+            self.lists = torch.empty(2 * nseg, dtype=torch.int32, device=d)
             self.list_counts = torch.empty(8, dtype=torch.int32, device=d)
         if self.ranges is None or self.ranges.numel() < 2 * nseg:
             self.ranges = torch.empty(2 * nseg, dtype=torch.int32, device=d)
         ranges = self.ranges[:2 * nseg]
         s = _stream()
         L.call("hs_tile_count", B, N, width, height, _p(records), _p(counts), _p(self.tile_counts), s)
-        L.call("hs_tile_scan", B, width, height, _p(self.tile_counts), _p(ranges), _p(self.cursor), _p(self.lists),
-               _p(self.list_counts), _p(err), _p(self.depth_range), _p(self.summary), s)
+        L.call("hs_tile_scan", B, width, height, _p(self.tile_counts), _p(ranges), _p(self.cursor),
+               _p(self.lists), _p(self.list_counts), _p(err), _p(self.depth_range), _p(self.summary), s)
         self.summary_host.copy_(self.summary, non_blocking=True)
         ready = torch.cuda.Event()
         ready.record()
