@@ -45,10 +45,40 @@ struct TileBox {
     int ty0, ty1, tx0, tx1;
 };
 
-__device__ __forceinline__ TileBox tile_box(const float *__restrict__ records, int64_t i) {
-    const float *rec = records + i * kRec;
-    const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);
-    return {unpack_lo(rows) / kTile, unpack_hi(rows) / kTile, unpack_lo(cols) / kTile, unpack_hi(cols) / kTile};
+
+// The CTA's items, kPer per thread (item k = threadIdx.x + j * kTileThreads), loaded
+// up front so the loads overlap: count, pixel bbox, frame.
+constexpr int kPer = kTileItems / kTileThreads;
+
+struct CtaItems {
+    uint32_t rows[kPer], cols[kPer], n[kPer], b[kPer];
+    bool live[kPer];
+};
+
+__device__ __forceinline__ void load_items(CtaItems &it, int64_t items, int64_t N, const float *__restrict__ records,
+                                           const uint32_t *__restrict__ counts) {
+    const int64_t i0 = blockIdx.x * (int64_t)kTileItems;
+    const int64_t b0 = i0 / N;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int64_t i = i0 + threadIdx.x + j * kTileThreads;
+        const bool in = i < items;
+        it.live[j] = in && counts[i] != 0u;
+        it.rows[j] = in ? __float_as_uint(records[i * kRec + 7]) : 0u;
+        it.cols[j] = in ? __float_as_uint(records[i * kRec + 8]) : 0u;
+        int64_t b = b0, n = i - b0 * N;
+        if (n >= N) {                            // past the CTA's first frame (rare)
+            b = i / N;
+            n = i - b * N;
+        }
+        it.b[j] = (uint32_t)b;
+        it.n[j] = (uint32_t)n;
+    }
+}
+
+__device__ __forceinline__ TileBox item_box(const CtaItems &it, int j) {
+    return {unpack_lo(it.rows[j]) / kTile, unpack_hi(it.rows[j]) / kTile, unpack_lo(it.cols[j]) / kTile,
+            unpack_hi(it.cols[j]) / kTile};
 }
 
 __global__ void __launch_bounds__(kTileThreads) tile_count_kernel(int64_t items, int64_t N, int tiles_x, int tiles,
@@ -56,18 +86,18 @@ __global__ void __launch_bounds__(kTileThreads) tile_count_kernel(int64_t items,
                                                                   const uint32_t *__restrict__ counts,
                                                                   uint32_t *__restrict__ tile_counts) {
     extern __shared__ uint32_t hist[];
-    const int64_t i0 = blockIdx.x * (int64_t)kTileItems;
-    const int64_t b0 = i0 / N;
+    const uint32_t b0 = (uint32_t)(blockIdx.x * (int64_t)kTileItems / N);
     const bool shared = tiles <= kTileSmemBins;
+    CtaItems it;
+    load_items(it, items, N, records, counts);
     if (shared)
         for (int t = threadIdx.x; t < tiles; t += kTileThreads) hist[t] = 0u;
     __syncthreads();
-    for (int k = threadIdx.x; k < kTileItems; k += kTileThreads) {
-        const int64_t i = i0 + k;
-        if (i >= items || counts[i] == 0u) continue;
-        const int64_t b = i / N;
-        const TileBox bx = tile_box(records, i);
-        uint32_t *dst = (shared && b == b0) ? hist : tile_counts + ((size_t)b << tile_bits);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        if (!it.live[j]) continue;
+        const TileBox bx = item_box(it, j);
+        uint32_t *dst = (shared && it.b[j] == b0) ? hist : tile_counts + ((size_t)it.b[j] << tile_bits);
         for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
             for (int tx = bx.tx0; tx <= bx.tx1; ++tx) atomicAdd(dst + ty * tiles_x + tx, 1u);
     }
@@ -188,16 +218,17 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
                                                                     uint32_t *__restrict__ vals) {
     extern __shared__ uint32_t hist[];
     if (summary[0] > capacity) return;               // the caller grows the buffers and re-runs
-    const int64_t i0 = blockIdx.x * (int64_t)kTileItems;
-    const int64_t b0 = i0 / N;
+    const uint32_t b0 = (uint32_t)(blockIdx.x * (int64_t)kTileItems / N);
     const bool shared = tiles <= kTileSmemBins;
+    CtaItems it;
+    load_items(it, items, N, records, counts);
     if (shared) {
         for (int t = threadIdx.x; t < tiles; t += kTileThreads) hist[t] = 0u;
         __syncthreads();
-        for (int k = threadIdx.x; k < kTileItems; k += kTileThreads) {
-            const int64_t i = i0 + k;
-            if (i >= items || counts[i] == 0u || i / N != b0) continue;
-            const TileBox bx = tile_box(records, i);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            if (!it.live[j] || it.b[j] != b0) continue;
+            const TileBox bx = item_box(it, j);
             for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
                 for (int tx = bx.tx0; tx <= bx.tx1; ++tx) atomicAdd(hist + ty * tiles_x + tx, 1u);
         }
@@ -209,20 +240,18 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
         }
         __syncthreads();
     }
-    for (int k = threadIdx.x; k < kTileItems; k += kTileThreads) {
-        const int64_t i = i0 + k;
-        if (i >= items || counts[i] == 0u) continue;
-        const int64_t b = i / N;
-        const uint32_t n = (uint32_t)(i - b * N);
-        const TileBox bx = tile_box(records, i);
-        const bool local = shared && b == b0;
-        const uint32_t hi = (uint32_t)b << tile_bits;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        if (!it.live[j]) continue;
+        const TileBox bx = item_box(it, j);
+        const bool local = shared && it.b[j] == b0;
+        const uint32_t hi = it.b[j] << tile_bits;
         for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
             for (int tx = bx.tx0; tx <= bx.tx1; ++tx) {
                 const uint32_t t = (uint32_t)(ty * tiles_x + tx);
-                const uint32_t pos = atomicAdd(local ? hist + t : cursor + (hi | t), 1u);
+                const uint32_t pos = local ? atomicAdd(hist + t, 1u) : atomicAdd(cursor + (hi | t), 1u);
                 keys[pos] = hi | t;
-                vals[pos] = n;
+                vals[pos] = it.n[j];
             }
     }
 }
