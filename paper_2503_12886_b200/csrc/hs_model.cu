@@ -264,19 +264,23 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
 // basis k are reduce-scattered across the warp (16 values in 16 shuffles) and
 // accumulated per warp in shared memory, then summed over the CTA's warps.
 #ifndef HS_BLEND_MINB
-#define HS_BLEND_MINB 3
+#define HS_BLEND_MINB 2
 #endif
 constexpr int kBT = 256;
 constexpr int kBMaxB = 16;
 constexpr int kBMaxK = 32;
 #ifndef HS_BLEND_BLOCKS
-#define HS_BLEND_BLOCKS 444          // one wave at 3 CTAs per SM (148 x 3)
+#define HS_BLEND_BLOCKS 296          // one wave at 2 CTAs per SM (148 x 2)
 #endif
 constexpr int kBBlocks = HS_BLEND_BLOCKS;   // persistent grid
 #ifndef HS_BLEND_KBB
-#define HS_BLEND_KBB 8
+#define HS_BLEND_KBB 2
 #endif
-constexpr int kKBB = HS_BLEND_KBB;  // delta loads in flight per lane
+constexpr int kKBB = HS_BLEND_KBB;  // delta loads in flight per lane (per chunk)
+#ifndef HS_BLEND_CPI
+#define HS_BLEND_CPI 4
+#endif
+constexpr int kCPI = HS_BLEND_CPI;  // chunks per warp iteration
 
 template <int BP>
 __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N, int K, int Bc, int b0,
@@ -298,40 +302,58 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
     __syncthreads();
     const int64_t E10 = 10 * N, E14 = 14 * N;
     const int64_t chunks = (E14 + 31) / 32;
-    for (int64_t c = (int64_t)blockIdx.x * (kBT / 32) + warp; c < chunks; c += (int64_t)gridDim.x * (kBT / 32)) {
-        const int64_t e = c * 32 + lane;
-        const bool in = e < E14;
-        float g[BP];
-        float s = 0.f;
+    // kCPI consecutive 32-channel chunks per warp iteration: the g_psi products of the
+    // chunks are summed in registers before the one reduce-scatter per basis
+    for (int64_t c0 = ((int64_t)blockIdx.x * (kBT / 32) + warp) * kCPI; c0 < chunks;
+         c0 += (int64_t)gridDim.x * (kBT / 32) * kCPI) {
+        float g[kCPI][BP];
+        bool in10[kCPI];
 #pragma unroll
-        for (int b = 0; b < BP; ++b) {
-            g[b] = (in && b < Bc) ? __ldcs(g_raw + (int64_t)(b0 + b) * E14 + e) : 0.f;
-            s += g[b];
+        for (int j = 0; j < kCPI; ++j) {
+            const int64_t e = (c0 + j) * 32 + lane;
+            const bool in = e < E14;
+            in10[j] = e < E10;
+            float s = 0.f;
+#pragma unroll
+            for (int b = 0; b < BP; ++b) {
+                g[j][b] = (in && b < Bc) ? __ldcs(g_raw + (int64_t)(b0 + b) * E14 + e) : 0.f;
+                s += g[j][b];
+            }
+            if (in) g_base[e] = accumulate ? g_base[e] + s : s;
         }
-        if (in) g_base[e] = accumulate ? g_base[e] + s : s;
-        if (c * 32 >= E10) continue;                       // warp-uniform
-        const bool in10 = e < E10;
+        if (c0 * 32 >= E10) continue;                      // warp-uniform
+        const int64_t e0 = c0 * 32 + lane;
         for (int k0 = 0; k0 < K; k0 += kKBB) {
-          float dk[kKBB];
+          float dk[kCPI][kKBB];
 #pragma unroll
           for (int q = 0; q < kKBB; ++q)     // issue the round's loads before any use
-              dk[q] = in10 ? __ldcs(deltas + (int64_t)min(k0 + q, K - 1) * E10 + e) : 0.f;
+#pragma unroll
+              for (int j = 0; j < kCPI; ++j)
+                  dk[j][q] = in10[j] ? __ldcs(deltas + (int64_t)min(k0 + q, K - 1) * E10 + e0 + 32 * j) : 0.f;
 #pragma unroll
           for (int q = 0; q < kKBB; ++q) {
             const int k = k0 + q;
             if (k >= K) break;
-            const float d = dk[q];
-            float gd = 0.f;
+            float gd[kCPI];
             float v[BP];
 #pragma unroll
+            for (int j = 0; j < kCPI; ++j) gd[j] = 0.f;
+#pragma unroll
             for (int b = 0; b < BP; ++b) {
-                gd = fmaf(p_s[b * K + k], g[b], gd);
-                v[b] = d * g[b];
+                const float pk = p_s[b * K + k];
+                v[b] = 0.f;
+#pragma unroll
+                for (int j = 0; j < kCPI; ++j) {
+                    gd[j] = fmaf(pk, g[j][b], gd[j]);
+                    v[b] = fmaf(dk[j][q], g[j][b], v[b]);
+                }
             }
-            if (in10) {
-                float *o = g_deltas + (int64_t)k * E10 + e;
-                *o = accumulate ? *o + gd : gd;
-            }
+#pragma unroll
+            for (int j = 0; j < kCPI; ++j)
+                if (in10[j]) {
+                    float *o = g_deltas + (int64_t)k * E10 + e0 + 32 * j;
+                    *o = accumulate ? *o + gd[j] : gd[j];
+                }
             int vi;
             bool issue;
             const float r = reduce_scatter(v, lane, vi, issue);

@@ -452,9 +452,9 @@ def tile_sort_cap():
 
 
 def launches_tiles(binner):
-    """Kernel launches issued by Binner.bin_tiles: count, scan, scatter, the two list
-    sorts (+ the two-level fallback's)."""
-    n = 5
+    """Kernel launches issued by Binner.bin_tiles: count, scan, scatter, the four list
+    sorts (warp, CTA-cooperative, long-list, 64-bit fallback) (+ the two-level fallback's)."""
+    n = 7
     if binner.mode == "two_level":
         n += 6 + launches_binning(1, binner.passes, True)
     return n
