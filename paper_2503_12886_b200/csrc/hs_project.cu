@@ -221,13 +221,15 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
     float dz = 0.f;
+    // the step's per-(frame, splat) accumulators, zeroed here instead of by separate
+    // fills (the raster adds into them with atomics); g_splat: the CTA's contiguous
+    // 256 x kGS floats with coalesced stores
+    if (zero_gsplat) {
+        const int64_t lo = blockIdx.x * (int64_t)blockDim.x * kGS;
+        const int64_t hi = min((int64_t)B * N, (blockIdx.x + 1) * (int64_t)blockDim.x) * kGS;
+        for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) zero_gsplat[k] = 0.f;
+    }
     if (i < (int64_t)B * N) {
-        // the step's per-(frame, splat) accumulators, zeroed here instead of by
-        // separate fills: the raster adds into them with atomics
-        if (zero_gsplat) {
-#pragma unroll
-            for (int k = 0; k < kGS; ++k) zero_gsplat[i * kGS + k] = 0.f;
-        }
         if (zero_maxw) zero_maxw[i] = 0.f;
         if (zero_wsums) reinterpret_cast<float4 *>(zero_wsums)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         const int b = (int)(i / N);
