@@ -201,9 +201,9 @@ def test_binning_bit_exact():
         check_tiles(dev, res, s, regrow=True)
 
 
-@pytest.mark.parametrize("n", [200, 1000, 9000])
+@pytest.mark.parametrize("n", [200, 1000, 3000, 9000])
 def test_binning_bit_exact_crowded_tiles(n):
-    """One 16x16 tile holding 200 / 1000 / 9000 splats with many exact depth ties
+    """One 16x16 tile holding 200 / 1000 / 3000 / 9000 splats with many exact depth ties
     (quantized positions): the stable sort must break ties by Gaussian index."""
     from paper_2503_12886_b200 import compat as C
     rng = np.random.default_rng(n)
