@@ -114,9 +114,10 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height,
                           float *records, float *depth, uint32_t *counts,
                           uint32_t *block_sums, uint32_t *depth_range, float *radius,
                           float *zero_gsplat, float *zero_maxw, float *zero_wsums,
-                          unsigned long long *err, void *stream);
+                          uint32_t *tile_counts, unsigned long long *err, void *stream);
 /* (zero_gsplat [B*N*9], zero_maxw [B*N], zero_wsums [B*N*4]: optional accumulators of
- *  the step's raster, zero-filled in the same pass -- NULL to skip.)
+ *  the step's raster, zero-filled in the same pass -- NULL to skip.  tile_counts
+ *  [B << tile_bits]: optional, hs_tile_count done in the same pass (zero on entry).)
  * Projection of already-activated world Gaussians (compat preprocess).
  * radius (B*N, 0 for culled splats), x_cam (B*N*3) and cov_cam (B*N*9) are
  * optional outputs (NULL to skip) in both projection calls. */

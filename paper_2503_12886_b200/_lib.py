@@ -45,7 +45,7 @@ SIGNATURES = {
     "hs_blend_bwd": (_I, [_L, _I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I), _P]),
     "hs_blend_bwd_partials": (_I, [_L]),
     "hs_project_avatar_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                                   _P, _P]),
+                                   _P, _P, _P]),
     "hs_project_world_fwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_project_avatar_bwd": (_I, [_I, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_project_world_bwd": (_I, [_I, _L, _P, _P, _P, _P, _P]),

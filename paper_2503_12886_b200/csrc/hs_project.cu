@@ -79,8 +79,12 @@ __device__ __forceinline__ void project_one(const float pw[3], const float q[4],
 // Record + tile count.  Pixel bbox per SURVEY Appendix B step 2: IEEE fp32, one
 // rounding per op (the __f*_rn intrinsics forbid FMA contraction) so the key
 // list is bit-exact against oracle/binning.py.
+struct TileRect {
+    int ty0, ty1, tx0, tx1;
+};
+
 __device__ __forceinline__ uint32_t write_record(const Proj &p, float op, const float col[3], int W, int H,
-                                                 float *__restrict__ rec) {
+                                                 float *__restrict__ rec, TileRect *rect = nullptr) {
     int r_lo = 1, r_hi = 0, c_lo = 1, c_hi = 0;
     if (p.valid) {
         const float rl = ceilf(__fsub_rn(__fsub_rn(p.my, p.rad), 0.5f));
@@ -105,7 +109,21 @@ __device__ __forceinline__ uint32_t write_record(const Proj &p, float op, const 
     r4[1] = make_float4(p.cc, op, qmax, __uint_as_float(pack_lohi(r_lo, r_hi)));
     r4[2] = make_float4(__uint_as_float(pack_lohi(c_lo, c_hi)), col[0], col[1], col[2]);
     if (!live) return 0u;
+    if (rect) *rect = {r_lo / kTile, r_hi / kTile, c_lo / kTile, c_hi / kTile};
     return (uint32_t)((r_hi / kTile - r_lo / kTile + 1) * (c_hi / kTile - c_lo / kTile + 1));
+}
+
+// Tile-major binning's count (hs_tile_count), fused: each (frame, splat) adds one per
+// tile of its bbox -- into a shared histogram over the CTA's first frame's tiles,
+// flushed with one global atomic per touched tile, or straight to the global counters.
+constexpr int kProjHistBins = 4096;
+
+__device__ __forceinline__ void count_tiles(uint32_t cnt, const TileRect &r, int b, int b0, bool shared, int tiles_x,
+                                            int tile_bits, uint32_t *hist, uint32_t *tile_counts) {
+    if (!cnt) return;
+    uint32_t *dst = (shared && b == b0) ? hist : tile_counts + ((size_t)b << tile_bits);
+    for (int ty = r.ty0; ty <= r.ty1; ++ty)
+        for (int tx = r.tx0; tx <= r.tx1; ++tx) atomicAdd(dst + ty * tiles_x + tx, 1u);
 }
 
 // Per-256-item sum of tile counts (the key-offset scan input) and the range of the
@@ -217,10 +235,19 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     const float *__restrict__ cams, float *__restrict__ records, float *__restrict__ depth,
     uint32_t *__restrict__ counts, uint32_t *__restrict__ block_sums, uint32_t *__restrict__ depth_range,
     float *__restrict__ radius, float *__restrict__ zero_gsplat, float *__restrict__ zero_maxw,
-    float *__restrict__ zero_wsums, unsigned long long *err) {
+    float *__restrict__ zero_wsums, uint32_t *__restrict__ tile_counts, unsigned long long *err) {
+    extern __shared__ uint32_t hist[];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
     float dz = 0.f;
+    const int tiles_x = (W + kTile - 1) / kTile, tiles = tiles_x * ((H + kTile - 1) / kTile);
+    const int tile_bits = bit_length_u32((uint32_t)(tiles - 1));
+    const int b0 = (int)((blockIdx.x * (int64_t)blockDim.x) / N);
+    const bool shared = tile_counts && tiles <= kProjHistBins;
+    if (shared) {
+        for (int t = threadIdx.x; t < tiles; t += blockDim.x) hist[t] = 0u;
+        __syncthreads();
+    }
     // the step's per-(frame, splat) accumulators, zeroed here instead of by separate
     // fills (the raster adds into them with atomics); g_splat: the CTA's contiguous
     // 256 x kGS floats with coalesced stores
@@ -241,13 +268,22 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
         Proj p;
         project_one(a.pw, a.qw, a.s, cams + b * kCam, p);
         if (!ok) p.valid = false;
-        cnt = write_record(p, a.op, a.col, W, H, records + i * kRec);
+        TileRect rect;
+        cnt = write_record(p, a.op, a.col, W, H, records + i * kRec, &rect);
         depth[i] = p.zc;
         dz = p.zc;
         counts[i] = cnt;
         if (radius) radius[i] = p.valid ? p.rad : 0.f;
+        if (tile_counts) count_tiles(cnt, rect, b, b0, shared, tiles_x, tile_bits, hist, tile_counts);
     }
-    block_sum_store(cnt, dz, block_sums, depth_range);
+    block_sum_store(cnt, dz, block_sums, depth_range);   // (a CTA barrier: the histogram is complete)
+    if (shared) {
+        uint32_t *row = tile_counts + ((size_t)b0 << tile_bits);
+        for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+            const uint32_t c = hist[t];
+            if (c) atomicAdd(row + t, c);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256) project_world_fwd_kernel(
@@ -469,15 +505,22 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
                           const float *base14, const int32_t *tri_index, const float *bary, const float *frames,
                           const float *cameras, float *records, float *depth, uint32_t *counts,
                           uint32_t *block_sums, uint32_t *depth_range, float *radius, float *zero_gsplat,
-                          float *zero_maxw, float *zero_wsums, unsigned long long *err, void *stream) {
+                          float *zero_maxw, float *zero_wsums, uint32_t *tile_counts, unsigned long long *err,
+                          void *stream) {
     if (B < 1 || N < 1 || width < 1 || height < 1 || width > 32767 || height > 32767) {
         set_error("hs_project_avatar_fwd: bad sizes B=%d N=%lld %dx%d", B, (long long)N, width, height);
         return HS_ERR_SHAPE;
     }
     const int64_t items = (int64_t)B * N;
-    project_avatar_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream)>>>(
+    const int tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
+    if (tile_counts && bit_length_u32((uint32_t)(tiles - 1)) + bit_length_u32((uint32_t)(B - 1)) > 31) {
+        set_error("hs_project_avatar_fwd: frame/tile bits exceed 31");
+        return HS_ERR_SHAPE;
+    }
+    const size_t smem = tile_counts && tiles <= kProjHistBins ? sizeof(uint32_t) * tiles : 0;
+    project_avatar_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, smem, HS_CHECK_STREAM(stream)>>>(
         B, N, F, width, height, raw10, base14, tri_index, bary, frames, cameras, records, depth, counts,
-        block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, err);
+        block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, tile_counts, err);
     return check_launch("hs_project_avatar_fwd");
 }
 

@@ -381,7 +381,20 @@ class Binner:
         return self.result
 
 
-    def bin_tiles(self, B, N, width, height, records, depth, counts, err, after_scan=None):
+    def tile_count_buffer(self, B, width, height):
+        """The zeroed per-(frame, tile) counters, for a projection that counts the tiles
+        itself (hs_project_avatar_fwd's tile_counts); then bin_tiles(counted=True)."""
+        tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
+        nseg = B << tile_bits
+        d = self.device
+        if self.tile_counts is None or self.tile_counts.numel() < nseg:
+            self.tile_counts = torch.zeros(nseg, dtype=torch.int32, device=d)
+            self.cursor = torch.empty(nseg, dtype=torch.int32, device=d)
+            self.lists = torch.empty(2 * nseg, dtype=torch.int32, device=d)
+            self.list_counts = torch.empty(8, dtype=torch.int32, device=d)
+        return self.tile_counts
+
+    def bin_tiles(self, B, N, width, height, records, depth, counts, err, after_scan=None, counted=False):
         """Tile-major binning (hs_tile_count / hs_tile_scan / hs_tile_fill) with the
         step's single host read: the scatter and the per-list sorts are enqueued before
         the host waits, sized by the previous step's capacity; a step that needs more
@@ -391,16 +404,13 @@ class Binner:
         tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
         nseg = B << tile_bits
         d = self.device
-        if self.tile_counts is None or self.tile_counts.numel() < nseg:
-            self.tile_counts = torch.zeros(nseg, dtype=torch.int32, device=d)
-            self.cursor = torch.empty(nseg, dtype=torch.int32, device=d)
-            self.lists = torch.empty(2 * nseg, dtype=torch.int32, device=d)
-            self.list_counts = torch.empty(8, dtype=torch.int32, device=d)
+        self.tile_count_buffer(B, width, height)
         if self.ranges is None or self.ranges.numel() < 2 * nseg:
             self.ranges = torch.empty(2 * nseg, dtype=torch.int32, device=d)
         ranges = self.ranges[:2 * nseg]
         s = _stream()
-        L.call("hs_tile_count", B, N, width, height, _p(records), _p(counts), _p(self.tile_counts), s)
+        if not counted:
+            L.call("hs_tile_count", B, N, width, height, _p(records), _p(counts), _p(self.tile_counts), s)
         L.call("hs_tile_scan", B, width, height, _p(self.tile_counts), _p(ranges), _p(self.cursor),
                _p(self.lists), _p(self.list_counts), _p(err), _p(self.depth_range), _p(self.summary), s)
         self.summary_host.copy_(self.summary, non_blocking=True)
@@ -454,7 +464,7 @@ def tile_sort_cap():
 def launches_tiles(binner):
     """Kernel launches issued by Binner.bin_tiles: count, scan, scatter, the four list
     sorts (warp, CTA-cooperative, long-list, 64-bit fallback) (+ the two-level fallback's)."""
-    n = 7
+    n = 6                    # (the count runs inside the projection)
     if binner.mode == "two_level":
         n += 6 + launches_binning(1, binner.passes, True)
     return n
@@ -640,17 +650,19 @@ class Trainer:
         self._call("blend_fwd", "hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(self.psi),
                    _p(self.raw10), s)
         F = frames.shape[-2] if frames.dim() == 3 else frames.numel() // (B * 22)
+        # tile-major binning: the projection counts the tiles in the same pass
+        tile_counts = self.binner.tile_count_buffer(B, self.W, self.H) if self.tile_binning else None
         if self._rig_event is not None:
             torch.cuda.current_stream().wait_event(self._rig_event)
             self._rig_event = None
         self._call("project_fwd", "hs_project_avatar_fwd", B, N, F, self.W, self.H, _p(self.raw10), _p(av.base14),
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
                    _p(self.counts), _p(self.block_sums), _p(self.binner.reset_depth_range()), _p(self.radius),
-                   *(_p(z) for z in zero), _p(self.err), s)
+                   *(_p(z) for z in zero), _p(tile_counts), _p(self.err), s)
         if self.tile_binning:
             m = self._mark("bin_tiles")
             total, code = self.binner.bin_tiles(B, N, self.W, self.H, self.records, self.depth, self.counts,
-                                                self.err, self._tile_order if order else None)
+                                                self.err, self._tile_order if order else None, counted=True)
             self._done(m)
             self.launches += launches_tiles(self.binner)
             self.err.fill_(-1)
