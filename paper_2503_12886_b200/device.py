@@ -399,8 +399,9 @@ class Binner:
         step's single host read: the scatter and the per-list sorts are enqueued before
         the host waits, sized by the previous step's capacity; a step that needs more
         re-runs them on grown buffers.  Lists longer than hs_tile_sort_cap() fall back to
-        the two-level sort for that step.  ``after_scan(ranges, tile_bits)`` enqueues work
-        that needs only the ranges (the raster's tile order).  Returns (key total, error word)."""
+        the two-level sort for that step.  ``after_scan(ranges, tile_bits, scanned)`` enqueues
+        work that needs only the ranges (the raster's tile order; ``scanned`` is the event
+        after the scan).  Returns (key total, error word)."""
         tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
         nseg = B << tile_bits
         d = self.device
@@ -416,9 +417,6 @@ class Binner:
         self.summary_host.copy_(self.summary, non_blocking=True)
         ready = torch.cuda.Event()
         ready.record()
-        self.order_ready = False
-        if after_scan is not None:
-            self.order_ready = after_scan(ranges, tile_bits)
         if self.keys is None:
             self._ensure(4 * B * N)         # a first guess; grown below when short
 
@@ -426,7 +424,10 @@ class Binner:
             L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(depth), _p(ranges),
                    _p(self.cursor), _p(self.lists), _p(self.list_counts), _p(self.summary), self.cap,
                    _p(self.keys), _p(self.vals), s)
-        fill()
+        fill()                              # first: the GPU reaches it right after the scan
+        self.order_ready = False
+        if after_scan is not None:
+            self.order_ready = after_scan(ranges, tile_bits, ready)
         ready.synchronize()
         total = int(self.summary_host[0])
         code = int(self.summary_host[1]) & 0xFFFFFFFFFFFFFFFF
@@ -622,11 +623,11 @@ class Trainer:
         self.launches += 1
         return self._rig_frames
 
-    def _tile_order(self, ranges, tile_bits):
+    def _tile_order(self, ranges, tile_bits, scanned):
         """The raster's longest-first tile order, built on the side stream while the
         lists are scattered and sorted; the raster waits for ``_order_event``."""
         side = self._side_stream()
-        side.wait_stream(torch.cuda.current_stream())
+        side.wait_event(scanned)
         with torch.cuda.stream(side):
             L.call("hs_raster_tile_order", self.B, self.W, self.H, _p(ranges), tile_bits, _stream())
             ev = torch.cuda.Event()
