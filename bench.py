@@ -133,6 +133,20 @@ def stage_bytes(B, N, K, H, D, W, Hh, keys, params, color_init=True, passes=6):
     return out
 
 
+def mufu_bound(keys_per_image, sm_mhz, value):
+    """The SFU (MUFU) bound on images/s: 256 evaluations per (splat, tile) key, ~3 MUFU
+    ops per evaluation, 148 SMs x 16 MUFU/clk at the measured SM clock."""
+    import torch
+    if not sm_mhz:
+        return None
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    peak = sms * 16 * sm_mhz * 1e6
+    per_image = 256.0 * keys_per_image * 3.0
+    bound = peak / per_image
+    return {"evals_per_image": 256.0 * keys_per_image, "mufu_per_eval": 3, "peak_mufu_per_s": peak,
+            "bound_images_s": bound, "frac": value / bound}
+
+
 # --------------------------------------------------------------- workloads
 
 CONFIGS = {
@@ -349,6 +363,9 @@ def run_b200(args, cfg):
             "step_roofline": {"algorithmic_bytes_per_step": step_bytes,
                               "achieved_gbs": step_bytes / (ms / 1000.0) / 1e9,
                               "frac": step_bytes / (ms / 1000.0) / 1e9 / peak},
+            # SURVEY 8(d)'s secondary bound: 256 pixel evaluations per key, ~3 MUFU ops each
+            # (ex2 forward; ex2 + rcp in the adjoint) at 16 MUFU/clk/SM
+            "mufu_bound": mufu_bound(tr.last_total / B, clk.get("sm_mhz") or clk.get("sm_max_mhz"), value / world),
             "stages_ms": {k: round(v, 4) for k, v in per_step.items()},
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": tr.h2d_bytes(F, frames=False),
