@@ -419,6 +419,10 @@ __global__ void __launch_bounds__(256, HS_PBWD_MINB) project_avatar_bwd_kernel(
     const int b = (int)(i / N);
     const int64_t n = i - (int64_t)b * N;
     float *o = g_raw14 + (int64_t)b * 14 * N;
+    // the splat gradients first: their loads overlap the forward recomputation
+    float gs[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) gs[k] = __ldcs(g_splat + i * kGS + k);
     AvatarWorld a;
     avatar_world(N, b, n, F, raw10, base14, tri, bary, frames, a);
     Proj p;
@@ -426,9 +430,6 @@ __global__ void __launch_bounds__(256, HS_PBWD_MINB) project_avatar_bwd_kernel(
     float g_xt[3] = {0.f, 0.f, 0.f}, g_qraw[4] = {0.f, 0.f, 0.f, 0.f}, g_sr[3] = {0.f, 0.f, 0.f};
     float g_colr[3] = {0.f, 0.f, 0.f}, g_opr = 0.f;
     if (p.valid) {
-        float gs[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) gs[k] = g_splat[i * kGS + k];
         float g_pw[3], g_qw[4], g_s[3];
         preprocess_bwd_one(p, a.qw, a.s, cams + b * kCam, gs, g_pw, g_qw, g_s);
         // transform_backward (S/binding.py:191-204)
