@@ -754,10 +754,23 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
         attr = true;
     }
     // the long lists first (fewer, longer: their tail overlaps nothing otherwise)
+    // the short lists sort on a library-internal stream alongside the long ones (each
+    // kernel leaves SMs idle in its tail); the caller's stream waits for both
+    static cudaStream_t side = nullptr;
+    static cudaEvent_t scattered = nullptr, shorts_done = nullptr;
+    if (!side) {
+        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&scattered, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&shorts_done, cudaEventDisableTiming);
+    }
+    cudaEventRecord(scattered, s);
+    cudaStreamWaitEvent(side, scattered, 0);
+    tile_sort_warp_kernel<false><<<(unsigned)sms * 16, 32 * kWarpSortWarps, 0, side>>>(
+        N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
+    cudaEventRecord(shorts_done, side);
     tile_sort_long_kernel<<<(unsigned)sms * 8, 32 * kLongWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
-    tile_sort_warp_kernel<false><<<(unsigned)sms * 16, 32 * kWarpSortWarps, 0, s>>>(
-        N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
+    cudaStreamWaitEvent(s, shorts_done, 0);
     tile_sort_wide_kernel<<<(unsigned)sms * 4, 32 * kWarpSortWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     tile_sort_cta_kernel<<<(unsigned)sms * 2, kCtaSortThreads, csmem, s>>>(N, tile_bits, nseg, depth, ranges, lists,
