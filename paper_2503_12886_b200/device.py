@@ -250,6 +250,7 @@ class Binner:
         self.offsets = None
         self.summary = torch.empty(4, dtype=torch.int64, device=device)
         self.depth_range = torch.empty(2, dtype=torch.int32, device=device)
+        self._depth_range_init = None
         self.depth_bits = (0, 0)
         self.passes = 0
         self.ranges = None
@@ -275,9 +276,12 @@ class Binner:
         self.cap = cap
 
     def reset_depth_range(self):
-        """{0xFFFFFFFF, 0}: the projection atomically narrows it to the depths that emit keys."""
-        self.depth_range[0] = -1
-        self.depth_range[1] = 0
+        """{0xFFFFFFFF, 0}: the projection atomically narrows it to the depths that emit keys.
+        (A device-to-device copy: element assignment from a host scalar would be a
+        pageable host->device copy, which blocks the host until the stream drains.)"""
+        if self._depth_range_init is None:
+            self._depth_range_init = torch.tensor([-1, 0], dtype=torch.int32, device=self.device)
+        self.depth_range.copy_(self._depth_range_init)
         return self.depth_range
 
     def scan(self, block_sums, nblocks, err, overlap=None):
