@@ -4,6 +4,8 @@ device's compositing order and bbox, like test_c1_step_vs_oracle):
 * non-square image whose sides are not multiples of the 16-px tile, one frame, K = 1;
 * 17 frames (two frame chunks in blend_bwd, 5 frame bits), K = 25;
 * an image with more than 1024 tiles (12 tile bits in the sort keys);
+* Gaussian counts whose CTAs straddle frames, and 16,384 tiles per frame (past the
+  shared-memory tile histograms);
 and, at each shape, the fused training raster against the separate forward/adjoint
 kernels."""
 import numpy as np
@@ -20,6 +22,10 @@ CASES = {
     "nonsquare_b1_k1": dict(uv=40, B=1, W=200, H=136, K=1, hidden=8),
     "b17_k25": dict(uv=32, B=17, W=64, H=64, K=25, hidden=16),
     "tiles3185": dict(uv=48, B=2, W=1040, H=784, K=4, hidden=16),
+    # 1,296 Gaussians: projection / scatter CTAs straddle frame boundaries
+    "b3_unaligned": dict(uv=36, B=3, W=96, H=80, K=3, hidden=8),
+    # 16,384 tiles per frame: the tile counts and the scatter take the global-atomic path
+    "tiles16384": dict(uv=24, B=1, W=2048, H=2048, K=2, hidden=8),
 }
 
 
