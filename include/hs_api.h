@@ -114,10 +114,14 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height,
                           float *records, float *depth, uint32_t *counts,
                           uint32_t *block_sums, uint32_t *depth_range, float *radius,
                           float *zero_gsplat, float *zero_maxw, float *zero_wsums,
-                          uint32_t *tile_counts, unsigned long long *err, void *stream);
+                          uint32_t *tile_counts, uint32_t *tile_rects, unsigned long long *err,
+                          void *stream);
 /* (zero_gsplat [B*N*9], zero_maxw [B*N], zero_wsums [B*N*4]: optional accumulators of
  *  the step's raster, zero-filled in the same pass -- NULL to skip.  tile_counts
- *  [B << tile_bits]: optional, hs_tile_count done in the same pass (zero on entry).)
+ *  [B << tile_bits]: optional, hs_tile_count done in the same pass (zero on entry).
+ *  tile_rects [B*N]: optional, each item's tile rectangle packed ty0 | ty1 << 8 | tx0 << 16
+ *  | tx1 << 24 (ty0 > ty1 for items without keys) for hs_tile_fill; at most 256 tiles per
+ *  image axis.)
  * Projection of already-activated world Gaussians (compat preprocess).
  * radius (B*N, 0 for culled splats), x_cam (B*N*3) and cov_cam (B*N*9) are
  * optional outputs (NULL to skip) in both projection calls. */
@@ -196,6 +200,7 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   longest list}, and in lists [2 * (B << tile_bits)] / list_counts [8] the lists the
  *   fill sorts per CTA (the rest of lists is the fill's scratch).
  * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
+ *   entry from the items' tile_rects (NULL: from the records' bboxes and counts); each
  *   list in (depth, Gaussian index) order -- the reference order.  Skipped on the device
  *   when summary[0] > capacity (grow the buffers, reset the cursors to the range starts
  *   and call again).  Lists longer than hs_tile_sort_cap() are scattered but NOT sorted:
@@ -207,7 +212,8 @@ int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *
                  uint32_t *lists, uint32_t *list_counts, const unsigned long long *err,
                  const uint32_t *depth_range, unsigned long long *summary, void *stream);
 int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
-                 const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
+                 const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor,
+                 uint32_t *lists,
                  uint32_t *list_counts, const unsigned long long *summary, uint64_t capacity,
                  uint32_t *keys, uint32_t *values, void *stream);
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */

@@ -45,7 +45,7 @@ SIGNATURES = {
     "hs_blend_bwd": (_I, [_L, _I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I), _P]),
     "hs_blend_bwd_partials": (_I, [_L]),
     "hs_project_avatar_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                                   _P, _P, _P]),
+                                   _P, _P, _P, _P]),
     "hs_project_world_fwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_project_avatar_bwd": (_I, [_I, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_project_world_bwd": (_I, [_I, _L, _P, _P, _P, _P, _P]),
@@ -67,7 +67,7 @@ SIGNATURES = {
     "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P]),
     "hs_tile_count": (_I, [_I, _L, _I, _I, _P, _P, _P, _P]),
     "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint64, _P, _P, _P]),
+    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint64, _P, _P, _P]),
     "hs_bin_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_raster_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_adam": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _P]),

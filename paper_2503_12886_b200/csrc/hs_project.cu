@@ -235,7 +235,8 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     const float *__restrict__ cams, float *__restrict__ records, float *__restrict__ depth,
     uint32_t *__restrict__ counts, uint32_t *__restrict__ block_sums, uint32_t *__restrict__ depth_range,
     float *__restrict__ radius, float *__restrict__ zero_gsplat, float *__restrict__ zero_maxw,
-    float *__restrict__ zero_wsums, uint32_t *__restrict__ tile_counts, unsigned long long *err) {
+    float *__restrict__ zero_wsums, uint32_t *__restrict__ tile_counts, uint32_t *__restrict__ tile_rects,
+    unsigned long long *err) {
     extern __shared__ uint32_t hist[];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
@@ -268,8 +269,12 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
         Proj p;
         project_one(a.pw, a.qw, a.s, cams + b * kCam, p);
         if (!ok) p.valid = false;
-        TileRect rect;
+        TileRect rect{1, 0, 1, 0};
         cnt = write_record(p, a.op, a.col, W, H, records + i * kRec, &rect);
+        if (tile_rects)
+            tile_rects[i] = cnt ? (uint32_t)rect.ty0 | (uint32_t)rect.ty1 << 8 | (uint32_t)rect.tx0 << 16 |
+                                      (uint32_t)rect.tx1 << 24
+                                : 0x00010001u;
         depth[i] = p.zc;
         dz = p.zc;
         counts[i] = cnt;
@@ -506,8 +511,8 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
                           const float *base14, const int32_t *tri_index, const float *bary, const float *frames,
                           const float *cameras, float *records, float *depth, uint32_t *counts,
                           uint32_t *block_sums, uint32_t *depth_range, float *radius, float *zero_gsplat,
-                          float *zero_maxw, float *zero_wsums, uint32_t *tile_counts, unsigned long long *err,
-                          void *stream) {
+                          float *zero_maxw, float *zero_wsums, uint32_t *tile_counts, uint32_t *tile_rects,
+                          unsigned long long *err, void *stream) {
     if (B < 1 || N < 1 || width < 1 || height < 1 || width > 32767 || height > 32767) {
         set_error("hs_project_avatar_fwd: bad sizes B=%d N=%lld %dx%d", B, (long long)N, width, height);
         return HS_ERR_SHAPE;
@@ -518,10 +523,14 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
         set_error("hs_project_avatar_fwd: frame/tile bits exceed 31");
         return HS_ERR_SHAPE;
     }
+    if (tile_rects && (((width + kTile - 1) / kTile) > 256 || ((height + kTile - 1) / kTile) > 256)) {
+        set_error("hs_project_avatar_fwd: tile_rects needs at most 256 tiles per image axis");
+        return HS_ERR_SHAPE;
+    }
     const size_t smem = tile_counts && tiles <= kProjHistBins ? sizeof(uint32_t) * tiles : 0;
     project_avatar_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, smem, HS_CHECK_STREAM(stream)>>>(
         B, N, F, width, height, raw10, base14, tri_index, bary, frames, cameras, records, depth, counts,
-        block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, tile_counts, err);
+        block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, tile_counts, tile_rects, err);
     return check_launch("hs_project_avatar_fwd");
 }
 

@@ -55,17 +55,26 @@ struct CtaItems {
     bool live[kPer];
 };
 
+// rects (optional, hs_project_avatar_fwd's tile_rects): the item's tile rectangle packed
+// ty0 | ty1 << 8 | tx0 << 16 | tx1 << 24 (dead items: ty0 > ty1) -- one coalesced word
+// instead of the count and two words of the 48-byte record
 __device__ __forceinline__ void load_items(CtaItems &it, int64_t items, int64_t N, const float *__restrict__ records,
-                                           const uint32_t *__restrict__ counts) {
+                                           const uint32_t *__restrict__ counts, const uint32_t *__restrict__ rects) {
     const int64_t i0 = blockIdx.x * (int64_t)kTileItems;
     const int64_t b0 = i0 / N;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
         const int64_t i = i0 + threadIdx.x + j * kTileThreads;
         const bool in = i < items;
-        it.live[j] = in && counts[i] != 0u;
-        it.rows[j] = in ? __float_as_uint(records[i * kRec + 7]) : 0u;
-        it.cols[j] = in ? __float_as_uint(records[i * kRec + 8]) : 0u;
+        if (rects) {
+            const uint32_t r = in ? rects[i] : 0x00010001u;
+            it.rows[j] = r;
+            it.live[j] = (r & 0xFFu) <= ((r >> 8) & 0xFFu);
+        } else {
+            it.live[j] = in && counts[i] != 0u;
+            it.rows[j] = in ? __float_as_uint(records[i * kRec + 7]) : 0u;
+            it.cols[j] = in ? __float_as_uint(records[i * kRec + 8]) : 0u;
+        }
         int64_t b = b0, n = i - b0 * N;
         if (n >= N) {                            // past the CTA's first frame (rare)
             b = i / N;
@@ -76,7 +85,11 @@ __device__ __forceinline__ void load_items(CtaItems &it, int64_t items, int64_t 
     }
 }
 
-__device__ __forceinline__ TileBox item_box(const CtaItems &it, int j) {
+__device__ __forceinline__ TileBox item_box(const CtaItems &it, int j, bool packed) {
+    if (packed) {
+        const uint32_t r = it.rows[j];
+        return {(int)(r & 0xFFu), (int)((r >> 8) & 0xFFu), (int)((r >> 16) & 0xFFu), (int)(r >> 24)};
+    }
     return {unpack_lo(it.rows[j]) / kTile, unpack_hi(it.rows[j]) / kTile, unpack_lo(it.cols[j]) / kTile,
             unpack_hi(it.cols[j]) / kTile};
 }
@@ -89,14 +102,14 @@ __global__ void __launch_bounds__(kTileThreads) tile_count_kernel(int64_t items,
     const uint32_t b0 = (uint32_t)(blockIdx.x * (int64_t)kTileItems / N);
     const bool shared = tiles <= kTileSmemBins;
     CtaItems it;
-    load_items(it, items, N, records, counts);
+    load_items(it, items, N, records, counts, nullptr);
     if (shared)
         for (int t = threadIdx.x; t < tiles; t += kTileThreads) hist[t] = 0u;
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
         if (!it.live[j]) continue;
-        const TileBox bx = item_box(it, j);
+        const TileBox bx = item_box(it, j, false);
         uint32_t *dst = (shared && it.b[j] == b0) ? hist : tile_counts + ((size_t)it.b[j] << tile_bits);
         for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
             for (int tx = bx.tx0; tx <= bx.tx1; ++tx) atomicAdd(dst + ty * tiles_x + tx, 1u);
@@ -212,6 +225,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
 __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t items, int64_t N, int tiles_x, int tiles,
                                                                     int tile_bits, const float *__restrict__ records,
                                                                     const uint32_t *__restrict__ counts,
+                                                                    const uint32_t *__restrict__ rects,
                                                                     uint32_t *__restrict__ cursor, uint64_t capacity,
                                                                     const unsigned long long *__restrict__ summary,
                                                                     uint32_t *__restrict__ keys,
@@ -221,14 +235,15 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
     const uint32_t b0 = (uint32_t)(blockIdx.x * (int64_t)kTileItems / N);
     const bool shared = tiles <= kTileSmemBins;
     CtaItems it;
-    load_items(it, items, N, records, counts);
+    load_items(it, items, N, records, counts, rects);
+    const bool packed = rects != nullptr;
     if (shared) {
         for (int t = threadIdx.x; t < tiles; t += kTileThreads) hist[t] = 0u;
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
             if (!it.live[j] || it.b[j] != b0) continue;
-            const TileBox bx = item_box(it, j);
+            const TileBox bx = item_box(it, j, packed);
             for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
                 for (int tx = bx.tx0; tx <= bx.tx1; ++tx) atomicAdd(hist + ty * tiles_x + tx, 1u);
         }
@@ -243,7 +258,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
         if (!it.live[j]) continue;
-        const TileBox bx = item_box(it, j);
+        const TileBox bx = item_box(it, j, packed);
         const bool local = shared && it.b[j] == b0;
         const uint32_t hi = it.b[j] << tile_bits;
         for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
@@ -732,7 +747,7 @@ int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *
 }
 
 int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
-                 const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
+                 const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
                  uint32_t *list_counts, const unsigned long long *summary, uint64_t capacity,
                  uint32_t *keys, uint32_t *values, void *stream) {
     const int64_t items = (int64_t)B * N;
@@ -744,7 +759,7 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     const int tiles = tiles_x * tiles_y;
     const size_t tsmem = tiles <= kTileSmemBins ? sizeof(uint32_t) * tiles : 0;
     tile_scatter_kernel<<<grid_for(items, kTileItems), kTileThreads, tsmem, s>>>(
-        items, N, tiles_x, tiles, tile_bits, records, counts, cursor, capacity, summary, keys, values);
+        items, N, tiles_x, tiles, tile_bits, records, counts, tile_rects, cursor, capacity, summary, keys, values);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     static bool attr = false;

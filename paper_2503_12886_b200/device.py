@@ -259,6 +259,7 @@ class Binner:
         self._ordered = None
         self.tile_counts = None
         self.order_ready = False
+        self.rects = None
         self.mode = None             # how the last bin() built its lists
         self.longest = 0             # longest (frame, tile) list of the last tile-major binning
 
@@ -398,7 +399,18 @@ class Binner:
             self.list_counts = torch.empty(8, dtype=torch.int32, device=d)
         return self.tile_counts
 
-    def bin_tiles(self, B, N, width, height, records, depth, counts, err, after_scan=None, counted=False):
+    def tile_rects_buffer(self, B, N, width, height):
+        """Per-item packed tile rectangles (hs_project_avatar_fwd's tile_rects) for the
+        fill, or None when an image axis has more than 256 tiles."""
+        tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
+        if tiles_x > 256 or tiles_y > 256:
+            return None
+        if self.rects is None or self.rects.numel() < B * N:
+            self.rects = torch.empty(B * N, dtype=torch.int32, device=self.device)
+        return self.rects[:B * N]
+
+    def bin_tiles(self, B, N, width, height, records, depth, counts, err, after_scan=None, counted=False,
+                  rects=None):
         """Tile-major binning (hs_tile_count / hs_tile_scan / hs_tile_fill) with the
         step's single host read: the scatter and the per-list sorts are enqueued before
         the host waits, sized by the previous step's capacity; a step that needs more
@@ -425,7 +437,7 @@ class Binner:
             self._ensure(4 * B * N)         # a first guess; grown below when short
 
         def fill():
-            L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(depth), _p(ranges),
+            L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(rects), _p(depth), _p(ranges),
                    _p(self.cursor), _p(self.lists), _p(self.list_counts), _p(self.summary), self.cap,
                    _p(self.keys), _p(self.vals), s)
         fill()                              # first: the GPU reaches it right after the scan
@@ -657,17 +669,19 @@ class Trainer:
         F = frames.shape[-2] if frames.dim() == 3 else frames.numel() // (B * 22)
         # tile-major binning: the projection counts the tiles in the same pass
         tile_counts = self.binner.tile_count_buffer(B, self.W, self.H) if self.tile_binning else None
+        rects = self.binner.tile_rects_buffer(B, N, self.W, self.H) if self.tile_binning else None
         if self._rig_event is not None:
             torch.cuda.current_stream().wait_event(self._rig_event)
             self._rig_event = None
         self._call("project_fwd", "hs_project_avatar_fwd", B, N, F, self.W, self.H, _p(self.raw10), _p(av.base14),
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
                    _p(self.counts), _p(self.block_sums), _p(self.binner.reset_depth_range()), _p(self.radius),
-                   *(_p(z) for z in zero), _p(tile_counts), _p(self.err), s)
+                   *(_p(z) for z in zero), _p(tile_counts), _p(rects), _p(self.err), s)
         if self.tile_binning:
             m = self._mark("bin_tiles")
             total, code = self.binner.bin_tiles(B, N, self.W, self.H, self.records, self.depth, self.counts,
-                                                self.err, self._tile_order if order else None, counted=True)
+                                                self.err, self._tile_order if order else None, counted=True,
+                                                rects=rects)
             self._done(m)
             self.launches += launches_tiles(self.binner)
             self.err.fill_(-1)
