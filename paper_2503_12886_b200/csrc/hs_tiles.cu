@@ -538,13 +538,17 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB
 // then finds its merged position by binary search in the other runs (keys are unique),
 // and the equal-depth-field fix-up runs over the merged list.  Lists the fix-up does
 // not settle go to the 64-bit fallback.
-constexpr int kLongWarps = kWarpCap / kWarpShort;
+#ifndef HS_LONG_RUN
+#define HS_LONG_RUN 256
+#endif
+constexpr int kRun = HS_LONG_RUN;               // entries per warp-sorted run
+constexpr int kLongWarps = kWarpCap / kRun;
 
 __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
     uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
-    constexpr int E = kWarpShort / 32, IB = 10;
+    constexpr int E = kRun / 32, IB = 10;
     constexpr uint32_t kSlot = (1u << IB) - 1u;
     __shared__ unsigned long long s_k64[kWarpCap];
     __shared__ uint32_t s_run[kWarpCap], s_out[kWarpCap];
@@ -565,7 +569,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
         uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const uint32_t q = (uint32_t)(w * kWarpShort + e * 32 + lane);
+            const uint32_t q = (uint32_t)(w * kRun + e * 32 + lane);
             key[e] = 0xFFFFFFFFu;
             if (q < len) {
                 const uint32_t n = vals[start + q];
@@ -593,16 +597,16 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
         const int sh = max(0, (32 - __clz(dmax - dmin)) - (31 - IB));
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const uint32_t q = (uint32_t)(w * kWarpShort + e * 32 + lane);
+            const uint32_t q = (uint32_t)(w * kRun + e * 32 + lane);
             if (q < len) key[e] = (((key[e] - dmin) >> sh) << IB) | q;
         }
-        if (w * kWarpShort < (int)len) bitonic_u32<E>(key, lane);   // (runs past the end: padding)
+        if (w * kRun < (int)len) bitonic_u32<E>(key, lane);   // (runs past the end: padding)
 #pragma unroll
-        for (int e = 0; e < E; ++e) s_run[w * kWarpShort + e * 32 + lane] = key[e];
+        for (int e = 0; e < E; ++e) s_run[w * kRun + e * 32 + lane] = key[e];
         __syncthreads();
         // merged position: own rank + the keys below it in every other run (runs past
         // the list's end hold padding only and count nothing)
-        const int runs = (int)((len + kWarpShort - 1) / kWarpShort);
+        const int runs = (int)((len + kRun - 1) / kRun);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const uint32_t x = key[e];
@@ -610,13 +614,13 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
             uint32_t pos = (uint32_t)(e * 32 + lane);
             for (int v = 0; v < runs; ++v) {
                 if (v == w) continue;
-                // count of run v's keys below x: a branch-free search over its kWarpShort keys
-                int lo = v * kWarpShort;
+                // count of run v's keys below x: a branch-free search over its kRun keys
+                int lo = v * kRun;
 #pragma unroll
-                for (int step = kWarpShort / 2; step > 0; step >>= 1)
+                for (int step = kRun / 2; step > 0; step >>= 1)
                     if (s_run[lo + step - 1] < x) lo += step;
                 if (s_run[lo] < x) ++lo;
-                pos += (uint32_t)(lo - v * kWarpShort);
+                pos += (uint32_t)(lo - v * kRun);
             }
             if (pos < len) s_out[pos] = x;
         }
