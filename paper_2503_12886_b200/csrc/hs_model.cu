@@ -274,7 +274,7 @@ constexpr int kBMaxK = 32;
 #endif
 constexpr int kBBlocks = HS_BLEND_BLOCKS;   // persistent grid
 #ifndef HS_BLEND_KBB
-#define HS_BLEND_KBB 2
+#define HS_BLEND_KBB 1
 #endif
 constexpr int kKBB = HS_BLEND_KBB;  // delta loads in flight per lane (per chunk)
 #ifndef HS_BLEND_CPI
