@@ -37,7 +37,10 @@ def _p(t):
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    """The current CUDA stream as a raw handle for the C ABI.  (Straight from the torch
+    stream registry: torch.cuda.current_stream() re-resolves the device through
+    availability checks on every call, ~10 us of host time a step's worth of calls.)"""
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def require_cuda():
@@ -574,6 +577,7 @@ class Trainer:
         self._rig_frames = None
         self._rig_event = None
         self._order_event = None
+        self._cur = None                # the compute stream of the step in flight
         self._side = None               # side stream: rig || mlp_fwd + blend_fwd, loss || backward,
         self._side_events = []          # base/delta Adam || mlp_bwd
         self._last_frames = None
@@ -628,7 +632,7 @@ class Trainer:
         # the rig depends on theta only: it runs on a side stream concurrently with
         # mlp_fwd + blend_fwd, and project_fwd waits for it
         side = self._side_stream()
-        side.wait_stream(torch.cuda.current_stream())
+        side.wait_stream(self._cur)
         with torch.cuda.stream(side):
             m = self._mark("rig_frames")
             self.rig.frames(thetas, out=self._rig_frames, err=self.err)     # errors surface at the scan read
@@ -660,6 +664,7 @@ class Trainer:
     def _forward_project(self, thetas, frames, cameras, zero=(None, None, None), order=False):
         av = self.av
         N, K, B = av.N, av.K, self.B
+        self._cur = torch.cuda.current_stream()     # the step's compute stream (looked up once)
         s = _stream()
         frames = self._frames(thetas, frames)
         self._call("mlp_fwd", "hs_mlp_fwd", B, av.H, av.D, K, _p(av.mlp), _p(thetas), _p(self.cache), _p(self.psi),
@@ -671,7 +676,7 @@ class Trainer:
         tile_counts = self.binner.tile_count_buffer(B, self.W, self.H) if self.tile_binning else None
         rects = self.binner.tile_rects_buffer(B, N, self.W, self.H) if self.tile_binning else None
         if self._rig_event is not None:
-            torch.cuda.current_stream().wait_event(self._rig_event)
+            self._cur.wait_event(self._rig_event)
             self._rig_event = None
         self._call("project_fwd", "hs_project_avatar_fwd", B, N, F, self.W, self.H, _p(self.raw10), _p(av.base14),
                    _p(av.tri_index), _p(av.barycentric), _p(frames), _p(cameras), _p(self.records), _p(self.depth),
@@ -736,7 +741,7 @@ class Trainer:
         if ci:
             flags |= L.RASTER_MAXW_UNVISITED | L.RASTER_WSUMS
         if self._targets_ready is not None:     # step_from_host: targets arrive on the copy stream
-            torch.cuda.current_stream().wait_event(self._targets_ready)
+            self._cur.wait_event(self._targets_ready)
             self._targets_ready = None
         # d loss_b / d pred = sign / (H W 3) / B_global  (S/metrics.py:19-22, S/train.py:244)
         grad_scale = 1.0 / (self.H * self.W * 3.0) / self.global_batch
@@ -744,7 +749,7 @@ class Trainer:
             # forward + adjoint of every pixel block in one pass (hs_raster_train)
             kernels = 2                         # tile order + the fused raster
             if self._order_event is not None:   # built on the side stream (see _tile_order)
-                torch.cuda.current_stream().wait_event(self._order_event)
+                self._cur.wait_event(self._order_event)
                 if self.binner.mode == "tiles" and self.binner.order_ready:
                     flags |= L.RASTER_ORDER_READY
                     kernels = 1                 # (the order was counted in _tile_order)
@@ -756,7 +761,7 @@ class Trainer:
                 self._color_collectives()   # on the comm stream, overlapping the rest of the backward
             # the loss is only read after the step: reduce it on the side stream
             side = self._side_stream()
-            side.wait_stream(torch.cuda.current_stream())
+            side.wait_stream(self._cur)
             with torch.cuda.stream(side):
                 self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
                            _p(self.loss_out), _stream(), kernels=2)
@@ -789,7 +794,7 @@ class Trainer:
             # one rank: Adam on base + deltas (+ colour init) needs only blend_bwd's output;
             # it runs on the side stream while mlp_bwd runs
             side = self._side_stream()
-            side.wait_stream(torch.cuda.current_stream())
+            side.wait_stream(self._cur)
             with torch.cuda.stream(side):
                 m = self._mark("adam")
                 self._adam(0, 14 * N + 10 * K * N, ci_mode, _stream())
@@ -806,7 +811,7 @@ class Trainer:
             # init fused into the bucket holding the base colours
             m = self._mark("adam")
             for i, (lo, hi) in enumerate(buckets):
-                torch.cuda.current_stream().wait_event(self._bucket_events[i])
+                self._cur.wait_event(self._bucket_events[i])
                 self._adam(lo, hi, ci_mode, s)
             self._done(m)
         else:
@@ -814,7 +819,7 @@ class Trainer:
             self._adam(14 * N + 10 * K * N, av.size, 0, s)
             self._done(m)
         for ev in self._side_events:      # the step ends when the side-stream work has
-            torch.cuda.current_stream().wait_event(ev)
+            self._cur.wait_event(ev)
         self._side_events = []
         return self.loss_out
 
