@@ -313,8 +313,9 @@ def run_b200(args, cfg):
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()            # host wall clock over K steps back to back (each
-    for _ in range(args.steps):         # step ends with its loss read, i.e. a host sync)
-        tr.step_from_host(*hb, prefetch=hb)
+    for _ in range(args.steps):         # step returns after its loss read, a host sync on the
+        tr.step_from_host(*hb, prefetch=hb)     # loss copy; the backward finishes under the next)
+    torch.cuda.synchronize()            # the last step's backward and Adam are in the region
     e2e_ms = (time.perf_counter() - t0) * 1000.0
     t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:

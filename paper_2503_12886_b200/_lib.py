@@ -134,8 +134,18 @@ def check(rc: int, what: str = ""):
     raise RuntimeError(f"CUDA error: {msg}")
 
 
+_FNS = {}
+
+
 def call(name: str, *args):
-    check(getattr(load(), name)(*args), name)
+    """Call an entry point; raises on a non-zero status (the function objects are
+    cached: the per-call cost is on the training step's host path)."""
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(load(), name)
+    rc = fn(*args)
+    if rc != HS_OK:
+        check(rc, name)
 
 
 ATTR_NAMES = ("position", "rotation", "scale", "opacity", "color")

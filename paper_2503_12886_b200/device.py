@@ -578,6 +578,9 @@ class Trainer:
         self._rig_event = None
         self._order_event = None
         self._cur = None                # the compute stream of the step in flight
+        self._read_loss = False         # step_from_host: copy the losses to the host in the step
+        self._slot_free = [None, None]  # step_from_host: per input buffer set, its last step's end
+        self._loss_event = None
         self._side = None               # side stream: rig || mlp_fwd + blend_fwd, loss || backward,
         self._side_events = []          # base/delta Adam || mlp_bwd
         self._last_frames = None
@@ -765,9 +768,12 @@ class Trainer:
             with torch.cuda.stream(side):
                 self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
                            _p(self.loss_out), _stream(), kernels=2)
+                if self._read_loss:      # step_from_host: the D2H read right behind the reduction
+                    self._loss_host.copy_(self.loss_out, non_blocking=True)
                 loss_ev = torch.cuda.Event()
                 loss_ev.record(side)
             self._side_events.append(loss_ev)
+            self._loss_event = loss_ev
         else:
             self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
@@ -971,6 +977,9 @@ class Trainer:
         dt = {"thetas": np.float32, "targets": np.uint8, "frames": np.float32, "cameras": np.float32,
               "backgrounds": np.float32}
         dev = {}
+        if self._slot_free[slot] is not None:
+            # the step that last read this buffer set may still be in its backward
+            self._copy.wait_event(self._slot_free[slot])
         with torch.cuda.stream(self._copy):
             for k, v in arrays.items():
                 if v is None:
@@ -985,7 +994,9 @@ class Trainer:
 
     def step_from_host(self, thetas, targets, frames, cameras, backgrounds, prefetch=None):
         """End-to-end step through host buffers (numpy): H2D copies, the device step
-        and the D2H read of the losses.  Returns StepResult.
+        and the D2H read of the losses.  Returns StepResult once the losses are on the
+        host; the step's backward and Adam may still be running (stream-ordered before
+        anything the caller enqueues next; torch.cuda.synchronize() waits for them).
 
         The small inputs go first on the compute stream; the targets (the bulk of the
         bytes) go on a copy stream and only the forward raster waits for them, so
@@ -1028,14 +1039,29 @@ class Trainer:
                 ready = torch.cuda.Event()
                 ready.record(self._copy)
             self._targets_ready = ready
-        self.step(dev["thetas"], d, dev.get("frames"), dev["cameras"], dev["backgrounds"])
-        self._loss_host.copy_(self.loss_out, non_blocking=True)
+        # the losses are reduced and copied to the host on the side stream right after the
+        # forward raster; the host waits for that copy only, not for the backward and
+        # Adam, so it enqueues the next step while this one finishes
+        self._read_loss = self.fused_raster
+        try:
+            self.step(dev["thetas"], d, dev.get("frames"), dev["cameras"], dev["backgrounds"])
+        finally:
+            self._read_loss = False
+        loss_ready = self._loss_event if self.fused_raster else None
+        if loss_ready is None:
+            self._loss_host.copy_(self.loss_out, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(cur)                  # this buffer set is free once the step has finished
+        self._slot_free[slot] = done
         self._slot = 1 - slot
         if prefetch is not None:
             nxt = dict(zip(("thetas", "targets", "frames", "cameras", "backgrounds"), prefetch))
             ndev, nev = self._upload(self._slot, nxt)
             self._pending = (self._batch_key(nxt), ndev, nev, self._slot)
-        cur.synchronize()
+        if loss_ready is not None:
+            loss_ready.synchronize()
+        else:
+            cur.synchronize()
         lo = self._loss_host.numpy()
         B = self.B
         return StepResult(float(lo[2 * B]), lo[B:2 * B].copy(), lo[:B].copy(), self.last_total)
