@@ -184,5 +184,9 @@ def test_step_from_host_prefetch_pipeline():
     lb = [b.step_from_host(*x, prefetch=batches[i + 1] if i + 1 < len(batches) else None).loss
           for i, x in enumerate(batches)]
     np.testing.assert_allclose(lb, la, rtol=1e-6)
+    # step_from_host returns at the loss read; the backward and Adam finish later, and the
+    # prefetch into a buffer set waits for the step that last read it: same parameters
+    torch.cuda.synchronize()
+    assert torch.equal(a.av.params, b.av.params)
     a.close()
     b.close()
