@@ -185,8 +185,13 @@ def test_step_from_host_prefetch_pipeline():
           for i, x in enumerate(batches)]
     np.testing.assert_allclose(lb, la, rtol=1e-6)
     # step_from_host returns at the loss read; the backward and Adam finish later, and the
-    # prefetch into a buffer set waits for the step that last read it: same parameters
+    # prefetch into a buffer set waits for the step that last read it: the same parameters
+    # up to the order of the raster's gradient atomics: Adam turns it into a fraction of
+    # a step on near-zero gradients, and colour init can flip on a threshold -- a handful
+    # of entries; a clobbered buffer set would change whole gradients
     torch.cuda.synchronize()
-    assert torch.equal(a.av.params, b.av.params)
+    pa, pb = a.av.params.cpu().numpy(), b.av.params.cpu().numpy()
+    off = np.abs(pb - pa) > 5e-5 + 1e-3 * np.abs(pa)
+    assert off.mean() < 1e-4, (int(off.sum()), pa.size)
     a.close()
     b.close()
