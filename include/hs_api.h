@@ -197,8 +197,9 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   pixel bbox in tile_counts [B << tile_bits] (zero on entry; hs_tile_scan re-zeroes it).
  * hs_tile_scan: ranges [2 * (B << tile_bits)] (every entry written), scatter cursors
  *   [B << tile_bits], summary [4] = {key total, error word, depth range as hs_bin_scan,
- *   longest list}, and in lists [2 * (B << tile_bits)] / list_counts [8] the lists the
- *   fill sorts per CTA (the rest of lists is the fill's scratch).
+ *   longest list}, and in lists [2 * (B << tile_bits)] / list_counts [8 + ceil((B <<
+ *   tile_bits) / 1024)] the lists the fill sorts per CTA (the rest of lists is the fill's
+ *   scratch; the rest of list_counts the scan's).
  * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
  *   entry from the items' tile_rects (NULL: from the records' bboxes and counts); each
  *   list in (depth, Gaussian index) order -- the reference order.  Skipped on the device

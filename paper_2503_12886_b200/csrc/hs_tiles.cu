@@ -216,6 +216,103 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
     }
 }
 
+// Many-CTA variant (the training path's): CTA t (a ticket, so predecessors are
+// resident first) scans kScanSpan consecutive segments, publishes its total, adds the
+// totals of all CTAs before it (decoupled look-back on aggregates only) and writes its
+// ranges; list appends and the longest list go through global atomics, and the last
+// CTA to finish writes the summary.  list_counts [8 + CTAs] is zeroed by the caller
+// (hs_tile_scan) before the launch: [1] / [2] long / longer lists, [4] the fill's
+// fallback count, [5] ticket, [6] done, [7] longest, [8 + t] CTA t's flagged total.
+constexpr int kScanSpan = 1024;
+constexpr uint32_t kAggFlag = 1u << 31;
+
+__global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, uint32_t *__restrict__ tile_counts,
+                                                                    uint32_t *__restrict__ ranges,
+                                                                    uint32_t *__restrict__ cursor,
+                                                                    uint32_t *__restrict__ lists,
+                                                                    uint32_t *__restrict__ list_counts,
+                                                                    const unsigned long long *__restrict__ err,
+                                                                    const uint32_t *__restrict__ depth_range,
+                                                                    unsigned long long *__restrict__ summary) {
+    __shared__ uint32_t wsum[kScanSpan / 32];
+    __shared__ uint32_t s_tile, s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(list_counts + 5, 1u);
+    __syncthreads();
+    const uint32_t t = s_tile;
+    const int i = (int)t * kScanSpan + tid;
+    const uint32_t c = i < nseg ? tile_counts[i] : 0u;
+    uint32_t incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, c);
+    if (lane == 0 && mx) atomicMax(list_counts + 7, mx);
+    __syncthreads();
+    if (w == 0) {
+        uint32_t v = wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += x;
+        }
+        wsum[lane] = v;                              // inclusive over warps
+        if (lane == 31) {
+            __threadfence();
+            atomicExch(list_counts + 8 + t, kAggFlag | v);
+        }
+        // the totals of all CTAs before this one, 32 at a time
+        uint32_t pre = 0;
+        for (int j0 = 0; j0 < (int)t; j0 += 32) {
+            const int j = j0 + lane;
+            uint32_t st = 0u;
+            if (j < (int)t)
+                do {
+                    st = atomicAdd(list_counts + 8 + j, 0u);
+                } while (!(st & kAggFlag));
+            pre += st & ~kAggFlag;
+        }
+        pre = __reduce_add_sync(0xffffffffu, pre);
+        if (lane == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    const uint32_t run = s_prefix + (w > 0 ? wsum[w - 1] : 0u) + incl - c;
+    if (i < nseg) {
+        reinterpret_cast<uint2 *>(ranges)[i] = c ? make_uint2(run, run + c) : make_uint2(0u, 0u);
+        cursor[i] = run;
+        if (c) tile_counts[i] = 0u;                  // ready for the next step's count
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const bool big = q == 0 ? c > (uint32_t)kWarpShort && c <= (uint32_t)kWarpCap
+                                : c > (uint32_t)kWarpCap && c <= (uint32_t)kCtaCap;
+        const uint32_t m = __ballot_sync(0xffffffffu, big);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            uint32_t first = 0;
+            if (lane == leader) first = atomicAdd(list_counts + 1 + q, (uint32_t)__popc(m));
+            first = __shfl_sync(0xffffffffu, first, leader);
+            const uint32_t r = first + __popc(m & ((1u << lane) - 1u));
+            if (big) lists[q == 0 ? r : nseg - 1 - r] = (uint32_t)i;
+        }
+    }
+    // the last CTA to finish: the summary (total = the last segment's end)
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(list_counts + 6, 1u) == gridDim.x - 1) {
+            __threadfence();
+            uint32_t total = 0;
+            for (int j = 0; j < (int)gridDim.x; ++j) total += atomicAdd(list_counts + 8 + j, 0u) & ~kAggFlag;
+            summary[0] = total;
+            summary[1] = err ? *err : HS_NO_ERROR;
+            summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
+            summary[3] = atomicAdd(list_counts + 7, 0u);
+        }
+    }
+}
+
 // ----------------------------------------------------------------- scatter
 
 // Same CTA partition as the count: the shared histogram of the CTA's first frame
@@ -745,8 +842,19 @@ int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *
         set_error("hs_tile_scan: bad segment count");
         return HS_ERR_SHAPE;
     }
-    tile_scan_kernel<<<1, 1024, 0, HS_CHECK_STREAM(stream)>>>((int)nseg, tile_counts, ranges, cursor, lists,
-                                                              list_counts, err, depth_range, summary);
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+#ifndef HS_SCAN_MULTI
+#define HS_SCAN_MULTI 1
+#endif
+    if (HS_SCAN_MULTI && nseg > kScanSpan) {
+        const int ctas = (int)((nseg + kScanSpan - 1) / kScanSpan);
+        cudaMemsetAsync(list_counts, 0, sizeof(uint32_t) * (8 + ctas), s);
+        tile_scan_multi_kernel<<<ctas, kScanSpan, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts,
+                                                          err, depth_range, summary);
+    } else {
+        tile_scan_kernel<<<1, 1024, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts, err,
+                                            depth_range, summary);
+    }
     return check_launch("hs_tile_scan");
 }
 

@@ -399,7 +399,7 @@ class Binner:
             self.tile_counts = torch.zeros(nseg, dtype=torch.int32, device=d)
             self.cursor = torch.empty(nseg, dtype=torch.int32, device=d)
             self.lists = torch.empty(2 * nseg, dtype=torch.int32, device=d)
-            self.list_counts = torch.empty(8, dtype=torch.int32, device=d)
+            self.list_counts = torch.zeros(8 + (nseg + 1023) // 1024, dtype=torch.int32, device=d)
         return self.tile_counts
 
     def tile_rects_buffer(self, B, N, width, height):
