@@ -44,6 +44,9 @@ namespace hs {
 #ifndef HS_RASTER_EXACT_CULL
 #define HS_RASTER_EXACT_CULL 1       // cull blocks with the exact ellipse-rectangle distance
 #endif
+#ifndef HS_RASTER_DIRECT
+#define HS_RASTER_DIRECT 4           // adjoint: up to this many contributing lanes add directly
+#endif
 
 constexpr int kPX = HS_RASTER_PX;
 constexpr int kCW = HS_RASTER_CTA_WARPS;
@@ -702,7 +705,19 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
                 }
             }
 #endif
-            if (__any_sync(kFull, contrib)) {
+            const uint32_t cmask = __ballot_sync(kFull, contrib);
+            if (HS_RASTER_DIRECT && cmask && __popc(cmask) <= HS_RASTER_DIRECT) {
+                // few contributing pixels: their lanes add directly (9 atomics each) instead
+                // of the 9-value warp reduce-scatter
+                if (contrib) {
+                    float *gp = a.g_splat + (uint64_t)(__float_as_uint(p1.w)) * kGS;
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        const float sc = k < 2 ? -0.5f * kMeanScale : k == 3 ? -1.0f : k < 5 ? -0.5f : 1.0f;
+                        atomicAdd(gp + k, gv[k] * sc);
+                    }
+                }
+            } else if (cmask) {
                 int vi;
                 bool issue;
                 const float s = reduce_scatter(gv, lane, vi, issue);
