@@ -205,7 +205,10 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   list in (depth, Gaussian index) order -- the reference order.  Skipped on the device
  *   when summary[0] > capacity (grow the buffers, reset the cursors to the range starts
  *   and call again).  Lists longer than hs_tile_sort_cap() are scattered but NOT sorted:
- *   when summary[3] exceeds the cap, bin that step with the two-level sort instead. */
+ *   when summary[3] exceeds the cap, bin that step with the two-level sort instead.
+ *   The short lists sort on a library-internal stream (created on the device current at
+ *   the first call) that the caller's stream joins before returning work to it: calls
+ *   are stream-ordered like any other, but not thread-safe against each other. */
 int hs_tile_sort_cap(void);
 int hs_tile_count(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                   uint32_t *tile_counts, void *stream);
