@@ -590,8 +590,11 @@ __device__ __forceinline__ void sort_list(const float *__restrict__ depth, int64
 #ifndef HS_LONG_SORT_MINB
 #define HS_LONG_SORT_MINB 4
 #endif
+#ifndef HS_SHORT_SORT_MINB
+#define HS_SHORT_SORT_MINB 8
+#endif
 template <bool kLong>
-__global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB : 8) tile_sort_warp_kernel(
+__global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB : HS_SHORT_SORT_MINB) tile_sort_warp_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
     uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
