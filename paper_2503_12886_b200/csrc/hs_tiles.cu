@@ -898,7 +898,10 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     tile_sort_warp_kernel<false><<<(unsigned)sms * 16, 32 * kWarpSortWarps, 0, side>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     cudaEventRecord(shorts_done, side);
-    tile_sort_long_kernel<<<(unsigned)sms * 8, 32 * kLongWarps, 0, s>>>(
+#ifndef HS_LONG_SORT_CTAS_PER_SM
+#define HS_LONG_SORT_CTAS_PER_SM 16
+#endif
+    tile_sort_long_kernel<<<(unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     cudaStreamWaitEvent(s, shorts_done, 0);
     tile_sort_wide_kernel<<<(unsigned)sms * 4, 32 * kWarpSortWarps, 0, s>>>(
