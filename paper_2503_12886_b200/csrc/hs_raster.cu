@@ -45,7 +45,7 @@ namespace hs {
 #define HS_RASTER_EXACT_CULL 1       // cull blocks with the exact ellipse-rectangle distance
 #endif
 #ifndef HS_RASTER_DIRECT
-#define HS_RASTER_DIRECT 4           // adjoint: up to this many contributing lanes add directly
+#define HS_RASTER_DIRECT 5           // adjoint: up to this many contributing lanes add directly
 #endif
 
 constexpr int kPX = HS_RASTER_PX;
