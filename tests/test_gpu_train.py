@@ -250,3 +250,41 @@ def test_fused_raster_matches_separate_kernels():
         ga, gb = a.g_splat.cpu().numpy(), b.g_splat.cpu().numpy()
         assert np.linalg.norm(ga - gb) <= 1e-5 * np.linalg.norm(gb)
     assert torch.equal(a.visited, b.visited)
+
+
+@pytest.mark.parametrize("crowded", [False, True])
+def test_tile_binning_matches_two_level(crowded):
+    """The training step with tile-major binning against the two-level global sort: the
+    same lists, so the first step's losses are identical and the gradients equal up to
+    the order of the float atomics.  crowded: Gaussians inflated until some (frame,
+    tile) list exceeds hs_tile_sort_cap(), so the tile-major binner takes its
+    two-level fallback inside the step."""
+    from paper_2503_12886_b200 import synth
+    from paper_2503_12886_b200.device import AvatarParams, Trainer, tile_sort_cap
+    uv, size = (140, 64) if crowded else (64, 192)
+    wl = synth.make_workload(uv, 4, size, distinct_frames=4)
+    av = wl.avatar
+    base = {a: np.array(av.base[a], copy=True) for a in ATTRS}
+    if crowded:
+        base["scale"] = base["scale"] + 3.0
+    mk = lambda: AvatarParams.from_host(O.GSet(*(base[a] for a in ATTRS)), av.deltas, av.mlp, av.tri_index,
+                                        av.barycentric)
+    th = torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda()
+    tg = torch.from_numpy(wl.targets).cuda()
+    fr = torch.from_numpy(wl.frames).cuda()
+    cams = torch.from_numpy(np.tile(wl.camera.packed(), (4, 1))).cuda()
+    bg = torch.from_numpy(np.asarray(wl.backgrounds, np.float32)).cuda()
+    a, b = Trainer(mk(), size, size, 4), Trainer(mk(), size, size, 4)
+    b.tile_binning = False
+    for step in range(2):
+        la = a.step(th, tg, fr, cams, bg).clone()
+        lb = b.step(th, tg, fr, cams, bg).clone()
+        assert a.binner.mode == ("two_level" if crowded else "tiles"), a.binner.longest
+        if crowded:
+            assert a.binner.longest > tile_sort_cap()
+        if step == 0:
+            assert torch.equal(la, lb)
+            ga, gb = a.g_splat.cpu().numpy(), b.g_splat.cpu().numpy()
+            assert np.linalg.norm(ga - gb) <= 1e-5 * np.linalg.norm(gb)
+        else:
+            assert torch.allclose(la, lb, rtol=1e-4, atol=1e-7)
