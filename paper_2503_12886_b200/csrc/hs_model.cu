@@ -739,7 +739,7 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
 #ifndef HS_BLEND_BC
-#define HS_BLEND_BC 4
+#define HS_BLEND_BC 8
 #endif
     if (vec) {
         // grid.y splits the frames into chunks of HS_BLEND_BC: few accumulators per
