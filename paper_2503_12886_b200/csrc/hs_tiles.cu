@@ -37,7 +37,10 @@ constexpr int kWarpSortWarps = 4;     // warps per CTA of the warp-level sort
 // into a shared-memory histogram over that frame's tiles (flushed with one global
 // atomic per touched tile); items past a frame boundary, or every item when the
 // frame has too many tiles for shared memory, add to the global counters directly.
-constexpr int kTileItems = 1024;
+#ifndef HS_TILE_ITEMS
+#define HS_TILE_ITEMS 512
+#endif
+constexpr int kTileItems = HS_TILE_ITEMS;
 constexpr int kTileThreads = 256;
 constexpr int kTileSmemBins = 12288;   // tiles per frame the shared histogram holds (48 KB)
 
