@@ -898,7 +898,10 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     }
     cudaEventRecord(scattered, s);
     cudaStreamWaitEvent(side, scattered, 0);
-    tile_sort_warp_kernel<false><<<(unsigned)sms * 16, 32 * kWarpSortWarps, 0, side>>>(
+#ifndef HS_SHORT_SORT_CTAS_PER_SM
+#define HS_SHORT_SORT_CTAS_PER_SM 16
+#endif
+    tile_sort_warp_kernel<false><<<(unsigned)sms * HS_SHORT_SORT_CTAS_PER_SM, 32 * kWarpSortWarps, 0, side>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     cudaEventRecord(shorts_done, side);
 #ifndef HS_LONG_SORT_CTAS_PER_SM
