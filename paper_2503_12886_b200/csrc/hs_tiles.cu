@@ -4,14 +4,20 @@
 // a stable depth argsort per frame, then the splats covering each tile in that
 // order) are built tile-first instead of by a global key sort:
 //
-//   hs_tile_count  every (frame, splat) adds one to each tile of its pixel bbox
-//   hs_tile_scan   one CTA: exclusive scan of the counts -> ranges + scatter cursors
-//                  and the step's single device->host summary (key total, error word,
-//                  depth range, longest list)
-//   hs_tile_fill   scatter (an atomic cursor per tile, arrival order), then each list
-//                  sorted by the 64-bit key (depth bits << 32 | Gaussian index): a
-//                  register bitonic sort per warp up to 32 entries, a shared-memory
-//                  bitonic sort per warp up to kWarpCap, per CTA up to kCtaCap
+//   counts         every (frame, splat) adds one to each tile of its pixel bbox -- in
+//                  the projection kernel (hs_project_avatar_fwd's tile_counts, which
+//                  also packs each item's tile rectangle) or hs_tile_count
+//   hs_tile_scan   exclusive scan of the counts -> ranges + scatter cursors (1,024 lists
+//                  per CTA, decoupled look-back), the lists longer than kWarpShort, and
+//                  the step's single device->host summary (key total, error word, depth
+//                  range, longest list)
+//   hs_tile_fill   scatter (per-CTA slot blocks, arrival order inside a list), then each
+//                  list sorted on chip by (depth bits, Gaussian index): warps sort lists
+//                  up to kWarpShort entries in registers (32-bit keys: depth offset |
+//                  slot, ties settled on the full keys), CTAs sort lists up to kWarpCap
+//                  (register runs merged by rank) -- concurrently on two streams -- and
+//                  up to kCtaCap (shared-memory bitonic); lists the 32-bit path cannot
+//                  settle take a 64-bit warp sort
 //
 // Sorting each list by (depth bits, index) is exactly the reference's order: positive
 // float depths compare like their bit patterns and the stable argsort breaks ties by
@@ -24,8 +30,8 @@
 
 namespace hs {
 
-constexpr int kWarpShort = 256;       // warp-sorted lists up to this length go last
-constexpr int kWarpCap = 1024;        // longest list one warp sorts in shared memory
+constexpr int kWarpShort = 256;       // longest list one warp sorts (in registers)
+constexpr int kWarpCap = 1024;        // longest list one CTA sorts as merged register runs
 constexpr int kCtaCap = 8192;         // longest list one CTA sorts in shared memory
 constexpr int kCtaSortThreads = 512;
 constexpr int kWarpSortWarps = 4;     // warps per CTA of the warp-level sort
