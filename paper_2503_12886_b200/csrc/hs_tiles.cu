@@ -594,21 +594,16 @@ __device__ __forceinline__ void sort_list(const float *__restrict__ depth, int64
     __syncwarp();
 }
 
-// One warp per list: kLong = class 1 (kWarpShort+1..kWarpCap entries, from the back
-// of `lists`), else class 0 (2..kWarpShort).
-#ifndef HS_LONG_SORT_MINB
-#define HS_LONG_SORT_MINB 4
-#endif
+// One warp per list of 2..kWarpShort entries, the warps striding over all segments.
 #ifndef HS_SHORT_SORT_MINB
 #define HS_SHORT_SORT_MINB 8
 #endif
-template <bool kLong>
-__global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB : HS_SHORT_SORT_MINB) tile_sort_warp_kernel(
+__global__ void __launch_bounds__(32 * kWarpSortWarps, HS_SHORT_SORT_MINB) tile_sort_warp_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
     uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
-    __shared__ unsigned long long s_k64_all[kWarpSortWarps][kLong ? kWarpCap : kWarpShort];
-    __shared__ uint32_t s_q_all[kWarpSortWarps][kLong ? kWarpCap : kWarpShort];
+    __shared__ unsigned long long s_k64_all[kWarpSortWarps][kWarpShort];
+    __shared__ uint32_t s_q_all[kWarpSortWarps][kWarpShort];
     uint32_t *wide = lists + nseg;
     if (summary[0] > capacity) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -617,27 +612,22 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, kLong ? HS_LONG_SORT_MINB
     // warp g takes segments g + j * stride; 32 candidates are read at once (one per lane)
     const uint32_t stride = gridDim.x * kWarpSortWarps;
     for (uint32_t base = blockIdx.x * kWarpSortWarps + w; base < (uint32_t)nseg; base += 32 * stride) {
-      const uint32_t seg_l = base + lane * stride;
-      const uint2 rg_l = seg_l < (uint32_t)nseg ? reinterpret_cast<const uint2 *>(ranges)[seg_l] : make_uint2(0u, 0u);
-      const uint32_t len_l = rg_l.y - rg_l.x;
-      uint32_t pick = __ballot_sync(0xffffffffu, kLong ? (len_l > (uint32_t)kWarpShort && len_l <= (uint32_t)kWarpCap)
-                                                        : (len_l >= 2u && len_l <= (uint32_t)kWarpShort));
-      while (pick) {
-        const int b = __ffs(pick) - 1;
-        pick &= pick - 1u;
-        const uint32_t seg = base + b * stride;
-        const uint32_t start = __shfl_sync(0xffffffffu, rg_l.x, b), len = __shfl_sync(0xffffffffu, len_l, b);
-        const int64_t fb = (int64_t)(seg >> tile_bits) * N;
-        if (kLong) {
-            if (len <= 512u) sort_list<16>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
-            else sort_list<32>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
-        } else {
-            if (len <= 32u) sort_list<1>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
-            else if (len <= 64u) sort_list<2>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
-            else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
-            else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, list_counts + 4);
+        const uint32_t seg_l = base + lane * stride;
+        const uint2 rg_l = seg_l < (uint32_t)nseg ? reinterpret_cast<const uint2 *>(ranges)[seg_l] : make_uint2(0u, 0u);
+        const uint32_t len_l = rg_l.y - rg_l.x;
+        uint32_t pick = __ballot_sync(0xffffffffu, len_l >= 2u && len_l <= (uint32_t)kWarpShort);
+        while (pick) {
+            const int b = __ffs(pick) - 1;
+            pick &= pick - 1u;
+            const uint32_t seg = base + b * stride;
+            const uint32_t start = __shfl_sync(0xffffffffu, rg_l.x, b), len = __shfl_sync(0xffffffffu, len_l, b);
+            const int64_t fb = (int64_t)(seg >> tile_bits) * N;
+            uint32_t *nw = list_counts + 4;
+            if (len <= 32u) sort_list<1>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
+            else if (len <= 64u) sort_list<2>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
+            else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
+            else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
         }
-      }
     }
 }
 
@@ -907,7 +897,7 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
 #ifndef HS_SHORT_SORT_CTAS_PER_SM
 #define HS_SHORT_SORT_CTAS_PER_SM 16
 #endif
-    tile_sort_warp_kernel<false><<<(unsigned)sms * HS_SHORT_SORT_CTAS_PER_SM, 32 * kWarpSortWarps, 0, side>>>(
+    tile_sort_warp_kernel<<<(unsigned)sms * HS_SHORT_SORT_CTAS_PER_SM, 32 * kWarpSortWarps, 0, side>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     cudaEventRecord(shorts_done, side);
 #ifndef HS_LONG_SORT_CTAS_PER_SM
