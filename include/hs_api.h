@@ -235,8 +235,8 @@ enum {
     HS_RASTER_MAXW_UNVISITED = 8,/* same, only for Gaussians with visited[n] == 0 */
     HS_RASTER_WSUMS = 16,        /* colour-init sums (sum w*target, sum w) for the same set */
     HS_RASTER_WSUMS_IMAGE = 32,  /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
-    HS_RASTER_ORDER_READY = 64   /* hs_raster_train: the tile order hs_raster_tile_order built for these
-                                    ranges is in place (the call then skips building it) */
+    HS_RASTER_ORDER_READY = 64   /* hs_raster_train / hs_raster_fwd: the tile order hs_raster_tile_order
+                                    built for these ranges is in place (the call skips building it) */
 };
 /* The persistent raster's longest-list-first tile order for these ranges; lets a caller
  * build it off the critical path (e.g. on a side stream while the lists are sorted) and

@@ -865,7 +865,7 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    launch_tile_order(B, nblk, tile_bits, ranges, s);
+    if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, s);
     if (loss && img) launch_fwd_ci<true, true>(ci, grid, nblk, s, a);
     else if (loss) launch_fwd_ci<true, false>(ci, grid, nblk, s, a);
     else if (img) launch_fwd_ci<false, true>(ci, grid, nblk, s, a);

@@ -914,10 +914,16 @@ class Trainer:
         returns images (B, H, W, 3) fp32 = C + T * background."""
         av = self.av
         cameras = self._cameras(cameras)
-        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras)
+        self._order_event = None
+        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, order=True)
         if out is None:
             out = torch.empty(self.B, self.H, self.W, 3, dtype=torch.float32, device=av.device)
-        self._call("raster_fwd", "hs_raster_fwd", self.B, av.N, self.W, self.H, L.RASTER_IMAGE, _p(self.records),
+        flags = L.RASTER_IMAGE
+        if self._order_event is not None:       # built on the side stream (see _tile_order)
+            self._cur.wait_event(self._order_event)
+            if self.binner.mode == "tiles" and self.binner.order_ready:
+                flags |= L.RASTER_ORDER_READY
+        self._call("raster_fwd", "hs_raster_fwd", self.B, av.N, self.W, self.H, flags, _p(self.records),
                    _p(vals), _p(ranges), tile_bits, _p(backgrounds), None, None, None, _p(self.pix_T),
                    _p(self.pix_state), _p(out), None, None, None, _stream())
         return out
