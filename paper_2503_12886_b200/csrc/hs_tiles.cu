@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                                                                  uint32_t *__restrict__ cursor,
                                                                  uint32_t *__restrict__ lists,
                                                                  uint32_t *__restrict__ list_counts,
-                                                                 const unsigned long long *__restrict__ err,
+                                                                 unsigned long long *__restrict__ err,
                                                                  const uint32_t *__restrict__ depth_range,
                                                                  unsigned long long *__restrict__ summary) {
     __shared__ uint32_t wt[kScanPer][kScanThreads / 32];   // per k: inclusive scan over warps
@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
     if (tid == 0) {
         summary[0] = carry;
         summary[1] = err ? *err : HS_NO_ERROR;
+        if (err) *err = HS_NO_ERROR;                 // read once per step: reset for the next
         summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
         summary[3] = s_max;
     }
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, ui
                                                                     uint32_t *__restrict__ cursor,
                                                                     uint32_t *__restrict__ lists,
                                                                     uint32_t *__restrict__ list_counts,
-                                                                    const unsigned long long *__restrict__ err,
+                                                                    unsigned long long *__restrict__ err,
                                                                     const uint32_t *__restrict__ depth_range,
                                                                     unsigned long long *__restrict__ summary) {
     __shared__ uint32_t wsum[kScanSpan / 32];
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, ui
             for (int j = 0; j < (int)gridDim.x; ++j) total += atomicAdd(list_counts + 8 + j, 0u) & ~kAggFlag;
             summary[0] = total;
             summary[1] = err ? *err : HS_NO_ERROR;
+            if (err) *err = HS_NO_ERROR;             // read once per step: reset for the next
             summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
             summary[3] = atomicAdd(list_counts + 7, 0u);
         }
@@ -835,7 +837,7 @@ int hs_tile_count(int B, int64_t N, int width, int height, const float *records,
 }
 
 int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,
-                 uint32_t *lists, uint32_t *list_counts, const unsigned long long *err,
+                 uint32_t *lists, uint32_t *list_counts, unsigned long long *err,
                  const uint32_t *depth_range, unsigned long long *summary, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));

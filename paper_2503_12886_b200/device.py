@@ -692,7 +692,7 @@ class Trainer:
                                                 rects=rects)
             self._done(m)
             self.launches += launches_tiles(self.binner)
-            self.err.fill_(-1)
+            # (the scan reset the error word after reading it into the summary)
             L.raise_device_error(code, self.frame_offset)
             self.last_total = total
             self._last_frames = frames
