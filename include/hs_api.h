@@ -197,7 +197,8 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   pixel bbox in tile_counts [B << tile_bits] (zero on entry; hs_tile_scan re-zeroes it).
  * hs_tile_scan: ranges [2 * (B << tile_bits)] (every entry written), scatter cursors
  *   [B << tile_bits], summary [4] = {key total, error word (err is reset to HS_NO_ERROR
- *   after the read), depth range as hs_bin_scan, longest list}, and in lists [2 * (B << tile_bits)] / list_counts [8 + ceil((B <<
+ *   after the read), depth range as hs_bin_scan (depth_range is reset to {~0, 0} after the
+ *   read unless the longest list exceeds hs_tile_sort_cap()), longest list}, and in lists [2 * (B << tile_bits)] / list_counts [8 + ceil((B <<
  *   tile_bits) / 1024)] the lists the fill sorts per CTA (the rest of lists is the fill's
  *   scratch; the rest of list_counts the scan's).
  * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
@@ -214,7 +215,7 @@ int hs_tile_count(int B, int64_t N, int width, int height, const float *records,
                   uint32_t *tile_counts, void *stream);
 int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,
                  uint32_t *lists, uint32_t *list_counts, unsigned long long *err,
-                 const uint32_t *depth_range, unsigned long long *summary, void *stream);
+                 uint32_t *depth_range, unsigned long long *summary, void *stream);
 int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                  const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor,
                  uint32_t *lists,

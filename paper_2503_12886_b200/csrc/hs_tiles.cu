@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                                                                  uint32_t *__restrict__ lists,
                                                                  uint32_t *__restrict__ list_counts,
                                                                  unsigned long long *__restrict__ err,
-                                                                 const uint32_t *__restrict__ depth_range,
+                                                                 uint32_t *__restrict__ depth_range,
                                                                  unsigned long long *__restrict__ summary) {
     __shared__ uint32_t wt[kScanPer][kScanThreads / 32];   // per k: inclusive scan over warps
     __shared__ uint32_t s_max, s_big[2];
@@ -223,6 +223,10 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
         if (err) *err = HS_NO_ERROR;                 // read once per step: reset for the next
         summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
         summary[3] = s_max;
+        if (depth_range && s_max <= (uint32_t)kCtaCap) {   // (a fallback step still needs it)
+            depth_range[0] = 0xFFFFFFFFu;
+            depth_range[1] = 0u;
+        }
     }
 }
 
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, ui
                                                                     uint32_t *__restrict__ lists,
                                                                     uint32_t *__restrict__ list_counts,
                                                                     unsigned long long *__restrict__ err,
-                                                                    const uint32_t *__restrict__ depth_range,
+                                                                    uint32_t *__restrict__ depth_range,
                                                                     unsigned long long *__restrict__ summary) {
     __shared__ uint32_t wsum[kScanSpan / 32];
     __shared__ uint32_t s_tile, s_prefix;
@@ -319,7 +323,12 @@ __global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, ui
             summary[1] = err ? *err : HS_NO_ERROR;
             if (err) *err = HS_NO_ERROR;             // read once per step: reset for the next
             summary[2] = depth_range ? ((unsigned long long)depth_range[1] << 32) | depth_range[0] : 0xFFFFFFFFull;
-            summary[3] = atomicAdd(list_counts + 7, 0u);
+            const uint32_t longest = atomicAdd(list_counts + 7, 0u);
+            summary[3] = longest;
+            if (depth_range && longest <= (uint32_t)kCtaCap) {   // (a fallback step still needs it)
+                depth_range[0] = 0xFFFFFFFFu;
+                depth_range[1] = 0u;
+            }
         }
     }
 }
@@ -838,7 +847,7 @@ int hs_tile_count(int B, int64_t N, int width, int height, const float *records,
 
 int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,
                  uint32_t *lists, uint32_t *list_counts, unsigned long long *err,
-                 const uint32_t *depth_range, unsigned long long *summary, void *stream) {
+                 uint32_t *depth_range, unsigned long long *summary, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
     const int64_t nseg = (int64_t)B << tile_bits;

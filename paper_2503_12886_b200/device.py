@@ -254,6 +254,7 @@ class Binner:
         self.summary = torch.empty(4, dtype=torch.int64, device=device)
         self.depth_range = torch.empty(2, dtype=torch.int32, device=device)
         self._depth_range_init = None
+        self._depth_range_clean = False     # hs_tile_scan reset it (no fallback that step)
         self.depth_bits = (0, 0)
         self.passes = 0
         self.ranges = None
@@ -282,7 +283,11 @@ class Binner:
     def reset_depth_range(self):
         """{0xFFFFFFFF, 0}: the projection atomically narrows it to the depths that emit keys.
         (A device-to-device copy: element assignment from a host scalar would be a
-        pageable host->device copy, which blocks the host until the stream drains.)"""
+        pageable host->device copy, which blocks the host until the stream drains.)  After a
+        tile-major binning that needed no fallback, hs_tile_scan has already reset it."""
+        if self._depth_range_clean:
+            self._depth_range_clean = False
+            return self.depth_range
         if self._depth_range_init is None:
             self._depth_range_init = torch.tensor([-1, 0], dtype=torch.int32, device=self.device)
         self.depth_range.copy_(self._depth_range_init)
@@ -458,6 +463,7 @@ class Binner:
             self._ensure(total)
             self.cursor[:nseg].copy_(ranges.view(-1, 2)[:, 0])
             fill()
+        self._depth_range_clean = self.longest <= tile_sort_cap()
         if self.longest > tile_sort_cap():
             # a list too long to sort in shared memory: the global two-level sort
             # (whose ranges replace the ones the tile order was built from)
