@@ -211,6 +211,13 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   the first call) that the caller's stream joins before returning work to it: calls
  *   are stream-ordered like any other, but not thread-safe against each other. */
 int hs_tile_sort_cap(void);
+/* Lists of hs_tile_cta_sort_min()..hs_tile_sort_cap() entries are sorted by
+ * hs_tile_fill_longest (one CTA each), which the caller enqueues after hs_tile_fill when
+ * the summary's longest list is in that range (arguments as hs_tile_fill). */
+int hs_tile_cta_sort_min(void);
+int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *depth, const uint32_t *ranges,
+                         uint32_t *lists, uint32_t *list_counts, const unsigned long long *summary,
+                         uint64_t capacity, uint32_t *values, void *stream);
 int hs_tile_count(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                   uint32_t *tile_counts, void *stream);
 int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,

@@ -64,6 +64,8 @@ SIGNATURES = {
     "hs_sort_pairs32": (_I, [_L, ctypes.c_uint32, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges32": (_I, [_L, _P, _P, _P]),
     "hs_tile_sort_cap": (_I, []),
+    "hs_tile_cta_sort_min": (_I, []),
+    "hs_tile_fill_longest": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, ctypes.c_uint64, _P, _P]),
     "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P]),
     "hs_tile_count": (_I, [_I, _L, _I, _I, _P, _P, _P, _P]),
     "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -827,6 +827,7 @@ using namespace hs;
 extern "C" {
 
 int hs_tile_sort_cap(void) { return kCtaCap; }
+int hs_tile_cta_sort_min(void) { return kWarpCap + 1; }
 
 int hs_tile_count(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                   uint32_t *tile_counts, void *stream) {
@@ -887,12 +888,6 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
         items, N, tiles_x, tiles, tile_bits, records, counts, tile_rects, cursor, capacity, summary, keys, values);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    static bool attr = false;
-    const int csmem = kCtaCap * (int)sizeof(unsigned long long);
-    if (!attr) {
-        cudaFuncSetAttribute(tile_sort_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
-        attr = true;
-    }
     // the long lists first (fewer, longer: their tail overlaps nothing otherwise)
     // the short lists sort on a library-internal stream alongside the long ones (each
     // kernel leaves SMs idle in its tail); the caller's stream waits for both
@@ -919,9 +914,28 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     cudaStreamWaitEvent(s, shorts_done, 0);
     tile_sort_wide_kernel<<<(unsigned)sms * 4, 32 * kWarpSortWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
+    return check_launch("hs_tile_fill");
+}
+
+int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *depth, const uint32_t *ranges,
+                         uint32_t *lists, uint32_t *list_counts, const unsigned long long *summary,
+                         uint64_t capacity, uint32_t *values, void *stream) {
+    if ((int64_t)B * N <= 0) return HS_OK;
+    cudaStream_t s = HS_CHECK_STREAM(stream);
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
+    const int nseg = B << tile_bits;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    static bool attr = false;
+    const int csmem = kCtaCap * (int)sizeof(unsigned long long);
+    if (!attr) {
+        cudaFuncSetAttribute(tile_sort_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
+        attr = true;
+    }
     tile_sort_cta_kernel<<<(unsigned)sms * 2, kCtaSortThreads, csmem, s>>>(N, tile_bits, nseg, depth, ranges, lists,
                                                                           list_counts, capacity, summary, values);
-    return check_launch("hs_tile_fill");
+    return check_launch("hs_tile_fill_longest");
 }
 
 }  // extern "C"

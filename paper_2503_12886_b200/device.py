@@ -463,6 +463,13 @@ class Binner:
             self._ensure(total)
             self.cursor[:nseg].copy_(ranges.view(-1, 2)[:, 0])
             fill()
+        if int(L.load().hs_tile_cta_sort_min()) <= self.longest <= tile_sort_cap():
+            # lists long enough for the shared-memory CTA sort (rare): after the fill
+            L.call("hs_tile_fill_longest", B, N, width, height, _p(depth), _p(ranges), _p(self.lists),
+                   _p(self.list_counts), _p(self.summary), self.cap, _p(self.vals), s)
+            self.launches_extra = 1
+        else:
+            self.launches_extra = 0
         self._depth_range_clean = self.longest <= tile_sort_cap()
         if self.longest > tile_sort_cap():
             # a list too long to sort in shared memory: the global two-level sort
@@ -490,7 +497,7 @@ def tile_sort_cap():
 def launches_tiles(binner):
     """Kernel launches issued by Binner.bin_tiles: count, scan, scatter, the four list
     sorts (warp, CTA-cooperative, long-list, 64-bit fallback) (+ the two-level fallback's)."""
-    n = 6                    # (the count runs inside the projection)
+    n = 5 + getattr(binner, "launches_extra", 0)   # (the count runs inside the projection)
     if binner.mode == "two_level":
         n += 6 + launches_binning(1, binner.passes, True)
     return n
