@@ -196,17 +196,18 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  * hs_tile_count: each (frame, splat) with counts[i] > 0 adds one to every tile of its
  *   pixel bbox in tile_counts [B << tile_bits] (zero on entry; hs_tile_scan re-zeroes it).
  * hs_tile_scan: ranges [2 * (B << tile_bits)] (every entry written), scatter cursors
- *   [B << tile_bits], summary [4] = {key total, error word (err is reset to HS_NO_ERROR
- *   after the read), depth range as hs_bin_scan (depth_range is reset to {~0, 0} after the
- *   read unless the longest list exceeds hs_tile_sort_cap()), longest list}, and in lists [2 * (B << tile_bits)] / list_counts [8 + ceil((B <<
- *   tile_bits) / 1024)] the lists the fill sorts per CTA (the rest of lists is the fill's
- *   scratch; the rest of list_counts the scan's).
+ *   [B << tile_bits], summary [4] = {key total, error word, depth range as hs_bin_scan,
+ *   longest list} -- err is reset to HS_NO_ERROR after the read, and depth_range to
+ *   {~0, 0} unless the longest list exceeds hs_tile_sort_cap() -- and, in lists
+ *   [2 * (B << tile_bits)] / list_counts [8 + ceil((B << tile_bits) / 1024)], the lists the
+ *   fill sorts per CTA (the rest of list_counts is the scan's scratch).
  * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
  *   entry from the items' tile_rects (NULL: from the records' bboxes and counts); each
- *   list in (depth, Gaussian index) order -- the reference order.  Skipped on the device
- *   when summary[0] > capacity (grow the buffers, reset the cursors to the range starts
- *   and call again).  Lists longer than hs_tile_sort_cap() are scattered but NOT sorted:
- *   when summary[3] exceeds the cap, bin that step with the two-level sort instead.
+ *   list of at most hs_tile_cta_sort_min() - 1 entries in (depth, Gaussian index) order --
+ *   the reference order.  Skipped on the device when summary[0] > capacity (grow the
+ *   buffers, reset the cursors to the range starts and call again).  Longer lists are
+ *   scattered but sorted by hs_tile_fill_longest (up to hs_tile_sort_cap()) or, past the
+ *   cap, not at all: then bin that step with the two-level sort instead.
  *   The short lists sort on a library-internal stream (created on the device current at
  *   the first call) that the caller's stream joins before returning work to it: calls
  *   are stream-ordered like any other, but not thread-safe against each other. */

@@ -17,7 +17,7 @@
 //                  slot, ties settled on the full keys), CTAs sort lists up to kWarpCap
 //                  (register runs merged by rank) -- concurrently on two streams -- and
 //                  up to kCtaCap (shared-memory bitonic); lists the 32-bit path cannot
-//                  settle take a 64-bit warp sort
+//                  settle are sorted on their full 64-bit keys in shared memory
 //
 // Sorting each list by (depth bits, index) is exactly the reference's order: positive
 // float depths compare like their bit patterns and the stable argsort breaks ties by
@@ -432,45 +432,6 @@ __device__ __forceinline__ void swap_regs(K (&key)[E], int k) {
     }
 }
 
-template <int E>
-__device__ __forceinline__ void sort_list_warp(const float *__restrict__ depth, int64_t fb, uint32_t start,
-                                               uint32_t len, uint32_t *__restrict__ vals, int lane) {
-    constexpr int P = 32 * E;
-    unsigned long long key[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const uint32_t q = (uint32_t)(e * 32 + lane);
-        key[e] = q < len ? sort_key(depth, fb, vals[start + q]) : ~0ull;
-    }
-#pragma unroll 1
-    for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll 1
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-                const int je = j >> 5;
-                if (E >= 32 && je == 16) swap_regs<E, (E >= 32 ? 16 : 0)>(key, k);
-                else if (E >= 16 && je == 8) swap_regs<E, (E >= 16 ? 8 : 0)>(key, k);
-                else if (E >= 8 && je == 4) swap_regs<E, (E >= 8 ? 4 : 0)>(key, k);
-                else if (E >= 4 && je == 2) swap_regs<E, (E >= 4 ? 2 : 0)>(key, k);
-                else if (E >= 2 && je == 1) swap_regs<E, (E >= 2 ? 1 : 0)>(key, k);
-            } else {
-                const bool lower = (lane & j) == 0;
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const bool up = k >= 32 ? ((e * 32) & k) == 0 : (lane & k) == 0;
-                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, key[e], j);
-                    const unsigned long long lo = key[e] < o ? key[e] : o, hi = key[e] < o ? o : key[e];
-                    key[e] = (lower == up) ? lo : hi;
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const uint32_t q = (uint32_t)(e * 32 + lane);
-        if (q < len) vals[start + q] = (uint32_t)key[e];
-    }
-}
 
 // The common case in 32-bit keys: ((depth bits - the list's smallest) >> sh) << IB |
 // slot, slot = the entry's position in the unsorted list, whose full 64-bit key
@@ -479,7 +440,7 @@ __device__ __forceinline__ void sort_list_warp(const float *__restrict__ depth, 
 // depth ties, or depths that differ only in the dropped bits) are then put in full-key
 // order by odd-even transposition over the sorted slots.  Returns false -- `vals`
 // untouched -- when that does not settle within kFixRounds rounds (long runs of equal
-// depths); the caller then sorts the list with 64-bit keys.
+// depths); the caller then sorts the full 64-bit keys in shared memory.
 constexpr int kFixRounds = 32;
 
 // ascending bitonic network over the 32 * E 32-bit keys of a warp (key q = e * 32 + lane)
@@ -594,14 +555,20 @@ __device__ __forceinline__ bool sort_list_warp32(const float *__restrict__ depth
     return true;
 }
 
-// lists the 32-bit sort declines go to lists[nseg + ...] (count list_counts[4])
+// a list the 32-bit sort declines is sorted on its 64-bit keys in the warp's shared memory
 template <int E>
 __device__ __forceinline__ void sort_list(const float *__restrict__ depth, int64_t fb, uint32_t start,
                                           uint32_t len, uint32_t *__restrict__ vals, int lane,
-                                          unsigned long long *__restrict__ s_k64, uint32_t *__restrict__ s_q,
-                                          uint32_t seg, uint32_t *__restrict__ wide, uint32_t *__restrict__ n_wide) {
-    if (!sort_list_warp32<E>(depth, fb, start, len, vals, lane, s_k64, s_q) && lane == 0)
-        wide[atomicAdd(n_wide, 1u)] = seg;
+                                          unsigned long long *__restrict__ s_k64, uint32_t *__restrict__ s_q) {
+    if (!sort_list_warp32<E>(depth, fb, start, len, vals, lane, s_k64, s_q)) {
+        // the full 64-bit keys are still in shared memory: sort them there (rare)
+        int P = 32;
+        while (P < (int)len) P <<= 1;
+        for (int q = (int)len + lane; q < P; q += 32) s_k64[q] = ~0ull;
+        __syncwarp();
+        bitonic_smem<false>(s_k64, P, lane, 32);
+        for (uint32_t q = lane; q < len; q += 32) vals[start + q] = (uint32_t)s_k64[q];
+    }
     __syncwarp();
 }
 
@@ -615,7 +582,6 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, HS_SHORT_SORT_MINB) tile_
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
     __shared__ unsigned long long s_k64_all[kWarpSortWarps][kWarpShort];
     __shared__ uint32_t s_q_all[kWarpSortWarps][kWarpShort];
-    uint32_t *wide = lists + nseg;
     if (summary[0] > capacity) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned long long *s_k64 = s_k64_all[w];
@@ -633,11 +599,10 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, HS_SHORT_SORT_MINB) tile_
             const uint32_t seg = base + b * stride;
             const uint32_t start = __shfl_sync(0xffffffffu, rg_l.x, b), len = __shfl_sync(0xffffffffu, len_l, b);
             const int64_t fb = (int64_t)(seg >> tile_bits) * N;
-            uint32_t *nw = list_counts + 4;
-            if (len <= 32u) sort_list<1>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
-            else if (len <= 64u) sort_list<2>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
-            else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
-            else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q, seg, wide, nw);
+            if (len <= 32u) sort_list<1>(depth, fb, start, len, vals, lane, s_k64, s_q);
+            else if (len <= 64u) sort_list<2>(depth, fb, start, len, vals, lane, s_k64, s_q);
+            else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q);
+            else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q);
         }
     }
 }
@@ -666,7 +631,6 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
     __shared__ int s_flag;
     if (summary[0] > capacity) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t *wide = lists + nseg;
     // the lists longer than kWarpShort, collected by the scan: CTA c takes c + j * gridDim.x
     const uint32_t nbig = list_counts[1];
     for (uint32_t li = blockIdx.x; li < nbig; li += gridDim.x) {
@@ -763,34 +727,17 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
         }
         if (ok) {
             for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) vals[start + q] = (uint32_t)s_k64[s_out[q] & kSlot];
-        } else if (threadIdx.x == 0) {
-            wide[atomicAdd(list_counts + 4, 1u)] = seg;
+        } else {
+            // the full 64-bit keys are still in shared memory: sort them there (rare)
+            int P = 2 * kRun;
+            while (P < (int)len) P <<= 1;
+            for (int q = (int)len + threadIdx.x; q < P; q += blockDim.x) s_k64[q] = ~0ull;
+            __syncthreads();
+            bitonic_smem<true>(s_k64, P, threadIdx.x, blockDim.x);
+            for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) vals[start + q] = (uint32_t)s_k64[q];
         }
         __syncthreads();
       }
-    }
-}
-
-// 64-bit keys (depth bits << 32 | index) for the lists the 32-bit sort declined
-__global__ void __launch_bounds__(32 * kWarpSortWarps) tile_sort_wide_kernel(
-    int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
-    const uint32_t *__restrict__ lists, const uint32_t *__restrict__ list_counts, uint64_t capacity,
-    const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
-    if (summary[0] > capacity) return;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t count = list_counts[4];
-    const uint32_t stride = gridDim.x * kWarpSortWarps;
-    for (uint32_t e = blockIdx.x * kWarpSortWarps + w; e < count; e += stride) {
-        const uint32_t seg = lists[nseg + e];
-        const uint2 rg = reinterpret_cast<const uint2 *>(ranges)[seg];
-        const uint32_t start = rg.x, len = rg.y - rg.x;
-        const int64_t fb = (int64_t)(seg >> tile_bits) * N;
-        if (len <= 32u) sort_list_warp<1>(depth, fb, start, len, vals, lane);
-        else if (len <= 64u) sort_list_warp<2>(depth, fb, start, len, vals, lane);
-        else if (len <= 128u) sort_list_warp<4>(depth, fb, start, len, vals, lane);
-        else if (len <= 256u) sort_list_warp<8>(depth, fb, start, len, vals, lane);
-        else if (len <= 512u) sort_list_warp<16>(depth, fb, start, len, vals, lane);
-        else sort_list_warp<32>(depth, fb, start, len, vals, lane);
     }
 }
 
@@ -912,8 +859,6 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     tile_sort_long_kernel<<<(unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     cudaStreamWaitEvent(s, shorts_done, 0);
-    tile_sort_wide_kernel<<<(unsigned)sms * 4, 32 * kWarpSortWarps, 0, s>>>(
-        N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     return check_launch("hs_tile_fill");
 }
 
