@@ -199,8 +199,9 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   [B << tile_bits], summary [4] = {key total, error word, depth range as hs_bin_scan,
  *   longest list} -- err is reset to HS_NO_ERROR after the read, and depth_range to
  *   {~0, 0} unless the longest list exceeds hs_tile_sort_cap() -- and, in lists
- *   [2 * (B << tile_bits)] / list_counts [8 + ceil((B << tile_bits) / 1024)], the lists the
- *   fill sorts per CTA (the rest of list_counts is the scan's scratch).
+ *   [2 * (B << tile_bits)] / list_counts [1 + 2 * list_half, zero on first use; list_half
+ *   >= 8 + ceil((B << tile_bits) / 1024), the same in every call], the lists the fill sorts
+ *   per CTA (list_counts alternates halves between steps: no reset is needed).
  * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
  *   entry from the items' tile_rects (NULL: from the records' bboxes and counts); each
  *   list of at most hs_tile_cta_sort_min() - 1 entries in (depth, Gaussian index) order --
@@ -217,17 +218,17 @@ int hs_tile_sort_cap(void);
  * the summary's longest list is in that range (arguments as hs_tile_fill). */
 int hs_tile_cta_sort_min(void);
 int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *depth, const uint32_t *ranges,
-                         uint32_t *lists, uint32_t *list_counts, const unsigned long long *summary,
-                         uint64_t capacity, uint32_t *values, void *stream);
+                         uint32_t *lists, uint32_t *list_counts, int list_half,
+                         const unsigned long long *summary, uint64_t capacity, uint32_t *values, void *stream);
 int hs_tile_count(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                   uint32_t *tile_counts, void *stream);
 int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,
-                 uint32_t *lists, uint32_t *list_counts, unsigned long long *err,
+                 uint32_t *lists, uint32_t *list_counts, int list_half, unsigned long long *err,
                  uint32_t *depth_range, unsigned long long *summary, void *stream);
 int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                  const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor,
                  uint32_t *lists,
-                 uint32_t *list_counts, const unsigned long long *summary, uint64_t capacity,
+                 uint32_t *list_counts, int list_half, const unsigned long long *summary, uint64_t capacity,
                  uint32_t *keys, uint32_t *values, void *stream);
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);

@@ -65,11 +65,11 @@ SIGNATURES = {
     "hs_tile_ranges32": (_I, [_L, _P, _P, _P]),
     "hs_tile_sort_cap": (_I, []),
     "hs_tile_cta_sort_min": (_I, []),
-    "hs_tile_fill_longest": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, ctypes.c_uint64, _P, _P]),
+    "hs_tile_fill_longest": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P]),
     "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P]),
     "hs_tile_count": (_I, [_I, _L, _I, _I, _P, _P, _P, _P]),
-    "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint64, _P, _P, _P]),
+    "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
+    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P, _P]),
     "hs_bin_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_raster_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_adam": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _P]),

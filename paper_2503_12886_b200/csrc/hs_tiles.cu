@@ -36,6 +36,17 @@ constexpr int kCtaCap = 8192;         // longest list one CTA sorts in shared me
 constexpr int kCtaSortThreads = 512;
 constexpr int kWarpSortWarps = 4;     // warps per CTA of the warp-level sort
 
+// list_counts = [the half the next scan uses | half 0 | half 1], halves of `half` words:
+// [1] / [2] the CTA-sorted list counts, [5] scan ticket, [6] scan done, [7] longest,
+// [8 + t] scan CTA t's flagged total.  A scan works in its half and zeroes the other one
+// (the previous step's, whose fill has finished) for the next, so no memset is needed.
+__device__ __forceinline__ uint32_t *counts_half(uint32_t *list_counts, int half, uint32_t p) {
+    return list_counts + 1 + (size_t)p * half;
+}
+__device__ __forceinline__ const uint32_t *filled_half(const uint32_t *list_counts, int half) {
+    return list_counts + 1 + (size_t)(1u - list_counts[0]) * half;   // the scan flipped [0]
+}
+
 // ------------------------------------------------------------------- count
 
 // A CTA covers kTileItems consecutive (frame, Gaussian) items -- neighbours on the
@@ -144,7 +155,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                                                                  uint32_t *__restrict__ ranges,
                                                                  uint32_t *__restrict__ cursor,
                                                                  uint32_t *__restrict__ lists,
-                                                                 uint32_t *__restrict__ list_counts,
+                                                                 uint32_t *__restrict__ list_counts, int half,
                                                                  unsigned long long *__restrict__ err,
                                                                  uint32_t *__restrict__ depth_range,
                                                                  unsigned long long *__restrict__ summary) {
@@ -215,9 +226,16 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) atomicMax(&s_max, mx);
     __syncthreads();
-    // [1] / [2]: the long / longer lists, [4]: the fallback's count
-    if (tid < 8) list_counts[tid] = tid == 1 ? s_big[0] : tid == 2 ? s_big[1] : 0u;
+    // [1] / [2]: the long / longer lists, in this step's half; the other half zeroed
+    const uint32_t p = list_counts[0];
+    __syncthreads();
+    uint32_t *lc = counts_half(list_counts, half, p), *other = counts_half(list_counts, half, 1u - p);
+    if (tid == 1) lc[1] = s_big[0];
+    if (tid == 2) lc[2] = s_big[1];
+    for (int k = tid; k < half; k += blockDim.x) other[k] = 0u;
+    __syncthreads();
     if (tid == 0) {
+        list_counts[0] = 1u - p;
         summary[0] = carry;
         summary[1] = err ? *err : HS_NO_ERROR;
         if (err) *err = HS_NO_ERROR;                 // read once per step: reset for the next
@@ -244,13 +262,15 @@ __global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, ui
                                                                     uint32_t *__restrict__ ranges,
                                                                     uint32_t *__restrict__ cursor,
                                                                     uint32_t *__restrict__ lists,
-                                                                    uint32_t *__restrict__ list_counts,
+                                                                    uint32_t *__restrict__ all_counts, int half,
                                                                     unsigned long long *__restrict__ err,
                                                                     uint32_t *__restrict__ depth_range,
                                                                     unsigned long long *__restrict__ summary) {
     __shared__ uint32_t wsum[kScanSpan / 32];
     __shared__ uint32_t s_tile, s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t p = all_counts[0];            // flipped only by the last CTA, after all read it
+    uint32_t *list_counts = counts_half(all_counts, half, p);
     if (tid == 0) s_tile = atomicAdd(list_counts + 5, 1u);
     __syncthreads();
     const uint32_t t = s_tile;
@@ -329,6 +349,9 @@ __global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, ui
                 depth_range[0] = 0xFFFFFFFFu;
                 depth_range[1] = 0u;
             }
+            uint32_t *other = counts_half(all_counts, half, 1u - p);
+            for (int k = 0; k < half; ++k) other[k] = 0u;
+            all_counts[0] = 1u - p;
         }
     }
 }
@@ -621,7 +644,7 @@ constexpr int kLongWarps = kWarpCap / kRun;
 
 __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
-    uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, uint64_t capacity,
+    uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, int half, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
     constexpr int E = kRun / 32, IB = 10;
     constexpr uint32_t kSlot = (1u << IB) - 1u;
@@ -632,7 +655,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
     if (summary[0] > capacity) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // the lists longer than kWarpShort, collected by the scan: CTA c takes c + j * gridDim.x
-    const uint32_t nbig = list_counts[1];
+    const uint32_t nbig = filled_half(list_counts, half)[1];
     for (uint32_t li = blockIdx.x; li < nbig; li += gridDim.x) {
       {
         const uint32_t seg = lists[li];
@@ -744,11 +767,11 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
 // one CTA per list of kWarpCap+1..kCtaCap entries
 __global__ void __launch_bounds__(kCtaSortThreads) tile_sort_cta_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
-    const uint32_t *__restrict__ lists, const uint32_t *__restrict__ list_counts, uint64_t capacity,
+    const uint32_t *__restrict__ lists, const uint32_t *__restrict__ list_counts, int half, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
     extern __shared__ unsigned long long s_keys[];
     if (summary[0] > capacity) return;
-    const uint32_t nbig = list_counts[2];
+    const uint32_t nbig = filled_half(list_counts, half)[2];
     for (uint32_t li = blockIdx.x; li < nbig; li += gridDim.x) {
       {
         const uint32_t seg = lists[nseg - 1 - li];
@@ -794,7 +817,7 @@ int hs_tile_count(int B, int64_t N, int width, int height, const float *records,
 }
 
 int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *ranges, uint32_t *cursor,
-                 uint32_t *lists, uint32_t *list_counts, unsigned long long *err,
+                 uint32_t *lists, uint32_t *list_counts, int list_half, unsigned long long *err,
                  uint32_t *depth_range, unsigned long long *summary, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
@@ -809,19 +832,22 @@ int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *
 #endif
     if (HS_SCAN_MULTI && nseg > kScanSpan) {
         const int ctas = (int)((nseg + kScanSpan - 1) / kScanSpan);
-        cudaMemsetAsync(list_counts, 0, sizeof(uint32_t) * (8 + ctas), s);
+        if (list_half < 8 + ctas) {
+            set_error("hs_tile_scan: list_counts halves of %d words, need %d", list_half, 8 + ctas);
+            return HS_ERR_SHAPE;
+        }
         tile_scan_multi_kernel<<<ctas, kScanSpan, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts,
-                                                          err, depth_range, summary);
+                                                          list_half, err, depth_range, summary);
     } else {
-        tile_scan_kernel<<<1, 1024, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts, err,
-                                            depth_range, summary);
+        tile_scan_kernel<<<1, 1024, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts, list_half,
+                                            err, depth_range, summary);
     }
     return check_launch("hs_tile_scan");
 }
 
 int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                  const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
-                 uint32_t *list_counts, const unsigned long long *summary, uint64_t capacity,
+                 uint32_t *list_counts, int list_half, const unsigned long long *summary, uint64_t capacity,
                  uint32_t *keys, uint32_t *values, void *stream) {
     const int64_t items = (int64_t)B * N;
     if (items <= 0) return HS_OK;
@@ -857,14 +883,14 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
 #define HS_LONG_SORT_CTAS_PER_SM 16
 #endif
     tile_sort_long_kernel<<<(unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s>>>(
-        N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
+        N, tile_bits, nseg, depth, ranges, lists, list_counts, list_half, capacity, summary, values);
     cudaStreamWaitEvent(s, shorts_done, 0);
     return check_launch("hs_tile_fill");
 }
 
 int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *depth, const uint32_t *ranges,
-                         uint32_t *lists, uint32_t *list_counts, const unsigned long long *summary,
-                         uint64_t capacity, uint32_t *values, void *stream) {
+                         uint32_t *lists, uint32_t *list_counts, int list_half,
+                         const unsigned long long *summary, uint64_t capacity, uint32_t *values, void *stream) {
     if ((int64_t)B * N <= 0) return HS_OK;
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
@@ -879,7 +905,8 @@ int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *d
         attr = true;
     }
     tile_sort_cta_kernel<<<(unsigned)sms * 2, kCtaSortThreads, csmem, s>>>(N, tile_bits, nseg, depth, ranges, lists,
-                                                                          list_counts, capacity, summary, values);
+                                                                          list_counts, list_half, capacity, summary,
+                                                                          values);
     return check_launch("hs_tile_fill_longest");
 }
 

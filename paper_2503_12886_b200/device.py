@@ -404,7 +404,8 @@ class Binner:
             self.tile_counts = torch.zeros(nseg, dtype=torch.int32, device=d)
             self.cursor = torch.empty(nseg, dtype=torch.int32, device=d)
             self.lists = torch.empty(2 * nseg, dtype=torch.int32, device=d)
-            self.list_counts = torch.zeros(8 + (nseg + 1023) // 1024, dtype=torch.int32, device=d)
+            self.list_half = 8 + (nseg + 1023) // 1024
+            self.list_counts = torch.zeros(1 + 2 * self.list_half, dtype=torch.int32, device=d)
         return self.tile_counts
 
     def tile_rects_buffer(self, B, N, width, height):
@@ -437,7 +438,8 @@ class Binner:
         if not counted:
             L.call("hs_tile_count", B, N, width, height, _p(records), _p(counts), _p(self.tile_counts), s)
         L.call("hs_tile_scan", B, width, height, _p(self.tile_counts), _p(ranges), _p(self.cursor),
-               _p(self.lists), _p(self.list_counts), _p(err), _p(self.depth_range), _p(self.summary), s)
+               _p(self.lists), _p(self.list_counts), self.list_half, _p(err), _p(self.depth_range), _p(self.summary),
+               s)
         self.summary_host.copy_(self.summary, non_blocking=True)
         ready = torch.cuda.Event()
         ready.record()
@@ -446,7 +448,7 @@ class Binner:
 
         def fill():
             L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(rects), _p(depth), _p(ranges),
-                   _p(self.cursor), _p(self.lists), _p(self.list_counts), _p(self.summary), self.cap,
+                   _p(self.cursor), _p(self.lists), _p(self.list_counts), self.list_half, _p(self.summary), self.cap,
                    _p(self.keys), _p(self.vals), s)
         fill()                              # first: the GPU reaches it right after the scan
         self.order_ready = False
@@ -466,7 +468,7 @@ class Binner:
         if int(L.load().hs_tile_cta_sort_min()) <= self.longest <= tile_sort_cap():
             # lists long enough for the shared-memory CTA sort (rare): after the fill
             L.call("hs_tile_fill_longest", B, N, width, height, _p(depth), _p(ranges), _p(self.lists),
-                   _p(self.list_counts), _p(self.summary), self.cap, _p(self.vals), s)
+                   _p(self.list_counts), self.list_half, _p(self.summary), self.cap, _p(self.vals), s)
             self.launches_extra = 1
         else:
             self.launches_extra = 0

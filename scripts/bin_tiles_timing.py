@@ -31,10 +31,11 @@ for r in range(reps):
     L.call("hs_tile_count", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts), _p(bn.tile_counts), s)
     e[1].record()
     L.call("hs_tile_scan", B, tr.W, tr.H, _p(bn.tile_counts), _p(ranges), _p(bn.cursor), _p(bn.lists),
-           _p(bn.list_counts), _p(tr.err), _p(bn.depth_range), _p(bn.summary), s)
+           _p(bn.list_counts), bn.list_half, _p(tr.err), _p(bn.depth_range), _p(bn.summary), s)
     e[2].record()
     L.call("hs_tile_fill", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts), _p(bn.rects), _p(tr.depth), _p(ranges),
-           _p(bn.cursor), _p(bn.lists), _p(bn.list_counts), _p(bn.summary), bn.cap, _p(bn.keys), _p(bn.vals), s)
+           _p(bn.cursor), _p(bn.lists), _p(bn.list_counts), bn.list_half, _p(bn.summary), bn.cap, _p(bn.keys),
+           _p(bn.vals), s)
     e[3].record()
 torch.cuda.synchronize()
 acc = [0.0, 0.0, 0.0]
