@@ -323,6 +323,49 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
         }
         if (c0 * 32 >= E10) continue;                      // warp-uniform
         const int64_t e0 = c0 * 32 + lane;
+        if constexpr (kKBB == 1) {
+            // software pipeline over the bases: basis k+1's delta loads are issued before
+            // basis k's FMAs and reduce-scatter, so a load's latency hides behind a whole
+            // basis of work instead of stalling the warp once per basis
+            float dn[kCPI];
+#pragma unroll
+            for (int j = 0; j < kCPI; ++j) dn[j] = in10[j] ? __ldcs(deltas + e0 + 32 * j) : 0.f;
+            for (int k = 0; k < K; ++k) {
+                float dk[kCPI];
+#pragma unroll
+                for (int j = 0; j < kCPI; ++j) dk[j] = dn[j];
+                if (k + 1 < K) {
+#pragma unroll
+                    for (int j = 0; j < kCPI; ++j)
+                        dn[j] = in10[j] ? __ldcs(deltas + (int64_t)(k + 1) * E10 + e0 + 32 * j) : 0.f;
+                }
+                float gd[kCPI];
+                float v[BP];
+#pragma unroll
+                for (int j = 0; j < kCPI; ++j) gd[j] = 0.f;
+#pragma unroll
+                for (int b = 0; b < BP; ++b) {
+                    const float pk = p_s[b * K + k];
+                    v[b] = 0.f;
+#pragma unroll
+                    for (int j = 0; j < kCPI; ++j) {
+                        gd[j] = fmaf(pk, g[j][b], gd[j]);
+                        v[b] = fmaf(dk[j], g[j][b], v[b]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kCPI; ++j)
+                    if (in10[j]) {
+                        float *o = g_deltas + (int64_t)k * E10 + e0 + 32 * j;
+                        *o = accumulate ? *o + gd[j] : gd[j];
+                    }
+                int vi;
+                bool issue;
+                const float r = reduce_scatter(v, lane, vi, issue);
+                if (issue) accw[warp][k * BP + vi] += r;
+            }
+            continue;
+        }
         for (int k0 = 0; k0 < K; k0 += kKBB) {
           float dk[kCPI][kKBB];
 #pragma unroll
