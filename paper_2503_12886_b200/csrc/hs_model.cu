@@ -183,6 +183,9 @@ __global__ void mlp_bwd_weights_kernel(int B, int H, int D, int K, const float *
 #define HS_BLEND_KB 4
 #endif
 constexpr int kKB = HS_BLEND_KB;
+#ifndef HS_BLEND_FWD_PF
+#define HS_BLEND_FWD_PF 0   // 1: next round prefetched (111 registers; measured 33 -> 39 us, slower)
+#endif
 template <int VEC, int BC>
 __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
                                                         const float *__restrict__ base,
@@ -212,18 +215,30 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
                 for (int c = 0; c < VEC; ++c) acc[j][c] = bv[c];
             // kKB bases per round: all their loads are issued before any use, so a
             // thread keeps kKB * 16 B in flight instead of one dependent load per basis
-            for (int k0 = 0; k0 < K; k0 += kKB) {
-                float dv[kKB][VEC];
+            // software pipeline (HS_BLEND_FWD_PF): the next round's loads are issued
+            // before this round's FMAs
+            float dn[kKB][VEC];
+            auto load_round = [&](int k0) {
 #pragma unroll
                 for (int q = 0; q < kKB; ++q) {
                     const int k = min(k0 + q, K - 1);
                     if constexpr (VEC == 4) {
                         float4 t = __ldg(reinterpret_cast<const float4 *>(deltas + (int64_t)k * E + e));
-                        dv[q][0] = t.x; dv[q][1] = t.y; dv[q][2] = t.z; dv[q][3] = t.w;
+                        dn[q][0] = t.x; dn[q][1] = t.y; dn[q][2] = t.z; dn[q][3] = t.w;
                     } else {
-                        dv[q][0] = __ldcs(deltas + (int64_t)k * E + e);
+                        dn[q][0] = __ldcs(deltas + (int64_t)k * E + e);
                     }
                 }
+            };
+            if (HS_BLEND_FWD_PF) load_round(0);
+            for (int k0 = 0; k0 < K; k0 += kKB) {
+                float dv[kKB][VEC];
+                if (!HS_BLEND_FWD_PF) load_round(k0);
+#pragma unroll
+                for (int q = 0; q < kKB; ++q)
+#pragma unroll
+                    for (int c = 0; c < VEC; ++c) dv[q][c] = dn[q][c];
+                if (HS_BLEND_FWD_PF && k0 + kKB < K) load_round(k0 + kKB);
 #pragma unroll
                 for (int q = 0; q < kKB; ++q) {
                     if (k0 + q < K) {
