@@ -519,6 +519,53 @@ void or_composite_backward(int64_t M, const double *mean2d, const double *conic,
     free(suffix);
 }
 
+/* Checker extension (not in the reference): the pixels where one of the
+ * compositing decisions of S/render.py:233-273 sits within fp32 noise of its
+ * threshold, so an fp32 implementation and this float64 restatement may decide
+ * it differently.  The loop is or_composite's; a pixel is flagged when, for some
+ * splat it tests,
+ *   |alpha - 1/255| < 2e-6         (alpha cutoff, :266)
+ *   |q - qmax| < 1e-4 (1 + qmax)   (ellipse cutoff, :262)
+ *   alpha > 1 - 1e-6               (fp32 rounds alpha to 1, T to ~0)
+ *   T (1 - alpha) within 1e-3 relative of 1e-14 (termination, :254)
+ * mask (h*w bytes) is OR-ed, so a caller can accumulate over frames. */
+void or_flip_mask(int64_t M, const double *mean2d, const double *conic,
+                  const double *opacity, const double *radius, const int32_t *bbox,
+                  int h, int w, uint8_t *mask) {
+    int64_t P = (int64_t)h * w;
+    double *trans = (double *)malloc(sizeof(double) * P);
+    for (int64_t p = 0; p < P; ++p) trans[p] = 1.0;
+    for (int64_t s = 0; s < M; ++s) {
+        double op = opacity[s];
+        if (op < ALPHA_CUTOFF) continue;
+        double qmax = 2.0 * log(op * 255.0) + 1e-9;
+        double mx = mean2d[2 * s], my = mean2d[2 * s + 1], rad = radius[s];
+        double a = conic[3 * s], b = conic[3 * s + 1], c = conic[3 * s + 2];
+        int r_lo, r_hi, c_lo, c_hi;
+        splat_bbox(bbox, s, mx, my, rad, h, w, &r_lo, &r_hi, &c_lo, &c_hi);
+        for (int r = r_lo; r <= r_hi; ++r) {
+            double dy = r + 0.5 - my;
+            for (int cc = c_lo; cc <= c_hi; ++cc) {
+                int64_t p = (int64_t)r * w + cc;
+                double t = trans[p];
+                if (t < TERMINATION_EPS) continue;
+                double dx = cc + 0.5 - mx;
+                double q = a * dx * dx + 2.0 * b * dx * dy + c * dy * dy;
+                if (fabs(q - qmax) < 1e-4 * (1.0 + fabs(qmax))) mask[p] = 1;
+                if (q > qmax) continue;
+                double alpha = op * exp(-0.5 * q);
+                if (fabs(alpha - ALPHA_CUTOFF) < 2e-6) mask[p] = 1;
+                if (alpha < ALPHA_CUTOFF) continue;
+                if (alpha > 1.0 - 1e-6) mask[p] = 1;
+                double tn = t * (1.0 - alpha);
+                if (fabs(tn - TERMINATION_EPS) < 1e-3 * TERMINATION_EPS) mask[p] = 1;
+                trans[p] = tn;
+            }
+        }
+    }
+    free(trans);
+}
+
 /* S/render.py:339-377  _weight_sums_kernel (arrays in depth order); num (M*3) and
  * den (M) accumulate into zero-initialized caller buffers. */
 void or_weight_sums(int64_t M, const double *mean2d, const double *conic,

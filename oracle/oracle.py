@@ -384,6 +384,21 @@ def rasterize(splats: Splats, camera: Cam, background, order=None, bbox=None):
     return image, aux
 
 
+def flip_mask(splats: Splats, camera: Cam, order=None, bbox=None, out=None):
+    """Checker extension (hs_oracle.c:or_flip_mask): (h, w) bool, the pixels where an
+    alpha-cutoff / ellipse-cutoff / alpha->1 / termination decision of the reference's
+    compositing (S/render.py:233-273) is within fp32 noise of its threshold.  ``out``
+    (h, w) uint8 accumulates across calls."""
+    h, w = camera.height, camera.width
+    mask = np.zeros((h, w), np.uint8) if out is None else out
+    m = len(splats)
+    if m:
+        order = splats.sort_order if order is None else np.asarray(order, dtype=np.int64)
+        mean, con, op, _, rad, sb = _sorted(splats, order, bbox)
+        lib().or_flip_mask(m, _p(mean), _p(con), _p(op), _p(rad), _p(sb, _I32), h, w, _p(mask, _U8))
+    return mask.astype(bool) if out is None else mask
+
+
 def render_backward(splats: Splats, aux: Aux, grad_image) -> GSet:
     """S/render.py:410-429 (+ _preprocess_backward :432-497)."""
     grad_image = _f64(grad_image)
@@ -659,7 +674,10 @@ def train_step(state: State, thetas, images, frames_list, backgrounds, replay=No
     ``replay`` (checker extension): per frame a dict with ``order``
     (compositing order over the kept splats) and ``bbox`` (int pixel bbox per kept
     splat) taken from the implementation under test, so the fp32-vs-fp64 decision
-    boundaries (depth ties, the 3-sigma bbox edge) are identical on both sides."""
+    boundaries (depth ties, the 3-sigma bbox edge) are identical on both sides.
+    Optional per-frame ``signs`` ((H, W, 3) in {-1, 0, 1}: the implementation's L1
+    sign per pixel channel, replacing the oracle's) and ``gmask`` ((H, W) bool:
+    pixels whose image gradient is zeroed on both sides, see ``flip_mask``)."""
     model = state.model
     cam = state.camera
     B = len(thetas)
@@ -687,12 +705,19 @@ def train_step(state: State, thetas, images, frames_list, backgrounds, replay=No
         ctxs[b].aux = aux
         target = composite_over(images[b], backgrounds[b])
         loss, gimg = l1_loss(image, target)
+        if replay is not None and replay[b].get("signs") is not None:
+            # the implementation's own L1 sign per pixel channel (a decision like the
+            # depth order: fp32 and fp64 differ where |pred - target| ~ 1e-7)
+            gimg = np.asarray(replay[b]["signs"], np.float64) / image.size
+        if replay is not None and replay[b].get("gmask") is not None:
+            gimg = gimg * ~np.asarray(replay[b]["gmask"], bool)[:, :, None]
         losses[b] = loss
         grads_img.append(gimg / (global_batch or B))
         bp = image - aux.transmittance[:, :, None] * _f64(backgrounds[b])[None, None, :]
         bt = _f64(images[b])[:, :, :3] * _f64(images[b])[:, :, 3:4]
         black[b] = float(np.mean(np.abs(bp - bt)))
     per_item = state.map(lambda c, g: frame_backward(model, c, g), list(zip(ctxs, grads_img)))
+    state.last_items = (ctxs, grads_img, per_item)      # checker: per-frame stages
     # ParamGradients reduction in item order (S/train.py:253-255)
     n = model.count
     g_base14 = np.zeros(14 * n)

@@ -123,6 +123,19 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 1 - alpha for the transmittance update, floored at 2^-24 (the spacing of fp32 below 1).
+// The floor only changes alpha == 1.0f exactly: fp32 rounds sigmoid(logit) to 1 above
+// logit ~16.6 and the Gaussian to 1 at a pixel within ~1e-3 px of the mean, where the
+// reference's float64 alpha is still < 1 (its opacity saturates only near logit 36.7).
+// Unfloored, T would become exactly 0 and the adjoint's t_rev / (1 - alpha) would be
+// 0 * inf = NaN (S/render.py:318-319).  Forward and adjoint use the same floor, so
+// t_rev * rcp(one_minus_alpha) still recovers the transmittance before the splat.
+#ifndef HS_ONE_MINUS_FLOOR
+#define HS_ONE_MINUS_FLOOR 5.9604644775390625e-8f               // 2^-24 (0: the unguarded A/B build)
+#endif
+constexpr float kOneMinusFloor = HS_ONE_MINUS_FLOOR;
+__device__ __forceinline__ float one_minus_alpha(float alpha) { return fmaxf(1.0f - alpha, kOneMinusFloor); }
+
 // e2 = k q(dx, dy) given kadx = k a dx; one rounding per operation
 __device__ __forceinline__ float splat_e2(float dx, float dy, float kadx, float kb2, float kc) {
     return __fmaf_rn(__fmul_rn(kc, dy), dy, __fmul_rn(dx, __fmaf_rn(kb2, dy, kadx)));
@@ -334,7 +347,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                     C[p][0] += w[p] * col.x;
                     C[p][1] += w[p] * col.y;
                     C[p][2] += w[p] * col.z;
-                    T[p] = T[p] * (1.0f - alpha);
+                    T[p] = T[p] * one_minus_alpha(alpha);
                     if (T[p] < kTermEps) {
                         live[p] = false;
                         stop[p] = c0 - start + (uint32_t)j + 1u;
@@ -674,7 +687,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
                 const bool ok = jl < stop[p] && inb[p] && e2 >= p1.y && alpha0 >= kAlphaCutoff;
                 contrib = contrib || ok;
                 const float G = ok ? G0 : 0.f, alpha = ok ? alpha0 : 0.f;
-                const float inv = rcp_approx(1.0f - alpha);
+                const float inv = rcp_approx(one_minus_alpha(alpha));
                 const float t_prior = t_rev[p] * inv;
                 const float gw = g[p][0] * col.x + g[p][1] * col.y + g[p][2] * col.z;
                 const float wgt = alpha * t_prior;

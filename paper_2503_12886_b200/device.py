@@ -565,6 +565,11 @@ class Trainer:
         self.records = torch.empty(B * N * 12, **f32)
         self.depth = torch.empty(B * N, **f32)
         self.radius = None          # optional debug output (set to a tensor to capture)
+        # checker hook (unfused raster only): called on the host between the forward
+        # raster and the adjoint; may edit pix_state (e.g. clear the L1 sign bits of
+        # pixels a parity test excludes) on the current stream
+        self.debug_before_backward = None
+        self.capture_pixels = False     # fused raster also writes pix_T / pix_state (checker)
         self.counts = torch.empty(B * N, dtype=torch.int32, device=d)
         self.nblocks = int(L.load().hs_scan_blocks(B * N))
         self.block_sums = torch.empty(self.nblocks, dtype=torch.int32, device=d)
@@ -773,8 +778,9 @@ class Trainer:
                     kernels = 1                 # (the order was counted in _tile_order)
             self._call("raster", "hs_raster_train", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), _p(self.visited), _p(self.maxw),
-                       _p(self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale), _p(self.g_splat), None,
-                       None, s, kernels=kernels)
+                       _p(self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale), _p(self.g_splat),
+                       _p(self.pix_T) if self.capture_pixels else None,
+                       _p(self.pix_state) if self.capture_pixels else None, s, kernels=kernels)
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the rest of the backward
             # the loss is only read after the step: reduce it on the side stream
@@ -797,6 +803,8 @@ class Trainer:
                 self._color_collectives()   # on the comm stream, overlapping the backward
             self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
                        _p(self.loss_out), s, kernels=2)
+            if self.debug_before_backward is not None:
+                self.debug_before_backward(self)
             self._call("raster_bwd", "hs_raster_bwd", B, N, self.W, self.H, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(self.pix_T), _p(self.pix_state), None,
                        ctypes.c_float(grad_scale), _p(self.g_splat), s)

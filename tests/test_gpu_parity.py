@@ -77,23 +77,10 @@ def record_fields(dev, b=0):
 
 
 def flip_mask(splats, order, bbox, h, w):
-    """Pixels where an oracle decision (alpha cutoff / qmax) is within fp32 noise."""
-    mask = np.zeros((h, w), bool)
-    py, px = np.mgrid[0:h, 0:w]
-    for s in order:
-        r0, r1, c0, c1 = bbox[s]
-        if r0 > r1 or c0 > c1:
-            continue
-        inb = (py >= r0) & (py <= r1) & (px >= c0) & (px <= c1)
-        dx = px + 0.5 - splats.mean2d[s, 0]
-        dy = py + 0.5 - splats.mean2d[s, 1]
-        a, b, c = splats.conic[s]
-        q = a * dx * dx + 2 * b * dx * dy + c * dy * dy
-        op = splats.opacity[s]
-        alpha = op * np.exp(-0.5 * q)
-        qmax = 2.0 * np.log(op * 255.0)
-        mask |= inb & ((np.abs(alpha - 1 / 255.0) < 2e-6) | (np.abs(q - qmax) < 1e-4))
-    return mask
+    """Pixels where an oracle decision (alpha cutoff / qmax / alpha -> 1 / termination)
+    is within fp32 noise (oracle.flip_mask)."""
+    cam = type("Hw", (), {"height": h, "width": w})()
+    return O.flip_mask(splats, cam, order=order, bbox=bbox)
 
 
 def oracle_from_device(sp_dev, dev, world, cam):
@@ -256,8 +243,31 @@ def test_rasterize_matches_oracle():
     assert flips <= 3
 
 
+def _touching(splats, bbox, mask):
+    """Per kept splat: does a masked pixel lie inside its integer bbox and its
+    alpha >= 1/255 ellipse (q <= qmax, plus a margin)?"""
+    out = np.zeros(len(bbox), bool)
+    if not mask.any():
+        return out
+    ys, xs = np.nonzero(mask)
+    for s, (r0, r1, c0, c1) in enumerate(bbox):
+        inb = (ys >= r0) & (ys <= r1) & (xs >= c0) & (xs <= c1)
+        if not inb.any():
+            continue
+        dx = xs[inb] + 0.5 - splats.mean2d[s, 0]
+        dy = ys[inb] + 0.5 - splats.mean2d[s, 1]
+        a, b, c = splats.conic[s]
+        q = a * dx * dx + 2 * b * dx * dy + c * dy * dy
+        out[s] = np.any(q <= 2.0 * np.log(splats.opacity[s] * 255.0) + 1e-3)
+    return out
+
+
 def test_weight_sums_and_estimate_colors():
+    """Every non-empty scene is compared; splats whose bbox holds a flip-masked pixel
+    are excluded (their weight sums legitimately differ by one alpha ~ 1/255 term) and
+    counted."""
     from paper_2503_12886_b200 import compat as C
+    compared = excluded = scenes_done = 0
     for s, p, d, world, cam in scenes():
         sp = C.preprocess(world, cam)
         if len(sp) == 0:
@@ -269,28 +279,39 @@ def test_weight_sums_and_estimate_colors():
         osp, order, bbox = oracle_from_device(sp, sp._dev["batch"], world, cam)
         _, oaux = O.rasterize(osp, cam, bg, order=order, bbox=bbox)
         onum, oden = O.splat_weight_sums(oaux, target)
-        if flip_mask(osp, order, bbox, cam.height, cam.width).any():
-            continue
-        np.testing.assert_allclose(den, oden, rtol=1e-4, atol=1e-5)
-        np.testing.assert_allclose(num, onum, rtol=1e-4, atol=1e-5)
+        mask = flip_mask(osp, order, bbox, cam.height, cam.width)
+        keep = np.ones(world.count, bool)
+        keep[osp.index[_touching(osp, bbox, mask)]] = False
+        compared += int(keep[osp.index].sum())
+        excluded += int((~keep[osp.index]).sum())
+        scenes_done += 1
+        np.testing.assert_allclose(den[keep], oden[keep], rtol=1e-4, atol=1e-5)
+        np.testing.assert_allclose(num[keep], onum[keep], rtol=1e-4, atol=1e-5)
         est, eligible = C.estimate_colors(aux, target, 0.1)
         oest, oelig = O.estimate_colors(oaux, target, 0.1)
-        assert np.array_equal(eligible, oelig)
-        np.testing.assert_allclose(est[eligible], oest[eligible], rtol=1e-4, atol=1e-5)
+        assert np.array_equal(eligible[keep], oelig[keep])
+        e = eligible & keep
+        np.testing.assert_allclose(est[e], oest[e], rtol=1e-4, atol=1e-5)
+    print(f"weight sums: {scenes_done} scenes, {compared} splats compared, {excluded} excluded")
+    assert scenes_done >= 5
+    assert excluded <= 0.25 * compared
 
 
 def test_render_backward_matches_oracle():
+    """Every non-empty scene: the image gradient is zeroed on the flip-masked pixels on
+    both sides, so every gradient entry is compared (rel 1e-3, floor 1e-6 max|g|)."""
     from paper_2503_12886_b200 import compat as C
+    scenes_done = masked = 0
     for s, p, d, world, cam in scenes():
         sp = C.preprocess(world, cam)
         if len(sp) == 0:
             continue
         bg = f32(d[p + "bg"])
-        gimg = f32(d[p + "grad_image"])
         _, aux = C.rasterize(sp, cam, bg)
         osp, order, bbox = oracle_from_device(sp, sp._dev["batch"], world, cam)
-        if flip_mask(osp, order, bbox, cam.height, cam.width).any():
-            continue
+        mask = flip_mask(osp, order, bbox, cam.height, cam.width)
+        masked += int(mask.sum())
+        gimg = f32(d[p + "grad_image"]) * ~mask[:, :, None]
         _, oaux = O.rasterize(osp, cam, bg, order=order, bbox=bbox)
         # splat-space adjoint (S/render.py:276-336)
         gs = C.splat_space_grads(aux, gimg)[sp.index]
@@ -303,7 +324,10 @@ def test_render_backward_matches_oracle():
         g = C.render_backward(sp, aux, gimg)
         og = O.render_backward(osp, oaux, gimg)
         for a in ATTRS:
-            assert rel_err(getattr(g, a), getattr(og, a)) < 2e-3, (s, a)
+            assert rel_err(getattr(g, a), getattr(og, a)) < 1e-3, (s, a, rel_err(getattr(g, a), getattr(og, a)))
+        scenes_done += 1
+    print(f"render backward: {scenes_done} scenes, {masked} masked pixels")
+    assert scenes_done >= 5
 
 
 # ---------------------------------------------------------------- model ops
