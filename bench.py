@@ -158,7 +158,7 @@ CONFIGS = {
 
 def make_trainer(cfg, rank=0, world=1, pg=None):
     import torch
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     wl = synth.make_workload(cfg["uv"], cfg["batch"], cfg["size"], distinct_frames=min(cfg["batch"], 8),
                              frames_seed=1 + rank)
@@ -183,7 +183,7 @@ def cpu_reference_step_fn(cfg, frames_per_step, workers):
     """The oracle port's train_step on a bounded sample of the workload (host cores)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     wl = synth.make_workload(cfg["uv"], frames_per_step, cfg["size"], distinct_frames=frames_per_step)
     av = wl.avatar
     f = lambda a: np.asarray(a, np.float32).astype(np.float64)
@@ -402,7 +402,7 @@ def cpu_baseline(cfg, args):
 def render_fps(args):
     """Render-only FPS (BASELINE configs[2]: 100,489 Gaussians, 512^2, batch 64), device-resident."""
     import torch
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     wl = synth.make_workload(317, 64, 512, distinct_frames=8)
     av = wl.avatar
@@ -436,7 +436,7 @@ def online_rate(args, frames=120, steps=200):
     eta 0.7): optimisation steps/s on device-resident frame pools and the ingestion
     rate that sustains 25 steps per arriving frame (S/stream.py run_online)."""
     import torch
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     from paper_2503_12886_b200.online import OnlineConfig, OnlineTrainer
     wl = synth.make_workload(224, frames, 512, distinct_frames=frames)

@@ -1,4 +1,5 @@
-"""Host-side synthetic workload: the head rig, UV binding, mesh frames and avatar init.
+"""BENCH / TEST SUPPORT (not the product): host-side synthetic workload -- the head rig,
+UV binding, mesh frames and avatar init.
 
 These are the data producers on either side of the hot path (SURVEY §8f #2 marks
 the device rig as "next"; today they run once per frame on the host, cached,
@@ -20,28 +21,12 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from paper_2503_12886_b200.io import Rig
+
 # ------------------------------------------------------------------------ rig
 
 
-@dataclass
-class HeadRig:
-    base_vertices: np.ndarray   # (V, 3)
-    faces: np.ndarray           # (F, 3)
-    uv_coords: np.ndarray       # (V, 2)
-    expr_bases: np.ndarray      # (E, V, 3)
-    pose_dim: int = 3
-
-    @property
-    def num_faces(self):
-        return self.faces.shape[0]
-
-    @property
-    def num_expressions(self):
-        return self.expr_bases.shape[0]
-
-    @property
-    def param_dim(self):
-        return self.num_expressions + self.pose_dim
+HeadRig = Rig     # the rig container of the product's io module
 
 
 def build_head_rig(rows=16, cols=32, num_expressions=10, seed=7) -> HeadRig:

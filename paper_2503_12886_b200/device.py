@@ -199,7 +199,7 @@ class DeviceRig:
     rig_evaluate (S/rig.py:57-66) + mesh_frames (S/binding.py:67-115).
 
     ``rig`` is any object with base_vertices (V,3), faces (F,3), uv_coords (V,2) and
-    expr_bases (E,V,3) -- the reference's rig or synth.HeadRig."""
+    expr_bases (E,V,3) -- the reference's rig or io.Rig."""
 
     def __init__(self, rig, device="cuda"):
         require_cuda()

@@ -132,7 +132,7 @@ class Sequence:
     """S/dataset.py:37-57 SequenceDataset, images kept as u8 RGBA (T, H, W, 4)."""
     directory: Path
     camera: dict              # Camera.to_dict() fields
-    rig: object               # synth.HeadRig
+    rig: object               # Rig
     thetas: np.ndarray        # (T, H_params) float64
     images: np.ndarray        # (T, H, W, 4) uint8
 
@@ -146,9 +146,30 @@ class Sequence:
                                [c["fx"], c["fy"], c["cx"], c["cy"]]]).astype(np.float32)
 
 
+@dataclass
+class Rig:
+    """The rig arrays of S/rig.py:18-54 ParametricHeadRig (what DeviceRig consumes)."""
+    base_vertices: np.ndarray   # (V, 3)
+    faces: np.ndarray           # (F, 3)
+    uv_coords: np.ndarray       # (V, 2)
+    expr_bases: np.ndarray      # (E, V, 3)
+    pose_dim: int = 3
+
+    @property
+    def num_faces(self):
+        return self.faces.shape[0]
+
+    @property
+    def num_expressions(self):
+        return self.expr_bases.shape[0]
+
+    @property
+    def param_dim(self):
+        return self.num_expressions + self.pose_dim
+
+
 def load_rig(path):
     """S/dataset.py:229-245."""
-    from .synth import HeadRig
     path = Path(path)
     try:
         d = json.loads(path.read_text())
@@ -157,7 +178,7 @@ def load_rig(path):
     for key in ("base_vertices", "faces", "uv_coords", "expr_bases"):
         if key not in d:
             raise ValueError(f"{path}: missing field {key!r}")
-    return HeadRig(np.asarray(d["base_vertices"], np.float64), np.asarray(d["faces"], np.int64),
+    return Rig(np.asarray(d["base_vertices"], np.float64), np.asarray(d["faces"], np.int64),
                    np.asarray(d["uv_coords"], np.float64), np.asarray(d["expr_bases"], np.float64),
                    pose_dim=int(d.get("pose_dim", 3)))
 

@@ -9,7 +9,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
 import oracle as O  # noqa: E402
-from paper_2503_12886_b200 import synth  # noqa: E402
+from bench_support import synth  # noqa: E402
 from paper_2503_12886_b200.device import AvatarParams, Trainer, split_flat  # noqa: E402
 
 ATTRS = ("position", "rotation", "scale", "opacity", "color")

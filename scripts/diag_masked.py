@@ -10,7 +10,7 @@ import torch
 
 import oracle as O
 from test_gpu_train import masked_step_parity
-from paper_2503_12886_b200 import synth
+from bench_support import synth
 
 uv, B, size = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (141, 4, 256)))
 wl = synth.make_workload(uv, B, size)

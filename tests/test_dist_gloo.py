@@ -45,7 +45,7 @@ def unpack(packed):
 def _workload():
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     import oracle as O
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     wl = synth.make_workload(16, 4, 32, K=3, hidden=16, seed=3)
     av = wl.avatar
     f = lambda a: np.asarray(a, np.float32).astype(np.float64)

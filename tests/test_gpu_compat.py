@@ -24,7 +24,7 @@ def _cuda():
 
 
 def _ref_state(d):
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     n = d["base0.position"].shape[0]
     base = NS(**{a: d[f"base0.{a}"].copy() for a in ATTRS})
     deltas = [NS(position=x[:3 * n].reshape(n, 3).copy(), rotation=x[3 * n:7 * n].reshape(n, 4).copy(),

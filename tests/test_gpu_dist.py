@@ -23,7 +23,7 @@ ATTRS = ("position", "rotation", "scale", "opacity", "color")
 
 def _setup(B):
     sys.path[:0] = [ROOT]
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     wl = synth.make_workload(48, B, 96, K=6, hidden=32, seed=5)
     return wl
 

@@ -23,7 +23,7 @@ def _cuda():
 
 
 def _setup(B=4, frames=14, size=96, seed=0):
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     import oracle as O
     wl = synth.make_workload(40, frames, size, distinct_frames=frames, frames_seed=seed + 1)

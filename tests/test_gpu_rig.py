@@ -104,7 +104,7 @@ def test_rig_shape_errors():
 
 def test_step_and_render_on_device_frames():
     """A Trainer holding a DeviceRig (frames=None) reproduces the step on host frames."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     import oracle as O
     wl = synth.make_workload(48, 4, 128, distinct_frames=4)
@@ -165,7 +165,7 @@ def test_compat_mesh_frames_drop_in():
 def test_step_from_host_prefetch_pipeline():
     """step_from_host with prefetch (double-buffered uploads) gives the same losses as
     uploads on demand, across a sequence of distinct batches."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     import oracle as O
     wl = synth.make_workload(40, 12, 96, distinct_frames=12)

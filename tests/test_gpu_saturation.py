@@ -129,7 +129,7 @@ def test_saturated_training_step():
     """C1 shape (19,881 Gaussians, 4 x 256^2) with every opacity logit in {15, 17, 20,
     30, 40}: two fused steps stay finite; the unfused step with the masked replay
     matches the oracle entrywise."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, Trainer, split_flat
     wl = synth.make_workload(141, 4, 256)
     av = wl.avatar

@@ -37,7 +37,7 @@ def _cuda():
 
 
 def _setup(c, seed=0):
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     wl = synth.make_workload(c["uv"], c["B"], 16, K=c["K"], hidden=c["hidden"], seed=seed,
                              distinct_frames=c["B"])
     W, H = c["W"], c["H"]

@@ -163,7 +163,7 @@ def check_masked_parity(rep, errs, tag):
 
 def test_c1_step_vs_oracle():
     """BASELINE configs[0]: every gradient entry within rel 1e-3 (floor 1e-6 max|g|)."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     wl = synth.make_workload(141, 4, 256)
     rep, errs, _ = masked_step_parity(wl, 4, 256, 256)
     check_masked_parity(rep, errs, "C1")
@@ -173,7 +173,7 @@ def test_c2_step_vs_oracle():
     """BASELINE configs[1] (the bench workload: 50,176 Gaussians, 16 x 512^2), one step,
     stage-exact replay, every gradient entry within rel 1e-3."""
     import os
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     wl = synth.make_workload(224, 16, 512)
     rep, errs, _ = masked_step_parity(wl, 16, 512, 512, workers=min(16, os.cpu_count() or 1))
     check_masked_parity(rep, errs, "C2")
@@ -181,7 +181,7 @@ def test_c2_step_vs_oracle():
 
 def test_c1_blend_mlp_stagewise():
     """blend_bwd + mlp_bwd fed the device's own per-frame g_raw (C1 sizes)."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, Trainer
     wl = synth.make_workload(141, 4, 256)
     av = wl.avatar
@@ -213,7 +213,7 @@ def test_c1_blend_mlp_stagewise():
 
 
 def test_c2_full_size_properties():
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, Trainer
     wl = synth.make_workload(224, 16, 512, distinct_frames=4)
     av = wl.avatar
@@ -255,7 +255,7 @@ def test_fused_raster_matches_separate_kernels():
     """hs_raster_train (forward + adjoint per pixel block) against hs_raster_fwd +
     hs_raster_bwd: identical losses and visited flags; gradients equal up to the
     order of the float atomics."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, Trainer
     wl = synth.make_workload(64, 4, 192, distinct_frames=4)
     av = wl.avatar
@@ -287,7 +287,7 @@ def test_tile_binning_matches_two_level(crowded):
     the order of the float atomics.  crowded: Gaussians inflated until some (frame,
     tile) list exceeds hs_tile_sort_cap(), so the tile-major binner takes its
     two-level fallback inside the step."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, Trainer, tile_sort_cap
     uv, size = (140, 64) if crowded else (64, 192)
     wl = synth.make_workload(uv, 4, size, distinct_frames=4)
@@ -325,7 +325,7 @@ def test_fused_raster_pixels_and_grads_c2():
     separate adjoint entrywise (rel 1e-4, floor 1e-6 max|g|: float-atomic order only).
     With test_c2_step_vs_oracle (separate kernels vs the oracle) this pins the fused
     kernel to the oracle."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, Trainer
     wl = synth.make_workload(224, 16, 512)
     av = wl.avatar
@@ -357,7 +357,7 @@ def test_c3_render_vs_oracle():
     images against the oracle's own float64 forward (map_params -> blend -> activate
     -> transform -> project -> composite) in the device's order and bbox, on 4 of the
     64 frames: max-abs 1e-4 outside the flip-masked pixels."""
-    from paper_2503_12886_b200 import synth
+    from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, Trainer
     B = 64
     wl = synth.make_workload(317, B, 512, distinct_frames=B)

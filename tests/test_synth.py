@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN, golden
-from paper_2503_12886_b200 import synth
+from bench_support import synth
 
 
 def test_rig_matches_reference():
