@@ -29,7 +29,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -56,7 +55,10 @@ def load_peaks():
 # ------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.  nvidia-smi
+    writes its samples to a file (-f) from its own process: no reader thread in the
+    benchmark process (a Python thread would contend for the GIL with the host-side
+    kernel enqueue of the timed steps)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -65,21 +67,18 @@ class ClockSampler:
     def __init__(self, gpu_index=0):
         self.gpu = gpu_index
         self.proc = None
-        self.lines = []
+        self.path = None
 
     def start(self):
+        import tempfile
         try:
+            fd, self.path = tempfile.mkstemp(prefix="hs_clocks_", suffix=".csv")
+            os.close(fd)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "10"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                          "--format=csv,noheader,nounits", "-lms", "20", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def stop(self):
         if self.proc is None:
@@ -89,9 +88,15 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        try:
+            with open(self.path) as f:
+                lines = f.read().splitlines()
+            os.unlink(self.path)
+        except Exception:
+            lines = []
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -152,22 +157,33 @@ def mufu_bound(keys_per_image, sm_mhz, value):
 CONFIGS = {
     "C1": dict(uv=141, batch=4, size=256, desc="synthetic head avatar: 20 bases, 19,881 Gaussians, 256x256, batch 4"),
     "C2": dict(uv=224, batch=16, size=512, desc="paper default: 20 bases, 50,176 Gaussians, 512x512, batch 16"),
-    "C4": dict(uv=317, batch=16, size=512, desc="batch-sharded: 20 bases, 100,489 Gaussians, 512x512, 16/GPU"),
+    # BASELINE configs[3]: global batch 128 split over the ranks (strong scaling)
+    "C4": dict(uv=317, global_batch=128, size=512,
+               desc="batch-sharded training: 20 bases, 100,489 Gaussians, 512x512, global batch 128"),
 }
+
+
+def per_rank_batch(cfg, world):
+    if "batch" in cfg:
+        return cfg["batch"], cfg["batch"] * world, "weak"
+    gb = cfg["global_batch"]
+    if gb % world:
+        raise SystemExit(f"global batch {gb} does not split over {world} ranks")
+    return gb // world, gb, "strong"
 
 
 def make_trainer(cfg, rank=0, world=1, pg=None):
     import torch
     from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
-    wl = synth.make_workload(cfg["uv"], cfg["batch"], cfg["size"], distinct_frames=min(cfg["batch"], 8),
-                             frames_seed=1 + rank)
+    B, GB, _ = per_rank_batch(cfg, world)
+    # theta ~ N(0, 0.3) per frame: every frame of every rank distinct
+    wl = synth.make_workload(cfg["uv"], B, cfg["size"], frames_seed=1 + rank)
     av = wl.avatar
     dev = AvatarParams.from_host(type("G", (), {a: av.base[a] for a in av.base})(), av.deltas, av.mlp,
                                  av.tri_index, av.barycentric)
-    B = cfg["batch"]
     # mesh frames come from theta on the device (hs_rig_frames) inside every step
-    tr = Trainer(dev, cfg["size"], cfg["size"], B, process_group=pg, global_batch=B * world, frame_offset=B * rank,
+    tr = Trainer(dev, cfg["size"], cfg["size"], B, process_group=pg, global_batch=GB, frame_offset=B * rank,
                  rig=DeviceRig(wl.rig))
     d = {
         "thetas": torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda(),
@@ -179,12 +195,16 @@ def make_trainer(cfg, rank=0, world=1, pg=None):
     return tr, d, wl
 
 
-def cpu_reference_step_fn(cfg, frames_per_step, workers):
-    """The oracle port's train_step on a bounded sample of the workload (host cores)."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def port_step_fn(cfg, frames_per_step, workers):
+    """The oracle port (float64 C restatement under oracle/) of train_step on a
+    bounded sample of the workload (host cores)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     from bench_support import synth
-    wl = synth.make_workload(cfg["uv"], frames_per_step, cfg["size"], distinct_frames=frames_per_step)
+    wl = synth.make_workload(cfg["uv"], frames_per_step, cfg["size"])
     av = wl.avatar
     f = lambda a: np.asarray(a, np.float32).astype(np.float64)
     model = O.Model(O.GSet(*(f(av.base[a]) for a in ("position", "rotation", "scale", "opacity", "color"))),
@@ -198,7 +218,77 @@ def cpu_reference_step_fn(cfg, frames_per_step, workers):
 
     def step():
         O.train_step(state, wl.thetas, images, frames, wl.backgrounds)
-    return step, state
+    return step, state.close
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "headsplat"))
+
+
+def reference_step_fn(cfg, frames_per_step, workers):
+    """The reference package's own train_step (S/train.py:214-260: numpy + numba,
+    BatchRenderer two-stage schedule on ``workers`` threads) from baseline/_ref, on the
+    same synthetic avatar (identical bindings, perturbations, theta, targets and
+    backgrounds as the device arm's workload), mesh frames cached per sample like
+    SequenceDataset.mesh_for (S/dataset.py:54-57)."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "hs_numba_cache"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from headsplat.binding import mesh_frames
+    from headsplat.color_init import ColorInitState
+    from headsplat.dataset import FrameSample
+    from headsplat.render import Camera
+    from headsplat.rig import build_head_rig, rig_evaluate
+    from headsplat.scheduler import BatchRenderer
+    from headsplat.train import Optimizer, TrainConfig, TrainState, init_avatar, train_step
+    from bench_support import synth
+    wl = synth.make_workload(cfg["uv"], frames_per_step, cfg["size"])
+    av = wl.avatar
+    rig = build_head_rig()
+    tcfg = TrainConfig(uv_resolution=cfg["uv"], num_blendshapes=av.K, batch_size=frames_per_step, workers=workers)
+    model = init_avatar(rig, tcfg)
+    n = model.count
+    if n != av.count:
+        raise RuntimeError(f"reference binding count {n} != workload {av.count}")
+    for a in ("position", "rotation", "scale", "opacity", "color"):
+        getattr(model.base, a)[...] = np.asarray(av.base[a], np.float64).reshape(getattr(model.base, a).shape)
+    for k, dl in enumerate(model.deltas):
+        row = np.asarray(av.deltas[k], np.float64)
+        dl.position[...] = row[:3 * n].reshape(n, 3)
+        dl.rotation[...] = row[3 * n:7 * n].reshape(n, 4)
+        dl.color[...] = row[7 * n:].reshape(n, 3)
+    for k in ("w1", "b1", "w2", "b2", "w3", "b3"):
+        getattr(model.mlp, k)[...] = np.asarray(av.mlp[k], np.float64)
+    cam = Camera.frontal(cfg["size"])
+    samples = [FrameSample(i + 1, wl.targets[i].astype(np.float64) / 255.0, np.asarray(wl.thetas[i], np.float64))
+               for i in range(frames_per_step)]
+
+    def mesh_of(sample):
+        if sample.mesh is None:
+            sample.mesh = mesh_frames(rig, rig_evaluate(rig, sample.theta))
+        return sample.mesh
+    renderer = BatchRenderer(workers)
+    state = TrainState(model, Optimizer(model, tcfg), renderer, ColorInitState.create(n, 0.1), tcfg, cam)
+    bgs = np.asarray(wl.backgrounds, np.float64)
+
+    def step():
+        train_step(state, samples, bgs, mesh_of)
+    return step, renderer.close
+
+
+def time_cpu(step_fn, cfg, frames, cores, warmup, steps):
+    step, close = step_fn(cfg, frames, cores)
+    try:
+        for _ in range(warmup):
+            step()
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            step()
+            times.append(time.perf_counter() - t0)
+    finally:
+        close()
+    return statistics.median(times), times
 
 
 def host_cores():
@@ -208,30 +298,36 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_frames(cfg, world=1):
+    """Frames per reference step: the config's per-GPU batch (the whole C2 step),
+    capped at 16 so a step stays a bounded sample."""
+    b, _, _ = per_rank_batch(cfg, world)
+    return min(b, 16)
+
+
 def run_reference(args, cfg):
+    """--impl reference: the reference's own CPU train_step (baseline/_ref, numba) on the
+    host cores, rank 0 only; the oracle port when baseline/_ref is absent."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cores = host_cores()
-    fps = max(1, min(cfg["batch"], cores))
-    step, state = cpu_reference_step_fn(cfg, fps, cores)
-    for _ in range(min(args.warmup, 1)):
-        step()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t0)
-    state.close()
-    ms = 1000.0 * statistics.median(times)
-    value = fps / (ms / 1000.0)
-    sample = (f"oracle train_step (float64 C port of headsplat, oracle/) on {fps} frames of the "
-              f"{args.config} workload per step, {cores} threads, median of {args.steps}")
+    fps = cpu_frames(cfg)
+    kind = "reference" if reference_available() else "port"
+    fn = reference_step_fn if kind == "reference" else port_step_fn
+    # the first reference call JIT-compiles the numba kernels: one extra untimed step
+    med, _ = time_cpu(fn, cfg, fps, cores, max(1, min(args.warmup, 2)), args.steps)
+    ms = 1000.0 * med
+    value = fps / med
+    what = ("headsplat train_step (the reference package itself, numpy + numba, baseline/_ref)" if kind == "reference"
+            else "oracle train_step (float64 C port of headsplat, oracle/; baseline/_ref missing)")
+    sample = (f"{what} on {fps} frames of the {args.config} workload per step, BatchRenderer with {cores} "
+              f"workers, median of {args.steps} steps after warm-up")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": per_rank_batch(cfg, 1)[2], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "frames_per_step": fps},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -250,13 +346,15 @@ def run_b200(args, cfg):
     torch.cuda.set_device(dev_index)
     pg = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator / NVLS lines on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
         else:
             dist.init_process_group(backend)
         pg = dist.group.WORLD
     tr, d, wl = make_trainer(cfg, rank, world, pg)
-    B = cfg["batch"]
+    B, GB, scaling = per_rank_batch(cfg, world)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
@@ -347,10 +445,11 @@ def run_b200(args, cfg):
         step_bytes = sum(sb.values())
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "gaussians": av.N, "blendshapes": av.K, "image": tr.W,
-                       "frames_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world}",
+                       "frames_per_gpu": B, "global_batch": GB, "parallelism": f"dp{world}",
+                       "backend": backend if world > 1 else None,
                        "l2": "inputs larger than L2: each step touches ~0.4 GB (> 126 MB L2); the K steps are timed "
                              "back to back",
                        "keys_per_step": tr.last_total, "colour_init": "active (unvisited Gaussians)",
@@ -374,10 +473,17 @@ def run_b200(args, cfg):
             "gpu_launches": launches,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg, args)
+            line["cpu_baseline"], port = cpu_baseline(cfg, args)
+            if port is not None:
+                line["cpu_port"] = port
         if world == 1 and not args.no_render:
             line["render"] = render_fps(args)
-            line["online"] = online_rate(args)
+            line["e2e_compat"] = compat_e2e(cfg, min(args.steps, 20))
+    if not args.no_render:
+        online = online_rate(args, rank=rank, world=world, pg=pg)
+        if rank == 0:
+            line["online"] = online
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -386,17 +492,65 @@ def run_b200(args, cfg):
 
 
 def cpu_baseline(cfg, args):
+    """The reference's own train_step (baseline/_ref) on the box's host cores: median
+    of 3 steps after one warm-up step (which also JIT-compiles the numba kernels), on
+    the config's whole per-GPU frame batch; the oracle port beside it."""
     cores = host_cores()
-    fps = max(1, min(4, cores))
-    step, state = cpu_reference_step_fn(cfg, fps, cores)
+    fps = cpu_frames(cfg)
+    out = {}
+    if reference_available():
+        med, ts = time_cpu(reference_step_fn, cfg, fps, cores, 1, 3)
+        out = {"value": fps / med, "unit": UNIT, "cores": cores, "kind": "reference",
+               "sample": f"headsplat train_step (baseline/_ref, numpy + numba) on {fps} frames of the {args.config} "
+                         f"workload, BatchRenderer with {cores} workers: median of 3 steps after 1 warm-up "
+                         f"({', '.join(f'{t:.2f}' for t in ts)} s)"}
+    med, ts = time_cpu(port_step_fn, cfg, fps, cores, 1, 3)
+    port = {"value": fps / med, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle train_step (float64 C port, oracle/) on {fps} frames of the {args.config} workload, "
+                      f"{cores} threads: median of 3 steps after 1 warm-up ({', '.join(f'{t:.2f}' for t in ts)} s)"}
+    if not out:
+        return port, None
+    return out, port
+
+
+def compat_e2e(cfg, steps):
+    """images/s through compat.train_step -- the drop-in for S/train.py:214 with the
+    reference's own argument types: FrameSample-like items holding float64 RGBA images,
+    cached MeshFrames, float64 backgrounds, and the updated parameters written back into
+    the caller's float64 model every step (wall clock, K steps after 2 warm-up)."""
+    from types import SimpleNamespace as NS
+    from bench_support import synth
+    from paper_2503_12886_b200 import compat
+    B, _, _ = per_rank_batch(cfg, 1)
+    wl = synth.make_workload(cfg["uv"], B, cfg["size"])
+    av = wl.avatar
+    n = av.count
+    f64 = lambda a: np.array(a, np.float64)
+    base = NS(**{a: f64(av.base[a]) for a in ("position", "rotation", "scale", "opacity", "color")})
+    deltas = [NS(position=f64(x[:3 * n].reshape(n, 3)), rotation=f64(x[3 * n:7 * n].reshape(n, 4)),
+                 color=f64(x[7 * n:].reshape(n, 3))) for x in av.deltas]
+    mlp = NS(**{k: f64(v) for k, v in av.mlp.items()})
+    model = NS(base=base, deltas=deltas, mlp=mlp,
+               bindings=NS(triangle_index=av.tri_index, barycentric=f64(av.barycentric)))
+    tcfg = NS(lr_position=0.0008, lr_opacity=0.25, lr_scale=0.025, lr_rotation=0.005, lr_color=0.0125,
+              delta_position_scale=0.05, delta_rotation_scale=0.5, delta_color_scale=0.5, lr_mlp=0.001,
+              color_init=True, use_mlp=True)
+    state = NS(model=model, config=tcfg, camera=wl.camera, color_state=NS(visited=np.zeros(n, bool), threshold=0.1))
+    samples = [NS(index=i + 1, image=wl.targets[i].astype(np.float64) / 255.0, theta=f64(wl.thetas[i]), mesh=None)
+               for i in range(B)]
+    meshes = list(wl.mesh)
+    mesh_of = lambda smp: meshes[smp.index - 1]
+    bgs = np.asarray(wl.backgrounds, np.float64)
+    for _ in range(2):
+        compat.train_step(state, samples, bgs, mesh_of)
     t0 = time.perf_counter()
-    step()
-    t1 = time.perf_counter()
-    state.close()
-    v = fps / (t1 - t0)
-    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"one oracle train_step (float64 C port, oracle/) on {fps} frames of the {args.config} "
-                      f"workload, {cores} threads: {t1 - t0:.2f} s"}
+    for _ in range(steps):
+        compat.train_step(state, samples, bgs, mesh_of)
+    dt = time.perf_counter() - t0
+    return {"value": B * steps / dt, "unit": UNIT, "ms_per_step": 1000.0 * dt / steps,
+            "path": "compat.train_step (reference signature; float64 model written back each step)",
+            "d2h_bytes_per_step": 4 * (14 * n + 10 * av.K * n) + 4 * int(sum(np.size(v) for v in av.mlp.values()))
+            + n}
 
 
 def render_fps(args):
@@ -431,36 +585,74 @@ def render_fps(args):
             "keys_per_batch": tr.last_total}
 
 
-def online_rate(args, frames=120, steps=200):
-    """Online stream (BASELINE configs[4] per GPU: 10 frames/step, 512^2, pools 150 / 1000,
-    eta 0.7): optimisation steps/s on device-resident frame pools and the ingestion
-    rate that sustains 25 steps per arriving frame (S/stream.py run_online)."""
+def online_rate(args, frames=120, steps=200, rank=0, world=1, pg=None):
+    """Online stream (BASELINE configs[4]: 10 frames/step per GPU, 512^2, pools 150 /
+    1000, eta 0.7): optimisation steps/s on device-resident frame pools and the
+    ingestion rate that sustains 25 steps per arriving frame (S/stream.py run_online).
+    On N ranks every rank ingests the stream and trains on its slice of the same global
+    draw of 10 N frames (OnlineTrainer, sharded draws); the time is the max over ranks."""
     import torch
     from bench_support import synth
     from paper_2503_12886_b200.device import AvatarParams, DeviceRig, Trainer
     from paper_2503_12886_b200.online import OnlineConfig, OnlineTrainer
-    wl = synth.make_workload(224, frames, 512, distinct_frames=frames)
+    B = 10
+    wl = synth.make_workload(224, frames, 512)
     av = wl.avatar
     dev = AvatarParams.from_host(type("G", (), {a: av.base[a] for a in av.base})(), av.deltas, av.mlp,
                                  av.tri_index, av.barycentric)
-    tr = Trainer(dev, 512, 512, 10, rig=DeviceRig(wl.rig))
-    cfg = OnlineConfig(batch_size=10, steps_per_frame=0, check_every=10_000)
+    tr = Trainer(dev, 512, 512, B, process_group=pg, global_batch=B * world, frame_offset=B * rank,
+                 rig=DeviceRig(wl.rig))
+    cfg = OnlineConfig(batch_size=B * world, steps_per_frame=0, check_every=10_000)
     on = OnlineTrainer(tr, wl.camera.packed(), cfg)
     for i in range(frames):
         on.ingest(i + 1, wl.targets[i], wl.thetas[i])
     for _ in range(5):
         on.optimize_once()
     torch.cuda.synchronize()
+    if pg is not None:
+        torch.distributed.barrier(group=pg)
     t0 = time.perf_counter()
     for _ in range(steps):
         on.optimize_once()
     on.flush()
+    torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    if pg is not None:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=pg)
+        dt = float(t.item())
     sps = steps / dt
-    return {"metric": "online optimisation steps/s (device frame pools, 10 frames/step, 512^2, 50,176 Gaussians)",
-            "value": sps, "unit": "steps/s", "ms_per_step": 1000.0 / sps,
+    return {"metric": f"online optimisation steps/s (device frame pools, {B} frames/step per GPU, global batch "
+                      f"{B * world}, 512^2, 50,176 Gaussians)",
+            "value": sps, "unit": "steps/s", "ms_per_step": 1000.0 / sps, "n_gpus": world,
+            "training_frames_per_s": sps * B * world,
             "sustained_ingest_fps_at_25_steps_per_frame": sps / 25.0,
-            "pooled_frames": frames, "timing": "host wall clock incl. draws, gathers and the per-step sync"}
+            "pooled_frames": frames,
+            "timing": "host wall clock incl. draws, gathers and the per-step sync (max over ranks)"}
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: re-run this script under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous); rank 0 prints the
+    line.  NCCL needs one GPU per rank; HS_BENCH_BACKEND=gloo lets N ranks share fewer
+    GPUs (host-mediated allreduce) to exercise the multi-rank path."""
+    import socket
+    import torch
+    backend = os.environ.get("HS_BENCH_BACKEND", "nccl")
+    ngpu = torch.cuda.device_count()
+    if backend == "nccl" and ngpu < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} GPUs for NCCL, "
+                          f"{ngpu} visible (HS_BENCH_BACKEND=gloo shares one GPU between ranks)"}), flush=True)
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -474,8 +666,13 @@ def main():
     ap.add_argument("--no-render", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     return run_b200(args, cfg)
 
 

@@ -168,14 +168,15 @@ class AvatarParams:
     def host_flat(self) -> np.ndarray:
         return self.params.detach().cpu().numpy()
 
-    def split_host(self, flat=None):
-        """(base dict, deltas (K,10N), mlp dict) float64 numpy from the device copy."""
+    def split_host(self, flat=None, dtype=np.float64):
+        """(base dict, deltas (K,10N), mlp dict) numpy (float64, or views of ``flat``
+        with dtype=None) from the device copy."""
         flat = self.host_flat() if flat is None else flat
-        return split_flat(flat, self.N, self.K, self.H, self.D)
+        return split_flat(flat, self.N, self.K, self.H, self.D, dtype)
 
 
-def split_flat(flat, N, K, H, D):
-    flat = np.asarray(flat, np.float64)
+def split_flat(flat, N, K, H, D, dtype=np.float64):
+    flat = np.asarray(flat, dtype)
     n = N
     base = {"position": flat[0:3 * n].reshape(n, 3), "rotation": flat[3 * n:7 * n].reshape(n, 4),
             "color": flat[7 * n:10 * n].reshape(n, 3), "scale": flat[10 * n:13 * n].reshape(n, 3),
@@ -1049,6 +1050,11 @@ class Trainer:
             cur.wait_event(ev)
             d = dev["targets"]
         else:
+            if self._pending is not None:
+                # a prefetch of a different batch may still be writing (device side) into
+                # the buffer set and pinned staging this upload reuses: let it land first
+                self._pending[2].synchronize()
+                self._pending = None
             slot = self._slot
             small = {"thetas": (thetas, np.float32), "cameras": (cameras, np.float32),
                      "backgrounds": (backgrounds, np.float32)}

@@ -113,6 +113,22 @@ def sample_batch(pools: SamplePools, batch_size: int, eta: float, rng):
     return picks
 
 
+def draw_step(pools: SamplePools, cfg, rng, batch_size):
+    """One step's draws (S/stream.py:124-137): the sampled frames by the configured
+    mode, then the per-item backgrounds, from one rng."""
+    if cfg.sampling == "no_global":
+        batch = sample_batch(pools, batch_size, 1.0, rng)
+    elif cfg.sampling == "no_local":
+        if len(pools.global_pool) == 0:
+            batch = sample_batch(pools, batch_size, 1.0, rng)
+        else:
+            batch = [pools.global_pool[int(i)] for i in rng.integers(0, len(pools.global_pool), size=batch_size)]
+    else:
+        batch = sample_batch(pools, batch_size, cfg.eta, rng)
+    bgs = rng.uniform(0.0, 1.0, size=(batch_size, 3))
+    return batch, bgs
+
+
 class DeviceFramePool:
     """HBM-resident slots of (u8 RGBA image, theta); slot 0..capacity-1."""
 
@@ -168,17 +184,26 @@ class OnlineConfig:
 class OnlineTrainer:
     """run_online (S/stream.py:104-172) on one device Trainer holding a DeviceRig.
 
-    ``trainer.B`` must equal ``config.batch_size``; every step draws its batch with
-    the reference's rule and rng order (sample_batch, then the backgrounds) and
-    trains on the gathered device frames."""
+    ``trainer.global_batch`` must equal ``config.batch_size``; every step draws its
+    batch with the reference's rule and rng order (sample_batch, then the backgrounds)
+    and trains on the gathered device frames.
+
+    Data-parallel (a Trainer with a process group, SURVEY §8e / BASELINE configs[4]):
+    every rank ingests every frame into its own HBM pool and keeps identical host
+    bookkeeping (same seed, same stream), draws the same GLOBAL batch, and trains on
+    its slice [frame_offset, frame_offset + B) of it -- so the ranks together take
+    exactly the single-process step of S/stream.py:73-90 on the whole batch, with the
+    gradients summed by the Trainer's allreduce."""
 
     def __init__(self, trainer: Trainer, camera, config: OnlineConfig):
         if config.sampling not in ("full", "no_global", "no_local"):
             raise ValueError(f"unknown sampling mode {config.sampling!r}")
         if trainer.rig is None:
             raise ValueError("OnlineTrainer needs a Trainer with a DeviceRig (frames from theta)")
-        if trainer.B != config.batch_size:
-            raise ValueError(f"trainer batch {trainer.B} != config.batch_size {config.batch_size}")
+        if trainer.global_batch != config.batch_size:
+            raise ValueError(f"trainer global batch {trainer.global_batch} != config.batch_size {config.batch_size}")
+        if trainer.frame_offset % trainer.B or trainer.frame_offset + trainer.B > trainer.global_batch:
+            raise ValueError("trainer.frame_offset must be rank * trainer.B")
         self.tr = trainer
         self.cfg = config
         self.rng = np.random.default_rng(config.seed)
@@ -212,18 +237,14 @@ class OnlineTrainer:
 
     # -------------------------------------------------------------------- step
     def _draw(self):
-        cfg, pools, rng, B = self.cfg, self.pools, self.rng, self.tr.B
-        if cfg.sampling == "no_global":
-            return sample_batch(pools, B, 1.0, rng)
-        if cfg.sampling == "no_local":
-            if len(pools.global_pool) == 0:
-                return sample_batch(pools, B, 1.0, rng)
-            return [pools.global_pool[int(i)] for i in rng.integers(0, len(pools.global_pool), size=B)]
-        return sample_batch(pools, B, cfg.eta, rng)
+        """The global batch (the reference's draws, in its order), this rank's slice of
+        it and the slice's backgrounds."""
+        batch, bgs = draw_step(self.pools, self.cfg, self.rng, self.tr.global_batch)
+        lo = self.tr.frame_offset
+        return batch, batch[lo:lo + self.tr.B], bgs[lo:lo + self.tr.B]
 
     def optimize_once(self):
-        batch = self._draw()
-        bgs = self.rng.uniform(0.0, 1.0, size=(self.tr.B, 3))
+        full, batch, bgs = self._draw()
         # the slots and backgrounds of this step (B ints + 3B floats) are the only H2D bytes
         self._slots_host.numpy()[:] = [r.slot for r in batch]
         self._bg_host.numpy()[:] = bgs
@@ -232,23 +253,34 @@ class OnlineTrainer:
         self.pool.gather(self.slots, self.targets, self.thetas)
         self.tr.launches += 2
         loss = self.tr.step(self.thetas, self.targets, None, self.cameras, self.bgs)
-        self._loss_log.append((self.steps, loss.clone(), [r.index for r in batch]))
+        self._loss_log.append((self.steps, loss.clone(), [r.index for r in full]))
         self.steps += 1
         if len(self._loss_log) >= self.cfg.check_every:
             self.flush()
 
     def flush(self):
-        """Read back the queued step losses (S/stream.py:141-148 bookkeeping)."""
+        """Read back the queued step losses (S/stream.py:141-148 bookkeeping).  With a
+        process group the ranks' rows are all-gathered first, so every rank logs the
+        global batch's loss (mean of the equal-sized slices) and per-frame L1s."""
         if not self._loss_log:
             return
-        rows = torch.stack([r for _, r, _ in self._loss_log]).cpu().numpy()
+        rows = torch.stack([r for _, r, _ in self._loss_log])
         B = self.tr.B
-        for (step, _, idx), row in zip(self._loss_log, rows):
-            loss = float(row[2 * B])
+        pg = self.tr.pg
+        if pg is not None:
+            import torch.distributed as dist
+            parts = [torch.empty_like(rows) for _ in range(dist.get_world_size(pg))]
+            dist.all_gather(parts, rows, group=pg)
+        else:
+            parts = [rows]
+        parts = [p.cpu().numpy() for p in parts]
+        for j, (step, _, idx) in enumerate(self._loss_log):
+            loss = float(np.mean([p[j, 2 * B] for p in parts]))
             if not np.isfinite(loss):
                 self._loss_log = []
                 raise RuntimeError(f"non-finite loss at online step {step}")
-            for i, bl in zip(idx, row[B:2 * B]):
+            black = np.concatenate([p[j, B:2 * B] for p in parts])
+            for i, bl in zip(idx, black):
                 prev = self.min_l1.get(i)
                 if prev is None or bl < prev:
                     self.min_l1[i] = float(bl)

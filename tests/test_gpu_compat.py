@@ -85,3 +85,31 @@ def test_batch_renderer_matches_single_calls():
         img1, aux1 = compat.rasterize(compat.preprocess(world, cam), cam, bg)
         assert np.array_equal(img, img1)             # batched == per-item, bitwise
         assert np.array_equal(aux.max_weight, aux1.max_weight)
+
+
+def test_step_from_host_prefetch_then_other_batch():
+    """step_from_host(X, prefetch=B), then a different batch C, then B: every step must
+    train on its own inputs (a pending prefetch of B may not leak into C's buffers, and
+    B must be re-uploaded after C reused them) -- same losses and parameters as the
+    same steps without prefetch."""
+    from bench_support import synth
+    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    wl = synth.make_workload(48, 4, 96, K=6, hidden=32, seed=5)
+    av = wl.avatar
+    mk = lambda: Trainer(AvatarParams.from_host(NS(**{a: av.base[a] for a in ATTRS}), av.deltas, av.mlp,
+                                                av.tri_index, av.barycentric), 96, 96, 4)
+    rng = np.random.default_rng(9)
+    cams = np.tile(wl.camera.packed(), (4, 1))
+
+    def batch(k):
+        return (np.asarray(wl.thetas, np.float32) + np.float32(0.01 * k),
+                rng.integers(0, 256, wl.targets.shape, dtype=np.uint8), wl.frames, cams,
+                rng.uniform(0, 1, (4, 3)).astype(np.float32))
+    X, Bb, C = batch(0), batch(1), batch(2)
+    a, b = mk(), mk()
+    la = [a.step_from_host(*X, prefetch=Bb).loss, a.step_from_host(*C).loss, a.step_from_host(*Bb).loss]
+    lb = [b.step_from_host(*X).loss, b.step_from_host(*C).loss, b.step_from_host(*Bb).loss]
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(la, lb, rtol=1e-5)
+    pa, pb = a.av.params.cpu().numpy(), b.av.params.cpu().numpy()
+    assert np.mean(np.abs(pa - pb) > 1e-5) < 1e-3
