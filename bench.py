@@ -367,7 +367,18 @@ def run_b200(args, cfg):
 
     clocks = ClockSampler(dev_index)
     clocks.start()                      # sampled through warm-up + timed region (>= 1 s of load)
+    # warm-up: W steps (>= 3), continued until ~2 s of load so the SM clock and the
+    # caching allocator have settled (a 5-step warm-up left the first timed steps ~10 %
+    # slower than steady state)
+    t_w = time.perf_counter()
     for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    per = (time.perf_counter() - t_w) / max(args.warmup, 3)
+    extra = torch.tensor([max(0.0, (2.0 - (time.perf_counter() - t_w)) / max(per, 1e-4))], device="cuda")
+    if world > 1:                       # every rank runs the same number of steps (collectives)
+        dist.all_reduce(extra, op=dist.ReduceOp.MAX)
+    for _ in range(int(min(extra.item(), 5000))):
         step()
     barrier()
     # ---- device-resident timed region: K consecutive steps between one pair of events,

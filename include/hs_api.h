@@ -235,9 +235,11 @@ int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, voi
 
 /* ---- Raster (render.py:233-273 _composite_kernel, :339-377 _weight_sums_kernel,
  *      metrics.py:10-22 l1_loss, :80-85 composite_over, train.py:238-247) ----
- * The raster kernels are persistent and share a per-process work counter: within
- * one process, hs_raster_fwd / hs_raster_bwd launches must be ordered (same stream
- * or synchronised), not concurrent on different streams. */
+ * The raster kernels are persistent: their work counters and item order live in a
+ * caller-provided workspace of hs_raster_workspace_size(B, width, height) bytes
+ * (16-byte aligned, zero-filled once at allocation; every launch leaves the counters
+ * zeroed).  Launches on different workspaces are independent (re-entrant: several
+ * streams / devices); launches sharing one workspace must be stream-ordered. */
 enum {
     HS_RASTER_LOSS = 1,          /* fused L1 loss vs targets (u8 RGBA) composited over bg */
     HS_RASTER_IMAGE = 2,         /* write image[B,H,W,3] */
@@ -248,11 +250,13 @@ enum {
     HS_RASTER_ORDER_READY = 64   /* hs_raster_train / hs_raster_fwd: the tile order hs_raster_tile_order
                                     built for these ranges is in place (the call skips building it) */
 };
-/* The persistent raster's longest-list-first tile order for these ranges; lets a caller
- * build it off the critical path (e.g. on a side stream while the lists are sorted) and
- * pass HS_RASTER_ORDER_READY.  Shares process-wide state with the raster launches:
- * order it before the raster that uses it and after the raster that used the last one. */
-int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, int tile_bits, void *stream);
+size_t hs_raster_workspace_size(int B, int width, int height);
+/* The persistent raster's longest-list-first tile order for these ranges, written into
+ * the workspace; lets a caller build it off the critical path (e.g. on a side stream
+ * while the lists are sorted) and pass HS_RASTER_ORDER_READY to the raster that uses
+ * the same workspace (ordered after this call and after the workspace's last raster). */
+int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, int tile_bits, void *workspace,
+                         void *stream);
 /* loss_partials holds B * num_tiles * HS_LOSS_PARTIALS_PER_TILE floats (one (L1,
  * black L1) pair per pixel block of the kernel, at most 8 per tile), reduced by
  * hs_loss_reduce. */
@@ -261,14 +265,15 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const uint8_t *targets, const float *wsum_image,
                   const uint8_t *visited, float *pix_T, uint32_t *pix_state, float *image,
-                  float *maxw, float *wsums, float *loss_partials, void *stream);
+                  float *maxw, float *wsums, float *loss_partials, void *workspace, void *stream);
 /* Adjoint (render.py:276-336 _backward_kernel).  grad_image (B,H,W,3) may be NULL:
  * then the L1 gradient sign(pred - target) * grad_scale recorded by the forward is used.
  * g_splat must be zero-filled by the caller (accumulated with atomics after a warp reduce). */
 int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const float *pix_T, const uint32_t *pix_state,
-                  const float *grad_image, float grad_scale, float *g_splat, void *stream);
+                  const float *grad_image, float grad_scale, float *g_splat, void *workspace,
+                  void *stream);
 /* Training-step raster: hs_raster_fwd (HS_RASTER_LOSS plus the colour-init flags)
  * and hs_raster_bwd with the L1 gradient sign(pred - target) * grad_scale, fused per
  * pixel block -- T, stop and the gradient stay in registers and the adjoint reuses
@@ -278,7 +283,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
                     const uint32_t *values, const uint32_t *ranges, int tile_bits,
                     const float *backgrounds, const uint8_t *targets, const uint8_t *visited,
                     float *maxw, float *wsums, float *loss_partials, float grad_scale, float *g_splat,
-                    float *pix_T, uint32_t *pix_state, void *stream);
+                    float *pix_T, uint32_t *pix_state, void *workspace, void *stream);
 /* Diagnostics: raster counters accumulated when built with -DHS_RASTER_STATS (zeros
  * otherwise); synchronous copy to host_out[16]:
  *   forward [warp iterations, pixel tests, q <= qmax, alpha >= 1/255, iterations with

@@ -55,10 +55,11 @@ SIGNATURES = {
     "hs_sort_workspace_size": (_Z, [_L]),
     "hs_sort_pairs": (_I, [_L, ctypes.c_uint64, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges": (_I, [_L, _P, _P, _P]),
-    "hs_raster_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "hs_raster_bwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _F, _P, _P]),
+    "hs_raster_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_raster_bwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _F, _P, _P, _P]),
     "hs_loss_reduce": (_I, [_I, _I, _I, _I, _P, _P, _P]),
-    "hs_raster_train": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P]),
+    "hs_raster_train": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P]),
+    "hs_raster_workspace_size": (_Z, [_I, _I, _I]),
     "hs_depth_order": (_I, [_L, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "hs_bin_emit_sorted": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_sort_pairs32": (_I, [_L, ctypes.c_uint32, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
@@ -66,7 +67,7 @@ SIGNATURES = {
     "hs_tile_sort_cap": (_I, []),
     "hs_tile_cta_sort_min": (_I, []),
     "hs_tile_fill_longest": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P]),
-    "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P]),
+    "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P, _P]),
     "hs_tile_count": (_I, [_I, _L, _I, _I, _P, _P, _P, _P]),
     "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P, _P]),

@@ -353,6 +353,8 @@ def _project_batch(worlds, cameras):
     dev["binned"] = binner.bin(B, n, W, H, dev["records"], dev["depth"], dev["counts"], total)
     dev["binner"] = binner
     dev["total"] = total
+    # the persistent raster's workspace for this batch (counters zeroed once)
+    dev["raster_ws"] = torch.zeros(int(L.load().hs_raster_workspace_size(B, W, H)), dtype=torch.uint8, device=d)
     return dev
 
 
@@ -429,7 +431,7 @@ def _raster_batch(dev, backgrounds, flags=L.RASTER_IMAGE | L.RASTER_MAXW_ALL, ws
         flags |= L.RASTER_WSUMS | L.RASTER_WSUMS_IMAGE | L.RASTER_MAXW_ALL
     L.call("hs_raster_fwd", B, n, W, H, flags, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(bgs), None,
            _p(wimg), None, _p(out["pix_T"]), _p(out["pix_state"]), _p(out["image"]), _p(out["maxw"]),
-           _p(out["wsums"]), None, _stream())
+           _p(out["wsums"]), None, _p(dev["raster_ws"]), _stream())
     return out
 
 
@@ -469,7 +471,8 @@ def render_backward(splats: ProjectedSplats, aux: RenderAux, grad_image) -> Gaus
     g[b] = np.asarray(grad_image, np.float64)
     g_splat = torch.zeros(B * n * 9, dtype=torch.float32, device=_dev())
     L.call("hs_raster_bwd", B, n, W, H, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(out["bgs"]),
-           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat), _stream())
+           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat),
+           _p(dev["raster_ws"]), _stream())
     g14 = torch.empty(B * 14 * n, dtype=torch.float32, device=_dev())
     L.call("hs_project_world_bwd", B, n, _p(dev["world14"]), _p(dev["cams"]), _p(g_splat), _p(g14), _stream())
     return _unpack14(g14[b * 14 * n:(b + 1) * 14 * n].cpu().numpy(), n)
@@ -484,7 +487,8 @@ def splat_space_grads(aux: RenderAux, grad_image):
     g[b] = np.asarray(grad_image, np.float64)
     g_splat = torch.zeros(B * n * 9, dtype=torch.float32, device=_dev())
     L.call("hs_raster_bwd", B, n, W, H, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(out["bgs"]),
-           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat), _stream())
+           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat),
+           _p(dev["raster_ws"]), _stream())
     return g_splat.view(B, n, 9)[b].cpu().numpy().astype(np.float64)
 
 

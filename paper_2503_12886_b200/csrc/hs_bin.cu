@@ -529,8 +529,7 @@ static int sort_pairs_impl(const char *what, int64_t num_keys, uint64_t bit_mask
     cudaMemsetAsync(workspace, 0,
                     sizeof(uint32_t) * ((size_t)kMaxPasses * kRadix + (size_t)ps.n * tiles * kRadix), s);
     cudaMemsetAsync(counters, 0, sizeof(uint32_t) * kMaxPasses, s);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = current_sm_count();
 #ifndef HS_HIST_CTAS_PER_SM
 #define HS_HIST_CTAS_PER_SM 4
 #endif

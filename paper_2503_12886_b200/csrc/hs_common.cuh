@@ -29,6 +29,8 @@ __host__ __device__ inline unsigned long long err_code(int stage, int frame, int
 
 void set_error(const char *fmt, ...);
 int check_launch(const char *what);
+// SM count of the calling thread's current device (cached per device)
+int current_sm_count();
 
 inline unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 

@@ -23,6 +23,19 @@ void set_error(const char *fmt, ...) {
     va_end(ap);
 }
 
+int current_sm_count() {
+    static int cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (dev < 0 || dev >= 64) dev = 0;
+    int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+    if (v == 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
+    }
+    return v;
+}
+
 int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -794,8 +807,7 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
 #endif
     const bool vec = HS_BLEND_VEC4 && (E % 4 == 0) && ((uintptr_t)base14 % 16 == 0) &&
                      ((uintptr_t)deltas % 16 == 0) && ((uintptr_t)raw10 % 16 == 0);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = current_sm_count();
 #ifndef HS_BLEND_BC
 #define HS_BLEND_BC 8
 #endif
@@ -898,8 +910,7 @@ int hs_adam_fused(int64_t N, int K, int64_t mlp_size, float *params, const float
     const int ci = has_colour ? ci_mode : 0;
     const bool vec = N % 4 == 0 && begin % 4 == 0 && end % 4 == 0 && (uintptr_t)params % 16 == 0 &&
                      (uintptr_t)grads % 16 == 0 && (uintptr_t)m % 16 == 0 && (uintptr_t)v % 16 == 0;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = current_sm_count();
 #ifndef HS_ADAM_CTAS_PER_SM
 #define HS_ADAM_CTAS_PER_SM 8
 #endif

@@ -31,30 +31,30 @@
 
 namespace hs {
 
-#ifndef HS_RASTER_PX
-#define HS_RASTER_PX 2               // pixels per lane (a warp owns an 8 x 4*PX block)
-#endif
 #ifndef HS_RASTER_CTA_WARPS
-#define HS_RASTER_CTA_WARPS 1        // warps per CTA (each warp owns one 8 x 4*PX block)
+#define HS_RASTER_CTA_WARPS 1        // warps per CTA (each warp owns one 8 x 8 block)
 #endif
 #ifndef HS_RASTER_MINB
-#define HS_RASTER_MINB (56 / HS_RASTER_PX / HS_RASTER_CTA_WARPS)   // resident CTAs per SM (28 one-warp CTAs: 72 registers)
+#define HS_RASTER_MINB (28 / HS_RASTER_CTA_WARPS)   // resident CTAs per SM (28 one-warp CTAs: <= 72 registers)
 #endif
 
 #ifndef HS_RASTER_EXACT_CULL
-#define HS_RASTER_EXACT_CULL 1       // cull blocks with the exact ellipse-rectangle distance
+#define HS_RASTER_EXACT_CULL 1       // cull row groups with the exact ellipse-rectangle distance
 #endif
 #ifndef HS_RASTER_DIRECT
 #define HS_RASTER_DIRECT 5           // adjoint: up to this many contributing lanes add directly
 #endif
 
-constexpr int kPX = HS_RASTER_PX;
+// Two pixels per lane (rows r and r + 4 of one column of the warp's 8 x 8 block): the
+// pair is evaluated with sm_100a's packed FP32 (fma/mul/add.rn.f32x2 -> FFMA2 / FMUL2 /
+// FADD2), one instruction for both pixels.
+constexpr int kPX = 2;
 constexpr int kCW = HS_RASTER_CTA_WARPS;
 
 // Optional instrumentation (-DHS_RASTER_STATS): forward-pass counts of warp
 // iterations and pixel tests, read with hs_raster_stats().
 __device__ unsigned long long g_raster_stats[16];
-constexpr int kBlocks = kTile * kTile / (32 * kPX);   // 8 x 4*PX pixel blocks per tile
+constexpr int kBlocks = kTile * kTile / (32 * kPX);   // 8 x 8 pixel blocks per tile
 constexpr int kRT = 32 * kCW;                          // threads per CTA
 static_assert(kBlocks % kCW == 0, "CTA warps must divide the blocks of a tile");
 constexpr unsigned kFull = 0xffffffffu;
@@ -80,6 +80,9 @@ struct RasterArgs {
     const float *grad_image;
     float grad_scale;
     float *g_splat;
+    // persistent scheduling (caller workspace, see hs_raster_workspace_size)
+    unsigned int *work;
+    const uint32_t *tile_order;
 };
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -88,30 +91,34 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-// ---- staged splat layout (shared memory, 64 B per splat) -------------------
-//   p0: mx - 0.5, my - 0.5, k*a, 2k*b     with k = -0.5 log2(e), so that
-//       e2 = k*q = dx (k a dx + 2k b dy) + k c dy^2 and alpha = op * 2^e2;
-//       q <= qmax  <=>  e2 >= k*qmax  (k < 0)
-//   p1: k*c, k*qmax, opacity, gidx | visited << 31   (gidx = frame * N + n)
-//   p2: c_lo, c_hi, r_lo, r_hi  (the reference's pixel bbox, S/render.py:248-251)
-//   p3: colour r, g, b, 0
-// Forward and adjoint evaluate e2 / alpha with the same explicit-rounding
-// expression, so both make identical pair decisions.
+// ---- staged splat layout (shared memory, 96 B per splat) -------------------
+//   q0: nmx nmx nmy nmy        nm = 0.5 - mean: dx = px + nmx = px + 0.5 - mx
+//   q1: ka  ka  kb2 kb2        k = -0.5 log2(e): e2 = k q = dx (ka dx + kb2 dy) + kc dy^2,
+//   q2: kc  kc  nop nop          alpha = op 2^e2; nop = -op
+//   q3: ncr ncr ncg ncg        nc = -colour
+//   q4: ncb ncb kqmax gidx     q <= qmax <=> e2 >= k qmax; gidx = frame * N + n | visited << 31
+//   q5: mlo mhi kb  kb         64-bit pixel mask of the warp's 8 x 8 block (bit 32 p + lane:
+//                              pixel p of the lane) = the reference's integer bbox
+//                              (S/render.py:248-251) minus row groups the alpha >= 1/255
+//                              ellipse cannot reach; kb = kb2 / 2 for the adjoint
+// Each value a lane needs for both of its pixels is stored twice, so one LDS.128 yields
+// register pairs for the packed instructions.  Negated opacity / colour make
+// 1 - alpha an FADD2 and the weighted colour an FFMA2 with no extra negation.
+// Forward and adjoint evaluate e2 / alpha with the same explicitly rounded operations
+// (per element identical to __fmaf_rn / __fmul_rn), so both make identical decisions.
 constexpr float kK = -0.72134752044448170f;      // -0.5 * log2(e)
 constexpr float kMeanScale = -2.0f / kK;         // d q / d(k q) folded into g_mean
-constexpr int kStageBytes = 64;
+constexpr int kStageBytes = 96;
 
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
     return v;
 }
-__device__ __forceinline__ int4 lds4i(uint32_t addr) {
-    int4 v;
-    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
+__device__ __forceinline__ void sts4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d));
 }
-// 1/x for x in (0, 1] (x = 1 - alpha, alpha < 1): the MUFU reciprocal without the
+// 1/x for x in [2^-24, 1] (x = 1 - alpha floored): the MUFU reciprocal without the
 // denormal-range fix-up __fdividef adds (same result for normal x)
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
@@ -123,101 +130,123 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// 1 - alpha for the transmittance update, floored at 2^-24 (the spacing of fp32 below 1).
-// The floor only changes alpha == 1.0f exactly: fp32 rounds sigmoid(logit) to 1 above
+// 1 - alpha for the transmittance update is floored at 2^-24 (the spacing of fp32 below
+// 1).  The floor only changes alpha == 1.0f exactly: fp32 rounds sigmoid(logit) to 1 above
 // logit ~16.6 and the Gaussian to 1 at a pixel within ~1e-3 px of the mean, where the
 // reference's float64 alpha is still < 1 (its opacity saturates only near logit 36.7).
 // Unfloored, T would become exactly 0 and the adjoint's t_rev / (1 - alpha) would be
 // 0 * inf = NaN (S/render.py:318-319).  Forward and adjoint use the same floor, so
-// t_rev * rcp(one_minus_alpha) still recovers the transmittance before the splat.
+// t_rev * rcp(floored 1 - alpha) still recovers the transmittance before the splat.
 #ifndef HS_ONE_MINUS_FLOOR
 #define HS_ONE_MINUS_FLOOR 5.9604644775390625e-8f               // 2^-24 (0: the unguarded A/B build)
 #endif
 constexpr float kOneMinusFloor = HS_ONE_MINUS_FLOOR;
-__device__ __forceinline__ float one_minus_alpha(float alpha) { return fmaxf(1.0f - alpha, kOneMinusFloor); }
 
-// e2 = k q(dx, dy) given kadx = k a dx; one rounding per operation
-__device__ __forceinline__ float splat_e2(float dx, float dy, float kadx, float kb2, float kc) {
-    return __fmaf_rn(__fmul_rn(kc, dy), dy, __fmul_rn(dx, __fmaf_rn(kb2, dy, kadx)));
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+// The staged splat of slot `ad`, unpacked into register pairs.
+struct Staged {
+    float2 nmx, nmy, ka, kb2, kc, nop, ncr, ncg, ncb, kb;
+    float kq;
+    uint32_t gidx, mlo, mhi;
+};
+__device__ __forceinline__ Staged load_staged(uint32_t ad) {
+    const float4 q0 = lds4(ad), q1 = lds4(ad + 16), q2 = lds4(ad + 32), q3 = lds4(ad + 48), q4 = lds4(ad + 64),
+                 q5 = lds4(ad + 80);
+    Staged t;
+    t.nmx = f2(q0.x, q0.y);
+    t.nmy = f2(q0.z, q0.w);
+    t.ka = f2(q1.x, q1.y);
+    t.kb2 = f2(q1.z, q1.w);
+    t.kc = f2(q2.x, q2.y);
+    t.nop = f2(q2.z, q2.w);
+    t.ncr = f2(q3.x, q3.y);
+    t.ncg = f2(q3.z, q3.w);
+    t.ncb = f2(q4.x, q4.y);
+    t.kq = q4.z;
+    t.gidx = __float_as_uint(q4.w);
+    t.mlo = __float_as_uint(q5.x);
+    t.mhi = __float_as_uint(q5.y);
+    t.kb = f2(q5.z, q5.w);
+    return t;
 }
 
-// Pixels of lane l in block w of a tile: block w covers cols (w & 1) * 8 .. +7 and
-// rows (w >> 1) * 4 kPX .. +4 kPX - 1; lane l holds column l & 7 and rows
-// (l >> 3) + 4 p for p < kPX.
-__device__ __forceinline__ void pixels_of(int w, int l, int tx, int ty, int &px, int &py0) {
-    px = tx * kTile + (w & 1) * 8 + (l & 7);
-    py0 = ty * kTile + (w >> 1) * 4 * kPX + (l >> 3);
+// e2 = k q at both pixels of the lane: per element
+// __fmaf_rn(__fmul_rn(kc, dy), dy, __fmul_rn(dx, __fmaf_rn(kb2, dy, __fmul_rn(ka, dx))))
+__device__ __forceinline__ float2 splat_e2(const Staged &t, float2 fpx2, float2 fpy2, float2 &dx2, float2 &dy2) {
+    dx2 = add2(fpx2, t.nmx);
+    dy2 = add2(fpy2, t.nmy);
+    const float2 kadx = mul2(t.ka, dx2);
+    return fma2(mul2(t.kc, dy2), dy2, mul2(dx2, fma2(t.kb2, dy2, kadx)));
 }
 
-// Stage one splat record into the lane's slot.  Returns bit 0: the warp's block
-// [x0, x0+7] x [y0, y0+4 kPX-1] can hold a contributing pixel; bit 1: the splat's
-// integer bbox covers the whole block (the per-pixel bbox test can be skipped);
-// bit 2+p: row group p (every lane's p-th pixel) can hold one -- a group the splat
-// cannot reach is skipped by the whole warp.
+// Stage one splat record into the lane's slot for the warp's 8 x 8 block with origin
+// (x0, y0).  Returns true when a pixel of the block can be touched (its mask is nonzero).
 template <bool kCull = true>
-__device__ __forceinline__ uint32_t stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
+__device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
                                             uint32_t saddr) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
     const float4 A = __ldg(r), Bv = __ldg(r + 1), Cv = __ldg(r + 2);
     const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
     const int rl = unpack_lo(rows), rh = unpack_hi(rows), cl = unpack_lo(cols), ch = unpack_hi(cols);
     const float a = A.z, b = A.w, c = Bv.x, qmax = Bv.z;
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "f"(A.x - 0.5f), "f"(A.y - 0.5f),
-                 "f"(kK * a), "f"(2.0f * kK * b));
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 16), "f"(kK * c), "f"(kK * qmax),
-                 "f"(Bv.y), "f"(__uint_as_float(gflag)));
-    asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 32), "r"(cl), "r"(ch), "r"(rl), "r"(rh));
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + 48), "f"(Cv.y), "f"(Cv.z), "f"(Cv.w),
-                 "f"(0.f));
-    if (!kCull) return 0u;
-    if (!(qmax >= 0.f)) return 0u;
-    // columns of the block the reference's bbox admits
-    const int xs = max(x0, cl), xe = min(x0 + 7, ch);
-    if (xs > xe) return 0u;
-    const bool full = cl <= x0 && ch >= x0 + 7 && rl <= y0 && rh >= y0 + 4 * kPX - 1;
-    const float det = a * c - b * b;
-    const bool exact = HS_RASTER_EXACT_CULL && det > 0.f && a > 0.f && c > 0.f;
-    const float dxlo = (float)xs + 0.5f - A.x, dxhi = (float)xe + 0.5f - A.x;
-    const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
-    const float dyv0 = __fdividef(-b * dxv, c);                 // (margin covers the approx.)
-    uint32_t groups = 0u;
+    const float nmx = 0.5f - A.x, nmy = 0.5f - A.y, ka = kK * a, kb2 = 2.0f * kK * b, kb = kK * b, kc = kK * c;
+    // the block's pixels inside the reference's bbox
+    const int cs = max(cl - x0, 0), ce = min(ch - x0, 7), rs = max(rl - y0, 0), re = min(rh - y0, 7);
+    uint64_t mask = 0;
+    if (qmax >= 0.f && cs <= ce && rs <= re) {
+        const uint32_t colbits = (0xFFu >> (7 - (ce - cs))) << cs;
+        const uint64_t rowsp = (0x0101010101010101ull >> (8 * (7 - (re - rs)))) << (8 * rs);
+        mask = rowsp * colbits;
+        if (kCull && HS_RASTER_EXACT_CULL) {
+            const float det = a * c - b * b;
+            if (det > 0.f && a > 0.f && c > 0.f) {
+                const float dxlo = (float)(x0 + cs) + 0.5f - A.x, dxhi = (float)(x0 + ce) + 0.5f - A.x;
+                const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
+                const float dyv0 = __fdividef(-b * dxv, c);                 // (margin covers the approx.)
 #pragma unroll
-    for (int p = 0; p < kPX; ++p) {
-        // row group p (the lanes' p-th pixels: rows y0 + 4p .. y0 + 4p + 3)
-        const int ys = max(y0 + 4 * p, rl), ye = min(y0 + 4 * p + 3, rh);
-        if (ys > ye) continue;
-        bool hit = true;
-        if (exact) {
-            // minimum of q(d) = a dx^2 + 2b dx dy + c dy^2 over the rectangle spanned
-            // by those pixel centres (d = centre - mean).  For a positive-definite q the
-            // minimiser is the mean if it lies inside, else on a rectangle edge facing
-            // it; the two candidate segments (x nearest the mean with the best y, and
-            // vice versa) are both inside the rectangle, so their minimum is exact.
-            const float dylo = (float)ys + 0.5f - A.y, dyhi = (float)ye + 0.5f - A.y;
-            const float dyv = fminf(fmaxf(dyv0, dylo), dyhi);
-            const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
-            const float dxh = fminf(fmaxf(__fdividef(-b * dyh, a), dxlo), dxhi);
-            const float qv = a * dxv * dxv + 2.f * b * dxv * dyv + c * dyv * dyv;
-            const float qh = a * dxh * dxh + 2.f * b * dxh * dyh + c * dyh * dyh;
-            // margin for the fp32 rounding of this bound and of the per-pixel q
-            hit = !(fminf(qv, qh) * 0.999f - 1e-3f > qmax);
+                for (int p = 0; p < kPX; ++p) {
+                    // row group p (rows y0 + 4p .. y0 + 4p + 3) within the bbox rows: the minimum
+                    // of q(d) = a dx^2 + 2b dx dy + c dy^2 over the rectangle of those pixel
+                    // centres (d = centre - mean).  For a positive-definite q the minimiser is
+                    // the mean if it lies inside, else on an edge facing it; the two candidate
+                    // segments (x nearest the mean with the best y, and vice versa) are inside
+                    // the rectangle, so their minimum is exact.
+                    const int ys = max(4 * p, rs), ye = min(4 * p + 3, re);
+                    if (ys > ye) continue;
+                    const float dylo = (float)(y0 + ys) + 0.5f - A.y, dyhi = (float)(y0 + ye) + 0.5f - A.y;
+                    const float dyv = fminf(fmaxf(dyv0, dylo), dyhi);
+                    const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
+                    const float dxh = fminf(fmaxf(__fdividef(-b * dyh, a), dxlo), dxhi);
+                    const float qv = a * dxv * dxv + 2.f * b * dxv * dyv + c * dyv * dyv;
+                    const float qh = a * dxh * dxh + 2.f * b * dxh * dyh + c * dyh * dyh;
+                    // margin for the fp32 rounding of this bound and of the per-pixel q
+                    if (fminf(qv, qh) * 0.999f - 1e-3f > qmax) mask &= ~(0xFFFFFFFFull << (32 * p));
+                }
+            }
         }
-        if (hit) groups |= 4u << p;
     }
-    if (!groups) return 0u;
-    return 1u | ((uint32_t)full << 1) | groups;
+    sts4(saddr, nmx, nmx, nmy, nmy);
+    sts4(saddr + 16, ka, ka, kb2, kb2);
+    sts4(saddr + 32, kc, kc, -Bv.y, -Bv.y);
+    sts4(saddr + 48, -Cv.y, -Cv.y, -Cv.z, -Cv.z);
+    sts4(saddr + 64, -Cv.w, -Cv.w, kK * qmax, __uint_as_float(gflag));
+    sts4(saddr + 80, __uint_as_float((uint32_t)mask), __uint_as_float((uint32_t)(mask >> 32)), kb, kb);
+    return mask != 0;
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
 //     3 max weight + weight sums for splats whose Gaussian is not yet visited.
 constexpr int kMaskBatches = 64;     // per-warp hit masks kept from the forward for the fused adjoint
-constexpr int kMaskWords = 2 + kPX;  // per batch: hit, full-cover, one per row group
 
 template <bool kExplicitGrad>
-__device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
-                                                uint32_t start, uint32_t last, const float (&g)[kPX][3],
-                                                float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
-                                                int lane, uint32_t wbase, const uint32_t *masks);
+__device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, float2 fpx2, float2 fpy2, int x0, int y0,
+                                                uint32_t start, uint32_t last, const float2 (&ng)[3], float2 t_rev,
+                                                float2 nsuf, uint2 stop, int lane, uint32_t wbase,
+                                                const uint32_t *masks);
 
 template <bool kLoss, bool kImage, int CI, bool kTrain = false>
 __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int gw, int nblk, int lane,
@@ -225,31 +254,24 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     // gw = tile * kBlocks + blk: the pixel block of frame b this warp composites
     const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    int px, py0;
-    pixels_of(blk, lane, tx, ty, px, py0);
-    const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 4 * kPX;
+    const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 8;
+    const int px = x0 + (lane & 7), py0 = y0 + (lane >> 3);      // pixel p: (px, py0 + 4 p)
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
-    const float fpx = (float)px;
+    const float2 fpx2 = f2((float)px, (float)px), fpy2 = f2((float)py0, (float)(py0 + 4));
+    const uint32_t lanebit = 1u << lane;
+    const bool in0 = px < a.W && py0 < a.H, in1 = px < a.W && py0 + 4 < a.H;
 
-    // live state across the splat loop is kept small (T, C, stop, and the colour-init
-    // source only when needed); the target is re-read in the epilogue
-    float fpy[kPX], T[kPX], C[kPX][3], src[CI >= 2 ? kPX : 1][3];
-    uint32_t stop[kPX];
-    bool live[kPX];
+    // per pixel pair: transmittance, colour (C[c] = channel c of both pixels), stop index
+    float2 T = f2(1.f, 1.f), C[3] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
+    uint2 stop = make_uint2(0u, 0u);
+    float src[CI >= 2 ? kPX : 1][3];
+    if constexpr (CI >= 2) {
 #pragma unroll
-    for (int p = 0; p < kPX; ++p) {
-        const int py = py0 + 4 * p;
-        const bool inside = px < a.W && py < a.H;
-        fpy[p] = (float)py;
-        T[p] = 1.0f;
-        live[p] = inside;
-        stop[p] = end - start;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) C[p][c] = 0.f;
-        if constexpr (CI >= 2) {
-            const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
+        for (int p = 0; p < kPX; ++p) {
+            const bool inside = p ? in1 : in0;
+            const int64_t pix = ((int64_t)b * a.H + (inside ? py0 + 4 * p : 0)) * a.W + (inside ? px : 0);
 #pragma unroll
             for (int c = 0; c < 3; ++c) src[p][c] = 0.f;
             if (inside && a.wsum_image) {
@@ -264,40 +286,28 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             }
         }
     }
+    const float2 one2 = f2(1.f, 1.f);
 
 #ifdef HS_RASTER_STATS
-    unsigned long long st_iter = 0, st_test = 0, st_q = 0, st_c = 0, st_empty = 0, st_full = 0, st_batches = 0;
+    unsigned long long st_iter = 0, st_test = 0, st_c = 0, st_batches = 0;
 #endif
     for (uint32_t c0 = start; c0 < end; c0 += 32) {
-        bool any_live = false;
-#pragma unroll
-        for (int p = 0; p < kPX; ++p) any_live = any_live || live[p];
-        if (!__any_sync(kFull, any_live)) break;
+        // pixels outside the image have no mask bits; the loop ends when every pixel of
+        // the block has terminated
+        if (!__any_sync(kFull, (in0 && T.x >= kTermEps) || (in1 && T.y >= kTermEps))) break;
         const uint32_t idx = c0 + lane;
-        uint32_t code = 0u;
-        bool want = false;
+        bool hit = false, want = false;
         if (idx < end) {
             const uint32_t n = a.vals[idx];
             const uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
-            code = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, x0, y0, wbase + lane * kStageBytes);
-            want = CI > 0 && (code & 1u) && (CI != 3 || !a.visited[n]);   // visited: no colour-init work
+            hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, x0, y0, wbase + lane * kStageBytes);
+            want = CI > 0 && hit && (CI != 3 || !a.visited[n]);   // visited: no colour-init work
         }
-        uint32_t bits = __ballot_sync(kFull, code & 1u);
-        const uint32_t fullb = __ballot_sync(kFull, code & 2u);
+        uint32_t bits = __ballot_sync(kFull, hit);
         const uint32_t wantb = __ballot_sync(kFull, want);
-        uint32_t grpb[kPX];
-#pragma unroll
-        for (int p = 0; p < kPX; ++p) grpb[p] = __ballot_sync(kFull, code & (4u << p));
         if (kTrain && lane == 0) {
             const uint32_t k = (c0 - start) >> 5;
-            if (k < (uint32_t)kMaskBatches)
-            {
-                uint32_t *m = masks + k * kMaskWords;
-                m[0] = bits;
-                m[1] = fullb;
-#pragma unroll
-                for (int p = 0; p < kPX; ++p) m[2 + p] = grpb[p];
-            }
+            if (k < (uint32_t)kMaskBatches) masks[k] = bits;
         }
 #ifdef HS_RASTER_STATS
         st_batches += lane == 0;
@@ -306,73 +316,42 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         while (bits) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1u;
-            const uint32_t ad = wbase + j * kStageBytes;
-            const float4 p0 = lds4(ad), p1 = lds4(ad + 16), col = lds4(ad + 48);
-            bool inb[kPX];
-            if ((fullb >> j) & 1u) {                 // warp-uniform: bbox covers the block
-#pragma unroll
-                for (int p = 0; p < kPX; ++p) inb[p] = true;
-            } else {
-                const int4 bb = lds4i(ad + 32);
-                const bool inx = px >= bb.x && px <= bb.y;
-#pragma unroll
-                for (int p = 0; p < kPX; ++p) inb[p] = inx && py0 + 4 * p >= bb.z && py0 + 4 * p <= bb.w;
-            }
-            const float dx = fpx - p0.x;
-            const float kadx = __fmul_rn(p0.z, dx);
-            float w[kPX];
-#pragma unroll
-            for (int p = 0; p < kPX; ++p) w[p] = 0.f;
+            const Staged t = load_staged(wbase + j * kStageBytes);
+            float2 dx2, dy2;
+            const float2 e2 = splat_e2(t, fpx2, fpy2, dx2, dy2);
+            float2 nal = mul2(t.nop, f2(ex2_approx(e2.x), ex2_approx(e2.y)));     // -alpha
+            // the reference's tests (S/render.py:248-266): bbox, not terminated, q <= qmax,
+            // alpha >= 1/255; a failing pixel gets alpha = 0 (no change to C or T)
+            const bool live0 = (t.mlo & lanebit) && T.x >= kTermEps, live1 = (t.mhi & lanebit) && T.y >= kTermEps;
+            const uint32_t jl1 = c0 - start + (uint32_t)j + 1u;
+            if (live0) stop.x = jl1;          // after the last splat tested while live
+            if (live1) stop.y = jl1;
+            const bool ok0 = live0 && e2.x >= t.kq && nal.x <= -kAlphaCutoff;
+            const bool ok1 = live1 && e2.y >= t.kq && nal.y <= -kAlphaCutoff;
+            nal.x = ok0 ? nal.x : 0.f;
+            nal.y = ok1 ? nal.y : 0.f;
 #ifdef HS_RASTER_STATS
             st_iter += (lane == 0);
-            st_full += (lane == 0) && ((fullb >> j) & 1u);
-            bool anyq = false;
+            st_test += live0 + live1;
+            st_c += ok0 + ok1;
 #endif
-            // branch-free per pixel: alpha is evaluated for every slot and the
-            // update predicated on the reference's tests (bbox, q <= qmax, cutoff)
-#pragma unroll
-            for (int p = 0; p < kPX; ++p) {
-                if (!((grpb[p] >> j) & 1u)) continue;          // warp-uniform: group out of reach
-                const float e2 = splat_e2(dx, fpy[p] - p0.y, kadx, p0.w, p1.x);
-                const float alpha = __fmul_rn(p1.z, ex2_approx(e2));
-                const bool ok = live[p] && inb[p] && e2 >= p1.y && alpha >= kAlphaCutoff;
-#ifdef HS_RASTER_STATS
-                st_test += live[p] && inb[p];
-                st_q += live[p] && inb[p] && e2 >= p1.y;
-                anyq = anyq || (live[p] && inb[p] && e2 >= p1.y);
-                st_c += ok;
-#endif
-                if (ok) {
-                    w[p] = alpha * T[p];
-                    C[p][0] += w[p] * col.x;
-                    C[p][1] += w[p] * col.y;
-                    C[p][2] += w[p] * col.z;
-                    T[p] = T[p] * one_minus_alpha(alpha);
-                    if (T[p] < kTermEps) {
-                        live[p] = false;
-                        stop[p] = c0 - start + (uint32_t)j + 1u;
-                    }
-                }
-            }
-#ifdef HS_RASTER_STATS
-            st_empty += !__any_sync(kFull, anyq) && lane == 0;
-#endif
+            const float2 nw = mul2(nal, T);                    // -alpha T
+            C[0] = fma2(nw, t.ncr, C[0]);
+            C[1] = fma2(nw, t.ncg, C[1]);
+            C[2] = fma2(nw, t.ncb, C[2]);
+            float2 om = add2(one2, nal);                       // 1 - alpha
+            om.x = fmaxf(om.x, kOneMinusFloor);
+            om.y = fmaxf(om.y, kOneMinusFloor);
+            T = mul2(T, om);
             if (CI > 0 && ((wantb >> j) & 1u)) {
-                float wmax = 0.f;
-#pragma unroll
-                for (int p = 0; p < kPX; ++p) wmax = fmaxf(wmax, w[p]);
+                const float wmax = -fminf(nw.x, nw.y);
                 if (__any_sync(kFull, wmax > 0.f)) {
-                    const int64_t g = __float_as_uint(p1.w);
+                    const int64_t g = t.gidx;
                     const float wm = warp_max(wmax);
                     if (CI >= 2) {
-                        float v[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                        for (int p = 0; p < kPX; ++p) {
-                            v[0] += w[p] * src[p][0];
-                            v[1] += w[p] * src[p][1];
-                            v[2] += w[p] * src[p][2];
-                            v[3] += w[p];
-                        }
+                        const float v[4] = {-(nw.x * src[0][0] + nw.y * src[1][0]),
+                                            -(nw.x * src[0][1] + nw.y * src[1][1]),
+                                            -(nw.x * src[0][2] + nw.y * src[1][2]), -(nw.x + nw.y)};
                         int vi;
                         bool issue;
                         const float s = reduce_scatter(v, lane, vi, issue);
@@ -388,48 +367,56 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
 #ifdef HS_RASTER_STATS
     atomicAdd(&g_raster_stats[0], st_iter);
     atomicAdd(&g_raster_stats[1], st_test);
-    atomicAdd(&g_raster_stats[2], st_q);
     atomicAdd(&g_raster_stats[3], st_c);
-    atomicAdd(&g_raster_stats[4], st_empty);
-    atomicAdd(&g_raster_stats[5], st_full);
     atomicAdd(&g_raster_stats[6], st_batches);
 #endif
+    // pixel p: a terminated pixel keeps the stop index found above (its terminating
+    // splat + 1); a live one gets the list length (S/render.py:254-259: no stop)
+    const uint32_t len = end - start;
+    if (T.x >= kTermEps) stop.x = len;
+    if (T.y >= kTermEps) stop.y = len;
     float l1 = 0.f, black = 0.f;
-    float g[kTrain ? kPX : 1][3];            // fused adjoint: the L1 gradient of each pixel
+    float2 ng[3];                            // fused adjoint: minus the L1 gradient of each pixel
 #pragma unroll
     for (int p = 0; p < kPX; ++p) {
         const int py = py0 + 4 * p;
-        if (kTrain) {
+        const float Tp = p ? T.y : T.x;
+        float g3[3] = {0.f, 0.f, 0.f};
+        if (px < a.W && py < a.H) {
+            const int64_t pix = ((int64_t)b * a.H + py) * a.W + px;
+            float pred[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) g[p][c] = 0.f;
-        }
-        if (px >= a.W || py >= a.H) continue;
-        const int64_t pix = ((int64_t)b * a.H + py) * a.W + px;
-        float pred[3];
+            for (int c = 0; c < 3; ++c) pred[c] = (p ? C[c].y : C[c].x) + Tp * bg[c];
+            uint32_t signs = 0;
+            if (kLoss) {
+                const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
+                const float al = (float)t.w / 255.0f;
+                const float rgb[3] = {(float)t.x / 255.0f, (float)t.y / 255.0f, (float)t.z / 255.0f};
 #pragma unroll
-        for (int c = 0; c < 3; ++c) pred[c] = C[p][c] + T[p] * bg[c];
-        uint32_t signs = 0;
-        if (kLoss) {
-            const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
-            const float al = (float)t.w / 255.0f;
-            const float rgb[3] = {(float)t.x / 255.0f, (float)t.y / 255.0f, (float)t.z / 255.0f};
+                for (int c = 0; c < 3; ++c) {
+                    const float tgt = rgb[c] * al + (1.0f - al) * bg[c];
+                    const float d = pred[c] - tgt;
+                    l1 += fabsf(d);
+                    black += fabsf((p ? C[c].y : C[c].x) - rgb[c] * al);
+                    signs |= (d > 0.f ? 1u : d < 0.f ? 2u : 0u) << (2 * c);
+                    if (kTrain) g3[c] = d > 0.f ? -a.grad_scale : d < 0.f ? a.grad_scale : 0.f;
+                }
+            }
+            if (!kTrain || a.pix_T) {
+                a.pix_T[pix] = Tp;
+                a.pix_state[pix] = (p ? stop.y : stop.x) | (signs << 26);
+            }
+            if (kImage) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float tgt = rgb[c] * al + (1.0f - al) * bg[c];
-                const float d = pred[c] - tgt;
-                l1 += fabsf(d);
-                black += fabsf(C[p][c] - rgb[c] * al);
-                signs |= (d > 0.f ? 1u : d < 0.f ? 2u : 0u) << (2 * c);
-                if (kTrain) g[p][c] = d > 0.f ? a.grad_scale : d < 0.f ? -a.grad_scale : 0.f;
+                for (int c = 0; c < 3; ++c) a.image[pix * 3 + c] = pred[c];
             }
         }
-        if (!kTrain || a.pix_T) {
-            a.pix_T[pix] = T[p];
-            a.pix_state[pix] = stop[p] | (signs << 26);
-        }
-        if (kImage) {
+        if (kTrain) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) a.image[pix * 3 + c] = pred[c];
+            for (int c = 0; c < 3; ++c) {
+                if (p) ng[c].y = g3[c];
+                else ng[c].x = g3[c];
+            }
         }
     }
     if (kLoss) {            // per-block partials: no CTA barrier, warps retire independently
@@ -445,33 +432,28 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         // the adjoint of this block right away: T, stop and the loss gradient are in
         // registers and the forward's hit masks are in shared memory
         if (start >= end) return;
-        float t_rev[kPX], suffix[kPX];
-        uint32_t smax = 0;
-#pragma unroll
-        for (int p = 0; p < kPX; ++p) {
-            const bool inside = px < a.W && py0 + 4 * p < a.H;
-            if (!inside) stop[p] = 0;
-            t_rev[p] = inside ? T[p] : 0.f;
-            suffix[p] = inside ? T[p] * (g[p][0] * bg[0] + g[p][1] * bg[1] + g[p][2] * bg[2]) : 0.f;
-            smax = max(smax, stop[p]);
-        }
-        const uint32_t last = start + __reduce_max_sync(kFull, smax);
+        if (!in0) stop.x = 0;
+        if (!in1) stop.y = 0;
+        const float2 t_rev = f2(in0 ? T.x : 0.f, in1 ? T.y : 0.f);
+        // -suffix = -T <g, bg> = T <ng, bg>
+        const float2 nsuf = mul2(t_rev, fma2(ng[2], f2(bg[2], bg[2]), fma2(ng[1], f2(bg[1], bg[1]),
+                                                                          mul2(ng[0], f2(bg[0], bg[0])))));
+        const uint32_t last = start + __reduce_max_sync(kFull, max(stop.x, stop.y));
         __syncwarp();
-        raster_bwd_loop<false>(a, b, px, py0, x0, y0, start, last, g, t_rev, suffix, stop, lane, wbase, masks);
+        raster_bwd_loop<false>(a, b, fpx2, fpy2, x0, y0, start, last, ng, t_rev, nsuf, stop, lane, wbase, masks);
     }
 }
 
 // Work distribution (HS_RASTER_PERSIST, default): a persistent grid of resident
-// one-warp CTAs where every warp pulls (frame, block) items from a global counter
-// (frame-major, tile order), so short and long blocks mix freely and no CTA launch
-// happens per block (-8 % raster time vs one CTA per block).  The last warp to
-// finish resets the counters for the next launch, so raster launches of one process
-// must not run concurrently on different streams (hs_api.h).  HS_RASTER_PERSIST=0:
-// one CTA per block.
+// one-warp CTAs where every warp pulls (frame, block) items from a counter, so short and
+// long blocks mix freely and no CTA launch happens per block (-8 % raster time vs one CTA
+// per block).  The counters and the item order live in a caller-provided workspace
+// (hs_raster_workspace_size; zeroed once at allocation): the last warp to finish resets
+// the counters, so launches on different workspaces are independent and one workspace
+// serves its stream's launches back to back.  HS_RASTER_PERSIST=0: one CTA per block.
 #ifndef HS_RASTER_PERSIST
 #define HS_RASTER_PERSIST 1
 #endif
-__device__ unsigned int g_raster_work[6];   // [fwd next, done, bwd next, done, train next, done]
 
 // Longest-first item order (HS_RASTER_LPT): tiles bucketed by the bit length of their
 // key count, heaviest bucket first, so the long tiles start early and the persistent
@@ -482,11 +464,11 @@ __device__ unsigned int g_raster_work[6];   // [fwd next, done, bwd next, done, 
 #ifndef HS_RASTER_LPT_SUB
 #define HS_RASTER_LPT_SUB 2
 #endif
-constexpr int kMaxOrder = 1 << 20;
-__device__ uint32_t g_tile_order[kMaxOrder];
+constexpr int kWsCounters = 16;      // workspace head: [next, done] (+ padding), then the order
 
 __global__ void __launch_bounds__(1024) tile_order_kernel(int total_tiles, int tile_bits, int tiles,
-                                                          const uint32_t *__restrict__ ranges) {
+                                                          const uint32_t *__restrict__ ranges,
+                                                          uint32_t *__restrict__ order) {
     constexpr int kSub = HS_RASTER_LPT_SUB;         // sub-buckets per octave
     constexpr int kNB = 33 << kSub;
     __shared__ uint32_t hist[kNB], cursor[kNB];
@@ -510,25 +492,25 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(int total_tiles, int t
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < total_tiles; t += blockDim.x) g_tile_order[atomicAdd(&cursor[bucket(t)], 1u)] = t;
+    for (int t = threadIdx.x; t < total_tiles; t += blockDim.x) order[atomicAdd(&cursor[bucket(t)], 1u)] = t;
 }
 
 template <typename F>
-__device__ __forceinline__ void for_each_block(int B, int nblk, int lane, int warp, unsigned int *work, F &&fn) {
+__device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, int lane, int warp, F &&fn) {
     if (!HS_RASTER_PERSIST) {
         fn((int)blockIdx.y, (int)blockIdx.x * kCW + warp);
         return;
     }
-    const int total = B * nblk;
-    const bool lpt = HS_RASTER_LPT && total / kBlocks <= kMaxOrder;
+    const int total = a.B * nblk;
     const int tiles = nblk / kBlocks;
+    unsigned int *work = a.work;
     for (;;) {
         int item = 0;
         if (lane == 0) item = (int)atomicAdd(work, 1u);
         item = __shfl_sync(kFull, item, 0);
         if (item >= total) break;
-        if (lpt) {
-            const uint32_t bt = g_tile_order[item / kBlocks];
+        if (HS_RASTER_LPT) {
+            const uint32_t bt = a.tile_order[item / kBlocks];
             fn((int)(bt / tiles), (int)(bt % tiles) * kBlocks + item % kBlocks);
         } else {
             fn(item / nblk, item % nblk);
@@ -549,7 +531,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
-    for_each_block(a.B, nblk, lane, warp, g_raster_work,
+    for_each_block(a, nblk, lane, warp,
                    [&](int b, int gw) { raster_fwd_block<kLoss, kImage, CI>(a, b, gw, nblk, lane, wbase); });
 }
 
@@ -557,81 +539,73 @@ template <bool kExplicitGrad>
 __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int gw, int lane, uint32_t wbase) {
     const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    int px, py0;
-    pixels_of(blk, lane, tx, ty, px, py0);
-    const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 4 * kPX;
+    const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 8;
+    const int px = x0 + (lane & 7), py0 = y0 + (lane >> 3);
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
     if (start >= end) return;
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
-
-    float g[kPX][3], t_rev[kPX], suffix[kPX];
-    uint32_t stop[kPX];
+    float2 ng[3], t_rev, nsuf;
+    uint2 stop;
 #pragma unroll
     for (int p = 0; p < kPX; ++p) {
         const int py = py0 + 4 * p;
         const bool inside = px < a.W && py < a.H;
         const int64_t pix = ((int64_t)b * a.H + (inside ? py : 0)) * a.W + (inside ? px : 0);
-        g[p][0] = g[p][1] = g[p][2] = 0.f;
-        stop[p] = 0;
-        t_rev[p] = 0.f;
-        suffix[p] = 0.f;
+        float g[3] = {0.f, 0.f, 0.f}, Tf = 0.f;
+        uint32_t st = 0;
         if (inside) {
-            const uint32_t st = a.pix_state[pix];
-            stop[p] = st & kStopMask;
-            const float Tf = a.pix_T[pix];
+            const uint32_t w = a.pix_state[pix];
+            st = w & kStopMask;
+            Tf = a.pix_T[pix];
             if (kExplicitGrad) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) g[p][c] = a.grad_image[pix * 3 + c];
+                for (int c = 0; c < 3; ++c) g[c] = -a.grad_image[pix * 3 + c];
             } else {
-                const uint32_t sg = st >> 26;
+                const uint32_t sg = w >> 26;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     const uint32_t s2 = (sg >> (2 * c)) & 3u;
-                    g[p][c] = s2 == 1u ? a.grad_scale : s2 == 2u ? -a.grad_scale : 0.f;
+                    g[c] = s2 == 1u ? -a.grad_scale : s2 == 2u ? a.grad_scale : 0.f;
                 }
             }
-            t_rev[p] = Tf;
-            suffix[p] = Tf * (g[p][0] * bg[0] + g[p][1] * bg[1] + g[p][2] * bg[2]);
         }
-    }
-    // this warp only needs the list up to its pixels' largest stop index
-    uint32_t smax = 0;
 #pragma unroll
-    for (int p = 0; p < kPX; ++p) smax = max(smax, stop[p]);
-    const uint32_t last = start + __reduce_max_sync(kFull, smax);
-    raster_bwd_loop<kExplicitGrad>(a, b, px, py0, x0, y0, start, last, g, t_rev, suffix, stop, lane, wbase, nullptr);
+        for (int c = 0; c < 3; ++c) {
+            if (p) ng[c].y = g[c];
+            else ng[c].x = g[c];
+        }
+        if (p) { stop.y = st; t_rev.y = Tf; }
+        else { stop.x = st; t_rev.x = Tf; }
+    }
+    nsuf = mul2(t_rev, fma2(ng[2], f2(bg[2], bg[2]), fma2(ng[1], f2(bg[1], bg[1]), mul2(ng[0], f2(bg[0], bg[0])))));
+    // this warp only needs the list up to its pixels' largest stop index
+    const uint32_t last = start + __reduce_max_sync(kFull, max(stop.x, stop.y));
+    raster_bwd_loop<kExplicitGrad>(a, b, f2((float)px, (float)px), f2((float)py0, (float)(py0 + 4)), x0, y0, start,
+                                   last, ng, t_rev, nsuf, stop, lane, wbase, nullptr);
 }
 
-// Back-to-front walk of [start, last) in the forward's 32-key batches.  With the
-// forward's hit masks (fused kernel) a batch is staged only by its hit lanes and
-// skipped when empty; otherwise each batch is staged and culled again.
+// Back-to-front walk of [start, last) in the forward's 32-key batches (S/render.py:
+// 276-336, the suffix recurrence per pixel).  With the forward's hit masks (fused kernel)
+// a batch is staged only by its hit lanes and skipped when empty; otherwise each batch is
+// staged and culled again.  A batch holding no pixel's stop index takes the fast path
+// (no per-splat stop test).
 template <bool kExplicitGrad>
-__device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int px, int py0, int x0, int y0,
-                                                uint32_t start, uint32_t last, const float (&g)[kPX][3],
-                                                float (&t_rev)[kPX], float (&suffix)[kPX], const uint32_t (&stop)[kPX],
-                                                int lane, uint32_t wbase, const uint32_t *masks) {
-    const float fpx = (float)px;
-    int py[kPX];
-    float fpy[kPX];
-#pragma unroll
-    for (int p = 0; p < kPX; ++p) {
-        py[p] = py0 + 4 * p;
-        fpy[p] = (float)py[p];
-    }
+__device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, float2 fpx2, float2 fpy2, int x0, int y0,
+                                                uint32_t start, uint32_t last, const float2 (&ng)[3], float2 t_rev,
+                                                float2 nsuf, uint2 stop, int lane, uint32_t wbase,
+                                                const uint32_t *masks) {
     if (last <= start) return;
+    const uint32_t lanebit = 1u << lane;
+    const float2 one2 = f2(1.f, 1.f);
     for (int k = (int)((last - 1 - start) >> 5); k >= 0; --k) {
         const uint32_t c0 = start + 32u * (uint32_t)k;
         const uint32_t c_end = min(c0 + 32u, last);
         const uint32_t live_lanes = c_end - c0 >= 32u ? kFull : (1u << (c_end - c0)) - 1u;
-        uint32_t bits, fullb, grpb[kPX];
+        uint32_t bits;
         const uint32_t idx = c0 + lane;
         if (masks != nullptr && k < kMaskBatches) {
-            const uint32_t *m = masks + k * kMaskWords;
-            bits = m[0] & live_lanes;
-            fullb = m[1];
-#pragma unroll
-            for (int p = 0; p < kPX; ++p) grpb[p] = m[2 + p];
+            bits = masks[k] & live_lanes;
             if (bits == 0u) continue;                      // warp-uniform
             if ((bits >> lane) & 1u) {
                 const uint32_t n = a.vals[idx];
@@ -639,76 +613,70 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
                                    y0, wbase + lane * kStageBytes);
             }
         } else {
-            uint32_t code = 0u;
+            bool hit = false;
             if (idx < c_end) {
                 const uint32_t n = a.vals[idx];
-                code = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
-                                   y0, wbase + lane * kStageBytes);
+                hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
+                                  y0, wbase + lane * kStageBytes);
             }
-            bits = __ballot_sync(kFull, code & 1u);
-            fullb = __ballot_sync(kFull, code & 2u);
-#pragma unroll
-            for (int p = 0; p < kPX; ++p) grpb[p] = __ballot_sync(kFull, code & (4u << p));
+            bits = __ballot_sync(kFull, hit);
         }
+        // pixels whose stop index lies inside this batch need the per-splat test
+        // jl < stop; a pixel with stop <= c0 takes no part in this batch at all
+        const uint32_t b0 = stop.x > c0 - start ? lanebit : 0u, b1 = stop.y > c0 - start ? lanebit : 0u;
+        const bool partial = (stop.x > c0 - start && stop.x < c_end - start) ||
+                             (stop.y > c0 - start && stop.y < c_end - start);
+        const bool slow = __any_sync(kFull, partial);
         __syncwarp();
         while (bits) {
             const int j = 31 - __clz(bits);
             bits &= ~(1u << j);
             const uint32_t jl = c0 - start + (uint32_t)j;
-            const uint32_t ad = wbase + j * kStageBytes;
-            const float4 p0 = lds4(ad), p1 = lds4(ad + 16), col = lds4(ad + 48);
-            bool inb[kPX];
-            if ((fullb >> j) & 1u) {                 // warp-uniform: bbox covers the block
-#pragma unroll
-                for (int p = 0; p < kPX; ++p) inb[p] = true;
-            } else {
-                const int4 bb = lds4i(ad + 32);
-                const bool inx = px >= bb.x && px <= bb.y;
-#pragma unroll
-                for (int p = 0; p < kPX; ++p) inb[p] = inx && py[p] >= bb.z && py[p] <= bb.w;
+            const Staged t = load_staged(wbase + j * kStageBytes);
+            float2 dx2, dy2;
+            const float2 e2 = splat_e2(t, fpx2, fpy2, dx2, dy2);
+            float2 G = f2(ex2_approx(e2.x), ex2_approx(e2.y));
+            float2 nal = mul2(t.nop, G);
+            bool in0 = (t.mlo & b0) != 0u, in1 = (t.mhi & b1) != 0u;
+            if (slow) {
+                in0 = in0 && jl < stop.x;
+                in1 = in1 && jl < stop.y;
             }
-            const float dx = fpx - p0.x;
-            const float kadx = __fmul_rn(p0.z, dx);
-            const float hb2 = 0.5f * p0.w;
+            const bool ok0 = in0 && e2.x >= t.kq && nal.x <= -kAlphaCutoff;
+            const bool ok1 = in1 && e2.y >= t.kq && nal.y <= -kAlphaCutoff;
+            // a failing pixel runs the same instructions with alpha = G = 0, which leaves
+            // t_rev and the suffix unchanged (1 / (1 - 0) == 1 exactly) and adds zeros
+            G.x = ok0 ? G.x : 0.f;
+            G.y = ok1 ? G.y : 0.f;
+            nal = mul2(t.nop, G);                                  // -alpha
+            float2 om = add2(one2, nal);
+            om.x = fmaxf(om.x, kOneMinusFloor);
+            om.y = fmaxf(om.y, kOneMinusFloor);
+            const float2 inv = f2(rcp_approx(om.x), rcp_approx(om.y));
+            const float2 tp = mul2(t_rev, inv);                    // T before the splat
+            const float2 gw = fma2(ng[2], t.ncb, fma2(ng[1], t.ncg, mul2(ng[0], t.ncr)));   // <g, colour>
+            const float2 nwg = mul2(nal, tp);                      // -alpha T
             float gv[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) gv[k] = 0.f;
-            bool contrib = false;
-            // branch-free per pixel: a slot failing the reference's tests runs the same
-            // instructions with alpha = G = 0, which leaves t_rev and suffix unchanged
-            // (1 / (1 - 0) == 1 exactly) and adds zeros to the gradients
-#pragma unroll
-            for (int p = 0; p < kPX; ++p) {
-                if (!((grpb[p] >> j) & 1u)) continue;          // warp-uniform: group out of reach
-                const float dy = fpy[p] - p0.y;
-                const float e2 = splat_e2(dx, dy, kadx, p0.w, p1.x);
-                const float G0 = ex2_approx(e2);
-                const float alpha0 = __fmul_rn(p1.z, G0);
-                const bool ok = jl < stop[p] && inb[p] && e2 >= p1.y && alpha0 >= kAlphaCutoff;
-                contrib = contrib || ok;
-                const float G = ok ? G0 : 0.f, alpha = ok ? alpha0 : 0.f;
-                const float inv = rcp_approx(one_minus_alpha(alpha));
-                const float t_prior = t_rev[p] * inv;
-                const float gw = g[p][0] * col.x + g[p][1] * col.y + g[p][2] * col.z;
-                const float wgt = alpha * t_prior;
-                gv[6] += wgt * g[p][0];
-                gv[7] += wgt * g[p][1];
-                gv[8] += wgt * g[p][2];
-                const float d_alpha = t_prior * gw - suffix[p] * inv;
-                gv[5] += G * d_alpha;
-                // dq = -0.5 alpha d_alpha; the constant factors are applied once per
-                // reduced value (kGradScale) instead of per pixel
-                const float dq = alpha * d_alpha;
-                const float dqx = dq * dx, dqy = dq * dy;
-                gv[2] += dqx * dx;
-                gv[3] += dqx * dy;
-                gv[4] += dqy * dy;
-                // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
-                gv[0] += p0.z * dqx + hb2 * dqy;
-                gv[1] += hb2 * dqx + p1.x * dqy;
-                suffix[p] += wgt * gw;
-                t_rev[p] = t_prior;
-            }
+            // colour: alpha T g = (-alpha T)(-g)
+            gv[6] = nwg.x * ng[0].x + nwg.y * ng[0].y;
+            gv[7] = nwg.x * ng[1].x + nwg.y * ng[1].y;
+            gv[8] = nwg.x * ng[2].x + nwg.y * ng[2].y;
+            // d alpha = T gw - suffix / (1 - alpha)
+            const float2 da = fma2(nsuf, inv, mul2(tp, gw));
+            gv[5] = G.x * da.x + G.y * da.y;
+            const float2 ndq = mul2(nal, da);                      // -alpha d_alpha
+            const float2 dqx = mul2(ndq, dx2), dqy = mul2(ndq, dy2);
+            const float2 d2 = mul2(dqx, dx2), d3 = mul2(dqx, dy2), d4 = mul2(dqy, dy2);
+            gv[2] = d2.x + d2.y;
+            gv[3] = d3.x + d3.y;
+            gv[4] = d4.x + d4.y;
+            // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
+            const float2 m0 = fma2(t.kb, dqy, mul2(t.ka, dqx)), m1 = fma2(t.kc, dqy, mul2(t.kb, dqx));
+            gv[0] = m0.x + m0.y;
+            gv[1] = m1.x + m1.y;
+            nsuf = fma2(nwg, gw, nsuf);                            // suffix += alpha T gw
+            t_rev = tp;
+            const bool contrib = ok0 || ok1;
 #ifdef HS_RASTER_STATS
             {
                 const int nc = __popc(__ballot_sync(kFull, contrib));
@@ -718,24 +686,26 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
                 }
             }
 #endif
+            // constant factors applied once per reduced value: the mean and conic sums
+            // above carry -dq (sign folded here)
             const uint32_t cmask = __ballot_sync(kFull, contrib);
             if (HS_RASTER_DIRECT && cmask && __popc(cmask) <= HS_RASTER_DIRECT) {
                 // few contributing pixels: their lanes add directly (9 atomics each) instead
                 // of the 9-value warp reduce-scatter
                 if (contrib) {
-                    float *gp = a.g_splat + (uint64_t)(__float_as_uint(p1.w)) * kGS;
+                    float *gp = a.g_splat + (uint64_t)t.gidx * kGS;
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) {
-                        const float sc = k < 2 ? -0.5f * kMeanScale : k == 3 ? -1.0f : k < 5 ? -0.5f : 1.0f;
-                        atomicAdd(gp + k, gv[k] * sc);
+                    for (int v = 0; v < 9; ++v) {
+                        const float sc = v < 2 ? 0.5f * kMeanScale : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
+                        atomicAdd(gp + v, gv[v] * sc);
                     }
                 }
             } else if (cmask) {
                 int vi;
                 bool issue;
                 const float s = reduce_scatter(gv, lane, vi, issue);
-                const float sc = vi < 2 ? -0.5f * kMeanScale : vi == 3 ? -1.0f : vi < 5 ? -0.5f : 1.0f;
-                if (issue) atomicAdd(a.g_splat + (uint64_t)(__float_as_uint(p1.w)) * kGS + vi, s * sc);
+                const float sc = vi < 2 ? 0.5f * kMeanScale : vi == 3 ? 1.0f : vi < 5 ? 0.5f : 1.0f;
+                if (issue) atomicAdd(a.g_splat + (uint64_t)t.gidx * kGS + vi, s * sc);
             }
         }
         __syncwarp();
@@ -749,10 +719,10 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, int 
 template <int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
-    __shared__ uint32_t s_masks[kCW][kMaskBatches * kMaskWords];
+    __shared__ uint32_t s_masks[kCW][kMaskBatches];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
-    for_each_block(a.B, nblk, lane, warp, g_raster_work + 4, [&](int b, int gw) {
+    for_each_block(a, nblk, lane, warp, [&](int b, int gw) {
         raster_fwd_block<true, false, CI, true>(a, b, gw, nblk, lane, wbase, s_masks[warp]);
     });
 }
@@ -762,7 +732,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
     __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
-    for_each_block(a.B, nblk, lane, warp, g_raster_work + 2,
+    for_each_block(a, nblk, lane, warp,
                    [&](int b, int gw) { raster_bwd_block<kExplicitGrad>(a, b, gw, lane, wbase); });
 }
 
@@ -797,7 +767,7 @@ __global__ void loss_mean_kernel(int B, float *__restrict__ out) {
 }
 
 static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records, const uint32_t *values,
-                            const uint32_t *ranges, int tile_bits, const float *bgs) {
+                            const uint32_t *ranges, int tile_bits, const float *bgs, void *workspace) {
     RasterArgs a{};
     a.B = B;
     a.N = N;
@@ -809,6 +779,8 @@ static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records
     a.vals = values;
     a.ranges = ranges;
     a.bgs = bgs;
+    a.work = reinterpret_cast<unsigned int *>(workspace);
+    a.tile_order = reinterpret_cast<const uint32_t *>(workspace) + kWsCounters;
     return a;
 }
 
@@ -822,20 +794,33 @@ static void launch_fwd_ci(int ci, dim3 grid, int nblk, cudaStream_t s, const Ras
     }
 }
 
-// grid of the raster kernels: one CTA per kCW blocks, or a persistent grid of
-// resident CTAs (HS_RASTER_PERSIST)
-static void launch_tile_order(int B, int nblk, int tile_bits, const uint32_t *ranges, cudaStream_t s) {
-    const int tiles = nblk / kBlocks;
-    if (HS_RASTER_PERSIST && HS_RASTER_LPT && B * tiles <= kMaxOrder)
-        tile_order_kernel<<<1, 1024, 0, s>>>(B * tiles, tile_bits, tiles, ranges);
+static size_t workspace_bytes(int B, int W, int H) {
+    const int64_t tiles = (int64_t)((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+    return sizeof(uint32_t) * (size_t)(kWsCounters + B * tiles);
 }
 
+// the persistent raster's longest-first item order, into the workspace
+static void launch_tile_order(int B, int nblk, int tile_bits, const uint32_t *ranges, void *ws, cudaStream_t s) {
+    const int tiles = nblk / kBlocks;
+    if (HS_RASTER_PERSIST && HS_RASTER_LPT)
+        tile_order_kernel<<<1, 1024, 0, s>>>(B * tiles, tile_bits, tiles, ranges,
+                                             reinterpret_cast<uint32_t *>(ws) + kWsCounters);
+}
+
+// grid of the raster kernels: one CTA per kCW blocks, or a persistent grid of
+// resident CTAs (HS_RASTER_PERSIST) sized by the current device's SM count
 static dim3 raster_grid(int nblk, int B) {
     if (!HS_RASTER_PERSIST) return dim3(nblk / kCW, B);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t want = (int64_t)sms * HS_RASTER_MINB, items = (int64_t)nblk * B / kCW;
+    const int64_t want = (int64_t)current_sm_count() * HS_RASTER_MINB, items = (int64_t)nblk * B / kCW;
     return dim3((unsigned)std::max<int64_t>(1, std::min(want, items)), 1);
+}
+
+static int check_ws(const char *fn, void *ws) {
+    if (ws == nullptr || (reinterpret_cast<uintptr_t>(ws) & 15u)) {
+        set_error("%s: workspace must be a 16-byte aligned device buffer of hs_raster_workspace_size() bytes", fn);
+        return HS_ERR_SHAPE;
+    }
+    return HS_OK;
 }
 
 }  // namespace hs
@@ -844,16 +829,20 @@ using namespace hs;
 
 extern "C" {
 
-int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, int tile_bits, void *stream) {
+size_t hs_raster_workspace_size(int B, int width, int height) { return workspace_bytes(B, width, height); }
+
+int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, int tile_bits, void *workspace,
+                         void *stream) {
+    if (int e = check_ws("hs_raster_tile_order", workspace)) return e;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-    launch_tile_order(B, tiles_x * tiles_y * kBlocks, tile_bits, ranges, HS_CHECK_STREAM(stream));
+    launch_tile_order(B, tiles_x * tiles_y * kBlocks, tile_bits, ranges, workspace, HS_CHECK_STREAM(stream));
     return check_launch("hs_raster_tile_order");
 }
 
 int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records, const uint32_t *values,
                   const uint32_t *ranges, int tile_bits, const float *backgrounds, const uint8_t *targets,
                   const float *wsum_image, const uint8_t *visited, float *pix_T, uint32_t *pix_state, float *image,
-                  float *maxw, float *wsums, float *loss_partials, void *stream) {
+                  float *maxw, float *wsums, float *loss_partials, void *workspace, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const bool loss = flags & HS_RASTER_LOSS, img = flags & HS_RASTER_IMAGE;
     int ci = 0;
@@ -865,7 +854,8 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
         set_error("hs_raster_fwd: flags 0x%x need a buffer that is NULL", flags);
         return HS_ERR_SHAPE;
     }
-    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds);
+    if (int e = check_ws("hs_raster_fwd", workspace)) return e;
+    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
     a.targets = targets;
     a.wsum_image = (flags & HS_RASTER_WSUMS_IMAGE) ? wsum_image : nullptr;
     a.visited = visited;
@@ -878,7 +868,7 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, s);
+    if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, workspace, s);
     if (loss && img) launch_fwd_ci<true, true>(ci, grid, nblk, s, a);
     else if (loss) launch_fwd_ci<true, false>(ci, grid, nblk, s, a);
     else if (img) launch_fwd_ci<false, true>(ci, grid, nblk, s, a);
@@ -889,9 +879,10 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
 int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records, const uint32_t *values,
                   const uint32_t *ranges, int tile_bits, const float *backgrounds, const float *pix_T,
                   const uint32_t *pix_state, const float *grad_image, float grad_scale, float *g_splat,
-                  void *stream) {
+                  void *workspace, void *stream) {
+    if (int e = check_ws("hs_raster_bwd", workspace)) return e;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds);
+    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
     a.pix_T = const_cast<float *>(pix_T);
     a.pix_state = const_cast<uint32_t *>(pix_state);
     a.grad_image = grad_image;
@@ -900,7 +891,7 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    launch_tile_order(B, nblk, tile_bits, ranges, s);
+    launch_tile_order(B, nblk, tile_bits, ranges, workspace, s);
     if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a, nblk);
     else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a, nblk);
     return check_launch("hs_raster_bwd");
@@ -909,7 +900,7 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
 int hs_raster_train(int B, int64_t N, int width, int height, int flags, const float *records, const uint32_t *values,
                     const uint32_t *ranges, int tile_bits, const float *backgrounds, const uint8_t *targets,
                     const uint8_t *visited, float *maxw, float *wsums, float *loss_partials, float grad_scale,
-                    float *g_splat, float *pix_T, uint32_t *pix_state, void *stream) {
+                    float *g_splat, float *pix_T, uint32_t *pix_state, void *workspace, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     int ci = 0;
     if (flags & HS_RASTER_MAXW_UNVISITED) ci = 3;
@@ -920,7 +911,8 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
         set_error("hs_raster_train: flags 0x%x / buffers not supported (needs targets, loss_partials, g_splat)", flags);
         return HS_ERR_SHAPE;
     }
-    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds);
+    if (int e = check_ws("hs_raster_train", workspace)) return e;
+    RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
     a.targets = targets;
     a.visited = visited;
     a.maxw = maxw;
@@ -933,7 +925,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, s);
+    if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, workspace, s);
     switch (ci) {
         case 0: raster_train_kernel<0><<<grid, kRT, 0, s>>>(a, nblk); break;
         case 1: raster_train_kernel<1><<<grid, kRT, 0, s>>>(a, nblk); break;

@@ -859,8 +859,7 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     const size_t tsmem = tiles <= kTileSmemBins ? sizeof(uint32_t) * tiles : 0;
     tile_scatter_kernel<<<grid_for(items, kTileItems), kTileThreads, tsmem, s>>>(
         items, N, tiles_x, tiles, tile_bits, records, counts, tile_rects, cursor, capacity, summary, keys, values);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = current_sm_count();
     // the long lists first (fewer, longer: their tail overlaps nothing otherwise)
     // the short lists sort on a library-internal stream alongside the long ones (each
     // kernel leaves SMs idle in its tail); the caller's stream waits for both
@@ -896,8 +895,7 @@ int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *d
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
     const int nseg = B << tile_bits;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = current_sm_count();
     static bool attr = false;
     const int csmem = kCtaCap * (int)sizeof(unsigned long long);
     if (!attr) {

@@ -582,6 +582,10 @@ class Trainer:
         self.loss_partials = torch.empty(B * self.tiles * L.LOSS_PARTIALS_PER_TILE, **f32)
         self.loss_out = torch.empty(2 * B + 1, **f32)
         self.g_splat = torch.empty(B * N * 9, **f32)
+        # the persistent raster's work counters + item order (zeroed once; per Trainer, so
+        # Trainers on different streams / devices never share raster state)
+        self.raster_ws = torch.zeros(int(L.load().hs_raster_workspace_size(B, self.W, self.H)), dtype=torch.uint8,
+                                     device=d)
         self.g_raw14 = torch.empty(B * 14 * N, **f32)
         self.nparts = int(L.load().hs_blend_bwd_partials(N))
         self.gpsi_partials = torch.empty(B * K * self.nparts, **f32)
@@ -673,7 +677,8 @@ class Trainer:
         side = self._side_stream()
         side.wait_event(scanned)
         with torch.cuda.stream(side):
-            L.call("hs_raster_tile_order", self.B, self.W, self.H, _p(ranges), tile_bits, _stream())
+            L.call("hs_raster_tile_order", self.B, self.W, self.H, _p(ranges), tile_bits, _p(self.raster_ws),
+                   _stream())
             ev = torch.cuda.Event()
             ev.record(side)
         self._order_event = ev
@@ -781,7 +786,7 @@ class Trainer:
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), _p(self.visited), _p(self.maxw),
                        _p(self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale), _p(self.g_splat),
                        _p(self.pix_T) if self.capture_pixels else None,
-                       _p(self.pix_state) if self.capture_pixels else None, s, kernels=kernels)
+                       _p(self.pix_state) if self.capture_pixels else None, _p(self.raster_ws), s, kernels=kernels)
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the rest of the backward
             # the loss is only read after the step: reduce it on the side stream
@@ -799,7 +804,8 @@ class Trainer:
         else:
             self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
-                       _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials), s)
+                       _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials),
+                       _p(self.raster_ws), s)
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the backward
             self._call("loss_reduce", "hs_loss_reduce", B, tiles, self.W, self.H, _p(self.loss_partials),
@@ -808,7 +814,7 @@ class Trainer:
                 self.debug_before_backward(self)
             self._call("raster_bwd", "hs_raster_bwd", B, N, self.W, self.H, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(self.pix_T), _p(self.pix_state), None,
-                       ctypes.c_float(grad_scale), _p(self.g_splat), s)
+                       ctypes.c_float(grad_scale), _p(self.g_splat), _p(self.raster_ws), s)
         self._call("project_bwd", "hs_project_avatar_bwd", B, N, F, _p(self.raw10), _p(av.base14), _p(av.tri_index),
                    _p(av.barycentric), _p(frames), _p(cameras), _p(self.g_splat), _p(self.g_raw14), s)
         nparts = ctypes.c_int(0)
@@ -949,7 +955,7 @@ class Trainer:
                 flags |= L.RASTER_ORDER_READY
         self._call("raster_fwd", "hs_raster_fwd", self.B, av.N, self.W, self.H, flags, _p(self.records),
                    _p(vals), _p(ranges), tile_bits, _p(backgrounds), None, None, None, _p(self.pix_T),
-                   _p(self.pix_state), _p(out), None, None, None, _stream())
+                   _p(self.pix_state), _p(out), None, None, None, _p(self.raster_ws), _stream())
         return out
 
     # -------------------------------------------------------------- end to end
