@@ -26,6 +26,7 @@
 // then the 9 per-splat gradients are reduce-scattered across the warp (12 shuffles)
 // before one RED per value.
 #include <algorithm>
+#include <type_traits>
 
 #include "hs_common.cuh"
 
@@ -40,6 +41,9 @@ namespace hs {
 
 #ifndef HS_RASTER_EXACT_CULL
 #define HS_RASTER_EXACT_CULL 1       // cull row groups with the exact ellipse-rectangle distance
+#endif
+#ifndef HS_RASTER_FWD_ASM
+#define HS_RASTER_FWD_ASM 1          // forward: per-pixel decision as one predicate chain
 #endif
 #ifndef HS_RASTER_DIRECT
 #define HS_RASTER_DIRECT 5           // adjoint: up to this many contributing lanes add directly
@@ -108,7 +112,13 @@ __device__ __forceinline__ float warp_max(float v) {
 // (per element identical to __fmaf_rn / __fmul_rn), so both make identical decisions.
 constexpr float kK = -0.72134752044448170f;      // -0.5 * log2(e)
 constexpr float kMeanScale = -2.0f / kK;         // d q / d(k q) folded into g_mean
+// the adjoint's constant factor of gradient value v (g_mean 2, g_conic 3, g_opacity,
+// g_colour 3): the mean and conic partial sums carry -dq = -alpha d_alpha (S/render.py:323-330)
+__device__ __forceinline__ float grad_factor(int v) {
+    return v < 2 ? 0.5f * kMeanScale : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
+}
 constexpr int kStageBytes = 96;
+constexpr int kWarpSmem = 32 * kStageBytes;
 
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
     float4 v;
@@ -116,8 +126,9 @@ __device__ __forceinline__ float4 lds4(uint32_t addr) {
     return v;
 }
 __device__ __forceinline__ void sts4(uint32_t addr, float a, float b, float c, float d) {
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d));
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
+
 // 1/x for x in [2^-24, 1] (x = 1 - alpha floored): the MUFU reciprocal without the
 // denormal-range fix-up __fdividef adds (same result for normal x)
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -181,6 +192,25 @@ __device__ __forceinline__ float2 splat_e2(const Staged &t, float2 fpx2, float2 
     dy2 = add2(fpy2, t.nmy);
     const float2 kadx = mul2(t.ka, dx2);
     return fma2(mul2(t.kc, dy2), dy2, mul2(dx2, fma2(t.kb2, dy2, kadx)));
+}
+
+// Forward per-pixel decision, one predicate chain (LOP3 + 3 FSETP.AND + FSEL):
+//   live = pixel in the splat's mask && T >= 1e-14   (stop = live ? jl1 : stop)
+//   returns live && e2 >= k qmax && -alpha <= -1/255 ? -alpha : 0
+__device__ __forceinline__ float fwd_gate(uint32_t mask, uint32_t lanebit, float T, float e2, float kq, float nal,
+                                          uint32_t jl1, uint32_t &stop) {
+    float out;
+    asm("{\n\t.reg .pred p, q;\n\t.reg .b32 m;\n\t"
+        "and.b32 m, %2, %3;\n\t"
+        "setp.ne.u32 p, m, 0;\n\t"
+        "setp.ge.and.f32 p, %4, %5, p;\n\t"
+        "selp.u32 %1, %9, %1, p;\n\t"
+        "setp.ge.and.f32 q, %6, %7, p;\n\t"
+        "setp.le.and.f32 q, %8, %10, q;\n\t"
+        "selp.f32 %0, %8, 0f00000000, q;\n\t}"
+        : "=f"(out), "+r"(stop)
+        : "r"(mask), "r"(lanebit), "f"(T), "f"(kTermEps), "f"(e2), "f"(kq), "f"(nal), "r"(jl1), "f"(-kAlphaCutoff));
+    return out;
 }
 
 // Stage one splat record into the lane's slot for the warp's 8 x 8 block with origin
@@ -289,7 +319,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     const float2 one2 = f2(1.f, 1.f);
 
 #ifdef HS_RASTER_STATS
-    unsigned long long st_iter = 0, st_test = 0, st_c = 0, st_batches = 0;
+    unsigned long long st_iter = 0, st_c = 0, st_batches = 0;
 #endif
     for (uint32_t c0 = start; c0 < end; c0 += 32) {
         // pixels outside the image have no mask bits; the loop ends when every pixel of
@@ -313,27 +343,33 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         st_batches += lane == 0;
 #endif
         __syncwarp();
-        while (bits) {
-            const int j = __ffs(bits) - 1;
-            bits &= bits - 1u;
+        // one splat of the batch (kCI: with the colour-init sums); the batch runs the loop
+        // without the colour-init test when no staged splat wants it
+        auto splat = [&](int j, auto ci_tag) {
+            constexpr bool kCI = decltype(ci_tag)::value;
             const Staged t = load_staged(wbase + j * kStageBytes);
             float2 dx2, dy2;
             const float2 e2 = splat_e2(t, fpx2, fpy2, dx2, dy2);
             float2 nal = mul2(t.nop, f2(ex2_approx(e2.x), ex2_approx(e2.y)));     // -alpha
             // the reference's tests (S/render.py:248-266): bbox, not terminated, q <= qmax,
-            // alpha >= 1/255; a failing pixel gets alpha = 0 (no change to C or T)
-            const bool live0 = (t.mlo & lanebit) && T.x >= kTermEps, live1 = (t.mhi & lanebit) && T.y >= kTermEps;
+            // alpha >= 1/255; a failing pixel gets alpha = 0 (no change to C or T); stop
+            // records the list position after the last splat tested while live
             const uint32_t jl1 = c0 - start + (uint32_t)j + 1u;
-            if (live0) stop.x = jl1;          // after the last splat tested while live
-            if (live1) stop.y = jl1;
-            const bool ok0 = live0 && e2.x >= t.kq && nal.x <= -kAlphaCutoff;
-            const bool ok1 = live1 && e2.y >= t.kq && nal.y <= -kAlphaCutoff;
-            nal.x = ok0 ? nal.x : 0.f;
-            nal.y = ok1 ? nal.y : 0.f;
+            if (HS_RASTER_FWD_ASM) {
+                nal.x = fwd_gate(t.mlo, lanebit, T.x, e2.x, t.kq, nal.x, jl1, stop.x);
+                nal.y = fwd_gate(t.mhi, lanebit, T.y, e2.y, t.kq, nal.y, jl1, stop.y);
+            } else {
+                const bool live0 = (t.mlo & lanebit) && T.x >= kTermEps, live1 = (t.mhi & lanebit) && T.y >= kTermEps;
+                if (live0) stop.x = jl1;
+                if (live1) stop.y = jl1;
+                const bool ok0 = live0 && e2.x >= t.kq && nal.x <= -kAlphaCutoff;
+                const bool ok1 = live1 && e2.y >= t.kq && nal.y <= -kAlphaCutoff;
+                nal.x = ok0 ? nal.x : 0.f;
+                nal.y = ok1 ? nal.y : 0.f;
+            }
 #ifdef HS_RASTER_STATS
             st_iter += (lane == 0);
-            st_test += live0 + live1;
-            st_c += ok0 + ok1;
+            st_c += (nal.x != 0.f) + (nal.y != 0.f);
 #endif
             const float2 nw = mul2(nal, T);                    // -alpha T
             C[0] = fma2(nw, t.ncr, C[0]);
@@ -343,7 +379,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             om.x = fmaxf(om.x, kOneMinusFloor);
             om.y = fmaxf(om.y, kOneMinusFloor);
             T = mul2(T, om);
-            if (CI > 0 && ((wantb >> j) & 1u)) {
+            if (kCI && ((wantb >> j) & 1u)) {
                 const float wmax = -fminf(nw.x, nw.y);
                 if (__any_sync(kFull, wmax > 0.f)) {
                     const int64_t g = t.gidx;
@@ -360,13 +396,25 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                     if (lane == 0) atomicMax(reinterpret_cast<int *>(a.maxw) + g, __float_as_int(wm));
                 }
             }
+        };
+        if (CI > 0 && wantb) {
+            while (bits) {
+                const int j = __ffs(bits) - 1;
+                bits &= bits - 1u;
+                splat(j, std::true_type{});
+            }
+        } else {
+            while (bits) {
+                const int j = __ffs(bits) - 1;
+                bits &= bits - 1u;
+                splat(j, std::false_type{});
+            }
         }
         __syncwarp();
     }
 
 #ifdef HS_RASTER_STATS
     atomicAdd(&g_raster_stats[0], st_iter);
-    atomicAdd(&g_raster_stats[1], st_test);
     atomicAdd(&g_raster_stats[3], st_c);
     atomicAdd(&g_raster_stats[6], st_batches);
 #endif
@@ -528,9 +576,9 @@ __device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, in
 
 template <bool kLoss, bool kImage, int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a, int nblk) {
-    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
+    __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * kWarpSmem;
     for_each_block(a, nblk, lane, warp,
                    [&](int b, int gw) { raster_fwd_block<kLoss, kImage, CI>(a, b, gw, nblk, lane, wbase); });
 }
@@ -628,11 +676,12 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
                              (stop.y > c0 - start && stop.y < c_end - start);
         const bool slow = __any_sync(kFull, partial);
         __syncwarp();
-        while (bits) {
-            const int j = 31 - __clz(bits);
-            bits &= ~(1u << j);
+        // the adjoint of splat j at this lane's two pixels: its 9 gradient partial sums
+        // (returns whether a pixel of this lane contributed); advances t_rev / suffix
+        auto splat = [&](int j, float (&gv)[9], uint32_t &gidx) -> bool {
             const uint32_t jl = c0 - start + (uint32_t)j;
             const Staged t = load_staged(wbase + j * kStageBytes);
+            gidx = t.gidx;
             float2 dx2, dy2;
             const float2 e2 = splat_e2(t, fpx2, fpy2, dx2, dy2);
             float2 G = f2(ex2_approx(e2.x), ex2_approx(e2.y));
@@ -656,7 +705,6 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             const float2 tp = mul2(t_rev, inv);                    // T before the splat
             const float2 gw = fma2(ng[2], t.ncb, fma2(ng[1], t.ncg, mul2(ng[0], t.ncr)));   // <g, colour>
             const float2 nwg = mul2(nal, tp);                      // -alpha T
-            float gv[9];
             // colour: alpha T g = (-alpha T)(-g)
             gv[6] = nwg.x * ng[0].x + nwg.y * ng[0].y;
             gv[7] = nwg.x * ng[1].x + nwg.y * ng[1].y;
@@ -676,37 +724,41 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             gv[1] = m1.x + m1.y;
             nsuf = fma2(nwg, gw, nsuf);                            // suffix += alpha T gw
             t_rev = tp;
-            const bool contrib = ok0 || ok1;
-#ifdef HS_RASTER_STATS
-            {
-                const int nc = __popc(__ballot_sync(kFull, contrib));
-                if (lane == 0) {
-                    const int bin = nc == 0 ? 0 : nc == 1 ? 1 : nc == 2 ? 2 : nc <= 4 ? 3 : nc <= 8 ? 4 : nc <= 16 ? 5 : 6;
-                    atomicAdd(&g_raster_stats[8 + bin], 1ull);
-                }
-            }
-#endif
-            // constant factors applied once per reduced value: the mean and conic sums
-            // above carry -dq (sign folded here)
-            const uint32_t cmask = __ballot_sync(kFull, contrib);
-            if (HS_RASTER_DIRECT && cmask && __popc(cmask) <= HS_RASTER_DIRECT) {
-                // few contributing pixels: their lanes add directly (9 atomics each) instead
-                // of the 9-value warp reduce-scatter
+            return ok0 || ok1;
+        };
+        // one splat's 9 sums into g_splat: few contributing pixels (<= HS_RASTER_DIRECT
+        // lanes) add directly (9 atomics each), otherwise the 9-value warp reduce-scatter
+        // and one atomic per value.  Constant factors are applied once per reduced value
+        // (the mean and conic sums carry -dq, sign folded here).
+        auto flush1 = [&](const float (&gv)[9], uint32_t gidx, bool contrib, uint32_t cmask) {
+            if (HS_RASTER_DIRECT && __popc(cmask) <= HS_RASTER_DIRECT) {
                 if (contrib) {
-                    float *gp = a.g_splat + (uint64_t)t.gidx * kGS;
+                    float *gp = a.g_splat + (uint64_t)gidx * kGS;
 #pragma unroll
-                    for (int v = 0; v < 9; ++v) {
-                        const float sc = v < 2 ? 0.5f * kMeanScale : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
-                        atomicAdd(gp + v, gv[v] * sc);
-                    }
+                    for (int v = 0; v < 9; ++v) atomicAdd(gp + v, gv[v] * grad_factor(v));
                 }
-            } else if (cmask) {
+            } else {
                 int vi;
                 bool issue;
                 const float s = reduce_scatter(gv, lane, vi, issue);
-                const float sc = vi < 2 ? 0.5f * kMeanScale : vi == 3 ? 1.0f : vi < 5 ? 0.5f : 1.0f;
-                if (issue) atomicAdd(a.g_splat + (uint64_t)t.gidx * kGS + vi, s * sc);
+                if (issue) atomicAdd(a.g_splat + (uint64_t)gidx * kGS + vi, s * grad_factor(vi));
             }
+        };
+        while (bits) {
+            const int j = 31 - __clz(bits);
+            bits &= ~(1u << j);
+            float gv[9];
+            uint32_t gidx;
+            const bool contrib = splat(j, gv, gidx);
+            const uint32_t cmask = __ballot_sync(kFull, contrib);
+#ifdef HS_RASTER_STATS
+            if (lane == 0) {
+                const int nc = __popc(cmask);
+                const int bin = nc == 0 ? 0 : nc == 1 ? 1 : nc == 2 ? 2 : nc <= 4 ? 3 : nc <= 8 ? 4 : nc <= 16 ? 5 : 6;
+                atomicAdd(&g_raster_stats[8 + bin], 1ull);
+            }
+#endif
+            if (cmask) flush1(gv, gidx, contrib, cmask);
         }
         __syncwarp();
     }
@@ -718,10 +770,10 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
 // forward's per-batch hit masks.
 template <int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
-    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
+    __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     __shared__ uint32_t s_masks[kCW][kMaskBatches];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * kWarpSmem;
     for_each_block(a, nblk, lane, warp, [&](int b, int gw) {
         raster_fwd_block<true, false, CI, true>(a, b, gw, nblk, lane, wbase, s_masks[warp]);
     });
@@ -729,9 +781,9 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(Raste
 
 template <bool kExplicitGrad>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a, int nblk) {
-    __shared__ __align__(16) unsigned char s_stage[kRT * kStageBytes];
+    __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * 32 * kStageBytes;
+    const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * kWarpSmem;
     for_each_block(a, nblk, lane, warp,
                    [&](int b, int gw) { raster_bwd_block<kExplicitGrad>(a, b, gw, lane, wbase); });
 }
