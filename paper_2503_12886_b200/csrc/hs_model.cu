@@ -188,6 +188,126 @@ __global__ void mlp_bwd_weights_kernel(int B, int H, int D, int K, const float *
 
 // ----------------------------------------------------------------- blend
 
+// raw[b] = base + sum_k psi[b,k] delta_k (S/model.py:165-185: k ascending, fmaf, psi == 0
+// skipped), TMA-staged: a persistent CTA streams 512-channel tiles of the K delta rows and
+// the base row into shared memory with 1D bulk async copies (one elected thread, an mbarrier
+// per stage, two stages), so ~42 KB per CTA are in flight with no register staging; its 256
+// threads then own 2 channels x all frames each, reading the deltas from shared memory
+// (psi, transposed, broadcast from shared memory four frames per load) and storing each
+// frame's 2 KB row of raw coalesced.  Every delta byte is read from HBM once per step.
+#ifndef HS_BLEND_TE
+#define HS_BLEND_TE 256
+#endif
+#ifndef HS_BLEND_STAGES
+#define HS_BLEND_STAGES 2
+#endif
+constexpr int kBfTE = HS_BLEND_TE;        // channels per tile
+constexpr int kBfT = kBfTE / 2;           // threads per CTA (2 channels each)
+constexpr int kBfS = HS_BLEND_STAGES;     // pipeline stages
+
+__host__ __device__ inline int blend_fwd_bc(int B) { return B <= 4 ? 4 : B <= 8 ? 8 : 16; }
+__host__ __device__ inline int blend_fwd_bpad(int B) {
+    const int bc = blend_fwd_bc(B);
+    return (B + bc - 1) / bc * bc;
+}
+__host__ inline size_t blend_fwd_smem(int K, int B) {
+    return 64 + sizeof(float) * (2 * (size_t)K * blend_fwd_bpad(B) + kBfS * (size_t)(K + 1) * kBfTE);
+}
+
+// One tile: thread owns channels (c, c+1); frames in chunks of BC accumulators (pairs of
+// channels, updated with FFMA2 -- per element exactly fmaf(psi, delta, acc)).  s_psi2 holds
+// psi[b][k] twice per frame ([k][Bp][2]) so one LDS.128 yields two frames' (w, w) pairs.
+template <int BC, bool kAllNonzero>
+__device__ __forceinline__ void blend_fwd_tile(int64_t E, int K, int B, int Bp, const float *s_psi2,
+                                               const float *stage, int64_t e0, float *__restrict__ raw) {
+    const int c = 2 * threadIdx.x;
+    const int64_t e = e0 + c;
+    if (e >= E) return;
+    const float2 bv = *reinterpret_cast<const float2 *>(stage + (size_t)K * kBfTE + c);
+    for (int b0 = 0; b0 < B; b0 += BC) {
+        float2 acc[BC];
+#pragma unroll
+        for (int j = 0; j < BC; ++j) acc[j] = bv;
+        #pragma unroll 4
+        for (int k = 0; k < K; ++k) {
+            const float2 d = *reinterpret_cast<const float2 *>(stage + (size_t)k * kBfTE + c);
+            const float4 *w = reinterpret_cast<const float4 *>(s_psi2 + ((size_t)k * Bp + b0) * 2);
+#pragma unroll
+            for (int j2 = 0; j2 < BC / 2; ++j2) {
+                const float4 w4 = w[j2];                       // (w_j, w_j, w_j+1, w_j+1)
+                if (kAllNonzero) {
+                    acc[2 * j2] = __ffma2_rn(make_float2(w4.x, w4.y), d, acc[2 * j2]);
+                    acc[2 * j2 + 1] = __ffma2_rn(make_float2(w4.z, w4.w), d, acc[2 * j2 + 1]);
+                } else {
+                    if (w4.x != 0.0f) acc[2 * j2] = __ffma2_rn(make_float2(w4.x, w4.y), d, acc[2 * j2]);
+                    if (w4.z != 0.0f) acc[2 * j2 + 1] = __ffma2_rn(make_float2(w4.z, w4.w), d, acc[2 * j2 + 1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < BC; ++j)
+            if (b0 + j < B) __stcs(reinterpret_cast<float2 *>(raw + (int64_t)(b0 + j) * E + e), acc[j]);
+    }
+}
+
+__global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, int B, const float *__restrict__ base,
+                                                             const float *__restrict__ deltas,
+                                                             const float *__restrict__ psi, float *__restrict__ raw) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    const int Bp = blend_fwd_bpad(B);
+    float *s_psi2 = reinterpret_cast<float *>(smem_raw + 64);          // [K][Bp][2]
+    float *stages = s_psi2 + 2 * K * Bp;                                 // kBfS x [(K + 1)][kBfTE]
+    const int64_t ntiles = (E + kBfTE - 1) / kBfTE;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int st = 0; st < kBfS; ++st) mbar_init(&bars[st], 1);
+        mbar_fence_init();
+    }
+    int nz = 1;
+    for (int i = tid; i < K * Bp; i += kBfT) {
+        const int k = i / Bp, b = i % Bp;
+        const float w = b < B ? psi[b * K + k] : 0.f;
+        s_psi2[2 * i] = w;
+        s_psi2[2 * i + 1] = w;
+        nz &= (b >= B) || (w != 0.0f);
+    }
+    const bool all_nonzero = __syncthreads_and(nz);
+    auto issue = [&](int64_t t, int st) {
+        const int64_t e0 = t * kBfTE;
+        const uint32_t bytes = (uint32_t)((E - e0 < kBfTE ? E - e0 : (int64_t)kBfTE) * 4);
+        float *dst = stages + (size_t)st * (K + 1) * kBfTE;
+        mbar_expect_tx(&bars[st], bytes * (K + 1));
+        for (int k = 0; k < K; ++k) bulk_g2s(dst + (size_t)k * kBfTE, deltas + (int64_t)k * E + e0, bytes, &bars[st]);
+        bulk_g2s(dst + (size_t)K * kBfTE, base + e0, bytes, &bars[st]);
+    };
+    if (tid == 0) {
+        for (int st = 0; st < kBfS; ++st)
+            if (blockIdx.x + (int64_t)st * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)st * gridDim.x, st);
+    }
+    uint32_t phase = 0;         // bit st: parity of stage st's next completion
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % kBfS;
+        mbar_wait(&bars[st], (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const float *stage = stages + (size_t)st * (K + 1) * kBfTE;
+        const int64_t e0 = t * kBfTE;
+        if (Bp <= 4) {
+            if (all_nonzero) blend_fwd_tile<4, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
+            else blend_fwd_tile<4, false>(E, K, B, Bp, s_psi2, stage, e0, raw);
+        } else if (Bp <= 8) {
+            if (all_nonzero) blend_fwd_tile<8, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
+            else blend_fwd_tile<8, false>(E, K, B, Bp, s_psi2, stage, e0, raw);
+        } else {
+            if (all_nonzero) blend_fwd_tile<16, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
+            else blend_fwd_tile<16, false>(E, K, B, Bp, s_psi2, stage, e0, raw);
+        }
+        __syncthreads();                      // every thread is done with this stage
+        if (tid == 0 && t + kBfS * (int64_t)gridDim.x < ntiles) issue(t + kBfS * (int64_t)gridDim.x, st);
+    }
+}
+
 // raw[b] = base + sum_k psi[b,k] delta_k over the 10N blended channels.  Each
 // thread owns VEC consecutive channels and keeps BC frames of accumulators, so
 // every delta element is read from HBM once per BC frames (once per step for
@@ -811,7 +931,18 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
 #ifndef HS_BLEND_BC
 #define HS_BLEND_BC 8
 #endif
-    if (vec) {
+#ifndef HS_BLEND_TMA
+#define HS_BLEND_TMA 1
+#endif
+    const size_t tsm = blend_fwd_smem(K, B);
+    if (HS_BLEND_TMA && vec && tsm <= 200 * 1024) {
+        static_assert(kBfTE == 2 * kBfT, "two channels per thread");
+        cudaFuncSetAttribute(blend_fwd_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        const int per_sm = std::max(1, (int)((220 * 1024) / tsm));
+        const int64_t ntiles = (E + kBfTE - 1) / kBfTE;
+        const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * std::min(per_sm, 8));
+        blend_fwd_tma_kernel<<<grid, kBfT, tsm, s>>>(E, K, B, base14, deltas, psi, raw10);
+    } else if (vec) {
         // grid.y splits the frames into chunks of HS_BLEND_BC: few accumulators per
         // thread (occupancy) while the 40 MB of deltas stay L2-resident across chunks
         int64_t nv = E / 4;

@@ -1,0 +1,62 @@
+"""Kernel-level timing of one stage of the C2 step in isolation (after 100 steps):
+    HS_B200_LIB=... python scripts/stage_ab.py <stage> [reps] [flush]
+stage: blend_fwd | blend_bwd | project_fwd | project_bwd | adam.  flush=1 writes 256 MB
+between launches (cold L2), else the stage's inputs may be L2-resident."""
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+
+import bench
+from paper_2503_12886_b200 import _lib as L
+from paper_2503_12886_b200.device import _p
+
+stage = sys.argv[1]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+flush_on = len(sys.argv) > 3 and sys.argv[3] == "1"
+tr, d, wl = bench.make_trainer(bench.CONFIGS["C2"])
+for _ in range(int(os.environ.get("RAB_STEPS", "100"))):
+    tr.step(d["thetas"], d["targets"], None, d["cameras"], d["backgrounds"])
+torch.cuda.synchronize()
+av = tr.av
+N, K, B = av.N, av.K, tr.B
+s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
+frames = tr._last_frames
+F = frames.shape[-2]
+
+
+def call():
+    if stage == "blend_fwd":
+        L.call("hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(tr.psi), _p(tr.raw10), s)
+    elif stage == "blend_bwd":
+        n = ctypes.c_int(0)
+        L.call("hs_blend_bwd", N, K, B, _p(av.deltas), _p(tr.psi), _p(tr.g_raw14), _p(tr.grads),
+               _p(tr.grads[14 * N:]), _p(tr.gpsi_partials), ctypes.byref(n), s)
+    elif stage == "project_bwd":
+        L.call("hs_project_avatar_bwd", B, N, F, _p(tr.raw10), _p(av.base14), _p(av.tri_index), _p(av.barycentric),
+               _p(frames), _p(d["cameras"]), _p(tr.g_splat), _p(tr.g_raw14), s)
+    elif stage == "adam":
+        tr._adam(0, 14 * N + 10 * K * N, 0, s)
+    else:
+        raise SystemExit("unknown stage")
+
+
+times = []
+for r in range(reps + 3):
+    if flush_on:
+        flush.fill_(1.0)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    call()
+    b.record()
+    b.synchronize()
+    if r >= 3:
+        times.append(a.elapsed_time(b))
+t = np.array(times) * 1000
+print(f"{os.path.basename(os.environ.get('HS_B200_LIB', 'default'))} {stage} flush={int(flush_on)}: "
+      f"median {np.median(t):.1f} us (p10 {np.percentile(t, 10):.1f}, p90 {np.percentile(t, 90):.1f})")
