@@ -209,10 +209,16 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   buffers, reset the cursors to the range starts and call again).  Longer lists are
  *   scattered but sorted by hs_tile_fill_longest (up to hs_tile_sort_cap()) or, past the
  *   cap, not at all: then bin that step with the two-level sort instead.
- *   The short lists sort on a library-internal stream (created on the device current at
- *   the first call) that the caller's stream joins before returning work to it: calls
- *   are stream-ordered like any other, but not thread-safe against each other. */
+ *   With a fork context (hs_fork_create, caller-owned) the short lists sort on the
+ *   context's side stream concurrently with the long ones, and the caller's stream joins
+ *   it before the call returns (stream-ordered like any other call); fork == NULL sorts
+ *   both on the caller's stream.  A context serves one caller at a time (one per Trainer
+ *   / thread), so calls with different contexts are re-entrant. */
 int hs_tile_sort_cap(void);
+/* A fork context: a non-blocking side stream and two events on the device current at
+ * creation; destroy it on the same device. */
+void *hs_fork_create(void);
+void hs_fork_destroy(void *fork);
 /* Lists of hs_tile_cta_sort_min()..hs_tile_sort_cap() entries are sorted by
  * hs_tile_fill_longest (one CTA each), which the caller enqueues after hs_tile_fill when
  * the summary's longest list is in that range (arguments as hs_tile_fill). */
@@ -229,7 +235,7 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
                  const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor,
                  uint32_t *lists,
                  uint32_t *list_counts, int list_half, const unsigned long long *summary, uint64_t capacity,
-                 uint32_t *keys, uint32_t *values, void *stream);
+                 uint32_t *keys, uint32_t *values, void *fork, void *stream);
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);
 
@@ -247,8 +253,11 @@ enum {
     HS_RASTER_MAXW_UNVISITED = 8,/* same, only for Gaussians with visited[n] == 0 */
     HS_RASTER_WSUMS = 16,        /* colour-init sums (sum w*target, sum w) for the same set */
     HS_RASTER_WSUMS_IMAGE = 32,  /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
-    HS_RASTER_ORDER_READY = 64   /* hs_raster_train / hs_raster_fwd: the tile order hs_raster_tile_order
+    HS_RASTER_ORDER_READY = 64,  /* hs_raster_train / hs_raster_fwd: the tile order hs_raster_tile_order
                                     built for these ranges is in place (the call skips building it) */
+    HS_RASTER_DETERMINISTIC = 128 /* hs_raster_train / hs_raster_fwd: g_splat and wsums are int64
+                                    fixed-point accumulators (zeroed by the caller, converted with
+                                    hs_fixed_to_float): bitwise run-to-run reproducible sums */
 };
 size_t hs_raster_workspace_size(int B, int width, int height);
 /* The persistent raster's longest-list-first tile order for these ranges, written into
@@ -290,6 +299,9 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
  *   no q pass, full-cover iterations, staged batches, 0], adjoint iterations by the
  *   number of contributing lanes [0, 1, 2, 3-4, 5-8, 9-16, 17-32, 0]. */
 int hs_raster_stats(unsigned long long *host_out, int reset);
+/* out[i] = fixed[i] * 2^-48 (sums == 0: splat gradients) or * 2^-40 (sums != 0: the
+ * colour-init weight sums) -- the HS_RASTER_DETERMINISTIC accumulators as float. */
+int hs_fixed_to_float(int64_t n, const long long *fixed, float *out, int sums, void *stream);
 /* loss_out[b] = sum|pred-target| / (H*W*3), loss_out[B+b] = black-bg L1,
  * loss_out[2B] = mean over frames. */
 int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *loss_partials,

@@ -26,6 +26,7 @@ RASTER_MAXW_UNVISITED = 8
 RASTER_WSUMS = 16
 RASTER_WSUMS_IMAGE = 32
 RASTER_ORDER_READY = 64
+RASTER_DETERMINISTIC = 128
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -60,6 +61,7 @@ SIGNATURES = {
     "hs_loss_reduce": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "hs_raster_train": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P]),
     "hs_raster_workspace_size": (_Z, [_I, _I, _I]),
+    "hs_fixed_to_float": (_I, [_L, _P, _P, _I, _P]),
     "hs_depth_order": (_I, [_L, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "hs_bin_emit_sorted": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_sort_pairs32": (_I, [_L, ctypes.c_uint32, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
@@ -70,7 +72,9 @@ SIGNATURES = {
     "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P, _P]),
     "hs_tile_count": (_I, [_I, _L, _I, _I, _P, _P, _P, _P]),
     "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
-    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P, _P]),
+    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P, _P, _P]),
+    "hs_fork_create": (_P, []),
+    "hs_fork_destroy": (None, [_P]),
     "hs_bin_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_raster_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_adam": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _P]),

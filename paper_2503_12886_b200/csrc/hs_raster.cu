@@ -87,7 +87,22 @@ struct RasterArgs {
     // persistent scheduling (caller workspace, see hs_raster_workspace_size)
     unsigned int *work;
     const uint32_t *tile_order;
+    // HS_RASTER_DETERMINISTIC: g_splat / wsums are int64 fixed-point accumulators
+    int det;
 };
+
+// Deterministic accumulation (HS_RASTER_DETERMINISTIC): every contribution rounded once to
+// a fixed-point int64 (2^-48 resolution for the splat gradients, 2^-40 for the colour-init
+// sums) and added with integer atomics, which are associative -- the totals no longer
+// depend on the order in which warps finish (float atomics do, by an ulp or so).
+constexpr float kFxGrad = 281474976710656.0f;     // 2^48
+constexpr float kFxSums = 1099511627776.0f;       // 2^40
+__device__ __forceinline__ void acc_add(const RasterArgs &a, float *fp, int64_t i, float v, float fx) {
+    if (a.det)
+        atomicAdd(reinterpret_cast<unsigned long long *>(fp) + i, (unsigned long long)__float2ll_rn(v * fx));
+    else
+        atomicAdd(fp + i, v);
+}
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -391,7 +406,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                         int vi;
                         bool issue;
                         const float s = reduce_scatter(v, lane, vi, issue);
-                        if (issue) atomicAdd(a.wsums + g * 4 + vi, s);
+                        if (issue) acc_add(a, a.wsums, g * 4 + vi, s, kFxSums);
                     }
                     if (lane == 0) atomicMax(reinterpret_cast<int *>(a.maxw) + g, __float_as_int(wm));
                 }
@@ -733,15 +748,14 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
         auto flush1 = [&](const float (&gv)[9], uint32_t gidx, bool contrib, uint32_t cmask) {
             if (HS_RASTER_DIRECT && __popc(cmask) <= HS_RASTER_DIRECT) {
                 if (contrib) {
-                    float *gp = a.g_splat + (uint64_t)gidx * kGS;
 #pragma unroll
-                    for (int v = 0; v < 9; ++v) atomicAdd(gp + v, gv[v] * grad_factor(v));
+                    for (int v = 0; v < 9; ++v) acc_add(a, a.g_splat, (int64_t)gidx * kGS + v, gv[v] * grad_factor(v), kFxGrad);
                 }
             } else {
                 int vi;
                 bool issue;
                 const float s = reduce_scatter(gv, lane, vi, issue);
-                if (issue) atomicAdd(a.g_splat + (uint64_t)gidx * kGS + vi, s * grad_factor(vi));
+                if (issue) acc_add(a, a.g_splat, (int64_t)gidx * kGS + vi, s * grad_factor(vi), kFxGrad);
             }
         };
         while (bits) {
@@ -816,6 +830,12 @@ __global__ void loss_mean_kernel(int B, float *__restrict__ out) {
         for (int b = 0; b < B; ++b) s += out[b];
         out[2 * B] = s / (float)B;
     }
+}
+
+__global__ void fixed_to_float_kernel(int64_t n, const long long *__restrict__ fixed, float *__restrict__ out,
+                                      float inv) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (float)((double)fixed[i] * (double)inv);
 }
 
 static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records, const uint32_t *values,
@@ -908,6 +928,7 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     }
     if (int e = check_ws("hs_raster_fwd", workspace)) return e;
     RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
+    a.det = (flags & HS_RASTER_DETERMINISTIC) != 0;
     a.targets = targets;
     a.wsum_image = (flags & HS_RASTER_WSUMS_IMAGE) ? wsum_image : nullptr;
     a.visited = visited;
@@ -965,6 +986,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     }
     if (int e = check_ws("hs_raster_train", workspace)) return e;
     RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
+    a.det = (flags & HS_RASTER_DETERMINISTIC) != 0;
     a.targets = targets;
     a.visited = visited;
     a.maxw = maxw;
@@ -994,6 +1016,13 @@ int hs_raster_stats(unsigned long long *host_out, int reset) {
         cudaMemcpyToSymbol(g_raster_stats, z, sizeof(z));
     }
     return check_launch("hs_raster_stats");
+}
+
+int hs_fixed_to_float(int64_t n, const long long *fixed, float *out, int sums, void *stream) {
+    if (n <= 0) return HS_OK;
+    fixed_to_float_kernel<<<grid_for(n, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(n, fixed, out,
+                                                                                1.0f / (sums ? kFxSums : kFxGrad));
+    return check_launch("hs_fixed_to_float");
 }
 
 int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *loss_partials, float *loss_out,

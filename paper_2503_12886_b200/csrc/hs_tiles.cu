@@ -794,6 +794,15 @@ __global__ void __launch_bounds__(kCtaSortThreads) tile_sort_cta_kernel(
 
 using namespace hs;
 
+namespace hs {
+// caller-owned fork context of hs_tile_fill (see hs_api.h)
+struct HsFork {
+    int device = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t forked = nullptr, joined = nullptr;
+};
+}  // namespace hs
+
 extern "C" {
 
 int hs_tile_sort_cap(void) { return kCtaCap; }
@@ -845,10 +854,33 @@ int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *
     return check_launch("hs_tile_scan");
 }
 
+void *hs_fork_create(void) {
+    HsFork *f = new HsFork();
+    cudaGetDevice(&f->device);
+    if (cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->forked, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->joined, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("hs_fork_create: %s", cudaGetErrorString(cudaGetLastError()));
+        delete f;
+        return nullptr;
+    }
+    return f;
+}
+
+void hs_fork_destroy(void *fork) {
+    HsFork *f = reinterpret_cast<HsFork *>(fork);
+    if (!f) return;
+    cudaStreamSynchronize(f->side);
+    cudaEventDestroy(f->forked);
+    cudaEventDestroy(f->joined);
+    cudaStreamDestroy(f->side);
+    delete f;
+}
+
 int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                  const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
                  uint32_t *list_counts, int list_half, const unsigned long long *summary, uint64_t capacity,
-                 uint32_t *keys, uint32_t *values, void *stream) {
+                 uint32_t *keys, uint32_t *values, void *fork, void *stream) {
     const int64_t items = (int64_t)B * N;
     if (items <= 0) return HS_OK;
     cudaStream_t s = HS_CHECK_STREAM(stream);
@@ -860,30 +892,28 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     tile_scatter_kernel<<<grid_for(items, kTileItems), kTileThreads, tsmem, s>>>(
         items, N, tiles_x, tiles, tile_bits, records, counts, tile_rects, cursor, capacity, summary, keys, values);
     const int sms = current_sm_count();
-    // the long lists first (fewer, longer: their tail overlaps nothing otherwise)
-    // the short lists sort on a library-internal stream alongside the long ones (each
-    // kernel leaves SMs idle in its tail); the caller's stream waits for both
-    static cudaStream_t side = nullptr;
-    static cudaEvent_t scattered = nullptr, shorts_done = nullptr;
-    if (!side) {
-        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&scattered, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&shorts_done, cudaEventDisableTiming);
+    // the long lists first (fewer, longer: their tail overlaps nothing otherwise); the
+    // short lists sort on the fork context's side stream alongside them (each kernel
+    // leaves SMs idle in its tail), and the caller's stream waits for both
+    HsFork *f = reinterpret_cast<HsFork *>(fork);
+    cudaStream_t side = s;
+    if (f) {
+        cudaEventRecord(f->forked, s);
+        cudaStreamWaitEvent(f->side, f->forked, 0);
+        side = f->side;
     }
-    cudaEventRecord(scattered, s);
-    cudaStreamWaitEvent(side, scattered, 0);
 #ifndef HS_SHORT_SORT_CTAS_PER_SM
 #define HS_SHORT_SORT_CTAS_PER_SM 16
 #endif
     tile_sort_warp_kernel<<<(unsigned)sms * HS_SHORT_SORT_CTAS_PER_SM, 32 * kWarpSortWarps, 0, side>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
-    cudaEventRecord(shorts_done, side);
+    if (f) cudaEventRecord(f->joined, f->side);
 #ifndef HS_LONG_SORT_CTAS_PER_SM
 #define HS_LONG_SORT_CTAS_PER_SM 16
 #endif
     tile_sort_long_kernel<<<(unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s>>>(
         N, tile_bits, nseg, depth, ranges, lists, list_counts, list_half, capacity, summary, values);
-    cudaStreamWaitEvent(s, shorts_done, 0);
+    if (f) cudaStreamWaitEvent(s, f->joined, 0);
     return check_launch("hs_tile_fill");
 }
 
@@ -896,12 +926,10 @@ int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *d
     const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
     const int nseg = B << tile_bits;
     const int sms = current_sm_count();
-    static bool attr = false;
     const int csmem = kCtaCap * (int)sizeof(unsigned long long);
-    if (!attr) {
-        cudaFuncSetAttribute(tile_sort_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
-        attr = true;
-    }
+    // (a per-device function attribute: set on every call, so any device a caller drives
+    // has it -- a cheap host call)
+    cudaFuncSetAttribute(tile_sort_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
     tile_sort_cta_kernel<<<(unsigned)sms * 2, kCtaSortThreads, csmem, s>>>(N, tile_bits, nseg, depth, ranges, lists,
                                                                           list_counts, list_half, capacity, summary,
                                                                           values);

@@ -267,6 +267,16 @@ class Binner:
         self.rects = None
         self.mode = None             # how the last bin() built its lists
         self.longest = 0             # longest (frame, tile) list of the last tile-major binning
+        self.fork = None             # hs_fork_create context (side stream of the list sorts)
+
+    def __del__(self):
+        try:
+            if self.fork is not None and self.fork.value:
+                with torch.cuda.device(self._fork_dev):
+                    L.load().hs_fork_destroy(self.fork)
+                self.fork = None
+        except Exception:
+            pass
 
     def _ensure(self, total):
         if total <= self.cap and self.keys is not None:
@@ -447,10 +457,16 @@ class Binner:
         if self.keys is None:
             self._ensure(4 * B * N)         # a first guess; grown below when short
 
+        if self.fork is None:
+            self._fork_dev = torch.cuda.current_device()
+            self.fork = ctypes.c_void_p(L.load().hs_fork_create())
+            if not self.fork.value:
+                raise RuntimeError(f"hs_fork_create: {L.last_error()}")
+
         def fill():
             L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(rects), _p(depth), _p(ranges),
                    _p(self.cursor), _p(self.lists), _p(self.list_counts), self.list_half, _p(self.summary), self.cap,
-                   _p(self.keys), _p(self.vals), s)
+                   _p(self.keys), _p(self.vals), self.fork, s)
         fill()                              # first: the GPU reaches it right after the scan
         self.order_ready = False
         if after_scan is not None:
@@ -534,9 +550,13 @@ class Trainer:
     """
 
     def __init__(self, avatar: AvatarParams, width, height, batch, lrs=None, color_init=True, threshold=0.1,
-                 process_group=None, global_batch=None, frame_offset=0, rig: DeviceRig = None):
+                 process_group=None, global_batch=None, frame_offset=0, rig: DeviceRig = None, deterministic=False):
         require_cuda()
         self.av = avatar
+        # bitwise run-to-run reproducible gradients: the fused raster accumulates the splat
+        # gradients and colour-init sums in int64 fixed point (HS_RASTER_DETERMINISTIC);
+        # every other reduction of the step is already in a fixed order
+        self.deterministic = bool(deterministic)
         self.rig = rig              # DeviceRig: frames computed from theta on device
         self.fused_raster = True    # hs_raster_train (False: hs_raster_fwd + hs_raster_bwd)
         self.two_level_binning = True   # depth order + 32-bit tile sort (False: one 64-bit sort)
@@ -582,6 +602,9 @@ class Trainer:
         self.loss_partials = torch.empty(B * self.tiles * L.LOSS_PARTIALS_PER_TILE, **f32)
         self.loss_out = torch.empty(2 * B + 1, **f32)
         self.g_splat = torch.empty(B * N * 9, **f32)
+        if self.deterministic:
+            self.g_splat_fx = torch.empty(B * N * 9, dtype=torch.int64, device=d)
+            self.wsums_fx = torch.empty(B * N * 4, dtype=torch.int64, device=d)
         # the persistent raster's work counters + item order (zeroed once; per Trainer, so
         # Trainers on different streams / devices never share raster state)
         self.raster_ws = torch.zeros(int(L.load().hs_raster_workspace_size(B, self.W, self.H)), dtype=torch.uint8,
@@ -759,8 +782,14 @@ class Trainer:
         cameras = self._cameras(cameras)
         self._bucket_events = []
         ci = self.color_init and not self._all_visited()
-        # the raster's accumulators are zero-filled by the projection pass
-        zero = (self.g_splat, self.maxw if ci else None, self.wsums if ci else None)
+        det = self.deterministic and self.fused_raster
+        # the raster's accumulators are zero-filled by the projection pass (the int64
+        # fixed-point ones of the deterministic mode by a memset)
+        zero = (None if det else self.g_splat, self.maxw if ci else None, self.wsums if ci and not det else None)
+        if det:
+            self.g_splat_fx.zero_()
+            if ci:
+                self.wsums_fx.zero_()
         self._order_event = None
         F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero,
                                                                           order=self.fused_raster)
@@ -782,11 +811,18 @@ class Trainer:
                 if self.binner.mode == "tiles" and self.binner.order_ready:
                     flags |= L.RASTER_ORDER_READY
                     kernels = 1                 # (the order was counted in _tile_order)
+            if det:
+                flags |= L.RASTER_DETERMINISTIC
             self._call("raster", "hs_raster_train", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), _p(self.visited), _p(self.maxw),
-                       _p(self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale), _p(self.g_splat),
+                       _p(self.wsums_fx if det else self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale),
+                       _p(self.g_splat_fx if det else self.g_splat),
                        _p(self.pix_T) if self.capture_pixels else None,
                        _p(self.pix_state) if self.capture_pixels else None, _p(self.raster_ws), s, kernels=kernels)
+            if det:
+                self._call("raster", "hs_fixed_to_float", B * N * 9, _p(self.g_splat_fx), _p(self.g_splat), 0, s)
+                if ci:
+                    self._call("raster", "hs_fixed_to_float", B * N * 4, _p(self.wsums_fx), _p(self.wsums), 1, s)
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the rest of the backward
             # the loss is only read after the step: reduce it on the side stream
