@@ -252,9 +252,11 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
 // resident first) scans kScanSpan consecutive segments, publishes its total, adds the
 // totals of all CTAs before it (decoupled look-back on aggregates only) and writes its
 // ranges; list appends and the longest list go through global atomics, and the last
-// CTA to finish writes the summary.  list_counts [8 + CTAs] is zeroed by the caller
-// (hs_tile_scan) before the launch: [1] / [2] long / longer lists, [4] the fill's
-// fallback count, [5] ticket, [6] done, [7] longest, [8 + t] CTA t's flagged total.
+// CTA to finish writes the summary.  list_counts alternates between two halves of
+// `half` words (word 0 selects the half being filled; counts_half): in the half of
+// this step [1] / [2] count the long / longer lists, [5] is the CTA ticket, [6] the
+// done count, [7] the longest list and [8 + t] CTA t's flagged total; the last CTA
+// zeroes the other half for the next step, so no host-side reset is needed.
 constexpr int kScanSpan = 1024;
 constexpr uint32_t kAggFlag = 1u << 31;
 
@@ -634,13 +636,15 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, HS_SHORT_SORT_MINB) tile_
 // Each warp sorts a run of kWarpShort entries in registers (the 32-bit keys of
 // sort_list_warp32, on the list-wide depth offset and shift, 10 slot bits); every key
 // then finds its merged position by binary search in the other runs (keys are unique),
-// and the equal-depth-field fix-up runs over the merged list.  Lists the fix-up does
-// not settle go to the 64-bit fallback.
+// and the equal-depth-field fix-up runs over the merged list.  A list the fix-up does
+// not settle is sorted on its full 64-bit keys in place, in the same shared memory.
 #ifndef HS_LONG_RUN
 #define HS_LONG_RUN 256
 #endif
 constexpr int kRun = HS_LONG_RUN;               // entries per warp-sorted run
 constexpr int kLongWarps = kWarpCap / kRun;
+static_assert(kRun >= 32 && kRun <= kWarpCap / 2 && kWarpCap % kRun == 0,
+              "a long list is merged from >= 2 warp runs that fill s_k64[kWarpCap]");
 
 __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
@@ -751,8 +755,9 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
         if (ok) {
             for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) vals[start + q] = (uint32_t)s_k64[s_out[q] & kSlot];
         } else {
-            // the full 64-bit keys are still in shared memory: sort them there (rare)
-            int P = 2 * kRun;
+            // the full 64-bit keys are still in shared memory: sort them there (rare); P is
+            // the next power of two >= len (<= kWarpCap: these lists hold at most kWarpCap)
+            int P = 32;
             while (P < (int)len) P <<= 1;
             for (int q = (int)len + threadIdx.x; q < P; q += blockDim.x) s_k64[q] = ~0ull;
             __syncthreads();
@@ -848,6 +853,10 @@ int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *
         tile_scan_multi_kernel<<<ctas, kScanSpan, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts,
                                                           list_half, err, depth_range, summary);
     } else {
+        if (list_half < 8) {
+            set_error("hs_tile_scan: list_counts halves of %d words, need >= 8", list_half);
+            return HS_ERR_SHAPE;
+        }
         tile_scan_kernel<<<1, 1024, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts, list_half,
                                             err, depth_range, summary);
     }
