@@ -3,10 +3,29 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "../../include/hs_api.h"
 
 namespace hs {
+
+// Device-side bounds checks of the debug build (-DHS_DEBUG_BOUNDS; compute-sanitizer is not
+// available on the GPU pool): a violated index bound prints its site and traps, which
+// fails the launch loudly.  Compiled out otherwise.
+#ifdef HS_DEBUG_BOUNDS
+#define HS_CHECK(cond, what, v)                                                                        \
+    do {                                                                                               \
+        if (!(cond)) {                                                                                 \
+            printf("HS_CHECK failed: %s (%lld) at %s:%d block %d thread %d\n", what, (long long)(v),   \
+                   __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#else
+#define HS_CHECK(cond, what, v) \
+    do {                        \
+    } while (0)
+#endif
 
 // S/render.py:34-37
 constexpr float kNearPlane = 0.01f;

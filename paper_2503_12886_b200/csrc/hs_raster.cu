@@ -98,6 +98,7 @@ struct RasterArgs {
 constexpr float kFxGrad = 281474976710656.0f;     // 2^48
 constexpr float kFxSums = 1099511627776.0f;       // 2^40
 __device__ __forceinline__ void acc_add(const RasterArgs &a, float *fp, int64_t i, float v, float fx) {
+    HS_CHECK(i >= 0 && i < (int64_t)a.B * a.N * (fp == a.wsums ? 4 : kGS), "raster accumulator index", i);
     if (a.det)
         atomicAdd(reinterpret_cast<unsigned long long *>(fp) + i, (unsigned long long)__float2ll_rn(v * fx));
     else
@@ -303,6 +304,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     const int px = x0 + (lane & 7), py0 = y0 + (lane >> 3);      // pixel p: (px, py0 + 4 p)
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
     const uint32_t start = rg.x, end = rg.y;
+    HS_CHECK(start <= end && b < a.B, "raster range", (int64_t)end - start);
     const float bg[3] = {a.bgs[3 * b], a.bgs[3 * b + 1], a.bgs[3 * b + 2]};
     const float2 fpx2 = f2((float)px, (float)px), fpy2 = f2((float)py0, (float)(py0 + 4));
     const uint32_t lanebit = 1u << lane;
@@ -344,6 +346,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         bool hit = false, want = false;
         if (idx < end) {
             const uint32_t n = a.vals[idx];
+            HS_CHECK(n < a.N, "raster list value", n);
             const uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
             hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, x0, y0, wbase + lane * kStageBytes);
             want = CI > 0 && hit && (CI != 3 || !a.visited[n]);   // visited: no colour-init work
@@ -672,6 +675,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             if (bits == 0u) continue;                      // warp-uniform
             if ((bits >> lane) & 1u) {
                 const uint32_t n = a.vals[idx];
+                HS_CHECK(n < a.N, "raster list value", n);
                 stage_splat<false>(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
                                    y0, wbase + lane * kStageBytes);
             }
@@ -679,6 +683,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             bool hit = false;
             if (idx < c_end) {
                 const uint32_t n = a.vals[idx];
+                HS_CHECK(n < a.N, "raster list value", n);
                 hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
                                   y0, wbase + lane * kStageBytes);
             }

@@ -407,6 +407,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
             for (int tx = bx.tx0; tx <= bx.tx1; ++tx) {
                 const uint32_t t = (uint32_t)(ty * tiles_x + tx);
                 const uint32_t pos = local ? atomicAdd(hist + t, 1u) : atomicAdd(cursor + (hi | t), 1u);
+                HS_CHECK(pos < capacity, "tile scatter slot", pos);
                 keys[pos] = hi | t;
                 vals[pos] = it.n[j];
             }
