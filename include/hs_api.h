@@ -202,7 +202,8 @@ int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, v
  *   [2 * (B << tile_bits)] / list_counts [1 + 2 * list_half, zero on first use; list_half
  *   >= 8 + ceil((B << tile_bits) / 1024), the same in every call], the lists the fill sorts
  *   per CTA (list_counts alternates halves between steps: no reset is needed).
- * hs_tile_fill: values [key total] (keys too: the (frame, tile) key of each entry), each
+ * hs_tile_fill: values [key total] (keys, when not NULL: the (frame, tile) key of each entry --
+ *   the raster needs only values and ranges, so the training step passes NULL), each
  *   entry from the items' tile_rects (NULL: from the records' bboxes and counts); each
  *   list of at most hs_tile_cta_sort_min() - 1 entries in (depth, Gaussian index) order --
  *   the reference order.  Skipped on the device when summary[0] > capacity (grow the
@@ -260,6 +261,16 @@ enum {
                                     hs_fixed_to_float): bitwise run-to-run reproducible sums */
 };
 size_t hs_raster_workspace_size(int B, int width, int height);
+/* Optional guard of a raster enqueued before the host has read the step's binning summary
+ * (hs_tile_scan's summary): the launch exits at once -- leaving every output untouched --
+ * unless summary[0] <= capacity (the fill ran), summary[3] <= longest_max (every list
+ * sorted by hs_tile_fill) and summary[1] == HS_NO_ERROR.  The caller re-launches it after
+ * handling the rare case.  NULL (or summary NULL): no guard. */
+typedef struct {
+    const unsigned long long *summary;
+    uint64_t capacity;
+    uint32_t longest_max;
+} hs_raster_guard_t;
 /* The persistent raster's longest-list-first tile order for these ranges, written into
  * the workspace; lets a caller build it off the critical path (e.g. on a side stream
  * while the lists are sorted) and pass HS_RASTER_ORDER_READY to the raster that uses
@@ -274,7 +285,8 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const uint8_t *targets, const float *wsum_image,
                   const uint8_t *visited, float *pix_T, uint32_t *pix_state, float *image,
-                  float *maxw, float *wsums, float *loss_partials, void *workspace, void *stream);
+                  float *maxw, float *wsums, float *loss_partials, const hs_raster_guard_t *guard,
+                  void *workspace, void *stream);
 /* Adjoint (render.py:276-336 _backward_kernel).  grad_image (B,H,W,3) may be NULL:
  * then the L1 gradient sign(pred - target) * grad_scale recorded by the forward is used.
  * g_splat must be zero-filled by the caller (accumulated with atomics after a warp reduce). */
@@ -292,7 +304,8 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
                     const uint32_t *values, const uint32_t *ranges, int tile_bits,
                     const float *backgrounds, const uint8_t *targets, const uint8_t *visited,
                     float *maxw, float *wsums, float *loss_partials, float grad_scale, float *g_splat,
-                    float *pix_T, uint32_t *pix_state, void *workspace, void *stream);
+                    float *pix_T, uint32_t *pix_state, const hs_raster_guard_t *guard, void *workspace,
+                    void *stream);
 /* Diagnostics: raster counters accumulated when built with -DHS_RASTER_STATS (zeros
  * otherwise); synchronous copy to host_out[16]:
  *   forward [warp iterations, pixel tests, q <= qmax, alpha >= 1/255, iterations with

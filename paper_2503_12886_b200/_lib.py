@@ -29,6 +29,11 @@ RASTER_ORDER_READY = 64
 RASTER_DETERMINISTIC = 128
 
 _P = ctypes.c_void_p
+
+
+class RasterGuard(ctypes.Structure):
+    """hs_raster_guard_t"""
+    _fields_ = [("summary", ctypes.c_void_p), ("capacity", ctypes.c_uint64), ("longest_max", ctypes.c_uint32)]
 _I = ctypes.c_int
 _L = ctypes.c_int64
 _F = ctypes.c_float
@@ -56,10 +61,10 @@ SIGNATURES = {
     "hs_sort_workspace_size": (_Z, [_L]),
     "hs_sort_pairs": (_I, [_L, ctypes.c_uint64, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges": (_I, [_L, _P, _P, _P]),
-    "hs_raster_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_raster_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_raster_bwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _F, _P, _P, _P]),
     "hs_loss_reduce": (_I, [_I, _I, _I, _I, _P, _P, _P]),
-    "hs_raster_train": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P]),
+    "hs_raster_train": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P, _P]),
     "hs_raster_workspace_size": (_Z, [_I, _I, _I]),
     "hs_fixed_to_float": (_I, [_L, _P, _P, _I, _P]),
     "hs_depth_order": (_I, [_L, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),

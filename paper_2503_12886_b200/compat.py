@@ -431,7 +431,7 @@ def _raster_batch(dev, backgrounds, flags=L.RASTER_IMAGE | L.RASTER_MAXW_ALL, ws
         flags |= L.RASTER_WSUMS | L.RASTER_WSUMS_IMAGE | L.RASTER_MAXW_ALL
     L.call("hs_raster_fwd", B, n, W, H, flags, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(bgs), None,
            _p(wimg), None, _p(out["pix_T"]), _p(out["pix_state"]), _p(out["image"]), _p(out["maxw"]),
-           _p(out["wsums"]), None, _p(dev["raster_ws"]), _stream())
+           _p(out["wsums"]), None, None, _p(dev["raster_ws"]), _stream())
     return out
 
 

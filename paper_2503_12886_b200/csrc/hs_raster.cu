@@ -89,7 +89,21 @@ struct RasterArgs {
     const uint32_t *tile_order;
     // HS_RASTER_DETERMINISTIC: g_splat / wsums are int64 fixed-point accumulators
     int det;
+    // speculative launch guard (hs_raster_guard_t): the binning summary and the limits
+    // under which its lists are complete; NULL: no guard
+    const unsigned long long *guard;
+    unsigned long long guard_capacity;
+    unsigned int guard_longest;
 };
+
+// A raster enqueued before the host has read the step's binning summary (the one host
+// sync) exits at once unless the lists are complete: the fill ran (key total within the
+// buffers), no list needs the CTA / two-level sorts, and no error was flagged.  The host
+// re-launches it after fixing up the rare case.
+__device__ __forceinline__ bool guard_blocks(const RasterArgs &a) {
+    if (a.guard == nullptr) return false;
+    return a.guard[0] > a.guard_capacity || a.guard[3] > a.guard_longest || a.guard[1] != HS_NO_ERROR;
+}
 
 // Deterministic accumulation (HS_RASTER_DETERMINISTIC): every contribution rounded once to
 // a fixed-point int64 (2^-48 resolution for the splat gradients, 2^-40 for the colour-init
@@ -594,6 +608,7 @@ __device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, in
 
 template <bool kLoss, bool kImage, int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a, int nblk) {
+    if (guard_blocks(a)) return;
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * kWarpSmem;
@@ -789,6 +804,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
 // forward's per-batch hit masks.
 template <int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
+    if (guard_blocks(a)) return;
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     __shared__ uint32_t s_masks[kCW][kMaskBatches];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -892,6 +908,14 @@ static dim3 raster_grid(int nblk, int B) {
     return dim3((unsigned)std::max<int64_t>(1, std::min(want, items)), 1);
 }
 
+static void take_guard(RasterArgs &a, const hs_raster_guard_t *g) {
+    if (g != nullptr && g->summary != nullptr) {
+        a.guard = g->summary;
+        a.guard_capacity = g->capacity;
+        a.guard_longest = g->longest_max;
+    }
+}
+
 static int check_ws(const char *fn, void *ws) {
     if (ws == nullptr || (reinterpret_cast<uintptr_t>(ws) & 15u)) {
         set_error("%s: workspace must be a 16-byte aligned device buffer of hs_raster_workspace_size() bytes", fn);
@@ -908,6 +932,8 @@ extern "C" {
 
 size_t hs_raster_workspace_size(int B, int width, int height) { return workspace_bytes(B, width, height); }
 
+
+
 int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, int tile_bits, void *workspace,
                          void *stream) {
     if (int e = check_ws("hs_raster_tile_order", workspace)) return e;
@@ -919,7 +945,8 @@ int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, i
 int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records, const uint32_t *values,
                   const uint32_t *ranges, int tile_bits, const float *backgrounds, const uint8_t *targets,
                   const float *wsum_image, const uint8_t *visited, float *pix_T, uint32_t *pix_state, float *image,
-                  float *maxw, float *wsums, float *loss_partials, void *workspace, void *stream) {
+                  float *maxw, float *wsums, float *loss_partials, const hs_raster_guard_t *guard, void *workspace,
+                  void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const bool loss = flags & HS_RASTER_LOSS, img = flags & HS_RASTER_IMAGE;
     int ci = 0;
@@ -934,6 +961,7 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     if (int e = check_ws("hs_raster_fwd", workspace)) return e;
     RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
     a.det = (flags & HS_RASTER_DETERMINISTIC) != 0;
+    take_guard(a, guard);
     a.targets = targets;
     a.wsum_image = (flags & HS_RASTER_WSUMS_IMAGE) ? wsum_image : nullptr;
     a.visited = visited;
@@ -978,7 +1006,8 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
 int hs_raster_train(int B, int64_t N, int width, int height, int flags, const float *records, const uint32_t *values,
                     const uint32_t *ranges, int tile_bits, const float *backgrounds, const uint8_t *targets,
                     const uint8_t *visited, float *maxw, float *wsums, float *loss_partials, float grad_scale,
-                    float *g_splat, float *pix_T, uint32_t *pix_state, void *workspace, void *stream) {
+                    float *g_splat, float *pix_T, uint32_t *pix_state, const hs_raster_guard_t *guard,
+                    void *workspace, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     int ci = 0;
     if (flags & HS_RASTER_MAXW_UNVISITED) ci = 3;
@@ -992,6 +1021,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     if (int e = check_ws("hs_raster_train", workspace)) return e;
     RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
     a.det = (flags & HS_RASTER_DETERMINISTIC) != 0;
+    take_guard(a, guard);
     a.targets = targets;
     a.visited = visited;
     a.maxw = maxw;

@@ -408,9 +408,79 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
                 const uint32_t t = (uint32_t)(ty * tiles_x + tx);
                 const uint32_t pos = local ? atomicAdd(hist + t, 1u) : atomicAdd(cursor + (hi | t), 1u);
                 HS_CHECK(pos < capacity, "tile scatter slot", pos);
-                keys[pos] = hi | t;
+                if (keys) keys[pos] = hi | t;
                 vals[pos] = it.n[j];
             }
+    }
+}
+
+// Warp-flattened scatter (the training path, packed tile rectangles): a warp takes 32
+// consecutive (frame, Gaussian) items, scans their rectangle areas, and then walks the
+// resulting (item, tile) keys 32 at a time -- every lane one key, whatever the rectangle
+// sizes (the per-item tile loops of tile_scatter_kernel left ~12 of 32 lanes active).
+// A key finds its item by a binary search over the scan (shuffles), and lanes holding
+// the same (frame, tile) key take consecutive slots behind one global atomic per group
+// (__match_any_sync).  Slot order inside a list is arbitrary; the list sorts fix it.
+#ifndef HS_SCATTER_WARP_ROUNDS
+#define HS_SCATTER_WARP_ROUNDS 1
+#endif
+constexpr int kSwRounds = HS_SCATTER_WARP_ROUNDS;   // 32-item rounds per warp
+__global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, int64_t N, int tiles_x, int tile_bits,
+                                                                const uint32_t *__restrict__ rects,
+                                                                uint32_t *__restrict__ cursor, uint64_t capacity,
+                                                                const unsigned long long *__restrict__ summary,
+                                                                uint32_t *__restrict__ keys,
+                                                                uint32_t *__restrict__ vals) {
+    if (summary[0] > capacity) return;               // the caller grows the buffers and re-runs
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+#pragma unroll 1
+    for (int rd = 0; rd < kSwRounds; ++rd) {
+        const int64_t i = (warp * kSwRounds + rd) * 32 + lane;
+        if ((warp * kSwRounds + rd) * 32 >= items) break;                 // warp-uniform
+        const uint32_t r = i < items ? rects[i] : 0x00010001u;            // dead: ty0 > ty1
+        const int ty0 = r & 0xFF, ty1 = (r >> 8) & 0xFF, tx0 = (r >> 16) & 0xFF, tx1 = r >> 24;
+        const int w = tx1 - tx0 + 1;
+        const uint32_t c = ty0 <= ty1 ? (uint32_t)((ty1 - ty0 + 1) * w) : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t excl = incl - c, total = __shfl_sync(0xffffffffu, incl, 31);
+        const int64_t b = i / N;
+        const uint32_t n = (uint32_t)(i - b * N), hi = (uint32_t)b << tile_bits;
+        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const bool act = k < total;
+            // the item of key k: the largest lane whose exclusive offset is <= k (lanes with
+            // no keys share their offset with the next lane, so the search lands past them)
+            int o = 0;
+#pragma unroll
+            for (int st = 16; st; st >>= 1) {
+                const uint32_t e = __shfl_sync(0xffffffffu, excl, o + st);
+                if (e <= k) o += st;
+            }
+            const uint32_t lo = k - __shfl_sync(0xffffffffu, excl, o);
+            const uint32_t ro = __shfl_sync(0xffffffffu, r, o);
+            const uint32_t no = __shfl_sync(0xffffffffu, n, o), ho = __shfl_sync(0xffffffffu, hi, o);
+            const uint32_t wo = (ro >> 24) - ((ro >> 16) & 0xFFu) + 1u;
+            const uint32_t dy = lo / wo, dx = lo - dy * wo;
+            const uint32_t key = ho | ((( ro & 0xFFu) + dy) * (uint32_t)tiles_x + ((ro >> 16) & 0xFFu) + dx);
+            const uint32_t grp = __match_any_sync(0xffffffffu, act ? key : 0xFFFFFFFFu);
+            const int leader = __ffs(grp) - 1;
+            uint32_t base = 0;
+            if (act && lane == leader) base = atomicAdd(cursor + key, (uint32_t)__popc(grp));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (act) {
+                const uint32_t pos = base + (uint32_t)__popc(grp & lt_mask);
+                HS_CHECK(pos < capacity, "tile scatter slot", pos);
+                vals[pos] = no;
+                if (keys) keys[pos] = key;
+            }
+        }
     }
 }
 
@@ -899,8 +969,17 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
     const int nseg = B << tile_bits;
     const int tiles = tiles_x * tiles_y;
     const size_t tsmem = tiles <= kTileSmemBins ? sizeof(uint32_t) * tiles : 0;
-    tile_scatter_kernel<<<grid_for(items, kTileItems), kTileThreads, tsmem, s>>>(
-        items, N, tiles_x, tiles, tile_bits, records, counts, tile_rects, cursor, capacity, summary, keys, values);
+#ifndef HS_SCATTER_WARP
+#define HS_SCATTER_WARP 1
+#endif
+    if (HS_SCATTER_WARP && tile_rects && tiles_x <= 256) {
+        const int64_t warps = (items + 32 * kSwRounds - 1) / (32 * kSwRounds);
+        tile_scatter_warp_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(items, N, tiles_x, tile_bits, tile_rects,
+                                                                            cursor, capacity, summary, keys, values);
+    } else {
+        tile_scatter_kernel<<<grid_for(items, kTileItems), kTileThreads, tsmem, s>>>(
+            items, N, tiles_x, tiles, tile_bits, records, counts, tile_rects, cursor, capacity, summary, keys, values);
+    }
     const int sms = current_sm_count();
     // the long lists first (fewer, longer: their tail overlaps nothing otherwise); the
     // short lists sort on the fork context's side stream alongside them (each kernel

@@ -268,6 +268,9 @@ class Binner:
         self.mode = None             # how the last bin() built its lists
         self.longest = 0             # longest (frame, tile) list of the last tile-major binning
         self.fork = None             # hs_fork_create context (side stream of the list sorts)
+        # tile-major binning writes the (frame, tile) key of every entry only when asked
+        # (checkers); the raster reads values and ranges only
+        self.write_keys = True
 
     def __del__(self):
         try:
@@ -430,7 +433,7 @@ class Binner:
         return self.rects[:B * N]
 
     def bin_tiles(self, B, N, width, height, records, depth, counts, err, after_scan=None, counted=False,
-                  rects=None):
+                  rects=None, speculate=None):
         """Tile-major binning (hs_tile_count / hs_tile_scan / hs_tile_fill) with the
         step's single host read: the scatter and the per-list sorts are enqueued before
         the host waits, sized by the previous step's capacity; a step that needs more
@@ -466,11 +469,20 @@ class Binner:
         def fill():
             L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(rects), _p(depth), _p(ranges),
                    _p(self.cursor), _p(self.lists), _p(self.list_counts), self.list_half, _p(self.summary), self.cap,
-                   _p(self.keys), _p(self.vals), self.fork, s)
+                   _p(self.keys) if self.write_keys else None, _p(self.vals), self.fork, s)
         fill()                              # first: the GPU reaches it right after the scan
         self.order_ready = False
         if after_scan is not None:
             self.order_ready = after_scan(ranges, tile_bits, ready)
+        # the consumer of the lists, enqueued before the host reads the summary: it runs
+        # right after the fill unless the device-side guard (hs_raster_guard_t) finds the
+        # lists incomplete, in which case it exits and spec_valid tells the caller to
+        # launch it again once the rare case is handled
+        cap_at_fill = self.cap
+        self.spec_valid = False
+        if speculate is not None:
+            guard = L.RasterGuard(self.summary.data_ptr(), cap_at_fill, _cta_sort_min() - 1)
+            speculate(self.vals[:cap_at_fill], ranges, tile_bits, guard)
         ready.synchronize()
         total = int(self.summary_host[0])
         code = int(self.summary_host[1]) & 0xFFFFFFFFFFFFFFFF
@@ -482,7 +494,7 @@ class Binner:
             self._ensure(total)
             self.cursor[:nseg].copy_(ranges.view(-1, 2)[:, 0])
             fill()
-        if int(L.load().hs_tile_cta_sort_min()) <= self.longest <= tile_sort_cap():
+        if _cta_sort_min() <= self.longest <= tile_sort_cap():
             # lists long enough for the shared-memory CTA sort (rare): after the fill
             L.call("hs_tile_fill_longest", B, N, width, height, _p(depth), _p(ranges), _p(self.lists),
                    _p(self.list_counts), self.list_half, _p(self.summary), self.cap, _p(self.vals), s)
@@ -490,6 +502,8 @@ class Binner:
         else:
             self.launches_extra = 0
         self._depth_range_clean = self.longest <= tile_sort_cap()
+        self.spec_valid = (speculate is not None and total <= cap_at_fill and self.longest < _cta_sort_min()
+                           and code == L.HS_NO_ERROR)
         if self.longest > tile_sort_cap():
             # a list too long to sort in shared memory: the global two-level sort
             # (whose ranges replace the ones the tile order was built from)
@@ -504,6 +518,14 @@ class Binner:
 
 
 _SORT_CAP = None
+_CTA_MIN = None
+
+
+def _cta_sort_min():
+    global _CTA_MIN
+    if _CTA_MIN is None:
+        _CTA_MIN = int(L.load().hs_tile_cta_sort_min())
+    return _CTA_MIN
 
 
 def tile_sort_cap():
@@ -591,6 +613,7 @@ class Trainer:
         # pixels a parity test excludes) on the current stream
         self.debug_before_backward = None
         self.capture_pixels = False     # fused raster also writes pix_T / pix_state (checker)
+        self.speculative = True         # enqueue the raster before the step's host sync (guarded)
         self.counts = torch.empty(B * N, dtype=torch.int32, device=d)
         self.nblocks = int(L.load().hs_scan_blocks(B * N))
         self.block_sums = torch.empty(self.nblocks, dtype=torch.int32, device=d)
@@ -616,6 +639,7 @@ class Trainer:
         self.packed = torch.empty(N, dtype=torch.int64, device=d)
         self.est4 = torch.empty(N * 4, **f32)
         self.binner = Binner(d)
+        self.binner.write_keys = False
         self.last_total = 0
         self.launches = 0           # libhs_b200 kernel launches issued so far
         self.events = None          # {stage: [(start, end), ...]} when profiling is enabled
@@ -713,7 +737,7 @@ class Trainer:
             self._side = torch.cuda.Stream(device=self.av.device)
         return self._side
 
-    def _forward_project(self, thetas, frames, cameras, zero=(None, None, None), order=False):
+    def _forward_project(self, thetas, frames, cameras, zero=(None, None, None), order=False, speculate=None):
         av = self.av
         N, K, B = av.N, av.K, self.B
         self._cur = torch.cuda.current_stream()     # the step's compute stream (looked up once)
@@ -738,7 +762,7 @@ class Trainer:
             m = self._mark("bin_tiles")
             total, code = self.binner.bin_tiles(B, N, self.W, self.H, self.records, self.depth, self.counts,
                                                 self.err, self._tile_order if order else None, counted=True,
-                                                rects=rects)
+                                                rects=rects, speculate=speculate)
             self._done(m)
             self.launches += launches_tiles(self.binner)
             # (the scan reset the error word after reading it into the summary)
@@ -791,34 +815,44 @@ class Trainer:
             if ci:
                 self.wsums_fx.zero_()
         self._order_event = None
-        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero,
-                                                                          order=self.fused_raster)
-        frames = self._last_frames
-        s = _stream()
         flags = L.RASTER_LOSS
         if ci:
             flags |= L.RASTER_MAXW_UNVISITED | L.RASTER_WSUMS
-        if self._targets_ready is not None:     # step_from_host: targets arrive on the copy stream
-            self._cur.wait_event(self._targets_ready)
-            self._targets_ready = None
+        if det:
+            flags |= L.RASTER_DETERMINISTIC
         # d loss_b / d pred = sign / (H W 3) / B_global  (S/metrics.py:19-22, S/train.py:244)
         grad_scale = 1.0 / (self.H * self.W * 3.0) / self.global_batch
-        if self.fused_raster:
+
+        def raster(vals, ranges, tile_bits, guard=None):
             # forward + adjoint of every pixel block in one pass (hs_raster_train)
-            kernels = 2                         # tile order + the fused raster
-            if self._order_event is not None:   # built on the side stream (see _tile_order)
+            s = _stream()
+            if self._targets_ready is not None:     # step_from_host: targets arrive on the copy stream
+                self._cur.wait_event(self._targets_ready)
+                self._targets_ready = None
+            fl, kernels = flags, 2                  # tile order + the fused raster
+            if self._order_event is not None:       # built on the side stream (see _tile_order)
                 self._cur.wait_event(self._order_event)
-                if self.binner.mode == "tiles" and self.binner.order_ready:
-                    flags |= L.RASTER_ORDER_READY
-                    kernels = 1                 # (the order was counted in _tile_order)
-            if det:
-                flags |= L.RASTER_DETERMINISTIC
-            self._call("raster", "hs_raster_train", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
+                if self.binner.order_ready and (guard is not None or self.binner.mode == "tiles"):
+                    fl |= L.RASTER_ORDER_READY
+                    kernels = 1                     # (the order was counted in _tile_order)
+            self._call("raster", "hs_raster_train", B, N, self.W, self.H, fl, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), _p(self.visited), _p(self.maxw),
                        _p(self.wsums_fx if det else self.wsums), _p(self.loss_partials), ctypes.c_float(grad_scale),
                        _p(self.g_splat_fx if det else self.g_splat),
                        _p(self.pix_T) if self.capture_pixels else None,
-                       _p(self.pix_state) if self.capture_pixels else None, _p(self.raster_ws), s, kernels=kernels)
+                       _p(self.pix_state) if self.capture_pixels else None,
+                       ctypes.byref(guard) if guard is not None else None, _p(self.raster_ws), s, kernels=kernels)
+
+        # fused raster: enqueued speculatively before the step's host sync (device-guarded,
+        # see Binner.bin_tiles), so the GPU goes from the list sorts straight into it
+        spec = raster if (self.fused_raster and self.tile_binning and self.speculative) else None
+        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero,
+                                                                          order=self.fused_raster, speculate=spec)
+        frames = self._last_frames
+        s = _stream()
+        if self.fused_raster:
+            if spec is None or not self.binner.spec_valid:
+                raster(vals, ranges, tile_bits)
             if det:
                 self._call("raster", "hs_fixed_to_float", B * N * 9, _p(self.g_splat_fx), _p(self.g_splat), 0, s)
                 if ci:
@@ -838,9 +872,12 @@ class Trainer:
             self._side_events.append(loss_ev)
             self._loss_event = loss_ev
         else:
+            if self._targets_ready is not None:
+                self._cur.wait_event(self._targets_ready)
+                self._targets_ready = None
             self._call("raster_fwd", "hs_raster_fwd", B, N, self.W, self.H, flags, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(targets), None, _p(self.visited), _p(self.pix_T),
-                       _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials),
+                       _p(self.pix_state), None, _p(self.maxw), _p(self.wsums), _p(self.loss_partials), None,
                        _p(self.raster_ws), s)
             if ci and self.pg is not None:
                 self._color_collectives()   # on the comm stream, overlapping the backward
@@ -981,17 +1018,25 @@ class Trainer:
         av = self.av
         cameras = self._cameras(cameras)
         self._order_event = None
-        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, order=True)
         if out is None:
             out = torch.empty(self.B, self.H, self.W, 3, dtype=torch.float32, device=av.device)
-        flags = L.RASTER_IMAGE
-        if self._order_event is not None:       # built on the side stream (see _tile_order)
-            self._cur.wait_event(self._order_event)
-            if self.binner.mode == "tiles" and self.binner.order_ready:
-                flags |= L.RASTER_ORDER_READY
-        self._call("raster_fwd", "hs_raster_fwd", self.B, av.N, self.W, self.H, flags, _p(self.records),
-                   _p(vals), _p(ranges), tile_bits, _p(backgrounds), None, None, None, _p(self.pix_T),
-                   _p(self.pix_state), _p(out), None, None, None, _p(self.raster_ws), _stream())
+
+        def raster(vals, ranges, tile_bits, guard=None):
+            flags = L.RASTER_IMAGE
+            if self._order_event is not None:       # built on the side stream (see _tile_order)
+                self._cur.wait_event(self._order_event)
+                if self.binner.order_ready and (guard is not None or self.binner.mode == "tiles"):
+                    flags |= L.RASTER_ORDER_READY
+            self._call("raster_fwd", "hs_raster_fwd", self.B, av.N, self.W, self.H, flags, _p(self.records),
+                       _p(vals), _p(ranges), tile_bits, _p(backgrounds), None, None, None, _p(self.pix_T),
+                       _p(self.pix_state), _p(out), None, None, None,
+                       ctypes.byref(guard) if guard is not None else None, _p(self.raster_ws), _stream())
+
+        spec = raster if (self.tile_binning and self.speculative) else None
+        F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, order=True,
+                                                                          speculate=spec)
+        if spec is None or not self.binner.spec_valid:
+            raster(vals, ranges, tile_bits)
         return out
 
     # -------------------------------------------------------------- end to end

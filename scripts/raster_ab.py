@@ -33,7 +33,7 @@ for r in range(reps + 3):
     a.record()
     L.call("hs_raster_train", B, N, tr.W, tr.H, flags, _p(tr.records), _p(vals), _p(ranges), tile_bits,
            _p(d["backgrounds"]), _p(d["targets"]), _p(tr.visited), _p(tr.maxw), _p(tr.wsums), _p(tr.loss_partials),
-           ctypes.c_float(1.0 / (tr.H * tr.W * 3.0) / B), _p(tr.g_splat), None, None, _p(tr.raster_ws),
+           ctypes.c_float(1.0 / (tr.H * tr.W * 3.0) / B), _p(tr.g_splat), None, None, None, _p(tr.raster_ws),
            ctypes.c_void_p(s.cuda_stream))
     b.record()
     b.synchronize()

@@ -30,8 +30,23 @@ frames = tr._last_frames
 F = frames.shape[-2]
 
 
+bn = tr.binner
+keys_, vals_, ranges_, tile_bits_, tiles_ = bn.result
+nseg = B << tile_bits_
+
+
+def prep():
+    if stage == "fill":        # the fill consumes the scan's cursors: reset them (untimed)
+        bn.cursor[:nseg].copy_(ranges_.view(-1, 2)[:, 0])
+
+
 def call():
-    if stage == "blend_fwd":
+    if stage == "fill":
+        rects = bn.tile_rects_buffer(B, N, tr.W, tr.H)
+        L.call("hs_tile_fill", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts), _p(rects), _p(tr.depth),
+               _p(ranges_), _p(bn.cursor), _p(bn.lists), _p(bn.list_counts), bn.list_half, _p(bn.summary), bn.cap,
+               None, _p(bn.vals), bn.fork, s)
+    elif stage == "blend_fwd":
         L.call("hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(tr.psi), _p(tr.raw10), s)
     elif stage == "blend_bwd":
         n = ctypes.c_int(0)
@@ -50,6 +65,7 @@ times = []
 for r in range(reps + 3):
     if flush_on:
         flush.fill_(1.0)
+    prep()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     call()

@@ -223,6 +223,7 @@ def test_c2_full_size_properties():
     B = 16
     tr = Trainer(dev, 512, 512, B)
     tr.radius = torch.empty(B * dev.N, device="cuda")
+    tr.binner.write_keys = True                  # (the step itself does not need the keys)
     cams = torch.from_numpy(np.tile(wl.camera.packed(), (B, 1))).cuda()
     th = torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda()
     fr = torch.from_numpy(wl.frames).cuda()
@@ -400,3 +401,43 @@ def test_c3_render_vs_oracle():
         print(f"C3 frame {b}: max-abs {err:.2e}, masked {int(mask.sum())} of {mask.size}")
         assert err <= 1e-4, (b, err)
     assert masked <= 1e-2 * 4 * 512 * 512
+
+
+@pytest.mark.parametrize("case", ["valid", "regrow", "crowded"])
+def test_speculative_raster(case):
+    """The fused raster enqueued before the step's host sync (hs_raster_guard_t): when the
+    lists are complete it is the step's raster (spec_valid); when the fill was skipped
+    (buffers too small: regrow) or a list needs the CTA / two-level sorts (crowded), it
+    exits on the device and the re-launch gives the same result as a non-speculative
+    step (deterministic mode: bitwise)."""
+    from bench_support import synth
+    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    uv, size = (140, 64) if case == "crowded" else (64, 192)
+    wl = synth.make_workload(uv, 4, size)
+    av = wl.avatar
+    base = {a: np.array(av.base[a], copy=True) for a in ATTRS}
+    if case == "crowded":
+        base["scale"] = base["scale"] + 2.0
+    mk = lambda: Trainer(AvatarParams.from_host(O.GSet(*(base[a] for a in ATTRS)), av.deltas, av.mlp,
+                                                av.tri_index, av.barycentric), size, size, 4, deterministic=True)
+    th = torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda()
+    tg = torch.from_numpy(wl.targets).cuda()
+    fr = torch.from_numpy(wl.frames).cuda()
+    cams = torch.from_numpy(np.tile(wl.camera.packed(), (4, 1))).cuda()
+    bg = torch.from_numpy(np.asarray(wl.backgrounds, np.float32)).cuda()
+    a, b = mk(), mk()
+    b.speculative = False
+    for step in range(2):
+        if case == "regrow" and step == 0:
+            a.binner._ensure(1)
+            a.binner.cap = 1
+        la = a.step(th, tg, fr, cams, bg).clone()
+        lb = b.step(th, tg, fr, cams, bg).clone()
+        torch.cuda.synchronize()
+        if case == "valid" or step == 1 and case == "regrow":
+            assert a.binner.spec_valid
+        elif step == 0:
+            assert not a.binner.spec_valid, (case, a.binner.longest)
+        assert torch.equal(la, lb)
+        assert torch.equal(a.grads, b.grads)
+    assert torch.equal(a.av.params, b.av.params)
