@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(int nb, const uint32_t *__re
                                                     const unsigned long long *__restrict__ err,
                                                     const uint32_t *__restrict__ depth_range,
                                                     unsigned long long *__restrict__ summary) {
+    pdl_prologue();
     __shared__ unsigned long long warp_tot[32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int per = (nb + blockDim.x - 1) / blockDim.x;
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
                                                           const uint32_t *__restrict__ offs,
                                                           uint64_t *__restrict__ keys,
                                                           uint32_t *__restrict__ vals) {
+    pdl_prologue();
     __shared__ uint32_t warp_tot[kScanBlock / 32];
     const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
     const bool in = i < (int64_t)B * N;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
 __global__ void __launch_bounds__(kScanBlock) sorted_block_sums_kernel(int64_t items, const uint32_t *__restrict__ order,
                                                                        const uint32_t *__restrict__ counts,
                                                                        uint32_t *__restrict__ block_sums) {
+    pdl_prologue();
     const int64_t j = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
     uint32_t v = j < items ? counts[order[j]] : 0u;
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_sorted_kernel(int64_t items, 
                                                                  const uint32_t *__restrict__ offs,
                                                                  uint32_t *__restrict__ keys,
                                                                  uint32_t *__restrict__ vals) {
+    pdl_prologue();
     __shared__ uint32_t warp_tot[kScanBlock / 32];
     const int64_t j = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
     const bool in = j < items;
@@ -193,6 +197,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_sorted_kernel(int64_t items, 
 }
 
 __global__ void tile_ranges32_kernel(int64_t n, const uint32_t *__restrict__ keys, uint32_t *__restrict__ ranges) {
+    pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t t = keys[i];
@@ -243,6 +248,7 @@ struct PassShifts {
 template <typename KT>
 __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const KT *__restrict__ keys,
                                                              PassShifts ps, uint32_t *__restrict__ hist) {
+    pdl_prologue();
     __shared__ uint32_t h[kMaxPasses][kRadix];
     for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
@@ -277,6 +283,7 @@ __global__ void __launch_bounds__(256) radix_hist_all_kernel(int64_t n, const KT
 
 // exclusive scan of each pass's 256 digit counts (one CTA, one thread per digit)
 __global__ void __launch_bounds__(kRadix) radix_digit_scan_kernel(int npass, uint32_t *__restrict__ hist) {
+    pdl_prologue();
     __shared__ uint32_t warp_tot[kRadix / 32];
     const int d = threadIdx.x, lane = d & 31, w = d >> 5;
     for (int p = 0; p < npass; ++p) {
@@ -328,6 +335,7 @@ __global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_ker
                                                                       uint32_t *__restrict__ status,
                                                                       uint32_t *__restrict__ counter,
                                                                       const uint32_t *__restrict__ live_bits) {
+    pdl_prologue();
     if (live_bits && ((depth_live_bits(live_bits) >> shift) & (kRadix - 1)) == 0u) {
         for (int64_t i = blockIdx.x * (int64_t)kSortTile + threadIdx.x; i < n && i < (blockIdx.x + 1) * (int64_t)kSortTile;
              i += kSortThreads) {
@@ -456,6 +464,7 @@ __global__ void __launch_bounds__(kSortThreads, HS_SORT_MINB) radix_onesweep_ker
 // ----------------------------------------------------------------- ranges
 
 __global__ void tile_ranges_kernel(int64_t n, const uint64_t *__restrict__ keys, uint32_t *__restrict__ ranges) {
+    pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t t = keys[i] >> 32;
@@ -471,7 +480,7 @@ extern "C" {
 
 int hs_bin_scan(int num_blocks, const uint32_t *block_sums, uint32_t *block_offsets, const unsigned long long *err,
                 const uint32_t *depth_range, unsigned long long *summary, void *stream) {
-    scan_kernel<<<1, 1024, 0, HS_CHECK_STREAM(stream)>>>(num_blocks, block_sums, block_offsets, err, depth_range,
+    launch_k(scan_kernel, 1, 1024, 0, HS_CHECK_STREAM(stream), num_blocks, block_sums, block_offsets, err, depth_range,
                                                          summary);
     return check_launch("hs_bin_scan");
 }
@@ -487,7 +496,7 @@ int hs_bin_emit(int B, int64_t N, int width, int height, const float *records, c
         return HS_ERR_SHAPE;
     }
     const int64_t items = (int64_t)B * N;
-    emit_kernel<<<hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream)>>>(
+    launch_k(emit_kernel, hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream), 
         B, N, tiles_x, tile_bits, records, depth, counts, block_offsets, keys, values);
     return check_launch("hs_bin_emit");
 }
@@ -534,8 +543,8 @@ static int sort_pairs_impl(const char *what, int64_t num_keys, uint64_t bit_mask
 #define HS_HIST_CTAS_PER_SM 4
 #endif
     const unsigned hgrid = (unsigned)std::min<int64_t>(grid_for(num_keys, 256 * 8), (int64_t)sms * HS_HIST_CTAS_PER_SM);
-    radix_hist_all_kernel<KT><<<hgrid, 256, 0, s>>>(num_keys, keys_in, ps, hist);
-    radix_digit_scan_kernel<<<1, kRadix, 0, s>>>(ps.n, hist);
+    launch_k(radix_hist_all_kernel<KT>, hgrid, 256, 0, s, num_keys, keys_in, ps, hist);
+    launch_k(radix_digit_scan_kernel, 1, kRadix, 0, s, ps.n, hist);
     // pass 0 reads keys_in (values implicit when values_in is null), then ping-pong;
     // the caller passes (keys, values) as pass 0's source when they are the input
     const KT *ki = keys_in;
@@ -544,7 +553,7 @@ static int sort_pairs_impl(const char *what, int64_t num_keys, uint64_t bit_mask
     uint32_t *vo = values_alt;
     int alt = 1;
     for (int p = 0; p < ps.n; ++p) {
-        radix_onesweep_kernel<KT><<<tiles, kSortThreads, 0, s>>>(num_keys, ps.shift[p], ki, vi, ko, vo,
+        launch_k(radix_onesweep_kernel<KT>, tiles, kSortThreads, 0, s, num_keys, ps.shift[p], ki, vi, ko, vo,
                                                                  hist + (size_t)p * kRadix,
                                                                  status + (size_t)p * tiles * kRadix, counters + p,
                                                                  depth_range);
@@ -607,16 +616,16 @@ int hs_bin_emit_sorted(int B, int64_t N, int width, int height, const float *rec
     const int64_t items = (int64_t)B * N;
     const int nb = hs_scan_blocks(items);
     cudaStream_t s = HS_CHECK_STREAM(stream);
-    sorted_block_sums_kernel<<<nb, kScanBlock, 0, s>>>(items, order, counts, block_sums);
-    scan_kernel<<<1, 1024, 0, s>>>(nb, block_sums, block_offsets, nullptr, nullptr, nullptr);
-    emit_sorted_kernel<<<nb, kScanBlock, 0, s>>>(items, N, tiles_x, tile_bits, records, order, counts, block_offsets,
+    launch_k(sorted_block_sums_kernel, nb, kScanBlock, 0, s, items, order, counts, block_sums);
+    launch_k(scan_kernel, 1, 1024, 0, s, nb, block_sums, block_offsets, nullptr, nullptr, nullptr);
+    launch_k(emit_sorted_kernel, nb, kScanBlock, 0, s, items, N, tiles_x, tile_bits, records, order, counts, block_offsets,
                                                  keys, values);
     return check_launch("hs_bin_emit_sorted");
 }
 
 int hs_tile_ranges32(int64_t num_keys, const uint32_t *keys, uint32_t *ranges, void *stream) {
     if (num_keys <= 0) return HS_OK;
-    tile_ranges32_kernel<<<grid_for(num_keys, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(num_keys, keys, ranges);
+    launch_k(tile_ranges32_kernel, grid_for(num_keys, 256), 256, 0, HS_CHECK_STREAM(stream), num_keys, keys, ranges);
     return check_launch("hs_tile_ranges32");
 }
 
@@ -636,7 +645,7 @@ int hs_bin_stats(unsigned long long *host_out, int reset) {
 
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream) {
     if (num_keys <= 0) return HS_OK;
-    tile_ranges_kernel<<<grid_for(num_keys, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(num_keys, keys, ranges);
+    launch_k(tile_ranges_kernel, grid_for(num_keys, 256), 256, 0, HS_CHECK_STREAM(stream), num_keys, keys, ranges);
     return check_launch("hs_tile_ranges");
 }
 

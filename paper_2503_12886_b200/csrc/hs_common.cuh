@@ -53,6 +53,36 @@ int current_sm_count();
 
 inline unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
+// ---- programmatic dependent launch (PDL) -------------------------------------------
+// Every kernel of the library is launched with programmatic stream serialization, and
+// every kernel starts with pdl_prologue(): it lets its dependents launch right away
+// (griddepcontrol.launch_dependents: the next kernel in the stream may be scheduled once
+// all of this grid's CTAs are resident) and then waits until the grids it depends on have
+// completed and their memory is visible (griddepcontrol.wait) -- so the next kernel's launch
+// latency hides behind the tail of the previous one instead of idling the GPU between
+// them.  Without a programmatic dependency both instructions are no-ops.  HS_PDL=0 in the
+// environment launches normally.
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                            Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ float sigmoidf_ref(float x) {
     // S/model.py:251-257 two-branch stable sigmoid
     if (x >= 0.0f) return 1.0f / (1.0f + expf(-x));

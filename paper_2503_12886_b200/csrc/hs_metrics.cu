@@ -36,6 +36,7 @@ __device__ __forceinline__ void load_px(const float *__restrict__ pred, const ui
 __global__ void __launch_bounds__(256) ssim_kernel(int H, int W, const float *__restrict__ pred,
                                                    const uint8_t *__restrict__ target, Window win, double c1,
                                                    double c2, double *__restrict__ out) {
+    pdl_prologue();
     __shared__ double hrow[5][kRows][kTW];
     __shared__ double red[8];
     const int Hv = H - kWin + 1, Wv = W - kWin + 1;
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(256) ssim_kernel(int H, int W, const float *__
 __global__ void __launch_bounds__(256) err_sums_kernel(int64_t HW, const float *__restrict__ pred,
                                                        const uint8_t *__restrict__ target,
                                                        double *__restrict__ out) {
+    pdl_prologue();
     __shared__ double red[2][8];
     const int b = blockIdx.y;
     double sq = 0.0, ab = 0.0;
@@ -143,9 +145,9 @@ int hs_image_metrics(int B, int H, int W, const float *pred, const uint8_t *targ
     for (int k = 0; k < kWin; ++k) win.w[k] /= tot;
     const int Hv = H - kWin + 1, Wv = W - kWin + 1;
     const dim3 sgrid((Wv + kTW - 1) / kTW, (Hv + kTH - 1) / kTH, 3 * B);
-    ssim_kernel<<<sgrid, 256, 0, s>>>(H, W, pred, target_rgba, win, 0.01 * 0.01, 0.03 * 0.03, sums);
+    launch_k(ssim_kernel, sgrid, 256, 0, s, H, W, pred, target_rgba, win, 0.01 * 0.01, 0.03 * 0.03, sums);
     const dim3 egrid((unsigned)std::min<int64_t>(grid_for((int64_t)H * W, 256), 148), B);
-    err_sums_kernel<<<egrid, 256, 0, s>>>((int64_t)H * W, pred, target_rgba, sums);
+    launch_k(err_sums_kernel, egrid, 256, 0, s, (int64_t)H * W, pred, target_rgba, sums);
     return check_launch("hs_image_metrics");
 }
 

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "hs_common.cuh"
@@ -21,6 +22,14 @@ void set_error(const char *fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("HS_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 int current_sm_count() {
@@ -59,6 +68,7 @@ __device__ __forceinline__ float row_dot(const float *__restrict__ row, const fl
 __global__ void mlp_fwd_kernel(int H, int D, int K, const float *__restrict__ mlp,
                                const float *__restrict__ theta, float *__restrict__ cache,
                                float *__restrict__ psi, unsigned long long *err) {
+    pdl_prologue();
     extern __shared__ float sm[];
     float *th = sm, *h1 = th + H, *h2 = h1 + D;
     const int b = blockIdx.x;
@@ -108,6 +118,7 @@ __global__ void mlp_bwd_frame_kernel(int H, int D, int K, const float *__restric
                                      const float *__restrict__ cache,
                                      const float *__restrict__ partials, int P,
                                      float *__restrict__ gpsi, float *__restrict__ scratch) {
+    pdl_prologue();
     extern __shared__ float sm[];
     const int nw = blockDim.x >> 5;
     float *gp = sm, *gz2 = gp + K, *part = gz2 + D;     // part: [nw][D]
@@ -159,6 +170,7 @@ __global__ void mlp_bwd_weights_kernel(int B, int H, int D, int K, const float *
                                        const float *__restrict__ cache,
                                        const float *__restrict__ gpsi,
                                        const float *__restrict__ scratch, float *__restrict__ g) {
+    pdl_prologue();
     const int64_t total = (int64_t)D * H + D + (int64_t)D * D + D + (int64_t)K * D + K;
     const float *gz2 = scratch, *gz1 = scratch + (int64_t)B * D;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -253,6 +265,7 @@ __device__ __forceinline__ void blend_fwd_tile(int64_t E, int K, int B, int Bp, 
 __global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, int B, const float *__restrict__ base,
                                                              const float *__restrict__ deltas,
                                                              const float *__restrict__ psi, float *__restrict__ raw) {
+    pdl_prologue();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     const int Bp = blend_fwd_bpad(B);
@@ -325,6 +338,7 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
                                                         const float *__restrict__ deltas,
                                                         const float *__restrict__ psi,
                                                         float *__restrict__ raw) {
+    pdl_prologue();
     extern __shared__ float s_psi[];
     for (int i = threadIdx.x; i < B * K; i += blockDim.x) s_psi[i] = psi[i];
     __syncthreads();
@@ -439,6 +453,7 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
                                                        float *__restrict__ g_deltas,
                                                        float *__restrict__ partials, int P,
                                                        int accumulate) {
+    pdl_prologue();
     __shared__ float p_s[kBMaxB * kBMaxK];
     __shared__ float accw[kBT / 32][BP * kBMaxK];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -617,6 +632,7 @@ __device__ __forceinline__ float logit_clip(float e) {
 
 template <int CI, bool kVec>
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
+    pdl_prologue();
     const int64_t N = a.N, c0 = 7 * N, c1 = 10 * N;      // base colour segment
     // element ranges of the generic update: [begin, end) minus the colour segment when fused
     int64_t lo0 = a.begin, hi0 = a.end, lo1 = 0, hi1 = 0;
@@ -712,6 +728,7 @@ __global__ void color_init_kernel(int B, int64_t N, const float *__restrict__ ma
                                   const float *__restrict__ wsums, float thr,
                                   uint8_t *__restrict__ visited, float *__restrict__ color,
                                   int *n_init, unsigned long long *err) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N) return;
     if (visited[n]) return;
@@ -742,6 +759,7 @@ __global__ void color_init_kernel(int B, int64_t N, const float *__restrict__ ma
 // int64 (non-negative weights keep the top bit clear).
 __global__ void color_pack_kernel(int B, int64_t N, int frame_offset, const float *__restrict__ maxw,
                                   const uint8_t *__restrict__ visited, int64_t *__restrict__ packed) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N) return;
     unsigned long long best = 0;
@@ -759,6 +777,7 @@ __global__ void color_pack_kernel(int B, int64_t N, int frame_offset, const floa
 __global__ void color_select_kernel(int B, int64_t N, int frame_offset, const int64_t *__restrict__ packed,
                                     const float *__restrict__ wsums, float *__restrict__ est4,
                                     unsigned long long *err) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N) return;
     const unsigned long long v = (unsigned long long)packed[n];
@@ -776,6 +795,7 @@ __global__ void color_select_kernel(int B, int64_t N, int frame_offset, const in
 __global__ void color_apply_kernel(int64_t N, const int64_t *__restrict__ packed, const float *__restrict__ est4,
                                    float thr, uint8_t *__restrict__ visited, float *__restrict__ color,
                                    int *n_init) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N || visited[n]) return;
     const float w = __uint_as_float((uint32_t)((unsigned long long)packed[n] >> 32));
@@ -796,6 +816,7 @@ __global__ void color_apply_kernel(int64_t N, const int64_t *__restrict__ packed
 // S/model.py:219-234 (layout [pos 3N | rot 4N | color 3N | scale 3N | opacity N])
 __global__ void activate_fwd_kernel(int64_t N, const float *__restrict__ raw, float *__restrict__ act,
                                     unsigned long long *err) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N) return;
     const float *q = raw + 3 * N + 4 * n;
@@ -812,6 +833,7 @@ __global__ void activate_fwd_kernel(int64_t N, const float *__restrict__ raw, fl
 __global__ void activate_bwd_kernel(int64_t N, const float *__restrict__ raw,
                                     const float *__restrict__ act, const float *__restrict__ g,
                                     float *__restrict__ o) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N) return;
     for (int c = 0; c < 3; ++c) o[3 * n + c] = g[3 * n + c];
@@ -832,6 +854,7 @@ __global__ void activate_bwd_kernel(int64_t N, const float *__restrict__ raw,
 __global__ void transform_fwd_kernel(int64_t N, const float *__restrict__ t, const float *__restrict__ frames,
                                      const int32_t *__restrict__ tri, const float *__restrict__ bary,
                                      float *__restrict__ w) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N) return;
     const float *fr = frames + (int64_t)tri[n] * kFrame;
@@ -855,6 +878,7 @@ __global__ void transform_fwd_kernel(int64_t N, const float *__restrict__ t, con
 __global__ void transform_bwd_kernel(int64_t N, const float *__restrict__ t, const float *__restrict__ frames,
                                      const int32_t *__restrict__ tri, const float *__restrict__ g,
                                      float *__restrict__ o) {
+    pdl_prologue();
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (n >= N) return;
     const float *fr = frames + (int64_t)tri[n] * kFrame;
@@ -898,7 +922,7 @@ int hs_mlp_fwd(int B, int H, int D, int K, const float *mlp, const float *theta,
         return HS_ERR_SHAPE;
     }
     size_t smem = sizeof(float) * (H + 2 * D);
-    mlp_fwd_kernel<<<B, 1024, smem, HS_CHECK_STREAM(stream)>>>(H, D, K, mlp, theta, cache, psi, err);
+    launch_k(mlp_fwd_kernel, B, 1024, smem, HS_CHECK_STREAM(stream), H, D, K, mlp, theta, cache, psi, err);
     return check_launch("hs_mlp_fwd");
 }
 
@@ -907,9 +931,9 @@ int hs_mlp_bwd(int B, int H, int D, int K, const float *mlp, const float *theta,
                void *stream) {
     cudaStream_t s = HS_CHECK_STREAM(stream);
     size_t smem = sizeof(float) * (K + D + 32 * D);
-    mlp_bwd_frame_kernel<<<B, 1024, smem, s>>>(H, D, K, mlp, cache, gpsi_partials, num_partials, gpsi, scratch);
+    launch_k(mlp_bwd_frame_kernel, B, 1024, smem, s, H, D, K, mlp, cache, gpsi_partials, num_partials, gpsi, scratch);
     int64_t total = hs_mlp_size(H, D, K);
-    mlp_bwd_weights_kernel<<<grid_for(total, 256), 256, 0, s>>>(B, H, D, K, theta, cache, gpsi, scratch, g_mlp);
+    launch_k(mlp_bwd_weights_kernel, grid_for(total, 256), 256, 0, s, B, H, D, K, theta, cache, gpsi, scratch, g_mlp);
     return check_launch("hs_mlp_bwd");
 }
 
@@ -941,17 +965,17 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
         const int per_sm = std::max(1, (int)((220 * 1024) / tsm));
         const int64_t ntiles = (E + kBfTE - 1) / kBfTE;
         const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * std::min(per_sm, 8));
-        blend_fwd_tma_kernel<<<grid, kBfT, tsm, s>>>(E, K, B, base14, deltas, psi, raw10);
+        launch_k(blend_fwd_tma_kernel, grid, kBfT, tsm, s, E, K, B, base14, deltas, psi, raw10);
     } else if (vec) {
         // grid.y splits the frames into chunks of HS_BLEND_BC: few accumulators per
         // thread (occupancy) while the 40 MB of deltas stay L2-resident across chunks
         int64_t nv = E / 4;
         const unsigned gy = (unsigned)((B + HS_BLEND_BC - 1) / HS_BLEND_BC);
         const dim3 grid((unsigned)grid_for(nv, 256), gy);
-        blend_fwd_kernel<4, HS_BLEND_BC><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
+        launch_k(blend_fwd_kernel<4, HS_BLEND_BC>, grid, 256, smem, s, E, K, B, base14, deltas, psi, raw10);
     } else {
         unsigned grid = (unsigned)std::min<int64_t>(grid_for(E, 256), (int64_t)sms * 16);
-        blend_fwd_kernel<1, 16><<<grid, 256, smem, s>>>(E, K, B, base14, deltas, psi, raw10);
+        launch_k(blend_fwd_kernel<1, 16>, grid, 256, smem, s, E, K, B, base14, deltas, psi, raw10);
     }
     return check_launch("hs_blend_fwd");
 }
@@ -973,13 +997,13 @@ int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
         const int Bc = std::min(kBMaxB, B - b0);
         const int acc = b0 > 0;
         if (Bc <= 4)
-            blend_bwd_kernel<4><<<P, kBT, 0, s>>>(N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
+            launch_k(blend_bwd_kernel<4>, P, kBT, 0, s, N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
                                                   gpsi_partials, P, acc);
         else if (Bc <= 8)
-            blend_bwd_kernel<8><<<P, kBT, 0, s>>>(N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
+            launch_k(blend_bwd_kernel<8>, P, kBT, 0, s, N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
                                                   gpsi_partials, P, acc);
         else
-            blend_bwd_kernel<16><<<P, kBT, 0, s>>>(N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
+            launch_k(blend_bwd_kernel<16>, P, kBT, 0, s, N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
                                                    gpsi_partials, P, acc);
     }
     if (num_partials) *num_partials = P;
@@ -1049,13 +1073,13 @@ int hs_adam_fused(int64_t N, int K, int64_t mlp_size, float *params, const float
                                                       (int64_t)sms * HS_ADAM_CTAS_PER_SM);
     cudaStream_t s = HS_CHECK_STREAM(stream);
     if (vec) {
-        if (ci == 0) adam_kernel<0, true><<<grid, 256, 0, s>>>(a);
-        else if (ci == 1) adam_kernel<1, true><<<grid, 256, 0, s>>>(a);
-        else adam_kernel<2, true><<<grid, 256, 0, s>>>(a);
+        if (ci == 0) launch_k(adam_kernel<0, true>, grid, 256, 0, s, a);
+        else if (ci == 1) launch_k(adam_kernel<1, true>, grid, 256, 0, s, a);
+        else launch_k(adam_kernel<2, true>, grid, 256, 0, s, a);
     } else {
-        if (ci == 0) adam_kernel<0, false><<<grid, 256, 0, s>>>(a);
-        else if (ci == 1) adam_kernel<1, false><<<grid, 256, 0, s>>>(a);
-        else adam_kernel<2, false><<<grid, 256, 0, s>>>(a);
+        if (ci == 0) launch_k(adam_kernel<0, false>, grid, 256, 0, s, a);
+        else if (ci == 1) launch_k(adam_kernel<1, false>, grid, 256, 0, s, a);
+        else launch_k(adam_kernel<2, false>, grid, 256, 0, s, a);
     }
     return check_launch("hs_adam");
 }
@@ -1069,53 +1093,53 @@ int hs_adam(int64_t N, int K, int64_t mlp_size, float *params, const float *grad
 
 int hs_color_init(int B, int64_t N, const float *maxw, const float *wsums, float threshold,
                   uint8_t *visited, float *params, int *n_init, unsigned long long *err, void *stream) {
-    color_init_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(
+    launch_k(color_init_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), 
         B, N, maxw, wsums, threshold, visited, params + 7 * N, n_init, err);
     return check_launch("hs_color_init");
 }
 
 int hs_color_pack(int B, int64_t N, int frame_offset, const float *maxw, const uint8_t *visited, int64_t *packed,
                   void *stream) {
-    color_pack_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(B, N, frame_offset, maxw, visited,
+    launch_k(color_pack_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), B, N, frame_offset, maxw, visited,
                                                                               packed);
     return check_launch("hs_color_pack");
 }
 
 int hs_color_select(int B, int64_t N, int frame_offset, const int64_t *packed, const float *wsums, float *est4,
                     unsigned long long *err, void *stream) {
-    color_select_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(B, N, frame_offset, packed, wsums,
+    launch_k(color_select_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), B, N, frame_offset, packed, wsums,
                                                                                 est4, err);
     return check_launch("hs_color_select");
 }
 
 int hs_color_apply(int64_t N, const int64_t *packed, const float *est4, float threshold, uint8_t *visited,
                    float *params, int *n_init, void *stream) {
-    color_apply_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, packed, est4, threshold, visited,
+    launch_k(color_apply_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), N, packed, est4, threshold, visited,
                                                                                params + 7 * N, n_init);
     return check_launch("hs_color_apply");
 }
 
 int hs_activate_fwd(int64_t N, const float *raw14, float *act14, unsigned long long *err, void *stream) {
-    activate_fwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, raw14, act14, err);
+    launch_k(activate_fwd_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), N, raw14, act14, err);
     return check_launch("hs_activate_fwd");
 }
 
 int hs_activate_bwd(int64_t N, const float *raw14, const float *act14, const float *g_act14, float *g_raw14,
                     void *stream) {
-    activate_bwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, raw14, act14, g_act14, g_raw14);
+    launch_k(activate_bwd_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), N, raw14, act14, g_act14, g_raw14);
     return check_launch("hs_activate_bwd");
 }
 
 int hs_transform_fwd(int64_t N, const float *tangent14, const float *frames, const int32_t *tri_index,
                      const float *bary, float *world14, void *stream) {
-    transform_fwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, tangent14, frames, tri_index,
+    launch_k(transform_fwd_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), N, tangent14, frames, tri_index,
                                                                                   bary, world14);
     return check_launch("hs_transform_fwd");
 }
 
 int hs_transform_bwd(int64_t N, const float *tangent14, const float *frames, const int32_t *tri_index,
                      const float *g_world14, float *g_tangent14, void *stream) {
-    transform_bwd_kernel<<<grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(N, tangent14, frames, tri_index,
+    launch_k(transform_bwd_kernel, grid_for(N, 256), 256, 0, HS_CHECK_STREAM(stream), N, tangent14, frames, tri_index,
                                                                                   g_world14, g_tangent14);
     return check_launch("hs_transform_bwd");
 }

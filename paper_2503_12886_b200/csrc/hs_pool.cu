@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_rows_kernel(int64_t row
                                                                     const int32_t *__restrict__ idx,
                                                                     const unsigned char *__restrict__ src,
                                                                     unsigned char *__restrict__ dst, bool vec) {
+    pdl_prologue();
     const int64_t r = blockIdx.y;
     const int64_t c0 = (int64_t)blockIdx.x * kGatherChunk;
     const int64_t n = min(kGatherChunk, row_bytes - c0);
@@ -48,7 +49,7 @@ int hs_gather_rows(int num_rows, int64_t row_bytes, const int32_t *slots, const 
     const bool vec = row_bytes % 16 == 0 && (uintptr_t)pool % 16 == 0 && (uintptr_t)out % 16 == 0;
     const int64_t chunks = (row_bytes + kGatherChunk - 1) / kGatherChunk;
     const dim3 grid((unsigned)chunks, (unsigned)num_rows);
-    gather_rows_kernel<<<grid, kGatherThreads, 0, HS_CHECK_STREAM(stream)>>>(
+    launch_k(gather_rows_kernel, grid, kGatherThreads, 0, HS_CHECK_STREAM(stream), 
         row_bytes, chunks, slots, reinterpret_cast<const unsigned char *>(pool), reinterpret_cast<unsigned char *>(out),
         vec);
     return check_launch("hs_gather_rows");

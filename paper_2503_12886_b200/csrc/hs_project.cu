@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     float *__restrict__ radius, float *__restrict__ zero_gsplat, float *__restrict__ zero_maxw,
     float *__restrict__ zero_wsums, uint32_t *__restrict__ tile_counts, uint32_t *__restrict__ tile_rects,
     unsigned long long *err) {
+    pdl_prologue();
     extern __shared__ uint32_t hist[];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(256) project_world_fwd_kernel(
     float *__restrict__ records, float *__restrict__ depth, uint32_t *__restrict__ counts,
     uint32_t *__restrict__ block_sums, uint32_t *__restrict__ depth_range, float *__restrict__ radius,
     float *__restrict__ x_cam, float *__restrict__ cov_cam, unsigned long long *err) {
+    pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
     float dz = 0.f;
@@ -419,6 +421,7 @@ __global__ void __launch_bounds__(256, HS_PBWD_MINB) project_avatar_bwd_kernel(
     int B, int64_t N, int F, const float *__restrict__ raw10, const float *__restrict__ base14,
     const int32_t *__restrict__ tri, const float *__restrict__ bary, const float *__restrict__ frames,
     const float *__restrict__ cams, const float *__restrict__ g_splat, float *__restrict__ g_raw14) {
+    pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
     const int b = (int)(i / N);
@@ -468,6 +471,7 @@ __global__ void __launch_bounds__(256) project_world_bwd_kernel(int B, int64_t N
                                                                 const float *__restrict__ cams,
                                                                 const float *__restrict__ g_splat,
                                                                 float *__restrict__ g_world14) {
+    pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
     const int b = (int)(i / N);
@@ -528,7 +532,7 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
         return HS_ERR_SHAPE;
     }
     const size_t smem = tile_counts && tiles <= kProjHistBins ? sizeof(uint32_t) * tiles : 0;
-    project_avatar_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, smem, HS_CHECK_STREAM(stream)>>>(
+    launch_k(project_avatar_fwd_kernel, hs_scan_blocks(items), kScanBlock, smem, HS_CHECK_STREAM(stream), 
         B, N, F, width, height, raw10, base14, tri_index, bary, frames, cameras, records, depth, counts,
         block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, tile_counts, tile_rects, err);
     return check_launch("hs_project_avatar_fwd");
@@ -543,7 +547,7 @@ int hs_project_world_fwd(int B, int64_t N, int width, int height, const float *w
         return HS_ERR_SHAPE;
     }
     const int64_t items = (int64_t)B * N;
-    project_world_fwd_kernel<<<hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream)>>>(
+    launch_k(project_world_fwd_kernel, hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream), 
         B, N, width, height, world14, cameras, records, depth, counts, block_sums, depth_range, radius, x_cam, cov_cam,
         err);
     return check_launch("hs_project_world_fwd");
@@ -553,7 +557,7 @@ int hs_project_avatar_bwd(int B, int64_t N, int F, const float *raw10, const flo
                           const int32_t *tri_index, const float *bary, const float *frames, const float *cameras,
                           const float *g_splat, float *g_raw14, void *stream) {
     const int64_t items = (int64_t)B * N;
-    project_avatar_bwd_kernel<<<grid_for(items, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(
+    launch_k(project_avatar_bwd_kernel, grid_for(items, 256), 256, 0, HS_CHECK_STREAM(stream), 
         B, N, F, raw10, base14, tri_index, bary, frames, cameras, g_splat, g_raw14);
     return check_launch("hs_project_avatar_bwd");
 }
@@ -561,7 +565,7 @@ int hs_project_avatar_bwd(int B, int64_t N, int F, const float *raw10, const flo
 int hs_project_world_bwd(int B, int64_t N, const float *world14, const float *cameras, const float *g_splat,
                          float *g_world14, void *stream) {
     const int64_t items = (int64_t)B * N;
-    project_world_bwd_kernel<<<grid_for(items, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(B, N, world14, cameras,
+    launch_k(project_world_bwd_kernel, grid_for(items, 256), 256, 0, HS_CHECK_STREAM(stream), B, N, world14, cameras,
                                                                                          g_splat, g_world14);
     return check_launch("hs_project_world_bwd");
 }

@@ -549,6 +549,7 @@ constexpr int kWsCounters = 16;      // workspace head: [next, done] (+ padding)
 __global__ void __launch_bounds__(1024) tile_order_kernel(int total_tiles, int tile_bits, int tiles,
                                                           const uint32_t *__restrict__ ranges,
                                                           uint32_t *__restrict__ order) {
+    pdl_prologue();
     constexpr int kSub = HS_RASTER_LPT_SUB;         // sub-buckets per octave
     constexpr int kNB = 33 << kSub;
     __shared__ uint32_t hist[kNB], cursor[kNB];
@@ -608,6 +609,7 @@ __device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, in
 
 template <bool kLoss, bool kImage, int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterArgs a, int nblk) {
+    pdl_prologue();
     if (guard_blocks(a)) return;
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -804,6 +806,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
 // forward's per-batch hit masks.
 template <int CI>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
+    pdl_prologue();
     if (guard_blocks(a)) return;
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     __shared__ uint32_t s_masks[kCW][kMaskBatches];
@@ -816,6 +819,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(Raste
 
 template <bool kExplicitGrad>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a, int nblk) {
+    pdl_prologue();
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * kWarpSmem;
@@ -826,6 +830,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterA
 // partials[b][tiles * kBlocks][2] (one pair per pixel block)
 __global__ void loss_reduce_kernel(int B, int tiles, float inv_count, const float *__restrict__ partials,
                                    float *__restrict__ out) {
+    pdl_prologue();
     __shared__ float red[2][32];
     const int b = blockIdx.x, tid = threadIdx.x;
     float s0 = 0.f, s1 = 0.f;
@@ -846,6 +851,7 @@ __global__ void loss_reduce_kernel(int B, int tiles, float inv_count, const floa
 }
 
 __global__ void loss_mean_kernel(int B, float *__restrict__ out) {
+    pdl_prologue();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         float s = 0.f;
         for (int b = 0; b < B; ++b) s += out[b];
@@ -855,6 +861,7 @@ __global__ void loss_mean_kernel(int B, float *__restrict__ out) {
 
 __global__ void fixed_to_float_kernel(int64_t n, const long long *__restrict__ fixed, float *__restrict__ out,
                                       float inv) {
+    pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) out[i] = (float)((double)fixed[i] * (double)inv);
 }
@@ -880,10 +887,10 @@ static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records
 template <bool L, bool I>
 static void launch_fwd_ci(int ci, dim3 grid, int nblk, cudaStream_t s, const RasterArgs &a) {
     switch (ci) {
-        case 0: raster_fwd_kernel<L, I, 0><<<grid, kRT, 0, s>>>(a, nblk); break;
-        case 1: raster_fwd_kernel<L, I, 1><<<grid, kRT, 0, s>>>(a, nblk); break;
-        case 2: raster_fwd_kernel<L, I, 2><<<grid, kRT, 0, s>>>(a, nblk); break;
-        default: raster_fwd_kernel<L, I, 3><<<grid, kRT, 0, s>>>(a, nblk); break;
+        case 0: launch_k(raster_fwd_kernel<L, I, 0>, grid, kRT, 0, s, a, nblk); break;
+        case 1: launch_k(raster_fwd_kernel<L, I, 1>, grid, kRT, 0, s, a, nblk); break;
+        case 2: launch_k(raster_fwd_kernel<L, I, 2>, grid, kRT, 0, s, a, nblk); break;
+        default: launch_k(raster_fwd_kernel<L, I, 3>, grid, kRT, 0, s, a, nblk); break;
     }
 }
 
@@ -896,7 +903,7 @@ static size_t workspace_bytes(int B, int W, int H) {
 static void launch_tile_order(int B, int nblk, int tile_bits, const uint32_t *ranges, void *ws, cudaStream_t s) {
     const int tiles = nblk / kBlocks;
     if (HS_RASTER_PERSIST && HS_RASTER_LPT)
-        tile_order_kernel<<<1, 1024, 0, s>>>(B * tiles, tile_bits, tiles, ranges,
+        launch_k(tile_order_kernel, 1, 1024, 0, s, B * tiles, tile_bits, tiles, ranges,
                                              reinterpret_cast<uint32_t *>(ws) + kWsCounters);
 }
 
@@ -998,8 +1005,8 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
     launch_tile_order(B, nblk, tile_bits, ranges, workspace, s);
-    if (grad_image) raster_bwd_kernel<true><<<grid, kRT, 0, s>>>(a, nblk);
-    else raster_bwd_kernel<false><<<grid, kRT, 0, s>>>(a, nblk);
+    if (grad_image) launch_k(raster_bwd_kernel<true>, grid, kRT, 0, s, a, nblk);
+    else launch_k(raster_bwd_kernel<false>, grid, kRT, 0, s, a, nblk);
     return check_launch("hs_raster_bwd");
 }
 
@@ -1036,10 +1043,10 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     cudaStream_t s = HS_CHECK_STREAM(stream);
     if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, workspace, s);
     switch (ci) {
-        case 0: raster_train_kernel<0><<<grid, kRT, 0, s>>>(a, nblk); break;
-        case 1: raster_train_kernel<1><<<grid, kRT, 0, s>>>(a, nblk); break;
-        case 2: raster_train_kernel<2><<<grid, kRT, 0, s>>>(a, nblk); break;
-        default: raster_train_kernel<3><<<grid, kRT, 0, s>>>(a, nblk); break;
+        case 0: launch_k(raster_train_kernel<0>, grid, kRT, 0, s, a, nblk); break;
+        case 1: launch_k(raster_train_kernel<1>, grid, kRT, 0, s, a, nblk); break;
+        case 2: launch_k(raster_train_kernel<2>, grid, kRT, 0, s, a, nblk); break;
+        default: launch_k(raster_train_kernel<3>, grid, kRT, 0, s, a, nblk); break;
     }
     return check_launch("hs_raster_train");
 }
@@ -1055,7 +1062,7 @@ int hs_raster_stats(unsigned long long *host_out, int reset) {
 
 int hs_fixed_to_float(int64_t n, const long long *fixed, float *out, int sums, void *stream) {
     if (n <= 0) return HS_OK;
-    fixed_to_float_kernel<<<grid_for(n, 256), 256, 0, HS_CHECK_STREAM(stream)>>>(n, fixed, out,
+    launch_k(fixed_to_float_kernel, grid_for(n, 256), 256, 0, HS_CHECK_STREAM(stream), n, fixed, out,
                                                                                 1.0f / (sums ? kFxSums : kFxGrad));
     return check_launch("hs_fixed_to_float");
 }
@@ -1065,8 +1072,8 @@ int hs_loss_reduce(int B, int num_tiles, int width, int height, const float *los
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const float inv = (float)(1.0 / ((double)width * height * 3.0));
     static_assert(HS_LOSS_PARTIALS_PER_TILE >= 2 * kBlocks, "hs_api.h partial count");
-    loss_reduce_kernel<<<B, 256, 0, s>>>(B, num_tiles * kBlocks, inv, loss_partials, loss_out);
-    loss_mean_kernel<<<1, 32, 0, s>>>(B, loss_out);
+    launch_k(loss_reduce_kernel, B, 256, 0, s, B, num_tiles * kBlocks, inv, loss_partials, loss_out);
+    launch_k(loss_mean_kernel, 1, 32, 0, s, B, loss_out);
     return check_launch("hs_loss_reduce");
 }
 

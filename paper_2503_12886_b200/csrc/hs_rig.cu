@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kRigThreads) rig_frames_kernel(int V, int F, i
                                                                  const double *__restrict__ vertices,
                                                                  float *__restrict__ frames,
                                                                  unsigned long long *err) {
+    pdl_prologue();
     extern __shared__ double s_verts[];           // [V][3]
     const int b = blockIdx.y;
     if (vertices) {                               // mesh_frames of given vertices (no rig)
@@ -249,7 +250,7 @@ int hs_rig_frames(int B, int V, int F, int E, const double *base_vertices, const
     }
     if (smem > 48 * 1024) cudaFuncSetAttribute(rig_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const dim3 grid((F + kRigThreads - 1) / kRigThreads, B);
-    rig_frames_kernel<<<grid, kRigThreads, smem, HS_CHECK_STREAM(stream)>>>(V, F, E, base_vertices, expr_bases, faces,
+    launch_k(rig_frames_kernel, grid, kRigThreads, smem, HS_CHECK_STREAM(stream), V, F, E, base_vertices, expr_bases, faces,
                                                                         uv_coords, theta, vertices, frames, err);
     return check_launch("hs_rig_frames");
 }

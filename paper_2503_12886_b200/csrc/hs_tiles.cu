@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_count_kernel(int64_t items,
                                                                   int tile_bits, const float *__restrict__ records,
                                                                   const uint32_t *__restrict__ counts,
                                                                   uint32_t *__restrict__ tile_counts) {
+    pdl_prologue();
     extern __shared__ uint32_t hist[];
     const uint32_t b0 = (uint32_t)(blockIdx.x * (int64_t)kTileItems / N);
     const bool shared = tiles <= kTileSmemBins;
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(int nseg, uint3
                                                                  unsigned long long *__restrict__ err,
                                                                  uint32_t *__restrict__ depth_range,
                                                                  unsigned long long *__restrict__ summary) {
+    pdl_prologue();
     __shared__ uint32_t wt[kScanPer][kScanThreads / 32];   // per k: inclusive scan over warps
     __shared__ uint32_t s_max, s_big[2];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -268,6 +270,7 @@ __global__ void __launch_bounds__(kScanSpan) tile_scan_multi_kernel(int nseg, ui
                                                                     unsigned long long *__restrict__ err,
                                                                     uint32_t *__restrict__ depth_range,
                                                                     unsigned long long *__restrict__ summary) {
+    pdl_prologue();
     __shared__ uint32_t wsum[kScanSpan / 32];
     __shared__ uint32_t s_tile, s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -372,6 +375,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
                                                                     const unsigned long long *__restrict__ summary,
                                                                     uint32_t *__restrict__ keys,
                                                                     uint32_t *__restrict__ vals) {
+    pdl_prologue();
     extern __shared__ uint32_t hist[];
     if (summary[0] > capacity) return;               // the caller grows the buffers and re-runs
     const uint32_t b0 = (uint32_t)(blockIdx.x * (int64_t)kTileItems / N);
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, i
                                                                 const unsigned long long *__restrict__ summary,
                                                                 uint32_t *__restrict__ keys,
                                                                 uint32_t *__restrict__ vals) {
+    pdl_prologue();
     if (summary[0] > capacity) return;               // the caller grows the buffers and re-runs
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -676,6 +681,7 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, HS_SHORT_SORT_MINB) tile_
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
     uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
+    pdl_prologue();
     __shared__ unsigned long long s_k64_all[kWarpSortWarps][kWarpShort];
     __shared__ uint32_t s_q_all[kWarpSortWarps][kWarpShort];
     if (summary[0] > capacity) return;
@@ -721,6 +727,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
     uint32_t *__restrict__ lists, uint32_t *__restrict__ list_counts, int half, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
+    pdl_prologue();
     constexpr int E = kRun / 32, IB = 10;
     constexpr uint32_t kSlot = (1u << IB) - 1u;
     __shared__ unsigned long long s_k64[kWarpCap];
@@ -845,6 +852,7 @@ __global__ void __launch_bounds__(kCtaSortThreads) tile_sort_cta_kernel(
     int64_t N, int tile_bits, int nseg, const float *__restrict__ depth, const uint32_t *__restrict__ ranges,
     const uint32_t *__restrict__ lists, const uint32_t *__restrict__ list_counts, int half, uint64_t capacity,
     const unsigned long long *__restrict__ summary, uint32_t *__restrict__ vals) {
+    pdl_prologue();
     extern __shared__ unsigned long long s_keys[];
     if (summary[0] > capacity) return;
     const uint32_t nbig = filled_half(list_counts, half)[2];
@@ -896,7 +904,7 @@ int hs_tile_count(int B, int64_t N, int width, int height, const float *records,
     }
     const int tiles = tiles_x * tiles_y;
     const size_t smem = tiles <= kTileSmemBins ? sizeof(uint32_t) * tiles : 0;
-    tile_count_kernel<<<grid_for(items, kTileItems), kTileThreads, smem, HS_CHECK_STREAM(stream)>>>(
+    launch_k(tile_count_kernel, grid_for(items, kTileItems), kTileThreads, smem, HS_CHECK_STREAM(stream), 
         items, N, tiles_x, tiles, tile_bits, records, counts, tile_counts);
     return check_launch("hs_tile_count");
 }
@@ -921,14 +929,14 @@ int hs_tile_scan(int B, int width, int height, uint32_t *tile_counts, uint32_t *
             set_error("hs_tile_scan: list_counts halves of %d words, need %d", list_half, 8 + ctas);
             return HS_ERR_SHAPE;
         }
-        tile_scan_multi_kernel<<<ctas, kScanSpan, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts,
+        launch_k(tile_scan_multi_kernel, ctas, kScanSpan, 0, s, (int)nseg, tile_counts, ranges, cursor, lists, list_counts,
                                                           list_half, err, depth_range, summary);
     } else {
         if (list_half < 8) {
             set_error("hs_tile_scan: list_counts halves of %d words, need >= 8", list_half);
             return HS_ERR_SHAPE;
         }
-        tile_scan_kernel<<<1, 1024, 0, s>>>((int)nseg, tile_counts, ranges, cursor, lists, list_counts, list_half,
+        launch_k(tile_scan_kernel, 1, 1024, 0, s, (int)nseg, tile_counts, ranges, cursor, lists, list_counts, list_half,
                                             err, depth_range, summary);
     }
     return check_launch("hs_tile_scan");
@@ -974,10 +982,10 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
 #endif
     if (HS_SCATTER_WARP && tile_rects && tiles_x <= 256) {
         const int64_t warps = (items + 32 * kSwRounds - 1) / (32 * kSwRounds);
-        tile_scatter_warp_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(items, N, tiles_x, tile_bits, tile_rects,
+        launch_k(tile_scatter_warp_kernel, (unsigned)((warps + 7) / 8), 256, 0, s, items, N, tiles_x, tile_bits, tile_rects,
                                                                             cursor, capacity, summary, keys, values);
     } else {
-        tile_scatter_kernel<<<grid_for(items, kTileItems), kTileThreads, tsmem, s>>>(
+        launch_k(tile_scatter_kernel, grid_for(items, kTileItems), kTileThreads, tsmem, s, 
             items, N, tiles_x, tiles, tile_bits, records, counts, tile_rects, cursor, capacity, summary, keys, values);
     }
     const int sms = current_sm_count();
@@ -994,13 +1002,13 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
 #ifndef HS_SHORT_SORT_CTAS_PER_SM
 #define HS_SHORT_SORT_CTAS_PER_SM 16
 #endif
-    tile_sort_warp_kernel<<<(unsigned)sms * HS_SHORT_SORT_CTAS_PER_SM, 32 * kWarpSortWarps, 0, side>>>(
+    launch_k(tile_sort_warp_kernel, (unsigned)sms * HS_SHORT_SORT_CTAS_PER_SM, 32 * kWarpSortWarps, 0, side, 
         N, tile_bits, nseg, depth, ranges, lists, list_counts, capacity, summary, values);
     if (f) cudaEventRecord(f->joined, f->side);
 #ifndef HS_LONG_SORT_CTAS_PER_SM
 #define HS_LONG_SORT_CTAS_PER_SM 16
 #endif
-    tile_sort_long_kernel<<<(unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s>>>(
+    launch_k(tile_sort_long_kernel, (unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s, 
         N, tile_bits, nseg, depth, ranges, lists, list_counts, list_half, capacity, summary, values);
     if (f) cudaStreamWaitEvent(s, f->joined, 0);
     return check_launch("hs_tile_fill");
@@ -1019,7 +1027,7 @@ int hs_tile_fill_longest(int B, int64_t N, int width, int height, const float *d
     // (a per-device function attribute: set on every call, so any device a caller drives
     // has it -- a cheap host call)
     cudaFuncSetAttribute(tile_sort_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
-    tile_sort_cta_kernel<<<(unsigned)sms * 2, kCtaSortThreads, csmem, s>>>(N, tile_bits, nseg, depth, ranges, lists,
+    launch_k(tile_sort_cta_kernel, (unsigned)sms * 2, kCtaSortThreads, csmem, s, N, tile_bits, nseg, depth, ranges, lists,
                                                                           list_counts, list_half, capacity, summary,
                                                                           values);
     return check_launch("hs_tile_fill_longest");

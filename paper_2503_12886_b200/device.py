@@ -268,6 +268,7 @@ class Binner:
         self.mode = None             # how the last bin() built its lists
         self.longest = 0             # longest (frame, tile) list of the last tile-major binning
         self.fork = None             # hs_fork_create context (side stream of the list sorts)
+        self._d2h = None             # stream of the step's summary read
         # tile-major binning writes the (frame, tile) key of every entry only when asked
         # (checkers); the raster reads values and ranges only
         self.write_keys = True
@@ -454,9 +455,18 @@ class Binner:
         L.call("hs_tile_scan", B, width, height, _p(self.tile_counts), _p(ranges), _p(self.cursor),
                _p(self.lists), _p(self.list_counts), self.list_half, _p(err), _p(self.depth_range), _p(self.summary),
                s)
-        self.summary_host.copy_(self.summary, non_blocking=True)
-        ready = torch.cuda.Event()
-        ready.record()
+        # the summary's D2H copy runs on a side stream behind the scan, so the compute
+        # stream goes straight on to the scatter (a copy in its own order would hold the
+        # scatter back by the copy's latency)
+        scanned = torch.cuda.Event()
+        scanned.record()
+        if self._d2h is None:
+            self._d2h = torch.cuda.Stream(device=torch.cuda.current_device())
+        self._d2h.wait_event(scanned)
+        with torch.cuda.stream(self._d2h):
+            self.summary_host.copy_(self.summary, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self._d2h)
         if self.keys is None:
             self._ensure(4 * B * N)         # a first guess; grown below when short
 
@@ -473,7 +483,7 @@ class Binner:
         fill()                              # first: the GPU reaches it right after the scan
         self.order_ready = False
         if after_scan is not None:
-            self.order_ready = after_scan(ranges, tile_bits, ready)
+            self.order_ready = after_scan(ranges, tile_bits, scanned)
         # the consumer of the lists, enqueued before the host reads the summary: it runs
         # right after the fill unless the device-side guard (hs_raster_guard_t) finds the
         # lists incomplete, in which case it exits and spec_valid tells the caller to
