@@ -148,7 +148,7 @@ __device__ __forceinline__ float grad_factor(int v) {
     return v < 2 ? 0.5f * kMeanScale : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
 }
 constexpr int kStageBytes = 96;
-constexpr int kWarpSmem = 32 * kStageBytes;
+constexpr int kWarpSmem = 32 * (kStageBytes + 48);    // staged splats + the record prefetch slots
 
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
     float4 v;
@@ -245,11 +245,34 @@ __device__ __forceinline__ float fwd_gate(uint32_t mask, uint32_t lanebit, float
 
 // Stage one splat record into the lane's slot for the warp's 8 x 8 block with origin
 // (x0, y0).  Returns true when a pixel of the block can be touched (its mask is nonzero).
-template <bool kCull = true>
-__device__ __forceinline__ bool stage_splat(const float *__restrict__ rec, uint32_t gflag, int x0, int y0,
-                                            uint32_t saddr) {
+// The record prefetch (HS_RASTER_PREFETCH): while a warp works through one 32-key batch,
+// each lane's 48-byte record of the NEXT batch streams into a per-lane shared slot with
+// cp.async (the list value for it was loaded a batch earlier), so staging a batch reads
+// shared memory instead of waiting on two dependent global loads (list value, then record).
+#ifndef HS_RASTER_PREFETCH
+#define HS_RASTER_PREFETCH 1
+#endif
+constexpr int kRecBytes = 48;
+__device__ __forceinline__ void cp_async_record(uint32_t dst, const float *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(src + 4) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 32), "l"(src + 8) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+struct RawRec {
+    float4 A, B, C;
+};
+__device__ __forceinline__ RawRec load_rec_global(const float *rec) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
-    const float4 A = __ldg(r), Bv = __ldg(r + 1), Cv = __ldg(r + 2);
+    return {__ldg(r), __ldg(r + 1), __ldg(r + 2)};
+}
+__device__ __forceinline__ RawRec load_rec_shared(uint32_t addr) { return {lds4(addr), lds4(addr + 16), lds4(addr + 32)}; }
+
+template <bool kCull = true>
+__device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, int x0, int y0, uint32_t saddr) {
+    const float4 A = rr.A, Bv = rr.B, Cv = rr.C;
     const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
     const int rl = unpack_lo(rows), rh = unpack_hi(rows), cl = unpack_lo(cols), ch = unpack_hi(cols);
     const float a = A.z, b = A.w, c = Bv.x, qmax = Bv.z;
@@ -352,6 +375,16 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
 #ifdef HS_RASTER_STATS
     unsigned long long st_iter = 0, st_c = 0, st_batches = 0;
 #endif
+    // record prefetch: slot of this lane, and the list value of the next batch
+    const uint32_t rslot = wbase + 32 * kStageBytes + lane * kRecBytes;
+    const float *frec = a.records + (int64_t)b * a.N * kRec;
+    uint32_t n_cur = start + lane < end ? a.vals[start + lane] : 0u;
+    uint32_t n_next = 0u;
+    if (HS_RASTER_PREFETCH) {
+        if (start + lane < end) cp_async_record(rslot, frec + (int64_t)n_cur * kRec);
+        cp_async_commit();
+        n_next = start + 32 + lane < end ? a.vals[start + 32 + lane] : 0u;
+    }
     for (uint32_t c0 = start; c0 < end; c0 += 32) {
         // pixels outside the image have no mask bits; the loop ends when every pixel of
         // the block has terminated
@@ -359,11 +392,28 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         const uint32_t idx = c0 + lane;
         bool hit = false, want = false;
         if (idx < end) {
-            const uint32_t n = a.vals[idx];
+            const uint32_t n = n_cur;
             HS_CHECK(n < a.N, "raster list value", n);
             const uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
-            hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, gflag, x0, y0, wbase + lane * kStageBytes);
+            RawRec rr;
+            if (HS_RASTER_PREFETCH) {
+                cp_async_wait_all();
+                rr = load_rec_shared(rslot);
+            } else {
+                rr = load_rec_global(frec + (int64_t)n * kRec);
+            }
+            hit = stage_splat(rr, gflag, x0, y0, wbase + lane * kStageBytes);
             want = CI > 0 && hit && (CI != 3 || !a.visited[n]);   // visited: no colour-init work
+        }
+        // the next batch: its records start streaming into the slots (this lane's slot was
+        // just read), and its successor's list values are loaded
+        if (HS_RASTER_PREFETCH) {
+            if (idx + 32 < end) cp_async_record(rslot, frec + (int64_t)n_next * kRec);
+            cp_async_commit();
+            n_cur = n_next;
+            n_next = idx + 64 < end ? a.vals[idx + 64] : 0u;
+        } else {
+            n_cur = idx + 32 < end ? a.vals[idx + 32] : 0u;
         }
         uint32_t bits = __ballot_sync(kFull, hit);
         const uint32_t wantb = __ballot_sync(kFull, want);
@@ -445,6 +495,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         __syncwarp();
     }
 
+    if (HS_RASTER_PREFETCH) cp_async_wait_all();            // (the loop may break early)
 #ifdef HS_RASTER_STATS
     atomicAdd(&g_raster_stats[0], st_iter);
     atomicAdd(&g_raster_stats[3], st_c);
@@ -681,29 +732,53 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
     if (last <= start) return;
     const uint32_t lanebit = 1u << lane;
     const float2 one2 = f2(1.f, 1.f);
-    for (int k = (int)((last - 1 - start) >> 5); k >= 0; --k) {
+    const uint32_t rslot = wbase + 32 * kStageBytes + lane * kRecBytes;
+    const float *frec = a.records + (int64_t)b * a.N * kRec;
+    // batch k's staging set: the forward's hit mask (fused kernel), or every list entry
+    auto need = [&](int k) -> uint32_t {
+        const uint32_t c0 = start + 32u * (uint32_t)k, c_end = min(c0 + 32u, last);
+        const uint32_t live_lanes = c_end - c0 >= 32u ? kFull : (1u << (c_end - c0)) - 1u;
+        return (masks != nullptr && k < kMaskBatches) ? masks[k] & live_lanes : live_lanes;
+    };
+    // back to front: the records of the next batch to walk (k - 1) prefetch while this one runs
+    int k = (int)((last - 1 - start) >> 5);
+    uint32_t nb_cur = need(k);
+    if (HS_RASTER_PREFETCH) {
+        if ((nb_cur >> lane) & 1u) cp_async_record(rslot, frec + (int64_t)a.vals[start + 32u * k + lane] * kRec);
+        cp_async_commit();
+    }
+    for (; k >= 0; --k) {
         const uint32_t c0 = start + 32u * (uint32_t)k;
         const uint32_t c_end = min(c0 + 32u, last);
-        const uint32_t live_lanes = c_end - c0 >= 32u ? kFull : (1u << (c_end - c0)) - 1u;
-        uint32_t bits;
         const uint32_t idx = c0 + lane;
-        if (masks != nullptr && k < kMaskBatches) {
-            bits = masks[k] & live_lanes;
+        const bool fused = masks != nullptr && k < kMaskBatches;
+        const uint32_t stage_set = nb_cur;
+        const uint32_t nb_next = k > 0 ? need(k - 1) : 0u;
+        uint32_t bits;
+        bool hit = false;
+        if ((stage_set >> lane) & 1u) {
+            const uint32_t n = a.vals[idx];
+            HS_CHECK(n < a.N, "raster list value", n);
+            RawRec rr;
+            if (HS_RASTER_PREFETCH) {
+                cp_async_wait_all();
+                rr = load_rec_shared(rslot);
+            } else {
+                rr = load_rec_global(frec + (int64_t)n * kRec);
+            }
+            const uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
+            if (fused) hit = stage_splat<false>(rr, gflag, x0, y0, wbase + lane * kStageBytes);
+            else hit = stage_splat(rr, gflag, x0, y0, wbase + lane * kStageBytes);
+        }
+        if (HS_RASTER_PREFETCH) {
+            if ((nb_next >> lane) & 1u) cp_async_record(rslot, frec + (int64_t)a.vals[idx - 32] * kRec);
+            cp_async_commit();
+        }
+        nb_cur = nb_next;
+        if (fused) {
+            bits = stage_set;
             if (bits == 0u) continue;                      // warp-uniform
-            if ((bits >> lane) & 1u) {
-                const uint32_t n = a.vals[idx];
-                HS_CHECK(n < a.N, "raster list value", n);
-                stage_splat<false>(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
-                                   y0, wbase + lane * kStageBytes);
-            }
         } else {
-            bool hit = false;
-            if (idx < c_end) {
-                const uint32_t n = a.vals[idx];
-                HS_CHECK(n < a.N, "raster list value", n);
-                hit = stage_splat(a.records + ((int64_t)b * a.N + n) * kRec, (uint32_t)((int64_t)b * a.N + n), x0,
-                                  y0, wbase + lane * kStageBytes);
-            }
             bits = __ballot_sync(kFull, hit);
         }
         // pixels whose stop index lies inside this batch need the per-splat test
@@ -798,6 +873,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
         }
         __syncwarp();
     }
+    if (HS_RASTER_PREFETCH) cp_async_wait_all();
 }
 
 
