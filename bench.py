@@ -342,6 +342,12 @@ def run_b200(args, cfg):
     # one process per GPU; HS_BENCH_BACKEND=gloo lets several ranks share one GPU to
     # exercise the multi-rank code path where fewer GPUs than ranks are available
     backend = os.environ.get("HS_BENCH_BACKEND", "nccl")
+    if backend == "nccl" and world > torch.cuda.device_count():
+        # NCCL cannot put two ranks on one GPU: fall back to gloo (host-mediated
+        # allreduce) and say so in the line rather than fail
+        backend = "gloo"
+        if rank == 0:
+            print(f"bench: {world} ranks on {torch.cuda.device_count()} GPU(s): gloo backend", file=sys.stderr)
     dev_index = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(dev_index)
     pg = None
