@@ -657,17 +657,16 @@ def self_launch(args):
     import torch
     backend = os.environ.get("HS_BENCH_BACKEND", "nccl")
     ngpu = torch.cuda.device_count()
+    env = dict(os.environ)
     if backend == "nccl" and ngpu < args.gpus:
-        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} GPUs for NCCL, "
-                          f"{ngpu} visible (HS_BENCH_BACKEND=gloo shares one GPU between ranks)"}), flush=True)
-        return 2
+        print(f"bench: --gpus {args.gpus} with {ngpu} GPU(s) visible: ranks share GPUs over gloo", file=sys.stderr)
+        env["HS_BENCH_BACKEND"] = "gloo"
     sk = socket.socket()
     sk.bind(("127.0.0.1", 0))
     port = sk.getsockname()[1]
     sk.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    env = dict(os.environ)
     env.setdefault("OMP_NUM_THREADS", "1")
     return subprocess.call(cmd, env=env)
 
