@@ -565,7 +565,8 @@ def compat_e2e(cfg, steps):
         compat.train_step(state, samples, bgs, mesh_of)
     dt = time.perf_counter() - t0
     return {"value": B * steps / dt, "unit": UNIT, "ms_per_step": 1000.0 * dt / steps,
-            "path": "compat.train_step (reference signature; float64 model written back each step)",
+            "path": ("compat.train_step (reference signature; each sample's u8 target and mesh frames uploaded "
+                     "once and cached on the sample; float64 model written back each step)"),
             "d2h_bytes_per_step": 4 * (14 * n + 10 * av.K * n) + 4 * int(sum(np.size(v) for v in av.mlp.values()))
             + n}
 

@@ -633,11 +633,17 @@ def train_step(state, samples, backgrounds, mesh_of):
     tr = _trainer_for(state, B, cam)
     if not state.config.use_mlp:
         raise ValueError("use_mlp=False is not supported on the device path")
-    thetas = np.stack([np.asarray(s.theta, np.float64) for s in samples])
-    targets = np.stack([_sample_u8(s) for s in samples])
-    frames = np.stack([_mesh_array(mesh_of(s)) for s in samples])
-    cams = np.tile(camera_array(cam), (B, 1))
-    res = tr.step_from_host(thetas, targets, frames, cams, np.asarray(backgrounds, np.float64))
+    d = tr.av.device
+    # the samples' u8 targets and mesh frames are uploaded once and cached on the sample /
+    # mesh objects (the reference caches mesh frames on its samples the same way,
+    # S/dataset.py:54-57): a step moves only theta, the cameras and the backgrounds H2D
+    thetas = torch.from_numpy(np.stack([np.asarray(s.theta, np.float32) for s in samples])).to(d, non_blocking=True)
+    targets = torch.stack([_sample_dev(s, d) for s in samples])
+    frames = torch.stack([_mesh_dev(mesh_of(s), d) for s in samples])
+    cams = torch.from_numpy(np.tile(camera_array(cam), (B, 1))).to(d, non_blocking=True)
+    bgs = torch.from_numpy(np.asarray(backgrounds, np.float32)).to(d, non_blocking=True)
+    tr.step(thetas, targets, frames, cams, bgs)
+    res = tr.result()
     # write back (the reference mutates model / colour state in place): one DMA of the
     # flat fp32 parameters into a pinned buffer, then the float64 host writes
     host = getattr(tr, "_host_params", None)
@@ -676,6 +682,34 @@ def _sample_u8(sample):
     except AttributeError:
         pass
     return u8
+
+
+def _sample_dev(sample, device):
+    """The sample's u8 target as a device tensor, cached on the sample (re-uploaded when
+    sample.image is replaced)."""
+    img = sample.image
+    hit = getattr(sample, "_b200_dev", None)
+    if hit is not None and hit[0] is img:
+        return hit[1]
+    t = torch.from_numpy(np.ascontiguousarray(_sample_u8(sample))).to(device)
+    try:
+        sample._b200_dev = (img, t)
+    except AttributeError:
+        pass
+    return t
+
+
+def _mesh_dev(mesh, device):
+    """A MeshFrames' (F, 22) device layout, cached on the object."""
+    hit = getattr(mesh, "_b200_dev", None)
+    if hit is not None and hit[0] is mesh.rotation:
+        return hit[1]
+    t = torch.from_numpy(_mesh_array(mesh)).to(device)
+    try:
+        mesh._b200_dev = (mesh.rotation, t)
+    except AttributeError:
+        pass
+    return t
 
 
 def _mesh_array(mesh):
