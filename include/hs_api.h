@@ -312,6 +312,9 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
  *   no q pass, full-cover iterations, staged batches, 0], adjoint iterations by the
  *   number of contributing lanes [0, 1, 2, 3-4, 5-8, 9-16, 17-32, 0]. */
 int hs_raster_stats(unsigned long long *host_out, int reset);
+/* Diagnostics (-DHS_RASTER_TIMING builds only): per persistent raster warp of the last
+ * launch, host_out[3 w .. 3 w + 2] = start and end %globaltimer (ns) and items processed. */
+int hs_raster_warp_times(unsigned long long *host_out, int n);
 /* out[i] = fixed[i] * 2^-48 (sums == 0: splat gradients) or * 2^-40 (sums != 0: the
  * colour-init weight sums) -- the HS_RASTER_DETERMINISTIC accumulators as float. */
 int hs_fixed_to_float(int64_t n, const long long *fixed, float *out, int sums, void *stream);

@@ -82,6 +82,7 @@ SIGNATURES = {
     "hs_fork_destroy": (None, [_P]),
     "hs_bin_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_raster_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
+    "hs_raster_warp_times": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),
     "hs_adam": (_I, [_L, _I, _L, _P, _P, _P, _P, ctypes.POINTER(_F), _I, _F, _F, _F, _P]),
     "hs_image_metrics": (_I, [_I, _I, _I, _P, _P, _P, _P]),
     "hs_host_register": (_I, [_P, _Z]),

@@ -58,6 +58,9 @@ constexpr int kCW = HS_RASTER_CTA_WARPS;
 // Optional instrumentation (-DHS_RASTER_STATS): forward-pass counts of warp
 // iterations and pixel tests, read with hs_raster_stats().
 __device__ unsigned long long g_raster_stats[16];
+#ifdef HS_RASTER_TIMING
+__device__ unsigned long long g_raster_times[3 * 8192];   // per warp: start, end (globaltimer ns), items
+#endif
 constexpr int kBlocks = kTile * kTile / (32 * kPX);   // 8 x 8 pixel blocks per tile
 constexpr int kRT = 32 * kCW;                          // threads per CTA
 static_assert(kBlocks % kCW == 0, "CTA warps must divide the blocks of a tile");
@@ -636,6 +639,11 @@ __device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, in
     const int total = a.B * nblk;
     const int tiles = nblk / kBlocks;
     unsigned int *work = a.work;
+#ifdef HS_RASTER_TIMING
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    unsigned int n_items = 0;
+#endif
     for (;;) {
         int item = 0;
         if (lane == 0) item = (int)atomicAdd(work, 1u);
@@ -648,7 +656,22 @@ __device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, in
             fn(item / nblk, item % nblk);
         }
         __syncwarp();
+#ifdef HS_RASTER_TIMING
+        ++n_items;
+#endif
     }
+#ifdef HS_RASTER_TIMING
+    if (lane == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        const unsigned int wid = blockIdx.x * kCW + warp;
+        if (wid < 8192) {
+            g_raster_times[3 * wid] = t_start;
+            g_raster_times[3 * wid + 1] = t_end;
+            g_raster_times[3 * wid + 2] = n_items;
+        }
+    }
+#endif
     if (lane == 0) {
         const unsigned int warps = gridDim.x * gridDim.y * kCW;
         if (atomicAdd(work + 1, 1u) == warps - 1) {
@@ -1125,6 +1148,18 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
         default: launch_k(raster_train_kernel<3>, grid, kRT, 0, s, a, nblk); break;
     }
     return check_launch("hs_raster_train");
+}
+
+int hs_raster_warp_times(unsigned long long *host_out, int n) {
+#ifdef HS_RASTER_TIMING
+    cudaMemcpyFromSymbol(host_out, g_raster_times, sizeof(unsigned long long) * 3 * std::min(n, 8192));
+    return check_launch("hs_raster_warp_times");
+#else
+    (void)host_out;
+    (void)n;
+    set_error("hs_raster_warp_times: build with -DHS_RASTER_TIMING");
+    return HS_ERR_SHAPE;
+#endif
 }
 
 int hs_raster_stats(unsigned long long *host_out, int reset) {
