@@ -205,6 +205,13 @@ __device__ __forceinline__ float reduce_scatter(const float (&v)[S], int lane, i
     return r;
 }
 
+// the value only (the slot index is a function of the lane: compute it once)
+template <int S>
+__device__ __forceinline__ float reduce_scatter_value(const float (&v)[S], int lane) {
+    int cnt = S, dup = 0, idx = 0;
+    return ReduceScatter<S, 0>::run(v, lane, idx, cnt, dup);
+}
+
 // ---- 1D bulk async copies (the TMA engine without a tensor map) + mbarriers ----------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {

@@ -92,6 +92,8 @@ struct RasterArgs {
     const uint32_t *tile_order;
     // HS_RASTER_DETERMINISTIC: g_splat / wsums are int64 fixed-point accumulators
     int det;
+    // float mode with a 16-byte aligned g_splat: the adjoint may use vector REDs
+    int vec;
     // speculative launch guard (hs_raster_guard_t): the binning summary and the limits
     // under which its lists are complete; NULL: no guard
     const unsigned long long *guard;
@@ -150,7 +152,12 @@ constexpr float kMeanScale = -2.0f / kK;         // d q / d(k q) folded into g_m
 __device__ __forceinline__ float grad_factor(int v) {
     return v < 2 ? 0.5f * kMeanScale : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
 }
-constexpr int kStageBytes = 96;
+// HS_STAGE_DUP=0: each value stored once (64 B per splat); the packed instructions take
+// the scalar as a broadcast operand (the .F32 form of FFMA2 / FMUL2 / FADD2)
+#ifndef HS_STAGE_DUP
+#define HS_STAGE_DUP 0
+#endif
+constexpr int kStageBytes = HS_STAGE_DUP ? 96 : 64;
 constexpr int kWarpSmem = 32 * (kStageBytes + 48);    // staged splats + the record prefetch slots
 
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
@@ -198,9 +205,10 @@ struct Staged {
     uint32_t gidx, mlo, mhi;
 };
 __device__ __forceinline__ Staged load_staged(uint32_t ad) {
+    Staged t;
+#if HS_STAGE_DUP
     const float4 q0 = lds4(ad), q1 = lds4(ad + 16), q2 = lds4(ad + 32), q3 = lds4(ad + 48), q4 = lds4(ad + 64),
                  q5 = lds4(ad + 80);
-    Staged t;
     t.nmx = f2(q0.x, q0.y);
     t.nmy = f2(q0.z, q0.w);
     t.ka = f2(q1.x, q1.y);
@@ -215,6 +223,25 @@ __device__ __forceinline__ Staged load_staged(uint32_t ad) {
     t.mlo = __float_as_uint(q5.x);
     t.mhi = __float_as_uint(q5.y);
     t.kb = f2(q5.z, q5.w);
+#else
+    const float4 q0 = lds4(ad), q1 = lds4(ad + 16), q2 = lds4(ad + 32);
+    uint32_t mlo, mhi;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mlo), "=r"(mhi) : "r"(ad + 48));
+    t.nmx = f2(q0.x, q0.x);
+    t.nmy = f2(q0.y, q0.y);
+    t.ka = f2(q0.z, q0.z);
+    t.kb2 = f2(q0.w, q0.w);
+    t.kc = f2(q1.x, q1.x);
+    t.nop = f2(q1.y, q1.y);
+    t.ncr = f2(q1.z, q1.z);
+    t.ncg = f2(q1.w, q1.w);
+    t.ncb = f2(q2.x, q2.x);
+    t.kq = q2.y;
+    t.gidx = __float_as_uint(q2.z);
+    t.kb = f2(q2.w, q2.w);
+    t.mlo = mlo;
+    t.mhi = mhi;
+#endif
     return t;
 }
 
@@ -315,18 +342,66 @@ __device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, in
             }
         }
     }
+#if HS_STAGE_DUP
     sts4(saddr, nmx, nmx, nmy, nmy);
     sts4(saddr + 16, ka, ka, kb2, kb2);
     sts4(saddr + 32, kc, kc, -Bv.y, -Bv.y);
     sts4(saddr + 48, -Cv.y, -Cv.y, -Cv.z, -Cv.z);
     sts4(saddr + 64, -Cv.w, -Cv.w, kK * qmax, __uint_as_float(gflag));
     sts4(saddr + 80, __uint_as_float((uint32_t)mask), __uint_as_float((uint32_t)(mask >> 32)), kb, kb);
+#else
+    sts4(saddr, nmx, nmy, ka, kb2);
+    sts4(saddr + 16, kc, -Bv.y, -Cv.y, -Cv.z);
+    sts4(saddr + 32, -Cv.w, kK * qmax, __uint_as_float(gflag), kb);
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr + 48), "r"((uint32_t)mask), "r"((uint32_t)(mask >> 32))
+                 : "memory");
+#endif
     return mask != 0;
 }
 
 // CI: 0 none, 1 max weight (all splats), 2 max weight + weight sums (all splats),
 //     3 max weight + weight sums for splats whose Gaussian is not yet visited.
-constexpr int kMaskBatches = 64;     // per-warp hit masks kept from the forward for the fused adjoint
+constexpr int kMaskBatches = 64;
+
+// HS_FLUSH_VEC: the adjoint's direct adds as vector REDs.  Splat gidx's 9 sums start at
+// float 9 gidx, whose offset mod 4 is gidx mod 4; each alignment class splits the 9 values
+// into 16 / 8 / 4-byte aligned pieces (3 or 4 REDs instead of 9).  Needs a 16-byte
+// aligned g_splat (checked by the launcher) and the float mode.
+#ifndef HS_FLUSH_VEC
+#define HS_FLUSH_VEC 1
+#endif
+__device__ __forceinline__ void red4(float *p, float x, float y, float z, float w) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ void red2(float *p, float x, float y) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ void red_splat9(float *gp, uint32_t gidx, const float (&f)[9]) {
+    switch (gidx & 3u) {
+        case 0:
+            red4(gp, f[0], f[1], f[2], f[3]);
+            red4(gp + 4, f[4], f[5], f[6], f[7]);
+            atomicAdd(gp + 8, f[8]);
+            break;
+        case 1:
+            atomicAdd(gp, f[0]);
+            red2(gp + 1, f[1], f[2]);
+            red4(gp + 3, f[3], f[4], f[5], f[6]);
+            red2(gp + 7, f[7], f[8]);
+            break;
+        case 2:
+            red2(gp, f[0], f[1]);
+            red4(gp + 2, f[2], f[3], f[4], f[5]);
+            red2(gp + 6, f[6], f[7]);
+            atomicAdd(gp + 8, f[8]);
+            break;
+        default:
+            atomicAdd(gp, f[0]);
+            red4(gp + 1, f[1], f[2], f[3], f[4]);
+            red4(gp + 5, f[5], f[6], f[7], f[8]);
+            break;
+    }
+}     // per-warp hit masks kept from the forward for the fused adjoint
 
 template <bool kExplicitGrad>
 __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, float2 fpx2, float2 fpy2, int x0, int y0,
@@ -763,6 +838,16 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
         const uint32_t live_lanes = c_end - c0 >= 32u ? kFull : (1u << (c_end - c0)) - 1u;
         return (masks != nullptr && k < kMaskBatches) ? masks[k] & live_lanes : live_lanes;
     };
+#if HS_FLUSH_VEC
+    // the reduce-scatter's result slot of this lane (a function of the lane only)
+    int rs_vi;
+    bool rs_issue;
+    {
+        const float z[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        (void)reduce_scatter(z, lane, rs_vi, rs_issue);
+    }
+    const float rs_factor = grad_factor(rs_vi);
+#endif
     // back to front: the records of the next batch to walk (k - 1) prefetch while this one runs
     int k = (int)((last - 1 - start) >> 5);
     uint32_t nb_cur = need(k);
@@ -866,6 +951,28 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
         // and one atomic per value.  Constant factors are applied once per reduced value
         // (the mean and conic sums carry -dq, sign folded here).
         auto flush1 = [&](const float (&gv)[9], uint32_t gidx, bool contrib, uint32_t cmask) {
+#if HS_FLUSH_VEC
+            float *gp = a.g_splat + (size_t)gidx * kGS;
+            if (HS_RASTER_DIRECT && __popc(cmask) <= HS_RASTER_DIRECT) {
+                if (contrib) {
+                    if (a.vec) {
+                        float f[9];
+#pragma unroll
+                        for (int v = 0; v < 9; ++v) f[v] = gv[v] * grad_factor(v);
+                        red_splat9(gp, gidx, f);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < 9; ++v) acc_add(a, a.g_splat, (int64_t)gidx * kGS + v, gv[v] * grad_factor(v), kFxGrad);
+                    }
+                }
+            } else {
+                const float s = reduce_scatter_value(gv, lane);
+                if (rs_issue) {
+                    if (a.det) acc_add(a, a.g_splat, (int64_t)gidx * kGS + rs_vi, s * rs_factor, kFxGrad);
+                    else atomicAdd(gp + rs_vi, s * rs_factor);
+                }
+            }
+#else
             if (HS_RASTER_DIRECT && __popc(cmask) <= HS_RASTER_DIRECT) {
                 if (contrib) {
 #pragma unroll
@@ -877,6 +984,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
                 const float s = reduce_scatter(gv, lane, vi, issue);
                 if (issue) acc_add(a, a.g_splat, (int64_t)gidx * kGS + vi, s * grad_factor(vi), kFxGrad);
             }
+#endif
         };
         while (bits) {
             const int j = 31 - __clz(bits);
@@ -1100,6 +1208,7 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     a.grad_image = grad_image;
     a.grad_scale = grad_scale;
     a.g_splat = g_splat;
+    a.vec = !a.det && (reinterpret_cast<uintptr_t>(g_splat) & 15u) == 0;
     const int nblk = tiles_x * tiles_y * kBlocks;
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
@@ -1135,6 +1244,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     a.loss_partials = loss_partials;
     a.grad_scale = grad_scale;
     a.g_splat = g_splat;
+    a.vec = !a.det && (reinterpret_cast<uintptr_t>(g_splat) & 15u) == 0;
     a.pix_T = pix_T;
     a.pix_state = pix_state;
     const int nblk = tiles_x * tiles_y * kBlocks;
