@@ -854,8 +854,9 @@ class Trainer:
                        ctypes.byref(guard) if guard is not None else None, _p(self.raster_ws), s, kernels=kernels)
 
         # fused raster: enqueued speculatively before the step's host sync (device-guarded,
-        # see Binner.bin_tiles), so the GPU goes from the list sorts straight into it
-        spec = raster if (self.fused_raster and self.tile_binning and self.speculative) else None
+        # see Binner.bin_tiles), so the GPU goes from the list sorts straight into it.  Not
+        # while profiling: the stage events would then bracket the raster inside bin_tiles.
+        spec = raster if (self.fused_raster and self.tile_binning and self.speculative and self.events is None) else None
         F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero,
                                                                           order=self.fused_raster, speculate=spec)
         frames = self._last_frames
@@ -1042,7 +1043,7 @@ class Trainer:
                        _p(self.pix_state), _p(out), None, None, None,
                        ctypes.byref(guard) if guard is not None else None, _p(self.raster_ws), _stream())
 
-        spec = raster if (self.tile_binning and self.speculative) else None
+        spec = raster if (self.tile_binning and self.speculative and self.events is None) else None
         F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, order=True,
                                                                           speculate=spec)
         if spec is None or not self.binner.spec_valid:
