@@ -121,9 +121,20 @@ constexpr int kProjHistBins = 4096;
 __device__ __forceinline__ void count_tiles(uint32_t cnt, const TileRect &r, int b, int b0, bool shared, int tiles_x,
                                             int tile_bits, uint32_t *hist, uint32_t *tile_counts) {
     if (!cnt) return;
-    uint32_t *dst = (shared && b == b0) ? hist : tile_counts + ((size_t)b << tile_bits);
-    for (int ty = r.ty0; ty <= r.ty1; ++ty)
-        for (int tx = r.tx0; tx <= r.tx1; ++tx) atomicAdd(dst + ty * tiles_x + tx, 1u);
+    // two loops, so the shared one compiles to shared-memory atomics (a pointer that may
+    // be either would make every add a generic atomic)
+    if (shared && b == b0) {
+        for (int ty = r.ty0; ty <= r.ty1; ++ty) {
+            uint32_t *row = hist + ty * tiles_x;
+            for (int tx = r.tx0; tx <= r.tx1; ++tx) atomicAdd(row + tx, 1u);
+        }
+    } else {
+        uint32_t *dst = tile_counts + ((size_t)b << tile_bits);
+        for (int ty = r.ty0; ty <= r.ty1; ++ty) {
+            uint32_t *row = dst + ty * tiles_x;
+            for (int tx = r.tx0; tx <= r.tx1; ++tx) atomicAdd(row + tx, 1u);
+        }
+    }
 }
 
 // Per-256-item sum of tile counts (the key-offset scan input) and the range of the
@@ -246,17 +257,24 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     const int tile_bits = bit_length_u32((uint32_t)(tiles - 1));
     const int b0 = (int)((blockIdx.x * (int64_t)blockDim.x) / N);
     const bool shared = tile_counts && tiles <= kProjHistBins;
+    // (the histogram is padded to a multiple of 4 bins: 16-byte clears and reads)
+    const int tiles4 = (tiles + 3) >> 2;
     if (shared) {
-        for (int t = threadIdx.x; t < tiles; t += blockDim.x) hist[t] = 0u;
+        for (int t = threadIdx.x; t < tiles4; t += blockDim.x) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
     }
     // the step's per-(frame, splat) accumulators, zeroed here instead of by separate
     // fills (the raster adds into them with atomics); g_splat: the CTA's contiguous
-    // 256 x kGS floats with coalesced stores
+    // 256 x kGS floats with coalesced 16-byte stores (a full CTA's span is 9216 bytes)
     if (zero_gsplat) {
-        const int64_t lo = blockIdx.x * (int64_t)blockDim.x * kGS;
-        const int64_t hi = min((int64_t)B * N, (blockIdx.x + 1) * (int64_t)blockDim.x) * kGS;
-        for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) zero_gsplat[k] = 0.f;
+        float *z = zero_gsplat + blockIdx.x * (int64_t)blockDim.x * kGS;
+        const int items = (int)min((int64_t)blockDim.x, (int64_t)B * N - blockIdx.x * (int64_t)blockDim.x);
+        if (items == (int)blockDim.x && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
+            for (int k = threadIdx.x; k < items * kGS / 4; k += blockDim.x)
+                reinterpret_cast<float4 *>(z)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            for (int k = threadIdx.x; k < items * kGS; k += blockDim.x) z[k] = 0.f;
+        }
     }
     if (i < (int64_t)B * N) {
         if (zero_maxw) zero_maxw[i] = 0.f;
@@ -285,9 +303,12 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     block_sum_store(cnt, dz, block_sums, depth_range);   // (a CTA barrier: the histogram is complete)
     if (shared) {
         uint32_t *row = tile_counts + ((size_t)b0 << tile_bits);
-        for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-            const uint32_t c = hist[t];
-            if (c) atomicAdd(row + t, c);
+        for (int t = threadIdx.x; t < tiles4; t += blockDim.x) {
+            const uint4 c = reinterpret_cast<const uint4 *>(hist)[t];
+            if (c.x) atomicAdd(row + 4 * t, c.x);
+            if (c.y) atomicAdd(row + 4 * t + 1, c.y);
+            if (c.z) atomicAdd(row + 4 * t + 2, c.z);
+            if (c.w) atomicAdd(row + 4 * t + 3, c.w);
         }
     }
 }
@@ -531,7 +552,7 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
         set_error("hs_project_avatar_fwd: tile_rects needs at most 256 tiles per image axis");
         return HS_ERR_SHAPE;
     }
-    const size_t smem = tile_counts && tiles <= kProjHistBins ? sizeof(uint32_t) * tiles : 0;
+    const size_t smem = tile_counts && tiles <= kProjHistBins ? sizeof(uint32_t) * ((tiles + 3) & ~3) : 0;
     launch_k(project_avatar_fwd_kernel, hs_scan_blocks(items), kScanBlock, smem, HS_CHECK_STREAM(stream), 
         B, N, F, width, height, raw10, base14, tri_index, bary, frames, cameras, records, depth, counts,
         block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, tile_counts, tile_rects, err);

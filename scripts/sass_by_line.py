@@ -36,9 +36,10 @@ for l in lines[i0 + 1:]:
         table[int(m.group(1), 16)] = (cur, m.group(2), tuple(chain))
 
 rows = list(csv.reader(open(src_csv)))
-hdr = rows[1]
+h0 = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+hdr = rows[h0]
 ie, st = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
-data = [r for r in rows[2:] if len(r) >= len(hdr)]
+data = [r for r in rows[h0 + 1:] if len(r) >= len(hdr) and r[0].startswith("0x")]
 base = int(data[0][0], 16)
 per, mism, tot, tst = {}, 0, 0, 0
 reg = {name: [0, 0] for name, *_ in ranges}

@@ -1,6 +1,6 @@
 """Kernel-level timing of one stage of the C2 step in isolation (after 100 steps):
     HS_B200_LIB=... python scripts/stage_ab.py <stage> [reps] [flush]
-stage: blend_fwd | blend_bwd | project_fwd | project_bwd | adam.  flush=1 writes 256 MB
+stage: blend_fwd | blend_bwd | project_fwd | project_bwd | adam | fill.  flush=1 writes 256 MB
 between launches (cold L2), else the stage's inputs may be L2-resident."""
 import ctypes
 import os
@@ -31,11 +31,14 @@ F = frames.shape[-2]
 
 
 bn = tr.binner
+bn.depth_range_scratch = torch.tensor([0xFFFFFFFF, 0], dtype=torch.int64, device="cuda").to(torch.int32)
 keys_, vals_, ranges_, tile_bits_, tiles_ = bn.result
 nseg = B << tile_bits_
 
 
 def prep():
+    if stage == "project_fwd":   # the fused tile count adds into zeroed counters (untimed)
+        bn.tile_counts.zero_()
     if stage == "fill":        # the fill consumes the scan's cursors: reset them (untimed)
         bn.cursor[:nseg].copy_(ranges_.view(-1, 2)[:, 0])
 
@@ -46,6 +49,12 @@ def call():
         L.call("hs_tile_fill", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts), _p(rects), _p(tr.depth),
                _p(ranges_), _p(bn.cursor), _p(bn.lists), _p(bn.list_counts), bn.list_half, _p(bn.summary), bn.cap,
                None, _p(bn.vals), bn.fork, s)
+    elif stage == "project_fwd":
+        rects = bn.tile_rects_buffer(B, N, tr.W, tr.H)
+        L.call("hs_project_avatar_fwd", B, N, F, tr.W, tr.H, _p(tr.raw10), _p(av.base14), _p(av.tri_index),
+               _p(av.barycentric), _p(frames), _p(d["cameras"]), _p(tr.records), _p(tr.depth), _p(tr.counts),
+               _p(tr.block_sums), _p(bn.depth_range_scratch), _p(tr.radius), _p(tr.g_splat), None, None,
+               _p(bn.tile_counts), _p(rects), _p(tr.err), s)
     elif stage == "blend_fwd":
         L.call("hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(tr.psi), _p(tr.raw10), s)
     elif stage == "blend_bwd":
