@@ -262,6 +262,63 @@ __device__ __forceinline__ void blend_fwd_tile(int64_t E, int K, int B, int Bp, 
     }
 }
 
+// HS_BLEND_V2: thread owns channels 4 cg .. 4 cg + 3 of the tile and one half of the
+// frames (FB = Bp / 2 of them): per basis one LDS.128 of deltas and FB / 4 LDS.128 of
+// weights feed 2 FB FFMA2 (the weight is the packed instruction's broadcast operand, so
+// psi is stored once per frame); per element still exactly fmaf(psi, delta, acc).
+#ifndef HS_BLEND_V2
+#define HS_BLEND_V2 1
+#endif
+template <int FB, bool kAllNonzero>
+__device__ __forceinline__ void blend_fwd_tile4(int64_t E, int K, int B, int Bp, const float *s_psi,
+                                                const float *stage, int64_t e0, float *__restrict__ raw) {
+    constexpr int kGroups = kBfTE / 4;                 // channel groups per tile
+    const int cg = threadIdx.x % kGroups, fg = threadIdx.x / kGroups;
+    const int c = 4 * cg;
+    const int64_t e = e0 + c;
+    if (e >= E) return;
+    const float4 bv = *reinterpret_cast<const float4 *>(stage + (size_t)K * kBfTE + c);
+    for (int f0 = fg * FB; f0 < B; f0 += 2 * FB) {          // (Bp > 2 FB: frame blocks in turn)
+        float2 acc[FB][2];
+#pragma unroll
+        for (int j = 0; j < FB; ++j) {
+            acc[j][0] = make_float2(bv.x, bv.y);
+            acc[j][1] = make_float2(bv.z, bv.w);
+        }
+#pragma unroll 2
+        for (int k = 0; k < K; ++k) {
+            const float4 d = *reinterpret_cast<const float4 *>(stage + (size_t)k * kBfTE + c);
+            const float2 d01 = make_float2(d.x, d.y), d23 = make_float2(d.z, d.w);
+            float w[FB];
+            if constexpr (FB >= 4) {
+#pragma unroll
+                for (int q = 0; q < FB / 4; ++q) {
+                    const float4 w4 = *reinterpret_cast<const float4 *>(s_psi + (size_t)k * Bp + f0 + 4 * q);
+                    w[4 * q] = w4.x;
+                    w[4 * q + 1] = w4.y;
+                    w[4 * q + 2] = w4.z;
+                    w[4 * q + 3] = w4.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < FB; ++q) w[q] = s_psi[(size_t)k * Bp + f0 + q];
+            }
+#pragma unroll
+            for (int j = 0; j < FB; ++j) {
+                if (kAllNonzero || w[j] != 0.0f) {
+                    acc[j][0] = __ffma2_rn(make_float2(w[j], w[j]), d01, acc[j][0]);
+                    acc[j][1] = __ffma2_rn(make_float2(w[j], w[j]), d23, acc[j][1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < FB; ++j)
+            if (f0 + j < B)
+                __stcs(reinterpret_cast<float4 *>(raw + (int64_t)(f0 + j) * E + e),
+                       make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y));
+    }
+}
+
 __global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, int B, const float *__restrict__ base,
                                                              const float *__restrict__ deltas,
                                                              const float *__restrict__ psi, float *__restrict__ raw) {
@@ -281,8 +338,12 @@ __global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, i
     for (int i = tid; i < K * Bp; i += kBfT) {
         const int k = i / Bp, b = i % Bp;
         const float w = b < B ? psi[b * K + k] : 0.f;
-        s_psi2[2 * i] = w;
-        s_psi2[2 * i + 1] = w;
+        if (HS_BLEND_V2) {
+            s_psi2[i] = w;                                   // [K][Bp]
+        } else {
+            s_psi2[2 * i] = w;
+            s_psi2[2 * i + 1] = w;
+        }
         nz &= (b >= B) || (w != 0.0f);
     }
     const bool all_nonzero = __syncthreads_and(nz);
@@ -306,7 +367,18 @@ __global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, i
         phase ^= 1u << st;
         const float *stage = stages + (size_t)st * (K + 1) * kBfTE;
         const int64_t e0 = t * kBfTE;
-        if (Bp <= 4) {
+        if (HS_BLEND_V2) {
+            if (Bp <= 4) {
+                if (all_nonzero) blend_fwd_tile4<2, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
+                else blend_fwd_tile4<2, false>(E, K, B, Bp, s_psi2, stage, e0, raw);
+            } else if (Bp <= 8) {
+                if (all_nonzero) blend_fwd_tile4<4, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
+                else blend_fwd_tile4<4, false>(E, K, B, Bp, s_psi2, stage, e0, raw);
+            } else {
+                if (all_nonzero) blend_fwd_tile4<8, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
+                else blend_fwd_tile4<8, false>(E, K, B, Bp, s_psi2, stage, e0, raw);
+            }
+        } else if (Bp <= 4) {
             if (all_nonzero) blend_fwd_tile<4, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
             else blend_fwd_tile<4, false>(E, K, B, Bp, s_psi2, stage, e0, raw);
         } else if (Bp <= 8) {
@@ -435,14 +507,16 @@ constexpr int kBMaxK = 32;
 #define HS_BLEND_BLOCKS 296          // one wave at 2 CTAs per SM (148 x 2)
 #endif
 constexpr int kBBlocks = HS_BLEND_BLOCKS;   // persistent grid
-#ifndef HS_BLEND_KBB
-#define HS_BLEND_KBB 1
-#endif
-constexpr int kKBB = HS_BLEND_KBB;  // delta loads in flight per lane (per chunk)
 #ifndef HS_BLEND_CPI
 #define HS_BLEND_CPI 4
 #endif
 constexpr int kCPI = HS_BLEND_CPI;  // chunks per warp iteration
+#ifndef HS_BLEND_PF
+#define HS_BLEND_PF 0                // L2 prefetch distance of the delta rows (bases; 0: off)
+#endif
+#ifndef HS_BLEND_DEPTH
+#define HS_BLEND_DEPTH 0             // cp.async ring depth of the delta rows (bases; 0: registers)
+#endif
 
 template <int BP>
 __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N, int K, int Bc, int b0,
@@ -454,117 +528,125 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
                                                        float *__restrict__ partials, int P,
                                                        int accumulate) {
     pdl_prologue();
-    __shared__ float p_s[kBMaxB * kBMaxK];
+    static_assert(BP % 4 == 0, "frames per pass: a multiple of 4");
+    // psi transposed to [k][b]: a basis' BP weights are BP / 4 16-byte loads
+    __shared__ __align__(16) float p_t[kBMaxK * kBMaxB];
     __shared__ float accw[kBT / 32][BP * kBMaxK];
+#if HS_BLEND_DEPTH
+    __shared__ float s_ring[kBT / 32][HS_BLEND_DEPTH][kCPI * 32];
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < BP * K; i += kBT) {
-        const int b = i / K, k = i % K;
-        p_s[i] = b < Bc ? psi[(b0 + b) * K + k] : 0.f;
+        const int k = i / BP, b = i % BP;
+        p_t[i] = b < Bc ? psi[(b0 + b) * K + k] : 0.f;
     }
     for (int i = lane; i < BP * K; i += 32) accw[warp][i] = 0.f;
     __syncthreads();
     const int64_t E10 = 10 * N, E14 = 14 * N;
     const int64_t chunks = (E14 + 31) / 32;
     // kCPI consecutive 32-channel chunks per warp iteration: the g_psi products of the
-    // chunks are summed in registers before the one reduce-scatter per basis
+    // chunks are summed in registers before the one reduce-scatter per basis.  The frame
+    // values are register pairs (frames b, b + 1): the FMAs are packed FFMA2.
     for (int64_t c0 = ((int64_t)blockIdx.x * (kBT / 32) + warp) * kCPI; c0 < chunks;
          c0 += (int64_t)gridDim.x * (kBT / 32) * kCPI) {
-        float g[kCPI][BP];
+        float2 g[kCPI][BP / 2];
         bool in10[kCPI];
 #pragma unroll
         for (int j = 0; j < kCPI; ++j) {
             const int64_t e = (c0 + j) * 32 + lane;
             const bool in = e < E14;
             in10[j] = e < E10;
-            float s = 0.f;
+            float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int b = 0; b < BP; ++b) {
-                g[j][b] = (in && b < Bc) ? __ldcs(g_raw + (int64_t)(b0 + b) * E14 + e) : 0.f;
-                s += g[j][b];
+            for (int h = 0; h < BP / 2; ++h) {
+                const int b = 2 * h;
+                g[j][h].x = (in && b < Bc) ? __ldcs(g_raw + (int64_t)(b0 + b) * E14 + e) : 0.f;
+                g[j][h].y = (in && b + 1 < Bc) ? __ldcs(g_raw + (int64_t)(b0 + b + 1) * E14 + e) : 0.f;
+                s2 = __fadd2_rn(s2, g[j][h]);
             }
+            const float s = s2.x + s2.y;
             if (in) g_base[e] = accumulate ? g_base[e] + s : s;
         }
         if (c0 * 32 >= E10) continue;                      // warp-uniform
         const int64_t e0 = c0 * 32 + lane;
-        if constexpr (kKBB == 1) {
-            // software pipeline over the bases: basis k+1's delta loads are issued before
-            // basis k's FMAs and reduce-scatter, so a load's latency hides behind a whole
-            // basis of work instead of stalling the warp once per basis
-            float dn[kCPI];
-#pragma unroll
-            for (int j = 0; j < kCPI; ++j) dn[j] = in10[j] ? __ldcs(deltas + e0 + 32 * j) : 0.f;
-            for (int k = 0; k < K; ++k) {
-                float dk[kCPI];
-#pragma unroll
-                for (int j = 0; j < kCPI; ++j) dk[j] = dn[j];
-                if (k + 1 < K) {
-#pragma unroll
-                    for (int j = 0; j < kCPI; ++j)
-                        dn[j] = in10[j] ? __ldcs(deltas + (int64_t)(k + 1) * E10 + e0 + 32 * j) : 0.f;
-                }
-                float gd[kCPI];
-                float v[BP];
-#pragma unroll
-                for (int j = 0; j < kCPI; ++j) gd[j] = 0.f;
-#pragma unroll
-                for (int b = 0; b < BP; ++b) {
-                    const float pk = p_s[b * K + k];
-                    v[b] = 0.f;
-#pragma unroll
-                    for (int j = 0; j < kCPI; ++j) {
-                        gd[j] = fmaf(pk, g[j][b], gd[j]);
-                        v[b] = fmaf(dk[j], g[j][b], v[b]);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < kCPI; ++j)
-                    if (in10[j]) {
-                        float *o = g_deltas + (int64_t)k * E10 + e0 + 32 * j;
-                        *o = accumulate ? *o + gd[j] : gd[j];
-                    }
-                int vi;
-                bool issue;
-                const float r = reduce_scatter(v, lane, vi, issue);
-                if (issue) accw[warp][k * BP + vi] += r;
-            }
-            continue;
-        }
-        for (int k0 = 0; k0 < K; k0 += kKBB) {
-          float dk[kCPI][kKBB];
-#pragma unroll
-          for (int q = 0; q < kKBB; ++q)     // issue the round's loads before any use
-#pragma unroll
-              for (int j = 0; j < kCPI; ++j)
-                  dk[j][q] = in10[j] ? __ldcs(deltas + (int64_t)min(k0 + q, K - 1) * E10 + e0 + 32 * j) : 0.f;
-#pragma unroll
-          for (int q = 0; q < kKBB; ++q) {
-            const int k = k0 + q;
-            if (k >= K) break;
-            float gd[kCPI];
-            float v[BP];
-#pragma unroll
-            for (int j = 0; j < kCPI; ++j) gd[j] = 0.f;
-#pragma unroll
-            for (int b = 0; b < BP; ++b) {
-                const float pk = p_s[b * K + k];
-                v[b] = 0.f;
+#if HS_BLEND_DEPTH
+        // the delta rows stream through a per-warp ring of HS_BLEND_DEPTH bases in shared
+        // memory with cp.async (each lane copies the 4 floats it reads: no cross-lane
+        // dependency), so that many bases' loads are in flight without holding registers
+        const uint32_t ring = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]);
+        auto issue = [&](int k) {
+            if (k < K) {
 #pragma unroll
                 for (int j = 0; j < kCPI; ++j) {
-                    gd[j] = fmaf(pk, g[j][b], gd[j]);
-                    v[b] = fmaf(dk[j][q], g[j][b], v[b]);
+                    const uint32_t dst = ring + (uint32_t)(((k % HS_BLEND_DEPTH) * kCPI * 32 + 32 * j + lane) * 4);
+                    const float *src = deltas + (int64_t)k * E10 + e0 + 32 * j;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(in10[j] ? src : deltas),
+                                 "r"(in10[j] ? 4 : 0) : "memory");
                 }
             }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+#pragma unroll
+        for (int k = 0; k < HS_BLEND_DEPTH - 1; ++k) issue(k);
+        for (int k = 0; k < K; ++k) {
+            issue(k + HS_BLEND_DEPTH - 1);
+            asm volatile("cp.async.wait_group %0;" ::"n"(HS_BLEND_DEPTH - 1) : "memory");
+            float dk[kCPI];
+#pragma unroll
+            for (int j = 0; j < kCPI; ++j) dk[j] = s_ring[warp][k % HS_BLEND_DEPTH][32 * j + lane];
+#else
+        // software pipeline over the bases: basis k+1's delta loads are issued before
+        // basis k's FMAs and reduce-scatter, so a load's latency hides behind a whole
+        // basis of work instead of stalling the warp once per basis
+        float dn[kCPI];
+#pragma unroll
+        for (int j = 0; j < kCPI; ++j) dn[j] = in10[j] ? __ldcs(deltas + e0 + 32 * j) : 0.f;
+        for (int k = 0; k < K; ++k) {
+            float dk[kCPI];
+#pragma unroll
+            for (int j = 0; j < kCPI; ++j) dk[j] = dn[j];
+            if (k + 1 < K) {
+#pragma unroll
+                for (int j = 0; j < kCPI; ++j)
+                    dn[j] = in10[j] ? __ldcs(deltas + (int64_t)(k + 1) * E10 + e0 + 32 * j) : 0.f;
+            }
+#endif
+            float2 pk[BP / 2];
+#pragma unroll
+            for (int q = 0; q < BP / 4; ++q) {
+                const float4 w = *reinterpret_cast<const float4 *>(p_t + k * BP + 4 * q);
+                pk[2 * q] = make_float2(w.x, w.y);
+                pk[2 * q + 1] = make_float2(w.z, w.w);
+            }
+            float2 gd[kCPI], v[BP / 2];
+#pragma unroll
+            for (int j = 0; j < kCPI; ++j) gd[j] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int h = 0; h < BP / 2; ++h) v[h] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int h = 0; h < BP / 2; ++h)
+#pragma unroll
+                for (int j = 0; j < kCPI; ++j) {
+                    gd[j] = __ffma2_rn(pk[h], g[j][h], gd[j]);
+                    v[h] = __ffma2_rn(make_float2(dk[j], dk[j]), g[j][h], v[h]);
+                }
 #pragma unroll
             for (int j = 0; j < kCPI; ++j)
                 if (in10[j]) {
                     float *o = g_deltas + (int64_t)k * E10 + e0 + 32 * j;
-                    *o = accumulate ? *o + gd[j] : gd[j];
+                    const float r = gd[j].x + gd[j].y;
+                    *o = accumulate ? *o + r : r;
                 }
+            float vf[BP];
+#pragma unroll
+            for (int h = 0; h < BP / 2; ++h) {
+                vf[2 * h] = v[h].x;
+                vf[2 * h + 1] = v[h].y;
+            }
             int vi;
             bool issue;
-            const float r = reduce_scatter(v, lane, vi, issue);
+            const float r = reduce_scatter(vf, lane, vi, issue);
             if (issue) accw[warp][k * BP + vi] += r;
-          }
         }
     }
     __syncthreads();
@@ -573,6 +655,207 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < kBT / 32; ++w) s += accw[w][k * BP + b];
+        partials[((int64_t)(b0 + b) * K + k) * P + blockIdx.x] = s;
+    }
+}
+
+// HS_BLEND_BWD_TMA: the same adjoint over kBbTE-channel tiles staged in shared memory by
+// 1D bulk copies (the frames' g rows and the bases' delta rows, kBbS stages in flight)
+// for 9..16-frame passes with K <= 20 and N % (kBbTE / 2) == 0 (every tile full, every
+// row 16-byte aligned).  Per tile, with 256 threads:
+//   g_base / g_delta: thread (cg = t % (TE / 4), kg = t / (TE / 4)) owns channels 4 cg ..
+//     4 cg + 3 and bases kg, kg + kBbKG, ...: its frames' g (LDS.128 each) times psi (the
+//     packed FFMA2's broadcast operand), one 16-byte store per basis;
+//   g_psi: thread (c = t % 16, blk = t / 16) accumulates frames 4 (blk % 4) .. + 3 x bases
+//     5 (blk / 4) .. + 4 over channels 64 h + 4 c .. + 3 (packed pairs of channels, 40
+//     FFMA2 per 64 channels), kept in registers across the CTA's tiles and reduced over
+//     the 16 channel groups once at the end (one partial per CTA).
+// Per tile the FFMA2 count is the floor of both products (2 x 16 x 20 x TE / 2 / 256 per
+// thread); the loads are 36 rows of 4 TE bytes.
+#ifndef HS_BLEND_BWD_TMA
+#define HS_BLEND_BWD_TMA 1
+#endif
+#ifndef HS_BLEND_BWD_STAGES
+#define HS_BLEND_BWD_STAGES 2
+#endif
+#ifndef HS_BB_DIAG
+#define HS_BB_DIAG 0                 // diagnostics: 1 skips g_psi, 2 skips the g_delta stores
+#endif
+#ifndef HS_BB_TE
+#define HS_BB_TE 256                 // (1 KB rows: 128-channel tiles' 512-byte copies load at ~2/3 the rate)
+#endif
+constexpr int kBbTE = HS_BB_TE;                    // channels per tile
+constexpr int kBbKG = 1024 / kBbTE;                // g_delta: basis groups (threads per channel quad: 256 / (TE / 4))
+constexpr int kBbKPT = (20 + kBbKG - 1) / kBbKG;   // bases per thread
+constexpr int kBbS = HS_BLEND_BWD_STAGES;
+constexpr int kBbK = 20;                           // max bases of this path (4 blocks of 5)
+constexpr int kBbStage = (16 + kBbK) * kBbTE;      // floats per stage: 16 g rows + 20 delta rows
+__host__ inline size_t blend_bwd_tma_smem() {
+    return 64 + sizeof(float) * ((size_t)kBbS * kBbStage + kBbK * 16 + 16 * 16 * 20);
+}
+
+__global__ void __launch_bounds__(256, 2) blend_bwd_tma_kernel(int64_t N, int K, int Bc, int b0,
+                                                               const float *__restrict__ deltas,
+                                                               const float *__restrict__ psi,
+                                                               const float *__restrict__ g_raw,
+                                                               float *__restrict__ g_base,
+                                                               float *__restrict__ g_deltas,
+                                                               float *__restrict__ partials, int P, int accumulate) {
+    pdl_prologue();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    float *stages = reinterpret_cast<float *>(smem_raw + 64);          // kBbS x [16 g | K d] x kBbTE
+    float *p_t = stages + (size_t)kBbS * kBbStage;                     // psi [k][16]
+    float *red = p_t + kBbK * 16;                                      // [16 blk][16 c][20] g_psi reduce
+    const int tid = threadIdx.x;
+    const int64_t E10 = 10 * N, E14 = 14 * N;
+    const int64_t ntiles = E14 / kBbTE, ntiles10 = E10 / kBbTE;
+    if (tid == 0) {
+        for (int st = 0; st < kBbS; ++st) mbar_init(&bars[st], 1);
+        mbar_fence_init();
+    }
+    for (int i = tid; i < kBbK * 16; i += 256) {
+        const int k = i / 16, b = i % 16;
+        p_t[i] = (k < K && b < Bc) ? psi[(b0 + b) * K + k] : 0.f;
+    }
+    __syncthreads();
+    // warp 0 issues a stage: lane 0 registers the bytes, lanes issue one row each
+    auto issue = [&](int64_t t, int st) {
+        const int lane = tid & 31;
+        const int64_t e0 = t * kBbTE;
+        const int rows = Bc + (t < ntiles10 ? K : 0);
+        float *dst = stages + (size_t)st * kBbStage;
+        if (lane == 0) mbar_expect_tx(&bars[st], (uint32_t)(rows * kBbTE * 4));
+        __syncwarp();
+        for (int r = lane; r < rows; r += 32) {
+            if (r < Bc) bulk_g2s(dst + (size_t)r * kBbTE, g_raw + (int64_t)(b0 + r) * E14 + e0, kBbTE * 4, &bars[st]);
+            else bulk_g2s(dst + (size_t)(16 + r - Bc) * kBbTE, deltas + (int64_t)(r - Bc) * E10 + e0, kBbTE * 4, &bars[st]);
+        }
+    };
+    if (tid < 32) {
+        for (int st = 0; st < kBbS; ++st)
+            if (blockIdx.x + (int64_t)st * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)st * gridDim.x, st);
+    }
+    // g_psi accumulators: frames 4 bb .. 4 bb + 3, bases 5 kb .. 5 kb + 4, channel pairs
+    const int rc = tid & 15, blk = tid >> 4, bb = blk & 3, kb = blk >> 2;
+    float2 acc[4][5];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[i][q] = make_float2(0.f, 0.f);
+    const int cg = tid % (kBbTE / 4), kg = tid / (kBbTE / 4);
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % kBbS;
+        mbar_wait(&bars[st], (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const float *sg = stages + (size_t)st * kBbStage, *sd = sg + 16 * kBbTE;
+        const int64_t e0 = t * kBbTE;
+        const bool blended = t < ntiles10;
+        // g_base and g_delta
+        if (blended || kg == 0) {
+            // frames in two halves of 8 (registers); each thread's <= 3 bases accumulate
+            float2 a[kBbKPT][2], s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < kBbKPT; ++j) a[j][0] = a[j][1] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float4 g[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int b = 8 * h + i;
+                    g[i] = b < Bc ? *reinterpret_cast<const float4 *>(sg + b * kBbTE + 4 * cg)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                if (kg == 0) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        s01 = __fadd2_rn(s01, make_float2(g[i].x, g[i].y));
+                        s23 = __fadd2_rn(s23, make_float2(g[i].z, g[i].w));
+                    }
+                }
+                if (blended) {
+#pragma unroll
+                    for (int j = 0; j < kBbKPT; ++j) {
+                        const int k = kg + kBbKG * j;
+                        if (k < K) {
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) {
+                                const float4 w = *reinterpret_cast<const float4 *>(p_t + k * 16 + 8 * h + 4 * q);
+                                const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float4 gb = g[4 * q + i];
+                                    a[j][0] = __ffma2_rn(make_float2(wv[i], wv[i]), make_float2(gb.x, gb.y), a[j][0]);
+                                    a[j][1] = __ffma2_rn(make_float2(wv[i], wv[i]), make_float2(gb.z, gb.w), a[j][1]);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if (kg == 0) {
+                float4 *o = reinterpret_cast<float4 *>(g_base + e0 + 4 * cg);
+                float4 r = make_float4(s01.x, s01.y, s23.x, s23.y);
+                if (accumulate) {
+                    const float4 q = *o;
+                    r = make_float4(q.x + r.x, q.y + r.y, q.z + r.z, q.w + r.w);
+                }
+                *o = r;
+            }
+            if (blended && !(HS_BB_DIAG & 2)) {
+#pragma unroll
+                for (int j = 0; j < kBbKPT; ++j) {
+                    const int k = kg + kBbKG * j;
+                    if (k < K) {
+                        float4 *o = reinterpret_cast<float4 *>(g_deltas + (int64_t)k * E10 + e0 + 4 * cg);
+                        float4 r = make_float4(a[j][0].x, a[j][0].y, a[j][1].x, a[j][1].y);
+                        if (accumulate) {
+                            const float4 q = *o;
+                            r = make_float4(q.x + r.x, q.y + r.y, q.z + r.z, q.w + r.w);
+                        }
+                        __stcs(o, r);
+                    }
+                }
+            }
+        }
+        // g_psi partial sums
+        if (blended && !(HS_BB_DIAG & 1)) {
+#pragma unroll
+            for (int h = 0; h < kBbTE / 64; ++h) {
+                const int c = 64 * h + 4 * rc;
+                float4 gv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) gv[i] = *reinterpret_cast<const float4 *>(sg + (4 * bb + i) * kBbTE + c);
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const int k = 5 * kb + q;
+                    if (k < K) {
+                        const float4 dv = *reinterpret_cast<const float4 *>(sd + k * kBbTE + c);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            acc[i][q] = __ffma2_rn(make_float2(gv[i].x, gv[i].y), make_float2(dv.x, dv.y), acc[i][q]);
+                            acc[i][q] = __ffma2_rn(make_float2(gv[i].z, gv[i].w), make_float2(dv.z, dv.w), acc[i][q]);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();                     // every thread is done with this stage
+        if (tid < 32 && t + kBbS * (int64_t)gridDim.x < ntiles) issue(t + kBbS * (int64_t)gridDim.x, st);
+    }
+    // g_psi: sum the 16 channel groups of each (frame, basis) block in a fixed order
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) red[(blk * 16 + rc) * 20 + i * 5 + q] = acc[i][q].x + acc[i][q].y;
+    __syncthreads();
+    for (int o = tid; o < Bc * K; o += 256) {
+        const int b = o / K, k = o % K;
+        const int ob = (b >> 2) | ((k / 5) << 2), oi = (b & 3) * 5 + k % 5;
+        float s = 0.f;
+        for (int c = 0; c < 16; ++c) s += red[(ob * 16 + c) * 20 + oi];
         partials[((int64_t)(b0 + b) * K + k) * P + blockIdx.x] = s;
     }
 }
@@ -993,10 +1276,18 @@ int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
     }
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const int P = hs_blend_bwd_partials(N);
+    const bool tma = HS_BLEND_BWD_TMA && N % (kBbTE / 2) == 0 && K <= kBbK && P == kBBlocks &&
+                     (uintptr_t)deltas % 16 == 0 && (uintptr_t)g_raw14 % 16 == 0 && (uintptr_t)g_base14 % 16 == 0 &&
+                     (uintptr_t)g_deltas % 16 == 0;
+    if (tma) cudaFuncSetAttribute(blend_bwd_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)blend_bwd_tma_smem());
     for (int b0 = 0; b0 < B; b0 += kBMaxB) {
         const int Bc = std::min(kBMaxB, B - b0);
         const int acc = b0 > 0;
-        if (Bc <= 4)
+        if (tma && Bc > 8)
+            launch_k(blend_bwd_tma_kernel, P, 256, blend_bwd_tma_smem(), s, N, K, Bc, b0, deltas, psi, g_raw14,
+                     g_base14, g_deltas, gpsi_partials, P, acc);
+        else if (Bc <= 4)
             launch_k(blend_bwd_kernel<4>, P, kBT, 0, s, N, K, Bc, b0, deltas, psi, g_raw14, g_base14, g_deltas,
                                                   gpsi_partials, P, acc);
         else if (Bc <= 8)

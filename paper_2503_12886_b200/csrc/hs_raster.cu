@@ -461,7 +461,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     const float2 one2 = f2(1.f, 1.f);
 
 #ifdef HS_RASTER_STATS
-    unsigned long long st_iter = 0, st_c = 0, st_batches = 0;
+    unsigned long long st_iter = 0, st_c = 0, st_batches = 0, st_empty = 0, st_live = 0;
 #endif
     // record prefetch: slot of this lane, and the list value of the next batch
     const uint32_t rslot = wbase + 32 * kStageBytes + lane * kRecBytes;
@@ -540,6 +540,13 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
 #ifdef HS_RASTER_STATS
             st_iter += (lane == 0);
             st_c += (nal.x != 0.f) + (nal.y != 0.f);
+            {
+                const bool any_c = __any_sync(kFull, nal.x != 0.f || nal.y != 0.f);
+                const int nlive = __popc(__ballot_sync(kFull, (t.mlo & lanebit) && T.x >= kTermEps)) +
+                                  __popc(__ballot_sync(kFull, (t.mhi & lanebit) && T.y >= kTermEps));
+                st_empty += (lane == 0) && !any_c;
+                st_live += (lane == 0) ? nlive : 0;
+            }
 #endif
             const float2 nw = mul2(nal, T);                    // -alpha T
             C[0] = fma2(nw, t.ncr, C[0]);
@@ -588,6 +595,8 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     atomicAdd(&g_raster_stats[0], st_iter);
     atomicAdd(&g_raster_stats[3], st_c);
     atomicAdd(&g_raster_stats[6], st_batches);
+    atomicAdd(&g_raster_stats[4], st_empty);
+    atomicAdd(&g_raster_stats[1], st_live);
 #endif
     // pixel p: a terminated pixel keeps the stop index found above (its terminating
     // splat + 1); a live one gets the list length (S/render.py:254-259: no stop)

@@ -624,6 +624,7 @@ class Trainer:
         self.debug_before_backward = None
         self.capture_pixels = False     # fused raster also writes pix_T / pix_state (checker)
         self.speculative = True         # enqueue the raster before the step's host sync (guarded)
+        self.profile_speculative = False  # keep speculating while stage events are recorded
         self.counts = torch.empty(B * N, dtype=torch.int32, device=d)
         self.nblocks = int(L.load().hs_scan_blocks(B * N))
         self.block_sums = torch.empty(self.nblocks, dtype=torch.int32, device=d)
@@ -856,7 +857,7 @@ class Trainer:
         # fused raster: enqueued speculatively before the step's host sync (device-guarded,
         # see Binner.bin_tiles), so the GPU goes from the list sorts straight into it.  Not
         # while profiling: the stage events would then bracket the raster inside bin_tiles.
-        spec = raster if (self.fused_raster and self.tile_binning and self.speculative and self.events is None) else None
+        spec = raster if (self.fused_raster and self.tile_binning and self.speculative and (self.events is None or self.profile_speculative)) else None
         F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, zero,
                                                                           order=self.fused_raster, speculate=spec)
         frames = self._last_frames
@@ -1043,7 +1044,7 @@ class Trainer:
                        _p(self.pix_state), _p(out), None, None, None,
                        ctypes.byref(guard) if guard is not None else None, _p(self.raster_ws), _stream())
 
-        spec = raster if (self.tile_binning and self.speculative and self.events is None) else None
+        spec = raster if (self.tile_binning and self.speculative and (self.events is None or self.profile_speculative)) else None
         F, (keys, vals, ranges, tile_bits, tiles) = self._forward_project(thetas, frames, cameras, order=True,
                                                                           speculate=spec)
         if spec is None or not self.binner.spec_valid:

@@ -16,6 +16,9 @@ torch.cuda.synchronize()
 L.load().hs_raster_stats(buf, 1)
 it, test, q, c, empty, full, batches, _ = list(buf)[:8]
 hist = list(buf)[8:15]
+print(f"forward: iterations {it}, live pixel slots per iteration {test / max(it, 1):.1f} of 64, "
+      f"iterations with no composited pixel {empty} ({empty / max(it, 1) * 100:.1f}%), composited pixels per iteration "
+      f"{c / max(it, 1):.1f}")
 print(f"keys {tr.last_total}  warp-iters {it}  per key {it / tr.last_total:.2f}  pixel-tests {test} "
       f"({test / max(it, 1):.1f} per iter of 64 slots)  q-pass {q} ({q / max(test, 1) * 100:.1f}%)  contrib {c} "
       f"({c / max(test, 1) * 100:.1f}%)  no-q iters {empty} ({empty / max(it, 1) * 100:.1f}%)  full-cover iters {full} "

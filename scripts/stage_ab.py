@@ -1,7 +1,8 @@
 """Kernel-level timing of one stage of the C2 step in isolation (after 100 steps):
     HS_B200_LIB=... python scripts/stage_ab.py <stage> [reps] [flush]
-stage: blend_fwd | blend_bwd | project_fwd | project_bwd | adam | fill.  flush=1 writes 256 MB
-between launches (cold L2), else the stage's inputs may be L2-resident."""
+stage: blend_fwd | blend_bwd | project_fwd | project_bwd | adam | fill | copy.  flush=1 writes
+256 MB between launches (cold L2, but the evicted lines are dirty: their write-back lands in
+the timed kernel), flush=2 reads 256 MB (cold and clean), else the inputs may be L2-resident."""
 import ctypes
 import os
 import sys
@@ -17,7 +18,8 @@ from paper_2503_12886_b200.device import _p
 
 stage = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-flush_on = len(sys.argv) > 3 and sys.argv[3] == "1"
+flush_on = len(sys.argv) > 3 and sys.argv[3] in ("1", "2")
+flush_read = len(sys.argv) > 3 and sys.argv[3] == "2"     # 2: evict L2 by reading (no dirty lines left)
 tr, d, wl = bench.make_trainer(bench.CONFIGS["C2"])
 for _ in range(int(os.environ.get("RAB_STEPS", "100"))):
     tr.step(d["thetas"], d["targets"], None, d["cameras"], d["backgrounds"])
@@ -34,6 +36,10 @@ bn = tr.binner
 bn.depth_range_scratch = torch.tensor([0xFFFFFFFF, 0], dtype=torch.int64, device="cuda").to(torch.int32)
 keys_, vals_, ranges_, tile_bits_, tiles_ = bn.result
 nseg = B << tile_bits_
+
+
+copy_src = torch.empty(37 << 18, dtype=torch.float32, device="cuda").fill_(1.0)
+copy_dst = torch.empty_like(copy_src)
 
 
 def prep():
@@ -55,6 +61,8 @@ def call():
                _p(av.barycentric), _p(frames), _p(d["cameras"]), _p(tr.records), _p(tr.depth), _p(tr.counts),
                _p(tr.block_sums), _p(bn.depth_range_scratch), _p(tr.radius), _p(tr.g_splat), None, None,
                _p(bn.tile_counts), _p(rects), _p(tr.err), s)
+    elif stage == "copy":        # calibration: a 37 MB device copy (74 MB of traffic, blend_fwd's size)
+        copy_dst.copy_(copy_src)
     elif stage == "blend_fwd":
         L.call("hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(tr.psi), _p(tr.raw10), s)
     elif stage == "blend_bwd":
@@ -72,7 +80,9 @@ def call():
 
 times = []
 for r in range(reps + 3):
-    if flush_on:
+    if flush_read:
+        flush_sum = flush.sum()
+    elif flush_on:
         flush.fill_(1.0)
     prep()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
