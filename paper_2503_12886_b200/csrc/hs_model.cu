@@ -511,12 +511,6 @@ constexpr int kBBlocks = HS_BLEND_BLOCKS;   // persistent grid
 #define HS_BLEND_CPI 4
 #endif
 constexpr int kCPI = HS_BLEND_CPI;  // chunks per warp iteration
-#ifndef HS_BLEND_PF
-#define HS_BLEND_PF 0                // L2 prefetch distance of the delta rows (bases; 0: off)
-#endif
-#ifndef HS_BLEND_DEPTH
-#define HS_BLEND_DEPTH 0             // cp.async ring depth of the delta rows (bases; 0: registers)
-#endif
 
 template <int BP>
 __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N, int K, int Bc, int b0,
@@ -532,9 +526,6 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
     // psi transposed to [k][b]: a basis' BP weights are BP / 4 16-byte loads
     __shared__ __align__(16) float p_t[kBMaxK * kBMaxB];
     __shared__ float accw[kBT / 32][BP * kBMaxK];
-#if HS_BLEND_DEPTH
-    __shared__ float s_ring[kBT / 32][HS_BLEND_DEPTH][kCPI * 32];
-#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < BP * K; i += kBT) {
         const int k = i / BP, b = i % BP;
@@ -569,32 +560,6 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
         }
         if (c0 * 32 >= E10) continue;                      // warp-uniform
         const int64_t e0 = c0 * 32 + lane;
-#if HS_BLEND_DEPTH
-        // the delta rows stream through a per-warp ring of HS_BLEND_DEPTH bases in shared
-        // memory with cp.async (each lane copies the 4 floats it reads: no cross-lane
-        // dependency), so that many bases' loads are in flight without holding registers
-        const uint32_t ring = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]);
-        auto issue = [&](int k) {
-            if (k < K) {
-#pragma unroll
-                for (int j = 0; j < kCPI; ++j) {
-                    const uint32_t dst = ring + (uint32_t)(((k % HS_BLEND_DEPTH) * kCPI * 32 + 32 * j + lane) * 4);
-                    const float *src = deltas + (int64_t)k * E10 + e0 + 32 * j;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(in10[j] ? src : deltas),
-                                 "r"(in10[j] ? 4 : 0) : "memory");
-                }
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-#pragma unroll
-        for (int k = 0; k < HS_BLEND_DEPTH - 1; ++k) issue(k);
-        for (int k = 0; k < K; ++k) {
-            issue(k + HS_BLEND_DEPTH - 1);
-            asm volatile("cp.async.wait_group %0;" ::"n"(HS_BLEND_DEPTH - 1) : "memory");
-            float dk[kCPI];
-#pragma unroll
-            for (int j = 0; j < kCPI; ++j) dk[j] = s_ring[warp][k % HS_BLEND_DEPTH][32 * j + lane];
-#else
         // software pipeline over the bases: basis k+1's delta loads are issued before
         // basis k's FMAs and reduce-scatter, so a load's latency hides behind a whole
         // basis of work instead of stalling the warp once per basis
@@ -610,7 +575,6 @@ __global__ void __launch_bounds__(kBT, HS_BLEND_MINB) blend_bwd_kernel(int64_t N
                 for (int j = 0; j < kCPI; ++j)
                     dn[j] = in10[j] ? __ldcs(deltas + (int64_t)(k + 1) * E10 + e0 + 32 * j) : 0.f;
             }
-#endif
             float2 pk[BP / 2];
 #pragma unroll
             for (int q = 0; q < BP / 4; ++q) {
