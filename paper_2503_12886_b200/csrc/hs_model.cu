@@ -1240,7 +1240,7 @@ int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
     }
     cudaStream_t s = HS_CHECK_STREAM(stream);
     const int P = hs_blend_bwd_partials(N);
-    const bool tma = HS_BLEND_BWD_TMA && N % (kBbTE / 2) == 0 && K <= kBbK && P == kBBlocks &&
+    const bool tma = HS_BLEND_BWD_TMA && N % (kBbTE / 2) == 0 && K <= kBbK &&
                      (uintptr_t)deltas % 16 == 0 && (uintptr_t)g_raw14 % 16 == 0 && (uintptr_t)g_base14 % 16 == 0 &&
                      (uintptr_t)g_deltas % 16 == 0;
     if (tma) cudaFuncSetAttribute(blend_bwd_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -35,7 +35,7 @@ def _rel(a, b):
     return float((a - b).abs().max() / max(float(b.abs().max()), 1e-30))
 
 
-@pytest.mark.parametrize("N,K,B", [(50176, 20, 16), (256, 20, 32), (19881, 20, 4), (1000, 7, 12), (1280, 20, 9)])
+@pytest.mark.parametrize("N,K,B", [(50176, 20, 16), (4096, 20, 16), (256, 20, 32), (19881, 20, 4), (1000, 7, 12), (1280, 20, 9)])
 def test_blend_bwd_matches_float64(N, K, B):
     from paper_2503_12886_b200 import _lib as L
     g = torch.Generator().manual_seed(N + K + B)
@@ -80,3 +80,4 @@ def test_blend_fwd_matches_float64(B, zero):
     ref = base14[:10 * N].double()[None] + psi.double() @ deltas.view(K, 10 * N).double()
     assert torch.isfinite(raw).all()
     assert _rel(raw.view(B, 10 * N).double(), ref) <= 2e-6
+
