@@ -1211,7 +1211,10 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
         cudaFuncSetAttribute(blend_fwd_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
         const int per_sm = std::max(1, (int)((220 * 1024) / tsm));
         const int64_t ntiles = (E + kBfTE - 1) / kBfTE;
-        const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * std::min(per_sm, 8));
+#ifndef HS_BLEND_CTAS_PER_SM
+#define HS_BLEND_CTAS_PER_SM 8
+#endif
+        const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * std::min(per_sm, HS_BLEND_CTAS_PER_SM));
         launch_k(blend_fwd_tma_kernel, grid, kBfT, tsm, s, E, K, B, base14, deltas, psi, raw10);
     } else if (vec) {
         // grid.y splits the frames into chunks of HS_BLEND_BC: few accumulators per
