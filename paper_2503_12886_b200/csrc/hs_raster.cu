@@ -158,17 +158,7 @@ __device__ __forceinline__ float grad_factor(int v) {
 #define HS_STAGE_DUP 0
 #endif
 constexpr int kStageBytes = HS_STAGE_DUP ? 96 : 64;
-// HS_FLUSH_SMEM: the adjoint's 9-value warp reduction through shared memory instead of
-// the shuffle reduce-scatter: every lane stores its 9 partial sums as one column of a
-// 9 x 36-float table (rows padded to 36 floats: the readers' 16-byte loads then fall in
-// distinct banks), then 18 lanes each sum half a row (4 LDS.128, packed adds) and pairs
-// combine with one shuffle.
-#ifndef HS_FLUSH_SMEM
-#define HS_FLUSH_SMEM 0
-#endif
-constexpr int kRedRow = 36;
-constexpr int kRedBytes = HS_FLUSH_SMEM ? 9 * kRedRow * 4 : 0;
-constexpr int kWarpSmem = 32 * (kStageBytes + 48) + kRedBytes;   // staged splats, record prefetch slots, reduce table
+constexpr int kWarpSmem = 32 * (kStageBytes + 48);    // staged splats + the record prefetch slots
 
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
     float4 v;
@@ -867,13 +857,6 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
     }
     const float rs_factor = grad_factor(rs_vi);
 #endif
-#if HS_FLUSH_SMEM
-    const uint32_t red_base = wbase + 32 * (kStageBytes + kRecBytes);
-    const int red_v = lane >> 1;                          // lanes < 18: row red_v, half lane & 1
-    const uint32_t red_rd = red_base + (uint32_t)(red_v * kRedRow + (lane & 1) * 16) * 4u;
-    const uint32_t red_wr = red_base + (uint32_t)lane * 4u;
-    const float red_factor = grad_factor(red_v < 9 ? red_v : 0);
-#endif
     // back to front: the records of the next batch to walk (k - 1) prefetch while this one runs
     int k = (int)((last - 1 - start) >> 5);
     uint32_t nb_cur = need(k);
@@ -992,30 +975,11 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
                     }
                 }
             } else {
-#if HS_FLUSH_SMEM
-#pragma unroll
-                for (int v = 0; v < 9; ++v)
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(red_wr + v * kRedRow * 4), "f"(gv[v]) : "memory");
-                __syncwarp();
-                if (lane < 18) {
-                    const float4 q0 = lds4(red_rd), q1 = lds4(red_rd + 16), q2 = lds4(red_rd + 32), q3 = lds4(red_rd + 48);
-                    const float2 s2 = add2(add2(add2(f2(q0.x, q0.y), f2(q0.z, q0.w)), add2(f2(q1.x, q1.y), f2(q1.z, q1.w))),
-                                           add2(add2(f2(q2.x, q2.y), f2(q2.z, q2.w)), add2(f2(q3.x, q3.y), f2(q3.z, q3.w))));
-                    float s = s2.x + s2.y;
-                    s += __shfl_xor_sync(0x3FFFFu, s, 1);
-                    if (!(lane & 1)) {
-                        if (a.det) acc_add(a, a.g_splat, (int64_t)gidx * kGS + red_v, s * red_factor, kFxGrad);
-                        else atomicAdd(gp + red_v, s * red_factor);
-                    }
-                }
-                __syncwarp();
-#else
                 const float s = reduce_scatter_value(gv, lane);
                 if (rs_issue) {
                     if (a.det) acc_add(a, a.g_splat, (int64_t)gidx * kGS + rs_vi, s * rs_factor, kFxGrad);
                     else atomicAdd(gp + rs_vi, s * rs_factor);
                 }
-#endif
             }
 #else
             if (HS_RASTER_DIRECT && __popc(cmask) <= HS_RASTER_DIRECT) {
