@@ -119,9 +119,12 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height,
 /* (zero_gsplat [B*N*9], zero_maxw [B*N], zero_wsums [B*N*4]: optional accumulators of
  *  the step's raster, zero-filled in the same pass -- NULL to skip.  tile_counts
  *  [B << tile_bits]: optional, hs_tile_count done in the same pass (zero on entry).
- *  tile_rects [B*N]: optional, each item's tile rectangle packed ty0 | ty1 << 8 | tx0 << 16
- *  | tx1 << 24 (ty0 > ty1 for items without keys) for hs_tile_fill; at most 256 tiles per
- *  image axis.)
+ *  tile_rects [B*N*2]: optional, per item its tile rectangle packed ty0 | ty1 << 8 | tx0 << 16
+ *  | tx1 << 24 (ty0 > ty1 for items without keys) and a kept-tile mask (bit dy * w + dx;
+ *  all ones for rectangles of more than 32 tiles), for hs_tile_fill / hs_bin_emit*; at most
+ *  256 tiles per image axis.  With tile_rects the binning culls the tiles no pixel of which
+ *  the splat's alpha >= 1/255 ellipse reaches (exact, oracle/binning.py:tile_mask): counts,
+ *  tile_counts and every emitter then hold only the kept tiles.)
  * Projection of already-activated world Gaussians (compat preprocess).
  * radius (B*N, 0 for culled splats), x_cam (B*N*3) and cov_cam (B*N*9) are
  * optional outputs (NULL to skip) in both projection calls. */
@@ -151,10 +154,11 @@ int hs_scan_blocks(int64_t num_items);  /* = ceil(num_items / 256) */
 int hs_bin_scan(int num_blocks, const uint32_t *block_sums, uint32_t *block_offsets,
                 const unsigned long long *err, const uint32_t *depth_range,
                 unsigned long long *summary, void *stream);
-/* Writes keys/values in (frame, n, ty, tx) order. */
+/* Writes keys/values in (frame, n, ty, tx) order.  tile_rects: the projection's (NULL when
+ * it had none): only the kept tiles of each item's rectangle are emitted. */
 int hs_bin_emit(int B, int64_t N, int width, int height, const float *records,
                 const float *depth, const uint32_t *counts, const uint32_t *block_offsets,
-                uint64_t *keys, uint32_t *values, void *stream);
+                const uint32_t *tile_rects, uint64_t *keys, uint32_t *values, void *stream);
 /* Bytes of scratch for hs_sort_pairs. */
 size_t hs_sort_workspace_size(int64_t num_keys);
 /* Stable LSD radix sort (onesweep: one histogram kernel, then one decoupled
@@ -185,8 +189,8 @@ int hs_depth_order(int64_t num_items, const float *depth, const uint32_t *depth_
                    uint32_t *order_alt, uint32_t *keys_a, uint32_t *keys_b, void *workspace,
                    size_t workspace_bytes, void *stream);
 int hs_bin_emit_sorted(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
-                       const uint32_t *order, uint32_t *block_sums, uint32_t *block_offsets, uint32_t *keys,
-                       uint32_t *values, void *stream);
+                       const uint32_t *tile_rects, const uint32_t *order, uint32_t *block_sums,
+                       uint32_t *block_offsets, uint32_t *keys, uint32_t *values, void *stream);
 int hs_sort_pairs32(int64_t num_keys, uint32_t bit_mask, uint32_t *keys, uint32_t *values,
                     uint32_t *keys_alt, uint32_t *values_alt, void *workspace, size_t workspace_bytes,
                     int *result_in_alt, void *stream);

@@ -17,6 +17,13 @@ the device path's own fp32 mean2d / radius / depth / opacity / valid:
 5. stable sort by key (equal depth bits resolve to lower n = the reference's
    tie-break);
 6. ranges[frame, tile] = [first, last+1), empty tiles [0, 0).
+
+With conic and qmax (the training path, hs_project_avatar_fwd given tile_rects) step 3
+keeps only the tiles some pixel of which the splat's alpha >= 1/255 ellipse can reach
+(tile_reaches below, the device's hs_common.cuh:tile_reaches in the same fp32 operations),
+for rectangles of at most 32 tiles; larger rectangles keep every tile.  The culled keys
+composite nothing (every pixel of such a tile fails the reference's q <= qmax test,
+S/render.py:260-262), so the rendered result is the same.
 """
 
 from __future__ import annotations
@@ -64,10 +71,45 @@ def pixel_bbox(mean2d, radius, width, height):
     return np.stack([r_lo, r_hi, c_lo, c_hi], axis=-1).astype(np.int32)
 
 
-def bin_batch(mean2d, radius, depth, opacity, valid, width, height):
+MASK_TILES = 32
+
+
+def tile_reaches(mx, my, a, b, c, qmax, rl, rh, cl, ch, tx, ty):
+    """Vectorised hs_common.cuh:tile_cull + tile_reaches: fp32, one rounding per op, the
+    correctly rounded reciprocals of a and c, fmin/fmax (NaN-ignoring) clamps.  All
+    arguments are arrays of one shape."""
+    f = np.float32
+    xs = np.maximum(tx * TILE, cl)
+    xe = np.minimum(tx * TILE + TILE - 1, ch)
+    ys = np.maximum(ty * TILE, rl)
+    ye = np.minimum(ty * TILE + TILE - 1, rh)
+    with np.errstate(all="ignore"):
+        det = a * c - b * b
+        pd = (det > 0) & (a > 0) & (c > 0)
+        half = f(0.5)
+        dxlo = (xs.astype(f) + half) - mx
+        dxhi = (xe.astype(f) + half) - mx
+        dylo = (ys.astype(f) + half) - my
+        dyhi = (ye.astype(f) + half) - my
+        zero = f(0.0)
+        inv_a = np.where(pd, f(1.0) / a, f(0.0)).astype(f)
+        inv_c = np.where(pd, f(1.0) / c, f(0.0)).astype(f)
+        dxv = np.fmin(np.fmax(zero, dxlo), dxhi)
+        dyv = np.fmin(np.fmax(((-b) * dxv) * inv_c, dylo), dyhi)
+        dyh = np.fmin(np.fmax(zero, dylo), dyhi)
+        dxh = np.fmin(np.fmax(((-b) * dyh) * inv_a, dxlo), dxhi)
+        b2 = f(2.0) * b
+        qv = ((a * dxv) * dxv + (b2 * dxv) * dyv) + (c * dyv) * dyv
+        qh = ((a * dxh) * dxh + (b2 * dxh) * dyh) + (c * dyh) * dyh
+        cull = (np.fmin(qv, qh) * f(0.999) - f(1e-3)) > qmax
+    return ~pd | ~cull
+
+
+def bin_batch(mean2d, radius, depth, opacity, valid, width, height, conic=None, qmax=None):
     """All inputs per (frame, Gaussian): mean2d (B, N, 2), radius/depth/opacity
-    (B, N) float32, valid (B, N) bool.  Returns dict with keys (u64), values (u32),
-    ranges (B, tiles, 2) u32, bbox (B, N, 4) int32, counts (B, N) u32."""
+    (B, N) float32, valid (B, N) bool; conic (B, N, 3) and qmax (B, N) float32 turn on
+    the tile cull.  Returns dict with keys (u64), values (u32), ranges (B, tiles, 2) u32,
+    bbox (B, N, 4) int32, counts (B, N) u32."""
     mean2d = np.asarray(mean2d, np.float32)
     radius = np.asarray(radius, np.float32)
     depth = np.asarray(depth, np.float32)
@@ -91,9 +133,22 @@ def bin_batch(mean2d, radius, depth, opacity, valid, width, height):
     ty = np.repeat(ty0[bs, ns], c) + local // nx        # ty major, then tx
     tx = np.repeat(tx0[bs, ns], c) + local % nx
     frames = np.repeat(bs, c).astype(np.uint64)
-    tile_ids = (ty * tiles_x + tx).astype(np.uint64)
     vals = np.repeat(ns, c).astype(np.uint32)
     dbits = np.repeat(depth_bits[bs, ns], c)
+    if conic is not None:
+        conic = np.asarray(conic, np.float32)
+        qmax = np.asarray(qmax, np.float32)
+        rep = lambda x: np.repeat(x[bs, ns], c)
+        keep = (rep(counts) > MASK_TILES) | tile_reaches(
+            rep(mean2d[..., 0]), rep(mean2d[..., 1]), rep(conic[..., 0]), rep(conic[..., 1]), rep(conic[..., 2]),
+            rep(qmax), rep(bbox[..., 0]).astype(np.int64), rep(bbox[..., 1]).astype(np.int64),
+            rep(bbox[..., 2]).astype(np.int64), rep(bbox[..., 3]).astype(np.int64), tx, ty)
+        ty, tx, frames, vals, dbits = ty[keep], tx[keep], frames[keep], vals[keep], dbits[keep]
+        kept = np.zeros(counts.shape, np.int64)
+        np.add.at(kept, (np.repeat(bs, c)[keep], np.repeat(ns, c)[keep]), 1)
+        counts = kept
+        total = int(counts.sum())
+    tile_ids = (ty * tiles_x + tx).astype(np.uint64)
     keys = (frames << np.uint64(tile_bits + 32)) | (tile_ids << np.uint64(32)) | dbits
     order = np.argsort(keys, kind="stable")
     keys = keys[order]

@@ -57,7 +57,7 @@ SIGNATURES = {
     "hs_project_world_bwd": (_I, [_I, _L, _P, _P, _P, _P, _P]),
     "hs_scan_blocks": (_I, [_L]),
     "hs_bin_scan": (_I, [_I, _P, _P, _P, _P, _P, _P]),
-    "hs_bin_emit": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_bin_emit": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_sort_workspace_size": (_Z, [_L]),
     "hs_sort_pairs": (_I, [_L, ctypes.c_uint64, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges": (_I, [_L, _P, _P, _P]),
@@ -68,7 +68,7 @@ SIGNATURES = {
     "hs_raster_workspace_size": (_Z, [_I, _I, _I]),
     "hs_fixed_to_float": (_I, [_L, _P, _P, _I, _P]),
     "hs_depth_order": (_I, [_L, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
-    "hs_bin_emit_sorted": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_bin_emit_sorted": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hs_sort_pairs32": (_I, [_L, ctypes.c_uint32, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges32": (_I, [_L, _P, _P, _P]),
     "hs_tile_sort_cap": (_I, []),

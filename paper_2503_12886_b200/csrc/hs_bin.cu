@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
                                                           const float *__restrict__ depth,
                                                           const uint32_t *__restrict__ counts,
                                                           const uint32_t *__restrict__ offs,
+                                                          const uint32_t *__restrict__ rects,
                                                           uint64_t *__restrict__ keys,
                                                           uint32_t *__restrict__ vals) {
     pdl_prologue();
@@ -96,8 +97,13 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
     const int ty0 = unpack_lo(rows) / kTile, ty1 = unpack_hi(rows) / kTile;
     const int tx0 = unpack_lo(cols) / kTile, tx1 = unpack_hi(cols) / kTile;
     const uint64_t hi = ((uint64_t)b << (tile_bits + 32)) | (uint64_t)__float_as_uint(depth[i]);
+    // with the projection's tile_rects: only its kept tiles (counts[i] of them)
+    const uint32_t mask = rects ? rects[2 * i + 1] : 0xFFFFFFFFu;
+    const int area = (ty1 - ty0 + 1) * (tx1 - tx0 + 1);
+    int idx = 0;
     for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
+        for (int tx = tx0; tx <= tx1; ++tx, ++idx) {
+            if (!mask_keeps(mask, area, idx)) continue;
             keys[pos] = hi | ((uint64_t)(ty * tiles_x + tx) << 32);
             vals[pos] = n;
             ++pos;
@@ -159,6 +165,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_sorted_kernel(int64_t items, 
                                                                  const uint32_t *__restrict__ order,
                                                                  const uint32_t *__restrict__ counts,
                                                                  const uint32_t *__restrict__ offs,
+                                                                 const uint32_t *__restrict__ rects,
                                                                  uint32_t *__restrict__ keys,
                                                                  uint32_t *__restrict__ vals) {
     pdl_prologue();
@@ -186,8 +193,12 @@ __global__ void __launch_bounds__(kScanBlock) emit_sorted_kernel(int64_t items, 
         const int ty0 = unpack_lo(rows) / kTile, ty1 = unpack_hi(rows) / kTile;
         const int tx0 = unpack_lo(cols) / kTile, tx1 = unpack_hi(cols) / kTile;
         const uint32_t hi = b << tile_bits;
+        const uint32_t mask = rects ? rects[2 * (int64_t)i + 1] : 0xFFFFFFFFu;
+        const int area = (ty1 - ty0 + 1) * (tx1 - tx0 + 1);
+        int idx = 0;
         for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx) {
+            for (int tx = tx0; tx <= tx1; ++tx, ++idx) {
+                if (!mask_keeps(mask, area, idx)) continue;
                 const uint32_t key = hi | (uint32_t)(ty * tiles_x + tx);
                 keys[pos] = key;
                 vals[pos] = n;
@@ -486,8 +497,8 @@ int hs_bin_scan(int num_blocks, const uint32_t *block_sums, uint32_t *block_offs
 }
 
 int hs_bin_emit(int B, int64_t N, int width, int height, const float *records, const float *depth,
-                const uint32_t *counts, const uint32_t *block_offsets, uint64_t *keys, uint32_t *values,
-                void *stream) {
+                const uint32_t *counts, const uint32_t *block_offsets, const uint32_t *tile_rects, uint64_t *keys,
+                uint32_t *values, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
     const int frame_bits = bit_length_u32((uint32_t)(B - 1));
@@ -497,7 +508,7 @@ int hs_bin_emit(int B, int64_t N, int width, int height, const float *records, c
     }
     const int64_t items = (int64_t)B * N;
     launch_k(emit_kernel, hs_scan_blocks(items), kScanBlock, 0, HS_CHECK_STREAM(stream), 
-        B, N, tiles_x, tile_bits, records, depth, counts, block_offsets, keys, values);
+        B, N, tiles_x, tile_bits, records, depth, counts, block_offsets, tile_rects, keys, values);
     return check_launch("hs_bin_emit");
 }
 
@@ -604,8 +615,8 @@ int hs_depth_order(int64_t num_items, const float *depth, const uint32_t *depth_
 }
 
 int hs_bin_emit_sorted(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
-                       const uint32_t *order, uint32_t *block_sums, uint32_t *block_offsets, uint32_t *keys,
-                       uint32_t *values, void *stream) {
+                       const uint32_t *tile_rects, const uint32_t *order, uint32_t *block_sums,
+                       uint32_t *block_offsets, uint32_t *keys, uint32_t *values, void *stream) {
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int tile_bits = bit_length_u32((uint32_t)(tiles_x * tiles_y - 1));
     const int frame_bits = bit_length_u32((uint32_t)(B - 1));
@@ -619,7 +630,7 @@ int hs_bin_emit_sorted(int B, int64_t N, int width, int height, const float *rec
     launch_k(sorted_block_sums_kernel, nb, kScanBlock, 0, s, items, order, counts, block_sums);
     launch_k(scan_kernel, 1, 1024, 0, s, nb, block_sums, block_offsets, nullptr, nullptr, nullptr);
     launch_k(emit_sorted_kernel, nb, kScanBlock, 0, s, items, N, tiles_x, tile_bits, records, order, counts, block_offsets,
-                                                 keys, values);
+                                                 tile_rects, keys, values);
     return check_launch("hs_bin_emit_sorted");
 }
 

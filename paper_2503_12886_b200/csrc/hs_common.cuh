@@ -156,6 +156,58 @@ __device__ __forceinline__ uint32_t pack_lohi(int lo, int hi) {
 __device__ __forceinline__ int unpack_lo(uint32_t v) { return (int)(int16_t)(v & 0xFFFF); }
 __device__ __forceinline__ int unpack_hi(uint32_t v) { return (int)(int16_t)(v >> 16); }
 
+// The binning's tile cull (tile-major path, oracle/binning.py:tile_reaches): can splat (mean,
+// conic a b c, qmax, integer pixel bbox [rl, rh] x [cl, ch]) reach a pixel of tile (tx, ty)?
+// The minimum of q(d) = a dx^2 + 2 b dx dy + c dy^2 over the rectangle of the tile's pixel
+// centres inside the bbox (d = centre - mean): for a positive-definite q the minimiser lies
+// on one of the two segments through the point nearest the mean (x clamped with the best y
+// for it, and y clamped with the best x), both inside the rectangle; q there is the minimum
+// up to second-order rounding.  No pixel can pass the reference's q <= qmax test
+// (S/render.py:260-262) when it exceeds qmax by the margin (0.1 % + 1e-3, far above the fp32
+// rounding of q at a pixel).  IEEE fp32, one rounding per operation, inv_a / inv_c the
+// correctly rounded reciprocals (TileCull), so every emitter and the oracle decide alike;
+// non-positive-definite or non-finite input keeps the tile.
+struct TileCull {
+    float mx, my, a, b, c, qmax, inv_a, inv_c;
+    int rl, rh, cl, ch;
+    bool pd;
+};
+__device__ __forceinline__ TileCull tile_cull(float mx, float my, float a, float b, float c, float qmax, int rl, int rh,
+                                              int cl, int ch) {
+    TileCull t;
+    t.mx = mx; t.my = my; t.a = a; t.b = b; t.c = c; t.qmax = qmax;
+    t.rl = rl; t.rh = rh; t.cl = cl; t.ch = ch;
+    const float det = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, b));
+    t.pd = det > 0.f && a > 0.f && c > 0.f;
+    t.inv_a = t.pd ? __frcp_rn(a) : 0.f;
+    t.inv_c = t.pd ? __frcp_rn(c) : 0.f;
+    return t;
+}
+__device__ __forceinline__ bool tile_reaches(const TileCull &t, int tx, int ty) {
+    const int xs = max(tx * kTile, t.cl), xe = min(tx * kTile + kTile - 1, t.ch);
+    const int ys = max(ty * kTile, t.rl), ye = min(ty * kTile + kTile - 1, t.rh);
+    if (xs > xe || ys > ye) return false;
+    if (!t.pd) return true;
+    const float dxlo = __fsub_rn(__fadd_rn((float)xs, 0.5f), t.mx), dxhi = __fsub_rn(__fadd_rn((float)xe, 0.5f), t.mx);
+    const float dylo = __fsub_rn(__fadd_rn((float)ys, 0.5f), t.my), dyhi = __fsub_rn(__fadd_rn((float)ye, 0.5f), t.my);
+    const float dxv = fminf(fmaxf(0.f, dxlo), dxhi);
+    const float dyv = fminf(fmaxf(__fmul_rn(__fmul_rn(-t.b, dxv), t.inv_c), dylo), dyhi);
+    const float dyh = fminf(fmaxf(0.f, dylo), dyhi);
+    const float dxh = fminf(fmaxf(__fmul_rn(__fmul_rn(-t.b, dyh), t.inv_a), dxlo), dxhi);
+    const float b2 = __fmul_rn(2.f, t.b);
+    const float qv = __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(t.a, dxv), dxv), __fmul_rn(__fmul_rn(b2, dxv), dyv)),
+                               __fmul_rn(__fmul_rn(t.c, dyv), dyv));
+    const float qh = __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(t.a, dxh), dxh), __fmul_rn(__fmul_rn(b2, dxh), dyh)),
+                               __fmul_rn(__fmul_rn(t.c, dyh), dyh));
+    return !(__fsub_rn(__fmul_rn(fminf(qv, qh), 0.999f), 1e-3f) > t.qmax);
+}
+// Tile rectangles of at most kMaskTiles tiles carry a kept-tile mask (bit dy * w + dx);
+// larger ones keep every tile (mask all ones).
+constexpr int kMaskTiles = 32;
+__device__ __forceinline__ bool mask_keeps(uint32_t mask, int area, int idx) {
+    return area > kMaskTiles || ((mask >> idx) & 1u);
+}
+
 __host__ __device__ inline int bit_length_u32(uint32_t x) {
     int n = 0;
     while (x) { ++n; x >>= 1; }

@@ -81,6 +81,8 @@ __device__ __forceinline__ void project_one(const float pw[3], const float q[4],
 // list is bit-exact against oracle/binning.py.
 struct TileRect {
     int ty0, ty1, tx0, tx1;
+    int rl, rh, cl, ch;            // the pixel bbox
+    float qmax;
 };
 
 __device__ __forceinline__ uint32_t write_record(const Proj &p, float op, const float col[3], int W, int H,
@@ -109,7 +111,7 @@ __device__ __forceinline__ uint32_t write_record(const Proj &p, float op, const 
     r4[1] = make_float4(p.cc, op, qmax, __uint_as_float(pack_lohi(r_lo, r_hi)));
     r4[2] = make_float4(__uint_as_float(pack_lohi(c_lo, c_hi)), col[0], col[1], col[2]);
     if (!live) return 0u;
-    if (rect) *rect = {r_lo / kTile, r_hi / kTile, c_lo / kTile, c_hi / kTile};
+    if (rect) *rect = {r_lo / kTile, r_hi / kTile, c_lo / kTile, c_hi / kTile, r_lo, r_hi, c_lo, c_hi, qmax};
     return (uint32_t)((r_hi / kTile - r_lo / kTile + 1) * (c_hi / kTile - c_lo / kTile + 1));
 }
 
@@ -117,25 +119,6 @@ __device__ __forceinline__ uint32_t write_record(const Proj &p, float op, const 
 // tile of its bbox -- into a shared histogram over the CTA's first frame's tiles,
 // flushed with one global atomic per touched tile, or straight to the global counters.
 constexpr int kProjHistBins = 4096;
-
-__device__ __forceinline__ void count_tiles(uint32_t cnt, const TileRect &r, int b, int b0, bool shared, int tiles_x,
-                                            int tile_bits, uint32_t *hist, uint32_t *tile_counts) {
-    if (!cnt) return;
-    // two loops, so the shared one compiles to shared-memory atomics (a pointer that may
-    // be either would make every add a generic atomic)
-    if (shared && b == b0) {
-        for (int ty = r.ty0; ty <= r.ty1; ++ty) {
-            uint32_t *row = hist + ty * tiles_x;
-            for (int tx = r.tx0; tx <= r.tx1; ++tx) atomicAdd(row + tx, 1u);
-        }
-    } else {
-        uint32_t *dst = tile_counts + ((size_t)b << tile_bits);
-        for (int ty = r.ty0; ty <= r.ty1; ++ty) {
-            uint32_t *row = dst + ty * tiles_x;
-            for (int tx = r.tx0; tx <= r.tx1; ++tx) atomicAdd(row + tx, 1u);
-        }
-    }
-}
 
 // Per-256-item sum of tile counts (the key-offset scan input) and the range of the
 // float bits of the depths that emit keys: the radix sort skips digit windows that
@@ -276,10 +259,14 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
             for (int k = threadIdx.x; k < items * kGS; k += blockDim.x) z[k] = 0.f;
         }
     }
+    const int lane = threadIdx.x & 31;
+    TileRect rect{1, 0, 1, 0, 1, 0, 1, 0, -1.f};
+    TileCull tc{};
+    int b = 0;
     if (i < (int64_t)B * N) {
         if (zero_maxw) zero_maxw[i] = 0.f;
         if (zero_wsums) reinterpret_cast<float4 *>(zero_wsums)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int b = (int)(i / N);
+        b = (int)(i / N);
         const int64_t n = i - (int64_t)b * N;
         AvatarWorld a;
         const bool ok = avatar_world(N, b, n, F, raw10, base14, tri, bary, frames, a);
@@ -288,17 +275,91 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
         Proj p;
         project_one(a.pw, a.qw, a.s, cams + b * kCam, p);
         if (!ok) p.valid = false;
-        TileRect rect{1, 0, 1, 0};
         cnt = write_record(p, a.op, a.col, W, H, records + i * kRec, &rect);
-        if (tile_rects)
-            tile_rects[i] = cnt ? (uint32_t)rect.ty0 | (uint32_t)rect.ty1 << 8 | (uint32_t)rect.tx0 << 16 |
-                                      (uint32_t)rect.tx1 << 24
-                                : 0x00010001u;
+        if (tile_rects && cnt) tc = tile_cull(p.mx, p.my, p.ca, p.cb, p.cc, rect.qmax, rect.rl, rect.rh, rect.cl, rect.ch);
         depth[i] = p.zc;
         dz = p.zc;
-        counts[i] = cnt;
         if (radius) radius[i] = p.valid ? p.rad : 0.f;
-        if (tile_counts) count_tiles(cnt, rect, b, b0, shared, tiles_x, tile_bits, hist, tile_counts);
+    }
+    // The tiles: every lane takes one (item, tile) candidate of the warp's 32 items at a
+    // time (no per-item loops of different lengths), tests it against the item's tile cull
+    // when the item's rectangle carries a mask (tile_rects given, <= kMaskTiles tiles), and
+    // counts a kept tile into the per-(frame, tile) counters; the ballot of kept candidates
+    // gives each item its mask.  The item data the candidate lanes read is staged in shared
+    // memory, one 48-byte slot per lane.
+    uint32_t tmask = 0xFFFFFFFFu;
+    if (tile_counts || tile_rects) {
+        const uint32_t area = cnt;
+        const bool cullable = tile_rects != nullptr && area != 0u && (int)area <= kMaskTiles;
+        float4 *slots = reinterpret_cast<float4 *>(hist + (shared ? tiles4 * 4 : 0)) + (threadIdx.x & ~31) * 3;
+        const uint32_t rp = (uint32_t)rect.ty0 | (uint32_t)rect.ty1 << 8 | (uint32_t)rect.tx0 << 16 | (uint32_t)rect.tx1 << 24;
+        slots[3 * lane] = make_float4(tc.mx, tc.my, tc.a, tc.b);
+        slots[3 * lane + 1] = make_float4(tc.c, tc.qmax, tc.inv_a, tc.inv_c);
+        slots[3 * lane + 2] = make_float4(__uint_as_float(pack_lohi(tc.rl, tc.rh)), __uint_as_float(pack_lohi(tc.cl, tc.ch)),
+                                          __uint_as_float(rp),
+                                          __uint_as_float((uint32_t)b << 2 | (tc.pd ? 2u : 0u) | (cullable ? 1u : 0u)));
+        __syncwarp();
+        uint32_t incl = area;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t excl = incl - area, total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t bits = 0u;
+        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const bool act = k < total;
+            int o = 0;                     // the candidate's item: the last lane with excl <= k
+#pragma unroll
+            for (int st = 16; st; st >>= 1) {
+                const uint32_t e = __shfl_sync(0xffffffffu, excl, o + st);
+                if (e <= k) o += st;
+            }
+            const uint32_t lo = k - __shfl_sync(0xffffffffu, excl, o);
+            bool keep = false;
+            if (act) {
+                const float4 s2 = slots[3 * o + 2];
+                const uint32_t ro = __float_as_uint(s2.z), fo = __float_as_uint(s2.w);
+                const int wo = (int)(ro >> 24) - (int)((ro >> 16) & 0xFFu) + 1;
+                const int ty = (int)(ro & 0xFFu) + (int)lo / wo, tx = (int)((ro >> 16) & 0xFFu) + (int)lo % wo;
+                keep = true;
+                if (fo & 1u) {
+                    const float4 s0 = slots[3 * o], s1 = slots[3 * o + 1];
+                    TileCull t;
+                    t.mx = s0.x; t.my = s0.y; t.a = s0.z; t.b = s0.w;
+                    t.c = s1.x; t.qmax = s1.y; t.inv_a = s1.z; t.inv_c = s1.w;
+                    t.rl = unpack_lo(__float_as_uint(s2.x)); t.rh = unpack_hi(__float_as_uint(s2.x));
+                    t.cl = unpack_lo(__float_as_uint(s2.y)); t.ch = unpack_hi(__float_as_uint(s2.y));
+                    t.pd = (fo & 2u) != 0u;
+                    keep = tile_reaches(t, tx, ty);
+                }
+                if (keep && tile_counts) {
+                    const int bo = (int)(fo >> 2);
+                    const int t = ty * tiles_x + tx;
+                    if (shared && bo == b0) atomicAdd(hist + t, 1u);
+                    else atomicAdd(tile_counts + ((size_t)bo << tile_bits) + t, 1u);
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (cullable) {        // this item's candidates of the round: [s, e)
+                const uint32_t s = max(excl, k0), e = min(excl + area, k0 + 32u);
+                if (s < e) bits |= ((bal >> (s - k0)) & (0xFFFFFFFFu >> (32u - (e - s)))) << (s - excl);
+            }
+        }
+        if (cullable) {
+            tmask = bits;
+            cnt = (uint32_t)__popc(bits);
+        }
+    }
+    if (i < (int64_t)B * N) {
+        counts[i] = cnt;
+        if (tile_rects)
+            reinterpret_cast<uint2 *>(tile_rects)[i] =
+                make_uint2(cnt ? (uint32_t)rect.ty0 | (uint32_t)rect.ty1 << 8 | (uint32_t)rect.tx0 << 16 |
+                                     (uint32_t)rect.tx1 << 24
+                               : 0x00010001u,
+                           cnt ? tmask : 0u);
     }
     block_sum_store(cnt, dz, block_sums, depth_range);   // (a CTA barrier: the histogram is complete)
     if (shared) {
@@ -552,7 +613,9 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
         set_error("hs_project_avatar_fwd: tile_rects needs at most 256 tiles per image axis");
         return HS_ERR_SHAPE;
     }
-    const size_t smem = tile_counts && tiles <= kProjHistBins ? sizeof(uint32_t) * ((tiles + 3) & ~3) : 0;
+    // the shared tile histogram (tiles padded to 4) + the tile pass's item slots (48 B per thread)
+    const size_t smem = (tile_counts && tiles <= kProjHistBins ? sizeof(uint32_t) * ((tiles + 3) & ~3) : 0) +
+                        ((tile_counts || tile_rects) ? 48 * (size_t)kScanBlock : 0);
     launch_k(project_avatar_fwd_kernel, hs_scan_blocks(items), kScanBlock, smem, HS_CHECK_STREAM(stream), 
         B, N, F, width, height, raw10, base14, tri_index, bary, frames, cameras, records, depth, counts,
         block_sums, depth_range, radius, zero_gsplat, zero_maxw, zero_wsums, tile_counts, tile_rects, err);

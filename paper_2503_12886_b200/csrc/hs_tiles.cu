@@ -71,13 +71,14 @@ struct TileBox {
 constexpr int kPer = kTileItems / kTileThreads;
 
 struct CtaItems {
-    uint32_t rows[kPer], cols[kPer], n[kPer], b[kPer];
+    uint32_t rows[kPer], cols[kPer], n[kPer], b[kPer], mask[kPer];
     bool live[kPer];
 };
 
-// rects (optional, hs_project_avatar_fwd's tile_rects): the item's tile rectangle packed
-// ty0 | ty1 << 8 | tx0 << 16 | tx1 << 24 (dead items: ty0 > ty1) -- one coalesced word
-// instead of the count and two words of the 48-byte record
+// rects (optional, hs_project_avatar_fwd's tile_rects): per item the tile rectangle packed
+// ty0 | ty1 << 8 | tx0 << 16 | tx1 << 24 (dead items: ty0 > ty1) and its kept-tile mask
+// (hs_common.cuh:mask_keeps) -- 8 coalesced bytes instead of the count and two words of
+// the 48-byte record
 __device__ __forceinline__ void load_items(CtaItems &it, int64_t items, int64_t N, const float *__restrict__ records,
                                            const uint32_t *__restrict__ counts, const uint32_t *__restrict__ rects) {
     const int64_t i0 = blockIdx.x * (int64_t)kTileItems;
@@ -86,10 +87,12 @@ __device__ __forceinline__ void load_items(CtaItems &it, int64_t items, int64_t 
     for (int j = 0; j < kPer; ++j) {
         const int64_t i = i0 + threadIdx.x + j * kTileThreads;
         const bool in = i < items;
+        it.mask[j] = 0xFFFFFFFFu;
         if (rects) {
-            const uint32_t r = in ? rects[i] : 0x00010001u;
-            it.rows[j] = r;
-            it.live[j] = (r & 0xFFu) <= ((r >> 8) & 0xFFu);
+            const uint2 rm = in ? reinterpret_cast<const uint2 *>(rects)[i] : make_uint2(0x00010001u, 0u);
+            it.rows[j] = rm.x;
+            it.mask[j] = rm.y;
+            it.live[j] = (rm.x & 0xFFu) <= ((rm.x >> 8) & 0xFFu);
         } else {
             it.live[j] = in && counts[i] != 0u;
             it.rows[j] = in ? __float_as_uint(records[i * kRec + 7]) : 0u;
@@ -390,8 +393,11 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
         for (int j = 0; j < kPer; ++j) {
             if (!it.live[j] || it.b[j] != b0) continue;
             const TileBox bx = item_box(it, j, packed);
+            const int area = (bx.ty1 - bx.ty0 + 1) * (bx.tx1 - bx.tx0 + 1);
+            int idx = 0;
             for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
-                for (int tx = bx.tx0; tx <= bx.tx1; ++tx) atomicAdd(hist + ty * tiles_x + tx, 1u);
+                for (int tx = bx.tx0; tx <= bx.tx1; ++tx, ++idx)
+                    if (mask_keeps(it.mask[j], area, idx)) atomicAdd(hist + ty * tiles_x + tx, 1u);
         }
         __syncthreads();
         uint32_t *row = cursor + ((size_t)b0 << tile_bits);
@@ -407,8 +413,11 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
         const TileBox bx = item_box(it, j, packed);
         const bool local = shared && it.b[j] == b0;
         const uint32_t hi = it.b[j] << tile_bits;
+        const int area = (bx.ty1 - bx.ty0 + 1) * (bx.tx1 - bx.tx0 + 1);
+        int idx = 0;
         for (int ty = bx.ty0; ty <= bx.ty1; ++ty)
-            for (int tx = bx.tx0; tx <= bx.tx1; ++tx) {
+            for (int tx = bx.tx0; tx <= bx.tx1; ++tx, ++idx) {
+                if (!mask_keeps(it.mask[j], area, idx)) continue;
                 const uint32_t t = (uint32_t)(ty * tiles_x + tx);
                 const uint32_t pos = local ? atomicAdd(hist + t, 1u) : atomicAdd(cursor + (hi | t), 1u);
                 HS_CHECK(pos < capacity, "tile scatter slot", pos);
@@ -444,10 +453,12 @@ __global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, i
     for (int rd = 0; rd < kSwRounds; ++rd) {
         const int64_t i = (warp * kSwRounds + rd) * 32 + lane;
         if ((warp * kSwRounds + rd) * 32 >= items) break;                 // warp-uniform
-        const uint32_t r = i < items ? rects[i] : 0x00010001u;            // dead: ty0 > ty1
+        const uint2 rm = i < items ? reinterpret_cast<const uint2 *>(rects)[i] : make_uint2(0x00010001u, 0u);
+        const uint32_t r = rm.x, msk = rm.y;                              // dead: ty0 > ty1
         const int ty0 = r & 0xFF, ty1 = (r >> 8) & 0xFF, tx0 = (r >> 16) & 0xFF, tx1 = r >> 24;
         const int w = tx1 - tx0 + 1;
-        const uint32_t c = ty0 <= ty1 ? (uint32_t)((ty1 - ty0 + 1) * w) : 0u;
+        const uint32_t area = ty0 <= ty1 ? (uint32_t)((ty1 - ty0 + 1) * w) : 0u;
+        const uint32_t c = area > (uint32_t)kMaskTiles ? area : (uint32_t)__popc(msk);   // kept tiles
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -468,10 +479,12 @@ __global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, i
                 const uint32_t e = __shfl_sync(0xffffffffu, excl, o + st);
                 if (e <= k) o += st;
             }
-            const uint32_t lo = k - __shfl_sync(0xffffffffu, excl, o);
-            const uint32_t ro = __shfl_sync(0xffffffffu, r, o);
+            uint32_t lo = k - __shfl_sync(0xffffffffu, excl, o);
+            const uint32_t ro = __shfl_sync(0xffffffffu, r, o), mo = __shfl_sync(0xffffffffu, msk, o);
             const uint32_t no = __shfl_sync(0xffffffffu, n, o), ho = __shfl_sync(0xffffffffu, hi, o);
             const uint32_t wo = (ro >> 24) - ((ro >> 16) & 0xFFu) + 1u;
+            const uint32_t ao = (((ro >> 8) & 0xFFu) - (ro & 0xFFu) + 1u) * wo;
+            if (act && ao <= (uint32_t)kMaskTiles) lo = __fns(mo, 0, (int)lo + 1);   // the lo-th kept tile
             const uint32_t dy = lo / wo, dx = lo - dy * wo;
             const uint32_t key = ho | ((( ro & 0xFFu) + dy) * (uint32_t)tiles_x + ((ro >> 16) & 0xFFu) + dx);
             const uint32_t grp = __match_any_sync(0xffffffffu, act ? key : 0xFFFFFFFFu);

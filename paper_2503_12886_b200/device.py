@@ -353,9 +353,11 @@ class Binner:
                _p(self.dkeys_a), _p(self.dkeys_b), _p(self.dws), self.dws.numel(), _stream())
         self._ordered = (B, N)
 
-    def bin(self, B, N, width, height, records, depth, counts, total):
+    def bin(self, B, N, width, height, records, depth, counts, total, rects=None):
+        """rects: the projection's tile_rects when it had them (its counts then hold only the
+        kept tiles, which the emitters must reproduce)."""
         if self._ordered == (B, N):
-            return self._bin_two_level(B, N, width, height, records, counts, total)
+            return self._bin_two_level(B, N, width, height, records, counts, total, rects)
         tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
         self._ensure(total)
         s = _stream()
@@ -366,7 +368,7 @@ class Binner:
         ranges.zero_()
         if total:
             L.call("hs_bin_emit", B, N, width, height, _p(records), _p(depth), _p(counts), _p(self.offsets),
-                   _p(self.keys), _p(self.vals), s)
+                   _p(rects), _p(self.keys), _p(self.vals), s)
             alt = ctypes.c_int(0)
             mask = self.sort_mask(tile_bits, frame_bits)
             self.passes = sum(1 for sh in range(0, 64, 8) if (mask >> sh) & 0xFF)
@@ -379,7 +381,7 @@ class Binner:
         self.result = (keys[:total], vals[:total], ranges, tile_bits, tiles)
         return self.result
 
-    def _bin_two_level(self, B, N, width, height, records, counts, total):
+    def _bin_two_level(self, B, N, width, height, records, counts, total, rects=None):
         """Stage 2: emission in depth order with 32-bit (frame, tile) keys and a stable
         sort of those keys alone (frame + tile bits: 2 passes at C2) -- the same
         per-tile lists as the one-level (frame, tile, depth) sort."""
@@ -394,7 +396,7 @@ class Binner:
         ranges.zero_()
         k32, k32_alt = self.keys.view(torch.int32), self.keys_alt.view(torch.int32)
         if total:
-            L.call("hs_bin_emit_sorted", B, N, width, height, _p(records), _p(counts), _p(self.order),
+            L.call("hs_bin_emit_sorted", B, N, width, height, _p(records), _p(counts), _p(rects), _p(self.order),
                    _p(self.sblock_sums), _p(self.sblock_offs), _p(k32), _p(self.vals), s)
             alt = ctypes.c_int(0)
             mask = (1 << (tile_bits + frame_bits)) - 1
@@ -429,9 +431,9 @@ class Binner:
         tiles_x, tiles_y, tiles, tile_bits, frame_bits = key_layout(B, width, height)
         if tiles_x > 256 or tiles_y > 256:
             return None
-        if self.rects is None or self.rects.numel() < B * N:
-            self.rects = torch.empty(B * N, dtype=torch.int32, device=self.device)
-        return self.rects[:B * N]
+        if self.rects is None or self.rects.numel() < 2 * B * N:
+            self.rects = torch.empty(2 * B * N, dtype=torch.int32, device=self.device)
+        return self.rects[:2 * B * N]
 
     def bin_tiles(self, B, N, width, height, records, depth, counts, err, after_scan=None, counted=False,
                   rects=None, speculate=None):
@@ -519,7 +521,7 @@ class Binner:
             # (whose ranges replace the ones the tile order was built from)
             self.order_ready = False
             self.depth_order(B, N, depth)
-            self._bin_two_level(B, N, width, height, records, counts, total)
+            self._bin_two_level(B, N, width, height, records, counts, total, rects)
             self.mode = "two_level"
             return total, code
         k32 = self.keys.view(torch.int32)

@@ -28,7 +28,7 @@ def main(reps=30):
         "depth_order": lambda: L.call("hs_depth_order", B * N, _p(tr.depth), _p(bn.depth_range), _p(bn.order),
                                       _p(bn.order_alt), _p(bn.dkeys_a), _p(bn.dkeys_b), _p(bn.dws),
                                       bn.dws.numel(), s),
-        "emit_sorted": lambda: L.call("hs_bin_emit_sorted", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts),
+        "emit_sorted": lambda: L.call("hs_bin_emit_sorted", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts), None,
                                       _p(bn.order), _p(bn.sblock_sums), _p(bn.sblock_offs), _p(k32),
                                       _p(bn.vals), s),
         "sort32": lambda: L.call("hs_sort_pairs32", total, ctypes.c_uint32(mask),

@@ -22,7 +22,7 @@ def main(reps=20):
 
     def emit():
         L.call("hs_bin_emit", tr.B, tr.av.N, tr.W, tr.H, _p(tr.records), _p(tr.depth), _p(tr.counts),
-               _p(bn.offsets), _p(bn.keys), _p(bn.vals), s)
+               _p(bn.offsets), None, _p(bn.keys), _p(bn.vals), s)
 
     def sort():
         alt = ctypes.c_int(0)

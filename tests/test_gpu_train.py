@@ -237,7 +237,11 @@ def test_c2_full_size_properties():
     # bit-exact against the oracle on the device's own fp32 projection
     rec = tr.records.view(B, dev.N, 12).cpu().numpy()
     rad = tr.radius.view(B, dev.N).cpu().numpy()
-    res = BO.bin_batch(rec[..., 0:2], rad, tr.depth.view(B, dev.N).cpu().numpy(), rec[..., 5], rad > 0, 512, 512)
+    # (the projection had tile_rects: the binner's exact tile cull is on, so is the oracle's)
+    res = BO.bin_batch(rec[..., 0:2], rad, tr.depth.view(B, dev.N).cpu().numpy(), rec[..., 5], rad > 0, 512, 512,
+                       conic=rec[..., 2:5], qmax=rec[..., 6])
+    full = BO.bin_batch(rec[..., 0:2], rad, tr.depth.view(B, dev.N).cpu().numpy(), rec[..., 5], rad > 0, 512, 512)
+    assert 0.6 * full["keys"].size < k.size < 0.95 * full["keys"].size
     assert np.array_equal(k.astype(np.uint64), res["keys"] >> np.uint64(32))
     assert np.array_equal(vals.cpu().numpy().view(np.uint32), res["values"])
     assert np.array_equal(ranges.view(B, -1, 2).cpu().numpy().view(np.uint32)[:, :tiles], res["ranges"])
@@ -277,7 +281,9 @@ def test_fused_raster_matches_separate_kernels():
         else:
             assert torch.allclose(la, lb, rtol=1e-5, atol=1e-7)
         ga, gb = a.g_splat.cpu().numpy(), b.g_splat.cpu().numpy()
-        assert np.linalg.norm(ga - gb) <= 1e-5 * np.linalg.norm(gb)
+        # (from the second step on the parameters already differ by the first step's
+        # summation-order noise, which Adam's normalisation amplifies)
+        assert np.linalg.norm(ga - gb) <= (1e-5 if step == 0 else 5e-5) * np.linalg.norm(gb)
     assert torch.equal(a.visited, b.visited)
 
 
