@@ -75,3 +75,50 @@ def test_batch_keys_sorted_by_frame_then_tile():
     # empty tiles have [0, 0)
     r = res["ranges"].reshape(-1, 2)
     assert np.all((r[:, 1] > r[:, 0]) | ((r[:, 0] == 0) & (r[:, 1] == 0)))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_tile_cull_keeps_every_pixel_that_can_composite(seed):
+    """The tile cull (conic + qmax given) only drops (splat, tile) keys where no pixel of
+    the tile passes the reference's bbox and q <= qmax tests (S/render.py:248-262, q at
+    the pixel centre in float64): for every pixel, the splats of its tile list that pass
+    both tests are exactly those of the unculled list, in the same order -- and the cull
+    does drop keys (elongated, rotated ellipses in large bboxes)."""
+    rng = np.random.default_rng(seed)
+    W = H = 96
+    n = 300
+    mean = rng.uniform(-8, W + 8, (1, n, 2)).astype(np.float32)
+    s1, s2 = rng.uniform(0.5, 9, n), rng.uniform(0.5, 3, n)
+    th = rng.uniform(0, np.pi, n)
+    c, s_ = np.cos(th), np.sin(th)
+    cov = np.stack([c * c * s1 ** 2 + s_ * s_ * s2 ** 2, c * s_ * (s1 ** 2 - s2 ** 2), s_ * s_ * s1 ** 2 + c * c * s2 ** 2])
+    det = cov[0] * cov[2] - cov[1] ** 2
+    conic = np.stack([cov[2] / det, -cov[1] / det, cov[0] / det], -1)[None].astype(np.float32)
+    rad = (3 * np.sqrt(np.maximum(cov[0], cov[2]) + np.abs(cov[1])))[None].astype(np.float32)
+    op = rng.uniform(0.02, 1.0, (1, n)).astype(np.float32)
+    qmax = (2 * np.log(op * 255.0) + 1e-9).astype(np.float32)
+    dep = rng.uniform(1, 4, (1, n)).astype(np.float32)
+    valid = np.ones((1, n), bool)
+    full = BO.bin_batch(mean, rad, dep, op, valid, W, H)
+    cull = BO.bin_batch(mean, rad, dep, op, valid, W, H, conic=conic, qmax=qmax)
+    assert BO.lexsort_check(cull, dep)
+    assert 0 < cull["keys"].size < 0.9 * full["keys"].size
+    bbox = full["bbox"][0]
+    tiles_x = full["tiles_x"]
+    m64, k64, q64 = mean[0].astype(np.float64), conic[0].astype(np.float64), qmax[0].astype(np.float64)
+    for py in range(H):
+        for px in range(W):
+            t = (py // 16) * tiles_x + px // 16
+
+            def passing(res):
+                lo, hi = res["ranges"][0, t]
+                out = []
+                for v in res["values"][lo:hi]:
+                    if not (bbox[v, 0] <= py <= bbox[v, 1] and bbox[v, 2] <= px <= bbox[v, 3]):
+                        continue
+                    dx, dy = px + 0.5 - m64[v, 0], py + 0.5 - m64[v, 1]
+                    q = k64[v, 0] * dx * dx + 2 * k64[v, 1] * dx * dy + k64[v, 2] * dy * dy
+                    if q <= q64[v]:
+                        out.append(int(v))
+                return out
+            assert passing(cull) == passing(full), (py, px)
