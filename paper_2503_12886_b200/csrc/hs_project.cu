@@ -233,30 +233,34 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     unsigned long long *err) {
     pdl_prologue();
     extern __shared__ uint32_t hist[];
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // (launched with kScanBlock threads and B * N < 2^31, so the index math is 32-bit and the
+    // loop trip counts are compile-time shifts)
+    const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
     uint32_t cnt = 0;
     float dz = 0.f;
     const int tiles_x = (W + kTile - 1) / kTile, tiles = tiles_x * ((H + kTile - 1) / kTile);
     const int tile_bits = bit_length_u32((uint32_t)(tiles - 1));
-    const int b0 = (int)((blockIdx.x * (int64_t)blockDim.x) / N);
+    const int b0 = (int)((blockIdx.x * (uint32_t)kScanBlock) / (uint32_t)N);
     const bool shared = tile_counts && tiles <= kProjHistBins;
     // (the histogram is padded to a multiple of 4 bins: 16-byte clears and reads)
     const int tiles4 = (tiles + 3) >> 2;
     if (shared) {
-        for (int t = threadIdx.x; t < tiles4; t += blockDim.x) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0u, 0u, 0u, 0u);
+        for (int t = threadIdx.x; t < tiles4; t += kScanBlock) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
     }
     // the step's per-(frame, splat) accumulators, zeroed here instead of by separate
     // fills (the raster adds into them with atomics); g_splat: the CTA's contiguous
     // 256 x kGS floats with coalesced 16-byte stores (a full CTA's span is 9216 bytes)
     if (zero_gsplat) {
-        float *z = zero_gsplat + blockIdx.x * (int64_t)blockDim.x * kGS;
-        const int items = (int)min((int64_t)blockDim.x, (int64_t)B * N - blockIdx.x * (int64_t)blockDim.x);
-        if (items == (int)blockDim.x && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
-            for (int k = threadIdx.x; k < items * kGS / 4; k += blockDim.x)
-                reinterpret_cast<float4 *>(z)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float *z = zero_gsplat + blockIdx.x * (int64_t)kScanBlock * kGS;
+        const int items = (int)min((int64_t)kScanBlock, (int64_t)B * N - blockIdx.x * (int64_t)kScanBlock);
+        if (items == kScanBlock && (reinterpret_cast<uintptr_t>(z) & 15u) == 0) {
+#pragma unroll
+            for (int k = 0; k < kScanBlock * kGS / 4; k += kScanBlock)
+                if (k + (int)threadIdx.x < kScanBlock * kGS / 4)
+                    reinterpret_cast<float4 *>(z)[k + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
         } else {
-            for (int k = threadIdx.x; k < items * kGS; k += blockDim.x) z[k] = 0.f;
+            for (int k = threadIdx.x; k < items * kGS; k += kScanBlock) z[k] = 0.f;
         }
     }
     const int lane = threadIdx.x & 31;
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     if (i < (int64_t)B * N) {
         if (zero_maxw) zero_maxw[i] = 0.f;
         if (zero_wsums) reinterpret_cast<float4 *>(zero_wsums)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        b = (int)(i / N);
+        b = (int)((uint32_t)i / (uint32_t)N);
         const int64_t n = i - (int64_t)b * N;
         AvatarWorld a;
         const bool ok = avatar_world(N, b, n, F, raw10, base14, tri, bary, frames, a);
@@ -322,7 +326,10 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
                 const float4 s2 = slots[3 * o + 2];
                 const uint32_t ro = __float_as_uint(s2.z), fo = __float_as_uint(s2.w);
                 const int wo = (int)(ro >> 24) - (int)((ro >> 16) & 0xFFu) + 1;
-                const int ty = (int)(ro & 0xFFu) + (int)lo / wo, tx = (int)((ro >> 16) & 0xFFu) + (int)lo % wo;
+                // lo / wo without an integer division: (lo + 1/2) / wo is at least 1 / (2 wo)
+                // >= 2^-9 from an integer, far beyond the approximate quotient's error
+                const int qy = (int)__fdividef((float)lo + 0.5f, (float)wo);
+                const int ty = (int)(ro & 0xFFu) + qy, tx = (int)((ro >> 16) & 0xFFu) + (int)lo - qy * wo;
                 keep = true;
                 if (fo & 1u) {
                     const float4 s0 = slots[3 * o], s1 = slots[3 * o + 1];
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
     block_sum_store(cnt, dz, block_sums, depth_range);   // (a CTA barrier: the histogram is complete)
     if (shared) {
         uint32_t *row = tile_counts + ((size_t)b0 << tile_bits);
-        for (int t = threadIdx.x; t < tiles4; t += blockDim.x) {
+        for (int t = threadIdx.x; t < tiles4; t += kScanBlock) {
             const uint4 c = reinterpret_cast<const uint4 *>(hist)[t];
             if (c.x) atomicAdd(row + 4 * t, c.x);
             if (c.y) atomicAdd(row + 4 * t + 1, c.y);
@@ -599,8 +606,9 @@ int hs_project_avatar_fwd(int B, int64_t N, int F, int width, int height, const 
                           uint32_t *block_sums, uint32_t *depth_range, float *radius, float *zero_gsplat,
                           float *zero_maxw, float *zero_wsums, uint32_t *tile_counts, uint32_t *tile_rects,
                           unsigned long long *err, void *stream) {
-    if (B < 1 || N < 1 || width < 1 || height < 1 || width > 32767 || height > 32767) {
-        set_error("hs_project_avatar_fwd: bad sizes B=%d N=%lld %dx%d", B, (long long)N, width, height);
+    if (B < 1 || N < 1 || width < 1 || height < 1 || width > 32767 || height > 32767 ||
+        (int64_t)B * N >= (int64_t(1) << 31)) {
+        set_error("hs_project_avatar_fwd: bad sizes B=%d N=%lld %dx%d (B*N < 2^31)", B, (long long)N, width, height);
         return HS_ERR_SHAPE;
     }
     const int64_t items = (int64_t)B * N;
