@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_kernel(int B, int64_t N, int 
     for (int k = 0; k < w; ++k) wpre += warp_tot[k];
     if (!in || cnt == 0) return;
     uint32_t pos = offs[blockIdx.x] + wpre + incl - cnt;
-    const int b = (int)(i / N);
+    const int b = (int)item_frame(i, N);
     const uint32_t n = (uint32_t)(i - (int64_t)b * N);
     const float *rec = records + i * kRec;
     const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kScanBlock) emit_sorted_kernel(int64_t items, 
     for (int k = 0; k < w; ++k) wpre += warp_tot[k];
     if (in && cnt) {
         uint32_t pos = offs[blockIdx.x] + wpre + incl - cnt;
-        const uint32_t b = (uint32_t)(i / N);
+        const uint32_t b = (uint32_t)item_frame(i, N);
         const uint32_t n = (uint32_t)(i - (int64_t)b * N);
         const float *rec = records + (int64_t)i * kRec;
         const uint32_t rows = __float_as_uint(rec[7]), cols = __float_as_uint(rec[8]);

@@ -208,6 +208,13 @@ __device__ __forceinline__ bool mask_keeps(uint32_t mask, int area, int idx) {
     return area > kMaskTiles || ((mask >> idx) & 1u);
 }
 
+// i / N for a (frame, Gaussian) item index: 32-bit when both fit (always, in practice; a
+// 64-bit division is ~70 instructions)
+__device__ __forceinline__ int64_t item_frame(int64_t i, int64_t N) {
+    if (((uint64_t)i | (uint64_t)N) < (1ull << 32)) return (int64_t)((uint32_t)i / (uint32_t)N);
+    return i / N;
+}
+
 __host__ __device__ inline int bit_length_u32(uint32_t x) {
     int n = 0;
     while (x) { ++n; x >>= 1; }

@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256) project_world_fwd_kernel(
     uint32_t cnt = 0;
     float dz = 0.f;
     if (i < (int64_t)B * N) {
-        const int b = (int)(i / N);
+        const int b = (int)item_frame(i, N);
         const int64_t n = i - (int64_t)b * N;
         const float *w = world14 + (int64_t)b * 14 * N;
         float pw[3], q[4], s[3], col[3];
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(256, HS_PBWD_MINB) project_avatar_bwd_kernel(
     pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
-    const int b = (int)(i / N);
+    const int b = (int)item_frame(i, N);
     const int64_t n = i - (int64_t)b * N;
     float *o = g_raw14 + (int64_t)b * 14 * N;
     // the splat gradients first: their loads overlap the forward recomputation
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(256) project_world_bwd_kernel(int B, int64_t N
     pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
-    const int b = (int)(i / N);
+    const int b = (int)item_frame(i, N);
     const int64_t n = i - (int64_t)b * N;
     const float *w = world14 + (int64_t)b * 14 * N;
     float *o = g_world14 + (int64_t)b * 14 * N;

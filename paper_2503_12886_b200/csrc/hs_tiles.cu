@@ -100,7 +100,7 @@ __device__ __forceinline__ void load_items(CtaItems &it, int64_t items, int64_t 
         }
         int64_t b = b0, n = i - b0 * N;
         if (n >= N) {                            // past the CTA's first frame (rare)
-            b = i / N;
+            b = item_frame(i, N);
             n = i - b * N;
         }
         it.b[j] = (uint32_t)b;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, i
             if (lane >= o) incl += v;
         }
         const uint32_t excl = incl - c, total = __shfl_sync(0xffffffffu, incl, 31);
-        const int64_t b = i / N;
+        const int64_t b = item_frame(i, N);
         const uint32_t n = (uint32_t)(i - b * N), hi = (uint32_t)b << tile_bits;
         for (uint32_t k0 = 0; k0 < total; k0 += 32) {
             const uint32_t k = k0 + lane;
