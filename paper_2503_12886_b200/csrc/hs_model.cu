@@ -269,6 +269,9 @@ __device__ __forceinline__ void blend_fwd_tile(int64_t E, int K, int B, int Bp, 
 #ifndef HS_BLEND_V2
 #define HS_BLEND_V2 1
 #endif
+#ifndef HS_BF_DIAG
+#define HS_BF_DIAG 0                 // diagnostics: 1 loads only, 2 no stores
+#endif
 template <int FB, bool kAllNonzero>
 __device__ __forceinline__ void blend_fwd_tile4(int64_t E, int K, int B, int Bp, const float *s_psi,
                                                 const float *stage, int64_t e0, float *__restrict__ raw) {
@@ -313,7 +316,7 @@ __device__ __forceinline__ void blend_fwd_tile4(int64_t E, int K, int B, int Bp,
         }
 #pragma unroll
         for (int j = 0; j < FB; ++j)
-            if (f0 + j < B)
+            if (f0 + j < B && (HS_BF_DIAG != 2 || acc[j][0].x == 1234.5f))
                 __stcs(reinterpret_cast<float4 *>(raw + (int64_t)(f0 + j) * E + e),
                        make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y));
     }
@@ -367,7 +370,9 @@ __global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, i
         phase ^= 1u << st;
         const float *stage = stages + (size_t)st * (K + 1) * kBfTE;
         const int64_t e0 = t * kBfTE;
-        if (HS_BLEND_V2) {
+        if (HS_BF_DIAG == 1) {
+            if (stage[threadIdx.x] == 1234.5f) raw[threadIdx.x] = 0.f;     // loads only
+        } else if (HS_BLEND_V2) {
             if (Bp <= 4) {
                 if (all_nonzero) blend_fwd_tile4<2, true>(E, K, B, Bp, s_psi2, stage, e0, raw);
                 else blend_fwd_tile4<2, false>(E, K, B, Bp, s_psi2, stage, e0, raw);

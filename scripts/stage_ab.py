@@ -21,25 +21,31 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 flush_on = len(sys.argv) > 3 and sys.argv[3] in ("1", "2")
 flush_read = len(sys.argv) > 3 and sys.argv[3] == "2"     # 2: evict L2 by reading (no dirty lines left)
 tr, d, wl = bench.make_trainer(bench.CONFIGS["C2"])
-for _ in range(int(os.environ.get("RAB_STEPS", "100"))):
+nsteps = int(os.environ.get("RAB_STEPS", "100"))
+for _ in range(nsteps):
     tr.step(d["thetas"], d["targets"], None, d["cameras"], d["backgrounds"])
+if nsteps == 0:               # (diagnostic builds that cannot train: blend inputs only)
+    tr.psi.normal_()
 torch.cuda.synchronize()
 av = tr.av
 N, K, B = av.N, av.K, tr.B
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
 frames = tr._last_frames
-F = frames.shape[-2]
+F = frames.shape[-2] if frames is not None else 0
 
 
 bn = tr.binner
 bn.depth_range_scratch = torch.tensor([0xFFFFFFFF, 0], dtype=torch.int64, device="cuda").to(torch.int32)
-keys_, vals_, ranges_, tile_bits_, tiles_ = bn.result
-nseg = B << tile_bits_
+if bn.result is not None:
+    keys_, vals_, ranges_, tile_bits_, tiles_ = bn.result
+    nseg = B << tile_bits_
 
 
 copy_src = torch.empty(37 << 18, dtype=torch.float32, device="cuda").fill_(1.0)
 copy_dst = torch.empty_like(copy_src)
+read_src = torch.empty(42 << 18, dtype=torch.float32, device="cuda").fill_(1.0)
+read_out = torch.empty((), dtype=torch.float32, device="cuda")
 
 
 def prep():
@@ -63,6 +69,8 @@ def call():
                _p(bn.tile_counts), _p(rects), _p(tr.err), s)
     elif stage == "copy":        # calibration: a 37 MB device copy (74 MB of traffic, blend_fwd's size)
         copy_dst.copy_(copy_src)
+    elif stage == "read":        # calibration: a 42 MB read (blend_fwd's loads)
+        read_out.copy_(read_src.sum())
     elif stage == "blend_fwd":
         L.call("hs_blend_fwd", N, K, B, _p(av.base14), _p(av.deltas), _p(tr.psi), _p(tr.raw10), s)
     elif stage == "blend_bwd":
