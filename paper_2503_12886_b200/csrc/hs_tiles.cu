@@ -434,6 +434,9 @@ __global__ void __launch_bounds__(kTileThreads) tile_scatter_kernel(int64_t item
 // A key finds its item by a binary search over the scan (shuffles), and lanes holding
 // the same (frame, tile) key take consecutive slots behind one global atomic per group
 // (__match_any_sync).  Slot order inside a list is arbitrary; the list sorts fix it.
+#ifndef HS_SCATTER_MATCH
+#define HS_SCATTER_MATCH 1           // lanes with equal (frame, tile) keys share one atomic
+#endif
 #ifndef HS_SCATTER_WARP_ROUNDS
 #define HS_SCATTER_WARP_ROUNDS 1
 #endif
@@ -488,6 +491,7 @@ __global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, i
             // lo / wo without an integer division (hs_project.cu: the tile pass)
             const uint32_t dy = (uint32_t)__fdividef((float)lo + 0.5f, (float)wo), dx = lo - dy * wo;
             const uint32_t key = ho | ((( ro & 0xFFu) + dy) * (uint32_t)tiles_x + ((ro >> 16) & 0xFFu) + dx);
+#if HS_SCATTER_MATCH
             const uint32_t grp = __match_any_sync(0xffffffffu, act ? key : 0xFFFFFFFFu);
             const int leader = __ffs(grp) - 1;
             uint32_t base = 0;
@@ -495,6 +499,10 @@ __global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, i
             base = __shfl_sync(0xffffffffu, base, leader);
             if (act) {
                 const uint32_t pos = base + (uint32_t)__popc(grp & lt_mask);
+#else
+            if (act) {
+                const uint32_t pos = atomicAdd(cursor + key, 1u);
+#endif
                 HS_CHECK(pos < capacity, "tile scatter slot", pos);
                 vals[pos] = no;
                 if (keys) keys[pos] = key;
