@@ -8,8 +8,8 @@ import json
 import subprocess
 import sys
 
-STAGE = [("raster", "raster_train_kernel"), ("raster_bwd", "raster_bwd_kernel"), ("raster_fwd", "raster_fwd_kernel"), ("blend_bwd", "blend_bwd_kernel"),
-         ("blend_fwd", "blend_fwd_kernel"), ("project_fwd", "project_avatar_fwd"),
+STAGE = [("raster", "raster_train_kernel"), ("raster_bwd", "raster_bwd_kernel"), ("raster_fwd", "raster_fwd_kernel"), ("blend_bwd", ("blend_bwd_kernel", "blend_bwd_tma_kernel")),
+         ("blend_fwd", ("blend_fwd_kernel", "blend_fwd_tma_kernel")), ("project_fwd", "project_avatar_fwd"),
          ("project_bwd", "project_avatar_bwd"), ("adam", "adam_kernel"), ("mlp_fwd", "mlp_fwd_kernel"),
          ("rig_frames", "rig_frames_kernel"),
          ("bin_sort", ("emit_kernel", "radix_hist_all", "radix_digit_scan", "radix_onesweep", "tile_ranges")),
@@ -40,6 +40,6 @@ for name, pat in STAGE:
         res[name] = tot
 res["_source"] = ("ncu --set full --clock-control none (dram__bytes_read.sum + dram__bytes_write.sum), one C2 "
                   "bench step; per stage: the sum over its kernels of each kernel's average per launch; "
-                  "profiles/r1_ncu_c2_step.md")
+                  "profiles/r2_ncu_c2_step.md")
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res, indent=1))
