@@ -370,6 +370,9 @@ constexpr int kMaskBatches = 64;
 #ifndef HS_FLUSH_VEC
 #define HS_FLUSH_VEC 1
 #endif
+#ifndef HS_RASTER_SPLIT_SLOW
+#define HS_RASTER_SPLIT_SLOW 1       // adjoint: separate loop bodies with / without the stop test
+#endif
 __device__ __forceinline__ void red4(float *p, float x, float y, float z, float w) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
@@ -907,7 +910,8 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
         __syncwarp();
         // the adjoint of splat j at this lane's two pixels: its 9 gradient partial sums
         // (returns whether a pixel of this lane contributed); advances t_rev / suffix
-        auto splat = [&](int j, float (&gv)[9], uint32_t &gidx) -> bool {
+        auto splat = [&](int j, float (&gv)[9], uint32_t &gidx, auto slow_tag) -> bool {
+            constexpr bool kSlow = decltype(slow_tag)::value;
             const uint32_t jl = c0 - start + (uint32_t)j;
             const Staged t = load_staged(wbase + j * kStageBytes);
             gidx = t.gidx;
@@ -916,7 +920,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             float2 G = f2(ex2_approx(e2.x), ex2_approx(e2.y));
             float2 nal = mul2(t.nop, G);
             bool in0 = (t.mlo & b0) != 0u, in1 = (t.mhi & b1) != 0u;
-            if (slow) {
+            if (kSlow) {
                 in0 = in0 && jl < stop.x;
                 in1 = in1 && jl < stop.y;
             }
@@ -995,22 +999,27 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             }
 #endif
         };
-        while (bits) {
-            const int j = 31 - __clz(bits);
-            bits &= ~(1u << j);
-            float gv[9];
-            uint32_t gidx;
-            const bool contrib = splat(j, gv, gidx);
-            const uint32_t cmask = __ballot_sync(kFull, contrib);
+        // (a batch holding no pixel's stop index runs the loop without the per-splat stop test)
+        auto walk = [&](auto slow_tag) {
+            while (bits) {
+                const int j = 31 - __clz(bits);
+                bits &= ~(1u << j);
+                float gv[9];
+                uint32_t gidx;
+                const bool contrib = splat(j, gv, gidx, slow_tag);
+                const uint32_t cmask = __ballot_sync(kFull, contrib);
 #ifdef HS_RASTER_STATS
-            if (lane == 0) {
-                const int nc = __popc(cmask);
-                const int bin = nc == 0 ? 0 : nc == 1 ? 1 : nc == 2 ? 2 : nc <= 4 ? 3 : nc <= 8 ? 4 : nc <= 16 ? 5 : 6;
-                atomicAdd(&g_raster_stats[8 + bin], 1ull);
-            }
+                if (lane == 0) {
+                    const int nc = __popc(cmask);
+                    const int bin = nc == 0 ? 0 : nc == 1 ? 1 : nc == 2 ? 2 : nc <= 4 ? 3 : nc <= 8 ? 4 : nc <= 16 ? 5 : 6;
+                    atomicAdd(&g_raster_stats[8 + bin], 1ull);
+                }
 #endif
-            if (cmask) flush1(gv, gidx, contrib, cmask);
-        }
+                if (cmask) flush1(gv, gidx, contrib, cmask);
+            }
+        };
+        if (HS_RASTER_SPLIT_SLOW && !slow) walk(std::false_type{});
+        else walk(std::true_type{});
         __syncwarp();
     }
     if (HS_RASTER_PREFETCH) cp_async_wait_all();
