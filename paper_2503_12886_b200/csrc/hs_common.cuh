@@ -201,6 +201,20 @@ __device__ __forceinline__ bool tile_reaches(const TileCull &t, int tx, int ty) 
                                __fmul_rn(__fmul_rn(t.c, dyh), dyh));
     return !(__fsub_rn(__fmul_rn(fminf(qv, qh), 0.999f), 1e-3f) > t.qmax);
 }
+// Position of the n-th (0-based) set bit of m (n < popc(m)): a branch-free popc search
+// (__fns compiles to a loop)
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t m, uint32_t n) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int w = 16; w; w >>= 1) {
+        const uint32_t c = __popc(m & ((1u << w) - 1u));
+        const bool hi = n >= c;
+        n = hi ? n - c : n;
+        m = hi ? m >> w : m;
+        pos = hi ? pos + w : pos;
+    }
+    return pos;
+}
 // Tile rectangles of at most kMaskTiles tiles carry a kept-tile mask (bit dy * w + dx);
 // larger ones keep every tile (mask all ones).
 constexpr int kMaskTiles = 32;
