@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(256) project_avatar_fwd_kernel(
                 if (keep && tile_counts) {
                     const int bo = (int)(fo >> 2);
                     const int t = ty * tiles_x + tx;
+                    HS_CHECK(t >= 0 && t < tiles && bo < B, "projection tile count index", t);
                     if (shared && bo == b0) atomicAdd(hist + t, 1u);
                     else atomicAdd(tile_counts + ((size_t)bo << tile_bits) + t, 1u);
                 }

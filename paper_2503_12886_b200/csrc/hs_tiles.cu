@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(256) tile_scatter_warp_kernel(int64_t items, i
             const uint32_t wo = (ro >> 24) - ((ro >> 16) & 0xFFu) + 1u;
             const uint32_t ao = (((ro >> 8) & 0xFFu) - (ro & 0xFFu) + 1u) * wo;
             if (act && ao <= (uint32_t)kMaskTiles) lo = nth_set_bit(mo, lo);        // the lo-th kept tile
+            HS_CHECK(!act || lo < ao, "tile scatter rectangle index", lo);
             // lo / wo without an integer division (hs_project.cu: the tile pass)
             const uint32_t dy = (uint32_t)__fdividef((float)lo + 0.5f, (float)wo), dx = lo - dy * wo;
             const uint32_t key = ho | ((( ro & 0xFFu) + dy) * (uint32_t)tiles_x + ((ro >> 16) & 0xFFu) + dx);
