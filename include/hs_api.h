@@ -135,10 +135,11 @@ int hs_project_world_fwd(int B, int64_t N, int width, int height, const float *w
                          void *stream);
 /* Adjoint of hs_project_avatar_fwd (render.py:432-497 _preprocess_backward,
  * binding.py:191-204 transform_backward, model.py:237-248 activate_backward):
- * g_splat[B,N,9] -> g_raw14[B,14N] (written). */
+ * g_splat[B,N,9] -> g_raw14[B,14N] (written).  raw_mean != 0: g_splat's mean entries are the
+ * HS_RASTER_RAW_MEAN sums (hs_raster_train's), converted here with the recomputed conic. */
 int hs_project_avatar_bwd(int B, int64_t N, int F, const float *raw10, const float *base14,
                           const int32_t *tri_index, const float *bary, const float *frames,
-                          const float *cameras, const float *g_splat, float *g_raw14,
+                          const float *cameras, const float *g_splat, int raw_mean, float *g_raw14,
                           void *stream);
 /* Adjoint of hs_project_world_fwd: g_splat -> g_world14[B,14N] (written). */
 int hs_project_world_bwd(int B, int64_t N, const float *world14, const float *cameras,
@@ -260,9 +261,12 @@ enum {
     HS_RASTER_WSUMS_IMAGE = 32,  /* weight sums against wsum_image[B,H,W,3] (fp32) instead of the target */
     HS_RASTER_ORDER_READY = 64,  /* hs_raster_train / hs_raster_fwd: the tile order hs_raster_tile_order
                                     built for these ranges is in place (the call skips building it) */
-    HS_RASTER_DETERMINISTIC = 128 /* hs_raster_train / hs_raster_fwd: g_splat and wsums are int64
+    HS_RASTER_DETERMINISTIC = 128, /* hs_raster_train / hs_raster_fwd: g_splat and wsums are int64
                                     fixed-point accumulators (zeroed by the caller, converted with
                                     hs_fixed_to_float): bitwise run-to-run reproducible sums */
+    HS_RASTER_RAW_MEAN = 256     /* hs_raster_bwd: g_splat[0:2] hold the raw sums (-sum dq dx, -sum dq dy)
+                                    (g_mean = [[a b][b c]] times them, a b c the conic) -- what
+                                    hs_raster_train always writes and hs_project_avatar_bwd takes */
 };
 size_t hs_raster_workspace_size(int B, int width, int height);
 /* Optional guard of a raster enqueued before the host has read the step's binning summary
@@ -293,17 +297,19 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
                   void *workspace, void *stream);
 /* Adjoint (render.py:276-336 _backward_kernel).  grad_image (B,H,W,3) may be NULL:
  * then the L1 gradient sign(pred - target) * grad_scale recorded by the forward is used.
- * g_splat must be zero-filled by the caller (accumulated with atomics after a warp reduce). */
+ * g_splat must be zero-filled by the caller (accumulated with atomics after a warp reduce).
+ * flags: 0 (g_splat as documented) or HS_RASTER_RAW_MEAN. */
 int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const float *pix_T, const uint32_t *pix_state,
-                  const float *grad_image, float grad_scale, float *g_splat, void *workspace,
+                  const float *grad_image, float grad_scale, float *g_splat, int flags, void *workspace,
                   void *stream);
 /* Training-step raster: hs_raster_fwd (HS_RASTER_LOSS plus the colour-init flags)
  * and hs_raster_bwd with the L1 gradient sign(pred - target) * grad_scale, fused per
  * pixel block -- T, stop and the gradient stay in registers and the adjoint reuses
  * the forward's per-batch hit masks.  pix_T / pix_state are written only when
- * non-NULL.  g_splat must be zero-filled; loss_partials as hs_raster_fwd. */
+ * non-NULL.  g_splat must be zero-filled; loss_partials as hs_raster_fwd.  g_splat's mean
+ * entries are the HS_RASTER_RAW_MEAN sums (the conic is applied by hs_project_avatar_bwd). */
 int hs_raster_train(int B, int64_t N, int width, int height, int flags, const float *records,
                     const uint32_t *values, const uint32_t *ranges, int tile_bits,
                     const float *backgrounds, const uint8_t *targets, const uint8_t *visited,

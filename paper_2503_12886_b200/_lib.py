@@ -27,6 +27,7 @@ RASTER_WSUMS = 16
 RASTER_WSUMS_IMAGE = 32
 RASTER_ORDER_READY = 64
 RASTER_DETERMINISTIC = 128
+RASTER_RAW_MEAN = 256
 
 _P = ctypes.c_void_p
 
@@ -53,7 +54,7 @@ SIGNATURES = {
     "hs_project_avatar_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                    _P, _P, _P, _P]),
     "hs_project_world_fwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "hs_project_avatar_bwd": (_I, [_I, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "hs_project_avatar_bwd": (_I, [_I, _L, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P]),
     "hs_project_world_bwd": (_I, [_I, _L, _P, _P, _P, _P, _P]),
     "hs_scan_blocks": (_I, [_L]),
     "hs_bin_scan": (_I, [_I, _P, _P, _P, _P, _P, _P]),
@@ -62,7 +63,7 @@ SIGNATURES = {
     "hs_sort_pairs": (_I, [_L, ctypes.c_uint64, _P, _P, _P, _P, _P, _Z, ctypes.POINTER(_I), _P]),
     "hs_tile_ranges": (_I, [_L, _P, _P, _P]),
     "hs_raster_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "hs_raster_bwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _F, _P, _P, _P]),
+    "hs_raster_bwd": (_I, [_I, _L, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _F, _P, _I, _P, _P]),
     "hs_loss_reduce": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "hs_raster_train": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P, _P]),
     "hs_raster_workspace_size": (_Z, [_I, _I, _I]),

@@ -471,7 +471,7 @@ def render_backward(splats: ProjectedSplats, aux: RenderAux, grad_image) -> Gaus
     g[b] = np.asarray(grad_image, np.float64)
     g_splat = torch.zeros(B * n * 9, dtype=torch.float32, device=_dev())
     L.call("hs_raster_bwd", B, n, W, H, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(out["bgs"]),
-           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat),
+           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat), 0,
            _p(dev["raster_ws"]), _stream())
     g14 = torch.empty(B * 14 * n, dtype=torch.float32, device=_dev())
     L.call("hs_project_world_bwd", B, n, _p(dev["world14"]), _p(dev["cams"]), _p(g_splat), _p(g14), _stream())
@@ -487,7 +487,7 @@ def splat_space_grads(aux: RenderAux, grad_image):
     g[b] = np.asarray(grad_image, np.float64)
     g_splat = torch.zeros(B * n * 9, dtype=torch.float32, device=_dev())
     L.call("hs_raster_bwd", B, n, W, H, _p(dev["records"]), _p(vals), _p(ranges), tile_bits, _p(out["bgs"]),
-           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat),
+           _p(out["pix_T"]), _p(out["pix_state"]), _keep(_t(g)), ctypes.c_float(0.0), _p(g_splat), 0,
            _p(dev["raster_ws"]), _stream())
     return g_splat.view(B, n, 9)[b].cpu().numpy().astype(np.float64)
 

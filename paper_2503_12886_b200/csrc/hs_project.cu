@@ -510,7 +510,7 @@ __device__ __forceinline__ void preprocess_bwd_one(const Proj &p, const float q[
 __global__ void __launch_bounds__(256, HS_PBWD_MINB) project_avatar_bwd_kernel(
     int B, int64_t N, int F, const float *__restrict__ raw10, const float *__restrict__ base14,
     const int32_t *__restrict__ tri, const float *__restrict__ bary, const float *__restrict__ frames,
-    const float *__restrict__ cams, const float *__restrict__ g_splat, float *__restrict__ g_raw14) {
+    const float *__restrict__ cams, const float *__restrict__ g_splat, int raw_mean, float *__restrict__ g_raw14) {
     pdl_prologue();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
@@ -528,6 +528,11 @@ __global__ void __launch_bounds__(256, HS_PBWD_MINB) project_avatar_bwd_kernel(
     float g_xt[3] = {0.f, 0.f, 0.f}, g_qraw[4] = {0.f, 0.f, 0.f, 0.f}, g_sr[3] = {0.f, 0.f, 0.f};
     float g_colr[3] = {0.f, 0.f, 0.f}, g_opr = 0.f;
     if (p.valid) {
+        if (raw_mean) {            // HS_RASTER_RAW_MEAN: g_mean = [[a b][b c]] (raw sums)
+            const float sx = gs[0], sy = gs[1];
+            gs[0] = p.ca * sx + p.cb * sy;
+            gs[1] = p.cb * sx + p.cc * sy;
+        }
         float g_pw[3], g_qw[4], g_s[3];
         preprocess_bwd_one(p, a.qw, a.s, cams + b * kCam, gs, g_pw, g_qw, g_s);
         // transform_backward (S/binding.py:191-204)
@@ -648,10 +653,10 @@ int hs_project_world_fwd(int B, int64_t N, int width, int height, const float *w
 
 int hs_project_avatar_bwd(int B, int64_t N, int F, const float *raw10, const float *base14,
                           const int32_t *tri_index, const float *bary, const float *frames, const float *cameras,
-                          const float *g_splat, float *g_raw14, void *stream) {
+                          const float *g_splat, int raw_mean, float *g_raw14, void *stream) {
     const int64_t items = (int64_t)B * N;
     launch_k(project_avatar_bwd_kernel, grid_for(items, 256), 256, 0, HS_CHECK_STREAM(stream), 
-        B, N, F, raw10, base14, tri_index, bary, frames, cameras, g_splat, g_raw14);
+        B, N, F, raw10, base14, tri_index, bary, frames, cameras, g_splat, raw_mean, g_raw14);
     return check_launch("hs_project_avatar_bwd");
 }
 

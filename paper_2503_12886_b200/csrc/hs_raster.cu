@@ -149,8 +149,11 @@ constexpr float kK = -0.72134752044448170f;      // -0.5 * log2(e)
 constexpr float kMeanScale = -2.0f / kK;         // d q / d(k q) folded into g_mean
 // the adjoint's constant factor of gradient value v (g_mean 2, g_conic 3, g_opacity,
 // g_colour 3): the mean and conic partial sums carry -dq = -alpha d_alpha (S/render.py:323-330)
+//   kRaw (the training path, HS_RASTER_RAW_MEAN): g_mean's two sums are the raw -sum dq dx,
+//   -sum dq dy; hs_project_avatar_bwd applies the conic, g_mean = [[a b] [b c]] (..)
+template <bool kRaw = false>
 __device__ __forceinline__ float grad_factor(int v) {
-    return v < 2 ? 0.5f * kMeanScale : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
+    return v < 2 ? (kRaw ? -1.0f : 0.5f * kMeanScale) : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
 }
 // HS_STAGE_DUP=0: each value stored once (64 B per splat); the packed instructions take
 // the scalar as a broadcast operand (the .F32 form of FFMA2 / FMUL2 / FADD2)
@@ -406,7 +409,7 @@ __device__ __forceinline__ void red_splat9(float *gp, uint32_t gidx, const float
     }
 }     // per-warp hit masks kept from the forward for the fused adjoint
 
-template <bool kExplicitGrad>
+template <bool kExplicitGrad, bool kRaw>
 __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, float2 fpx2, float2 fpy2, int x0, int y0,
                                                 uint32_t start, uint32_t last, const float2 (&ng)[3], float2 t_rev,
                                                 float2 nsuf, uint2 stop, int lane, uint32_t wbase,
@@ -661,7 +664,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                                                                           mul2(ng[0], f2(bg[0], bg[0])))));
         const uint32_t last = start + __reduce_max_sync(kFull, max(stop.x, stop.y));
         __syncwarp();
-        raster_bwd_loop<false>(a, b, fpx2, fpy2, x0, y0, start, last, ng, t_rev, nsuf, stop, lane, wbase, masks);
+        raster_bwd_loop<false, true>(a, b, fpx2, fpy2, x0, y0, start, last, ng, t_rev, nsuf, stop, lane, wbase, masks);
     }
 }
 
@@ -779,7 +782,7 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
                    [&](int b, int gw) { raster_fwd_block<kLoss, kImage, CI>(a, b, gw, nblk, lane, wbase); });
 }
 
-template <bool kExplicitGrad>
+template <bool kExplicitGrad, bool kRaw>
 __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int gw, int lane, uint32_t wbase) {
     const int tile = gw / kBlocks, blk = gw % kBlocks;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -825,7 +828,7 @@ __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int
     nsuf = mul2(t_rev, fma2(ng[2], f2(bg[2], bg[2]), fma2(ng[1], f2(bg[1], bg[1]), mul2(ng[0], f2(bg[0], bg[0])))));
     // this warp only needs the list up to its pixels' largest stop index
     const uint32_t last = start + __reduce_max_sync(kFull, max(stop.x, stop.y));
-    raster_bwd_loop<kExplicitGrad>(a, b, f2((float)px, (float)px), f2((float)py0, (float)(py0 + 4)), x0, y0, start,
+    raster_bwd_loop<kExplicitGrad, kRaw>(a, b, f2((float)px, (float)px), f2((float)py0, (float)(py0 + 4)), x0, y0, start,
                                    last, ng, t_rev, nsuf, stop, lane, wbase, nullptr);
 }
 
@@ -834,7 +837,7 @@ __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int
 // a batch is staged only by its hit lanes and skipped when empty; otherwise each batch is
 // staged and culled again.  A batch holding no pixel's stop index takes the fast path
 // (no per-splat stop test).
-template <bool kExplicitGrad>
+template <bool kExplicitGrad, bool kRaw>
 __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, float2 fpx2, float2 fpy2, int x0, int y0,
                                                 uint32_t start, uint32_t last, const float2 (&ng)[3], float2 t_rev,
                                                 float2 nsuf, uint2 stop, int lane, uint32_t wbase,
@@ -858,7 +861,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
         const float z[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         (void)reduce_scatter(z, lane, rs_vi, rs_issue);
     }
-    const float rs_factor = grad_factor(rs_vi);
+    const float rs_factor = grad_factor<kRaw>(rs_vi);
 #endif
     // back to front: the records of the next batch to walk (k - 1) prefetch while this one runs
     int k = (int)((last - 1 - start) >> 5);
@@ -951,10 +954,16 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             gv[2] = d2.x + d2.y;
             gv[3] = d3.x + d3.y;
             gv[4] = d4.x + d4.y;
-            // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
-            const float2 m0 = fma2(t.kb, dqy, mul2(t.ka, dqx)), m1 = fma2(t.kc, dqy, mul2(t.kb, dqx));
-            gv[0] = m0.x + m0.y;
-            gv[1] = m1.x + m1.y;
+            if constexpr (kRaw) {
+                // the raw sums; the conic is applied once per splat by hs_project_avatar_bwd
+                gv[0] = dqx.x + dqx.y;
+                gv[1] = dqy.x + dqy.y;
+            } else {
+                // -2 dq (a dx + b dy) with the k-scaled conic: (-2/k) dq (ka dx + kb dy)
+                const float2 m0 = fma2(t.kb, dqy, mul2(t.ka, dqx)), m1 = fma2(t.kc, dqy, mul2(t.kb, dqx));
+                gv[0] = m0.x + m0.y;
+                gv[1] = m1.x + m1.y;
+            }
             nsuf = fma2(nwg, gw, nsuf);                            // suffix += alpha T gw
             t_rev = tp;
             return ok0 || ok1;
@@ -971,11 +980,11 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
                     if (a.vec) {
                         float f[9];
 #pragma unroll
-                        for (int v = 0; v < 9; ++v) f[v] = gv[v] * grad_factor(v);
+                        for (int v = 0; v < 9; ++v) f[v] = gv[v] * grad_factor<kRaw>(v);
                         red_splat9(gp, gidx, f);
                     } else {
 #pragma unroll
-                        for (int v = 0; v < 9; ++v) acc_add(a, a.g_splat, (int64_t)gidx * kGS + v, gv[v] * grad_factor(v), kFxGrad);
+                        for (int v = 0; v < 9; ++v) acc_add(a, a.g_splat, (int64_t)gidx * kGS + v, gv[v] * grad_factor<kRaw>(v), kFxGrad);
                     }
                 }
             } else {
@@ -989,13 +998,13 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             if (HS_RASTER_DIRECT && __popc(cmask) <= HS_RASTER_DIRECT) {
                 if (contrib) {
 #pragma unroll
-                    for (int v = 0; v < 9; ++v) acc_add(a, a.g_splat, (int64_t)gidx * kGS + v, gv[v] * grad_factor(v), kFxGrad);
+                    for (int v = 0; v < 9; ++v) acc_add(a, a.g_splat, (int64_t)gidx * kGS + v, gv[v] * grad_factor<kRaw>(v), kFxGrad);
                 }
             } else {
                 int vi;
                 bool issue;
                 const float s = reduce_scatter(gv, lane, vi, issue);
-                if (issue) acc_add(a, a.g_splat, (int64_t)gidx * kGS + vi, s * grad_factor(vi), kFxGrad);
+                if (issue) acc_add(a, a.g_splat, (int64_t)gidx * kGS + vi, s * grad_factor<kRaw>(vi), kFxGrad);
             }
 #endif
         };
@@ -1042,14 +1051,14 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(Raste
     });
 }
 
-template <bool kExplicitGrad>
+template <bool kExplicitGrad, bool kRaw>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_bwd_kernel(RasterArgs a, int nblk) {
     pdl_prologue();
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * kWarpSmem;
     for_each_block(a, nblk, lane, warp,
-                   [&](int b, int gw) { raster_bwd_block<kExplicitGrad>(a, b, gw, lane, wbase); });
+                   [&](int b, int gw) { raster_bwd_block<kExplicitGrad, kRaw>(a, b, gw, lane, wbase); });
 }
 
 // partials[b][tiles * kBlocks][2] (one pair per pixel block)
@@ -1217,7 +1226,7 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
 int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records, const uint32_t *values,
                   const uint32_t *ranges, int tile_bits, const float *backgrounds, const float *pix_T,
                   const uint32_t *pix_state, const float *grad_image, float grad_scale, float *g_splat,
-                  void *workspace, void *stream) {
+                  int flags, void *workspace, void *stream) {
     if (int e = check_ws("hs_raster_bwd", workspace)) return e;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     RasterArgs a = make_args(B, N, width, height, records, values, ranges, tile_bits, backgrounds, workspace);
@@ -1231,8 +1240,14 @@ int hs_raster_bwd(int B, int64_t N, int width, int height, const float *records,
     const dim3 grid = raster_grid(nblk, B);
     cudaStream_t s = HS_CHECK_STREAM(stream);
     launch_tile_order(B, nblk, tile_bits, ranges, workspace, s);
-    if (grad_image) launch_k(raster_bwd_kernel<true>, grid, kRT, 0, s, a, nblk);
-    else launch_k(raster_bwd_kernel<false>, grid, kRT, 0, s, a, nblk);
+    const bool raw = (flags & HS_RASTER_RAW_MEAN) != 0;
+    if (grad_image) {
+        if (raw) launch_k(raster_bwd_kernel<true, true>, grid, kRT, 0, s, a, nblk);
+        else launch_k(raster_bwd_kernel<true, false>, grid, kRT, 0, s, a, nblk);
+    } else {
+        if (raw) launch_k(raster_bwd_kernel<false, true>, grid, kRT, 0, s, a, nblk);
+        else launch_k(raster_bwd_kernel<false, false>, grid, kRT, 0, s, a, nblk);
+    }
     return check_launch("hs_raster_bwd");
 }
 

@@ -901,9 +901,11 @@ class Trainer:
                 self.debug_before_backward(self)
             self._call("raster_bwd", "hs_raster_bwd", B, N, self.W, self.H, _p(self.records), _p(vals),
                        _p(ranges), tile_bits, _p(backgrounds), _p(self.pix_T), _p(self.pix_state), None,
-                       ctypes.c_float(grad_scale), _p(self.g_splat), _p(self.raster_ws), s)
+                       ctypes.c_float(grad_scale), _p(self.g_splat), L.RASTER_RAW_MEAN, _p(self.raster_ws), s)
+        # (both rasters leave g_splat's mean entries as the raw sums: the projection adjoint
+        # applies the conic)
         self._call("project_bwd", "hs_project_avatar_bwd", B, N, F, _p(self.raw10), _p(av.base14), _p(av.tri_index),
-                   _p(av.barycentric), _p(frames), _p(cameras), _p(self.g_splat), _p(self.g_raw14), s)
+                   _p(av.barycentric), _p(frames), _p(cameras), _p(self.g_splat), 1, _p(self.g_raw14), s)
         nparts = ctypes.c_int(0)
         self._call("blend_bwd", "hs_blend_bwd", N, K, B, _p(av.deltas), _p(self.psi), _p(self.g_raw14),
                    _p(self.grads), _p(self.grads[14 * N:]), _p(self.gpsi_partials), ctypes.byref(nparts), s,

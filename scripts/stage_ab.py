@@ -79,7 +79,7 @@ def call():
                _p(tr.grads[14 * N:]), _p(tr.gpsi_partials), ctypes.byref(n), s)
     elif stage == "project_bwd":
         L.call("hs_project_avatar_bwd", B, N, F, _p(tr.raw10), _p(av.base14), _p(av.tri_index), _p(av.barycentric),
-               _p(frames), _p(d["cameras"]), _p(tr.g_splat), _p(tr.g_raw14), s)
+               _p(frames), _p(d["cameras"]), _p(tr.g_splat), 1, _p(tr.g_raw14), s)
     elif stage == "adam":
         tr._adam(0, 14 * N + 10 * K * N, 0, s)
     else:
