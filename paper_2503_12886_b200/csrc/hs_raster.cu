@@ -184,17 +184,19 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// 1 - alpha for the transmittance update is floored at 2^-24 (the spacing of fp32 below
-// 1).  The floor only changes alpha == 1.0f exactly: fp32 rounds sigmoid(logit) to 1 above
-// logit ~16.6 and the Gaussian to 1 at a pixel within ~1e-3 px of the mean, where the
-// reference's float64 alpha is still < 1 (its opacity saturates only near logit 36.7).
-// Unfloored, T would become exactly 0 and the adjoint's t_rev / (1 - alpha) would be
-// 0 * inf = NaN (S/render.py:318-319).  Forward and adjoint use the same floor, so
-// t_rev * rcp(floored 1 - alpha) still recovers the transmittance before the splat.
+// Saturation guard: 1 - alpha must stay >= 2^-24 (the spacing of fp32 below 1).  fp32
+// rounds sigmoid(logit) to 1.0f above logit ~16.6 and the Gaussian to 1 at a pixel within
+// ~1e-3 px of the mean, where the reference's float64 alpha is still < 1 (its opacity
+// saturates only near logit 36.7); alpha == 1.0f would make T exactly 0 and the adjoint's
+// t_rev / (1 - alpha) 0 * inf = NaN (S/render.py:318-319).  The staging clamps the opacity
+// at 1 - 2^-24 (the largest float below 1, nearer the reference's value than 1.0f), so
+// alpha = op G <= 1 - 2^-24 and 1 - alpha >= 2^-24 exactly (Sterbenz) at every pixel: no
+// per-pixel floor in either pass.  HS_ONE_MINUS_FLOOR=0: the unguarded A/B build.
 #ifndef HS_ONE_MINUS_FLOOR
 #define HS_ONE_MINUS_FLOOR 5.9604644775390625e-8f               // 2^-24 (0: the unguarded A/B build)
 #endif
 constexpr float kOneMinusFloor = HS_ONE_MINUS_FLOOR;
+constexpr float kOpacityMax = 1.0f - kOneMinusFloor;
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
@@ -309,6 +311,7 @@ __device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, in
     const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
     const int rl = unpack_lo(rows), rh = unpack_hi(rows), cl = unpack_lo(cols), ch = unpack_hi(cols);
     const float a = A.z, b = A.w, c = Bv.x, qmax = Bv.z;
+    const float opv = kOneMinusFloor > 0.f ? fminf(Bv.y, kOpacityMax) : Bv.y;   // (the saturation guard)
     const float nmx = 0.5f - A.x, nmy = 0.5f - A.y, ka = kK * a, kb2 = 2.0f * kK * b, kb = kK * b, kc = kK * c;
     // the block's pixels inside the reference's bbox
     const int cs = max(cl - x0, 0), ce = min(ch - x0, 7), rs = max(rl - y0, 0), re = min(rh - y0, 7);
@@ -348,13 +351,13 @@ __device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, in
 #if HS_STAGE_DUP
     sts4(saddr, nmx, nmx, nmy, nmy);
     sts4(saddr + 16, ka, ka, kb2, kb2);
-    sts4(saddr + 32, kc, kc, -Bv.y, -Bv.y);
+    sts4(saddr + 32, kc, kc, -opv, -opv);
     sts4(saddr + 48, -Cv.y, -Cv.y, -Cv.z, -Cv.z);
     sts4(saddr + 64, -Cv.w, -Cv.w, kK * qmax, __uint_as_float(gflag));
     sts4(saddr + 80, __uint_as_float((uint32_t)mask), __uint_as_float((uint32_t)(mask >> 32)), kb, kb);
 #else
     sts4(saddr, nmx, nmy, ka, kb2);
-    sts4(saddr + 16, kc, -Bv.y, -Cv.y, -Cv.z);
+    sts4(saddr + 16, kc, -opv, -Cv.y, -Cv.z);
     sts4(saddr + 32, -Cv.w, kK * qmax, __uint_as_float(gflag), kb);
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr + 48), "r"((uint32_t)mask), "r"((uint32_t)(mask >> 32))
                  : "memory");
@@ -549,8 +552,6 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             C[1] = fma2(nw, t.ncg, C[1]);
             C[2] = fma2(nw, t.ncb, C[2]);
             float2 om = add2(one2, nal);                       // 1 - alpha
-            om.x = fmaxf(om.x, kOneMinusFloor);
-            om.y = fmaxf(om.y, kOneMinusFloor);
             T = mul2(T, om);
             if (kCI && ((wantb >> j) & 1u)) {
                 const float wmax = -fminf(nw.x, nw.y);
@@ -935,8 +936,6 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
             G.y = ok1 ? G.y : 0.f;
             nal = mul2(t.nop, G);                                  // -alpha
             float2 om = add2(one2, nal);
-            om.x = fmaxf(om.x, kOneMinusFloor);
-            om.y = fmaxf(om.y, kOneMinusFloor);
             const float2 inv = f2(rcp_approx(om.x), rcp_approx(om.y));
             const float2 tp = mul2(t_rev, inv);                    // T before the splat
             const float2 gw = fma2(ng[2], t.ncb, fma2(ng[1], t.ncg, mul2(ng[0], t.ncr)));   // <g, colour>

@@ -3,9 +3,10 @@
 
 The reference evaluates alpha in float64, where sigmoid(logit) < 1 until logit ~36.7;
 fp32 rounds the opacity to 1.0 above logit ~16.6, and the Gaussian factor to 1.0 at a
-pixel centre within ~1e-3 px of the mean, so alpha == 1.0f exactly.  The raster floors
-1 - alpha at 2^-24 in the transmittance update and in the adjoint's T recovery
-(hs_raster.cu:one_minus_alpha) instead of producing T = 0 and 0 * inf = NaN.
+pixel centre within ~1e-3 px of the mean, so alpha == 1.0f exactly.  The raster clamps the
+opacity at 1 - 2^-24 when it stages a splat, so 1 - alpha >= 2^-24 in the transmittance
+update and in the adjoint's T recovery (hs_raster.cu: kOpacityMax), instead of producing
+T = 0 and 0 * inf = NaN.
 
 Scenes: 32x32, stacks of three Gaussians (depths 2, 2.5, 3) whose means project 1.6e-5
 px from a pixel centre, opacity logit 15 / 17 / 20 / 30 / 40, over a layer of random
