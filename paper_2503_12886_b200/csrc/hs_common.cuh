@@ -31,6 +31,15 @@ namespace hs {
 constexpr float kNearPlane = 0.01f;
 constexpr float kMinRadius = 0.3f;
 constexpr float kAlphaCutoff = 1.0f / 255.0f;
+// x / 255 correctly rounded for a byte value x (0..255), without the IEEE division's
+// instruction sequence: the product with the rounded reciprocal, then one FMA residual
+// correction -- identical to (float)x / 255.0f for all 256 inputs (checked exhaustively
+// against exact rationals, tests/test_abi.py::test_u8_unit_is_exact).
+__device__ __forceinline__ float u8_unit(uint32_t x) {
+    const float xf = (float)x, r = 1.0f / 255.0f;
+    const float q = xf * r;
+    return __fmaf_rn(__fmaf_rn(-q, 255.0f, xf), r, q);
+}
 constexpr float kTermEps = 1e-14f;
 constexpr int kTile = 16;
 constexpr int kRec = 12;            // floats per splat record

@@ -450,8 +450,8 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                 for (int c = 0; c < 3; ++c) src[p][c] = a.wsum_image[pix * 3 + c];
             } else if (inside && a.targets) {
                 const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
-                const float al = (float)t.w / 255.0f;
-                const float rgb[3] = {(float)t.x / 255.0f, (float)t.y / 255.0f, (float)t.z / 255.0f};
+                const float al = u8_unit(t.w);
+                const float rgb[3] = {u8_unit(t.x), u8_unit(t.y), u8_unit(t.z)};
 #pragma unroll
                 for (int c = 0; c < 3; ++c) src[p][c] = rgb[c] * al + (1.0f - al) * bg[c];
             }
@@ -615,8 +615,8 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             uint32_t signs = 0;
             if (kLoss) {
                 const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
-                const float al = (float)t.w / 255.0f;
-                const float rgb[3] = {(float)t.x / 255.0f, (float)t.y / 255.0f, (float)t.z / 255.0f};
+                const float al = u8_unit(t.w);
+                const float rgb[3] = {u8_unit(t.x), u8_unit(t.y), u8_unit(t.z)};
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     const float tgt = rgb[c] * al + (1.0f - al) * bg[c];

@@ -47,3 +47,22 @@ def test_status_mapping():
         L.check(L.HS_ERR_SHAPE)
     with pytest.raises(RuntimeError):
         L.check(L.HS_ERR_COLOR_INIT)
+
+
+def test_u8_unit_is_exact():
+    """hs_common.cuh:u8_unit (x * r, then the FMA residual correction) is the correctly
+    rounded float32 x / 255 for every byte value: checked with exact rationals."""
+    from fractions import Fraction as Fr
+    import numpy as np
+
+    def r32(x):
+        c = np.float32(float(x))
+        cands = [np.nextafter(c, np.float32(-np.inf)), c, np.nextafter(c, np.float32(np.inf))]
+        return min(cands, key=lambda v: (abs(Fr(float(v)) - x), int(np.float32(v).view(np.uint32)) & 1))
+
+    r = np.float32(1.0) / np.float32(255.0)
+    for x in range(256):
+        q = r32(Fr(x) * Fr(float(r)))
+        res = r32(-Fr(float(q)) * 255 + x)
+        got = r32(Fr(float(res)) * Fr(float(r)) + Fr(float(q)))
+        assert got == np.float32(x) / np.float32(255.0), x
