@@ -70,6 +70,7 @@ struct RasterArgs {
     int B;
     int64_t N;
     int W, H, tiles_x, tile_bits;
+    float inv_tiles_x;
     const float *records;
     const uint32_t *vals;
     const uint32_t *ranges;
@@ -423,7 +424,9 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                                                  uint32_t wbase, uint32_t *masks = nullptr) {
     // gw = tile * kBlocks + blk: the pixel block of frame b this warp composites
     const int tile = gw / kBlocks, blk = gw % kBlocks;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    // tile / tiles_x without an integer division: (tile + 1/2) / tiles_x is >= 1 / (2 tiles_x)
+    // from an integer, far above the product's rounding (tile < 2^16)
+    const int ty = (int)(((float)tile + 0.5f) * a.inv_tiles_x), tx = tile - ty * a.tiles_x;
     const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 8;
     const int px = x0 + (lane & 7), py0 = y0 + (lane >> 3);      // pixel p: (px, py0 + 4 p)
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
@@ -718,7 +721,9 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(int total_tiles, int t
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < total_tiles; t += blockDim.x) order[atomicAdd(&cursor[bucket(t)], 1u)] = t;
+    // (the entries are b << tile_bits | tile: the raster splits them with a shift)
+    for (int t = threadIdx.x; t < total_tiles; t += blockDim.x)
+        order[atomicAdd(&cursor[bucket(t)], 1u)] = ((uint32_t)(t / tiles) << tile_bits) | (uint32_t)(t % tiles);
 }
 
 template <typename F>
@@ -742,7 +747,7 @@ __device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, in
         if (item >= total) break;
         if (HS_RASTER_LPT) {
             const uint32_t bt = a.tile_order[item / kBlocks];
-            fn((int)(bt / tiles), (int)(bt % tiles) * kBlocks + item % kBlocks);
+            fn((int)(bt >> a.tile_bits), (int)(bt & ((1u << a.tile_bits) - 1u)) * kBlocks + item % kBlocks);
         } else {
             fn(item / nblk, item % nblk);
         }
@@ -786,7 +791,9 @@ __global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_fwd_kernel(RasterA
 template <bool kExplicitGrad, bool kRaw>
 __device__ __forceinline__ void raster_bwd_block(const RasterArgs &a, int b, int gw, int lane, uint32_t wbase) {
     const int tile = gw / kBlocks, blk = gw % kBlocks;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    // tile / tiles_x without an integer division: (tile + 1/2) / tiles_x is >= 1 / (2 tiles_x)
+    // from an integer, far above the product's rounding (tile < 2^16)
+    const int ty = (int)(((float)tile + 0.5f) * a.inv_tiles_x), tx = tile - ty * a.tiles_x;
     const int x0 = tx * kTile + (blk & 1) * 8, y0 = ty * kTile + (blk >> 1) * 8;
     const int px = x0 + (lane & 7), py0 = y0 + (lane >> 3);
     const uint2 rg = reinterpret_cast<const uint2 *>(a.ranges)[((int64_t)b << a.tile_bits) + tile];
@@ -1107,6 +1114,7 @@ static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records
     a.W = W;
     a.H = H;
     a.tiles_x = (W + kTile - 1) / kTile;
+    a.inv_tiles_x = 1.0f / (float)a.tiles_x;
     a.tile_bits = tile_bits;
     a.records = records;
     a.vals = values;
