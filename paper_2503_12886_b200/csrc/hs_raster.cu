@@ -23,7 +23,8 @@
 //
 // The adjoint (S/render.py:276-336) walks the same lists back to front per pixel
 // with the suffix recurrence; each lane first adds its two pixels' contributions,
-// then the 9 per-splat gradients are reduce-scattered across the warp (12 shuffles)
+// then the 9 per-splat gradients go out as vector REDs from each contributing lane (at
+// most HS_RASTER_DIRECT of them) or are reduce-scattered across the warp (12 shuffles)
 // before one RED per value.
 #include <algorithm>
 #include <type_traits>
@@ -131,21 +132,22 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-// ---- staged splat layout (shared memory, 96 B per splat) -------------------
-//   q0: nmx nmx nmy nmy        nm = 0.5 - mean: dx = px + nmx = px + 0.5 - mx
-//   q1: ka  ka  kb2 kb2        k = -0.5 log2(e): e2 = k q = dx (ka dx + kb2 dy) + kc dy^2,
-//   q2: kc  kc  nop nop          alpha = op 2^e2; nop = -op
-//   q3: ncr ncr ncg ncg        nc = -colour
-//   q4: ncb ncb kqmax gidx     q <= qmax <=> e2 >= k qmax; gidx = frame * N + n | visited << 31
-//   q5: mlo mhi kb  kb         64-bit pixel mask of the warp's 8 x 8 block (bit 32 p + lane:
+// ---- staged splat layout (shared memory, 64 B per splat; HS_STAGE_DUP: 96 B) ------
+//   q0: nmx nmy ka  kb2        nm = 0.5 - mean: dx = px + nmx = px + 0.5 - mx;
+//                              k = -0.5 log2(e): e2 = k q = dx (ka dx + kb2 dy) + kc dy^2
+//   q1: kc  nop ncr ncg        alpha = op 2^e2; nop = -op (clamped, kOpacityMax); nc = -colour
+//   q2: ncb kqmax gidx kb      q <= qmax <=> e2 >= k qmax; gidx = frame * N + n;
+//                              kb = kb2 / 2 (the non-raw adjoint's conic term)
+//   q3: mlo mhi                64-bit pixel mask of the warp's 8 x 8 block (bit 32 p + lane:
 //                              pixel p of the lane) = the reference's integer bbox
 //                              (S/render.py:248-251) minus row groups the alpha >= 1/255
-//                              ellipse cannot reach; kb = kb2 / 2 for the adjoint
-// Each value a lane needs for both of its pixels is stored twice, so one LDS.128 yields
-// register pairs for the packed instructions.  Negated opacity / colour make
-// 1 - alpha an FADD2 and the weighted colour an FFMA2 with no extra negation.
-// Forward and adjoint evaluate e2 / alpha with the same explicitly rounded operations
-// (per element identical to __fmaf_rn / __fmul_rn), so both make identical decisions.
+//                              ellipse cannot reach
+// The packed instructions take each per-splat scalar as a broadcast operand (the .F32
+// form of FFMA2 / FMUL2 / FADD2), so one value serves both pixels of a lane.  Negated
+// opacity / colour make 1 - alpha an FADD2 and the weighted colour an FFMA2 with no extra
+// negation.  Forward and adjoint evaluate e2 / alpha with the same explicitly rounded
+// operations (per element identical to __fmaf_rn / __fmul_rn), so both make identical
+// decisions.
 constexpr float kK = -0.72134752044448170f;      // -0.5 * log2(e)
 constexpr float kMeanScale = -2.0f / kK;         // d q / d(k q) folded into g_mean
 // the adjoint's constant factor of gradient value v (g_mean 2, g_conic 3, g_opacity,
@@ -173,7 +175,7 @@ __device__ __forceinline__ void sts4(uint32_t addr, float a, float b, float c, f
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
-// 1/x for x in [2^-24, 1] (x = 1 - alpha floored): the MUFU reciprocal without the
+// 1/x for x in [2^-24, 1] (x = 1 - alpha, >= 2^-24 by the opacity clamp): the MUFU reciprocal without the
 // denormal-range fix-up __fdividef adds (same result for normal x)
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
