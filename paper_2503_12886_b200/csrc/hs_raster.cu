@@ -40,6 +40,14 @@ namespace hs {
 #define HS_RASTER_MINB (28 / HS_RASTER_CTA_WARPS)   // resident CTAs per SM (28 one-warp CTAs: <= 72 registers)
 #endif
 
+// The training raster with the colour-init sums (CI >= 2) fits 64 registers without spills:
+// 32 resident one-warp CTAs per SM (-2 % against 28 at 72 registers); the CI 0 / 1 variants
+// would spill there and keep HS_RASTER_MINB.
+#ifndef HS_RASTER_MINB_CI
+#define HS_RASTER_MINB_CI 32
+#endif
+constexpr int train_minb(int ci) { return ci >= 2 ? HS_RASTER_MINB_CI : HS_RASTER_MINB; }
+
 #ifndef HS_RASTER_EXACT_CULL
 #define HS_RASTER_EXACT_CULL 1       // cull row groups with the exact ellipse-rectangle distance
 #endif
@@ -1047,7 +1055,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
 // one pass -- no per-pixel state round trip through HBM, and the adjoint reuses the
 // forward's per-batch hit masks.
 template <int CI>
-__global__ void __launch_bounds__(kRT, HS_RASTER_MINB) raster_train_kernel(RasterArgs a, int nblk) {
+__global__ void __launch_bounds__(kRT, train_minb(CI)) raster_train_kernel(RasterArgs a, int nblk) {
     pdl_prologue();
     if (guard_blocks(a)) return;
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
@@ -1152,9 +1160,9 @@ static void launch_tile_order(int B, int nblk, int tile_bits, const uint32_t *ra
 
 // grid of the raster kernels: one CTA per kCW blocks, or a persistent grid of
 // resident CTAs (HS_RASTER_PERSIST) sized by the current device's SM count
-static dim3 raster_grid(int nblk, int B) {
+static dim3 raster_grid(int nblk, int B, int minb = HS_RASTER_MINB) {
     if (!HS_RASTER_PERSIST) return dim3(nblk / kCW, B);
-    const int64_t want = (int64_t)current_sm_count() * HS_RASTER_MINB, items = (int64_t)nblk * B / kCW;
+    const int64_t want = (int64_t)current_sm_count() * minb, items = (int64_t)nblk * B / kCW;
     return dim3((unsigned)std::max<int64_t>(1, std::min(want, items)), 1);
 }
 
@@ -1290,7 +1298,7 @@ int hs_raster_train(int B, int64_t N, int width, int height, int flags, const fl
     a.pix_T = pix_T;
     a.pix_state = pix_state;
     const int nblk = tiles_x * tiles_y * kBlocks;
-    const dim3 grid = raster_grid(nblk, B);
+    const dim3 grid = raster_grid(nblk, B, train_minb(ci));
     cudaStream_t s = HS_CHECK_STREAM(stream);
     if (!(flags & HS_RASTER_ORDER_READY)) launch_tile_order(B, nblk, tile_bits, ranges, workspace, s);
     switch (ci) {
