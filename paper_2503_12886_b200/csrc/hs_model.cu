@@ -663,7 +663,10 @@ __host__ inline size_t blend_bwd_tma_smem() {
     return 64 + sizeof(float) * ((size_t)kBbS * kBbStage + kBbK * 16 + 16 * 16 * 20);
 }
 
-__global__ void __launch_bounds__(256, 2) blend_bwd_tma_kernel(int64_t N, int K, int Bc, int b0,
+#ifndef HS_BB_MINB
+#define HS_BB_MINB 2
+#endif
+__global__ void __launch_bounds__(256, HS_BB_MINB) blend_bwd_tma_kernel(int64_t N, int K, int Bc, int b0,
                                                                const float *__restrict__ deltas,
                                                                const float *__restrict__ psi,
                                                                const float *__restrict__ g_raw,
