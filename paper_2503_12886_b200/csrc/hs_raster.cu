@@ -450,26 +450,32 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     // per pixel pair: transmittance, colour (C[c] = channel c of both pixels), stop index
     float2 T = f2(1.f, 1.f), C[3] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
     uint2 stop = make_uint2(0u, 0u);
+    // the colour-init source colours of the two pixels (target over bg, or wsum_image): loaded
+    // on the first batch that has colour-init work -- most blocks have none once the
+    // Gaussians in view are visited
     float src[CI >= 2 ? kPX : 1][3];
-    if constexpr (CI >= 2) {
+    bool src_ready = false;
+    auto load_src = [&]() {
+        if constexpr (CI >= 2) {
 #pragma unroll
-        for (int p = 0; p < kPX; ++p) {
-            const bool inside = p ? in1 : in0;
-            const int64_t pix = ((int64_t)b * a.H + (inside ? py0 + 4 * p : 0)) * a.W + (inside ? px : 0);
+            for (int p = 0; p < kPX; ++p) {
+                const bool inside = p ? in1 : in0;
+                const int64_t pix = ((int64_t)b * a.H + (inside ? py0 + 4 * p : 0)) * a.W + (inside ? px : 0);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) src[p][c] = 0.f;
-            if (inside && a.wsum_image) {
+                for (int c = 0; c < 3; ++c) src[p][c] = 0.f;
+                if (inside && a.wsum_image) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) src[p][c] = a.wsum_image[pix * 3 + c];
-            } else if (inside && a.targets) {
-                const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
-                const float al = u8_unit(t.w);
-                const float rgb[3] = {u8_unit(t.x), u8_unit(t.y), u8_unit(t.z)};
+                    for (int c = 0; c < 3; ++c) src[p][c] = a.wsum_image[pix * 3 + c];
+                } else if (inside && a.targets) {
+                    const uchar4 t = reinterpret_cast<const uchar4 *>(a.targets)[pix];
+                    const float al = u8_unit(t.w);
+                    const float rgb[3] = {u8_unit(t.x), u8_unit(t.y), u8_unit(t.z)};
 #pragma unroll
-                for (int c = 0; c < 3; ++c) src[p][c] = rgb[c] * al + (1.0f - al) * bg[c];
+                    for (int c = 0; c < 3; ++c) src[p][c] = rgb[c] * al + (1.0f - al) * bg[c];
+                }
             }
         }
-    }
+    };
     const float2 one2 = f2(1.f, 1.f);
 
 #ifdef HS_RASTER_STATS
@@ -584,6 +590,10 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                 }
             }
         };
+        if (CI >= 2 && wantb && !src_ready) {      // (warp-uniform)
+            load_src();
+            src_ready = true;
+        }
         if (CI > 0 && wantb) {
             while (bits) {
                 const int j = __ffs(bits) - 1;
