@@ -427,6 +427,9 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
         if constexpr (VEC == 4) {
             float4 t = __ldg(reinterpret_cast<const float4 *>(base + e));
             bv[0] = t.x; bv[1] = t.y; bv[2] = t.z; bv[3] = t.w;
+        } else if constexpr (VEC == 2) {
+            float2 t = __ldg(reinterpret_cast<const float2 *>(base + e));
+            bv[0] = t.x; bv[1] = t.y;
         } else {
             bv[0] = base[e];
         }
@@ -449,6 +452,9 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
                     if constexpr (VEC == 4) {
                         float4 t = __ldg(reinterpret_cast<const float4 *>(deltas + (int64_t)k * E + e));
                         dn[q][0] = t.x; dn[q][1] = t.y; dn[q][2] = t.z; dn[q][3] = t.w;
+                    } else if constexpr (VEC == 2) {
+                        float2 t = __ldg(reinterpret_cast<const float2 *>(deltas + (int64_t)k * E + e));
+                        dn[q][0] = t.x; dn[q][1] = t.y;
                     } else {
                         dn[q][0] = __ldcs(deltas + (int64_t)k * E + e);
                     }
@@ -484,6 +490,8 @@ __global__ void __launch_bounds__(256) blend_fwd_kernel(int64_t E, int K, int B,
                     float *o = raw + (int64_t)(b0 + j) * E + e;
                     if constexpr (VEC == 4) {
                         *reinterpret_cast<float4 *>(o) = make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+                    } else if constexpr (VEC == 2) {
+                        __stcs(reinterpret_cast<float2 *>(o), make_float2(acc[j][0], acc[j][1]));
                     } else {
                         o[0] = acc[j][0];
                     }
@@ -1231,6 +1239,16 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
         const unsigned gy = (unsigned)((B + HS_BLEND_BC - 1) / HS_BLEND_BC);
         const dim3 grid((unsigned)grid_for(nv, 256), gy);
         launch_k(blend_fwd_kernel<4, HS_BLEND_BC>, grid, 256, smem, s, E, K, B, base14, deltas, psi, raw10);
+    } else if (E % 2 == 0 && (uintptr_t)base14 % 8 == 0 && (uintptr_t)deltas % 8 == 0 && (uintptr_t)raw10 % 8 == 0) {
+        // odd N (every other delta / frame row only 8-byte aligned): float2 channel pairs,
+        // frames in chunks over grid.y (render at 100,489 Gaussians: 367 us -> see DESIGN)
+#ifndef HS_BLEND_BC2
+#define HS_BLEND_BC2 8
+#endif
+        int64_t nv = E / 2;
+        const unsigned gy = (unsigned)((B + HS_BLEND_BC2 - 1) / HS_BLEND_BC2);
+        const dim3 grid((unsigned)grid_for(nv, 256), gy);
+        launch_k(blend_fwd_kernel<2, HS_BLEND_BC2>, grid, 256, smem, s, E, K, B, base14, deltas, psi, raw10);
     } else {
         unsigned grid = (unsigned)std::min<int64_t>(grid_for(E, 256), (int64_t)sms * 16);
         launch_k(blend_fwd_kernel<1, 16>, grid, 256, smem, s, E, K, B, base14, deltas, psi, raw10);

@@ -62,10 +62,10 @@ def test_blend_bwd_matches_float64(N, K, B):
     assert _rel(gpsi, ref_psi) <= 1e-5
 
 
-@pytest.mark.parametrize("B,zero", [(4, False), (8, True), (16, False), (16, True), (24, False)])
-def test_blend_fwd_matches_float64(B, zero):
+@pytest.mark.parametrize("N,B,zero", [(2048, 4, False), (2048, 8, True), (2048, 16, False), (2048, 16, True), (2048, 24, False), (2049, 16, False), (2049, 64, True), (1023, 5, False)])
+def test_blend_fwd_matches_float64(N, B, zero):
     from paper_2503_12886_b200 import _lib as L
-    N, K = 2048, 20
+    K = 20
     g = torch.Generator().manual_seed(B)
     base14 = torch.randn(14 * N, generator=g).cuda()
     deltas = torch.randn(K * 10 * N, generator=g).cuda()
