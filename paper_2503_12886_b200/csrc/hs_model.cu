@@ -398,6 +398,181 @@ __global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, i
     }
 }
 
+// Rows only 8-byte aligned (odd N: E = 10 N = 2 mod 4, and the deltas start at float 14 N of
+// the parameters): the same TMA pipeline, shared row stride TE + 4.  A row whose address is
+// 8 mod 16 is copied from 2 floats before the tile (its compute offset 2); the first tile
+// copies from 2 floats after the row start instead (nothing before a row is read), and the
+// aligned rows' 2-float tails on the last tile (a bulk copy moves multiples of 16 bytes) are
+// read by threads.  Compute as blend_fwd_tile4, with 8-byte shared loads on the offset rows
+// and 8-byte stores into the frames whose output row is offset.
+constexpr int kBmRS = kBfTE + 4;
+__host__ inline size_t blend_fwd_mis_smem(int K, int B) {
+    return 64 + sizeof(float) * ((size_t)K * blend_fwd_bpad(B) + kBfS * (size_t)(K + 1) * kBmRS);
+}
+__device__ __forceinline__ int row_off(const float *rowp) { return ((uintptr_t)rowp & 15u) ? 2 : 0; }
+template <int FB, bool kAllNonzero>
+__device__ __forceinline__ void blend_fwd_tile4_mis(int64_t E, int K, int B, int Bp, const float *s_psi,
+                                                    const float *stage, int64_t e0, const float *__restrict__ deltas,
+                                                    const float *__restrict__ base, float *__restrict__ raw) {
+    constexpr int kGroups = kBfTE / 4;
+    const int cg = threadIdx.x % kGroups, fg = threadIdx.x / kGroups;
+    const int c = 4 * cg;
+    const int64_t e = e0 + c;
+    if (e >= E) return;
+    const bool full = e + 4 <= E;                      // (else 2 channels: E = 2 mod 4)
+    const float *brow = stage + (size_t)K * kBmRS + row_off(base) + c;
+    const float2 b01 = *reinterpret_cast<const float2 *>(brow), b23 = *reinterpret_cast<const float2 *>(brow + 2);
+    for (int f0 = fg * FB; f0 < B; f0 += 2 * FB) {
+        float2 acc[FB][2];
+#pragma unroll
+        for (int j = 0; j < FB; ++j) {
+            acc[j][0] = b01;
+            acc[j][1] = b23;
+        }
+#pragma unroll 2
+        for (int k = 0; k < K; ++k) {
+            const float *row = stage + (size_t)k * kBmRS + row_off(deltas + (int64_t)k * E) + c;
+            const float2 d01 = *reinterpret_cast<const float2 *>(row), d23 = *reinterpret_cast<const float2 *>(row + 2);
+            float w[FB];
+            if constexpr (FB >= 4) {
+#pragma unroll
+                for (int q = 0; q < FB / 4; ++q) {
+                    const float4 w4 = *reinterpret_cast<const float4 *>(s_psi + (size_t)k * Bp + f0 + 4 * q);
+                    w[4 * q] = w4.x;
+                    w[4 * q + 1] = w4.y;
+                    w[4 * q + 2] = w4.z;
+                    w[4 * q + 3] = w4.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < FB; ++q) w[q] = s_psi[(size_t)k * Bp + f0 + q];
+            }
+#pragma unroll
+            for (int j = 0; j < FB; ++j) {
+                if (kAllNonzero || w[j] != 0.0f) {
+                    acc[j][0] = __ffma2_rn(make_float2(w[j], w[j]), d01, acc[j][0]);
+                    acc[j][1] = __ffma2_rn(make_float2(w[j], w[j]), d23, acc[j][1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < FB; ++j) {
+            const int f = f0 + j;
+            if (f >= B) continue;
+            float *o = raw + (int64_t)f * E + e;
+            if (full && ((uintptr_t)o & 15u) == 0) {
+                __stcs(reinterpret_cast<float4 *>(o), make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y));
+            } else {
+                __stcs(reinterpret_cast<float2 *>(o), acc[j][0]);
+                if (full) __stcs(reinterpret_cast<float2 *>(o + 2), acc[j][1]);
+            }
+        }
+    }
+}
+
+// row r (< K: delta row r, K: base) for the tile at e0: the bulk copy global [src, src + len)
+// -> shared index dst, and up to 2 floats (global g, shared index g - e0 + off) for threads
+struct RowPlan {
+    const float *rowp;
+    int64_t src, len;
+    int dst, off, nfill;
+    int64_t fill[8];
+};
+__device__ __forceinline__ RowPlan row_plan(int r, int64_t e0, int64_t E, int K, const float *deltas,
+                                            const float *base) {
+    RowPlan p;
+    p.rowp = r < K ? deltas + (int64_t)r * E : base;
+    p.off = row_off(p.rowp);
+    if (p.off && e0 > 0) {                    // from 2 floats before the tile
+        p.src = e0 - 2;
+        p.dst = 0;
+    } else if (p.off) {                       // the first tile: from float 2 (nothing before the row)
+        p.src = 2;
+        p.dst = 4;
+    } else {
+        p.src = e0;
+        p.dst = 0;
+    }
+    p.len = max((int64_t)0, min((int64_t)(kBmRS - p.dst), E - p.src)) & ~(int64_t)3;
+    // the floats the tile's compute reads that the copy does not cover (first / last tile)
+    const int64_t hi = min(e0 + (int64_t)kBfTE, E);
+    p.nfill = 0;
+    for (int64_t g = e0; g < min(p.src, hi); ++g) p.fill[p.nfill++] = g;
+    for (int64_t g = max(p.src + p.len, e0); g < hi && p.nfill < 8; ++g) p.fill[p.nfill++] = g;
+    return p;
+}
+
+__global__ void __launch_bounds__(kBfT) blend_fwd_tma_mis_kernel(int64_t E, int K, int B,
+                                                                 const float *__restrict__ base,
+                                                                 const float *__restrict__ deltas,
+                                                                 const float *__restrict__ psi,
+                                                                 float *__restrict__ raw) {
+    pdl_prologue();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    const int Bp = blend_fwd_bpad(B);
+    float *s_psi = reinterpret_cast<float *>(smem_raw + 64);           // [K][Bp]
+    float *stages = s_psi + K * Bp;                                      // kBfS x [(K + 1)][kBmRS]
+    const int64_t ntiles = (E + kBfTE - 1) / kBfTE;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int st = 0; st < kBfS; ++st) mbar_init(&bars[st], 1);
+        mbar_fence_init();
+    }
+    int nz = 1;
+    for (int i = tid; i < K * Bp; i += kBfT) {
+        const int k = i / Bp, b = i % Bp;
+        const float w = b < B ? psi[b * K + k] : 0.f;
+        s_psi[i] = w;
+        nz &= (b >= B) || (w != 0.0f);
+    }
+    const bool all_nonzero = __syncthreads_and(nz);
+    auto issue = [&](int64_t t, int st) {
+        const int64_t e0 = t * kBfTE;
+        float *dst = stages + (size_t)st * (K + 1) * kBmRS;
+        uint32_t bytes = 0;
+        for (int r = 0; r <= K; ++r) bytes += (uint32_t)(row_plan(r, e0, E, K, deltas, base).len * 4);
+        mbar_expect_tx(&bars[st], bytes);
+        for (int r = 0; r <= K; ++r) {
+            const RowPlan p = row_plan(r, e0, E, K, deltas, base);
+            if (p.len > 0) bulk_g2s(dst + (size_t)r * kBmRS + p.dst, p.rowp + p.src, (uint32_t)(p.len * 4), &bars[st]);
+        }
+    };
+    if (tid == 0) {
+        for (int st = 0; st < kBfS; ++st)
+            if (blockIdx.x + (int64_t)st * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)st * gridDim.x, st);
+    }
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % kBfS;
+        mbar_wait(&bars[st], (phase >> st) & 1u);
+        phase ^= 1u << st;
+        float *stage = stages + (size_t)st * (K + 1) * kBmRS;
+        const int64_t e0 = t * kBfTE;
+        if (e0 == 0 || e0 + kBfTE > E) {        // the first / last tile: the floats no copy moved
+            for (int r = tid; r <= K; r += kBfT) {
+                const RowPlan p = row_plan(r, e0, E, K, deltas, base);
+                for (int q = 0; q < p.nfill; ++q)
+                    stage[(size_t)r * kBmRS + (p.fill[q] - e0 + p.off)] = p.rowp[p.fill[q]];
+            }
+            __syncthreads();
+        }
+        if (Bp <= 4) {
+            if (all_nonzero) blend_fwd_tile4_mis<2, true>(E, K, B, Bp, s_psi, stage, e0, deltas, base, raw);
+            else blend_fwd_tile4_mis<2, false>(E, K, B, Bp, s_psi, stage, e0, deltas, base, raw);
+        } else if (Bp <= 8) {
+            if (all_nonzero) blend_fwd_tile4_mis<4, true>(E, K, B, Bp, s_psi, stage, e0, deltas, base, raw);
+            else blend_fwd_tile4_mis<4, false>(E, K, B, Bp, s_psi, stage, e0, deltas, base, raw);
+        } else {
+            if (all_nonzero) blend_fwd_tile4_mis<8, true>(E, K, B, Bp, s_psi, stage, e0, deltas, base, raw);
+            else blend_fwd_tile4_mis<8, false>(E, K, B, Bp, s_psi, stage, e0, deltas, base, raw);
+        }
+        __syncthreads();                      // every thread is done with this stage
+        if (tid == 0 && t + kBfS * (int64_t)gridDim.x < ntiles) issue(t + kBfS * (int64_t)gridDim.x, st);
+    }
+}
+
 // raw[b] = base + sum_k psi[b,k] delta_k over the 10N blended channels.  Each
 // thread owns VEC consecutive channels and keeps BC frames of accumulators, so
 // every delta element is read from HBM once per BC frames (once per step for
@@ -1239,6 +1414,14 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
         const unsigned gy = (unsigned)((B + HS_BLEND_BC - 1) / HS_BLEND_BC);
         const dim3 grid((unsigned)grid_for(nv, 256), gy);
         launch_k(blend_fwd_kernel<4, HS_BLEND_BC>, grid, 256, smem, s, E, K, B, base14, deltas, psi, raw10);
+    } else if (HS_BLEND_TMA && E % 2 == 0 && (uintptr_t)base14 % 8 == 0 && (uintptr_t)deltas % 8 == 0 &&
+               (uintptr_t)raw10 % 8 == 0 && E > 2 && blend_fwd_mis_smem(K, B) <= 200 * 1024) {
+        const size_t msm = blend_fwd_mis_smem(K, B);
+        cudaFuncSetAttribute(blend_fwd_tma_mis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
+        const int per_sm = std::max(1, (int)((220 * 1024) / msm));
+        const int64_t ntiles = (E + kBfTE - 1) / kBfTE;
+        const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * std::min(per_sm, HS_BLEND_CTAS_PER_SM));
+        launch_k(blend_fwd_tma_mis_kernel, grid, kBfT, msm, s, E, K, B, base14, deltas, psi, raw10);
     } else if (E % 2 == 0 && (uintptr_t)base14 % 8 == 0 && (uintptr_t)deltas % 8 == 0 && (uintptr_t)raw10 % 8 == 0) {
         // odd N (every other delta / frame row only 8-byte aligned): float2 channel pairs,
         // frames in chunks over grid.y (render at 100,489 Gaussians: 367 us -> see DESIGN)
