@@ -30,7 +30,10 @@
 
 namespace hs {
 
-constexpr int kWarpShort = 256;       // longest list one warp sorts (in registers)
+#ifndef HS_WARP_SHORT
+#define HS_WARP_SHORT 256
+#endif
+constexpr int kWarpShort = HS_WARP_SHORT;   // longest list one warp sorts (in registers)
 constexpr int kWarpCap = 1024;        // longest list one CTA sorts as merged register runs
 constexpr int kCtaCap = 8192;         // longest list one CTA sorts in shared memory
 constexpr int kCtaSortThreads = 512;
@@ -779,7 +782,8 @@ __global__ void __launch_bounds__(32 * kWarpSortWarps, HS_SHORT_SORT_MINB) tile_
             if (len <= 32u) sort_list<1>(depth, fb, start, len, vals, lane, s_k64, s_q);
             else if (len <= 64u) sort_list<2>(depth, fb, start, len, vals, lane, s_k64, s_q);
             else if (len <= 128u) sort_list<4>(depth, fb, start, len, vals, lane, s_k64, s_q);
-            else sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q);
+            else if (kWarpShort <= 256 || len <= 256u) sort_list<8>(depth, fb, start, len, vals, lane, s_k64, s_q);
+            else sort_list<(kWarpShort > 256 ? 16 : 8)>(depth, fb, start, len, vals, lane, s_k64, s_q);
         }
     }
 }
