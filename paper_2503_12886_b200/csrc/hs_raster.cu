@@ -54,6 +54,9 @@ constexpr int train_minb(int ci) { return ci >= 2 ? HS_RASTER_MINB_CI : HS_RASTE
 #ifndef HS_RASTER_EXACT_CULL
 #define HS_RASTER_EXACT_CULL 1       // cull row groups with the exact ellipse-rectangle distance
 #endif
+#ifndef HS_QTEST
+#define HS_QTEST 1                   // the reference's q <= qmax test next to alpha >= 1/255 (0: A/B only)
+#endif
 #ifndef HS_RASTER_FWD_ASM
 #define HS_RASTER_FWD_ASM 1          // forward: per-pixel decision as one predicate chain
 #endif
@@ -284,7 +287,11 @@ __device__ __forceinline__ float fwd_gate(uint32_t mask, uint32_t lanebit, float
         "setp.ne.u32 p, m, 0;\n\t"
         "setp.ge.and.f32 p, %4, %5, p;\n\t"
         "selp.u32 %1, %9, %1, p;\n\t"
+#if HS_QTEST
         "setp.ge.and.f32 q, %6, %7, p;\n\t"
+#else
+        "mov.pred q, p;\n\t"
+#endif
         "setp.le.and.f32 q, %8, %10, q;\n\t"
         "selp.f32 %0, %8, 0f00000000, q;\n\t}"
         : "=f"(out), "+r"(stop)
@@ -958,8 +965,8 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
                 in0 = in0 && jl < stop.x;
                 in1 = in1 && jl < stop.y;
             }
-            const bool ok0 = in0 && e2.x >= t.kq && nal.x <= -kAlphaCutoff;
-            const bool ok1 = in1 && e2.y >= t.kq && nal.y <= -kAlphaCutoff;
+            const bool ok0 = in0 && (!HS_QTEST || e2.x >= t.kq) && nal.x <= -kAlphaCutoff;
+            const bool ok1 = in1 && (!HS_QTEST || e2.y >= t.kq) && nal.y <= -kAlphaCutoff;
             // a failing pixel runs the same instructions with alpha = G = 0, which leaves
             // t_rev and the suffix unchanged (1 / (1 - 0) == 1 exactly) and adds zeros
             G.x = ok0 ? G.x : 0.f;
