@@ -858,9 +858,12 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
             const uint32_t q = (uint32_t)(w * kRun + e * 32 + lane);
             if (q < len) key[e] = (((key[e] - dmin) >> sh) << IB) | q;
         }
-        if (w * kRun < (int)len) bitonic_u32<E>(key, lane);   // (runs past the end: padding)
+        if (w * kRun < (int)len) {                            // (runs past the end: padding)
+            if (HS_SORT_LANE_MAJOR) bitonic_u32_lm<E>(key, lane);
+            else bitonic_u32<E>(key, lane);
+        }
 #pragma unroll
-        for (int e = 0; e < E; ++e) s_run[w * kRun + e * 32 + lane] = key[e];
+        for (int e = 0; e < E; ++e) s_run[w * kRun + (HS_SORT_LANE_MAJOR ? lane * E + e : e * 32 + lane)] = key[e];
         __syncthreads();
         // merged position: own rank + the keys below it in every other run (runs past
         // the list's end hold padding only and count nothing)
@@ -869,7 +872,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) tile_sort_long_kernel(
         for (int e = 0; e < E; ++e) {
             const uint32_t x = key[e];
             if (x == 0xFFFFFFFFu) continue;          // padding (real keys stay below 2^31)
-            uint32_t pos = (uint32_t)(e * 32 + lane);
+            uint32_t pos = (uint32_t)(HS_SORT_LANE_MAJOR ? lane * E + e : e * 32 + lane);
             for (int v = 0; v < runs; ++v) {
                 if (v == w) continue;
                 // count of run v's keys below x: a branch-free search over its kRun keys
