@@ -19,6 +19,7 @@ Step (N Gaussians, K bases, B frames):
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -747,7 +748,10 @@ class Trainer:
 
     def _side_stream(self):
         if self._side is None:
-            self._side = torch.cuda.Stream(device=self.av.device)
+            # (HS_SIDE_PRIORITY=-1: the side stream -- rig, loss reduction, the one-rank Adam --
+            # at high priority)
+            self._side = torch.cuda.Stream(device=self.av.device,
+                                           priority=int(os.environ.get("HS_SIDE_PRIORITY", "0")))
         return self._side
 
     def _forward_project(self, thetas, frames, cameras, zero=(None, None, None), order=False, speculate=None):
