@@ -241,7 +241,12 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
                  const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor,
                  uint32_t *lists,
                  uint32_t *list_counts, int list_half, const unsigned long long *summary, uint64_t capacity,
-                 uint32_t *keys, uint32_t *values, void *fork, void *stream);
+                 uint32_t *keys, uint32_t *values, int flags, void *fork, void *stream);
+/* hs_tile_fill flags: HS_FILL_CTA_SORT also sorts the lists of
+ * hs_tile_cta_sort_min()..hs_tile_sort_cap() entries (a no-op on the device when there are
+ * none), first on the fork's side stream -- for a caller that expects such lists (its
+ * previous batch had them); otherwise hs_tile_fill_longest after the summary read. */
+#define HS_FILL_CTA_SORT 1
 /* ranges[frame*tiles + tile] = [start, end); caller zero-fills ranges first. */
 int hs_tile_ranges(int64_t num_keys, const uint64_t *keys, uint32_t *ranges, void *stream);
 

@@ -28,6 +28,7 @@ RASTER_WSUMS_IMAGE = 32
 RASTER_ORDER_READY = 64
 RASTER_DETERMINISTIC = 128
 RASTER_RAW_MEAN = 256
+FILL_CTA_SORT = 1                 # hs_tile_fill flags (HS_FILL_CTA_SORT)
 
 _P = ctypes.c_void_p
 
@@ -78,7 +79,7 @@ SIGNATURES = {
     "hs_raster_tile_order": (_I, [_I, _I, _I, _P, _I, _P, _P]),
     "hs_tile_count": (_I, [_I, _L, _I, _I, _P, _P, _P, _P]),
     "hs_tile_scan": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
-    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P, _P, _P]),
+    "hs_tile_fill": (_I, [_I, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, ctypes.c_uint64, _P, _P, _I, _P, _P]),
     "hs_fork_create": (_P, []),
     "hs_fork_destroy": (None, [_P]),
     "hs_bin_stats": (_I, [ctypes.POINTER(ctypes.c_uint64), _I]),

@@ -1050,7 +1050,7 @@ void hs_fork_destroy(void *fork) {
 int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, const uint32_t *counts,
                  const uint32_t *tile_rects, const float *depth, const uint32_t *ranges, uint32_t *cursor, uint32_t *lists,
                  uint32_t *list_counts, int list_half, const unsigned long long *summary, uint64_t capacity,
-                 uint32_t *keys, uint32_t *values, void *fork, void *stream) {
+                 uint32_t *keys, uint32_t *values, int flags, void *fork, void *stream) {
     const int64_t items = (int64_t)B * N;
     if (items <= 0) return HS_OK;
     cudaStream_t s = HS_CHECK_STREAM(stream);
@@ -1081,6 +1081,14 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
         cudaStreamWaitEvent(f->side, f->forked, 0);
         side = f->side;
     }
+    if (flags & HS_FILL_CTA_SORT) {
+        // lists of kWarpCap+1..kCtaCap entries expected: their CTA sorts go first on the
+        // side stream, so they start beside the long-list sort instead of after it
+        const int csmem = kCtaCap * (int)sizeof(unsigned long long);
+        cudaFuncSetAttribute(tile_sort_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
+        launch_k(tile_sort_cta_kernel, (unsigned)sms * 2, kCtaSortThreads, csmem, side, N, tile_bits, nseg, depth,
+                 ranges, lists, list_counts, list_half, capacity, summary, values);
+    }
 #ifndef HS_SHORT_SORT_CTAS_PER_SM
 #define HS_SHORT_SORT_CTAS_PER_SM 16
 #endif
@@ -1090,7 +1098,11 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
 #ifndef HS_LONG_SORT_CTAS_PER_SM
 #define HS_LONG_SORT_CTAS_PER_SM 16
 #endif
-    launch_k(tile_sort_long_kernel, (unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s, 
+#ifndef HS_LONG_SORT_CTAS_PER_SM_CTA
+#define HS_LONG_SORT_CTAS_PER_SM_CTA 16
+#endif
+    const int long_per_sm = (flags & HS_FILL_CTA_SORT) ? HS_LONG_SORT_CTAS_PER_SM_CTA : HS_LONG_SORT_CTAS_PER_SM;
+    launch_k(tile_sort_long_kernel, (unsigned)sms * long_per_sm, 32 * kLongWarps, 0, s, 
         N, tile_bits, nseg, depth, ranges, lists, list_counts, list_half, capacity, summary, values);
     if (f) cudaStreamWaitEvent(s, f->joined, 0);
     return check_launch("hs_tile_fill");

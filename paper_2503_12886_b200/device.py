@@ -382,6 +382,10 @@ class Binner:
         self.result = (keys[:total], vals[:total], ranges, tile_bits, tiles)
         return self.result
 
+    def _fill_longest(self, B, N, width, height, depth, ranges, s):
+        L.call("hs_tile_fill_longest", B, N, width, height, _p(depth), _p(ranges), _p(self.lists),
+               _p(self.list_counts), self.list_half, _p(self.summary), self.cap, _p(self.vals), s)
+
     def _bin_two_level(self, B, N, width, height, records, counts, total, rects=None):
         """Stage 2: emission in depth order with 32-bit (frame, tile) keys and a stable
         sort of those keys alone (frame + tile bits: 2 passes at C2) -- the same
@@ -479,10 +483,16 @@ class Binner:
             if not self.fork.value:
                 raise RuntimeError(f"hs_fork_create: {L.last_error()}")
 
+        # lists past the warp-run sorts expected (the previous batch had them: render
+        # batches of crowded tiles): the fill sorts them too, first on its side stream,
+        # instead of a CTA sort enqueued after the summary read
+        forked_longest = _cta_sort_min() <= self.longest <= tile_sort_cap()
+
         def fill():
             L.call("hs_tile_fill", B, N, width, height, _p(records), _p(counts), _p(rects), _p(depth), _p(ranges),
                    _p(self.cursor), _p(self.lists), _p(self.list_counts), self.list_half, _p(self.summary), self.cap,
-                   _p(self.keys) if self.write_keys else None, _p(self.vals), self.fork, s)
+                   _p(self.keys) if self.write_keys else None, _p(self.vals),
+                   L.FILL_CTA_SORT if forked_longest else 0, self.fork, s)
         fill()                              # first: the GPU reaches it right after the scan
         self.order_ready = False
         if after_scan is not None:
@@ -494,7 +504,8 @@ class Binner:
         cap_at_fill = self.cap
         self.spec_valid = False
         if speculate is not None:
-            guard = L.RasterGuard(self.summary.data_ptr(), cap_at_fill, _cta_sort_min() - 1)
+            guard = L.RasterGuard(self.summary.data_ptr(), cap_at_fill,
+                                  tile_sort_cap() if forked_longest else _cta_sort_min() - 1)
             speculate(self.vals[:cap_at_fill], ranges, tile_bits, guard)
         ready.synchronize()
         total = int(self.summary_host[0])
@@ -503,20 +514,20 @@ class Binner:
         self.depth_bits = (dr & 0xFFFFFFFF, dr >> 32)
         self.longest = int(self.summary_host[3])
         self.mode = "tiles"
-        if total > self.cap:
+        regrown = total > self.cap
+        if regrown:
             self._ensure(total)
             self.cursor[:nseg].copy_(ranges.view(-1, 2)[:, 0])
             fill()
-        if _cta_sort_min() <= self.longest <= tile_sort_cap():
-            # lists long enough for the shared-memory CTA sort (rare): after the fill
-            L.call("hs_tile_fill_longest", B, N, width, height, _p(depth), _p(ranges), _p(self.lists),
-                   _p(self.list_counts), self.list_half, _p(self.summary), self.cap, _p(self.vals), s)
-            self.launches_extra = 1
-        else:
-            self.launches_extra = 0
+        huge = _cta_sort_min() <= self.longest <= tile_sort_cap()
+        self.launches_extra = int(forked_longest) * (1 + int(regrown))
+        if huge and not forked_longest:
+            # lists long enough for the shared-memory CTA sort, not expected: after the fill
+            self._fill_longest(B, N, width, height, depth, ranges, s)
+            self.launches_extra += 1
         self._depth_range_clean = self.longest <= tile_sort_cap()
-        self.spec_valid = (speculate is not None and total <= cap_at_fill and self.longest < _cta_sort_min()
-                           and code == L.HS_NO_ERROR)
+        self.spec_valid = (speculate is not None and total <= cap_at_fill and code == L.HS_NO_ERROR
+                           and (self.longest < _cta_sort_min() or (forked_longest and huge)))
         if self.longest > tile_sort_cap():
             # a list too long to sort in shared memory: the global two-level sort
             # (whose ranges replace the ones the tile order was built from)

@@ -35,7 +35,7 @@ for r in range(reps):
     e[2].record()
     L.call("hs_tile_fill", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts), _p(bn.rects), _p(tr.depth), _p(ranges),
            _p(bn.cursor), _p(bn.lists), _p(bn.list_counts), bn.list_half, _p(bn.summary), bn.cap, _p(bn.keys),
-           _p(bn.vals), bn.fork, s)
+           _p(bn.vals), 0, bn.fork, s)
     e[3].record()
 torch.cuda.synchronize()
 acc = [0.0, 0.0, 0.0]

@@ -60,7 +60,7 @@ def call():
         rects = bn.tile_rects_buffer(B, N, tr.W, tr.H)
         L.call("hs_tile_fill", B, N, tr.W, tr.H, _p(tr.records), _p(tr.counts), _p(rects), _p(tr.depth),
                _p(ranges_), _p(bn.cursor), _p(bn.lists), _p(bn.list_counts), bn.list_half, _p(bn.summary), bn.cap,
-               None, _p(bn.vals), bn.fork, s)
+               None, _p(bn.vals), 0, bn.fork, s)
     elif stage == "project_fwd":
         rects = bn.tile_rects_buffer(B, N, tr.W, tr.H)
         L.call("hs_project_avatar_fwd", B, N, F, tr.W, tr.H, _p(tr.raw10), _p(av.base14), _p(av.tri_index),

@@ -213,6 +213,13 @@ def test_binning_bit_exact_crowded_tiles(n):
     check_two_level(dev, res, n)
     # lists past the shared-memory sort's cap take the two-level fallback
     assert check_tiles(dev, res, n) == ("two_level" if n > 8192 else "tiles")
+    # again with the same Binner: the previous batch had lists past the warp runs, so the
+    # fill sorts them itself (HS_FILL_CTA_SORT, before the summary read), with and without
+    # a capacity regrow
+    assert check_tiles(dev, res, n) == ("two_level" if n > 8192 else "tiles")
+    if 1024 < n <= 8192:
+        assert dev["binner"].launches_extra == 1
+    assert check_tiles(dev, res, n, regrow=True) == ("two_level" if n > 8192 else "tiles")
 
 
 # --------------------------------------------------------------------- raster
