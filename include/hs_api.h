@@ -98,6 +98,8 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
  * g_deltas[k] = sum_b psi[b,k] g_raw10[b];  gpsi partial sums per block.
  * Both outputs are written (not accumulated).  Returns the partial count in
  * *num_partials; gpsi_partials needs hs_blend_bwd_partials(N) * B * K floats. */
+/* Kernel launches hs_blend_bwd issues for these sizes (16-byte aligned buffers). */
+int hs_blend_bwd_kernels(int64_t N, int K, int B);
 int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
                  const float *g_raw14, float *g_base14, float *g_deltas,
                  float *gpsi_partials, int *num_partials, void *stream);

@@ -50,6 +50,7 @@ SIGNATURES = {
     "hs_mlp_fwd": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "hs_mlp_bwd": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "hs_blend_fwd": (_I, [_L, _I, _I, _P, _P, _P, _P, _P]),
+    "hs_blend_bwd_kernels": (_I, [_L, _I, _I]),
     "hs_blend_bwd": (_I, [_L, _I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I), _P]),
     "hs_blend_bwd_partials": (_I, [_L]),
     "hs_project_avatar_fwd": (_I, [_I, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,

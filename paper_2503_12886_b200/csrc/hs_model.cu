@@ -1015,6 +1015,196 @@ __global__ void __launch_bounds__(256, HS_BB_MINB) blend_bwd_tma_kernel(int64_t 
     }
 }
 
+// HS_BLEND_BWD_SPLIT: the adjoint as two streaming kernels, for any N alignment and any
+// frame count in one pass over g (the fused kernels above take <= 16 frames per launch,
+// so more frames mean read-modify-write passes over g_delta, and the TMA tiles need
+// N % 128 == 0):
+// (a) blend_bwd_gd_kernel -- g_base and g_delta.  One thread per channel pair (e, e + 1):
+//     the B frames' g[b][e..e+1] (8-byte loads, coalesced, 4 in flight) in ascending frame
+//     order into the running sum and, for e < 10N, into K packed accumulators with
+//     psi[b][k] as the FFMA2's broadcast operand (psi staged 128 frames at a time).  One
+//     store per output.
+// (b) blend_bwd_psi_kernel -- g_psi, one partial per CTA (fixed order).  The CTA's range
+//     of 64-channel tiles, double-buffered with cp.async (8-byte g pairs, zero-filled past
+//     10N; the delta rows transposed to [channel][basis] so basis pairs are adjacent).
+//     Thread item = 4 frames x 10 bases, G = 256 / items threads per item over the
+//     tile's channel pairs: 40 FFMA2 per 14 shared loads; the G channel groups are summed
+//     in a fixed order at the end.
+#ifndef HS_BLEND_BWD_SPLIT
+#define HS_BLEND_BWD_SPLIT 1          // 0: never, 1: for more than 16 frames, 2: always
+#endif
+constexpr int kGdT = 256;
+constexpr int kGdFrames = 128;        // psi frames staged per shared-memory round
+constexpr int kPsT = 256, kPsTE = 64;
+constexpr int kPsMaxB = 128;          // frames per psi launch
+
+#ifndef HS_GD_UNROLL
+#define HS_GD_UNROLL 8                // frames whose loads are in flight together
+#endif
+#ifndef HS_GD_MINB
+#define HS_GD_MINB 2
+#endif
+template <int KM>
+__global__ void __launch_bounds__(kGdT, HS_GD_MINB) blend_bwd_gd_kernel(int64_t N, int K, int B,
+                                                                        const float *__restrict__ psi,
+                                                                        const float *__restrict__ g_raw,
+                                                                        float *__restrict__ g_base,
+                                                                        float *__restrict__ g_deltas) {
+    constexpr int U = HS_GD_UNROLL;
+    pdl_prologue();
+    __shared__ __align__(16) float s_psi[kGdFrames * KM];
+    const int64_t E10 = 10 * N, E14 = 14 * N;
+    const int64_t e = 2 * ((int64_t)blockIdx.x * kGdT + threadIdx.x);
+    const bool in = e < E14, blended = e < E10;      // (10N even: a pair is wholly in or out)
+    float2 acc[KM], sum = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < KM; ++k) acc[k] = make_float2(0.f, 0.f);
+    for (int b0 = 0; b0 < B; b0 += kGdFrames) {
+        const int Bc = min(kGdFrames, B - b0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < Bc * KM; i += kGdT) {
+            const int b = i / KM, k = i % KM;
+            s_psi[i] = k < K ? psi[(int64_t)(b0 + b) * K + k] : 0.f;
+        }
+        __syncthreads();
+        if (!in) continue;
+        const float *gp = g_raw + (int64_t)b0 * E14 + e;
+        auto frame = [&](float2 g, int b) {
+            sum = __fadd2_rn(sum, g);
+            if (blended) {
+#pragma unroll
+                for (int k = 0; k < KM; ++k) {
+                    const float w = s_psi[b * KM + k];
+                    acc[k] = __ffma2_rn(make_float2(w, w), g, acc[k]);
+                }
+            }
+        };
+        int b = 0;
+        for (; b + U <= Bc; b += U) {
+            float2 g[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) g[j] = __ldcs(reinterpret_cast<const float2 *>(gp + (int64_t)(b + j) * E14));
+#pragma unroll
+            for (int j = 0; j < U; ++j) frame(g[j], b + j);
+        }
+        for (; b < Bc; ++b) frame(__ldcs(reinterpret_cast<const float2 *>(gp + (int64_t)b * E14)), b);
+    }
+    if (!in) return;
+    *reinterpret_cast<float2 *>(g_base + e) = sum;
+    if (blended) {
+#pragma unroll
+        for (int k = 0; k < KM; ++k)
+            if (k < K) __stcs(reinterpret_cast<float2 *>(g_deltas + (int64_t)k * E10 + e), acc[k]);
+    }
+}
+
+__device__ __forceinline__ void cp_async_zfill(void *dst, const void *src, int bytes, bool ok) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+
+__host__ __device__ inline int psi_kpad(int K) { return (K + 9) / 10 * 10; }
+constexpr int kPsRow = kPsTE + 2;     // g row stride (pad: the frame blocks of a warp on distinct banks)
+__host__ __device__ inline int psi_stage(int Bc, int K) { return ((Bc + 3) & ~3) * kPsRow + kPsTE * psi_kpad(K); }
+__host__ inline size_t blend_bwd_psi_smem(int Bc, int K) {
+    return sizeof(float) * (size_t)std::max(2 * psi_stage(Bc, K), kPsT * 40);
+}
+
+__global__ void __launch_bounds__(kPsT) blend_bwd_psi_kernel(int64_t N, int K, int Bc, int b0,
+                                                             const float *__restrict__ deltas,
+                                                             const float *__restrict__ g_raw,
+                                                             float *__restrict__ partials, int P) {
+    pdl_prologue();
+    extern __shared__ __align__(16) float sm[];
+    const int Bp = (Bc + 3) & ~3, Kp = psi_kpad(K);
+    const int nfb = Bp / 4, items = nfb * (Kp / 10);
+    const int G = kPsT / items;                      // (host: items <= 128)
+    const int tid = threadIdx.x, item = tid / G, cg = tid % G;
+    const bool active = item < items;
+    const int fb = item % nfb, kb = item / nfb;
+    const int stage = psi_stage(Bc, K);
+    const int64_t E10 = 10 * N, E14 = 14 * N;
+    const int64_t ntiles = (E10 + kPsTE - 1) / kPsTE;
+    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t_lo = (int64_t)blockIdx.x * per, t_hi = min(ntiles, t_lo + per);
+    for (int i = tid; i < 2 * stage; i += kPsT) sm[i] = 0.f;    // (padding rows / bases stay zero)
+    __syncthreads();
+    auto issue = [&](int64_t t, int buf) {
+        float *sg = sm + buf * stage, *sd = sg + Bp * kPsRow;
+        const int64_t e0 = t * kPsTE;
+        for (int i = tid; i < Bc * (kPsTE / 2); i += kPsT) {
+            const int b = i / (kPsTE / 2), c = 2 * (i % (kPsTE / 2));
+            const bool ok = e0 + c < E10;
+            cp_async_zfill(sg + b * kPsRow + c, g_raw + (int64_t)(b0 + b) * E14 + (ok ? e0 + c : 0), 8, ok);
+        }
+        for (int i = tid; i < K * kPsTE; i += kPsT) {
+            const int k = i / kPsTE, c = i % kPsTE;
+            const bool ok = e0 + c < E10;
+            cp_async_zfill(sd + c * Kp + k, deltas + (int64_t)k * E10 + (ok ? e0 + c : 0), 4, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float2 acc[4][5];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[f][q] = make_float2(0.f, 0.f);
+    if (t_lo < t_hi) issue(t_lo, 0);
+    int it = 0;
+    for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
+        const int buf = it & 1;
+        if (t + 1 < t_hi) {
+            issue(t + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        if (active) {
+            const float *sg = sm + buf * stage, *sd = sg + Bp * kPsRow;
+            for (int c = 2 * cg; c < kPsTE; c += 2 * G) {
+                float2 gv[4];
+#pragma unroll
+                for (int f = 0; f < 4; ++f) gv[f] = *reinterpret_cast<const float2 *>(sg + (4 * fb + f) * kPsRow + c);
+                const float *d0 = sd + c * Kp + 10 * kb, *d1 = d0 + Kp;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const float2 da = *reinterpret_cast<const float2 *>(d0 + 2 * q);
+                    const float2 db = *reinterpret_cast<const float2 *>(d1 + 2 * q);
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) {
+                        acc[f][q] = __ffma2_rn(make_float2(gv[f].x, gv[f].x), da, acc[f][q]);
+                        acc[f][q] = __ffma2_rn(make_float2(gv[f].y, gv[f].y), db, acc[f][q]);
+                    }
+                }
+            }
+        }
+        __syncthreads();                             // before this buffer is refilled
+    }
+    // the G channel groups of each item, summed in a fixed order
+    float *red = sm;                                 // [items][G][40]
+    if (active) {
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                red[(item * G + cg) * 40 + f * 10 + 2 * q] = acc[f][q].x;
+                red[(item * G + cg) * 40 + f * 10 + 2 * q + 1] = acc[f][q].y;
+            }
+    }
+    __syncthreads();
+    for (int o = tid; o < Bc * K; o += kPsT) {
+        const int b = o / K, k = o % K;
+        const int itm = b / 4 + (k / 10) * nfb, slot = (b % 4) * 10 + k % 10;
+        float s = 0.f;
+        for (int c = 0; c < G; ++c) s += red[(itm * G + c) * 40 + slot];
+        partials[((int64_t)(b0 + b) * K + k) * P + blockIdx.x] = s;
+    }
+}
+
 // ------------------------------------------------------------------ Adam
 
 // S/optim.py:28-40, one update of the flat parameter buffer [base | deltas | mlp]:
@@ -1444,6 +1634,12 @@ int hs_blend_bwd_partials(int64_t N) {
     return (int)std::min<int64_t>(kBBlocks, std::max<int64_t>(1, warps));
 }
 
+int hs_blend_bwd_kernels(int64_t N, int K, int B) {
+    if (N >= 17 && (HS_BLEND_BWD_SPLIT == 2 || (HS_BLEND_BWD_SPLIT == 1 && B > kBMaxB)))
+        return 1 + (B + kPsMaxB - 1) / kPsMaxB;
+    return (B + kBMaxB - 1) / kBMaxB;
+}
+
 int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi, const float *g_raw14,
                  float *g_base14, float *g_deltas, float *gpsi_partials, int *num_partials, void *stream) {
     if (K > kBMaxK || K < 1 || B < 1 || N < 1) {
@@ -1455,6 +1651,27 @@ int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
     const bool tma = HS_BLEND_BWD_TMA && N % (kBbTE / 2) == 0 && K <= kBbK &&
                      (uintptr_t)deltas % 16 == 0 && (uintptr_t)g_raw14 % 16 == 0 && (uintptr_t)g_base14 % 16 == 0 &&
                      (uintptr_t)g_deltas % 16 == 0;
+    const bool split_ok = N >= 17 && (uintptr_t)deltas % 8 == 0 && (uintptr_t)g_raw14 % 8 == 0 &&
+                          (uintptr_t)g_base14 % 8 == 0 && (uintptr_t)g_deltas % 8 == 0;
+    const bool split = split_ok && (HS_BLEND_BWD_SPLIT == 2 || (HS_BLEND_BWD_SPLIT == 1 && B > kBMaxB));
+    if (split) {
+        // g_base / g_delta over all frames in one launch, then g_psi per <= 128 frames
+        const int64_t pairs = 7 * N;
+        if (K <= 20)
+            launch_k(blend_bwd_gd_kernel<20>, (unsigned)((pairs + kGdT - 1) / kGdT), kGdT, 0, s, N, K, B, psi, g_raw14,
+                     g_base14, g_deltas);
+        else
+            launch_k(blend_bwd_gd_kernel<32>, (unsigned)((pairs + kGdT - 1) / kGdT), kGdT, 0, s, N, K, B, psi, g_raw14,
+                     g_base14, g_deltas);
+        for (int b0 = 0; b0 < B; b0 += kPsMaxB) {
+            const int Bc = std::min(kPsMaxB, B - b0);
+            const size_t smem = blend_bwd_psi_smem(Bc, K);
+            cudaFuncSetAttribute(blend_bwd_psi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            launch_k(blend_bwd_psi_kernel, P, kPsT, smem, s, N, K, Bc, b0, deltas, g_raw14, gpsi_partials, P);
+        }
+        if (num_partials) *num_partials = P;
+        return check_launch("hs_blend_bwd");
+    }
     if (tma) cudaFuncSetAttribute(blend_bwd_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)blend_bwd_tma_smem());
     for (int b0 = 0; b0 < B; b0 += kBMaxB) {

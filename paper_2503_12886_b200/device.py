@@ -924,7 +924,7 @@ class Trainer:
         nparts = ctypes.c_int(0)
         self._call("blend_bwd", "hs_blend_bwd", N, K, B, _p(av.deltas), _p(self.psi), _p(self.g_raw14),
                    _p(self.grads), _p(self.grads[14 * N:]), _p(self.gpsi_partials), ctypes.byref(nparts), s,
-                   kernels=(B + 15) // 16)
+                   kernels=int(L.load().hs_blend_bwd_kernels(N, K, B)))
         buckets = self.buckets()
         ci_mode = (2 if self.pg is not None else 1) if ci else 0
         self.step_count += 1

@@ -3,7 +3,10 @@ reduce of S/train.py:253-255), over the shapes that select each kernel variant:
 
 * N % 128 == 0 with 9..16-frame passes: the TMA-tiled adjoint (1 KB rows), incl. a
   32-frame batch (two passes, the second accumulating);
-* other N / frame counts: the register-streaming adjoint;
+* other N / frame counts up to 16: the register-streaming adjoint;
+* more than 16 frames: the split adjoint (g_base / g_delta over all frames in one pass,
+  then g_psi per <= 128 frames from cp.async-staged tiles), incl. odd N, K > 20 (the
+  32-basis instantiation), 130 frames (two g_psi launches) and N < 17 (the fused kernels);
 * the forward's TMA tiles (frames in two groups) for 4 / 8 / 16 / 24 frames, with and
   without zero weights (the reference skips psi == 0 terms).
 
@@ -35,7 +38,9 @@ def _rel(a, b):
     return float((a - b).abs().max() / max(float(b.abs().max()), 1e-30))
 
 
-@pytest.mark.parametrize("N,K,B", [(50176, 20, 16), (4096, 20, 16), (256, 20, 32), (19881, 20, 4), (1000, 7, 12), (1280, 20, 9)])
+@pytest.mark.parametrize("N,K,B", [(50176, 20, 16), (4096, 20, 16), (256, 20, 32), (19881, 20, 4), (1000, 7, 12),
+                                   (1280, 20, 9), (30011, 20, 48), (4097, 20, 40), (2048, 20, 32), (1000, 7, 130),
+                                   (1001, 25, 20), (16, 20, 20)])
 def test_blend_bwd_matches_float64(N, K, B):
     from paper_2503_12886_b200 import _lib as L
     g = torch.Generator().manual_seed(N + K + B)
