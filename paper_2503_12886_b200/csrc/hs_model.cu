@@ -1039,7 +1039,7 @@ constexpr int kPsT = 256, kPsTE = 64;
 constexpr int kPsMaxB = 128;          // frames per psi launch
 
 #ifndef HS_GD_UNROLL
-#define HS_GD_UNROLL 8                // frames whose loads are in flight together
+#define HS_GD_UNROLL 16               // frames whose loads are in flight together
 #endif
 #ifndef HS_GD_MINB
 #define HS_GD_MINB 2
@@ -1050,7 +1050,7 @@ __global__ void __launch_bounds__(kGdT, HS_GD_MINB) blend_bwd_gd_kernel(int64_t 
                                                                         const float *__restrict__ g_raw,
                                                                         float *__restrict__ g_base,
                                                                         float *__restrict__ g_deltas) {
-    constexpr int U = HS_GD_UNROLL;
+    constexpr int U = KM > 20 ? 8 : HS_GD_UNROLL;     // (32 bases: registers)
     pdl_prologue();
     __shared__ __align__(16) float s_psi[kGdFrames * KM];
     const int64_t E10 = 10 * N, E14 = 14 * N;
