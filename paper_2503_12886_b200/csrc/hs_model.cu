@@ -406,6 +406,9 @@ __global__ void __launch_bounds__(kBfT) blend_fwd_tma_kernel(int64_t E, int K, i
 // read by threads.  Compute as blend_fwd_tile4, with 8-byte shared loads on the offset rows
 // and 8-byte stores into the frames whose output row is offset.
 constexpr int kBmRS = kBfTE + 4;
+#ifndef HS_BLEND_MIS_WIDE_B
+#define HS_BLEND_MIS_WIDE_B 16
+#endif
 __host__ inline size_t blend_fwd_mis_smem(int K, int B) {
     return 64 + sizeof(float) * ((size_t)K * blend_fwd_bpad(B) + kBfS * (size_t)(K + 1) * kBmRS);
 }
@@ -415,14 +418,14 @@ __device__ __forceinline__ void blend_fwd_tile4_mis(int64_t E, int K, int B, int
                                                     const float *stage, int64_t e0, const float *__restrict__ deltas,
                                                     const float *__restrict__ base, float *__restrict__ raw) {
     constexpr int kGroups = kBfTE / 4;
-    const int cg = threadIdx.x % kGroups, fg = threadIdx.x / kGroups;
+    const int cg = threadIdx.x % kGroups, fg = threadIdx.x / kGroups, ng = blockDim.x / kGroups;
     const int c = 4 * cg;
     const int64_t e = e0 + c;
     if (e >= E) return;
     const bool full = e + 4 <= E;                      // (else 2 channels: E = 2 mod 4)
     const float *brow = stage + (size_t)K * kBmRS + row_off(base) + c;
     const float2 b01 = *reinterpret_cast<const float2 *>(brow), b23 = *reinterpret_cast<const float2 *>(brow + 2);
-    for (int f0 = fg * FB; f0 < B; f0 += 2 * FB) {
+    for (int f0 = fg * FB; f0 < B; f0 += ng * FB) {
         float2 acc[FB][2];
 #pragma unroll
         for (int j = 0; j < FB; ++j) {
@@ -502,7 +505,7 @@ __device__ __forceinline__ RowPlan row_plan(int r, int64_t e0, int64_t E, int K,
     return p;
 }
 
-__global__ void __launch_bounds__(kBfT) blend_fwd_tma_mis_kernel(int64_t E, int K, int B,
+__global__ void __launch_bounds__(2 * kBfT) blend_fwd_tma_mis_kernel(int64_t E, int K, int B,
                                                                  const float *__restrict__ base,
                                                                  const float *__restrict__ deltas,
                                                                  const float *__restrict__ psi,
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(kBfT) blend_fwd_tma_mis_kernel(int64_t E, int 
         mbar_fence_init();
     }
     int nz = 1;
-    for (int i = tid; i < K * Bp; i += kBfT) {
+    for (int i = tid; i < K * Bp; i += blockDim.x) {
         const int k = i / Bp, b = i % Bp;
         const float w = b < B ? psi[b * K + k] : 0.f;
         s_psi[i] = w;
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(kBfT) blend_fwd_tma_mis_kernel(int64_t E, int 
         float *stage = stages + (size_t)st * (K + 1) * kBmRS;
         const int64_t e0 = t * kBfTE;
         if (e0 == 0 || e0 + kBfTE > E) {        // the first / last tile: the floats no copy moved
-            for (int r = tid; r <= K; r += kBfT) {
+            for (int r = tid; r <= K; r += blockDim.x) {
                 const RowPlan p = row_plan(r, e0, E, K, deltas, base);
                 for (int q = 0; q < p.nfill; ++q)
                     stage[(size_t)r * kBmRS + (p.fill[q] - e0 + p.off)] = p.rowp[p.fill[q]];
@@ -1611,7 +1614,10 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
         const int per_sm = std::max(1, (int)((220 * 1024) / msm));
         const int64_t ntiles = (E + kBfTE - 1) / kBfTE;
         const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * std::min(per_sm, HS_BLEND_CTAS_PER_SM));
-        launch_k(blend_fwd_tma_mis_kernel, grid, kBfT, msm, s, E, K, B, base14, deltas, psi, raw10);
+        // more than 16 frames: 4 frame groups per tile (256 threads) instead of 2, twice the
+        // warps in flight at the same shared memory per CTA
+        launch_k(blend_fwd_tma_mis_kernel, grid, B > HS_BLEND_MIS_WIDE_B ? 2 * kBfT : kBfT, msm, s, E, K, B, base14,
+                 deltas, psi, raw10);
     } else if (E % 2 == 0 && (uintptr_t)base14 % 8 == 0 && (uintptr_t)deltas % 8 == 0 && (uintptr_t)raw10 % 8 == 0) {
         // odd N (every other delta / frame row only 8-byte aligned): float2 channel pairs,
         // frames in chunks over grid.y (render at 100,489 Gaussians: 367 us -> see DESIGN)

@@ -67,7 +67,8 @@ def test_blend_bwd_matches_float64(N, K, B):
     assert _rel(gpsi, ref_psi) <= 1e-5
 
 
-@pytest.mark.parametrize("N,B,zero", [(2048, 4, False), (2048, 8, True), (2048, 16, False), (2048, 16, True), (2048, 24, False), (2049, 16, False), (2049, 64, True), (1023, 5, False)])
+@pytest.mark.parametrize("N,B,zero", [(2048, 4, False), (2048, 8, True), (2048, 16, False), (2048, 16, True), (2048, 24, False), (2049, 16, False), (2049, 64, True), (1023, 5, False),
+                                      (1023, 24, False), (2049, 130, True)])
 def test_blend_fwd_matches_float64(N, B, zero):
     from paper_2503_12886_b200 import _lib as L
     K = 20
