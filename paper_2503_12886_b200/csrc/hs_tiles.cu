@@ -1098,11 +1098,7 @@ int hs_tile_fill(int B, int64_t N, int width, int height, const float *records, 
 #ifndef HS_LONG_SORT_CTAS_PER_SM
 #define HS_LONG_SORT_CTAS_PER_SM 16
 #endif
-#ifndef HS_LONG_SORT_CTAS_PER_SM_CTA
-#define HS_LONG_SORT_CTAS_PER_SM_CTA 16
-#endif
-    const int long_per_sm = (flags & HS_FILL_CTA_SORT) ? HS_LONG_SORT_CTAS_PER_SM_CTA : HS_LONG_SORT_CTAS_PER_SM;
-    launch_k(tile_sort_long_kernel, (unsigned)sms * long_per_sm, 32 * kLongWarps, 0, s, 
+    launch_k(tile_sort_long_kernel, (unsigned)sms * HS_LONG_SORT_CTAS_PER_SM, 32 * kLongWarps, 0, s, 
         N, tile_bits, nseg, depth, ranges, lists, list_counts, list_half, capacity, summary, values);
     if (f) cudaStreamWaitEvent(s, f->joined, 0);
     return check_launch("hs_tile_fill");
