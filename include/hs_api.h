@@ -97,13 +97,17 @@ int hs_blend_fwd(int64_t N, int K, int B, const float *base14, const float *delt
 /* Reduces over all B frames in-kernel:  g_base14 = sum_b g_raw14[b];
  * g_deltas[k] = sum_b psi[b,k] g_raw10[b];  gpsi partial sums per block.
  * Both outputs are written (not accumulated).  Returns the partial count in
- * *num_partials; gpsi_partials needs hs_blend_bwd_partials(N) * B * K floats. */
-/* Kernel launches hs_blend_bwd issues for these sizes (16-byte aligned buffers). */
-int hs_blend_bwd_kernels(int64_t N, int K, int B);
+ * *num_partials; gpsi_partials needs hs_blend_bwd_partials(N) * B * K floats.
+ * Up to 16 frames: one fused pass (TMA tiles when N % 128 == 0 and the buffers are
+ * 16-byte aligned, else register streaming); more frames (8-byte aligned buffers,
+ * N >= 17): one streaming pass for g_base / g_deltas over all frames, then g_psi per
+ * 128 frames -- no read-modify-write passes over the outputs. */
 int hs_blend_bwd(int64_t N, int K, int B, const float *deltas, const float *psi,
                  const float *g_raw14, float *g_base14, float *g_deltas,
                  float *gpsi_partials, int *num_partials, void *stream);
 int hs_blend_bwd_partials(int64_t N);
+/* Kernel launches hs_blend_bwd issues for these sizes (aligned buffers). */
+int hs_blend_bwd_kernels(int64_t N, int K, int B);
 
 /* ---- Projection (render.py:132-230 preprocess; model.py:219-234 activate;
  *      binding.py:174-188 transform_to_deformed) -------------------------- */
