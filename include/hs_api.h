@@ -300,6 +300,9 @@ int hs_raster_tile_order(int B, int width, int height, const uint32_t *ranges, i
  * black L1) pair per pixel block of the kernel, at most 8 per tile), reduced by
  * hs_loss_reduce. */
 #define HS_LOSS_PARTIALS_PER_TILE 16
+/* pix_T / pix_state (both or neither; both with the colour-init flags): per-pixel final
+ * transmittance and stop index for a later hs_raster_bwd.  NULL: a forward no adjoint
+ * follows (render) -- not tracked, not written. */
 int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const float *records,
                   const uint32_t *values, const uint32_t *ranges, int tile_bits,
                   const float *backgrounds, const uint8_t *targets, const float *wsum_image,

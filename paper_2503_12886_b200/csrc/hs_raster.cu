@@ -299,6 +299,25 @@ __device__ __forceinline__ float fwd_gate(uint32_t mask, uint32_t lanebit, float
     return out;
 }
 
+// the same without the stop index (a forward that no adjoint follows: render)
+__device__ __forceinline__ float fwd_gate_ns(uint32_t mask, uint32_t lanebit, float T, float e2, float kq, float nal) {
+    float out;
+    asm("{\n\t.reg .pred p, q;\n\t.reg .b32 m;\n\t"
+        "and.b32 m, %1, %2;\n\t"
+        "setp.ne.u32 p, m, 0;\n\t"
+        "setp.ge.and.f32 p, %3, %4, p;\n\t"
+#if HS_QTEST
+        "setp.ge.and.f32 q, %5, %6, p;\n\t"
+#else
+        "mov.pred q, p;\n\t"
+#endif
+        "setp.le.and.f32 q, %7, %8, q;\n\t"
+        "selp.f32 %0, %7, 0f00000000, q;\n\t}"
+        : "=f"(out)
+        : "r"(mask), "r"(lanebit), "f"(T), "f"(kTermEps), "f"(e2), "f"(kq), "f"(nal), "f"(-kAlphaCutoff));
+    return out;
+}
+
 // Stage one splat record into the lane's slot for the warp's 8 x 8 block with origin
 // (x0, y0).  Returns true when a pixel of the block can be touched (its mask is nonzero).
 // The record prefetch (HS_RASTER_PREFETCH): while a warp works through one 32-key batch,
@@ -439,7 +458,9 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
                                                 float2 nsuf, uint2 stop, int lane, uint32_t wbase,
                                                 const uint32_t *masks);
 
-template <bool kLoss, bool kImage, int CI, bool kTrain = false>
+// kState: track each pixel's stop index and write pix_T / pix_state (for an adjoint); false
+// for a forward nothing follows (render)
+template <bool kLoss, bool kImage, int CI, bool kTrain = false, bool kState = true>
 __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int gw, int nblk, int lane,
                                                  uint32_t wbase, uint32_t *masks = nullptr) {
     // gw = tile * kBlocks + blk: the pixel block of frame b this warp composites
@@ -553,7 +574,10 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             // alpha >= 1/255; a failing pixel gets alpha = 0 (no change to C or T); stop
             // records the list position after the last splat tested while live
             const uint32_t jl1 = c0 - start + (uint32_t)j + 1u;
-            if (HS_RASTER_FWD_ASM) {
+            if (HS_RASTER_FWD_ASM && !kState && !kTrain) {
+                nal.x = fwd_gate_ns(t.mlo, lanebit, T.x, e2.x, t.kq, nal.x);
+                nal.y = fwd_gate_ns(t.mhi, lanebit, T.y, e2.y, t.kq, nal.y);
+            } else if (HS_RASTER_FWD_ASM) {
                 nal.x = fwd_gate(t.mlo, lanebit, T.x, e2.x, t.kq, nal.x, jl1, stop.x);
                 nal.y = fwd_gate(t.mhi, lanebit, T.y, e2.y, t.kq, nal.y, jl1, stop.y);
             } else {
@@ -660,7 +684,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
                     if (kTrain) g3[c] = d > 0.f ? -a.grad_scale : d < 0.f ? a.grad_scale : 0.f;
                 }
             }
-            if (!kTrain || a.pix_T) {
+            if (kTrain ? a.pix_T != nullptr : kState) {
                 a.pix_T[pix] = Tp;
                 a.pix_state[pix] = (p ? stop.y : stop.x) | (signs << 26);
             }
@@ -807,15 +831,16 @@ __device__ __forceinline__ void for_each_block(const RasterArgs &a, int nblk, in
     }
 }
 
-template <bool kLoss, bool kImage, int CI>
+template <bool kLoss, bool kImage, int CI, bool kState = true>
 __global__ void __launch_bounds__(kRT, HS_RASTER_MINB_FWD) raster_fwd_kernel(RasterArgs a, int nblk) {
     pdl_prologue();
     if (guard_blocks(a)) return;
     __shared__ __align__(16) unsigned char s_stage[kCW * kWarpSmem];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(s_stage) + warp * kWarpSmem;
-    for_each_block(a, nblk, lane, warp,
-                   [&](int b, int gw) { raster_fwd_block<kLoss, kImage, CI>(a, b, gw, nblk, lane, wbase); });
+    for_each_block(a, nblk, lane, warp, [&](int b, int gw) {
+        raster_fwd_block<kLoss, kImage, CI, false, kState>(a, b, gw, nblk, lane, wbase);
+    });
 }
 
 template <bool kExplicitGrad, bool kRaw>
@@ -1157,6 +1182,10 @@ static RasterArgs make_args(int B, int64_t N, int W, int H, const float *records
 
 template <bool L, bool I>
 static void launch_fwd_ci(int ci, dim3 grid, int nblk, cudaStream_t s, const RasterArgs &a) {
+    if (!a.pix_T && ci == 0) {            // no per-pixel state: no adjoint follows (render)
+        launch_k(raster_fwd_kernel<L, I, 0, false>, grid, kRT, 0, s, a, nblk);
+        return;
+    }
     switch (ci) {
         case 0: launch_k(raster_fwd_kernel<L, I, 0>, grid, kRT, 0, s, a, nblk); break;
         case 1: launch_k(raster_fwd_kernel<L, I, 1>, grid, kRT, 0, s, a, nblk); break;
@@ -1232,8 +1261,10 @@ int hs_raster_fwd(int B, int64_t N, int width, int height, int flags, const floa
     else if ((flags & HS_RASTER_MAXW_ALL) && (flags & HS_RASTER_WSUMS)) ci = 2;
     else if (flags & HS_RASTER_MAXW_ALL) ci = 1;
     if ((loss && !targets) || (img && !image) || (ci && !maxw) || (ci >= 2 && !wsums) || (ci == 3 && !visited) ||
-        (ci >= 2 && !targets && !wsum_image) || (loss && !loss_partials)) {
-        set_error("hs_raster_fwd: flags 0x%x need a buffer that is NULL", flags);
+        (ci >= 2 && !targets && !wsum_image) || (loss && !loss_partials) || (!pix_T != !pix_state) ||
+        (ci && !pix_T)) {
+        set_error("hs_raster_fwd: flags 0x%x need a buffer that is NULL (pix_T and pix_state: both or neither, "
+                  "both with the colour-init flags)", flags);
         return HS_ERR_SHAPE;
     }
     if (int e = check_ws("hs_raster_fwd", workspace)) return e;

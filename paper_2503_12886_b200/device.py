@@ -1059,8 +1059,8 @@ class Trainer:
                 if self.binner.order_ready and (guard is not None or self.binner.mode == "tiles"):
                     flags |= L.RASTER_ORDER_READY
             self._call("raster_fwd", "hs_raster_fwd", self.B, av.N, self.W, self.H, flags, _p(self.records),
-                       _p(vals), _p(ranges), tile_bits, _p(backgrounds), None, None, None, _p(self.pix_T),
-                       _p(self.pix_state), _p(out), None, None, None,
+                       _p(vals), _p(ranges), tile_bits, _p(backgrounds), None, None, None, None, None, _p(out),
+                       None, None, None,
                        ctypes.byref(guard) if guard is not None else None, _p(self.raster_ws), _stream())
 
         spec = raster if (self.tile_binning and self.speculative and (self.events is None or self.profile_speculative)) else None

@@ -245,6 +245,19 @@ def test_c2_full_size_properties():
     assert np.array_equal(k.astype(np.uint64), res["keys"] >> np.uint64(32))
     assert np.array_equal(vals.cpu().numpy().view(np.uint32), res["values"])
     assert np.array_equal(ranges.view(B, -1, 2).cpu().numpy().view(np.uint32)[:, :tiles], res["ranges"])
+    # the render raster (no per-pixel state: no stop index, no pix_T / pix_state writes)
+    # against the stateful forward on the same lists: the same image bitwise
+    import ctypes
+    from paper_2503_12886_b200 import _lib as L
+    from paper_2503_12886_b200.device import _p
+    img_s = torch.empty_like(img1)
+    pix_T = torch.empty(B * 512 * 512, device="cuda")
+    pix_state = torch.empty(B * 512 * 512, dtype=torch.int32, device="cuda")
+    L.call("hs_raster_fwd", B, dev.N, 512, 512, L.RASTER_IMAGE, _p(tr.records), _p(vals), _p(ranges), tile_bits,
+           _p(bg), None, None, None, _p(pix_T), _p(pix_state), _p(img_s), None, None, None, None, _p(tr.raster_ws),
+           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert torch.equal(img1, img_s)
     img2 = tr.render(th, fr, cams, bg)
     assert torch.equal(img1, img2)                      # forward is deterministic
     assert float(img1.min()) >= -1e-6 and float(img1.max()) <= 1.0 + 1e-5
