@@ -372,6 +372,43 @@ def test_fused_raster_pixels_and_grads_c2():
     assert nbad == 0, worst
 
 
+def test_c3_binning_bit_exact():
+    """The render's tile-major binning at the C3 Gaussian count (100,489, 16 frames at 512^2:
+    lists of ~300 entries, thousands of 257..1,024 (the long-list sort), a few past 1,024
+    (the CTA sort, enqueued inside the fill on the second batch)): keys, values and ranges
+    bit-exact against the oracle, on both batches."""
+    from bench_support import synth
+    from paper_2503_12886_b200.device import AvatarParams, Trainer
+    B = 16
+    wl = synth.make_workload(317, B, 512, distinct_frames=B)
+    av = wl.avatar
+    dev = AvatarParams.from_host(O.GSet(*(av.base[a] for a in ATTRS)), av.deltas, av.mlp, av.tri_index,
+                                 av.barycentric)
+    tr = Trainer(dev, 512, 512, B)
+    tr.radius = torch.empty(B * dev.N, device="cuda")
+    tr.binner.write_keys = True
+    th = torch.from_numpy(np.asarray(wl.thetas, np.float32)).cuda()
+    fr = torch.from_numpy(wl.frames).cuda()
+    cams = torch.from_numpy(np.tile(wl.camera.packed(), (B, 1))).cuda()
+    bg = torch.zeros(B, 3, device="cuda")
+    for rep in range(2):
+        tr.render(th, fr, cams, bg)
+        torch.cuda.synchronize()
+        assert tr.binner.mode == "tiles"
+        keys, vals, ranges, tile_bits, tiles = tr.binner.result
+        rec = tr.records.view(B, dev.N, 12).cpu().numpy()
+        rad = tr.radius.view(B, dev.N).cpu().numpy()
+        res = BO.bin_batch(rec[..., 0:2], rad, tr.depth.view(B, dev.N).cpu().numpy(), rec[..., 5], rad > 0, 512,
+                           512, conic=rec[..., 2:5], qmax=rec[..., 6])
+        r = ranges.view(B, -1, 2).cpu().numpy().view(np.uint32)[:, :tiles]
+        ln = (r[..., 1] - r[..., 0]).ravel()
+        if rep == 0:
+            assert ((ln > 256) & (ln <= 512)).sum() > 1000 and (ln > 512).sum() > 100, np.bincount(ln // 256)
+        assert np.array_equal(keys.cpu().numpy().view(np.uint32).astype(np.uint64), res["keys"] >> np.uint64(32))
+        assert np.array_equal(vals.cpu().numpy().view(np.uint32), res["values"])
+        assert np.array_equal(r, res["ranges"])
+
+
 def test_c3_render_vs_oracle():
     """BASELINE configs[2] (100,489 Gaussians, 64 frames at 512^2): the render kernel's
     images against the oracle's own float64 forward (map_params -> blend -> activate
