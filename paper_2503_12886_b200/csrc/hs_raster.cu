@@ -146,7 +146,7 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-// ---- staged splat layout (shared memory, 64 B per splat; HS_STAGE_DUP: 96 B) ------
+// ---- staged splat layout (shared memory, 64 B per splat) -------------------------------
 //   q0: nmx nmy ka  kb2        nm = 0.5 - mean: dx = px + nmx = px + 0.5 - mx;
 //                              k = -0.5 log2(e): e2 = k q = dx (ka dx + kb2 dy) + kc dy^2
 //   q1: kc  nop ncr ncg        alpha = op 2^e2; nop = -op (clamped, kOpacityMax); nc = -colour
@@ -172,12 +172,19 @@ template <bool kRaw = false>
 __device__ __forceinline__ float grad_factor(int v) {
     return v < 2 ? (kRaw ? -1.0f : 0.5f * kMeanScale) : v == 3 ? 1.0f : v < 5 ? 0.5f : 1.0f;
 }
-// HS_STAGE_DUP=0: each value stored once (64 B per splat); the packed instructions take
-// the scalar as a broadcast operand (the .F32 form of FFMA2 / FMUL2 / FADD2)
-#ifndef HS_STAGE_DUP
-#define HS_STAGE_DUP 0
+// Each value stored once (64 B per splat); the packed instructions take the scalar as a
+// broadcast operand (the .F32 form of FFMA2 / FMUL2 / FADD2).
+// HS_STAGE_SOA: the warp's 32 slots as four 512-byte blocks (q0 of every slot, then q1, q2,
+// q3 at a 16-byte stride), so a lane's 16-byte stores of its own slot hit consecutive
+// addresses across the warp (conflict-free) instead of a 64-byte stride (4-way bank
+// conflicts on every staging store); the broadcast loads of one slot are one wavefront
+// either way.  The record prefetch slots likewise (three 512-byte blocks).
+#ifndef HS_STAGE_SOA
+#define HS_STAGE_SOA 1
 #endif
-constexpr int kStageBytes = HS_STAGE_DUP ? 96 : 64;
+constexpr int kStageBytes = 64;
+constexpr int kQStride = HS_STAGE_SOA ? 512 : 16;      // byte offset between a slot's q0, q1, q2, q3
+constexpr int kSlotStride = HS_STAGE_SOA ? 16 : kStageBytes;
 constexpr int kWarpSmem = 32 * (kStageBytes + 48);    // staged splats + the record prefetch slots
 
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
@@ -228,27 +235,9 @@ struct Staged {
 };
 __device__ __forceinline__ Staged load_staged(uint32_t ad) {
     Staged t;
-#if HS_STAGE_DUP
-    const float4 q0 = lds4(ad), q1 = lds4(ad + 16), q2 = lds4(ad + 32), q3 = lds4(ad + 48), q4 = lds4(ad + 64),
-                 q5 = lds4(ad + 80);
-    t.nmx = f2(q0.x, q0.y);
-    t.nmy = f2(q0.z, q0.w);
-    t.ka = f2(q1.x, q1.y);
-    t.kb2 = f2(q1.z, q1.w);
-    t.kc = f2(q2.x, q2.y);
-    t.nop = f2(q2.z, q2.w);
-    t.ncr = f2(q3.x, q3.y);
-    t.ncg = f2(q3.z, q3.w);
-    t.ncb = f2(q4.x, q4.y);
-    t.kq = q4.z;
-    t.gidx = __float_as_uint(q4.w);
-    t.mlo = __float_as_uint(q5.x);
-    t.mhi = __float_as_uint(q5.y);
-    t.kb = f2(q5.z, q5.w);
-#else
-    const float4 q0 = lds4(ad), q1 = lds4(ad + 16), q2 = lds4(ad + 32);
+    const float4 q0 = lds4(ad), q1 = lds4(ad + kQStride), q2 = lds4(ad + 2 * kQStride);
     uint32_t mlo, mhi;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mlo), "=r"(mhi) : "r"(ad + 48));
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mlo), "=r"(mhi) : "r"(ad + 3 * kQStride));
     t.nmx = f2(q0.x, q0.x);
     t.nmy = f2(q0.y, q0.y);
     t.ka = f2(q0.z, q0.z);
@@ -263,7 +252,6 @@ __device__ __forceinline__ Staged load_staged(uint32_t ad) {
     t.kb = f2(q2.w, q2.w);
     t.mlo = mlo;
     t.mhi = mhi;
-#endif
     return t;
 }
 
@@ -328,10 +316,12 @@ __device__ __forceinline__ float fwd_gate_ns(uint32_t mask, uint32_t lanebit, fl
 #define HS_RASTER_PREFETCH 1
 #endif
 constexpr int kRecBytes = 48;
+constexpr int kRecQStride = HS_STAGE_SOA ? 512 : 16;
+constexpr int kRecSlotStride = HS_STAGE_SOA ? 16 : kRecBytes;
 __device__ __forceinline__ void cp_async_record(uint32_t dst, const float *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(src + 4) : "memory");
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 32), "l"(src + 8) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + kRecQStride), "l"(src + 4) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 2 * kRecQStride), "l"(src + 8) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
@@ -343,7 +333,9 @@ __device__ __forceinline__ RawRec load_rec_global(const float *rec) {
     const float4 *r = reinterpret_cast<const float4 *>(rec);
     return {__ldg(r), __ldg(r + 1), __ldg(r + 2)};
 }
-__device__ __forceinline__ RawRec load_rec_shared(uint32_t addr) { return {lds4(addr), lds4(addr + 16), lds4(addr + 32)}; }
+__device__ __forceinline__ RawRec load_rec_shared(uint32_t addr) {
+    return {lds4(addr), lds4(addr + kRecQStride), lds4(addr + 2 * kRecQStride)};
+}
 
 template <bool kCull = true>
 __device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, int x0, int y0, uint32_t saddr) {
@@ -388,20 +380,11 @@ __device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, in
             }
         }
     }
-#if HS_STAGE_DUP
-    sts4(saddr, nmx, nmx, nmy, nmy);
-    sts4(saddr + 16, ka, ka, kb2, kb2);
-    sts4(saddr + 32, kc, kc, -opv, -opv);
-    sts4(saddr + 48, -Cv.y, -Cv.y, -Cv.z, -Cv.z);
-    sts4(saddr + 64, -Cv.w, -Cv.w, kK * qmax, __uint_as_float(gflag));
-    sts4(saddr + 80, __uint_as_float((uint32_t)mask), __uint_as_float((uint32_t)(mask >> 32)), kb, kb);
-#else
     sts4(saddr, nmx, nmy, ka, kb2);
-    sts4(saddr + 16, kc, -opv, -Cv.y, -Cv.z);
-    sts4(saddr + 32, -Cv.w, kK * qmax, __uint_as_float(gflag), kb);
-    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr + 48), "r"((uint32_t)mask), "r"((uint32_t)(mask >> 32))
+    sts4(saddr + kQStride, kc, -opv, -Cv.y, -Cv.z);
+    sts4(saddr + 2 * kQStride, -Cv.w, kK * qmax, __uint_as_float(gflag), kb);
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr + 3 * kQStride), "r"((uint32_t)mask), "r"((uint32_t)(mask >> 32))
                  : "memory");
-#endif
     return mask != 0;
 }
 
@@ -513,7 +496,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
     unsigned long long st_iter = 0, st_c = 0, st_batches = 0, st_empty = 0, st_live = 0;
 #endif
     // record prefetch: slot of this lane, and the list value of the next batch
-    const uint32_t rslot = wbase + 32 * kStageBytes + lane * kRecBytes;
+    const uint32_t rslot = wbase + 32 * kStageBytes + lane * kRecSlotStride;
     const float *frec = a.records + (int64_t)b * a.N * kRec;
     uint32_t n_cur = start + lane < end ? a.vals[start + lane] : 0u;
     uint32_t n_next = 0u;
@@ -539,7 +522,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
             } else {
                 rr = load_rec_global(frec + (int64_t)n * kRec);
             }
-            hit = stage_splat(rr, gflag, x0, y0, wbase + lane * kStageBytes);
+            hit = stage_splat(rr, gflag, x0, y0, wbase + lane * kSlotStride);
             want = CI > 0 && hit && (CI != 3 || !a.visited[n]);   // visited: no colour-init work
         }
         // the next batch: its records start streaming into the slots (this lane's slot was
@@ -566,7 +549,7 @@ __device__ __forceinline__ void raster_fwd_block(const RasterArgs &a, int b, int
         // without the colour-init test when no staged splat wants it
         auto splat = [&](int j, auto ci_tag) {
             constexpr bool kCI = decltype(ci_tag)::value;
-            const Staged t = load_staged(wbase + j * kStageBytes);
+            const Staged t = load_staged(wbase + j * kSlotStride);
             float2 dx2, dy2;
             const float2 e2 = splat_e2(t, fpx2, fpy2, dx2, dy2);
             float2 nal = mul2(t.nop, f2(ex2_approx(e2.x), ex2_approx(e2.y)));     // -alpha
@@ -908,7 +891,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
     if (last <= start) return;
     const uint32_t lanebit = 1u << lane;
     const float2 one2 = f2(1.f, 1.f);
-    const uint32_t rslot = wbase + 32 * kStageBytes + lane * kRecBytes;
+    const uint32_t rslot = wbase + 32 * kStageBytes + lane * kRecSlotStride;
     const float *frec = a.records + (int64_t)b * a.N * kRec;
     // batch k's staging set: the forward's hit mask (fused kernel), or every list entry
     auto need = [&](int k) -> uint32_t {
@@ -953,8 +936,8 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
                 rr = load_rec_global(frec + (int64_t)n * kRec);
             }
             const uint32_t gflag = (uint32_t)((int64_t)b * a.N + n);
-            if (fused) hit = stage_splat<false>(rr, gflag, x0, y0, wbase + lane * kStageBytes);
-            else hit = stage_splat(rr, gflag, x0, y0, wbase + lane * kStageBytes);
+            if (fused) hit = stage_splat<false>(rr, gflag, x0, y0, wbase + lane * kSlotStride);
+            else hit = stage_splat(rr, gflag, x0, y0, wbase + lane * kSlotStride);
         }
         if (HS_RASTER_PREFETCH) {
             if ((nb_next >> lane) & 1u) cp_async_record(rslot, frec + (int64_t)a.vals[idx - 32] * kRec);
@@ -979,7 +962,7 @@ __device__ __forceinline__ void raster_bwd_loop(const RasterArgs &a, int b, floa
         auto splat = [&](int j, float (&gv)[9], uint32_t &gidx, auto slow_tag) -> bool {
             constexpr bool kSlow = decltype(slow_tag)::value;
             const uint32_t jl = c0 - start + (uint32_t)j;
-            const Staged t = load_staged(wbase + j * kStageBytes);
+            const Staged t = load_staged(wbase + j * kSlotStride);
             gidx = t.gidx;
             float2 dx2, dy2;
             const float2 e2 = splat_e2(t, fpx2, fpy2, dx2, dy2);
