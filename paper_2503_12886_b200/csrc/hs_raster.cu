@@ -5,7 +5,8 @@
 // overhead (list walk, shared loads, the warp reduction of the adjoint) is paid
 // once per 64 pixels.  The four warps of a tile walk its depth-ordered key range
 // independently, 32 splats per batch: each lane gathers one 48-byte record, pre-transforms it
-// into a 64-byte staged form in the warp's private shared slot and votes whether
+// into a 64-byte staged form in the warp's private shared slots (four 512-byte quarter
+// blocks: conflict-free 16-byte stores) and votes whether
 // the warp's 8x8 block can be touched at all: the splat's integer pixel bbox must
 // admit a pixel of the block and its alpha >= 1/255 ellipse (q <= qmax) must reach
 // the rectangle of those pixel centres (exact minimum of q over the rectangle,
