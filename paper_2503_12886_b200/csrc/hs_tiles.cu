@@ -654,11 +654,18 @@ __device__ __forceinline__ bool sort_list_warp32(const float *__restrict__ depth
     constexpr uint32_t kSlot = (1u << IB) - 1u;
     // the list position of register e of this lane
     auto kQ = [&](int e) -> uint32_t { return HS_SORT_LANE_MAJOR ? (uint32_t)(lane * E + e) : (uint32_t)(e * 32 + lane); };
+    // the entries are read into the registers e-major (slot e * 32 + lane: coalesced loads,
+    // conflict-free 8-byte stores); the network sorts any placement, and the slot only
+    // names the entry's full key in s_k64
+#ifndef HS_SORT_LOAD_EMAJOR
+#define HS_SORT_LOAD_EMAJOR 1
+#endif
+    auto kL = [&](int e) -> uint32_t { return HS_SORT_LOAD_EMAJOR ? (uint32_t)(e * 32 + lane) : kQ(e); };
     uint32_t key[E];
     uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        const uint32_t q = kQ(e);
+        const uint32_t q = kL(e);
         key[e] = 0xFFFFFFFFu;
         if (q < len) {
             const uint32_t n = vals[start + q];
@@ -677,7 +684,7 @@ __device__ __forceinline__ bool sort_list_warp32(const float *__restrict__ depth
     const int sh = max(0, span - (31 - IB));           // real keys stay below 2^31
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        const uint32_t q = kQ(e);
+        const uint32_t q = kL(e);
         if (q < len) key[e] = (((key[e] - dmin) >> sh) << IB) | q;
     }
     if (HS_SORT_LANE_MAJOR) bitonic_u32_lm<E>(key, lane);
