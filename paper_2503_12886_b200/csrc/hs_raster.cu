@@ -338,14 +338,14 @@ __device__ __forceinline__ RawRec load_rec_shared(uint32_t addr) {
     return {lds4(addr), lds4(addr + kRecQStride), lds4(addr + 2 * kRecQStride)};
 }
 
+// The pixel mask of the 8 x 8 block at (x0, y0) for a splat record: the block's pixels inside
+// the reference's integer bbox minus the row groups (4 rows) its alpha >= 1/255 ellipse cannot reach.
 template <bool kCull = true>
-__device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, int x0, int y0, uint32_t saddr) {
+__device__ __forceinline__ uint64_t block_mask(const RawRec &rr, int x0, int y0) {
     const float4 A = rr.A, Bv = rr.B, Cv = rr.C;
     const uint32_t rows = __float_as_uint(Bv.w), cols = __float_as_uint(Cv.x);
     const int rl = unpack_lo(rows), rh = unpack_hi(rows), cl = unpack_lo(cols), ch = unpack_hi(cols);
     const float a = A.z, b = A.w, c = Bv.x, qmax = Bv.z;
-    const float opv = kOneMinusFloor > 0.f ? fminf(Bv.y, kOpacityMax) : Bv.y;   // (the saturation guard)
-    const float nmx = 0.5f - A.x, nmy = 0.5f - A.y, ka = kK * a, kb2 = 2.0f * kK * b, kb = kK * b, kc = kK * c;
     // the block's pixels inside the reference's bbox
     const int cs = max(cl - x0, 0), ce = min(ch - x0, 7), rs = max(rl - y0, 0), re = min(rh - y0, 7);
     uint64_t mask = 0;
@@ -381,6 +381,16 @@ __device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, in
             }
         }
     }
+    return mask;
+}
+
+template <bool kCull = true>
+__device__ __forceinline__ bool stage_splat(const RawRec &rr, uint32_t gflag, int x0, int y0, uint32_t saddr) {
+    const float4 A = rr.A, Bv = rr.B, Cv = rr.C;
+    const float a = A.z, b = A.w, c = Bv.x, qmax = Bv.z;
+    const float opv = kOneMinusFloor > 0.f ? fminf(Bv.y, kOpacityMax) : Bv.y;   // (the saturation guard)
+    const float nmx = 0.5f - A.x, nmy = 0.5f - A.y, ka = kK * a, kb2 = 2.0f * kK * b, kb = kK * b, kc = kK * c;
+    const uint64_t mask = block_mask<kCull>(rr, x0, y0);
     sts4(saddr, nmx, nmy, ka, kb2);
     sts4(saddr + kQStride, kc, -opv, -Cv.y, -Cv.z);
     sts4(saddr + 2 * kQStride, -Cv.w, kK * qmax, __uint_as_float(gflag), kb);
